@@ -1,0 +1,307 @@
+"""CPU oracle of the UltraSketchLLM AbsMaxMin sketch (arXiv 2506.17255).
+
+TEST INFRASTRUCTURE ONLY.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package.  It shares no code with
+the CUDA product path (``paper_2506_17255_b200``); neither imports the other.
+
+The arithmetic lives in ``usk_oracle.c`` (plain C99, scalar, fp64 references); this module
+only marshals numpy arrays through ctypes.  ``brute.py`` is a second, set-based enumerator
+of the same definitions for tiny inputs.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+import subprocess
+from dataclasses import dataclass, field
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+SRC = os.path.join(HERE, "usk_oracle.c")
+LIB = os.path.join(HERE, "liboracle.so")
+
+F32, BF16 = 0, 1
+HASH_X, HASH_IDENTITY = 0, 1
+GRAN_ROW, GRAN_LAYER = 0, 1
+OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE = 0, 1, 2, 3, 4
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle with gcc (no fast-math, no FP contraction)."""
+    if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        subprocess.check_call(
+            ["gcc", "-std=c99", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC", "-shared",
+             "-Wall", "-o", LIB, SRC, "-lm"])
+    return LIB
+
+
+_lib = None
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        _lib = ct.CDLL(build())
+        L = _lib
+        u32, u64, i32, i64, p = ct.c_uint32, ct.c_uint64, ct.c_int32, ct.c_int64, ct.c_void_p
+        L.uo_splitmix64.restype = u64
+        L.uo_splitmix64.argtypes = [u64]
+        L.uo_fmix32.restype = u32
+        L.uo_fmix32.argtypes = [u32]
+        L.uo_row_multiplier.restype = u32
+        L.uo_row_multiplier.argtypes = [u64, i32]
+        L.uo_unit_key.restype = u32
+        L.uo_unit_key.argtypes = [u64, u32, u32]
+        L.uo_position_mix.restype = u32
+        L.uo_position_mix.argtypes = [u64, u32]
+        L.uo_hash_index.restype = u32
+        L.uo_hash_index.argtypes = [i32, u64, u32, u32, i32, u32, u32]
+        L.uo_update.restype = u32
+        L.uo_update.argtypes = [i32, u32, u32]
+        L.uo_retrieve.restype = u32
+        L.uo_retrieve.argtypes = [i32, p, i32]
+        L.uo_sketch_unit.restype = i32
+        L.uo_sketch_unit.argtypes = [i32, p, p, i64, i32, u64, u32, u32, i32, u32, p]
+        L.uo_retrieve_unit.restype = i32
+        L.uo_retrieve_unit.argtypes = [i32, p, i32, u64, u32, u32, i32, u32, p, i64, p]
+        L.uo_importance.restype = i32
+        L.uo_importance.argtypes = [p, i64, i64, p]
+        L.uo_allocate.restype = i32
+        L.uo_allocate.argtypes = [i64, p, p, i64, i32, i32, i32, p, p]
+        L.uo_plan.restype = i32
+        L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, p, p, p, p, p]
+        L.uo_build_units.restype = i32
+        L.uo_build_units.argtypes = [i32, p, i64, i64, i32, i32, i32, i64, i64, p, p, i32, i32, u64, p]
+        L.uo_reconstruct_rows.restype = i32
+        L.uo_reconstruct_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, i64, i64, p]
+        L.uo_reconstruct_entries.restype = i32
+        L.uo_reconstruct_entries.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, p, i64, p]
+        L.uo_linear_rows.restype = i32
+        L.uo_linear_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, p, i64, i64, i64, p]
+        L.uo_peak_memory.restype = i64
+        L.uo_peak_memory.argtypes = [p, p, i32]
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    assert a.flags["C_CONTIGUOUS"]
+    return a.ctypes.data_as(ct.c_void_p)
+
+
+class OracleError(RuntimeError):
+    def __init__(self, status: int, what: str):
+        super().__init__(f"{what}: oracle status {status}")
+        self.status = status
+
+
+def _check(st: int, what: str):
+    if st != OK:
+        raise OracleError(st, what)
+
+
+# ------------------------------------------------------------------ dtype helpers
+def bits_of(w: np.ndarray, dtype: int) -> np.ndarray:
+    """Raw bit patterns as uint32 (bf16 in the low 16 bits)."""
+    if dtype == BF16:
+        assert w.dtype == np.uint16, "bf16 weights are passed as uint16 bit patterns"
+        return w.astype(np.uint32)
+    return np.ascontiguousarray(w, dtype=np.float32).view(np.uint32).copy()
+
+
+def value_of(bits: np.ndarray, dtype: int) -> np.ndarray:
+    """Bit patterns -> float64 values (exact)."""
+    b = np.asarray(bits).astype(np.uint32)
+    if dtype == BF16:
+        b = b << np.uint32(16)
+    return b.view(np.float32).astype(np.float64)
+
+
+# ------------------------------------------------------------------ scalar API
+def splitmix64(x: int) -> int:
+    return lib().uo_splitmix64(x)
+
+
+def hash_index(kind, seed, layer, t, row, p, ncols) -> int:
+    return lib().uo_hash_index(kind, seed, layer, t, row, p, ncols)
+
+
+def hash_indices(kind, seed, layer, t, M, positions, ncols) -> np.ndarray:
+    """[M, n] index table for positions (loops in Python over the C scalar hash)."""
+    L = lib()
+    return np.array([[L.uo_hash_index(kind, seed, layer, t, i, int(p), ncols) for p in positions]
+                     for i in range(M)], dtype=np.int64)
+
+
+def update(dtype, cell_bits, x_bits) -> int:
+    return lib().uo_update(dtype, cell_bits, x_bits)
+
+
+def retrieve(dtype, bonded_bits) -> int:
+    b = np.ascontiguousarray(bonded_bits, dtype=np.uint32)
+    return lib().uo_retrieve(dtype, _ptr(b), len(b))
+
+
+def sketch_unit(w_bits, positions, M, N, dtype=F32, hash_kind=HASH_X, seed=0, layer=0, t=0):
+    w = np.ascontiguousarray(w_bits, dtype=np.uint32)
+    p = np.ascontiguousarray(positions, dtype=np.uint32)
+    cells = np.zeros(M * N, dtype=np.uint32)
+    _check(lib().uo_sketch_unit(dtype, _ptr(w), _ptr(p), len(w), hash_kind, seed, layer, t, M, N,
+                                _ptr(cells)), "sketch_unit")
+    return cells.reshape(M, N)
+
+
+def retrieve_unit(cells, positions, dtype=F32, hash_kind=HASH_X, seed=0, layer=0, t=0):
+    cells = np.ascontiguousarray(cells, dtype=np.uint32)
+    M, N = cells.shape
+    p = np.ascontiguousarray(positions, dtype=np.uint32)
+    out = np.zeros(len(p), dtype=np.uint32)
+    _check(lib().uo_retrieve_unit(dtype, _ptr(cells), hash_kind, seed, layer, t, M, N, _ptr(p), len(p),
+                                  _ptr(out)), "retrieve_unit")
+    return out
+
+
+def importance(A: np.ndarray) -> np.ndarray:
+    """Eq. 7: I_j = (1/N) sum_k a_kj^2 (fp64)."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    N, d = A.shape
+    out = np.zeros(d, dtype=np.float64)
+    _check(lib().uo_importance(_ptr(A), N, d, _ptr(out)), "importance")
+    return out
+
+
+def allocate(scores, T, C=None, M=1, min_cols=1, lengths=None):
+    """Per-unit columns for unit scores under a budget of T cells (C defaults to U)."""
+    s = np.ascontiguousarray(scores, dtype=np.float64)
+    U = len(s)
+    C = U if C is None else C
+    L_u = np.ones(U, dtype=np.uint64) if lengths is None else np.ascontiguousarray(lengths, dtype=np.uint64)
+    cls = np.zeros(U, dtype=np.uint8)
+    ncols = np.zeros(U, dtype=np.int32)
+    _check(lib().uo_allocate(U, _ptr(s), _ptr(L_u), T, C, M, min_cols, _ptr(cls), _ptr(ncols)), "allocate")
+    return ncols, cls
+
+
+# ------------------------------------------------------------------ model plan
+@dataclass
+class Plan:
+    shapes: list            # [(out, in)]
+    dtype: int
+    M: int
+    gran: int
+    g: int
+    C: int
+    min_cols: int
+    hash_kind: int
+    seed: int
+    unit_base: np.ndarray   # [L+1]
+    cls: np.ndarray         # [U]
+    ncols: np.ndarray       # [U]
+    offsets: np.ndarray     # [U+1] cells
+    acct: np.ndarray        # [L, 4] budget bits, class-map bits, T, achieved bits
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def total_cells(self) -> int:
+        return int(self.offsets[-1])
+
+    def layer_units(self, l):
+        return int(self.unit_base[l]), int(self.unit_base[l + 1])
+
+    def layer_slices(self, l):
+        u0, u1 = self.layer_units(l)
+        return (np.ascontiguousarray(self.ncols[u0:u1]), np.ascontiguousarray(self.offsets[u0:u1 + 1]))
+
+
+def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None, min_cols=1,
+         hash_kind=HASH_X, seed=0) -> Plan:
+    L = len(shapes)
+    outf = np.array([s[0] for s in shapes], dtype=np.int64)
+    inf = np.array([s[1] for s in shapes], dtype=np.int64)
+    if C is None:
+        C = 4 if saliency is not None else 1
+    sal_arrays = None
+    sal_ptrs = None
+    if saliency is not None:
+        sal_arrays = [None if s is None else np.ascontiguousarray(s, dtype=np.float32) for s in saliency]
+        sal_ptrs = (ct.c_void_p * L)(*[None if a is None else a.ctypes.data for a in sal_arrays])
+    U = int(np.sum(inf // g)) if gran == GRAN_ROW else L
+    unit_base = np.zeros(L + 1, dtype=np.int64)
+    cls = np.zeros(max(U, 1), dtype=np.uint8)
+    ncols = np.zeros(max(U, 1), dtype=np.int32)
+    offsets = np.zeros(max(U, 1) + 1, dtype=np.int64)
+    acct = np.zeros(4 * L, dtype=np.int64)
+    st = lib().uo_plan(L, _ptr(outf), _ptr(inf), dtype,
+                       ct.cast(sal_ptrs, ct.c_void_p) if sal_ptrs is not None else None,
+                       float(bpw), M, gran, g, C, min_cols, _ptr(unit_base), _ptr(cls), _ptr(ncols),
+                       _ptr(offsets), _ptr(acct))
+    _check(st, "plan")
+    return Plan(list(map(tuple, zip(outf.tolist(), inf.tolist()))), dtype, M, gran, g, C, min_cols, hash_kind,
+                seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4))
+
+
+def _np_dtype(dtype):
+    return np.uint16 if dtype == BF16 else np.uint32
+
+
+def build_layer(pl: Plan, l: int, W: np.ndarray, sketch: np.ndarray, t_begin=0, t_end=None):
+    """Build units [t_begin, t_end) of layer l from W ([out,in] raw bits: uint16 bf16 / float32)
+    into the model sketch (raw cells, uint16 or uint32)."""
+    out, inn = pl.shapes[l]
+    u0, u1 = pl.layer_units(l)
+    t_end = (u1 - u0) if t_end is None else t_end
+    W = np.ascontiguousarray(W)
+    if pl.dtype == F32:
+        W = W.astype(np.float32, copy=False)
+    assert W.shape == (out, inn)
+    ncols, offs = pl.layer_slices(l)
+    assert sketch.dtype == _np_dtype(pl.dtype) and sketch.flags["C_CONTIGUOUS"]
+    _check(lib().uo_build_units(pl.dtype, _ptr(W), out, inn, l, pl.gran, pl.g, t_begin, t_end, _ptr(ncols),
+                                _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(sketch)), "build_units")
+
+
+def build_model(pl: Plan, weights) -> np.ndarray:
+    sketch = np.zeros(pl.total_cells, dtype=_np_dtype(pl.dtype))
+    for l, W in enumerate(weights):
+        build_layer(pl, l, W, sketch)
+    return sketch
+
+
+def reconstruct_rows(pl: Plan, sketch: np.ndarray, l: int, o_begin=0, o_end=None) -> np.ndarray:
+    out, inn = pl.shapes[l]
+    o_end = out if o_end is None else o_end
+    ncols, offs = pl.layer_slices(l)
+    res = np.zeros((o_end - o_begin, inn), dtype=_np_dtype(pl.dtype))
+    _check(lib().uo_reconstruct_rows(pl.dtype, _ptr(sketch), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs),
+                                     pl.M, pl.hash_kind, pl.seed, o_begin, o_end, _ptr(res)), "reconstruct_rows")
+    return res
+
+
+def reconstruct_entries(pl: Plan, sketch: np.ndarray, l: int, oj: np.ndarray) -> np.ndarray:
+    out, inn = pl.shapes[l]
+    ncols, offs = pl.layer_slices(l)
+    oj = np.ascontiguousarray(oj, dtype=np.int64)
+    res = np.zeros(len(oj), dtype=np.uint32)
+    _check(lib().uo_reconstruct_entries(pl.dtype, _ptr(sketch), out, inn, l, pl.gran, pl.g, _ptr(ncols),
+                                        _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(oj), len(oj), _ptr(res)),
+           "reconstruct_entries")
+    return res
+
+
+def linear_rows(pl: Plan, sketch: np.ndarray, l: int, x: np.ndarray, o_begin=0, o_end=None) -> np.ndarray:
+    """fp64 y[T, o_end-o_begin] = x[T, in] @ W'[o_begin:o_end]^T."""
+    out, inn = pl.shapes[l]
+    o_end = out if o_end is None else o_end
+    x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
+    T = x.shape[0]
+    ncols, offs = pl.layer_slices(l)
+    y = np.zeros((T, o_end - o_begin), dtype=np.float64)
+    _check(lib().uo_linear_rows(pl.dtype, _ptr(sketch), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs), pl.M,
+                                pl.hash_kind, pl.seed, _ptr(x), T, o_begin, o_end, _ptr(y)), "linear_rows")
+    return y
+
+
+def peak_memory(layer_bytes, sketch_bytes) -> int:
+    a = np.ascontiguousarray(layer_bytes, dtype=np.int64)
+    b = np.ascontiguousarray(sketch_bytes, dtype=np.int64)
+    return lib().uo_peak_memory(_ptr(a), _ptr(b), len(a))

@@ -1,0 +1,600 @@
+/*
+ * usk_oracle.c -- plain, slow, obviously-correct CPU ORACLE of the UltraSketchLLM
+ * (arXiv 2506.17255) index-free multi-row AbsMaxMin sketch.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no code,
+ * header, table or constant generator with the CUDA product path
+ * (paper_2506_17255_b200/csrc); the two meet only in the written contract
+ * ("Allocation").
+ *
+ * Everything is scalar C99, no intrinsics, compiled -O2 -fno-fast-math
+ * -ffp-contract=off.  Values are compared as IEEE doubles (exact for fp32/bf16),
+ * never as packed integer keys, so the oracle does not share the GPU's encoding.
+ *
+ * Citations: PAPER.md:<line> (section / equation), SPEC.md:<line>.
+ *
+ * Parity status per function (details in DESIGN.md "Oracle pins"):
+ *   uo_update / uo_retrieve / uo_sketch_unit / uo_retrieve_unit  -- pinned (SPEC worked
+ *       examples, brute-force preimage enumeration, underestimate, order independence)
+ *   uo_hash_index  -- exact values are OUR contract (paper fixes only "independent hash
+ *       functions"): "parity unpinned" for individual index values;
+ *       pinned statistically (Table 3 empty fractions, untouched closed forms).
+ *   uo_allocate / uo_plan -- pinned (SPEC allocation examples, conservation, monotonicity,
+ *       scale invariance, bpw accounting vs Table 1 arithmetic); class boundaries and the
+ *       remainder order are our reading (L9/L10): "parity unpinned" for those.
+ *   uo_importance -- pinned (SPEC Eq. 7 examples, constant activations).
+ *   uo_linear_rows -- pinned (numpy fp64 matmul of the oracle-verified W').
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+/* status codes: numerically identical to include/usk.h by written contract only */
+#define UO_OK 0
+#define UO_EINVAL 1
+#define UO_ESHAPE 2
+#define UO_EBUDGET 3
+#define UO_ENONFINITE 4
+
+#define UO_F32 0
+#define UO_BF16 1
+
+#define UO_HASH_X 0
+#define UO_HASH_IDENTITY 1
+
+#define UO_GRAN_ROW 0
+#define UO_GRAN_LAYER 1
+
+/* ------------------------------------------------------------------------------------
+ * Hash family "USK-X" (paper Eq. 3, PAPER.md:239-243:
+ * I = H(Addr(w)) with independent H_0..H_{M-1}; Addr(w) is the natural, storage-free
+ * index of the weight inside its compression unit).
+ * ------------------------------------------------------------------------------------ */
+uint64_t uo_splitmix64(uint64_t x) {
+  uint64_t z;
+  x = x + 0x9E3779B97F4A7C15ull;
+  z = x;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+uint32_t uo_fmix32(uint32_t h) {
+  h ^= h >> 16;
+  h *= 0x85EBCA6Bu;
+  h ^= h >> 13;
+  h *= 0xC2B2AE35u;
+  h ^= h >> 16;
+  return h;
+}
+
+/* a_i: per sketch row multiplier (odd) */
+uint32_t uo_row_multiplier(uint64_t seed, int32_t row) {
+  return ((uint32_t)uo_splitmix64(seed + 0x100ull + (uint64_t)row)) | 1u;
+}
+
+/* K_u: per compression unit u = (layer l, unit t) */
+uint32_t uo_unit_key(uint64_t seed, uint32_t layer, uint32_t t) {
+  uint64_t lt = ((uint64_t)layer << 32) | (uint64_t)t;
+  return (uint32_t)uo_splitmix64(seed ^ uo_splitmix64(lt));
+}
+
+/* R(p): per position, shared by all rows */
+uint32_t uo_position_mix(uint64_t seed, uint32_t p) {
+  uint32_t rho = (uint32_t)uo_splitmix64(seed);
+  return uo_fmix32(p ^ rho);
+}
+
+/* idx_i(u, p) in [0, ncols) */
+uint32_t uo_hash_index(int32_t kind, uint64_t seed, uint32_t layer, uint32_t t, int32_t row,
+                       uint32_t p, uint32_t ncols) {
+  if (kind == UO_HASH_IDENTITY) return p % ncols; /* SPEC.md:54 test_hash: flat_index mod columns */
+  {
+    uint32_t h = uo_position_mix(seed, p) ^ uo_unit_key(seed, layer, t);
+    uint32_t m = h * uo_row_multiplier(seed, row); /* wraps mod 2^32 */
+    return (uint32_t)(((uint64_t)m * (uint64_t)ncols) >> 32);
+  }
+}
+
+/* ------------------------------------------------------------------------------------
+ * Cell values.  A cell / weight is held as its raw bit pattern (bf16 in the low 16 bits).
+ * ------------------------------------------------------------------------------------ */
+static double uo_value(int32_t dtype, uint32_t bits) {
+  float f;
+  uint32_t b = (dtype == UO_BF16) ? (bits << 16) : bits;
+  memcpy(&f, &b, sizeof f);
+  return (double)f;
+}
+
+static uint32_t uo_inf_bits(int32_t dtype) { return dtype == UO_BF16 ? 0x7F80u : 0x7F800000u; }
+
+/* Eq. 4: S[i,I_i] = (Abs(S[i,I_i]) > Abs(X)) ? X : S[i,I_i].
+ * Tie |X| == |S| with opposite signs: prefer the non-negative value (L2,
+ * SPEC.md:110).  Returns the new cell. */
+uint32_t uo_update(int32_t dtype, uint32_t cell, uint32_t x) {
+  double s = uo_value(dtype, cell), v = uo_value(dtype, x);
+  if (fabs(s) > fabs(v)) return x;
+  if (fabs(s) == fabs(v) && signbit(s) && !signbit(v)) return x;
+  return cell;
+}
+
+/* Eq. 5: w' = Max_i S[i][H_i(Addr(w))], "Max" read as the maximum
+ * absolute value returning the signed cell (L1); tie -> the
+ * non-negative value (L2). */
+uint32_t uo_retrieve(int32_t dtype, const uint32_t* bonded, int32_t M) {
+  uint32_t best = bonded[0];
+  int32_t i;
+  for (i = 1; i < M; i++) {
+    double b = uo_value(dtype, best), c = uo_value(dtype, bonded[i]);
+    if (fabs(c) > fabs(b) || (fabs(c) == fabs(b) && signbit(b) && !signbit(c))) best = bonded[i];
+  }
+  return best;
+}
+
+static int uo_finite(int32_t dtype, uint32_t bits) { return isfinite(uo_value(dtype, bits)); }
+
+/* One compression unit ("S in AbsMaxMin is initialized as inf";
+ * select Eq. 3, update Eq. 4).  Inserts the n (position, weight) pairs in the order
+ * given (any order gives the same state).  cells: M*N, row-major by sketch
+ * row. */
+int32_t uo_sketch_unit(int32_t dtype, const uint32_t* w_bits, const uint32_t* pos, int64_t n,
+                       int32_t hash_kind, uint64_t seed, uint32_t layer, uint32_t t, int32_t M,
+                       uint32_t N, uint32_t* cells) {
+  int64_t k;
+  int32_t i;
+  uint32_t c;
+  if (M < 1 || N < 1) return UO_EINVAL;
+  for (i = 0; i < M; i++)
+    for (c = 0; c < N; c++) cells[(int64_t)i * N + c] = uo_inf_bits(dtype);
+  for (k = 0; k < n; k++) {
+    if (!uo_finite(dtype, w_bits[k])) return UO_ENONFINITE;
+    for (i = 0; i < M; i++) {
+      uint32_t idx = uo_hash_index(hash_kind, seed, layer, t, i, pos[k], N);
+      uint32_t* cell = &cells[(int64_t)i * N + idx];
+      *cell = uo_update(dtype, *cell, w_bits[k]);
+    }
+  }
+  return UO_OK;
+}
+
+/* Retrieval of n positions from one unit (hash, batched gather,
+ * interpret with Max). */
+int32_t uo_retrieve_unit(int32_t dtype, const uint32_t* cells, int32_t hash_kind, uint64_t seed,
+                         uint32_t layer, uint32_t t, int32_t M, uint32_t N, const uint32_t* pos,
+                         int64_t n, uint32_t* out_bits) {
+  int64_t k;
+  int32_t i;
+  uint32_t bonded[8];
+  if (M < 1 || M > 8 || N < 1) return UO_EINVAL;
+  for (k = 0; k < n; k++) {
+    for (i = 0; i < M; i++)
+      bonded[i] = cells[(int64_t)i * N + uo_hash_index(hash_kind, seed, layer, t, i, pos[k], N)];
+    out_bits[k] = uo_retrieve(dtype, bonded, M);
+  }
+  return UO_OK;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Eq. 7: I_j = E[a_j^2] = (1/N) sum_k a_{k,j}^2.  A is [N, d]
+ * row-major fp32; sequential fp64 sum over k.
+ * ------------------------------------------------------------------------------------ */
+int32_t uo_importance(const float* A, int64_t N, int64_t d, double* I) {
+  int64_t j, k;
+  if (N < 1 || d < 1) return UO_ESHAPE;
+  for (j = 0; j < d; j++) {
+    double s = 0.0;
+    for (k = 0; k < N; k++) {
+      double a = (double)A[k * d + j];
+      s += a * a;
+    }
+    I[j] = s / (double)N;
+  }
+  return UO_OK;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Allocation (§3.4: "assign I_j / sum_i I_i x Mem(Sketch)"; categories
+ * PAPER.md:523-528).  Deterministic integer reading, DESIGN.md "Allocation" (L8-L12):
+ *   q_u = floor(s_u / s_max * 2^24); rank by (q desc, u asc); class c = floor(rank*C/U);
+ *   W_c = sum_{u in c} q_u L_u; x_c = T W_c / (W n_c M); N_c = max(min_cols, floor x_c)
+ *   with water-filling of floor-clamped classes; largest remainder in (frac desc, c asc).
+ * ------------------------------------------------------------------------------------ */
+typedef unsigned __int128 uo_u128;
+
+typedef struct {
+  uint64_t q;
+  int64_t u;
+} uo_rank_item;
+
+static int uo_rank_cmp(const void* a, const void* b) {
+  const uo_rank_item* x = (const uo_rank_item*)a;
+  const uo_rank_item* y = (const uo_rank_item*)b;
+  if (x->q != y->q) return x->q > y->q ? -1 : 1; /* q descending */
+  return x->u < y->u ? -1 : (x->u > y->u ? 1 : 0); /* u ascending */
+}
+
+typedef struct {
+  uint64_t key;
+  int32_t c;
+} uo_rem_item;
+
+static int uo_rem_cmp(const void* a, const void* b) {
+  const uo_rem_item* x = (const uo_rem_item*)a;
+  const uo_rem_item* y = (const uo_rem_item*)b;
+  if (x->key != y->key) return x->key > y->key ? -1 : 1;
+  return x->c < y->c ? -1 : (x->c > y->c ? 1 : 0);
+}
+
+/* s_u: unit scores (>= 0, finite); L_u: unit lengths (weights per unit; pass 1 for a
+ * common length); T: cells available; C classes; M rows; min_cols floor.
+ * Outputs: cls[U], ncols[U]. */
+int32_t uo_allocate(int64_t U, const double* s_u, const uint64_t* L_u, int64_t T, int32_t C,
+                    int32_t M, int32_t min_cols, uint8_t* cls, int32_t* ncols) {
+  int64_t u, r;
+  int32_t c;
+  double s_max = 0.0;
+  uint64_t* q;
+  uo_rank_item* items;
+  int64_t n_c[256];
+  uo_u128 W_c[256];
+  int active[256];
+  int64_t N_c[256];
+  uo_u128 num_c[256], den_c[256];
+  if (U < 1) return UO_ESHAPE;
+  if (C < 1 || C > 255 || M < 1 || M > 8 || min_cols < 1 || T < 0) return UO_EINVAL;
+  q = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)U);
+  items = (uo_rank_item*)malloc(sizeof(uo_rank_item) * (size_t)U);
+  for (u = 0; u < U; u++) {
+    if (!(s_u[u] >= 0.0) || !isfinite(s_u[u])) {
+      free(q);
+      free(items);
+      return UO_EINVAL;
+    }
+    if (s_u[u] > s_max) s_max = s_u[u];
+  }
+  /* step 2: fixed point */
+  for (u = 0; u < U; u++) q[u] = (s_max > 0.0) ? (uint64_t)floor((s_u[u] / s_max) * 16777216.0) : 1u;
+  /* step 3: rank, classes */
+  for (u = 0; u < U; u++) {
+    items[u].q = q[u];
+    items[u].u = u;
+  }
+  qsort(items, (size_t)U, sizeof(uo_rank_item), uo_rank_cmp);
+  for (c = 0; c < C; c++) {
+    n_c[c] = 0;
+    W_c[c] = 0;
+  }
+  for (r = 0; r < U; r++) {
+    int64_t uu = items[r].u;
+    int32_t cc = (int32_t)((r * (int64_t)C) / U);
+    cls[uu] = (uint8_t)cc;
+    n_c[cc] += 1;
+    W_c[cc] += (uo_u128)q[uu] * (uo_u128)L_u[uu];
+  }
+  /* feasibility of the floor */
+  {
+    int64_t floor_cells = 0;
+    for (c = 0; c < C; c++) floor_cells += n_c[c] * (int64_t)M * (int64_t)min_cols;
+    if (floor_cells > T) {
+      free(q);
+      free(items);
+      return UO_EBUDGET;
+    }
+  }
+  /* steps 4-5: proportional share with water-filling of clamped classes */
+  for (c = 0; c < C; c++) active[c] = n_c[c] > 0;
+  for (;;) {
+    uo_u128 Wa = 0;
+    int64_t Ta = T;
+    int changed = 0;
+    for (c = 0; c < C; c++) {
+      if (n_c[c] == 0) continue;
+      if (active[c])
+        Wa += W_c[c];
+      else
+        Ta -= n_c[c] * (int64_t)M * (int64_t)min_cols;
+    }
+    for (c = 0; c < C; c++) {
+      if (!active[c]) continue;
+      num_c[c] = (uo_u128)Ta * W_c[c];
+      den_c[c] = Wa * (uo_u128)n_c[c] * (uo_u128)M;
+      N_c[c] = (den_c[c] == 0) ? 0 : (int64_t)(num_c[c] / den_c[c]);
+      if (N_c[c] < min_cols) {
+        active[c] = 0;
+        changed = 1;
+      }
+    }
+    if (!changed) break;
+  }
+  for (c = 0; c < C; c++)
+    if (!active[c]) N_c[c] = min_cols;
+  /* step 6: largest remainder over the unclamped classes */
+  {
+    int64_t left = T;
+    uo_rem_item rem[256];
+    int32_t n_rem = 0, k;
+    for (c = 0; c < C; c++) left -= n_c[c] * (int64_t)M * N_c[c];
+    for (c = 0; c < C; c++) {
+      if (!active[c]) continue;
+      rem[n_rem].key = (uint64_t)(((num_c[c] % den_c[c]) << 32) / den_c[c]);
+      rem[n_rem].c = c;
+      n_rem++;
+    }
+    qsort(rem, (size_t)n_rem, sizeof(uo_rem_item), uo_rem_cmp);
+    for (k = 0; k < n_rem; k++) {
+      int32_t cc = rem[k].c;
+      int64_t need = n_c[cc] * (int64_t)M;
+      if (need <= left) {
+        N_c[cc] += 1;
+        left -= need;
+      }
+    }
+  }
+  for (u = 0; u < U; u++) ncols[u] = (int32_t)N_c[cls[u]];
+  free(q);
+  free(items);
+  return UO_OK;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Model plan (scopes per PAPER.md:331-334).
+ *   ROW:   unit (l, t) = input dims [t*g, (t+1)*g) of layer l (L6/L7); each
+ *          layer is one budget scope of floor(bpw * numel_l) bits ("Mem(Sketch) is the target
+ *          storage by all sketch states in a layer"), minus the class map
+ *          U_l * ceil(log2 C) bits when C > 1.
+ *   LAYER: one unit per layer; one scope over the model; unit score = mean row
+ *          importance, share proportional to score x numel (L8).
+ * Offsets: exclusive prefix sum of M * N_u over units in (layer, t) order.
+ * layer_acct[4*l + {0,1,2,3}] = {budget bits, class-map bits, cells T (ROW; -1 for
+ * LAYER), achieved bits (states + class map)}.
+ * ------------------------------------------------------------------------------------ */
+static int32_t uo_ceil_log2(int32_t C) {
+  int32_t b = 0;
+  while ((1 << b) < C) b++;
+  return b;
+}
+
+int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32_t dtype,
+                const float* const* sal, double bpw, int32_t M, int32_t gran, int32_t g, int32_t C,
+                int32_t min_cols, int64_t* unit_base, uint8_t* cls, int32_t* ncols,
+                int64_t* offsets, int64_t* layer_acct) {
+  int32_t l;
+  int64_t U = 0, u;
+  int32_t state_bits = (dtype == UO_BF16) ? 16 : 32;
+  if (n_layers < 1 || M < 1 || M > 8 || C < 1 || C > 255 || min_cols < 1) return UO_EINVAL;
+  if (!(bpw > 0.0) || !isfinite(bpw)) return UO_EINVAL;
+  if (dtype != UO_F32 && dtype != UO_BF16) return UO_EINVAL;
+  if (gran != UO_GRAN_ROW && gran != UO_GRAN_LAYER) return UO_EINVAL;
+  for (l = 0; l < n_layers; l++) {
+    if (outf[l] < 1 || inf[l] < 1) return UO_ESHAPE;
+    if (outf[l] * inf[l] > 0xFFFFFFFFll) return UO_ESHAPE; /* positions are 32-bit */
+    if (gran == UO_GRAN_ROW && (g < 1 || inf[l] % g != 0)) return UO_EINVAL;
+  }
+  /* units */
+  for (l = 0; l < n_layers; l++) {
+    unit_base[l] = U;
+    U += (gran == UO_GRAN_ROW) ? inf[l] / g : 1;
+  }
+  unit_base[n_layers] = U;
+
+  if (gran == UO_GRAN_ROW) {
+    for (l = 0; l < n_layers; l++) {
+      int64_t Ul = inf[l] / g, t, j;
+      int64_t numel = outf[l] * inf[l];
+      int64_t budget = (int64_t)floor(bpw * (double)numel);
+      int64_t meta = (C > 1) ? Ul * (int64_t)uo_ceil_log2(C) : 0;
+      int64_t T;
+      double* s_u;
+      uint64_t* L_u;
+      int32_t st;
+      int64_t achieved = meta;
+      if (budget < meta) return UO_EBUDGET;
+      T = (budget - meta) / state_bits;
+      s_u = (double*)malloc(sizeof(double) * (size_t)Ul);
+      L_u = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)Ul);
+      for (t = 0; t < Ul; t++) {
+        double s = 0.0;
+        for (j = t * g; j < (t + 1) * g; j++) {
+          double v = sal && sal[l] ? (double)sal[l][j] : 1.0;
+          if (!(v >= 0.0) || !isfinite(v)) {
+            free(s_u);
+            free(L_u);
+            return UO_EINVAL;
+          }
+          s += v;
+        }
+        s_u[t] = s / (double)g;
+        L_u[t] = 1; /* common unit length within a layer */
+      }
+      st = uo_allocate(Ul, s_u, L_u, T, C, M, min_cols, cls + unit_base[l], ncols + unit_base[l]);
+      free(s_u);
+      free(L_u);
+      if (st != UO_OK) return st;
+      for (t = 0; t < Ul; t++) achieved += (int64_t)M * ncols[unit_base[l] + t] * state_bits;
+      layer_acct[4 * l + 0] = budget;
+      layer_acct[4 * l + 1] = meta;
+      layer_acct[4 * l + 2] = T;
+      layer_acct[4 * l + 3] = achieved;
+    }
+  } else {
+    int64_t numel = 0, budget, T;
+    double* s_u = (double*)malloc(sizeof(double) * (size_t)n_layers);
+    uint64_t* L_u = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)n_layers);
+    int32_t st;
+    for (l = 0; l < n_layers; l++) {
+      int64_t j;
+      double s = 0.0;
+      for (j = 0; j < inf[l]; j++) {
+        double v = sal && sal[l] ? (double)sal[l][j] : 1.0;
+        if (!(v >= 0.0) || !isfinite(v)) {
+          free(s_u);
+          free(L_u);
+          return UO_EINVAL;
+        }
+        s += v;
+      }
+      s_u[l] = s / (double)inf[l];
+      L_u[l] = (uint64_t)(outf[l] * inf[l]);
+      numel += outf[l] * inf[l];
+    }
+    budget = (int64_t)floor(bpw * (double)numel);
+    T = budget / state_bits;
+    st = uo_allocate(n_layers, s_u, L_u, T, C, M, min_cols, cls, ncols);
+    free(s_u);
+    free(L_u);
+    if (st != UO_OK) return st;
+    for (l = 0; l < n_layers; l++) {
+      layer_acct[4 * l + 0] = (l == 0) ? budget : 0;
+      layer_acct[4 * l + 1] = 0;
+      layer_acct[4 * l + 2] = (l == 0) ? T : 0;
+      layer_acct[4 * l + 3] = (int64_t)M * ncols[l] * state_bits;
+    }
+  }
+  offsets[0] = 0;
+  for (u = 0; u < U; u++) offsets[u + 1] = offsets[u] + (int64_t)M * ncols[u];
+  return UO_OK;
+}
+
+/* ------------------------------------------------------------------------------------
+ * Layer-level build / reconstruct / linear over a unit range of one layer.
+ * W: [out, in] row-major raw bits (uint16 bf16 or uint32 fp32).  Unit (l, t):
+ *   ROW g:  weights (o, j), j in [t g, (t+1) g), position p = (j - t g) * out + o
+ *   LAYER:  all weights, position p = j * out + o
+ * ncols/offsets: the layer's slice of the plan (offsets relative to the sketch base,
+ * in cells).  sketch: raw bits, one cell per element of the dtype.
+ * ------------------------------------------------------------------------------------ */
+static uint32_t uo_load(int32_t dtype, const void* base, int64_t idx) {
+  return dtype == UO_BF16 ? (uint32_t)((const uint16_t*)base)[idx] : ((const uint32_t*)base)[idx];
+}
+static void uo_store(int32_t dtype, void* base, int64_t idx, uint32_t bits) {
+  if (dtype == UO_BF16)
+    ((uint16_t*)base)[idx] = (uint16_t)bits;
+  else
+    ((uint32_t*)base)[idx] = bits;
+}
+
+static void uo_unit_span(int32_t gran, int32_t g, int64_t in, int64_t t, int64_t* j0, int64_t* j1) {
+  if (gran == UO_GRAN_ROW) {
+    *j0 = t * g;
+    *j1 = (t + 1) * g;
+  } else {
+    *j0 = 0;
+    *j1 = in;
+  }
+}
+
+int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, int32_t layer,
+                       int32_t gran, int32_t g, int64_t t_begin, int64_t t_end,
+                       const int32_t* ncols, const int64_t* offsets, int32_t M, int32_t hash_kind,
+                       uint64_t seed, void* sketch) {
+  int64_t t;
+  for (t = t_begin; t < t_end; t++) {
+    int64_t j0, j1, j, o, n, k = 0;
+    uint32_t *wb, *pos, *cells;
+    int32_t st;
+    int64_t c;
+    uo_unit_span(gran, g, in, t, &j0, &j1);
+    n = (j1 - j0) * out;
+    wb = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)n);
+    pos = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)n);
+    cells = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)M * (size_t)ncols[t]);
+    for (o = 0; o < out; o++) /* stream W in its row-major order */
+      for (j = j0; j < j1; j++) {
+        wb[k] = uo_load(dtype, W, o * in + j);
+        pos[k] = (uint32_t)((j - j0) * out + o);
+        k++;
+      }
+    st = uo_sketch_unit(dtype, wb, pos, n, hash_kind, seed, (uint32_t)layer, (uint32_t)t, M,
+                        (uint32_t)ncols[t], cells);
+    if (st == UO_OK)
+      for (c = 0; c < (int64_t)M * ncols[t]; c++) uo_store(dtype, sketch, offsets[t] + c, cells[c]);
+    free(wb);
+    free(pos);
+    free(cells);
+    if (st != UO_OK) return st;
+  }
+  return UO_OK;
+}
+
+static uint32_t uo_weight_at(int32_t dtype, const void* sketch, int64_t out, int64_t in,
+                             int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
+                             const int64_t* offsets, int32_t M, int32_t hash_kind, uint64_t seed,
+                             int64_t o, int64_t j) {
+  int64_t t = (gran == UO_GRAN_ROW) ? j / g : 0;
+  int64_t j0 = (gran == UO_GRAN_ROW) ? t * g : 0;
+  uint32_t p = (uint32_t)((j - j0) * out + o);
+  uint32_t N = (uint32_t)ncols[t];
+  uint32_t bonded[8];
+  int32_t i;
+  (void)in;
+  for (i = 0; i < M; i++)
+    bonded[i] = uo_load(dtype, sketch,
+                        offsets[t] + (int64_t)i * N +
+                            uo_hash_index(hash_kind, seed, (uint32_t)layer, (uint32_t)t, i, p, N));
+  return uo_retrieve(dtype, bonded, M);
+}
+
+/* W'[o, j] for o in [o_begin, o_end), all j; w_out is [(o_end-o_begin), in] raw bits. */
+int32_t uo_reconstruct_rows(int32_t dtype, const void* sketch, int64_t out, int64_t in,
+                            int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
+                            const int64_t* offsets, int32_t M, int32_t hash_kind, uint64_t seed,
+                            int64_t o_begin, int64_t o_end, void* w_out) {
+  int64_t o, j;
+  if (o_begin < 0 || o_end > out || o_begin > o_end) return UO_ESHAPE;
+  for (o = o_begin; o < o_end; o++)
+    for (j = 0; j < in; j++)
+      uo_store(dtype, w_out, (o - o_begin) * in + j,
+               uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets, M, hash_kind,
+                            seed, o, j));
+  return UO_OK;
+}
+
+/* W'[o, j] for an explicit list of (o, j) pairs (sampled parity at full size). */
+int32_t uo_reconstruct_entries(int32_t dtype, const void* sketch, int64_t out, int64_t in,
+                               int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
+                               const int64_t* offsets, int32_t M, int32_t hash_kind, uint64_t seed,
+                               const int64_t* oj, int64_t n, uint32_t* out_bits) {
+  int64_t k;
+  for (k = 0; k < n; k++)
+    out_bits[k] = uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets, M, hash_kind,
+                               seed, oj[2 * k], oj[2 * k + 1]);
+  return UO_OK;
+}
+
+/* Linear ("computation stage follows the original inference step"):
+ * y[tok, o] = sum_j x[tok, j] * w'(o, j) in fp64, o in [o_begin, o_end).
+ * x: [T, in] doubles; y: [T, o_end - o_begin]. */
+int32_t uo_linear_rows(int32_t dtype, const void* sketch, int64_t out, int64_t in, int32_t layer,
+                       int32_t gran, int32_t g, const int32_t* ncols, const int64_t* offsets,
+                       int32_t M, int32_t hash_kind, uint64_t seed, const double* x, int64_t T,
+                       int64_t o_begin, int64_t o_end, double* y) {
+  int64_t o, j, tok;
+  double* wrow;
+  if (o_begin < 0 || o_end > out || o_begin > o_end) return UO_ESHAPE;
+  wrow = (double*)malloc(sizeof(double) * (size_t)in);
+  for (o = o_begin; o < o_end; o++) {
+    for (j = 0; j < in; j++)
+      wrow[j] = uo_value(dtype, uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets,
+                                             M, hash_kind, seed, o, j));
+    for (tok = 0; tok < T; tok++) {
+      double s = 0.0;
+      for (j = 0; j < in; j++) s += x[tok * in + j] * wrow[j];
+      y[tok * (o_end - o_begin) + (o - o_begin)] = s;
+    }
+  }
+  free(wrow);
+  return UO_OK;
+}
+
+/* Peak memory model: sum_i Mem(Sketch_i) + max_i Mem(Layer_i). */
+int64_t uo_peak_memory(const int64_t* layer_bytes, const int64_t* sketch_bytes, int32_t n) {
+  int64_t s = 0, mx = 0;
+  int32_t i;
+  for (i = 0; i < n; i++) {
+    s += sketch_bytes[i];
+    if (layer_bytes[i] > mx) mx = layer_bytes[i];
+  }
+  return s + mx;
+}

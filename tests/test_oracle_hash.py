@@ -1,0 +1,64 @@
+"""The hash contract USK-X.  The paper fixes only "independent hash
+functions" of a storage-free address, so individual index values are our
+definition ("parity unpinned"); the statistics are pinned in test_oracle_stats.py.  Here a
+second implementation written from DESIGN.md's text checks the C oracle, and the frozen vectors
+in tests/golden/hash_vectors.json (written by tests/golden/gen_golden.py, which calls only
+oracle/) guard the contract against accidental change."""
+import json
+import os
+
+import numpy as np
+
+M64 = (1 << 64) - 1
+M32 = (1 << 32) - 1
+
+
+def splitmix64(x):
+    x = (x + 0x9E3779B97F4A7C15) & M64
+    z = x
+    z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & M64
+    z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & M64
+    return z ^ (z >> 31)
+
+
+def fmix32(h):
+    h ^= h >> 16
+    h = (h * 0x85EBCA6B) & M32
+    h ^= h >> 13
+    h = (h * 0xC2B2AE35) & M32
+    return h ^ (h >> 16)
+
+
+def usk_x(seed, layer, t, row, p, N):
+    rho = splitmix64(seed) & M32
+    K = splitmix64(seed ^ splitmix64((layer << 32) | t)) & M32
+    a = (splitmix64((seed + 0x100 + row) & M64) & M32) | 1
+    h = fmix32(p ^ rho) ^ K
+    return (((h * a) & M32) * N) >> 32
+
+
+def test_contract_second_implementation(orc):
+    rng = np.random.default_rng(0)
+    for _ in range(3000):
+        seed = int(rng.integers(0, 2**63)) * 2 + int(rng.integers(0, 2))
+        layer, t = int(rng.integers(0, 300)), int(rng.integers(0, 20000))
+        row, p = int(rng.integers(0, 8)), int(rng.integers(0, 2**32))
+        N = int(rng.integers(1, 2**31))
+        assert orc.hash_index(0, seed, layer, t, row, p, N) == usk_x(seed, layer, t, row, p, N)
+        assert orc.hash_index(1, seed, layer, t, row, p, N) == p % N
+
+
+def test_frozen_vectors(orc):
+    path = os.path.join(os.path.dirname(__file__), "golden", "hash_vectors.json")
+    vec = json.load(open(path))
+    for (seed, layer, t, row, p, N, idx) in vec["vectors"]:
+        assert orc.hash_index(0, seed, layer, t, row, p, N) == idx
+
+
+def test_rows_independent_of_M(orc):
+    """Adding rows never changes earlier rows (needed by SPEC.md:104 row monotonicity)."""
+    w = np.random.default_rng(1).standard_normal(500).astype(np.float32)
+    pos = np.arange(500, dtype=np.uint32)
+    c2 = orc.sketch_unit(w.view(np.uint32), pos, 2, 37, seed=4)
+    c5 = orc.sketch_unit(w.view(np.uint32), pos, 5, 37, seed=4)
+    np.testing.assert_array_equal(c5[:2], c2)
