@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark of the B200-native UltraSketchLLM sketch hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[2], "c3"): Llama-3.2-1B, all 112 linear layers (16 blocks x
+q,k,v,o,gate,up,down), synthetic random bf16 weights (synth recipe), ROW granularity, M = 3 rows,
+0.5 bits per weight, uniform importance.  One STEP = one batch-1 decode token = the 112 fused
+sketch-GEMV launches (usk_linear, T = 1) in model order, replayed as one CUDA graph.  L2 is
+flushed (256 MB write) before every timed step, so the 60.8 MB sketch is re-read from HBM.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl usk|reference]
+
+N > 1 (torchrun, one rank per GPU, NCCL): every linear's output features are sharded over the
+ranks and the fp32 y shards are all-gathered with NCCL after each linear (strong scaling).
+--impl reference times the CPU oracle (oracle/, plain C) on a bounded sample of the same
+workload, on rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "fused sketch-GEMV decode tokens/s + weights reconstructed/s, Llama-3.2-1B @0.5 bpw"
+UNIT = "tokens/s"
+BPW, ROWS, SEED = 0.5, 3, 0x5EED000000000003
+CFG = 3  # synth seed namespace (BASELINE.json configs[2])
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + self.FIELDS,
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = set()
+        for s in self.samples:
+            for k, n in enumerate(names):
+                if len(s) > 4 + k and s[4 + k].lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- CPU oracle leg
+def oracle_decode_sample(shapes, weights_for_layer, budget_s=12.0):
+    """Time the CPU oracle's fp64 sketch-GEMV (reconstruct-on-the-fly + FMA, oracle/usk_oracle.c)
+    on a bounded sample: the 7 linears of block 0, output rows in round-robin until ~budget_s of
+    oracle compute has run.  Returns tokens/s extrapolated by weights/s over all 112 linears."""
+    import oracle
+    blk = shapes[:7]
+    opl = oracle.plan(blk, BPW, M=ROWS, dtype=oracle.BF16, seed=SEED)
+    sk = np.zeros(opl.total_cells, np.uint16)
+    for l in range(7):
+        oracle.build_layer(opl, l, weights_for_layer(l), sk)
+    xs = [synth.vector(i, seed=1000 + l)[0].astype(np.float64) for l, (o, i) in enumerate(blk)]
+    done_w, spent, row = 0, 0.0, 0
+    while spent < budget_s:
+        for l, (o, i) in enumerate(blk):
+            r0 = (row * 8) % o
+            t0 = time.perf_counter()
+            oracle.linear_rows(opl, sk, l, xs[l], r0, r0 + 8)
+            spent += time.perf_counter() - t0
+            done_w += 8 * i
+        row += 1
+    wps = done_w / spent
+    total_w = sum(o * i for o, i in shapes)
+    return {"value": wps / total_w, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"oracle fp64 sketch-GEMV of {done_w} weights (8-row slices of the 7 block-0 linears, "
+                      f"{spent:.1f} s single-threaded), extrapolated to the 112-linear token by weights/s",
+            "weights_per_s": wps}
+
+
+def host_block0_weights(shapes):
+    import torch
+    def get(l):
+        o, i = shapes[l]
+        w = synth.torch_weights_bf16(o, i, synth.seed_for(CFG, 0, l), "cuda")
+        return w.cpu().view(torch.int16).numpy().view(np.uint16).copy()
+    return get
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import torch
+    shapes = synth.llama32_1b_shapes()
+    if torch.cuda.is_available():
+        getw = host_block0_weights(shapes)
+    else:
+        getw = lambda l: synth.weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, 0, l))
+    per_step = []
+    budget = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    for k in range(args.warmup + args.steps):
+        r = oracle_decode_sample(shapes, getw, budget_s=budget)
+        if k >= args.warmup:
+            per_step.append(r)
+    v = float(np.mean([r["value"] for r in per_step]))
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": "c3: Llama-3.2-1B 112 linears, batch-1 decode, 0.5 bpw, M=3, bf16 weights",
+                       "bpw": BPW, "rows": ROWS},
+            "cpu_baseline": {**{k: per_step[-1][k] for k in ("kind", "cores", "sample")}, "value": v, "unit": UNIT},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- GPU leg
+def run_usk(args):
+    import torch
+    import torch.distributed as dist
+    from paper_2506_17255_b200 import usk
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    peaks = _peaks()
+    shapes = synth.llama32_1b_shapes()
+    L = len(shapes)
+    numel = sum(o * i for o, i in shapes)
+
+    # ---- plan + build (layer-sharded across ranks, then a one-time replication of the sketch)
+    plan = usk.plan_allocation(shapes, bpw=BPW, rows=ROWS, seed=SEED)
+    sketch = plan.new_sketch(dev)
+    sketch.zero_()
+    owned = [l for l in range(L) if (l // 7) % world == rank]       # blocks round-robin over ranks
+    build_ms = 0.0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for b in sorted({l // 7 for l in owned}):
+        ids = [l for l in owned if l // 7 == b]
+        ws = [synth.torch_weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, b, l % 7), dev) for l in ids]
+        torch.cuda.synchronize()
+        ev0.record()
+        usk.build(plan, ws, sketch, layer_ids=ids)
+        ev1.record()
+        torch.cuda.synchronize()
+        build_ms += ev0.elapsed_time(ev1)
+        del ws
+    usk.check(plan)
+    owned_w = sum(shapes[l][0] * shapes[l][1] for l in owned)
+    if world > 1:
+        cb = 2  # bf16 cells
+        for l in range(L):
+            li = plan.layers[l]
+            src = (l // 7) % world
+            dist.broadcast(sketch[li.cell_begin * cb:(li.cell_begin + li.n_cells) * cb], src=src)
+        torch.cuda.synchronize()
+
+    # ---- decode buffers: fixed synthetic x per linear, y shards
+    def shard(o):
+        return (o * rank) // world, (o * (rank + 1)) // world
+    in_off = np.cumsum([0] + [i for o, i in shapes])
+    out_off = np.cumsum([0] + [o for o, i in shapes])
+    X = torch.empty(int(in_off[-1]), dtype=torch.bfloat16, device=dev)
+    for l, (o, i) in enumerate(shapes):
+        X[in_off[l]:in_off[l + 1]] = synth.torch_vector(i, 1000 + l, dev, torch.bfloat16)[0]
+    Y = torch.zeros(int(out_off[-1]), dtype=torch.float32, device=dev)
+    Yshard = [torch.empty(shard(o)[1] - shard(o)[0], dtype=torch.float32, device=dev) for o, i in shapes]
+    wss = [usk.new_workspace(plan, l, 1, *shard(o), device=dev) for l, (o, i) in enumerate(shapes)]
+    xs = [X[in_off[l]:in_off[l + 1]].view(1, -1) for l in range(L)]
+    ys_full = [Y[out_off[l]:out_off[l + 1]] for l in range(L)]
+
+    def step():
+        for l, (o, i) in enumerate(shapes):
+            o0, o1 = shard(o)
+            if world == 1:
+                usk.linear(plan, sketch, l, xs[l], ys_full[l].view(1, -1), wss[l], o0, o1)
+            else:
+                usk.linear(plan, sketch, l, xs[l], Yshard[l].view(1, -1), wss[l], o0, o1)
+                dist.all_gather_into_tensor(ys_full[l], Yshard[l])
+
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for _ in range(2):
+            step()  # warm (module load, attributes)
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    use_graph = True
+    usk.launch_count(reset=True)
+    try:
+        with torch.cuda.graph(graph, stream=stream):
+            step()
+    except Exception as e:  # NCCL capture unsupported -> eager steps
+        use_graph = False
+        print(f"[bench] graph capture failed ({e}); timing eager steps", file=sys.stderr)
+    launches_per_step = usk.launch_count(reset=True) if use_graph else L
+
+    def replay():
+        if use_graph:
+            graph.replay()
+        else:
+            with torch.cuda.stream(stream):
+                step()
+
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+    for _ in range(max(3, args.warmup)):
+        replay()
+    torch.cuda.synchronize()
+
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for k in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(k & 0xFF)          # untimed L2 flush
+                starts[k].record(stream)
+                replay()
+                ends[k].record(stream)
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = float(sum(step_ms))
+    if world > 1:
+        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    tok_s = 1000.0 / ms_per_step
+
+    # ---- per-launch kernel durations (same launches, eager, each bracketed by events behind a
+    #      GPU sleep so the host enqueue latency is hidden) -> roofline of the dominant kernel
+    kern_ms = np.zeros(L)
+    reps = 5
+    with torch.cuda.stream(stream):
+        for rep in range(reps):
+            for l, (o, i) in enumerate(shapes):
+                o0, o1 = shard(o)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                torch.cuda._sleep(20000)
+                a.record(stream)
+                usk.linear(plan, sketch, l, xs[l], (ys_full[l] if world == 1 else Yshard[l]).view(1, -1), wss[l], o0, o1,
+                           stream=stream)
+                b.record(stream)
+                b.synchronize()
+                kern_ms[l] += a.elapsed_time(b) / reps
+    w_rank = sum((shard(o)[1] - shard(o)[0]) * i for o, i in shapes)
+    sum_kern = float(kern_ms.sum())
+    clk = clocks.summary()
+    f_peak = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+    gather_peak = 148 * 32 * f_peak / ROWS / 1e9          # Gweight/s: M LDS lookups per weight
+    achieved = w_rank / (sum_kern * 1e-3) / 1e9
+    sketch_bytes = plan.info["total_cells"] * 2
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        traffic = json.load(open(tp)).get("k_gemv_fast_bytes_per_launch")
+
+    # ---- standalone reconstruct throughput (weights reconstructed/s, HBM-bound kernel)
+    scratch = torch.empty(max(o * i for o, i in shapes), dtype=torch.bfloat16, device=dev)
+    rec_ms = 0.0
+    for l, (o, i) in enumerate(shapes):
+        flush.fill_(1)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(20000)
+        a.record()
+        usk.reconstruct(plan, sketch, l, scratch[:o * i].view(o, i))
+        b.record()
+        b.synchronize()
+        rec_ms += a.elapsed_time(b)
+    rec_wps = numel / (rec_ms * 1e-3)
+
+    # ---- end-to-end through the binding: pinned host x -> device, 112 linears, y -> pinned host
+    Xh = X.cpu().pin_memory()
+    Yh = torch.empty(Y.numel(), dtype=torch.float32).pin_memory()
+    g2 = torch.cuda.CUDAGraph()
+    e2e_graph = True
+    try:
+        with torch.cuda.graph(g2, stream=stream):
+            X.copy_(Xh, non_blocking=True)
+            step()
+            Yh.copy_(Y, non_blocking=True)
+    except Exception:
+        e2e_graph = False
+    e_ms = []
+    for k in range(max(3, args.warmup) + args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(2)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            if e2e_graph:
+                g2.replay()
+            else:
+                X.copy_(Xh, non_blocking=True)
+                step()
+                Yh.copy_(Y, non_blocking=True)
+            b.record(stream)
+        b.synchronize()
+        if k >= max(3, args.warmup):
+            e_ms.append(a.elapsed_time(b))
+    e2e_ms = float(np.mean(e_ms))
+    if world > 1:
+        t = torch.tensor([e2e_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = oracle_decode_sample(shapes, host_block0_weights(shapes), budget_s=args.cpu_budget)
+        cpu.pop("weights_per_s", None)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": tok_s, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (seeded random bf16 weights shaped like Llama-3.2-1B; synth/ recipe)",
+            "config": {"workload": "c3: Llama-3.2-1B all 112 linears, batch-1 decode via fused sketch-GEMV",
+                       "bpw": BPW, "rows": ROWS, "granularity": "row (1 input dim per unit)", "classes": 1,
+                       "sketch_MB": sketch_bytes / 1e6, "weights": numel, "l2": "flushed (256 MB write) before each step",
+                       "parallelism": f"output-sharded x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                       "graph": use_graph},
+            "weights_reconstructed_per_s": tok_s * numel,
+            "reconstruct_standalone": {"weights_per_s": rec_wps, "GB_per_s_written": rec_wps * 2 / 1e9,
+                                       "hbm_frac": rec_wps * (2 + 2 * BPW / 16) / 1e9 / peaks["hbm_gbs"]},
+            "build": {"ms": build_ms, "weights_per_s": owned_w / (build_ms * 1e-3),
+                      "GB_per_s": owned_w * (2 + BPW / 8) / (build_ms * 1e-3) / 1e9},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": gather_peak, "unit": "Gweight/s",
+                         "frac": achieved / gather_peak, "traffic": traffic,
+                         "kernel": "k_gemv_fast", "peak_basis": f"M={ROWS} shared-memory lookups per weight at 1 LDS "
+                         f"wavefront/clk/SM x 148 SMs x {f_peak / 1e6:.0f} MHz (DESIGN.md §Rooflines)",
+                         "kernel_share_of_step": sum_kern / ms_per_step,
+                         "hbm_frac": sketch_bytes / (sum_kern * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "e2e": {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 2),
+                    "d2h_bytes_per_step": int(Yh.numel() * 4)},
+            "gpu_launches": int(launches_per_step * args.steps),
+            "clocks": clk,
+        }
+        if cpu is not None:
+            line["cpu_baseline"] = cpu
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="usk", choices=["usk", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_usk(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

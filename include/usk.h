@@ -1,0 +1,201 @@
+/*
+ * usk.h -- C ABI of the B200-native UltraSketchLLM sketch engine (arXiv 2506.17255).
+ *
+ * The library implements the paper's index-free multi-row AbsMaxMin sketch hot path on
+ * sm_100a: importance-aware space allocation (§3.4), the sketch build (§3.2 select/update,
+ * §3.5 "AbsMin Scatter operator"), and the query fused into the consuming linear layer
+ * (§3.1 decompression -> computation; §3.5 "modify the linear layer correspondingly").
+ *
+ * Conventions (all entry points):
+ *   - Plain pointers and sizes only.  "device" = CUDA device memory of the current device;
+ *     "host" = ordinary host memory.  Every large buffer is CALLER-OWNED.
+ *   - The plan is an opaque, library-owned, immutable handle (usk_plan_destroy frees it).
+ *   - usk_build / usk_reconstruct / usk_linear never allocate, are asynchronous on `stream`
+ *     (NULL = legacy default stream) and may run concurrently on different streams with one
+ *     plan.  usk_plan_allocation synchronises `stream` once (launch geometry lives on host).
+ *   - Return USK_OK (0) or an error code; no exception or abort crosses the ABI.  A one-line
+ *     diagnostic of the last failure on the calling thread is in usk_last_error().
+ *   - Results are a pure function of the inputs: sketch bytes and reconstructions do not
+ *     depend on launch configuration, stream, GPU count or thread interleaving
+ *     (order independence); usk_linear is deterministic for fixed inputs.
+ *
+ * Citations: PAPER.md:<line> (section / equation).  Readings where the paper is silent are
+ * listed in DESIGN.md ("ledger" L1..L24) and referenced below.
+ */
+#ifndef USK_H
+#define USK_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define USK_API __attribute__((visibility("default")))
+#else
+#define USK_API
+#endif
+
+typedef struct CUstream_st* usk_stream; /* == cudaStream_t */
+
+typedef enum {
+  USK_OK = 0,
+  USK_EINVAL = 1,       /* null pointer, bad enum, rows not in [1,8], bpw <= 0 or non-finite,
+                           dims_per_unit does not divide in_features, negative / NaN saliency,
+                           misaligned pointer (16 B required for x, y, weights, sketch, w_out) */
+  USK_ESHAPE = 2,       /* zero-size layer, layer id / row range / output range out of bounds,
+                           count mismatch, workspace too small */
+  USK_EBUDGET = 3,      /* infeasible floor: sum_c n_c * M * min_cols > T cells */
+  USK_ENONFINITE = 4,   /* the build saw NaN or +-Inf (sticky; reported by usk_check) --
+                           +Inf is the empty-cell sentinel (L4) */
+  USK_ECUDA = 5,        /* CUDA launch / runtime failure (text in usk_last_error) */
+  USK_EUNSUPPORTED = 6  /* valid request with no kernel (e.g. T > 1 with fp32 weights) */
+} usk_status;
+
+typedef enum { USK_F32 = 0, USK_BF16 = 1 } usk_dtype;
+
+/* Sketch-space granularity: ROW = one sketch per input dimension of a
+ * weight matrix (per `dims_per_unit` input dims; L6/L7); LAYER = one per matrix. */
+typedef enum { USK_GRAN_ROW = 0, USK_GRAN_LAYER = 1 } usk_granularity;
+
+/* Hash family (Eq. 3; contract in DESIGN.md "Hash contract"):
+ * USK_HASH_X = our independent multiply-high family; USK_HASH_IDENTITY = p mod N (SPEC.md:54,
+ * tests only). */
+typedef enum { USK_HASH_X = 0, USK_HASH_IDENTITY = 1 } usk_hash;
+
+/* One linear layer, PyTorch layout: weight is row-major [out_features, in_features]. */
+typedef struct {
+  int64_t out_features;
+  int64_t in_features;
+} usk_shape;
+
+typedef struct {
+  double bpw;            /* budget in bits per weight (Table 1 "Equivalent Bits", PAPER.md:376;
+                            states are raw, L3) */
+  int32_t rows;          /* M, sketch rows, [1, 8]; paper default 3 */
+  int32_t granularity;   /* usk_granularity */
+  int32_t dims_per_unit; /* g >= 1, ROW only; must divide in_features (L7) */
+  int32_t n_classes;     /* C >= 1 importance categories; 0 = default
+                            (4 when saliency is given, else 1) */
+  int32_t min_cols;      /* floor of columns per row, >= 1 (L12) */
+  int32_t hash;          /* usk_hash */
+  int32_t dtype;         /* usk_dtype of weights == dtype of sketch states (L3) */
+  uint64_t seed;         /* hash seed ("fixing random seed in hash functions") */
+} usk_params;
+
+typedef struct usk_plan usk_plan;
+
+typedef struct {
+  int32_t n_layers;
+  int32_t rows;
+  int32_t n_classes;
+  int32_t dtype;
+  int64_t n_units;
+  int64_t total_cells;    /* sum over units of M * N_u */
+  int64_t sketch_bytes;   /* bytes the caller must allocate for the sketch (cells + tail pad) */
+  int64_t numel;          /* weights covered */
+  int64_t budget_bits;    /* sum of floor(bpw * numel) over budget scopes */
+  int64_t achieved_bits;  /* states * state bits + charged class-map bits (<= budget_bits) */
+} usk_plan_info;
+
+typedef struct {
+  int64_t out_features;
+  int64_t in_features;
+  int64_t unit_begin;     /* first global unit id of the layer */
+  int64_t n_units;
+  int64_t cell_begin;     /* first cell of the layer in the sketch */
+  int64_t n_cells;
+  int64_t budget_bits;    /* ROW: floor(bpw * numel_l); LAYER: model budget on layer 0, else 0 */
+  int64_t meta_bits;      /* charged class-map bits (ROW with C > 1: U_l * ceil(log2 C)) */
+  int64_t cells_T;        /* cells available to the scope (ROW per layer; LAYER on layer 0) */
+  int64_t achieved_bits;  /* states of this layer * state bits + meta_bits */
+} usk_layer_info;
+
+/* Importance metric, Eq. 7: I[j] = (1/N) sum_k A[k, j]^2.
+ * A: device, row-major [N, d] of dtype a_dtype (USK_F32 or USK_BF16); I_out: device float[d].
+ * fp32 accumulation in a fixed order (deterministic).  Errors: EINVAL (null, dtype), ESHAPE
+ * (N < 1 or d < 1), ECUDA. */
+USK_API usk_status usk_importance(const void* A, int32_t a_dtype, int64_t N, int64_t d, float* I_out,
+                          usk_stream stream);
+
+/* Salient-weight-aware sketch space allocation (§3.4; categories
+ * PAPER.md:523-528), computed on the device: per-unit scores -> 2^24 fixed point -> rank ->
+ * equal-count classes -> per-class columns (proportional share, water-filled floor, largest
+ * remainder) -> device-wide exclusive prefix scan of unit sizes.
+ *   layers:   host array [n_layers] of shapes; list position = hash layer id.
+ *   saliency: host array [n_layers] of DEVICE pointers to float[in_features] scores (>= 0),
+ *             or NULL (uniform).  An individual NULL entry means uniform for that layer.
+ *   params:   host.
+ *   plan_out: receives the new plan.  On error *plan_out is NULL.
+ * Synchronises `stream`.  Errors: EINVAL, ESHAPE, EBUDGET, ECUDA. */
+USK_API usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers,
+                               const float* const* saliency, const usk_params* params,
+                               usk_plan** plan_out, usk_stream stream);
+
+USK_API usk_status usk_plan_query(const usk_plan* plan, usk_plan_info* out);
+USK_API usk_status usk_plan_layer(const usk_plan* plan, int32_t layer, usk_layer_info* out);
+
+/* Host copies of one layer's plan arrays (parity tests): cls[n_units], ncols[n_units],
+ * nrows[n_units], offsets[n_units + 1] (absolute cells).  Any output may be NULL.  Syncs. */
+USK_API usk_status usk_plan_export(const usk_plan* plan, int32_t layer, uint8_t* cls, int32_t* ncols,
+                           uint8_t* nrows, int64_t* offsets);
+
+/* Build (§3.2: select Eq. 3, update Eq. 4; "AbsMin Scatter"):
+ *   S[u, i, c] = the colliding weight of minimum |.| (ties -> non-negative, L2),
+ *   +Inf when no weight maps to the cell.
+ *   weights:   host array [n] of DEVICE pointers, weights[k] = row-major [out, in] of the plan
+ *              dtype for layer layer_ids[k].
+ *   layer_ids: host int32[n], distinct, or NULL = layers 0..n-1 (layer-sharded builds pass a
+ *              subset; only those layers' cells are written).
+ *   sketch:    device, >= sketch_bytes, 16-B aligned; cells of layer l at
+ *              [cell_begin, cell_begin + n_cells), unit-major, row-major (i, c) inside a unit.
+ * Non-finite weights set the plan's sticky flag (usk_check -> USK_ENONFINITE). */
+USK_API usk_status usk_build(const usk_plan* plan, const void* const* weights, const int32_t* layer_ids,
+                     int32_t n, void* sketch, usk_stream stream);
+
+/* Reconstruction / decompression (Eq. 5; §3.1):
+ *   w'(o, j) = the bonded cell of maximum |.| over the M rows (ties -> non-negative, L1/L2).
+ *   Writes rows [row_begin, row_end) of W' (output features) as a row-major device matrix of
+ *   the plan dtype with leading dimension ld_out (elements, >= in_features) at w_out. */
+USK_API usk_status usk_reconstruct(const usk_plan* plan, const void* sketch, int32_t layer,
+                           int64_t row_begin, int64_t row_end, void* w_out, int64_t ld_out,
+                           usk_stream stream);
+
+/* Workspace bytes usk_linear needs for (layer, T, output range).  0 on invalid arguments. */
+USK_API size_t usk_linear_workspace_bytes(const usk_plan* plan, int32_t layer, int64_t T,
+                                  int64_t out_begin, int64_t out_end);
+
+/* Sketch-fused linear (PAPER.md:183-189 decompress -> compute; §3.5 modified linear):
+ *   y[t, o - out_begin] = sum_j x[t, j] * w'(o, j),  o in [out_begin, out_end), t < T.
+ *   x: device [T, in_features] of x_dtype; y: device [T, out_end - out_begin] of y_dtype.
+ *   T <= 8 : sketch-GEMV, W' rebuilt in registers and never stored; fp32 accumulation and a
+ *            fixed-order split-K reduction (deterministic).
+ *   T >  8 : bf16 plans only -- W' rows rebuilt into `workspace` (the paper's decompression),
+ *            then a tcgen05 tensor-core GEMM with fp32 accumulation.
+ *   workspace: device, >= usk_linear_workspace_bytes(...), 16-B aligned; MUST be zero-filled
+ *   before its first use -- every call leaves it zero-filled again. */
+USK_API usk_status usk_linear(const usk_plan* plan, const void* sketch, int32_t layer, const void* x,
+                      int32_t x_dtype, int64_t T, void* y, int32_t y_dtype, int64_t out_begin,
+                      int64_t out_end, void* workspace, size_t workspace_bytes,
+                      usk_stream stream);
+
+/* Synchronises `stream`, returns and clears the plan's sticky device error (USK_ENONFINITE),
+ * or USK_ECUDA on a CUDA error, else USK_OK. */
+USK_API usk_status usk_check(const usk_plan* plan, usk_stream stream);
+
+USK_API void usk_plan_destroy(usk_plan* plan);
+
+USK_API const char* usk_status_string(usk_status status);
+USK_API const char* usk_last_error(void);
+
+/* Number of kernel launches this thread issued through the ABI since the last reset
+ * (bench evidence for "gpu_launches"). */
+USK_API int64_t usk_launch_count(int32_t reset);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* USK_H */

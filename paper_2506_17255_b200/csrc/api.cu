@@ -1,0 +1,311 @@
+// api.cu -- the C ABI (include/usk.h): validation, plan lifetime, dispatch.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+
+namespace usk {
+
+static thread_local std::string g_last_error;
+static thread_local int64_t g_launches = 0;
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+usk_status fail(usk_status st, const std::string& msg) {
+  g_last_error = msg;
+  return st;
+}
+usk_status cuda_fail(cudaError_t e, const char* what) {
+  g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return USK_ECUDA;
+}
+void count_launch(int n) { g_launches += n; }
+
+static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+static int ceil_log2(int c) {
+  int b = 0;
+  while ((1 << b) < c) ++b;
+  return b;
+}
+
+static void free_plan(usk_plan* p) {
+  if (!p) return;
+  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R, p->d_err};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  delete p;
+}
+
+}  // namespace usk
+
+using namespace usk;
+
+extern "C" {
+
+const char* usk_status_string(usk_status s) {
+  switch (s) {
+    case USK_OK: return "USK_OK";
+    case USK_EINVAL: return "USK_EINVAL";
+    case USK_ESHAPE: return "USK_ESHAPE";
+    case USK_EBUDGET: return "USK_EBUDGET";
+    case USK_ENONFINITE: return "USK_ENONFINITE";
+    case USK_ECUDA: return "USK_ECUDA";
+    case USK_EUNSUPPORTED: return "USK_EUNSUPPORTED";
+  }
+  return "USK_UNKNOWN";
+}
+
+const char* usk_last_error(void) { return g_last_error.c_str(); }
+
+int64_t usk_launch_count(int32_t reset) {
+  int64_t v = g_launches;
+  if (reset) g_launches = 0;
+  return v;
+}
+
+usk_status usk_importance(const void* A, int32_t a_dtype, int64_t N, int64_t d, float* I_out, usk_stream stream) {
+  if (!A || !I_out) return fail(USK_EINVAL, "usk_importance: null pointer");
+  if (a_dtype != USK_F32 && a_dtype != USK_BF16) return fail(USK_EINVAL, "usk_importance: dtype");
+  if (N < 1 || d < 1) return fail(USK_ESHAPE, "usk_importance: N and d must be >= 1");
+  return launch_importance(A, a_dtype, N, d, I_out, (cudaStream_t)stream);
+}
+
+usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const float* const* saliency,
+                               const usk_params* params, usk_plan** plan_out, usk_stream stream) {
+  if (!plan_out) return fail(USK_EINVAL, "usk_plan_allocation: plan_out is null");
+  *plan_out = nullptr;
+  if (!layers || !params) return fail(USK_EINVAL, "usk_plan_allocation: null layers/params");
+  if (n_layers < 1) return fail(USK_ESHAPE, "usk_plan_allocation: n_layers < 1");
+  const usk_params& P = *params;
+  if (!(P.bpw > 0.0) || !std::isfinite(P.bpw)) return fail(USK_EINVAL, "bpw must be finite and > 0");
+  if (P.rows < 1 || P.rows > 8) return fail(USK_EINVAL, "rows must be in [1, 8]");
+  if (P.granularity != USK_GRAN_ROW && P.granularity != USK_GRAN_LAYER) return fail(USK_EINVAL, "granularity");
+  if (P.hash != USK_HASH_X && P.hash != USK_HASH_IDENTITY) return fail(USK_EINVAL, "hash");
+  if (P.dtype != USK_F32 && P.dtype != USK_BF16) return fail(USK_EINVAL, "dtype");
+  if (P.min_cols < 1) return fail(USK_EINVAL, "min_cols must be >= 1");
+  if (P.n_classes < 0 || P.n_classes > 64) return fail(USK_EINVAL, "n_classes must be in [0, 64]");
+  const int g = P.granularity == USK_GRAN_ROW ? P.dims_per_unit : 1;
+  if (P.granularity == USK_GRAN_ROW && g < 1) return fail(USK_EINVAL, "dims_per_unit must be >= 1");
+  for (int l = 0; l < n_layers; ++l) {
+    if (layers[l].out_features < 1 || layers[l].in_features < 1)
+      return fail(USK_ESHAPE, "layer " + std::to_string(l) + " has a zero dimension");
+    if (layers[l].out_features * layers[l].in_features > 0xFFFFFFFFll)
+      return fail(USK_ESHAPE, "layer " + std::to_string(l) + " exceeds 2^32 weights (32-bit positions)");
+    if (P.granularity == USK_GRAN_ROW && layers[l].in_features % g != 0)
+      return fail(USK_EINVAL, "dims_per_unit does not divide in_features of layer " + std::to_string(l));
+  }
+  usk_plan* pl = new (std::nothrow) usk_plan();
+  if (!pl) return fail(USK_ECUDA, "out of host memory");
+  pl->n_layers = n_layers;
+  pl->M = P.rows;
+  pl->gran = P.granularity;
+  pl->g = g;
+  pl->C = P.n_classes > 0 ? P.n_classes : (saliency ? 4 : 1);
+  pl->min_cols = P.min_cols;
+  pl->hash = P.hash;
+  pl->dtype = P.dtype;
+  pl->bpw = P.bpw;
+  pl->seed = P.seed;
+  const int state_bits = P.dtype == USK_BF16 ? 16 : 32;
+  pl->hc.rho = (uint32_t)splitmix64(P.seed);
+  for (int i = 0; i < 8; ++i) pl->hc.a[i] = ((uint32_t)splitmix64(P.seed + 0x100ull + (uint64_t)i)) | 1u;
+  cudaGetDevice(&pl->device);
+
+  pl->layers.resize(n_layers);
+  int64_t U = 0, numel_all = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    LayerGeom& L = pl->layers[l];
+    L = LayerGeom{};
+    L.out = layers[l].out_features;
+    L.in = layers[l].in_features;
+    L.unit_begin = U;
+    L.n_units = P.granularity == USK_GRAN_ROW ? L.in / g : 1;
+    L.scope = P.granularity == USK_GRAN_ROW ? l : 0;
+    U += L.n_units;
+    numel_all += L.out * L.in;
+    pl->max_out = std::max<int64_t>(pl->max_out, L.out);
+  }
+  pl->U = U;
+  pl->numel = numel_all;
+  if (P.granularity == USK_GRAN_ROW) {
+    for (int l = 0; l < n_layers; ++l) {
+      LayerGeom& L = pl->layers[l];
+      const int64_t budget = (int64_t)std::floor(P.bpw * (double)(L.out * L.in));
+      const int64_t meta = pl->C > 1 ? L.n_units * ceil_log2(pl->C) : 0;
+      if (budget < meta) {
+        free_plan(pl);
+        return fail(USK_EBUDGET, "budget smaller than the class map of layer " + std::to_string(l));
+      }
+      L.budget_bits = budget;
+      L.meta_bits = meta;
+      L.cells_T = (budget - meta) / state_bits;
+      pl->budget_bits += budget;
+    }
+  } else {
+    const int64_t budget = (int64_t)std::floor(P.bpw * (double)numel_all);
+    pl->layers[0].budget_bits = budget;
+    pl->layers[0].cells_T = budget / state_bits;
+    pl->budget_bits = budget;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  cudaError_t e = cudaSuccess;
+  e = e ? e : cudaMalloc(&pl->d_cls, (size_t)U);
+  e = e ? e : cudaMalloc(&pl->d_ncols, sizeof(int32_t) * U);
+  e = e ? e : cudaMalloc(&pl->d_nrows, (size_t)U);
+  e = e ? e : cudaMalloc(&pl->d_offsets, sizeof(int64_t) * (U + 1));
+  e = e ? e : cudaMalloc(&pl->d_keys, sizeof(uint32_t) * U);
+  e = e ? e : cudaMalloc(&pl->d_R, sizeof(uint32_t) * (pl->max_out + 64));
+  e = e ? e : cudaMalloc(&pl->d_err, sizeof(int));
+  if (e != cudaSuccess) {
+    free_plan(pl);
+    return cuda_fail(e, "usk_plan_allocation: cudaMalloc");
+  }
+  usk_status s = build_plan_device(pl, saliency, st);
+  if (s != USK_OK) {
+    cudaStreamSynchronize(st);
+    free_plan(pl);
+    return s;
+  }
+  pl->total_cells = pl->h_offsets[U];
+  pl->achieved_bits = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    LayerGeom& L = pl->layers[l];
+    L.cell_begin = pl->h_offsets[L.unit_begin];
+    L.n_cells = pl->h_offsets[L.unit_begin + L.n_units] - L.cell_begin;
+    int32_t mx = 0;
+    for (int64_t u = L.unit_begin; u < L.unit_begin + L.n_units; ++u) mx = std::max(mx, pl->h_ncols[u]);
+    L.max_ncols = mx;
+    L.achieved_bits = L.n_cells * state_bits + L.meta_bits;
+    pl->achieved_bits += L.achieved_bits;
+  }
+  *plan_out = pl;
+  return USK_OK;
+}
+
+usk_status usk_plan_query(const usk_plan* pl, usk_plan_info* out) {
+  if (!pl || !out) return fail(USK_EINVAL, "usk_plan_query: null");
+  out->n_layers = pl->n_layers;
+  out->rows = pl->M;
+  out->n_classes = pl->C;
+  out->dtype = pl->dtype;
+  out->n_units = pl->U;
+  out->total_cells = pl->total_cells;
+  const int64_t bytes = pl->total_cells * pl->cell_bytes();
+  out->sketch_bytes = ((bytes + 255) / 256) * 256 + 256;
+  out->numel = pl->numel;
+  out->budget_bits = pl->budget_bits;
+  out->achieved_bits = pl->achieved_bits;
+  return USK_OK;
+}
+
+usk_status usk_plan_layer(const usk_plan* pl, int32_t layer, usk_layer_info* out) {
+  if (!pl || !out) return fail(USK_EINVAL, "usk_plan_layer: null");
+  if (layer < 0 || layer >= pl->n_layers) return fail(USK_ESHAPE, "usk_plan_layer: layer out of range");
+  const LayerGeom& L = pl->layers[layer];
+  *out = usk_layer_info{L.out, L.in, L.unit_begin, L.n_units, L.cell_begin, L.n_cells,
+                        L.budget_bits, L.meta_bits, L.cells_T, L.achieved_bits};
+  return USK_OK;
+}
+
+usk_status usk_plan_export(const usk_plan* pl, int32_t layer, uint8_t* cls, int32_t* ncols, uint8_t* nrows,
+                           int64_t* offsets) {
+  if (!pl) return fail(USK_EINVAL, "usk_plan_export: null plan");
+  if (layer < 0 || layer >= pl->n_layers) return fail(USK_ESHAPE, "usk_plan_export: layer out of range");
+  const LayerGeom& L = pl->layers[layer];
+  if (cls) USK_CUDA(cudaMemcpy(cls, pl->d_cls + L.unit_begin, (size_t)L.n_units, cudaMemcpyDeviceToHost));
+  if (ncols)
+    USK_CUDA(cudaMemcpy(ncols, pl->d_ncols + L.unit_begin, sizeof(int32_t) * L.n_units, cudaMemcpyDeviceToHost));
+  if (nrows) USK_CUDA(cudaMemcpy(nrows, pl->d_nrows + L.unit_begin, (size_t)L.n_units, cudaMemcpyDeviceToHost));
+  if (offsets)
+    USK_CUDA(cudaMemcpy(offsets, pl->d_offsets + L.unit_begin, sizeof(int64_t) * (L.n_units + 1),
+                        cudaMemcpyDeviceToHost));
+  return USK_OK;
+}
+
+usk_status usk_build(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
+                     void* sketch, usk_stream stream) {
+  if (!pl || !weights || !sketch) return fail(USK_EINVAL, "usk_build: null pointer");
+  if (!aligned16(sketch)) return fail(USK_EINVAL, "usk_build: sketch must be 16-B aligned");
+  if (n < 0 || n > pl->n_layers) return fail(USK_ESHAPE, "usk_build: bad layer count");
+  std::vector<char> seen(pl->n_layers, 0);
+  for (int32_t k = 0; k < n; ++k) {
+    const int32_t l = layer_ids ? layer_ids[k] : k;
+    if (l < 0 || l >= pl->n_layers) return fail(USK_ESHAPE, "usk_build: layer id out of range");
+    if (seen[l]) return fail(USK_EINVAL, "usk_build: duplicate layer id");
+    seen[l] = 1;
+    if (!weights[k]) return fail(USK_EINVAL, "usk_build: null weight pointer");
+    if (!aligned16(weights[k])) return fail(USK_EINVAL, "usk_build: weights must be 16-B aligned");
+  }
+  return launch_build(pl, weights, layer_ids, n, sketch, (cudaStream_t)stream);
+}
+
+usk_status usk_reconstruct(const usk_plan* pl, const void* sketch, int32_t layer, int64_t row_begin, int64_t row_end,
+                           void* w_out, int64_t ld_out, usk_stream stream) {
+  if (!pl || !sketch || !w_out) return fail(USK_EINVAL, "usk_reconstruct: null pointer");
+  if (layer < 0 || layer >= pl->n_layers) return fail(USK_ESHAPE, "usk_reconstruct: layer out of range");
+  const LayerGeom& L = pl->layers[layer];
+  if (row_begin < 0 || row_end > L.out || row_begin > row_end)
+    return fail(USK_ESHAPE, "usk_reconstruct: row range outside [0, out_features)");
+  if (ld_out < L.in) return fail(USK_ESHAPE, "usk_reconstruct: ld_out < in_features");
+  return launch_reconstruct(pl, sketch, layer, row_begin, row_end, w_out, ld_out, (cudaStream_t)stream);
+}
+
+size_t usk_linear_workspace_bytes(const usk_plan* pl, int32_t layer, int64_t T, int64_t out_begin,
+                                  int64_t out_end) {
+  if (!pl || layer < 0 || layer >= pl->n_layers || T < 1) return 0;
+  const LayerGeom& L = pl->layers[layer];
+  if (out_begin < 0 || out_end > L.out || out_begin > out_end) return 0;
+  if (T == 1) {
+    size_t b = gemv_workspace_bytes(pl, layer, out_begin, out_end);
+    return b ? b : 256;
+  }
+  return (size_t)((out_end - out_begin) * L.in * 2 + 255) / 256 * 256;
+}
+
+usk_status usk_linear(const usk_plan* pl, const void* sketch, int32_t layer, const void* x, int32_t x_dtype,
+                      int64_t T, void* y, int32_t y_dtype, int64_t out_begin, int64_t out_end, void* workspace,
+                      size_t workspace_bytes, usk_stream stream) {
+  if (!pl || !sketch || !x || !y) return fail(USK_EINVAL, "usk_linear: null pointer");
+  if (x_dtype != USK_F32 && x_dtype != USK_BF16) return fail(USK_EINVAL, "usk_linear: x_dtype");
+  if (y_dtype != USK_F32 && y_dtype != USK_BF16) return fail(USK_EINVAL, "usk_linear: y_dtype");
+  if (!aligned16(x) || !aligned16(y) || !aligned16(sketch)) return fail(USK_EINVAL, "usk_linear: 16-B alignment");
+  if (layer < 0 || layer >= pl->n_layers) return fail(USK_ESHAPE, "usk_linear: layer out of range");
+  const LayerGeom& L = pl->layers[layer];
+  if (T < 1) return fail(USK_ESHAPE, "usk_linear: T must be >= 1");
+  if (out_begin < 0 || out_end > L.out || out_begin > out_end)
+    return fail(USK_ESHAPE, "usk_linear: output range outside [0, out_features)");
+  const size_t need = usk_linear_workspace_bytes(pl, layer, T, out_begin, out_end);
+  if (workspace_bytes < need || (need && !workspace)) return fail(USK_ESHAPE, "usk_linear: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (T == 1)
+    return launch_gemv(pl, sketch, layer, x, x_dtype, y, y_dtype, out_begin, out_end, workspace, workspace_bytes, st);
+  if (pl->dtype != USK_BF16 || x_dtype != USK_BF16)
+    return fail(USK_EUNSUPPORTED, "usk_linear: T > 1 needs bf16 weights and bf16 x (tcgen05 kind::f16)");
+  const int64_t rows = out_end - out_begin;
+  if (rows == 0) return USK_OK;
+  if (!aligned16(workspace)) return fail(USK_EINVAL, "usk_linear: workspace alignment");
+  // the paper's decompression: rebuild the output-row slice of W' ...
+  usk_status s = launch_reconstruct(pl, sketch, layer, out_begin, out_end, workspace, L.in, st);
+  if (s != USK_OK) return s;
+  // ... then the computation stage on the tensor cores
+  return launch_gemm_bf16(x, workspace, y, y_dtype, T, rows, L.in, L.in, st);
+}
+
+usk_status usk_check(const usk_plan* pl, usk_stream stream) {
+  if (!pl) return fail(USK_EINVAL, "usk_check: null plan");
+  USK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+  int h = 0;
+  USK_CUDA(cudaMemcpy(&h, pl->d_err, sizeof(int), cudaMemcpyDeviceToHost));
+  if (h) {
+    USK_CUDA(cudaMemset(pl->d_err, 0, sizeof(int)));
+    return fail(USK_ENONFINITE, "the build saw NaN or Inf weights");
+  }
+  return USK_OK;
+}
+
+void usk_plan_destroy(usk_plan* pl) { free_plan(pl); }
+
+}  // extern "C"

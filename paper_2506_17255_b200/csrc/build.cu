@@ -1,0 +1,405 @@
+// build.cu -- K2: the sketch build ("AbsMin Scatter").
+//
+// Definition (Eq. 3-4; ledger L2/L4): cell S[u, i, c] holds the weight of
+// minimum |.| among those whose hash in row i is c (ties -> the non-negative one), +Inf if none.
+// On 32-bit keys kappa = rotl(bits_hi, 1) = (mag << 1) | sign this is a plain integer min, so
+// atomicMin gives the same bytes for every interleaving.
+//
+// Fast path (ROW granularity, one input dimension per unit -- DESIGN.md L6):
+//   * one CTA per tile of TJ = 32*UPL consecutive units (input dims) of a layer, all outputs;
+//   * warp 0 streams [32 rows x TJ] weight tiles (plus the 32 position mixes R(o)) into an
+//     8-stage shared-memory ring with cp.async.bulk + mbarrier (TMA bulk engine);
+//   * 8 consumer warps: lane L owns units UPL*L .. UPL*L+UPL-1; its keys live in shared memory
+//     at word (v * 32 * maxMN + k * 32 + L), i.e. always in bank L, so the M random bucket
+//     updates of a warp are bank-conflict free;  each update is a plain LDS pre-check and,
+//     only when the candidate is smaller, an ATOMS.MIN (candidates rarely win: ~H(n)/n);
+//   * the CTA then writes its units' cells (states, +Inf for empty) to the sketch.
+// Generic path (LAYER granularity, dims_per_unit > 1, odd shapes, oversize units): keys are
+// kept in place in the sketch buffer (32-bit atomicMin for fp32 cells, 16-bit CAS for bf16),
+// then converted to states.
+#include <algorithm>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace usk {
+namespace {
+
+constexpr int kRO = 32;         // weight rows per stage
+constexpr int kConsumers = 8;   // consumer warps
+constexpr int kBuildThreads = 32 * (kConsumers + 1);
+constexpr int kMaxTasks = 48;
+constexpr size_t kSmemLimit = 227 * 1024;
+
+struct BuildTask {
+  const void* W;
+  int64_t out, in;
+  int64_t unit_base;   // global unit id of the layer's first unit
+  int32_t tile_begin;  // first CTA of this task
+  int32_t pad;
+};
+
+struct BuildArgs {
+  BuildTask task[kMaxTasks];
+  int32_t n_tasks;
+  int32_t M;
+  int32_t maxMN;
+  HashConsts hc;
+  const int32_t* ncols;
+  const int64_t* offsets;
+  const uint32_t* ukeys;
+  const uint32_t* R;
+  void* sketch;
+  int* err;
+};
+
+template <int ES>
+constexpr int stages_for() { return ES == 2 ? 8 : 4; }
+
+template <typename E, int UPL>
+constexpr int stage_bytes() { return kRO * 4 + kRO * 32 * UPL * (int)sizeof(E); }
+
+template <typename E, int UPL, int MT, int HASH>
+__global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_constant__ BuildArgs A) {
+  constexpr int ES = sizeof(E);
+  constexpr int TJ = 32 * UPL;
+  constexpr int ROWB = TJ * ES;
+  constexpr int S = stages_for<ES>();
+  constexpr int STAGEB = stage_bytes<E, UPL>();
+  constexpr int MR = MT > 0 ? MT : 8;
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* empty = full + S;
+  uint8_t* stages = smem + 128;
+  uint32_t* keys = reinterpret_cast<uint32_t*>(stages + S * STAGEB);
+
+  const int b = blockIdx.x;
+  int ti = 0;
+  while (ti + 1 < A.n_tasks && A.task[ti + 1].tile_begin <= b) ++ti;
+  const BuildTask& T = A.task[ti];
+  const int64_t j0 = (int64_t)(b - T.tile_begin) * TJ;
+  const int nu = (int)min((int64_t)TJ, T.in - j0);
+  const int M = MT > 0 ? MT : A.M;
+  const int64_t n_it = (T.out + kRO - 1) / kRO;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int stride_v = 32 * A.maxMN;  // words per unit slot
+
+  {
+    const int nwords = TJ * A.maxMN;
+    uint4* k4 = reinterpret_cast<uint4*>(keys);
+    for (int i = threadIdx.x; i < nwords / 4; i += blockDim.x) k4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
+    for (int i = (nwords / 4) * 4 + threadIdx.x; i < nwords; i += blockDim.x) keys[i] = ~0u;
+  }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kConsumers);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 0) {
+    // ---------------- producer: bulk-copy weight row segments + R(o) into the ring
+    const E* W = reinterpret_cast<const E*>(T.W);
+    const uint32_t segb = (uint32_t)nu * ES;
+    for (int64_t it = 0; it < n_it; ++it) {
+      const int s = (int)(it % S);
+      if (it >= S) mbar_wait(&empty[s], (uint32_t)((it / S) - 1) & 1u);
+      const int64_t o0 = it * kRO;
+      const int rows = (int)min((int64_t)kRO, T.out - o0);
+      const uint32_t rbytes = (uint32_t)((rows + 3) & ~3) * 4u;
+      uint8_t* st = stages + s * STAGEB;
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[s], rbytes + (uint32_t)rows * segb);
+        bulk_g2s(st, A.R + o0, rbytes, &full[s]);
+      }
+      __syncwarp();
+      for (int r = lane; r < rows; r += 32)
+        bulk_g2s(st + kRO * 4 + r * ROWB, W + (o0 + r) * T.in + j0, segb, &full[s]);
+    }
+  } else {
+    // ---------------- consumers
+    const int cw = warp - 1;
+    uint32_t K[UPL], N[UPL];
+    int rb[UPL][MR];
+    bool valid[UPL];
+#pragma unroll
+    for (int v = 0; v < UPL; ++v) {
+      const int ul = UPL * lane + v;
+      valid[v] = ul < nu;
+      const int64_t u = T.unit_base + j0 + (valid[v] ? ul : 0);
+      K[v] = A.ukeys[u];
+      N[v] = (uint32_t)A.ncols[u];
+#pragma unroll
+      for (int i = 0; i < MR; ++i) rb[v][i] = v * stride_v + i * (int)N[v] * 32 + lane;
+    }
+    uint32_t kmax = 0;
+    for (int64_t it = 0; it < n_it; ++it) {
+      const int s = (int)(it % S);
+      mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
+      const uint8_t* st = stages + s * STAGEB;
+      const int64_t o0 = it * kRO;
+      const int rows = (int)min((int64_t)kRO, T.out - o0);
+      for (int r = cw; r < rows; r += kConsumers) {
+        const uint32_t Rv = reinterpret_cast<const uint32_t*>(st)[r];
+        const uint8_t* row = st + kRO * 4 + r * ROWB;
+        uint32_t bits[UPL];
+        if constexpr (ES == 2 && UPL == 2) {
+          const uint32_t v2 = reinterpret_cast<const uint32_t*>(row)[lane];
+          bits[0] = v2 << 16;
+          bits[1] = v2 & 0xFFFF0000u;
+        } else if constexpr (ES == 2) {
+          bits[0] = (uint32_t)reinterpret_cast<const uint16_t*>(row)[lane] << 16;
+        } else if constexpr (UPL == 2) {
+          const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
+          bits[0] = v2.x;
+          bits[1] = v2.y;
+        } else {
+          bits[0] = reinterpret_cast<const uint32_t*>(row)[lane];
+        }
+#pragma unroll
+        for (int v = 0; v < UPL; ++v) {
+          if (!valid[v]) continue;
+          const uint32_t kap = rotl1(bits[v]);
+          kmax = max(kmax, kap);
+          const uint32_t h = Rv ^ K[v];
+#pragma unroll
+          for (int i = 0; i < MR; ++i) {
+            if (MT == 0 && i >= M) break;
+            uint32_t idx;
+            if constexpr (HASH == USK_HASH_X) idx = __umulhi(h * A.hc.a[i], N[v]);
+            else idx = (uint32_t)((o0 + r) % N[v]);
+            volatile uint32_t* c = keys + rb[v][i] + idx * 32;
+            if (kap < *c) atomicMin(const_cast<uint32_t*>(c), kap);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    if (kmax >= 0xFF000000u) atomicOr(A.err, 1);  // NaN / Inf weight (USK_ENONFINITE)
+  }
+  __syncthreads();
+
+  // ---------------- write states: lane L's units, cells k spread over all warps
+  E* out = reinterpret_cast<E*>(A.sketch);
+#pragma unroll
+  for (int v = 0; v < UPL; ++v) {
+    const int ul = UPL * lane + v;
+    if (ul >= nu) continue;
+    const int64_t u = T.unit_base + j0 + ul;
+    const int mn = M * A.ncols[u];
+    const int64_t off = A.offsets[u];
+    for (int k = warp; k < mn; k += kConsumers + 1) {
+      const uint32_t key = keys[v * stride_v + k * 32 + lane];
+      const uint32_t b32 = (key == ~0u) ? 0x7F800000u : rotr1(key);
+      if constexpr (ES == 2) out[off + k] = (uint16_t)(b32 >> 16);
+      else out[off + k] = b32;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- generic path
+struct GenLayer {
+  int64_t out, in, unit_base, cell_begin, n_cells;
+  int32_t gran, g;
+};
+
+template <int ES>
+__global__ void k_gen_init(void* sketch, int64_t c0, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (ES == 2) reinterpret_cast<uint16_t*>(sketch)[c0 + i] = 0xFFFF;
+  else reinterpret_cast<uint32_t*>(sketch)[c0 + i] = 0xFFFFFFFFu;
+}
+
+__device__ __forceinline__ void cas_min16(uint16_t* cell, uint32_t key16) {
+  uint32_t* word = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(cell) & ~uintptr_t(3));
+  const int sh = (reinterpret_cast<uintptr_t>(cell) & 2) ? 16 : 0;
+  uint32_t old = *reinterpret_cast<volatile uint32_t*>(word);
+  for (;;) {
+    const uint32_t cur = (old >> sh) & 0xFFFFu;
+    if (key16 >= cur) return;
+    const uint32_t nw = (old & ~(0xFFFFu << sh)) | (key16 << sh);
+    const uint32_t prev = atomicCAS(word, old, nw);
+    if (prev == old) return;
+    old = prev;
+  }
+}
+
+template <int ES, int HASH>
+__global__ void k_gen_scatter(GenLayer G, const void* W, int32_t layer_M, HashConsts hc,
+                              const int32_t* ncols, const int64_t* offsets, const uint32_t* ukeys,
+                              void* sketch, int* err) {
+  const int64_t n = G.out * G.in;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = e / G.in, j = e - o * G.in;
+    int64_t t, p;
+    if (G.gran == USK_GRAN_ROW) { t = j / G.g; p = (j - t * G.g) * G.out + o; }
+    else { t = 0; p = j * G.out + o; }
+    const int64_t u = G.unit_base + t;
+    const uint32_t N = (uint32_t)ncols[u];
+    const int64_t off = offsets[u];
+    uint32_t bhi = (ES == 2) ? ((uint32_t)reinterpret_cast<const uint16_t*>(W)[e] << 16)
+                             : reinterpret_cast<const uint32_t*>(W)[e];
+    const uint32_t kap = rotl1(bhi);
+    if (kap >= 0xFF000000u) atomicOr(err, 1);
+    const uint32_t h = fmix32((uint32_t)p ^ hc.rho) ^ ukeys[u];
+    for (int i = 0; i < layer_M; ++i) {
+      const uint32_t idx = (HASH == USK_HASH_X) ? __umulhi(h * hc.a[i], N) : (uint32_t)(p % N);
+      const int64_t c = off + (int64_t)i * N + idx;
+      if (ES == 2) {
+        cas_min16(reinterpret_cast<uint16_t*>(sketch) + c, kap >> 16);
+      } else {
+        uint32_t* cell = reinterpret_cast<uint32_t*>(sketch) + c;
+        if (kap < *reinterpret_cast<volatile uint32_t*>(cell)) atomicMin(cell, kap);
+      }
+    }
+  }
+}
+
+template <int ES>
+__global__ void k_gen_final(void* sketch, int64_t c0, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (ES == 2) {
+    uint16_t* c = reinterpret_cast<uint16_t*>(sketch) + c0 + i;
+    const uint32_t k = *c;
+    *c = (k == 0xFFFFu) ? (uint16_t)0x7F80 : (uint16_t)((k >> 1) | ((k & 1u) << 15));
+  } else {
+    uint32_t* c = reinterpret_cast<uint32_t*>(sketch) + c0 + i;
+    const uint32_t k = *c;
+    *c = (k == 0xFFFFFFFFu) ? 0x7F800000u : ((k >> 1) | ((k & 1u) << 31));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+int fast_upl(const usk_plan* pl, int32_t l) {
+  // units per lane for the fast kernels, 0 = not eligible
+  const LayerGeom& L = pl->layers[l];
+  if (pl->gran != USK_GRAN_ROW || pl->g != 1) return 0;
+  const int es = pl->cell_bytes();
+  if ((L.in * es) % 16 != 0) return 0;
+  const int64_t mn = (int64_t)pl->M * L.max_ncols;
+  const int S = es == 2 ? 8 : 4;
+  auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 4 + kRO * 32 * upl * es) + 32LL * upl * mn * 4; };
+  if (smem(2) <= 120 * 1024) return 2;
+  if (smem(1) <= (int64_t)kSmemLimit) return 1;
+  return 0;
+}
+
+template <typename E, int UPL, int MT, int HASH>
+usk_status launch_fast_t(BuildArgs& A, int n_ctas, cudaStream_t st) {
+  constexpr int S = stages_for<sizeof(E)>();
+  const size_t smem = 128 + (size_t)S * stage_bytes<E, UPL>() + (size_t)32 * UPL * A.maxMN * 4;
+  auto kern = k_build_fast<E, UPL, MT, HASH>;
+  USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<n_ctas, kBuildThreads, smem, st>>>(A);
+  USK_LAUNCHED("k_build_fast");
+  return USK_OK;
+}
+
+template <typename E, int UPL>
+usk_status launch_fast_m(BuildArgs& A, int n_ctas, int hash, cudaStream_t st) {
+  if (hash == USK_HASH_IDENTITY) return launch_fast_t<E, UPL, 0, USK_HASH_IDENTITY>(A, n_ctas, st);
+  switch (A.M) {
+    case 1: return launch_fast_t<E, UPL, 1, USK_HASH_X>(A, n_ctas, st);
+    case 2: return launch_fast_t<E, UPL, 2, USK_HASH_X>(A, n_ctas, st);
+    case 3: return launch_fast_t<E, UPL, 3, USK_HASH_X>(A, n_ctas, st);
+    default: return launch_fast_t<E, UPL, 0, USK_HASH_X>(A, n_ctas, st);
+  }
+}
+
+usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_t, const void*>>& group,
+                       void* sketch, cudaStream_t st) {
+  // longest tasks first (largest out) so the big CTAs start in the first wave
+  std::stable_sort(group.begin(), group.end(), [&](auto& a, auto& b) {
+    return pl->layers[a.first].out > pl->layers[b.first].out;
+  });
+  for (size_t g0 = 0; g0 < group.size(); g0 += kMaxTasks) {
+    BuildArgs A{};
+    A.M = pl->M;
+    A.hc = pl->hc;
+    A.ncols = pl->d_ncols;
+    A.offsets = pl->d_offsets;
+    A.ukeys = pl->d_keys;
+    A.R = pl->d_R;
+    A.sketch = sketch;
+    A.err = pl->d_err;
+    int tiles = 0, maxmn = 1;
+    const int TJ = 32 * upl;
+    for (size_t k = g0; k < std::min(group.size(), g0 + kMaxTasks); ++k) {
+      const LayerGeom& L = pl->layers[group[k].first];
+      BuildTask& t = A.task[A.n_tasks++];
+      t.W = group[k].second;
+      t.out = L.out;
+      t.in = L.in;
+      t.unit_base = L.unit_begin;
+      t.tile_begin = tiles;
+      tiles += (int)((L.in + TJ - 1) / TJ);
+      maxmn = std::max(maxmn, pl->M * L.max_ncols);
+    }
+    A.maxMN = maxmn;
+    usk_status s;
+    if (pl->dtype == USK_BF16)
+      s = upl == 2 ? launch_fast_m<uint16_t, 2>(A, tiles, pl->hash, st) : launch_fast_m<uint16_t, 1>(A, tiles, pl->hash, st);
+    else
+      s = upl == 2 ? launch_fast_m<uint32_t, 2>(A, tiles, pl->hash, st) : launch_fast_m<uint32_t, 1>(A, tiles, pl->hash, st);
+    if (s != USK_OK) return s;
+  }
+  return USK_OK;
+}
+
+template <int ES>
+usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* sketch, cudaStream_t st) {
+  const LayerGeom& L = pl->layers[l];
+  GenLayer G{L.out, L.in, L.unit_begin, L.cell_begin, L.n_cells, pl->gran, pl->g};
+  const int T = 256;
+  k_gen_init<ES><<<(unsigned)((L.n_cells + T - 1) / T), T, 0, st>>>(sketch, L.cell_begin, L.n_cells);
+  USK_LAUNCHED("k_gen_init");
+  const int64_t n = L.out * L.in;
+  const unsigned blocks = (unsigned)std::min<int64_t>((n + T - 1) / T, 148 * 16);
+  if (pl->hash == USK_HASH_X)
+    k_gen_scatter<ES, USK_HASH_X><<<blocks, T, 0, st>>>(G, W, pl->M, pl->hc, pl->d_ncols, pl->d_offsets, pl->d_keys,
+                                                        sketch, pl->d_err);
+  else
+    k_gen_scatter<ES, USK_HASH_IDENTITY><<<blocks, T, 0, st>>>(G, W, pl->M, pl->hc, pl->d_ncols, pl->d_offsets,
+                                                               pl->d_keys, sketch, pl->d_err);
+  USK_LAUNCHED("k_gen_scatter");
+  k_gen_final<ES><<<(unsigned)((L.n_cells + T - 1) / T), T, 0, st>>>(sketch, L.cell_begin, L.n_cells);
+  USK_LAUNCHED("k_gen_final");
+  return USK_OK;
+}
+
+}  // namespace
+
+bool layer_fast_ok(const usk_plan* pl, int32_t l) { return fast_upl(pl, l) != 0; }
+
+usk_status launch_build(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
+                        void* sketch, cudaStream_t st) {
+  std::vector<std::pair<int32_t, const void*>> g1, g2;
+  for (int32_t k = 0; k < n; ++k) {
+    const int32_t l = layer_ids ? layer_ids[k] : k;
+    const int upl = fast_upl(pl, l);
+    if (upl == 2) g2.push_back({l, weights[k]});
+    else if (upl == 1) g1.push_back({l, weights[k]});
+    else {
+      usk_status s = pl->dtype == USK_BF16 ? launch_generic_t<2>(pl, l, weights[k], sketch, st)
+                                            : launch_generic_t<4>(pl, l, weights[k], sketch, st);
+      if (s != USK_OK) return s;
+    }
+  }
+  if (!g2.empty()) {
+    usk_status s = launch_fast(pl, 2, g2, sketch, st);
+    if (s != USK_OK) return s;
+  }
+  if (!g1.empty()) {
+    usk_status s = launch_fast(pl, 1, g1, sketch, st);
+    if (s != USK_OK) return s;
+  }
+  return USK_OK;
+}
+
+}  // namespace usk

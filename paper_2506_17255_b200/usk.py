@@ -1,0 +1,233 @@
+"""Thin Python binding of libusk (include/usk.h) -- argument marshalling only.
+
+Every step of the sketch path runs in the CUDA kernels of ``libusk.so``; this module only turns
+torch tensors into pointers/sizes and raises on non-zero status.  PyTorch is used for device
+memory and streams.  There is NO CPU fallback: importing this module without the built
+library raises.
+"""
+from __future__ import annotations
+
+import ctypes as ct
+import os
+from dataclasses import dataclass
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libusk.so")
+
+OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE, ECUDA, EUNSUPPORTED = range(7)
+F32, BF16 = 0, 1
+GRAN = {"row": 0, "layer": 1}
+HASH = {"x": 0, "identity": 1}
+DTYPE = {"f32": F32, "fp32": F32, "float32": F32, "bf16": BF16, "bfloat16": BF16}
+
+
+class UskError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{_STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+_STATUS = {0: "USK_OK", 1: "USK_EINVAL", 2: "USK_ESHAPE", 3: "USK_EBUDGET", 4: "USK_ENONFINITE", 5: "USK_ECUDA",
+           6: "USK_EUNSUPPORTED"}
+
+
+class _Shape(ct.Structure):
+    _fields_ = [("out_features", ct.c_int64), ("in_features", ct.c_int64)]
+
+
+class _Params(ct.Structure):
+    _fields_ = [("bpw", ct.c_double), ("rows", ct.c_int32), ("granularity", ct.c_int32),
+                ("dims_per_unit", ct.c_int32), ("n_classes", ct.c_int32), ("min_cols", ct.c_int32),
+                ("hash", ct.c_int32), ("dtype", ct.c_int32), ("seed", ct.c_uint64)]
+
+
+class _PlanInfo(ct.Structure):
+    _fields_ = [("n_layers", ct.c_int32), ("rows", ct.c_int32), ("n_classes", ct.c_int32), ("dtype", ct.c_int32),
+                ("n_units", ct.c_int64), ("total_cells", ct.c_int64), ("sketch_bytes", ct.c_int64),
+                ("numel", ct.c_int64), ("budget_bits", ct.c_int64), ("achieved_bits", ct.c_int64)]
+
+
+class _LayerInfo(ct.Structure):
+    _fields_ = [("out_features", ct.c_int64), ("in_features", ct.c_int64), ("unit_begin", ct.c_int64),
+                ("n_units", ct.c_int64), ("cell_begin", ct.c_int64), ("n_cells", ct.c_int64),
+                ("budget_bits", ct.c_int64), ("meta_bits", ct.c_int64), ("cells_T", ct.c_int64),
+                ("achieved_bits", ct.c_int64)]
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -m paper_2506_17255_b200.build` "
+                          "(or __graft_entry__.build()); there is no fallback path")
+    L = ct.CDLL(LIB_PATH)
+    p, i32, i64, u64 = ct.c_void_p, ct.c_int32, ct.c_int64, ct.c_uint64
+    sig = {
+        "usk_importance": (i32, [p, i32, i64, i64, p, p]),
+        "usk_plan_allocation": (i32, [ct.POINTER(_Shape), i32, p, ct.POINTER(_Params), ct.POINTER(p), p]),
+        "usk_plan_query": (i32, [p, ct.POINTER(_PlanInfo)]),
+        "usk_plan_layer": (i32, [p, i32, ct.POINTER(_LayerInfo)]),
+        "usk_plan_export": (i32, [p, i32, p, p, p, p]),
+        "usk_build": (i32, [p, p, p, i32, p, p]),
+        "usk_reconstruct": (i32, [p, p, i32, i64, i64, p, i64, p]),
+        "usk_linear_workspace_bytes": (ct.c_size_t, [p, i32, i64, i64, i64]),
+        "usk_linear": (i32, [p, p, i32, p, i32, i64, p, i32, i64, i64, p, ct.c_size_t, p]),
+        "usk_check": (i32, [p, p]),
+        "usk_plan_destroy": (None, [p]),
+        "usk_status_string": (ct.c_char_p, [i32]),
+        "usk_last_error": (ct.c_char_p, []),
+        "usk_launch_count": (i64, [i32]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(L, name)
+        f.restype = res
+        f.argtypes = args
+    return L
+
+
+lib = _load()
+
+
+def _check(st: int):
+    if st != OK:
+        raise UskError(st, lib.usk_last_error().decode())
+
+
+def _stream(stream):
+    import torch
+    if stream is None:
+        if not torch.cuda.is_available():
+            return ct.c_void_p(0)  # host-side validation still runs; device work reports USK_ECUDA
+        stream = torch.cuda.current_stream()
+    return ct.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return ct.c_void_p(t.data_ptr()) if t is not None else ct.c_void_p(0)
+
+
+def _dtype_code(t) -> int:
+    import torch
+    if t.dtype == torch.bfloat16:
+        return BF16
+    if t.dtype == torch.float32:
+        return F32
+    raise UskError(EINVAL, f"unsupported tensor dtype {t.dtype}")
+
+
+@dataclass
+class LayerInfo:
+    out_features: int
+    in_features: int
+    unit_begin: int
+    n_units: int
+    cell_begin: int
+    n_cells: int
+    budget_bits: int
+    meta_bits: int
+    cells_T: int
+    achieved_bits: int
+
+
+class Plan:
+    """Owns a usk_plan handle (destroyed on garbage collection)."""
+
+    def __init__(self, handle: ct.c_void_p, shapes, dtype: int):
+        self.handle = handle
+        self.shapes = [tuple(s) for s in shapes]
+        self.dtype = dtype
+        info = _PlanInfo()
+        _check(lib.usk_plan_query(handle, ct.byref(info)))
+        self.info = {k: getattr(info, k) for k, _ in _PlanInfo._fields_}
+        self.layers = []
+        for l in range(len(shapes)):
+            li = _LayerInfo()
+            _check(lib.usk_plan_layer(handle, l, ct.byref(li)))
+            self.layers.append(LayerInfo(*[getattr(li, k) for k, _ in _LayerInfo._fields_]))
+
+    @property
+    def sketch_bytes(self) -> int:
+        return self.info["sketch_bytes"]
+
+    def new_sketch(self, device=None):
+        import torch
+        return torch.empty(self.sketch_bytes, dtype=torch.uint8, device=device or "cuda")
+
+    def export(self, layer: int):
+        import numpy as np
+        n = self.layers[layer].n_units
+        cls = np.zeros(n, np.uint8)
+        ncols = np.zeros(n, np.int32)
+        nrows = np.zeros(n, np.uint8)
+        offs = np.zeros(n + 1, np.int64)
+        _check(lib.usk_plan_export(self.handle, layer, cls.ctypes.data, ncols.ctypes.data, nrows.ctypes.data,
+                                   offs.ctypes.data))
+        return cls, ncols, nrows, offs
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            lib.usk_plan_destroy(h)
+            self.handle = None
+
+
+def plan_allocation(shapes, *, bpw: float, rows: int = 3, granularity: str = "row", dims_per_unit: int = 1,
+                    n_classes: int = 0, min_cols: int = 1, hash: str = "x", dtype: str = "bf16", seed: int = 0,
+                    saliency=None, stream=None) -> Plan:
+    """usk_plan_allocation. saliency: None or list of (None | float32 CUDA tensor [in_features])."""
+    n = len(shapes)
+    arr = (_Shape * n)(*[_Shape(int(o), int(i)) for (o, i) in shapes])
+    prm = _Params(float(bpw), rows, GRAN[granularity], dims_per_unit, n_classes, min_cols, HASH[hash],
+                  DTYPE[dtype], seed & (2**64 - 1))
+    sal = ct.c_void_p(0)
+    keep = None
+    if saliency is not None:
+        keep = (ct.c_void_p * n)(*[None if s is None else s.data_ptr() for s in saliency])
+        sal = ct.cast(keep, ct.c_void_p)
+    h = ct.c_void_p(0)
+    _check(lib.usk_plan_allocation(arr, n, sal, ct.byref(prm), ct.byref(h), _stream(stream)))
+    return Plan(h, shapes, DTYPE[dtype])
+
+
+def build(plan: Plan, weights, sketch, layer_ids=None, stream=None):
+    n = len(weights)
+    wp = (ct.c_void_p * n)(*[w.data_ptr() for w in weights])
+    ids = None if layer_ids is None else (ct.c_int32 * n)(*layer_ids)
+    _check(lib.usk_build(plan.handle, wp, ids, n, _ptr(sketch), _stream(stream)))
+
+
+def reconstruct(plan: Plan, sketch, layer: int, w_out, row_begin: int = 0, row_end=None, stream=None):
+    row_end = plan.layers[layer].out_features if row_end is None else row_end
+    _check(lib.usk_reconstruct(plan.handle, _ptr(sketch), layer, row_begin, row_end, _ptr(w_out), w_out.stride(0),
+                               _stream(stream)))
+
+
+def linear_workspace_bytes(plan: Plan, layer: int, T: int = 1, out_begin: int = 0, out_end=None) -> int:
+    out_end = plan.layers[layer].out_features if out_end is None else out_end
+    return int(lib.usk_linear_workspace_bytes(plan.handle, layer, T, out_begin, out_end))
+
+
+def new_workspace(plan: Plan, layer: int, T: int = 1, out_begin: int = 0, out_end=None, device=None):
+    import torch
+    return torch.zeros(max(linear_workspace_bytes(plan, layer, T, out_begin, out_end), 256), dtype=torch.uint8,
+                       device=device or "cuda")
+
+
+def linear(plan: Plan, sketch, layer: int, x, y, workspace, out_begin: int = 0, out_end=None, stream=None):
+    """y[T, out_end-out_begin] = x[T, in] @ W'[out_begin:out_end]^T (x, y contiguous CUDA tensors)."""
+    out_end = plan.layers[layer].out_features if out_end is None else out_end
+    T = x.shape[0] if x.dim() == 2 else 1
+    _check(lib.usk_linear(plan.handle, _ptr(sketch), layer, _ptr(x), _dtype_code(x), T, _ptr(y), _dtype_code(y),
+                          out_begin, out_end, _ptr(workspace), workspace.numel() * workspace.element_size(),
+                          _stream(stream)))
+
+
+def importance(A, out, stream=None):
+    """Eq. 7: out[j] = mean_k A[k, j]^2 (A [N, d] bf16/fp32 CUDA, out float32 [d])."""
+    _check(lib.usk_importance(_ptr(A), _dtype_code(A), A.shape[0], A.shape[1], _ptr(out), _stream(stream)))
+
+
+def check(plan: Plan, stream=None):
+    _check(lib.usk_check(plan.handle, _stream(stream)))
+
+
+def launch_count(reset: bool = False) -> int:
+    return int(lib.usk_launch_count(1 if reset else 0))
