@@ -251,7 +251,7 @@ __global__ void k_gen_scatter(GenLayer G, const void* W, int32_t layer_M, HashCo
       const uint32_t idx = (HASH == USK_HASH_X) ? __umulhi(h * hc.a[i], N) : (uint32_t)(p % N);
       const int64_t c = off + (int64_t)i * N + idx;
       if (ES == 2) {
-        cas_min16(reinterpret_cast<uint16_t*>(sketch) + c, kap >> 16);
+        cas_min16(reinterpret_cast<uint16_t*>(sketch) + c, (kap >> 16) | (kap & 1u));  // kappa16 = (mag << 1) | s
       } else {
         uint32_t* cell = reinterpret_cast<uint32_t*>(sketch) + c;
         if (kap < *reinterpret_cast<volatile uint32_t*>(cell)) atomicMin(cell, kap);

@@ -1,9 +1,265 @@
-// gemm.cu -- tcgen05 GEMM for the prefill path (placeholder until the kernel lands).
+// gemm.cu -- the prefill computation stage on the 5th-generation tensor cores.
+//
+// PAPER.md:183-189 (§3.1): decompression -> computation -> release.  After usk_linear has
+// rebuilt the output-row slice W' [N, K] (bf16, K contiguous) into an L2-resident workspace,
+// this kernel computes Y[T, N] = X[T, K] . W'^T with tcgen05.mma (kind::f16, bf16 x bf16 ->
+// fp32 accumulation in TMEM).  DESIGN.md §Prefill explains why the reconstruction is not fused
+// into the B-tile producer (CUDA-core reconstruction would be 2-3x slower than the MMA at
+// 128-256-token reuse).
+//
+// Structure (one CTA per 128 x 256 output tile, 256 threads):
+//   warp 0      TMA producer: A tile [128 x 64] + B tile [256 x 64] per stage, SWIZZLE_128B,
+//               4-stage ring guarded by full/empty mbarriers;
+//   warp 1      MMA issuer (one elected lane): 4 x tcgen05.mma (K = 16 each) per stage,
+//               tcgen05.commit -> empty[stage]; final commit -> tmem_full;
+//   warp 2      TMEM allocator (256 fp32 columns = the 128 x 256 accumulator);
+//   warps 4..7  epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32*(w%4)..+31 = its 32
+//               output rows), convert, store.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <mutex>
+
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace usk {
-usk_status launch_gemm_bf16(const void*, const void*, void*, int32_t, int64_t, int64_t, int64_t, int64_t,
-                            cudaStream_t) {
-  return fail(USK_EUNSUPPORTED, "usk_linear: T > 1 tensor-core path not built yet");
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int kStages = 4;
+constexpr int kGemmThreads = 256;
+constexpr uint32_t kABytes = BM * BK * 2;  // 16 KB
+constexpr uint32_t kBBytes = BN * BK * 2;  // 32 KB
+constexpr uint32_t kStageBytes = kABytes + kBBytes;
+constexpr uint32_t kTmemCols = 256;
+constexpr size_t kGemmSmem = 1024 /*align slack*/ + kStages * kStageBytes + 256 /*barriers*/;
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
 }
+
+// tcgen05 shared-memory matrix descriptor: K-major, SWIZZLE_128B (8 rows x 128 B atoms,
+// SBO = 1024 B between 8-row groups, LBO unused = 1), version 1 (sm100).
+__device__ __forceinline__ uint64_t smem_desc_sw128(const void* p) {
+  const uint32_t a = smem_u32(p);
+  uint64_t d = 0;
+  d |= (uint64_t)((a & 0x3FFFF) >> 4);        // start address [0,14)
+  d |= (uint64_t)1 << 16;                      // LBO (ignored for swizzled K-major)
+  d |= (uint64_t)(1024 >> 4) << 32;            // SBO [32,46)
+  d |= (uint64_t)1 << 46;                      // version = 1
+  d |= (uint64_t)2 << 61;                      // SWIZZLE_128B
+  return d;
+}
+
+// instruction descriptor, kind::f16: D = F32, A = B = BF16, both K-major, M = 128, N = 256
+constexpr uint32_t kIdesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc), "r"(accumulate));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
+  const uint32_t b = __float_as_uint(f);
+  if ((b & 0x7F800000u) == 0x7F800000u) return (uint16_t)((b >> 16) | ((b & 0xFFFFu) ? 0x40u : 0u));
+  return (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+}
+
+struct GemmArgs {
+  void* Y;
+  int32_t y_bf16;
+  int64_t T, N, K;
+  int64_t ldy;
+};
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+              const __grid_constant__ GemmArgs G) {
+  extern __shared__ uint8_t gsm_raw[];
+  uint8_t* gsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = gsm;                                   // kStages x 16 KB
+  uint8_t* sB = gsm + kStages * kABytes;               // kStages x 32 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm + kStages * kStageBytes);
+  uint64_t* empty = full + kStages;
+  uint64_t* tmem_full = empty + kStages;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM;
+  const int n0 = blockIdx.y * BN;
+  const int nkb = (int)((G.K + BK - 1) / BK);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % kStages;
+        if (kb >= kStages) mbar_wait(&empty[s], (uint32_t)((kb / kStages) - 1) & 1u);
+        mbar_arrive_expect_tx(&full[s], kStageBytes);
+        tma_load_2d(sA + s * kABytes, &mapA, &full[s], kb * BK, m0);
+        tma_load_2d(sB + s * kBBytes, &mapB, &full[s], kb * BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % kStages;
+      mbar_wait(&full[s], (uint32_t)(kb / kStages) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k) {
+          const uint64_t da = smem_desc_sw128(sA + s * kABytes + k * 32);
+          const uint64_t db = smem_desc_sw128(sB + s * kBBytes + k * 32);
+          mma_bf16(tmem, da, db, (kb | k) != 0);
+        }
+        mma_commit(&empty[s]);
+        if (kb == nkb - 1) mma_commit(tmem_full);
+      }
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    mbar_wait(tmem_full, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const int64_t row = (int64_t)m0 + q * 32 + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 32) {
+      uint32_t r[32];
+      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
+      if (row >= G.T) continue;
+      const int64_t col = (int64_t)n0 + c0;
+      if (col >= G.N) continue;
+      const int nvalid = (int)min((int64_t)32, G.N - col);
+      if (G.y_bf16) {
+        uint16_t* dst = reinterpret_cast<uint16_t*>(G.Y) + row * G.ldy + col;
+        if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint4 pk;
+            pk.x = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 0])) |
+                   ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 1])) << 16);
+            pk.y = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 2])) |
+                   ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 3])) << 16);
+            pk.z = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 4])) |
+                   ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 5])) << 16);
+            pk.w = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 6])) |
+                   ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 7])) << 16);
+            reinterpret_cast<uint4*>(dst)[v] = pk;
+          }
+        } else {
+          for (int v = 0; v < nvalid; ++v) dst[v] = f32_to_bf16_rne(__uint_as_float(r[v]));
+        }
+      } else {
+        float* dst = reinterpret_cast<float*>(G.Y) + row * G.ldy + col;
+        if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+          for (int v = 0; v < 8; ++v)
+            reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+        } else {
+          for (int v = 0; v < nvalid; ++v) dst[v] = __uint_as_float(r[v]);
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int box_rows) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+  cuuint32_t box[2] = {(cuuint32_t)BK, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dtype, int64_t T, int64_t n_out,
+                            int64_t K, int64_t ldw, cudaStream_t st) {
+  if ((K * 2) % 16 != 0 || ldw != K)
+    return fail(USK_EUNSUPPORTED, "tcgen05 path needs in_features % 8 == 0 (16-B TMA row pitch)");
+  if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(W) & 15))
+    return fail(USK_EINVAL, "tcgen05 path needs 16-B aligned operands");
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, X, T, K, BM) || !make_map(&mb, W, n_out, K, BN))
+    return fail(USK_ECUDA, "cuTensorMapEncodeTiled failed");
+  GemmArgs G{Y, y_dtype == USK_BF16, T, n_out, K, n_out};
+  static std::once_flag attr_once;
+  std::call_once(attr_once, [] {
+    cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
+  });
+  dim3 grid((unsigned)((T + BM - 1) / BM), (unsigned)((n_out + BN - 1) / BN));
+  k_gemm_tc<<<grid, kGemmThreads, kGemmSmem, st>>>(ma, mb, G);
+  USK_LAUNCHED("k_gemm_tc");
+  return USK_OK;
+}
+
 }  // namespace usk

@@ -210,6 +210,7 @@ __global__ void __launch_bounds__(kQThreads) k_gemv_fast(const __grid_constant__
       float a = 0.f;
 #pragma unroll
       for (int v = 0; v < UPL; ++v) {
+        if (!U.valid[v]) continue;  // ragged unit tile: slot not staged
         const uint32_t best = select_rho<UPL, MT, HASH, MR>(A, cells, U, v, Rv, o);
         a = fmaf(nx[v], __uint_as_float(rotr1(best)), a);
       }

@@ -89,7 +89,7 @@ CASES = [
     # (shapes, dtype, bpw, M, gran, g, hash)
     ([(256, 256)], "f32", 1.0, 2, "layer", 1, "x"),          # config 1, LAYER
     ([(256, 256)], "f32", 1.0, 2, "row", 1, "x"),            # config 1, ROW
-    ([(100, 200), (64, 128)], "bf16", 0.5, 3, "row", 1, "x"),  # ragged unit tile (200 % 64 = 8), ragged rows
+    ([(100, 200), (64, 128)], "bf16", 1.0, 3, "row", 1, "x"),  # ragged unit tile (200 % 64 = 8), ragged rows
     ([(300, 96), (33, 64)], "bf16", 2.0, 1, "row", 1, "x"),
     ([(77, 96)], "f32", 4.0, 4, "row", 1, "x"),               # runtime-M kernel
     ([(130, 64)], "bf16", 1.0, 3, "row", 2, "x"),             # dims_per_unit = 2 (generic path)
@@ -249,7 +249,7 @@ def test_layer_sharded_build_equals_full(orc, usk):
     shapes = synth.llama_block(256, 64, 512)
     Ws = make_weights(shapes, "bf16", 3)
     dW = [to_dev(W, "bf16") for W in Ws]
-    pl = usk.plan_allocation(shapes, bpw=0.5, seed=9)
+    pl = usk.plan_allocation(shapes, bpw=2.0, seed=9)
     full = pl.new_sketch()
     usk.build(pl, dW, full)
     parts = []

@@ -1,0 +1,64 @@
+"""Prefill path (usk_linear with T > 1): reconstruct the output-row slice of W' into the workspace,
+then the tcgen05 GEMM.  Tolerance (BASELINE.json north_star, L23): scaled error
+max |Y - Y64| / sum_j |x_tj w'_oj| <= 2e-2 for bf16 Y, <= 1e-5 for fp32 Y (fp32 accumulation)."""
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def usk():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2506_17255_b200 import usk as u
+    return u
+
+
+def _bf16_dev(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16).copy()).view(torch.bfloat16).cuda()
+
+
+@pytest.mark.parametrize("shape,T", [((256, 128), 128), ((512, 256), 3), ((300, 192), 130), ((384, 640), 257),
+                                     ((1000, 64), 1000)])
+@pytest.mark.parametrize("ydt", ["bf16", "f32"])
+def test_prefill_matches_oracle(orc, usk, shape, T, ydt):
+    o, i = shape
+    W = synth.weights_bf16(o, i, seed=o + i)
+    pl = usk.plan_allocation([shape], bpw=1.0, rows=3, seed=77)
+    opl = orc.plan([shape], 1.0, M=3, dtype=orc.BF16, seed=77)
+    sk = pl.new_sketch()
+    usk.build(pl, [_bf16_dev(W)], sk)
+    osk = orc.build_model(opl, [W])
+    xb = synth.f32_to_bf16_bits(synth.vector(i, seed=T, T=T))
+    x = _bf16_dev(xb)
+    y = torch.empty((T, o), dtype=torch.bfloat16 if ydt == "bf16" else torch.float32, device="cuda")
+    usk.linear(pl, sk, 0, x, y, usk.new_workspace(pl, 0, T))
+    x64 = synth.bf16_bits_to_f32(xb).astype(np.float64)
+    rows = np.arange(0, o) if o * T <= 300_000 else np.random.default_rng(0).choice(o, 64, replace=False)
+    y64 = np.stack([orc.linear_rows(opl, osk, 0, x64, r, r + 1)[:, 0] for r in rows], 1)
+    Wr = orc.value_of(orc.reconstruct_rows(opl, osk, 0), orc.BF16).reshape(o, i)[rows]
+    got = y.float().cpu().numpy().astype(np.float64)[:, rows]
+    scale = np.abs(x64) @ np.abs(Wr).T
+    err = np.max(np.abs(got - y64) / np.maximum(scale, 1e-30))
+    assert err <= (2e-2 if ydt == "bf16" else 1e-5), err
+    big = np.abs(y64) >= 1e-3 * np.sqrt(np.mean(y64 ** 2))
+    rel = np.max(np.abs(got - y64)[big] / np.abs(y64)[big])
+    assert rel <= (1e-2 if ydt == "bf16" else 1e-3), rel
+
+
+def test_prefill_output_shard(orc, usk):
+    o, i, T = 512, 256, 200
+    W = synth.weights_bf16(o, i, seed=1)
+    pl = usk.plan_allocation([(o, i)], bpw=1.0, rows=3, seed=3)
+    sk = pl.new_sketch()
+    usk.build(pl, [_bf16_dev(W)], sk)
+    x = _bf16_dev(synth.f32_to_bf16_bits(synth.vector(i, seed=2, T=T)))
+    full = torch.empty((T, o), dtype=torch.float32, device="cuda")
+    usk.linear(pl, sk, 0, x, full, usk.new_workspace(pl, 0, T))
+    part = torch.empty((T, o - 100), dtype=torch.float32, device="cuda")
+    usk.linear(pl, sk, 0, x, part, usk.new_workspace(pl, 0, T, 100, o), out_begin=100, out_end=o)
+    assert torch.equal(part, full[:, 100:])
