@@ -203,98 +203,125 @@ def run_usk(args):
             dist.broadcast(sketch[li.cell_begin * cb:(li.cell_begin + li.n_cells) * cb], src=src)
         torch.cuda.synchronize()
 
-    # ---- decode buffers: fixed synthetic x per linear, y shards
+    # ---- decode buffers.  The linears of a block that read the same activation share one
+    #      synthetic x (q|k|v: attention input, o, gate|up: MLP input, down), exactly as in a
+    #      decode step; y is fp32.  Grouped launches (usk_linear_batch): 4 per block = 64/token.
     def shard(o):
         return (o * rank) // world, (o * (rank + 1)) // world
-    in_off = np.cumsum([0] + [i for o, i in shapes])
+    groups = []
+    for b in range(L // 7):
+        base = 7 * b
+        groups += [[base, base + 1, base + 2], [base + 3], [base + 4, base + 5], [base + 6]]
+    xin = [shapes[g[0]][1] for g in groups]
+    x_off = np.cumsum([0] + xin)
     out_off = np.cumsum([0] + [o for o, i in shapes])
-    X = torch.empty(int(in_off[-1]), dtype=torch.bfloat16, device=dev)
-    for l, (o, i) in enumerate(shapes):
-        X[in_off[l]:in_off[l + 1]] = synth.torch_vector(i, 1000 + l, dev, torch.bfloat16)[0]
+    X = torch.empty(int(x_off[-1]), dtype=torch.bfloat16, device=dev)
+    for gi, g in enumerate(groups):
+        X[x_off[gi]:x_off[gi + 1]] = synth.torch_vector(xin[gi], 1000 + gi, dev, torch.bfloat16)[0]
     Y = torch.zeros(int(out_off[-1]), dtype=torch.float32, device=dev)
-    Yshard = [torch.empty(shard(o)[1] - shard(o)[0], dtype=torch.float32, device=dev) for o, i in shapes]
-    wss = [usk.new_workspace(plan, l, 1, *shard(o), device=dev) for l, (o, i) in enumerate(shapes)]
-    xs = [X[in_off[l]:in_off[l + 1]].view(1, -1) for l in range(L)]
+    xg = [X[x_off[gi]:x_off[gi + 1]] for gi in range(len(groups))]
+    x_of_layer = {l: xg[gi] for gi, g in enumerate(groups) for l in g}
     ys_full = [Y[out_off[l]:out_off[l + 1]] for l in range(L)]
+    Yshard = [torch.empty(shard(o)[1] - shard(o)[0], dtype=torch.float32, device=dev) for o, i in shapes]
+    ranges = {l: shard(shapes[l][0]) for l in range(L)}
+    ws_group = [usk.new_batch_workspace(plan, g, [ranges[l] for l in g], device=dev) for g in groups]
+    ws_layer = [usk.new_workspace(plan, l, 1, *ranges[l], device=dev) for l in range(L)]
+    out_of = (lambda l: ys_full[l]) if world == 1 else (lambda l: Yshard[l])
 
-    def step():
-        for l, (o, i) in enumerate(shapes):
-            o0, o1 = shard(o)
-            if world == 1:
-                usk.linear(plan, sketch, l, xs[l], ys_full[l].view(1, -1), wss[l], o0, o1)
-            else:
-                usk.linear(plan, sketch, l, xs[l], Yshard[l].view(1, -1), wss[l], o0, o1)
+    def gather(ls):
+        if world > 1:
+            for l in ls:
                 dist.all_gather_into_tensor(ys_full[l], Yshard[l])
 
-    stream = torch.cuda.Stream(device=dev)
-    torch.cuda.synchronize()
-    with torch.cuda.stream(stream):
-        for _ in range(2):
-            step()  # warm (module load, attributes)
-    torch.cuda.synchronize()
-    graph = torch.cuda.CUDAGraph()
-    use_graph = True
-    usk.launch_count(reset=True)
-    try:
-        with torch.cuda.graph(graph, stream=stream):
-            step()
-    except Exception as e:  # NCCL capture unsupported -> eager steps
-        use_graph = False
-        print(f"[bench] graph capture failed ({e}); timing eager steps", file=sys.stderr)
-    launches_per_step = usk.launch_count(reset=True) if use_graph else L
+    def step_grouped():
+        for gi, g in enumerate(groups):
+            usk.linear_batch(plan, sketch, g, xg[gi], [out_of(l) for l in g], ws_group[gi],
+                             ranges=[ranges[l] for l in g])
+            gather(g)
 
-    def replay():
-        if use_graph:
-            graph.replay()
+    def step_single():
+        for l in range(L):
+            usk.linear(plan, sketch, l, x_of_layer[l].view(1, -1), out_of(l).view(1, -1), ws_layer[l], *ranges[l])
+            gather([l])
+
+    stream = torch.cuda.Stream(device=dev)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
+
+    def capture(fn):
+        torch.cuda.synchronize()
+        with torch.cuda.stream(stream):
+            for _ in range(2):
+                fn()  # warm (module load, smem attributes) before capture
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        usk.launch_count(reset=True)
+        try:
+            with torch.cuda.graph(g, stream=stream):
+                fn()
+            return g, usk.launch_count(reset=True)
+        except Exception as e:  # NCCL capture unsupported -> eager steps
+            print(f"[bench] graph capture failed ({e}); timing eager steps", file=sys.stderr)
+            return None, usk.launch_count(reset=True)
+
+    def replay(g, fn):
+        if g is not None:
+            g.replay()
         else:
             with torch.cuda.stream(stream):
-                step()
+                fn()
 
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
-    for _ in range(max(3, args.warmup)):
-        replay()
-    torch.cuda.synchronize()
-
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    with ClockSampler(local) as clocks:
-        for k in range(args.steps):
+    def time_steps(g, fn, steps, warmup, clocks=None):
+        for _ in range(max(3, warmup)):
+            replay(g, fn)
+        torch.cuda.synchronize()
+        starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        for k in range(steps):
             with torch.cuda.stream(stream):
                 flush.fill_(k & 0xFF)          # untimed L2 flush
                 starts[k].record(stream)
-                replay()
+                replay(g, fn)
                 ends[k].record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
-    total_ms = float(sum(step_ms))
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    ms_per_step = total_ms / args.steps
+        if world > 1:
+            dist.barrier()
+        total = float(sum(s.elapsed_time(e) for s, e in zip(starts, ends)))
+        if world > 1:
+            t = torch.tensor([total], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            total = float(t.item())
+        return total / steps
+
+    g_grp, launches_grp = capture(step_grouped)
+    g_one, launches_one = capture(step_single)
+    y_check = None
+    with ClockSampler(local) as clocks:
+        ms_per_step = time_steps(g_grp, step_grouped, args.steps, args.warmup)
+        y_check = Y.clone()
+        ms_single = time_steps(g_one, step_single, args.steps, args.warmup)
+    same = bool(torch.equal(y_check, Y))   # grouped and per-linear launches give identical bits
+    use_graph = g_grp is not None
+    launches_per_step = launches_grp
     tok_s = 1000.0 / ms_per_step
 
     # ---- per-launch kernel durations (same launches, eager, each bracketed by events behind a
     #      GPU sleep so the host enqueue latency is hidden) -> roofline of the dominant kernel
-    kern_ms = np.zeros(L)
+    kern_ms = np.zeros(len(groups))
     reps = 5
     with torch.cuda.stream(stream):
         for rep in range(reps):
-            for l, (o, i) in enumerate(shapes):
-                o0, o1 = shard(o)
+            for gi, g in enumerate(groups):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 torch.cuda._sleep(20000)
                 a.record(stream)
-                usk.linear(plan, sketch, l, xs[l], (ys_full[l] if world == 1 else Yshard[l]).view(1, -1), wss[l], o0, o1,
-                           stream=stream)
+                usk.linear_batch(plan, sketch, g, xg[gi], [out_of(l) for l in g], ws_group[gi],
+                                 ranges=[ranges[l] for l in g], stream=stream)
                 b.record(stream)
                 b.synchronize()
-                kern_ms[l] += a.elapsed_time(b) / reps
+                kern_ms[gi] += a.elapsed_time(b) / reps
     w_rank = sum((shard(o)[1] - shard(o)[0]) * i for o, i in shapes)
     sum_kern = float(kern_ms.sum())
     clk = clocks.summary()
@@ -329,7 +356,7 @@ def run_usk(args):
     try:
         with torch.cuda.graph(g2, stream=stream):
             X.copy_(Xh, non_blocking=True)
-            step()
+            step_grouped()
             Yh.copy_(Y, non_blocking=True)
     except Exception:
         e2e_graph = False
@@ -343,7 +370,7 @@ def run_usk(args):
                 g2.replay()
             else:
                 X.copy_(Xh, non_blocking=True)
-                step()
+                step_grouped()
                 Yh.copy_(Y, non_blocking=True)
             b.record(stream)
         b.synchronize()
@@ -370,7 +397,10 @@ def run_usk(args):
                        "bpw": BPW, "rows": ROWS, "granularity": "row (1 input dim per unit)", "classes": 1,
                        "sketch_MB": sketch_bytes / 1e6, "weights": numel, "l2": "flushed (256 MB write) before each step",
                        "parallelism": f"output-sharded x{world} + NCCL all-gather" if world > 1 else "single GPU",
-                       "graph": use_graph},
+                       "graph": use_graph, "launches_per_step": launches_per_step,
+                       "grouping": "q|k|v, o, gate|up, down per block share x (usk_linear_batch)"},
+            "per_linear_launches": {"ms_per_step": ms_single, "tokens_per_s": 1000.0 / ms_single,
+                                    "launches_per_step": launches_one, "bitwise_equal_to_grouped": same},
             "weights_reconstructed_per_s": tok_s * numel,
             "reconstruct_standalone": {"weights_per_s": rec_wps, "GB_per_s_written": rec_wps * 2 / 1e9,
                                        "hbm_frac": rec_wps * (2 + 2 * BPW / 16) / 1e9 / peaks["hbm_gbs"]},
@@ -378,7 +408,7 @@ def run_usk(args):
                       "GB_per_s": owned_w * (2 + BPW / 8) / (build_ms * 1e-3) / 1e9},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": gather_peak, "unit": "Gweight/s",
                          "frac": achieved / gather_peak, "traffic": traffic,
-                         "kernel": "k_gemv_fast", "peak_basis": f"M={ROWS} shared-memory lookups per weight at 1 LDS "
+                         "kernel": "k_gemv_fast", "kernel_ms_per_step": sum_kern, "peak_basis": f"M={ROWS} shared-memory lookups per weight at 1 LDS "
                          f"wavefront/clk/SM x 148 SMs x {f_peak / 1e6:.0f} MHz (DESIGN.md §Rooflines)",
                          "kernel_share_of_step": sum_kern / ms_per_step,
                          "hbm_frac": sketch_bytes / (sum_kern * 1e-3) / 1e9 / peaks["hbm_gbs"]},

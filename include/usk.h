@@ -170,16 +170,31 @@ USK_API size_t usk_linear_workspace_bytes(const usk_plan* plan, int32_t layer, i
 /* Sketch-fused linear (PAPER.md:183-189 decompress -> compute; §3.5 modified linear):
  *   y[t, o - out_begin] = sum_j x[t, j] * w'(o, j),  o in [out_begin, out_end), t < T.
  *   x: device [T, in_features] of x_dtype; y: device [T, out_end - out_begin] of y_dtype.
- *   T <= 8 : sketch-GEMV, W' rebuilt in registers and never stored; fp32 accumulation and a
- *            fixed-order split-K reduction (deterministic).
- *   T >  8 : bf16 plans only -- W' rows rebuilt into `workspace` (the paper's decompression),
- *            then a tcgen05 tensor-core GEMM with fp32 accumulation.
+ *   T == 1 : sketch-GEMV, W' rebuilt in registers and never stored; fp32 accumulation and a
+ *            fixed-order split-K reduction (deterministic).  Launched with programmatic
+ *            dependent launch: x may be produced by the previous kernel on the stream.
+ *   T >  1 : bf16 plans and bf16 x only -- W' rows rebuilt into `workspace` (the paper's
+ *            decompression), then a tcgen05 tensor-core GEMM with fp32 accumulation.
  *   workspace: device, >= usk_linear_workspace_bytes(...), 16-B aligned; MUST be zero-filled
  *   before its first use -- every call leaves it zero-filled again. */
 USK_API usk_status usk_linear(const usk_plan* plan, const void* sketch, int32_t layer, const void* x,
                       int32_t x_dtype, int64_t T, void* y, int32_t y_dtype, int64_t out_begin,
                       int64_t out_end, void* workspace, size_t workspace_bytes,
                       usk_stream stream);
+
+/* Several sketch-GEMVs that share one input vector in ONE launch (q|k|v, gate|up of a
+ * transformer block): for k < n,
+ *   y[k][o - ranges[2k]] = sum_j x[j] * w'_{layers[k]}(o, j),  o in [ranges[2k], ranges[2k+1]).
+ *   layers: host int32[n] (n <= 8), all with the same in_features; ranges: host int64[2n] or NULL
+ *   (full output range); x: device [in] (T = 1); y: host array of n device pointers.
+ *   Same numerics as n calls of usk_linear (T = 1).  workspace: zero-filled before first use,
+ *   left zero-filled, >= usk_linear_batch_workspace_bytes(...). */
+USK_API size_t usk_linear_batch_workspace_bytes(const usk_plan* plan, const int32_t* layers,
+                                                const int64_t* ranges, int32_t n);
+USK_API usk_status usk_linear_batch(const usk_plan* plan, const void* sketch, const int32_t* layers,
+                                    const int64_t* ranges, int32_t n, const void* x, int32_t x_dtype,
+                                    void* const* y, int32_t y_dtype, void* workspace,
+                                    size_t workspace_bytes, usk_stream stream);
 
 /* Synchronises `stream`, returns and clears the plan's sticky device error (USK_ENONFINITE),
  * or USK_ECUDA on a CUDA error, else USK_OK. */

@@ -294,6 +294,49 @@ usk_status usk_linear(const usk_plan* pl, const void* sketch, int32_t layer, con
   return launch_gemm_bf16(x, workspace, y, y_dtype, T, rows, L.in, L.in, st);
 }
 
+static usk_status batch_ranges(const usk_plan* pl, const int32_t* layers, const int64_t* ranges, int32_t n,
+                               std::vector<int64_t>& o0, std::vector<int64_t>& o1) {
+  if (!pl || !layers) return fail(USK_EINVAL, "usk_linear_batch: null pointer");
+  if (n < 1 || n > 8) return fail(USK_ESHAPE, "usk_linear_batch: n must be in [1, 8]");
+  o0.resize(n);
+  o1.resize(n);
+  for (int k = 0; k < n; ++k) {
+    if (layers[k] < 0 || layers[k] >= pl->n_layers) return fail(USK_ESHAPE, "usk_linear_batch: layer out of range");
+    const LayerGeom& L = pl->layers[layers[k]];
+    if (L.in != pl->layers[layers[0]].in) return fail(USK_ESHAPE, "usk_linear_batch: in_features differ");
+    o0[k] = ranges ? ranges[2 * k] : 0;
+    o1[k] = ranges ? ranges[2 * k + 1] : L.out;
+    if (o0[k] < 0 || o1[k] > L.out || o0[k] > o1[k])
+      return fail(USK_ESHAPE, "usk_linear_batch: output range outside [0, out_features)");
+  }
+  return USK_OK;
+}
+
+size_t usk_linear_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* ranges, int32_t n) {
+  std::vector<int64_t> o0, o1;
+  if (batch_ranges(pl, layers, ranges, n, o0, o1) != USK_OK) return 0;
+  return gemv_batch_workspace_bytes(pl, layers, o0.data(), o1.data(), n);
+}
+
+usk_status usk_linear_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* ranges,
+                            int32_t n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype, void* workspace,
+                            size_t workspace_bytes, usk_stream stream) {
+  std::vector<int64_t> o0, o1;
+  usk_status s = batch_ranges(pl, layers, ranges, n, o0, o1);
+  if (s != USK_OK) return s;
+  if (!sketch || !x || !y || !workspace) return fail(USK_EINVAL, "usk_linear_batch: null pointer");
+  if (x_dtype != USK_F32 && x_dtype != USK_BF16) return fail(USK_EINVAL, "usk_linear_batch: x_dtype");
+  if (y_dtype != USK_F32 && y_dtype != USK_BF16) return fail(USK_EINVAL, "usk_linear_batch: y_dtype");
+  if (!aligned16(x) || !aligned16(sketch) || !aligned16(workspace))
+    return fail(USK_EINVAL, "usk_linear_batch: 16-B alignment");
+  for (int k = 0; k < n; ++k)
+    if (!y[k] || !aligned16(y[k])) return fail(USK_EINVAL, "usk_linear_batch: y pointer");
+  if (workspace_bytes < gemv_batch_workspace_bytes(pl, layers, o0.data(), o1.data(), n))
+    return fail(USK_ESHAPE, "usk_linear_batch: workspace too small");
+  return launch_gemv_batch(pl, sketch, layers, o0.data(), o1.data(), n, x, x_dtype, y, y_dtype, workspace,
+                           (cudaStream_t)stream);
+}
+
 usk_status usk_check(const usk_plan* pl, usk_stream stream) {
   if (!pl) return fail(USK_EINVAL, "usk_check: null plan");
   USK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));

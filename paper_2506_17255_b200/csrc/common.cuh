@@ -115,6 +115,11 @@ usk_status launch_gemv(const usk_plan* pl, const void* sketch, int32_t layer, co
                        int32_t x_dtype, void* y, int32_t y_dtype, int64_t o0, int64_t o1,
                        void* ws, size_t ws_bytes, cudaStream_t st);
 size_t gemv_workspace_bytes(const usk_plan* pl, int32_t layer, int64_t o0, int64_t o1);
+size_t gemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* o0, const int64_t* o1,
+                                  int n);
+usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
+                             const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
+                             void* ws, cudaStream_t st);
 usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dtype, int64_t T,
                             int64_t n_out, int64_t K, int64_t ldw, cudaStream_t st);
 usk_status launch_importance(const void* A, int32_t a_dtype, int64_t N, int64_t d, float* I,

@@ -3,14 +3,25 @@
 // Query of one weight (Eq. 3 + Eq. 5; §3.1 "hash ... retrieved by the above
 // indices in a batch ... interpreting these intermediate results"):
 //   w'(o, j) = the bonded cell of maximum |.| over rows i < M (ties -> non-negative, L1/L2).
-// Shared-memory layout (fast path, ROW, one input dim per unit): a CTA owns TJ = 32*UPL
-// consecutive units; lane L owns units UPL*L+v, whose cells sit at word
-// (v*32*maxMN + k*32 + L) -- always bank L -- as rho codes  rho = rotl(bits_hi, 1) ^ 1
-// = (mag << 1) | (1 - sign).  The select is then an integer max and rotr(rho, 1) is the
-// bit pattern of -w', so the GEMV multiplies by -x (exact: only the sign bit moves).
-// Lanes therefore run over units (input dims) and warps over output rows; the per-row
-// position mix R(o) is staged once per CTA.  Split-K partial sums are reduced in a fixed
-// order by the last CTA of each row block (deterministic, no float atomics).
+//
+// Fast path (ROW granularity, one input dimension per unit).  A CTA owns TJ = 32*UPL
+// consecutive units (input dims) and a block of output rows.  Lane L owns units UPL*L+v; their
+// cells are staged once into shared memory as rho codes
+//     rho = rotl(bits_hi, 1) ^ 1 = (mag << 1) | (1 - sign)
+// at byte address  cells + 4*(v*32*maxMN + k*32 + L)  -- always bank L, so the M random
+// gathers of a warp never conflict.  The Eq. 5 select is then an integer max (VIMNMX3 for M=3)
+// and rotr(rho, 1) is the IEEE pattern of -w', so the GEMV multiplies by -x (exact).
+// Per weight and lane: 1 LOP3 (R(o) ^ K_u) + M x (IMAD, IMAD.HI, LEA, LDS) + max + SHF + FFMA.
+// Ragged unit tiles point the missing slots at a shared "zero" cell (rho of +0) with x = 0, so
+// the inner loop has no branches.
+//
+// GEMV: each warp takes 32-row subtiles; after a subtile lane L holds its units' contribution
+// to 32 rows, which a padded shared-memory transpose turns into one row sum per lane.  Split-K
+// partials are reduced in a fixed order by the last CTA of each row block (deterministic, no
+// float atomics).  Launched with programmatic dependent launch: the prologue (staging of the
+// sketch cells, which do not depend on x) overlaps the previous kernel; griddepcontrol.wait
+// precedes the first read of x.  One launch may cover several linears that share x
+// (q|k|v, gate|up) -- usk_linear_batch.
 #include <algorithm>
 
 #include "common.cuh"
@@ -20,228 +31,283 @@ namespace {
 
 constexpr int kQThreads = 256;
 constexpr int kQWarps = kQThreads / 32;
+constexpr int kMaxBatch = 8;
+constexpr int kScratchWords = kQWarps * 32 * 33;  // GEMV transpose scratch
 
-struct QueryArgs {
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+struct QLayer {
+  int64_t unit_base;   // global unit id of the layer's first unit
+  int64_t o_begin;     // first output row
+  int64_t rows;        // rows in [o_begin, o_end)
+  int32_t n_chunks;    // unit chunks of TJ
+  int32_t n_rb;        // row blocks
+  int32_t cta_begin;   // first CTA of this layer in the launch
+  int32_t pad;
+  // gemv
+  void* y;
+  float* partial;      // [n_chunks][rows]
+  uint32_t* counters;  // [n_rb]
+  // reconstruct
+  void* w_out;
+  int64_t ld_out;
+};
+
+struct QArgs {
+  QLayer layer[kMaxBatch];
+  int32_t n_layers;
+  int32_t M;
+  int32_t maxMN;       // smem slot stride (cells) = max over the launch's layers
+  int32_t rb_rows;     // rows per CTA
+  int64_t in;          // in_features (shared by the batch)
   const void* sketch;
   const int32_t* ncols;
   const int64_t* offsets;
   const uint32_t* ukeys;
   const uint32_t* R;
   HashConsts hc;
-  int64_t unit_base;  // global unit id of the layer's first unit
-  int64_t in;
-  int64_t o_begin, o_end;
-  int32_t M, maxMN;
-  int32_t rb_rows;    // rows per CTA (row block)
-  int32_t n_chunks;
-  // reconstruct
-  void* w_out;
-  int64_t ld_out;
-  // gemv
   const void* x;
   int32_t x_bf16;
-  void* y;
   int32_t y_bf16;
-  float* partial;     // [n_chunks][rows]
-  uint32_t* counters; // [n_rb]
 };
 
-// Stage the CTA's units into shared memory (rho layout) and R(o) for its rows.
-template <typename E, int UPL>
-__device__ __forceinline__ void stage_units(const QueryArgs& A, int64_t j0, int nu, int64_t r0, int rows,
-                                            uint32_t* cells, uint32_t* Rs) {
-  constexpr int TJ = 32 * UPL;
-  const int stride_v = 32 * A.maxMN;
-  const E* sk = reinterpret_cast<const E*>(A.sketch);
-  const int ul = threadIdx.x % TJ;
-  if (ul < nu) {
-    const int64_t u = A.unit_base + j0 + ul;
-    const int64_t off = A.offsets[u];
-    const int mn = A.M * A.ncols[u];
-    const int L = ul / UPL, v = ul % UPL;
-    for (int k = threadIdx.x / TJ; k < mn; k += kQThreads / TJ) {
-      uint32_t b = (uint32_t)sk[off + k];
-      if (sizeof(E) == 2) b <<= 16;
-      cells[v * stride_v + k * 32 + L] = rotl1(b) ^ 1u;
-    }
-  }
-  for (int r = threadIdx.x; r < rows; r += kQThreads) Rs[r] = A.R[A.o_begin + r0 + r];
+__device__ __forceinline__ int find_qlayer(const QArgs& A, int b) {
+  int t = 0;
+  while (t + 1 < A.n_layers && A.layer[t + 1].cta_begin <= b) ++t;
+  return t;
 }
 
-template <int UPL, int MR>
-struct LaneUnits {
+template <int UPL, int MT>
+struct LaneState {
+  static constexpr int MR = MT > 0 ? MT : 1;
   uint32_t K[UPL], N[UPL];
-  int rb[UPL][MR];
-  bool valid[UPL];
+  uint32_t rb[UPL][MR];  // shared byte address of (unit v, sketch row i, column 0) for this lane
+  uint32_t rstride[UPL]; // bytes between sketch rows (runtime-M kernels)
 };
 
-template <int UPL, int MR>
-__device__ __forceinline__ void load_lane_units(const QueryArgs& A, int64_t j0, int nu, LaneUnits<UPL, MR>& U) {
+// Stage the CTA's unit cells (rho codes, bank-private layout) + R(o) of its rows; set up the
+// per-lane unit state.  Reads only plan arrays and the sketch (independent of x).
+template <typename E, int UPL, int MT>
+__device__ __forceinline__ void stage(const QArgs& A, const QLayer& Ly, int64_t j0, int nu, int64_t r0,
+                                      uint32_t* Rs, uint32_t* cells, uint32_t* zero, LaneState<UPL, MT>& S) {
+  constexpr int TJ = 32 * UPL;
   const int lane = threadIdx.x & 31;
-  const int stride_v = 32 * A.maxMN;
+  const E* sk = reinterpret_cast<const E*>(A.sketch);
+  {
+    const int ul = threadIdx.x % TJ;
+    if (ul < nu) {
+      const int64_t u = Ly.unit_base + j0 + ul;
+      const int64_t off = A.offsets[u];
+      const int mn = A.M * A.ncols[u];
+      const int L = ul / UPL, v = ul % UPL;
+      uint32_t* dst = cells + v * 32 * A.maxMN + L;
+#pragma unroll 8
+      for (int k = threadIdx.x / TJ; k < mn; k += kQThreads / TJ) {
+        uint32_t b = (uint32_t)sk[off + k];
+        if (sizeof(E) == 2) b <<= 16;
+        dst[k * 32] = rotl1(b) ^ 1u;
+      }
+    }
+  }
+  for (int r = threadIdx.x; r < A.rb_rows; r += kQThreads) {
+    const int64_t rr = min(r0 + r, Ly.rows - 1);
+    Rs[r] = A.R[Ly.o_begin + rr];
+  }
+  if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
+  const uint32_t cbase = smem_u32(cells), zbase = smem_u32(zero);
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
     const int ul = UPL * lane + v;
-    U.valid[v] = ul < nu;
-    const int64_t u = A.unit_base + j0 + (U.valid[v] ? ul : 0);
-    U.K[v] = A.ukeys[u];
-    U.N[v] = (uint32_t)A.ncols[u];
+    if (ul < nu) {
+      const int64_t u = Ly.unit_base + j0 + ul;
+      S.K[v] = A.ukeys[u];
+      S.N[v] = (uint32_t)A.ncols[u];
+      const uint32_t b0 = cbase + 4u * (uint32_t)(v * 32 * A.maxMN + lane);
+      S.rstride[v] = S.N[v] * 128u;
 #pragma unroll
-    for (int i = 0; i < MR; ++i) U.rb[v][i] = v * stride_v + i * (int)U.N[v] * 32 + lane;
+      for (int i = 0; i < LaneState<UPL, MT>::MR; ++i) S.rb[v][i] = b0 + (uint32_t)i * S.rstride[v];
+    } else {
+      S.K[v] = 0;
+      S.N[v] = 1;  // idx is always 0
+      S.rstride[v] = 0;
+#pragma unroll
+      for (int i = 0; i < LaneState<UPL, MT>::MR; ++i) S.rb[v][i] = zbase + 4u * lane;
+    }
   }
 }
 
-// rho code of w'(o, unit v of this lane)
-template <int UPL, int MT, int HASH, int MR>
-__device__ __forceinline__ uint32_t select_rho(const QueryArgs& A, const uint32_t* cells,
-                                               const LaneUnits<UPL, MR>& U, int v, uint32_t Rv, int64_t o) {
-  const uint32_t h = Rv ^ U.K[v];
-  uint32_t best = 0;
+// rho code of w'(o, unit v) for this lane
+template <int UPL, int MT, int HASH>
+__device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<UPL, MT>& S, int v, uint32_t Rv,
+                                               int64_t o) {
+  const uint32_t h = Rv ^ S.K[v];
+  if constexpr (MT > 0 && HASH == USK_HASH_X) {
+    uint32_t m[MT];
 #pragma unroll
-  for (int i = 0; i < MR; ++i) {
-    if (MT == 0 && i >= A.M) break;
-    uint32_t idx;
-    if constexpr (HASH == USK_HASH_X) idx = __umulhi(h * A.hc.a[i], U.N[v]);
-    else idx = (uint32_t)(o % U.N[v]);
-    best = max(best, cells[U.rb[v][i] + idx * 32]);
+    for (int i = 0; i < MT; ++i) m[i] = lds32(S.rb[v][i] + (__umulhi(h * A.hc.a[i], S.N[v]) << 7));
+    uint32_t best = m[0];
+#pragma unroll
+    for (int i = 1; i < MT; ++i) best = max(best, m[i]);
+    return best;
+  } else {
+    uint32_t best = 0, base = S.rb[v][0];
+    for (int i = 0; i < A.M; ++i) {
+      const uint32_t idx = (HASH == USK_HASH_X) ? __umulhi(h * A.hc.a[i], S.N[v]) : (uint32_t)(o % S.N[v]);
+      best = max(best, lds32(base + (idx << 7)));
+      base += S.rstride[v];
+    }
+    return best;
   }
-  return best;
 }
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 // ------------------------------------------------------------------ K3: reconstruct
 template <typename E, int UPL, int MT, int HASH>
-__global__ void __launch_bounds__(kQThreads) k_reconstruct_fast(const __grid_constant__ QueryArgs A) {
+__global__ void __launch_bounds__(kQThreads) k_reconstruct_fast(const __grid_constant__ QArgs A) {
   constexpr int TJ = 32 * UPL;
-  constexpr int MR = MT > 0 ? MT : 8;
   extern __shared__ __align__(16) uint32_t qsm[];
-  uint32_t* Rs = qsm;
-  uint32_t* cells = qsm + A.rb_rows;
-  const int chunk = blockIdx.x % A.n_chunks;
-  const int rbk = blockIdx.x / A.n_chunks;
+  const int li = find_qlayer(A, blockIdx.x);
+  const QLayer& Ly = A.layer[li];
+  const int b = blockIdx.x - Ly.cta_begin;
+  const int chunk = b % Ly.n_chunks, rbk = b / Ly.n_chunks;
   const int64_t j0 = (int64_t)chunk * TJ;
   const int nu = (int)min((int64_t)TJ, A.in - j0);
-  const int64_t rows_total = A.o_end - A.o_begin;
   const int64_t r0 = (int64_t)rbk * A.rb_rows;
-  const int rows = (int)min((int64_t)A.rb_rows, rows_total - r0);
-  stage_units<E, UPL>(A, j0, nu, r0, rows, cells, Rs);
-  LaneUnits<UPL, MR> U;
-  load_lane_units<UPL, MR>(A, j0, nu, U);
+  const int rows = (int)min((int64_t)A.rb_rows, Ly.rows - r0);
+  uint32_t* Rs = qsm;
+  uint32_t* zero = qsm + A.rb_rows;
+  uint32_t* cells = zero + 32;
+  LaneState<UPL, MT> S;
+  stage<E, UPL, MT>(A, Ly, j0, nu, r0, Rs, cells, zero, S);
   __syncthreads();
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  E* out = reinterpret_cast<E*>(A.w_out);
-  for (int r = warp; r < rows; r += kQWarps) {
-    const int64_t o = A.o_begin + r0 + r;
+  const bool full_tile = (nu == TJ);
+  E* dst = reinterpret_cast<E*>(Ly.w_out) + (r0 + warp) * Ly.ld_out + j0 + UPL * lane;
+  const int64_t dstep = (int64_t)kQWarps * Ly.ld_out;
+#pragma unroll 2
+  for (int r = warp; r < rows; r += kQWarps, dst += dstep) {
+    const int64_t o = Ly.o_begin + r0 + r;
     const uint32_t Rv = Rs[r];
     uint32_t wb[UPL];
 #pragma unroll
-    for (int v = 0; v < UPL; ++v) wb[v] = rotr1(select_rho<UPL, MT, HASH, MR>(A, cells, U, v, Rv, o)) ^ 0x80000000u;
-    E* dst = out + (r0 + r) * A.ld_out + j0 + UPL * lane;
-    if constexpr (sizeof(E) == 2 && UPL == 2) {
-      if (U.valid[1]) *reinterpret_cast<uint32_t*>(dst) = __byte_perm(wb[0], wb[1], 0x7632);
-      else if (U.valid[0]) dst[0] = (E)(wb[0] >> 16);
-    } else if constexpr (sizeof(E) == 2) {
-      if (U.valid[0]) dst[0] = (E)(wb[0] >> 16);
-    } else {
+    for (int v = 0; v < UPL; ++v) wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, o)) ^ 0x80000000u;
+    if constexpr (sizeof(E) == 2) {
+      if (full_tile) {
+        if constexpr (UPL == 4) {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(wb[0], wb[1 % UPL], 0x7632),
+                                                      __byte_perm(wb[2 % UPL], wb[3 % UPL], 0x7632));
+        } else if constexpr (UPL == 2) {
+          *reinterpret_cast<uint32_t*>(dst) = __byte_perm(wb[0], wb[1 % UPL], 0x7632);
+        } else {
+          dst[0] = (E)(wb[0] >> 16);
+        }
+      } else {
 #pragma unroll
-      for (int v = 0; v < UPL; ++v)
-        if (U.valid[v]) dst[v] = wb[v];
+        for (int v = 0; v < UPL; ++v)
+          if (UPL * lane + v < nu) dst[v] = (E)(wb[v] >> 16);
+      }
+    } else {
+      if (full_tile && UPL == 4) {
+        *reinterpret_cast<uint4*>(dst) = make_uint4(wb[0], wb[1 % UPL], wb[2 % UPL], wb[3 % UPL]);
+      } else if (full_tile && UPL == 2) {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(wb[0], wb[1 % UPL]);
+      } else {
+#pragma unroll
+        for (int v = 0; v < UPL; ++v)
+          if (UPL * lane + v < nu) dst[v] = wb[v];
+      }
     }
   }
 }
 
 // ------------------------------------------------------------------ K4: sketch-GEMV
-// y[o] = sum_j x[j] w'(o, j), o in [o_begin, o_end).  Warp: 32-row subtiles; lane: UPL units.
-// After a subtile each lane holds acc[r] (its units' contribution to row r); a transpose
-// butterfly leaves the warp's 32 row partials one per lane.
-__device__ __forceinline__ void transpose_reduce32(float (&acc)[32], int lane) {
-#pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) {
-    const bool up = (lane & m) != 0;
-#pragma unroll
-    for (int i = 0; i < m; ++i) {
-      const float send = up ? acc[i] : acc[i + m];
-      const float keep = up ? acc[i + m] : acc[i];
-      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
-    }
-  }
-  // lane now holds, in acc[0], the sum for row r = lane (bit-reversal free: rows were split
-  // by their high bits first, so the surviving index is the lane's own row)
-}
-
 template <typename E, int UPL, int MT, int HASH>
-__global__ void __launch_bounds__(kQThreads) k_gemv_fast(const __grid_constant__ QueryArgs A) {
+__global__ void __launch_bounds__(kQThreads) k_gemv_fast(const __grid_constant__ QArgs A) {
   constexpr int TJ = 32 * UPL;
-  constexpr int MR = MT > 0 ? MT : 8;
   extern __shared__ __align__(16) uint32_t qsm[];
   __shared__ bool s_last;
-  uint32_t* Rs = qsm;
-  uint32_t* cells = qsm + A.rb_rows;
-  const int chunk = blockIdx.x % A.n_chunks;
-  const int rbk = blockIdx.x / A.n_chunks;
+  const int li = find_qlayer(A, blockIdx.x);
+  const QLayer& Ly = A.layer[li];
+  const int b = blockIdx.x - Ly.cta_begin;
+  const int chunk = b % Ly.n_chunks, rbk = b / Ly.n_chunks;
   const int64_t j0 = (int64_t)chunk * TJ;
   const int nu = (int)min((int64_t)TJ, A.in - j0);
-  const int64_t rows_total = A.o_end - A.o_begin;
   const int64_t r0 = (int64_t)rbk * A.rb_rows;
-  const int rows = (int)min((int64_t)A.rb_rows, rows_total - r0);
-  stage_units<E, UPL>(A, j0, nu, r0, rows, cells, Rs);
-  LaneUnits<UPL, MR> U;
-  load_lane_units<UPL, MR>(A, j0, nu, U);
+  const int rows = (int)min((int64_t)A.rb_rows, Ly.rows - r0);
+  float* scratch = reinterpret_cast<float*>(qsm);
+  uint32_t* Rs = qsm + kScratchWords;
+  uint32_t* zero = Rs + A.rb_rows;
+  uint32_t* cells = zero + 32;
+  LaneState<UPL, MT> S;
+  stage<E, UPL, MT>(A, Ly, j0, nu, r0, Rs, cells, zero, S);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+
+  // x depends on the previous kernel in the stream: wait for it only now
+  pdl_wait();
   float nx[UPL];
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
     const int64_t j = j0 + UPL * lane + v;
     float xv = 0.f;
-    if (U.valid[v]) {
-      if (A.x_bf16) xv = __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16);
-      else xv = reinterpret_cast<const float*>(A.x)[j];
-    }
+    if (UPL * lane + v < nu)
+      xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
+                    : reinterpret_cast<const float*>(A.x)[j];
     nx[v] = -xv;  // rotr(rho) decodes to -w'
   }
   __syncthreads();
-  float* P = A.partial + (int64_t)chunk * rows_total + r0;
+
+  float* P = Ly.partial + (int64_t)chunk * Ly.rows + r0;
+  float* sc = scratch + warp * (32 * 33);
   for (int s0 = warp * 32; s0 < rows; s0 += kQWarps * 32) {
     float acc[32];
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
-      const int rr = min(s0 + r, rows - 1);
-      const uint32_t Rv = Rs[rr];
-      const int64_t o = A.o_begin + r0 + rr;
+      const uint32_t Rv = Rs[s0 + r];
       float a = 0.f;
 #pragma unroll
-      for (int v = 0; v < UPL; ++v) {
-        if (!U.valid[v]) continue;  // ragged unit tile: slot not staged
-        const uint32_t best = select_rho<UPL, MT, HASH, MR>(A, cells, U, v, Rv, o);
-        a = fmaf(nx[v], __uint_as_float(rotr1(best)), a);
-      }
+      for (int v = 0; v < UPL; ++v)
+        a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + s0 + r))), a);
       acc[r] = a;
     }
-    transpose_reduce32(acc, lane);
-    if (s0 + lane < rows) P[s0 + lane] = acc[0];
+    // transpose through padded shared memory: lane r sums row r over the 32 lanes (fixed order)
+#pragma unroll
+    for (int r = 0; r < 32; ++r) sc[r * 33 + lane] = acc[r];
+    __syncwarp();
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) s += sc[lane * 33 + k];
+    __syncwarp();
+    if (s0 + lane < rows) P[s0 + lane] = s;
   }
   // ---- deterministic split-K: the last CTA of this row block sums chunks in order
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) {
-    const uint32_t prev = atomicAdd(&A.counters[rbk], 1u);
-    s_last = (prev == (uint32_t)A.n_chunks - 1);
+    const uint32_t prev = atomicAdd(&Ly.counters[rbk], 1u);
+    s_last = (prev == (uint32_t)Ly.n_chunks - 1);
   }
   __syncthreads();
+  pdl_trigger();
   if (!s_last) return;
   __threadfence();
   for (int r = threadIdx.x; r < rows; r += kQThreads) {
     float s = 0.f;
-    const float* p = A.partial + r0 + r;
-    for (int c = 0; c < A.n_chunks; ++c) s += __ldcg(p + (int64_t)c * rows_total);
+    const float* p = Ly.partial + r0 + r;
+    for (int c = 0; c < Ly.n_chunks; ++c) s += __ldcg(p + (int64_t)c * Ly.rows);
     if (A.y_bf16) {
-      const uint32_t b = __float_as_uint(s);
-      const uint32_t rnd = b + 0x7FFFu + ((b >> 16) & 1u);  // RNE (finite)
-      reinterpret_cast<uint16_t*>(A.y)[r0 + r] = (uint16_t)(rnd >> 16);
+      const uint32_t bb = __float_as_uint(s);
+      reinterpret_cast<uint16_t*>(Ly.y)[r0 + r] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
     } else {
-      reinterpret_cast<float*>(A.y)[r0 + r] = s;
+      reinterpret_cast<float*>(Ly.y)[r0 + r] = s;
     }
   }
-  if (threadIdx.x == 0) A.counters[rbk] = 0u;  // leave the workspace zeroed for the next call
+  if (threadIdx.x == 0) Ly.counters[rbk] = 0u;  // leave the workspace zeroed for the next call
 }
 
 // ------------------------------------------------------------------ generic query path
@@ -320,62 +386,124 @@ __global__ void k_importance(const void* A, int32_t bf16, int64_t N, int64_t d, 
   I[j] = (float)(s / (double)N);
 }
 
-// ------------------------------------------------------------------ host helpers
-int query_upl(const usk_plan* pl, int32_t l, size_t* smem_out, int rb_rows) {
-  const LayerGeom& L = pl->layers[l];
-  if (pl->gran != USK_GRAN_ROW || pl->g != 1) return 0;
-  const int64_t mn = (int64_t)pl->M * L.max_ncols;
-  for (int upl = 2; upl >= 1; --upl) {
-    const size_t smem = (size_t)rb_rows * 4 + (size_t)32 * upl * mn * 4;
-    if (smem <= (upl == 2 ? 100 * 1024 : 200 * 1024)) {
-      if (smem_out) *smem_out = smem;
-      return upl;
-    }
-  }
-  return 0;
-}
+// ------------------------------------------------------------------ host side
+bool fast_eligible(const usk_plan* pl) { return pl->gran == USK_GRAN_ROW && pl->g == 1; }
 
-struct Geometry {
+struct Geom {
   int upl = 0;
-  int n_chunks = 0, n_rb = 0, rb_rows = 0;
+  int rb_rows = 0;
+  int maxMN = 0;
   size_t smem = 0;
+  int ctas = 0;
+  std::vector<int> n_chunks, n_rb;
 };
 
-Geometry gemv_geometry(const usk_plan* pl, int32_t l, int64_t rows) {
-  Geometry G;
-  const LayerGeom& L = pl->layers[l];
-  // first pass at a 1024-row block to pick UPL, then size row blocks for ~3 CTAs per SM
-  G.upl = query_upl(pl, l, nullptr, 1024);
-  if (!G.upl) return G;
-  const int TJ = 32 * G.upl;
-  G.n_chunks = (int)((L.in + TJ - 1) / TJ);
-  const int64_t target = 148 * 3;
-  int64_t n_rb = std::max<int64_t>(1, (target + G.n_chunks - 1) / G.n_chunks);
-  int64_t rb = (rows + n_rb - 1) / n_rb;
-  rb = std::max<int64_t>(32, ((rb + 31) / 32) * 32);
-  rb = std::min<int64_t>(rb, 1024);
-  G.rb_rows = (int)rb;
-  G.n_rb = (int)((rows + rb - 1) / rb);
-  G.upl = query_upl(pl, l, &G.smem, G.rb_rows);
+size_t smem_bytes(bool gemv, int upl, int rb_rows, int maxMN) {
+  return (gemv ? (size_t)kScratchWords * 4 : 0) + (size_t)rb_rows * 4 + 128 + (size_t)32 * upl * maxMN * 4;
+}
+
+// Pick units-per-lane and the row block for a launch covering `layers` (rows each).
+Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n, bool gemv) {
+  Geom G;
+  int64_t maxrows = 0;
+  for (int k = 0; k < n; ++k) {
+    G.maxMN = std::max(G.maxMN, pl->M * pl->layers[layers[k]].max_ncols);
+    maxrows = std::max(maxrows, rows[k]);
+  }
+  const int64_t in = pl->layers[layers[0]].in;
+  G.rb_rows = gemv ? (int)std::min<int64_t>(256, ((maxrows + 31) / 32) * 32) : 256;
+  const size_t limit2 = 110 * 1024, limit1 = 220 * 1024;
+  int best = 0;
+  for (int upl : {4, 2, 1}) {
+    const size_t sm = smem_bytes(gemv, upl, G.rb_rows, G.maxMN);
+    if (sm > limit1) continue;
+    int ctas = 0;
+    for (int k = 0; k < n; ++k)
+      ctas += (int)((in + 32 * upl - 1) / (32 * upl)) * (int)((rows[k] + G.rb_rows - 1) / G.rb_rows);
+    if (!best) best = upl;                                        // largest that fits at all
+    if (sm <= limit2 && ctas >= 2 * 148) { best = upl; break; }   // enough CTAs at >= 2 CTAs/SM
+    if (sm <= limit2 && best > upl && ctas >= 148) best = upl;
+  }
+  if (!best) return G;
+  G.upl = best;
+  G.smem = smem_bytes(gemv, best, G.rb_rows, G.maxMN);
+  for (int k = 0; k < n; ++k) {
+    G.n_chunks.push_back((int)((in + 32 * best - 1) / (32 * best)));
+    G.n_rb.push_back((int)((rows[k] + G.rb_rows - 1) / G.rb_rows));
+    G.ctas += G.n_chunks.back() * G.n_rb.back();
+  }
   return G;
 }
 
-QueryArgs make_args(const usk_plan* pl, int32_t l, const void* sketch, int64_t o0, int64_t o1) {
-  const LayerGeom& L = pl->layers[l];
-  QueryArgs A{};
+size_t layer_ws_bytes(int n_chunks, int n_rb, int64_t rows) {
+  const size_t p = ((size_t)n_chunks * rows * 4 + 255) / 256 * 256;
+  return p + ((size_t)n_rb * 4 + 255) / 256 * 256;
+}
+
+QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& G) {
+  QArgs A{};
+  A.M = pl->M;
+  A.maxMN = G.maxMN;
+  A.rb_rows = G.rb_rows;
+  A.in = in;
   A.sketch = sketch;
   A.ncols = pl->d_ncols;
   A.offsets = pl->d_offsets;
   A.ukeys = pl->d_keys;
   A.R = pl->d_R;
   A.hc = pl->hc;
-  A.unit_base = L.unit_begin;
-  A.in = L.in;
-  A.o_begin = o0;
-  A.o_end = o1;
-  A.M = pl->M;
-  A.maxMN = pl->M * L.max_ncols;
   return A;
+}
+
+#define USK_PICK(KNAME)                                                                \
+  template <typename E, int UPL>                                                       \
+  void* pick_##KNAME(int M, int hash) {                                                \
+    if (hash == USK_HASH_IDENTITY) return (void*)KNAME<E, UPL, 0, USK_HASH_IDENTITY>;  \
+    switch (M) {                                                                       \
+      case 1: return (void*)KNAME<E, UPL, 1, USK_HASH_X>;                              \
+      case 2: return (void*)KNAME<E, UPL, 2, USK_HASH_X>;                              \
+      case 3: return (void*)KNAME<E, UPL, 3, USK_HASH_X>;                              \
+      default: return (void*)KNAME<E, UPL, 0, USK_HASH_X>;                             \
+    }                                                                                  \
+  }
+USK_PICK(k_reconstruct_fast)
+USK_PICK(k_gemv_fast)
+
+template <int UPL>
+void* pick_upl(bool gemv, bool bf16, int M, int hash) {
+  if (gemv) return bf16 ? pick_k_gemv_fast<uint16_t, UPL>(M, hash) : pick_k_gemv_fast<uint32_t, UPL>(M, hash);
+  return bf16 ? pick_k_reconstruct_fast<uint16_t, UPL>(M, hash) : pick_k_reconstruct_fast<uint32_t, UPL>(M, hash);
+}
+
+void* pick_fast(int upl, bool gemv, bool bf16, int M, int hash) {
+  switch (upl) {
+    case 4: return pick_upl<4>(gemv, bf16, M, hash);
+    case 2: return pick_upl<2>(gemv, bf16, M, hash);
+    default: return pick_upl<1>(gemv, bf16, M, hash);
+  }
+}
+
+usk_status launch_q(void* kern, const QArgs& A, int ctas, size_t smem, bool pdl, cudaStream_t st) {
+  // max dynamic smem is raised once per kernel (before any graph capture: callers warm up)
+  static std::vector<void*> raised;
+  if (std::find(raised.begin(), raised.end(), kern) == raised.end()) {
+    USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    raised.push_back(kern);
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)ctas);
+  cfg.blockDim = dim3(kQThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  void* args[] = {const_cast<QArgs*>(&A)};
+  USK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+  count_launch();
+  return USK_OK;
 }
 
 GenQ make_genq(const usk_plan* pl, int32_t l, const void* sketch) {
@@ -397,42 +525,73 @@ GenQ make_genq(const usk_plan* pl, int32_t l, const void* sketch) {
   return Q;
 }
 
-#define USK_PICK(KNAME)                                                                          \
-  template <typename E, int UPL>                                                                 \
-  void* pick_##KNAME(int M, int hash) {                                                          \
-    if (hash == USK_HASH_IDENTITY) return (void*)KNAME<E, UPL, 0, USK_HASH_IDENTITY>;            \
-    switch (M) {                                                                                 \
-      case 1: return (void*)KNAME<E, UPL, 1, USK_HASH_X>;                                        \
-      case 2: return (void*)KNAME<E, UPL, 2, USK_HASH_X>;                                        \
-      case 3: return (void*)KNAME<E, UPL, 3, USK_HASH_X>;                                        \
-      default: return (void*)KNAME<E, UPL, 0, USK_HASH_X>;                                       \
-    }                                                                                            \
-  }
-USK_PICK(k_reconstruct_fast)
-USK_PICK(k_gemv_fast)
+}  // namespace
 
-template <int UPL>
-void* pick_fast(bool gemv, bool bf16, int M, int hash) {
-  if (gemv) return bf16 ? pick_k_gemv_fast<uint16_t, UPL>(M, hash) : pick_k_gemv_fast<uint32_t, UPL>(M, hash);
-  return bf16 ? pick_k_reconstruct_fast<uint16_t, UPL>(M, hash) : pick_k_reconstruct_fast<uint32_t, UPL>(M, hash);
+size_t gemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* o0, const int64_t* o1,
+                                  int n) {
+  if (!fast_eligible(pl)) return 256;
+  std::vector<int64_t> rows(n);
+  for (int k = 0; k < n; ++k) rows[k] = o1[k] - o0[k];
+  Geom G = geometry(pl, layers, rows.data(), n, true);
+  if (!G.upl) return 256;
+  size_t b = 0;
+  for (int k = 0; k < n; ++k) b += layer_ws_bytes(G.n_chunks[k], G.n_rb[k], rows[k]);
+  return std::max<size_t>(b, 256);
 }
 
-usk_status launch_fast_query(void* kern, const QueryArgs& A, unsigned grid, size_t smem, cudaStream_t st) {
-  USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  void* args[] = {const_cast<QueryArgs*>(&A)};
-  USK_CUDA(cudaLaunchKernel(kern, dim3(grid), dim3(kQThreads), args, smem, st));
-  count_launch();
+size_t gemv_workspace_bytes(const usk_plan* pl, int32_t l, int64_t o0, int64_t o1) {
+  return gemv_batch_workspace_bytes(pl, &l, &o0, &o1, 1);
+}
+
+usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
+                             const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
+                             void* ws, cudaStream_t st) {
+  std::vector<int64_t> rows(n);
+  for (int k = 0; k < n; ++k) rows[k] = o1[k] - o0[k];
+  Geom G = fast_eligible(pl) ? geometry(pl, layers, rows.data(), n, true) : Geom{};
+  if (G.upl) {
+    const int64_t in = pl->layers[layers[0]].in;
+    QArgs A = base_args(pl, sketch, in, G);
+    A.x = x;
+    A.x_bf16 = x_dtype == USK_BF16;
+    A.y_bf16 = y_dtype == USK_BF16;
+    char* w = reinterpret_cast<char*>(ws);
+    int cta = 0;
+    for (int k = 0; k < n; ++k) {
+      if (rows[k] == 0) continue;
+      QLayer& Ly = A.layer[A.n_layers++];
+      Ly.unit_base = pl->layers[layers[k]].unit_begin;
+      Ly.o_begin = o0[k];
+      Ly.rows = rows[k];
+      Ly.n_chunks = G.n_chunks[k];
+      Ly.n_rb = G.n_rb[k];
+      Ly.cta_begin = cta;
+      cta += Ly.n_chunks * Ly.n_rb;
+      Ly.y = y[k];
+      Ly.partial = reinterpret_cast<float*>(w);
+      const size_t p = ((size_t)Ly.n_chunks * rows[k] * 4 + 255) / 256 * 256;
+      Ly.counters = reinterpret_cast<uint32_t*>(w + p);
+      w += layer_ws_bytes(Ly.n_chunks, Ly.n_rb, rows[k]);
+    }
+    if (!A.n_layers) return USK_OK;
+    void* k = pick_fast(G.upl, true, pl->dtype == USK_BF16, pl->M, pl->hash);
+    return launch_q(k, A, cta, G.smem, true, st);
+  }
+  for (int k = 0; k < n; ++k) {
+    if (rows[k] == 0) continue;
+    GenQ Q = make_genq(pl, layers[k], sketch);
+    const int rpb = 8;
+    k_gemv_gen<<<(unsigned)((rows[k] + rpb - 1) / rpb), 32 * rpb, 0, st>>>(Q, o0[k], o1[k], x, x_dtype == USK_BF16, y[k],
+                                                                          y_dtype == USK_BF16);
+    USK_LAUNCHED("k_gemv_gen");
+  }
   return USK_OK;
 }
 
-}  // namespace
-
-size_t gemv_workspace_bytes(const usk_plan* pl, int32_t l, int64_t o0, int64_t o1) {
-  const int64_t rows = o1 - o0;
-  Geometry G = gemv_geometry(pl, l, rows);
-  if (!G.upl) return 0;
-  const size_t p = (size_t)G.n_chunks * rows * 4;
-  return ((p + 255) / 256) * 256 + (size_t)G.n_rb * 4;
+usk_status launch_gemv(const usk_plan* pl, const void* sketch, int32_t l, const void* x, int32_t x_dtype, void* y,
+                       int32_t y_dtype, int64_t o0, int64_t o1, void* ws, size_t, cudaStream_t st) {
+  void* ys[1] = {y};
+  return launch_gemv_batch(pl, sketch, &l, &o0, &o1, 1, x, x_dtype, ys, y_dtype, ws, st);
 }
 
 usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l, int64_t r0, int64_t r1, void* w_out,
@@ -440,54 +599,27 @@ usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l,
   const LayerGeom& L = pl->layers[l];
   const int64_t rows = r1 - r0;
   if (rows == 0) return USK_OK;
-  size_t smem = 0;
-  const int rb_rows = 256;
-  const int upl = query_upl(pl, l, &smem, rb_rows);
-  const bool aligned = ((ld * pl->cell_bytes()) % 4 == 0) && (reinterpret_cast<uintptr_t>(w_out) % 4 == 0);
-  if (upl && aligned) {
-    QueryArgs A = make_args(pl, l, sketch, r0, r1);
-    A.rb_rows = rb_rows;
-    A.n_chunks = (int)((L.in + 32 * upl - 1) / (32 * upl));
-    A.w_out = w_out;
-    A.ld_out = ld;
-    const int n_rb = (int)((rows + rb_rows - 1) / rb_rows);
-    void* k = upl == 2 ? pick_fast<2>(false, pl->dtype == USK_BF16, pl->M, pl->hash)
-                       : pick_fast<1>(false, pl->dtype == USK_BF16, pl->M, pl->hash);
-    return launch_fast_query(k, A, (unsigned)(A.n_chunks * n_rb), smem, st);
+  const int es = pl->cell_bytes();
+  const bool aligned = ((ld * es) % 16 == 0) && (reinterpret_cast<uintptr_t>(w_out) % 16 == 0);
+  Geom G = (fast_eligible(pl) && aligned) ? geometry(pl, &l, &rows, 1, false) : Geom{};
+  if (G.upl) {
+    QArgs A = base_args(pl, sketch, L.in, G);
+    QLayer& Ly = A.layer[A.n_layers++];
+    Ly.unit_base = L.unit_begin;
+    Ly.o_begin = r0;
+    Ly.rows = rows;
+    Ly.n_chunks = G.n_chunks[0];
+    Ly.n_rb = G.n_rb[0];
+    Ly.cta_begin = 0;
+    Ly.w_out = w_out;
+    Ly.ld_out = ld;
+    void* k = pick_fast(G.upl, false, pl->dtype == USK_BF16, pl->M, pl->hash);
+    return launch_q(k, A, G.ctas, G.smem, false, st);
   }
   GenQ Q = make_genq(pl, l, sketch);
   const int64_t n = rows * L.in;
   k_reconstruct_gen<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(Q, r0, r1, w_out, ld);
   USK_LAUNCHED("k_reconstruct_gen");
-  return USK_OK;
-}
-
-usk_status launch_gemv(const usk_plan* pl, const void* sketch, int32_t l, const void* x, int32_t x_dtype, void* y,
-                       int32_t y_dtype, int64_t o0, int64_t o1, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const int64_t rows = o1 - o0;
-  if (rows == 0) return USK_OK;
-  Geometry G = gemv_geometry(pl, l, rows);
-  if (G.upl) {
-    QueryArgs A = make_args(pl, l, sketch, o0, o1);
-    A.rb_rows = G.rb_rows;
-    A.n_chunks = G.n_chunks;
-    A.x = x;
-    A.x_bf16 = x_dtype == USK_BF16;
-    A.y = y;
-    A.y_bf16 = y_dtype == USK_BF16;
-    const size_t p = (size_t)G.n_chunks * rows * 4;
-    A.partial = reinterpret_cast<float*>(ws);
-    A.counters = reinterpret_cast<uint32_t*>(reinterpret_cast<char*>(ws) + ((p + 255) / 256) * 256);
-    (void)ws_bytes;
-    void* k = G.upl == 2 ? pick_fast<2>(true, pl->dtype == USK_BF16, pl->M, pl->hash)
-                         : pick_fast<1>(true, pl->dtype == USK_BF16, pl->M, pl->hash);
-    return launch_fast_query(k, A, (unsigned)(G.n_chunks * G.n_rb), G.smem, st);
-  }
-  GenQ Q = make_genq(pl, l, sketch);
-  const int rows_per_block = 8;
-  k_gemv_gen<<<(unsigned)((rows + rows_per_block - 1) / rows_per_block), 32 * rows_per_block, 0, st>>>(
-      Q, o0, o1, x, x_dtype == USK_BF16, y, y_dtype == USK_BF16);
-  USK_LAUNCHED("k_gemv_gen");
   return USK_OK;
 }
 

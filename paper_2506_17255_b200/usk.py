@@ -70,6 +70,8 @@ def _load():
         "usk_reconstruct": (i32, [p, p, i32, i64, i64, p, i64, p]),
         "usk_linear_workspace_bytes": (ct.c_size_t, [p, i32, i64, i64, i64]),
         "usk_linear": (i32, [p, p, i32, p, i32, i64, p, i32, i64, i64, p, ct.c_size_t, p]),
+        "usk_linear_batch_workspace_bytes": (ct.c_size_t, [p, p, p, i32]),
+        "usk_linear_batch": (i32, [p, p, p, p, i32, p, i32, p, i32, p, ct.c_size_t, p]),
         "usk_check": (i32, [p, p]),
         "usk_plan_destroy": (None, [p]),
         "usk_status_string": (ct.c_char_p, [i32]),
@@ -218,6 +220,33 @@ def linear(plan: Plan, sketch, layer: int, x, y, workspace, out_begin: int = 0, 
     _check(lib.usk_linear(plan.handle, _ptr(sketch), layer, _ptr(x), _dtype_code(x), T, _ptr(y), _dtype_code(y),
                           out_begin, out_end, _ptr(workspace), workspace.numel() * workspace.element_size(),
                           _stream(stream)))
+
+
+def _batch_args(layers, ranges):
+    n = len(layers)
+    ids = (ct.c_int32 * n)(*layers)
+    rg = None if ranges is None else (ct.c_int64 * (2 * n))(*[v for r in ranges for v in r])
+    return n, ids, rg
+
+
+def linear_batch_workspace_bytes(plan: Plan, layers, ranges=None) -> int:
+    n, ids, rg = _batch_args(layers, ranges)
+    return int(lib.usk_linear_batch_workspace_bytes(plan.handle, ids, rg, n))
+
+
+def new_batch_workspace(plan: Plan, layers, ranges=None, device=None):
+    import torch
+    return torch.zeros(max(linear_batch_workspace_bytes(plan, layers, ranges), 256), dtype=torch.uint8,
+                       device=device or "cuda")
+
+
+def linear_batch(plan: Plan, sketch, layers, x, ys, workspace, ranges=None, stream=None):
+    """One launch for several T=1 sketch-GEMVs sharing x: ys[k] = x @ W'_{layers[k]}[range_k]^T."""
+    n, ids, rg = _batch_args(layers, ranges)
+    yp = (ct.c_void_p * n)(*[y.data_ptr() for y in ys])
+    _check(lib.usk_linear_batch(plan.handle, _ptr(sketch), ids, rg, n, _ptr(x), _dtype_code(x), yp,
+                                _dtype_code(ys[0]), _ptr(workspace), workspace.numel() * workspace.element_size(),
+                                _stream(stream)))
 
 
 def importance(A, out, stream=None):

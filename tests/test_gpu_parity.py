@@ -266,3 +266,32 @@ def test_layer_sharded_build_equals_full(orc, usk):
             a = full.view(torch.int16)[li.cell_begin:li.cell_begin + li.n_cells]
             b = sk.view(torch.int16)[li.cell_begin:li.cell_begin + li.n_cells]
             assert torch.equal(a, b)
+
+
+def test_linear_batch_equals_single(orc, usk):
+    """usk_linear_batch (one launch for linears sharing x) == per-linear usk_linear, bit for bit,
+    and within the GEMV tolerance of the oracle; with and without output ranges."""
+    shapes = synth.llama_block(256, 64, 512)[:3] + [(96, 256)]
+    Ws = make_weights(shapes, "bf16", 21)
+    pl = usk.plan_allocation(shapes, bpw=2.0, seed=4)
+    opl = orc.plan(shapes, 2.0, M=3, dtype=orc.BF16, seed=4)
+    sk = pl.new_sketch()
+    usk.build(pl, [to_dev(W, "bf16") for W in Ws], sk)
+    osk = orc.build_model(opl, Ws)
+    xb = synth.f32_to_bf16_bits(synth.vector(256, seed=9)[0])
+    x = torch.from_numpy(xb.view(np.int16).copy()).view(torch.bfloat16).cuda()
+    x64 = synth.bf16_bits_to_f32(xb).astype(np.float64)
+    layers = [0, 1, 2, 3]
+    for ranges in (None, [(10, 200), (0, 64), (5, 6), (0, 96)]):
+        rg = ranges or [(0, shapes[l][0]) for l in layers]
+        ys = [torch.empty(r1 - r0, dtype=torch.float32, device="cuda") for r0, r1 in rg]
+        usk.linear_batch(pl, sk, layers, x, ys, usk.new_batch_workspace(pl, layers, ranges), ranges=ranges)
+        for k, l in enumerate(layers):
+            r0, r1 = rg[k]
+            y1 = torch.empty(r1 - r0, dtype=torch.float32, device="cuda")
+            usk.linear(pl, sk, l, x.view(1, -1), y1.view(1, -1), usk.new_workspace(pl, l, 1, r0, r1), r0, r1)
+            y64 = orc.linear_rows(opl, osk, l, x64, r0, r1)[0]
+            Wr = orc.value_of(orc.reconstruct_rows(opl, osk, l, r0, r1), orc.BF16).reshape(r1 - r0, -1)
+            assert gemv_err(ys[k].cpu().numpy().astype(np.float64), y64, x64, Wr) <= 1e-5
+            if ranges is None:
+                assert torch.equal(ys[k], y1)
