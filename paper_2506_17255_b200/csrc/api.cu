@@ -19,6 +19,7 @@ usk_status fail(usk_status st, const std::string& msg) {
 }
 usk_status cuda_fail(cudaError_t e, const char* what) {
   g_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  (void)cudaGetLastError();  // do not let a non-sticky error leak into the next launch check
   return USK_ECUDA;
 }
 void count_launch(int n) { g_launches += n; }

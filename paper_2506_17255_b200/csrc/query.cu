@@ -487,7 +487,7 @@ usk_status launch_q(void* kern, const QArgs& A, int ctas, size_t smem, bool pdl,
   // max dynamic smem is raised once per kernel (before any graph capture: callers warm up)
   static std::vector<void*> raised;
   if (std::find(raised.begin(), raised.end(), kern) == raised.end()) {
-    USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     raised.push_back(kern);
   }
   cudaLaunchConfig_t cfg{};

@@ -166,7 +166,7 @@ class Plan:
 
     def __del__(self):
         h = getattr(self, "handle", None)
-        if h is not None and h.value:
+        if h is not None and h.value and lib is not None:
             lib.usk_plan_destroy(h)
             self.handle = None
 
