@@ -4,24 +4,25 @@
 // indices in a batch ... interpreting these intermediate results"):
 //   w'(o, j) = the bonded cell of maximum |.| over rows i < M (ties -> non-negative, L1/L2).
 //
-// Fast path (ROW granularity, one input dimension per unit).  A CTA owns TJ = 32*UPL
-// consecutive units (input dims) and a block of output rows.  Lane L owns units UPL*L+v; their
-// cells are staged once into shared memory as rho codes
+// Fast path (ROW granularity, one input dimension per unit).  Work is cut into ITEMS =
+// (layer, chunk of TJ = 32*UPL consecutive units, block of 32*warps output rows), ordered
+// layer-major, chunk-major.  A persistent grid (<= resident CTAs) takes contiguous item ranges,
+// so a CTA stages a chunk's cells once and reuses them over many row blocks.  Lane L owns units
+// UPL*L+v; their cells are staged into shared memory as rho codes
 //     rho = rotl(bits_hi, 1) ^ 1 = (mag << 1) | (1 - sign)
 // at byte address  cells + 4*(v*32*maxMN + k*32 + L)  -- always bank L, so the M random
-// gathers of a warp never conflict.  The Eq. 5 select is then an integer max (VIMNMX3 for M=3)
-// and rotr(rho, 1) is the IEEE pattern of -w', so the GEMV multiplies by -x (exact).
+// gathers of a warp never conflict.  The Eq. 5 select is an integer max (VIMNMX3 for M=3) and
+// rotr(rho, 1) is the IEEE pattern of -w', so the GEMV multiplies by -x (exact).
 // Per weight and lane: 1 LOP3 (R(o) ^ K_u) + M x (IMAD, IMAD.HI, LEA, LDS) + max + SHF + FFMA.
-// Ragged unit tiles point the missing slots at a shared "zero" cell (rho of +0) with x = 0, so
-// the inner loop has no branches.
+// Missing units of a ragged chunk point at a shared "zero" cell (rho of +0) with x = 0, so the
+// inner loop has no branches.
 //
-// GEMV: each warp takes 32-row subtiles; after a subtile lane L holds its units' contribution
-// to 32 rows, which a padded shared-memory transpose turns into one row sum per lane.  Split-K
-// partials are reduced in a fixed order by the last CTA of each row block (deterministic, no
-// float atomics).  Launched with programmatic dependent launch: the prologue (staging of the
-// sketch cells, which do not depend on x) overlaps the previous kernel; griddepcontrol.wait
-// precedes the first read of x.  One launch may cover several linears that share x
-// (q|k|v, gate|up) -- usk_linear_batch.
+// GEMV: a warp computes 32 rows; lane L then holds its units' share of 32 row sums, which a
+// padded shared-memory transpose turns into one row per lane.  Split-K partials are reduced in
+// a fixed chunk order by whichever CTA completes a row block last (deterministic, no float
+// atomics).  Programmatic dependent launch: the first chunk is staged (sketch only) before
+// griddepcontrol.wait, so it overlaps the previous kernel.  usk_linear_batch puts several
+// linears that share x (q|k|v, gate|up) in one launch.
 #include <algorithm>
 
 #include "common.cuh"
@@ -29,8 +30,9 @@
 namespace usk {
 namespace {
 
-constexpr int kQThreads = 256;
+constexpr int kQThreads = 512;
 constexpr int kQWarps = kQThreads / 32;
+constexpr int kRB = kQWarps * 32;                 // rows per item
 constexpr int kMaxBatch = 8;
 constexpr int kScratchWords = kQWarps * 32 * 33;  // GEMV transpose scratch
 
@@ -45,8 +47,8 @@ struct QLayer {
   int64_t o_begin;     // first output row
   int64_t rows;        // rows in [o_begin, o_end)
   int32_t n_chunks;    // unit chunks of TJ
-  int32_t n_rb;        // row blocks
-  int32_t cta_begin;   // first CTA of this layer in the launch
+  int32_t n_rb;        // row blocks of kRB
+  int32_t item_begin;  // first item of this layer in the launch
   int32_t pad;
   // gemv
   void* y;
@@ -60,9 +62,9 @@ struct QLayer {
 struct QArgs {
   QLayer layer[kMaxBatch];
   int32_t n_layers;
+  int32_t total_items;
   int32_t M;
   int32_t maxMN;       // smem slot stride (cells) = max over the launch's layers
-  int32_t rb_rows;     // rows per CTA
   int64_t in;          // in_features (shared by the batch)
   const void* sketch;
   const int32_t* ncols;
@@ -75,12 +77,6 @@ struct QArgs {
   int32_t y_bf16;
 };
 
-__device__ __forceinline__ int find_qlayer(const QArgs& A, int b) {
-  int t = 0;
-  while (t + 1 < A.n_layers && A.layer[t + 1].cta_begin <= b) ++t;
-  return t;
-}
-
 template <int UPL, int MT>
 struct LaneState {
   static constexpr int MR = MT > 0 ? MT : 1;
@@ -89,11 +85,10 @@ struct LaneState {
   uint32_t rstride[UPL]; // bytes between sketch rows (runtime-M kernels)
 };
 
-// Stage the CTA's unit cells (rho codes, bank-private layout) + R(o) of its rows; set up the
-// per-lane unit state.  Reads only plan arrays and the sketch (independent of x).
+// Stage one chunk's cells (rho codes, bank-private layout) and set up the lane state.
 template <typename E, int UPL, int MT>
-__device__ __forceinline__ void stage(const QArgs& A, const QLayer& Ly, int64_t j0, int nu, int64_t r0,
-                                      uint32_t* Rs, uint32_t* cells, uint32_t* zero, LaneState<UPL, MT>& S) {
+__device__ __forceinline__ void stage_chunk(const QArgs& A, const QLayer& Ly, int64_t j0, int nu, uint32_t* cells,
+                                            uint32_t* zero, LaneState<UPL, MT>& S) {
   constexpr int TJ = 32 * UPL;
   const int lane = threadIdx.x & 31;
   const E* sk = reinterpret_cast<const E*>(A.sketch);
@@ -113,11 +108,6 @@ __device__ __forceinline__ void stage(const QArgs& A, const QLayer& Ly, int64_t 
       }
     }
   }
-  for (int r = threadIdx.x; r < A.rb_rows; r += kQThreads) {
-    const int64_t rr = min(r0 + r, Ly.rows - 1);
-    Rs[r] = A.R[Ly.o_begin + rr];
-  }
-  if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
   const uint32_t cbase = smem_u32(cells), zbase = smem_u32(zero);
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
@@ -167,147 +157,155 @@ __device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<U
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// ------------------------------------------------------------------ K3: reconstruct
-template <typename E, int UPL, int MT, int HASH>
-__global__ void __launch_bounds__(kQThreads) k_reconstruct_fast(const __grid_constant__ QArgs A) {
+// ------------------------------------------------------------------ K3 / K4 persistent kernel
+template <typename E, int UPL, int MT, int HASH, bool GEMV>
+__global__ void __launch_bounds__(kQThreads) k_query_fast(const __grid_constant__ QArgs A) {
   constexpr int TJ = 32 * UPL;
   extern __shared__ __align__(16) uint32_t qsm[];
-  const int li = find_qlayer(A, blockIdx.x);
-  const QLayer& Ly = A.layer[li];
-  const int b = blockIdx.x - Ly.cta_begin;
-  const int chunk = b % Ly.n_chunks, rbk = b / Ly.n_chunks;
-  const int64_t j0 = (int64_t)chunk * TJ;
-  const int nu = (int)min((int64_t)TJ, A.in - j0);
-  const int64_t r0 = (int64_t)rbk * A.rb_rows;
-  const int rows = (int)min((int64_t)A.rb_rows, Ly.rows - r0);
-  uint32_t* Rs = qsm;
-  uint32_t* zero = qsm + A.rb_rows;
+  __shared__ int s_last;
+  float* scratch = reinterpret_cast<float*>(qsm);                // GEMV only
+  uint32_t* Rs = qsm + (GEMV ? kScratchWords : 0);
+  uint32_t* zero = Rs + kRB;
   uint32_t* cells = zero + 32;
-  LaneState<UPL, MT> S;
-  stage<E, UPL, MT>(A, Ly, j0, nu, r0, Rs, cells, zero, S);
-  __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bool full_tile = (nu == TJ);
-  E* dst = reinterpret_cast<E*>(Ly.w_out) + (r0 + warp) * Ly.ld_out + j0 + UPL * lane;
-  const int64_t dstep = (int64_t)kQWarps * Ly.ld_out;
-#pragma unroll 2
-  for (int r = warp; r < rows; r += kQWarps, dst += dstep) {
-    const int64_t o = Ly.o_begin + r0 + r;
-    const uint32_t Rv = Rs[r];
-    uint32_t wb[UPL];
-#pragma unroll
-    for (int v = 0; v < UPL; ++v) wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, o)) ^ 0x80000000u;
-    if constexpr (sizeof(E) == 2) {
-      if (full_tile) {
-        if constexpr (UPL == 4) {
-          *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(wb[0], wb[1 % UPL], 0x7632),
-                                                      __byte_perm(wb[2 % UPL], wb[3 % UPL], 0x7632));
-        } else if constexpr (UPL == 2) {
-          *reinterpret_cast<uint32_t*>(dst) = __byte_perm(wb[0], wb[1 % UPL], 0x7632);
-        } else {
-          dst[0] = (E)(wb[0] >> 16);
-        }
-      } else {
-#pragma unroll
-        for (int v = 0; v < UPL; ++v)
-          if (UPL * lane + v < nu) dst[v] = (E)(wb[v] >> 16);
-      }
-    } else {
-      if (full_tile && UPL == 4) {
-        *reinterpret_cast<uint4*>(dst) = make_uint4(wb[0], wb[1 % UPL], wb[2 % UPL], wb[3 % UPL]);
-      } else if (full_tile && UPL == 2) {
-        *reinterpret_cast<uint2*>(dst) = make_uint2(wb[0], wb[1 % UPL]);
-      } else {
-#pragma unroll
-        for (int v = 0; v < UPL; ++v)
-          if (UPL * lane + v < nu) dst[v] = wb[v];
-      }
-    }
-  }
-}
-
-// ------------------------------------------------------------------ K4: sketch-GEMV
-template <typename E, int UPL, int MT, int HASH>
-__global__ void __launch_bounds__(kQThreads) k_gemv_fast(const __grid_constant__ QArgs A) {
-  constexpr int TJ = 32 * UPL;
-  extern __shared__ __align__(16) uint32_t qsm[];
-  __shared__ bool s_last;
-  const int li = find_qlayer(A, blockIdx.x);
-  const QLayer& Ly = A.layer[li];
-  const int b = blockIdx.x - Ly.cta_begin;
-  const int chunk = b % Ly.n_chunks, rbk = b / Ly.n_chunks;
-  const int64_t j0 = (int64_t)chunk * TJ;
-  const int nu = (int)min((int64_t)TJ, A.in - j0);
-  const int64_t r0 = (int64_t)rbk * A.rb_rows;
-  const int rows = (int)min((int64_t)A.rb_rows, Ly.rows - r0);
-  float* scratch = reinterpret_cast<float*>(qsm);
-  uint32_t* Rs = qsm + kScratchWords;
-  uint32_t* zero = Rs + A.rb_rows;
-  uint32_t* cells = zero + 32;
-  LaneState<UPL, MT> S;
-  stage<E, UPL, MT>(A, Ly, j0, nu, r0, Rs, cells, zero, S);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  // x depends on the previous kernel in the stream: wait for it only now
-  pdl_wait();
+  const int it0 = (int)(((int64_t)blockIdx.x * A.total_items) / gridDim.x);
+  const int it1 = (int)(((int64_t)(blockIdx.x + 1) * A.total_items) / gridDim.x);
+  int cur_li = -1, cur_chunk = -1;
+  bool waited = false;
+  LaneState<UPL, MT> S;
   float nx[UPL];
 #pragma unroll
-  for (int v = 0; v < UPL; ++v) {
-    const int64_t j = j0 + UPL * lane + v;
-    float xv = 0.f;
-    if (UPL * lane + v < nu)
-      xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
-                    : reinterpret_cast<const float*>(A.x)[j];
-    nx[v] = -xv;  // rotr(rho) decodes to -w'
-  }
-  __syncthreads();
+  for (int v = 0; v < UPL; ++v) nx[v] = 0.f;
 
-  float* P = Ly.partial + (int64_t)chunk * Ly.rows + r0;
-  float* sc = scratch + warp * (32 * 33);
-  for (int s0 = warp * 32; s0 < rows; s0 += kQWarps * 32) {
-    float acc[32];
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const uint32_t Rv = Rs[s0 + r];
-      float a = 0.f;
-#pragma unroll
-      for (int v = 0; v < UPL; ++v)
-        a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + s0 + r))), a);
-      acc[r] = a;
+  for (int it = it0; it < it1; ++it) {
+    int li = 0;
+    while (li + 1 < A.n_layers && A.layer[li + 1].item_begin <= it) ++li;
+    const QLayer& Ly = A.layer[li];
+    const int local = it - Ly.item_begin;
+    const int chunk = local / Ly.n_rb, rbk = local % Ly.n_rb;
+    const int64_t j0 = (int64_t)chunk * TJ;
+    const int nu = (int)min((int64_t)TJ, A.in - j0);
+    const int64_t r0 = (int64_t)rbk * kRB;
+    const int rows = (int)min((int64_t)kRB, Ly.rows - r0);
+
+    if constexpr (GEMV) {
+      if (it == it1 - 1 && waited) pdl_trigger();  // let the next kernel's prologue start
     }
-    // transpose through padded shared memory: lane r sums row r over the 32 lanes (fixed order)
+    __syncthreads();  // previous item is done with cells / Rs
+    if (li != cur_li || chunk != cur_chunk) {
+      stage_chunk<E, UPL, MT>(A, Ly, j0, nu, cells, zero, S);
+      cur_li = li;
+      cur_chunk = chunk;
+      if constexpr (GEMV) {
+        if (!waited) {  // x may be written by the previous kernel on the stream
+          pdl_wait();
+          waited = true;
+        }
 #pragma unroll
-    for (int r = 0; r < 32; ++r) sc[r * 33 + lane] = acc[r];
-    __syncwarp();
-    float s = 0.f;
+        for (int v = 0; v < UPL; ++v) {
+          const int64_t j = j0 + UPL * lane + v;
+          float xv = 0.f;
+          if (UPL * lane + v < nu)
+            xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
+                          : reinterpret_cast<const float*>(A.x)[j];
+          nx[v] = -xv;  // rotr(rho) decodes to -w'
+        }
+      }
+    }
+    {
+      const int r = threadIdx.x;  // kQThreads == kRB
+      Rs[r] = A.R[Ly.o_begin + r0 + min(r, rows - 1)];
+      if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
+    }
+    __syncthreads();
+
+    const int s0 = warp * 32;
+    if constexpr (GEMV) {
+      float acc[32];
 #pragma unroll
-    for (int k = 0; k < 32; ++k) s += sc[lane * 33 + k];
-    __syncwarp();
-    if (s0 + lane < rows) P[s0 + lane] = s;
-  }
-  // ---- deterministic split-K: the last CTA of this row block sums chunks in order
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    const uint32_t prev = atomicAdd(&Ly.counters[rbk], 1u);
-    s_last = (prev == (uint32_t)Ly.n_chunks - 1);
-  }
-  __syncthreads();
-  pdl_trigger();
-  if (!s_last) return;
-  __threadfence();
-  for (int r = threadIdx.x; r < rows; r += kQThreads) {
-    float s = 0.f;
-    const float* p = Ly.partial + r0 + r;
-    for (int c = 0; c < Ly.n_chunks; ++c) s += __ldcg(p + (int64_t)c * Ly.rows);
-    if (A.y_bf16) {
-      const uint32_t bb = __float_as_uint(s);
-      reinterpret_cast<uint16_t*>(Ly.y)[r0 + r] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
+      for (int r = 0; r < 32; ++r) {
+        const uint32_t Rv = Rs[s0 + r];
+        float a = 0.f;
+#pragma unroll
+        for (int v = 0; v < UPL; ++v)
+          a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + s0 + r))), a);
+        acc[r] = a;
+      }
+      // transpose through padded shared memory: lane r sums row r over the 32 lanes (fixed order)
+      float* sc = scratch + warp * (32 * 33);
+#pragma unroll
+      for (int r = 0; r < 32; ++r) sc[r * 33 + lane] = acc[r];
+      __syncwarp();
+      float s = 0.f;
+#pragma unroll
+      for (int k = 0; k < 32; ++k) s += sc[lane * 33 + k];
+      if (s0 + lane < rows) Ly.partial[(int64_t)chunk * Ly.rows + r0 + s0 + lane] = s;
+      // ---- deterministic split-K: the CTA completing row block rbk sums its chunks in order
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) s_last = (atomicAdd(&Ly.counters[rbk], 1u) == (uint32_t)Ly.n_chunks - 1);
+      __syncthreads();
+      if (s_last) {
+        __threadfence();
+        const int r = threadIdx.x;
+        if (r < rows) {
+          float t = 0.f;
+          const float* p = Ly.partial + r0 + r;
+          for (int c = 0; c < Ly.n_chunks; ++c) t += __ldcg(p + (int64_t)c * Ly.rows);
+          if (A.y_bf16) {
+            const uint32_t bb = __float_as_uint(t);
+            reinterpret_cast<uint16_t*>(Ly.y)[r0 + r] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
+          } else {
+            reinterpret_cast<float*>(Ly.y)[r0 + r] = t;
+          }
+        }
+        if (threadIdx.x == 0) Ly.counters[rbk] = 0u;  // leave the workspace zeroed
+      }
     } else {
-      reinterpret_cast<float*>(Ly.y)[r0 + r] = s;
+      const bool full_tile = (nu == TJ);
+#pragma unroll 4
+      for (int r = 0; r < 32; ++r) {
+        if (s0 + r >= rows) break;
+        const int64_t o = Ly.o_begin + r0 + s0 + r;
+        const uint32_t Rv = Rs[s0 + r];
+        uint32_t wb[UPL];
+#pragma unroll
+        for (int v = 0; v < UPL; ++v) wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, o)) ^ 0x80000000u;
+        E* dst = reinterpret_cast<E*>(Ly.w_out) + (r0 + s0 + r) * Ly.ld_out + j0 + UPL * lane;
+        if constexpr (sizeof(E) == 2) {
+          if (full_tile) {
+            if constexpr (UPL == 4) {
+              *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(wb[0], wb[1 % UPL], 0x7632),
+                                                          __byte_perm(wb[2 % UPL], wb[3 % UPL], 0x7632));
+            } else if constexpr (UPL == 2) {
+              *reinterpret_cast<uint32_t*>(dst) = __byte_perm(wb[0], wb[1 % UPL], 0x7632);
+            } else {
+              dst[0] = (E)(wb[0] >> 16);
+            }
+          } else {
+#pragma unroll
+            for (int v = 0; v < UPL; ++v)
+              if (UPL * lane + v < nu) dst[v] = (E)(wb[v] >> 16);
+          }
+        } else {
+          if (full_tile && UPL == 4) {
+            *reinterpret_cast<uint4*>(dst) = make_uint4(wb[0], wb[1 % UPL], wb[2 % UPL], wb[3 % UPL]);
+          } else if (full_tile && UPL == 2) {
+            *reinterpret_cast<uint2*>(dst) = make_uint2(wb[0], wb[1 % UPL]);
+          } else {
+#pragma unroll
+            for (int v = 0; v < UPL; ++v)
+              if (UPL * lane + v < nu) dst[v] = wb[v];
+          }
+        }
+      }
     }
   }
-  if (threadIdx.x == 0) Ly.counters[rbk] = 0u;  // leave the workspace zeroed for the next call
+  if constexpr (GEMV) {
+    if (!waited) pdl_wait();
+    pdl_trigger();
+  }
 }
 
 // ------------------------------------------------------------------ generic query path
@@ -391,47 +389,50 @@ bool fast_eligible(const usk_plan* pl) { return pl->gran == USK_GRAN_ROW && pl->
 
 struct Geom {
   int upl = 0;
-  int rb_rows = 0;
   int maxMN = 0;
   size_t smem = 0;
-  int ctas = 0;
+  int items = 0;
+  int grid = 0;
   std::vector<int> n_chunks, n_rb;
 };
 
-size_t smem_bytes(bool gemv, int upl, int rb_rows, int maxMN) {
-  return (gemv ? (size_t)kScratchWords * 4 : 0) + (size_t)rb_rows * 4 + 128 + (size_t)32 * upl * maxMN * 4;
+size_t smem_bytes(bool gemv, int upl, int maxMN) {
+  return (gemv ? (size_t)kScratchWords * 4 : 0) + (size_t)kRB * 4 + 128 + (size_t)32 * upl * maxMN * 4;
 }
 
-// Pick units-per-lane and the row block for a launch covering `layers` (rows each).
+constexpr size_t kSmemMax = 220 * 1024;
+constexpr size_t kSmemPerSM = 228 * 1024;
+
+// Pick units-per-lane and the persistent grid for a launch covering `layers` (rows each).
+// Larger UPL amortises the per-row work (R(o) load, transpose) over more weights; it must still
+// leave >= 148 items so every SM gets work.
 Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n, bool gemv) {
   Geom G;
-  int64_t maxrows = 0;
-  for (int k = 0; k < n; ++k) {
-    G.maxMN = std::max(G.maxMN, pl->M * pl->layers[layers[k]].max_ncols);
-    maxrows = std::max(maxrows, rows[k]);
-  }
+  for (int k = 0; k < n; ++k) G.maxMN = std::max(G.maxMN, pl->M * pl->layers[layers[k]].max_ncols);
   const int64_t in = pl->layers[layers[0]].in;
-  G.rb_rows = gemv ? (int)std::min<int64_t>(256, ((maxrows + 31) / 32) * 32) : 256;
-  const size_t limit2 = 110 * 1024, limit1 = 220 * 1024;
+  auto items_for = [&](int upl) {
+    int it = 0;
+    for (int k = 0; k < n; ++k)
+      it += (int)((in + 32 * upl - 1) / (32 * upl)) * (int)((rows[k] + kRB - 1) / kRB);
+    return it;
+  };
   int best = 0;
   for (int upl : {4, 2, 1}) {
-    const size_t sm = smem_bytes(gemv, upl, G.rb_rows, G.maxMN);
-    if (sm > limit1) continue;
-    int ctas = 0;
-    for (int k = 0; k < n; ++k)
-      ctas += (int)((in + 32 * upl - 1) / (32 * upl)) * (int)((rows[k] + G.rb_rows - 1) / G.rb_rows);
-    if (!best) best = upl;                                        // largest that fits at all
-    if (sm <= limit2 && ctas >= 2 * 148) { best = upl; break; }   // enough CTAs at >= 2 CTAs/SM
-    if (sm <= limit2 && best > upl && ctas >= 148) best = upl;
+    if (smem_bytes(gemv, upl, G.maxMN) > kSmemMax) continue;
+    best = upl;
+    if (items_for(upl) >= 148) break;
   }
   if (!best) return G;
   G.upl = best;
-  G.smem = smem_bytes(gemv, best, G.rb_rows, G.maxMN);
+  G.smem = smem_bytes(gemv, best, G.maxMN);
   for (int k = 0; k < n; ++k) {
     G.n_chunks.push_back((int)((in + 32 * best - 1) / (32 * best)));
-    G.n_rb.push_back((int)((rows[k] + G.rb_rows - 1) / G.rb_rows));
-    G.ctas += G.n_chunks.back() * G.n_rb.back();
+    G.n_rb.push_back((int)((rows[k] + kRB - 1) / kRB));
+    G.items += G.n_chunks.back() * G.n_rb.back();
   }
+  const int per_sm = std::max<int>(1, std::min<int>(4, (int)(kSmemPerSM / (G.smem + 1024))));
+  const int resident = 148 * std::min(per_sm, 2048 / kQThreads);
+  G.grid = std::min(G.items, resident);
   return G;
 }
 
@@ -444,7 +445,7 @@ QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& 
   QArgs A{};
   A.M = pl->M;
   A.maxMN = G.maxMN;
-  A.rb_rows = G.rb_rows;
+  A.total_items = G.items;
   A.in = in;
   A.sketch = sketch;
   A.ncols = pl->d_ncols;
@@ -455,24 +456,21 @@ QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& 
   return A;
 }
 
-#define USK_PICK(KNAME)                                                                \
-  template <typename E, int UPL>                                                       \
-  void* pick_##KNAME(int M, int hash) {                                                \
-    if (hash == USK_HASH_IDENTITY) return (void*)KNAME<E, UPL, 0, USK_HASH_IDENTITY>;  \
-    switch (M) {                                                                       \
-      case 1: return (void*)KNAME<E, UPL, 1, USK_HASH_X>;                              \
-      case 2: return (void*)KNAME<E, UPL, 2, USK_HASH_X>;                              \
-      case 3: return (void*)KNAME<E, UPL, 3, USK_HASH_X>;                              \
-      default: return (void*)KNAME<E, UPL, 0, USK_HASH_X>;                             \
-    }                                                                                  \
+template <typename E, int UPL, bool GEMV>
+void* pick_m(int M, int hash) {
+  if (hash == USK_HASH_IDENTITY) return (void*)k_query_fast<E, UPL, 0, USK_HASH_IDENTITY, GEMV>;
+  switch (M) {
+    case 1: return (void*)k_query_fast<E, UPL, 1, USK_HASH_X, GEMV>;
+    case 2: return (void*)k_query_fast<E, UPL, 2, USK_HASH_X, GEMV>;
+    case 3: return (void*)k_query_fast<E, UPL, 3, USK_HASH_X, GEMV>;
+    default: return (void*)k_query_fast<E, UPL, 0, USK_HASH_X, GEMV>;
   }
-USK_PICK(k_reconstruct_fast)
-USK_PICK(k_gemv_fast)
+}
 
 template <int UPL>
 void* pick_upl(bool gemv, bool bf16, int M, int hash) {
-  if (gemv) return bf16 ? pick_k_gemv_fast<uint16_t, UPL>(M, hash) : pick_k_gemv_fast<uint32_t, UPL>(M, hash);
-  return bf16 ? pick_k_reconstruct_fast<uint16_t, UPL>(M, hash) : pick_k_reconstruct_fast<uint32_t, UPL>(M, hash);
+  if (gemv) return bf16 ? pick_m<uint16_t, UPL, true>(M, hash) : pick_m<uint32_t, UPL, true>(M, hash);
+  return bf16 ? pick_m<uint16_t, UPL, false>(M, hash) : pick_m<uint32_t, UPL, false>(M, hash);
 }
 
 void* pick_fast(int upl, bool gemv, bool bf16, int M, int hash) {
@@ -483,15 +481,23 @@ void* pick_fast(int upl, bool gemv, bool bf16, int M, int hash) {
   }
 }
 
-usk_status launch_q(void* kern, const QArgs& A, int ctas, size_t smem, bool pdl, cudaStream_t st) {
-  // max dynamic smem is raised once per kernel (before any graph capture: callers warm up)
+usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl, cudaStream_t st) {
+  // max dynamic smem is raised once per kernel (callers warm up before any graph capture)
   static std::vector<void*> raised;
   if (std::find(raised.begin(), raised.end(), kern) == raised.end()) {
-    USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
     raised.push_back(kern);
   }
+  int occ = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQThreads, smem) != cudaSuccess || occ < 1) occ = 1;
+  int sms = 148;
+  {
+    int dev = 0;
+    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  grid = std::min(grid, sms * occ);  // persistent: every CTA resident
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3((unsigned)ctas);
+  cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kQThreads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -556,26 +562,31 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
     A.x_bf16 = x_dtype == USK_BF16;
     A.y_bf16 = y_dtype == USK_BF16;
     char* w = reinterpret_cast<char*>(ws);
-    int cta = 0;
+    int item = 0;
     for (int k = 0; k < n; ++k) {
-      if (rows[k] == 0) continue;
+      const size_t wsb = layer_ws_bytes(G.n_chunks[k], G.n_rb[k], rows[k]);
+      if (rows[k] == 0) {
+        w += wsb;
+        continue;
+      }
       QLayer& Ly = A.layer[A.n_layers++];
       Ly.unit_base = pl->layers[layers[k]].unit_begin;
       Ly.o_begin = o0[k];
       Ly.rows = rows[k];
       Ly.n_chunks = G.n_chunks[k];
       Ly.n_rb = G.n_rb[k];
-      Ly.cta_begin = cta;
-      cta += Ly.n_chunks * Ly.n_rb;
+      Ly.item_begin = item;
+      item += Ly.n_chunks * Ly.n_rb;
       Ly.y = y[k];
       Ly.partial = reinterpret_cast<float*>(w);
       const size_t p = ((size_t)Ly.n_chunks * rows[k] * 4 + 255) / 256 * 256;
       Ly.counters = reinterpret_cast<uint32_t*>(w + p);
-      w += layer_ws_bytes(Ly.n_chunks, Ly.n_rb, rows[k]);
+      w += wsb;
     }
     if (!A.n_layers) return USK_OK;
+    A.total_items = item;
     void* k = pick_fast(G.upl, true, pl->dtype == USK_BF16, pl->M, pl->hash);
-    return launch_q(k, A, cta, G.smem, true, st);
+    return launch_q(k, A, std::min(G.grid, item), G.smem, true, st);
   }
   for (int k = 0; k < n; ++k) {
     if (rows[k] == 0) continue;
@@ -610,11 +621,11 @@ usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l,
     Ly.rows = rows;
     Ly.n_chunks = G.n_chunks[0];
     Ly.n_rb = G.n_rb[0];
-    Ly.cta_begin = 0;
+    Ly.item_begin = 0;
     Ly.w_out = w_out;
     Ly.ld_out = ld;
     void* k = pick_fast(G.upl, false, pl->dtype == USK_BF16, pl->M, pl->hash);
-    return launch_q(k, A, G.ctas, G.smem, false, st);
+    return launch_q(k, A, G.grid, G.smem, false, st);
   }
   GenQ Q = make_genq(pl, l, sketch);
   const int64_t n = rows * L.in;
