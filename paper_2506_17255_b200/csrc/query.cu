@@ -4,26 +4,31 @@
 // indices in a batch ... interpreting these intermediate results"):
 //   w'(o, j) = the bonded cell of maximum |.| over rows i < M (ties -> non-negative, L1/L2).
 //
-// Fast path (ROW granularity, one input dimension per unit).  Work is cut into ITEMS =
-// (layer, chunk of TJ = 32*UPL consecutive units, block of 32*warps output rows), ordered
-// layer-major, chunk-major.  A persistent grid (<= resident CTAs) takes contiguous item ranges,
-// so a CTA stages a chunk's cells once and reuses them over many row blocks.  Lane L owns units
-// UPL*L+v; their cells are staged into shared memory as rho codes
-//     rho = rotl(bits_hi, 1) ^ 1 = (mag << 1) | (1 - sign)
-// at byte address  cells + 4*(v*32*maxMN + k*32 + L)  -- always bank L, so the M random
-// gathers of a warp never conflict.  The Eq. 5 select is an integer max (VIMNMX3 for M=3) and
-// rotr(rho, 1) is the IEEE pattern of -w', so the GEMV multiplies by -x (exact).
-// Per weight and lane: 1 LOP3 (R(o) ^ K_u) + M x (IMAD, IMAD.HI, LEA, LDS) + max + SHF + FFMA.
-// Missing units of a ragged chunk point at a shared "zero" cell (rho of +0) with x = 0, so the
-// inner loop has no branches.
-//
-// GEMV: a warp computes 32 rows; lane L then holds its units' share of 32 row sums, which a
-// padded shared-memory transpose turns into one row per lane.  Split-K partials are reduced in
-// a fixed chunk order by whichever CTA completes a row block last (deterministic, no float
-// atomics).  Programmatic dependent launch: the first chunk is staged (sketch only) before
-// griddepcontrol.wait, so it overlaps the previous kernel.  usk_linear_batch puts several
-// linears that share x (q|k|v, gate|up) in one launch.
+// Fast path (ROW granularity, one input dimension per unit).
+//   * Each CTA owns one CHUNK of TJ = 32*UPL consecutive units (input dims) of one layer and a
+//     contiguous range of 32-row SUBTILES; the chunk's cells are staged into shared memory once
+//     and reused over the whole row range (a cell is hit by ~out/N rows, so a CTA must cover
+//     many rows for the staging to amortise).  Grid = sum over layers of n_chunks x cpc, with
+//     cpc (CTAs per chunk) chosen so that the grid is one resident wave.
+//   * Lane L owns units UPL*L+v.  Their cells sit in shared memory as rho codes
+//         rho = rotl(bits_hi, 1) ^ 1 = (mag << 1) | (1 - sign)
+//     at byte address  cells + 4*(v*32*maxMN + k*32 + L)  -- always bank L, so the M random
+//     gathers of a warp never conflict.  The Eq. 5 select is an integer max (VIMNMX3 for M=3)
+//     and rotr(rho, 1) is the IEEE pattern of -w', so the GEMV multiplies by -x (exact).
+//     Per weight and lane: 1 LOP3 (R(o) ^ K_u) + M x (IMAD, IMAD.HI, LEA, LDS) + max + SHF + FFMA.
+//   * Missing units of a ragged chunk point at a shared "zero" cell (rho of +0) with x = 0, so
+//     the inner loop has no branches.  R(o) for a subtile is one register per lane (lane r holds
+//     R(o0 + r)), broadcast with SHFL, prefetched one subtile ahead.
+//   * GEMV: per subtile a warp holds 32 row partials per lane; a transpose butterfly leaves row r
+//     on lane r.  Partials go to a row-major [rows][CP] workspace; the warp that completes a
+//     subtile's last chunk (atomic counter per subtile) sums the chunks in fixed order with
+//     float4 loads (deterministic, no float atomics) and writes y.
+//   * Programmatic dependent launch: the chunk is staged (sketch only) before
+//     griddepcontrol.wait, overlapping the previous kernel; x is read after it.
+//     usk_linear_batch puts several linears that share x (q|k|v, gate|up) in one launch.
 #include <algorithm>
+#include <cstdlib>
+#include <mutex>
 
 #include "common.cuh"
 
@@ -32,9 +37,7 @@ namespace {
 
 constexpr int kQThreads = 512;
 constexpr int kQWarps = kQThreads / 32;
-constexpr int kRB = kQWarps * 32;                 // rows per item
 constexpr int kMaxBatch = 8;
-constexpr int kScratchWords = kQWarps * 32 * 33;  // GEMV transpose scratch
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
@@ -47,13 +50,15 @@ struct QLayer {
   int64_t o_begin;     // first output row
   int64_t rows;        // rows in [o_begin, o_end)
   int32_t n_chunks;    // unit chunks of TJ
-  int32_t n_rb;        // row blocks of kRB
-  int32_t item_begin;  // first item of this layer in the launch
+  int32_t n_sub;       // 32-row subtiles
+  int32_t cpc;         // CTAs per chunk
+  int32_t cta_begin;   // first CTA of this layer in the launch
+  int32_t CP;          // row stride of the partial workspace (>= n_chunks, multiple of 4)
   int32_t pad;
   // gemv
   void* y;
-  float* partial;      // [n_chunks][rows]
-  uint32_t* counters;  // [n_rb]
+  float* partial;      // [rows][CP]
+  uint32_t* counters;  // [n_sub]
   // reconstruct
   void* w_out;
   int64_t ld_out;
@@ -62,9 +67,9 @@ struct QLayer {
 struct QArgs {
   QLayer layer[kMaxBatch];
   int32_t n_layers;
-  int32_t total_items;
   int32_t M;
   int32_t maxMN;       // smem slot stride (cells) = max over the launch's layers
+  int32_t early_trigger;
   int64_t in;          // in_features (shared by the batch)
   const void* sketch;
   const int32_t* ncols;
@@ -108,6 +113,7 @@ __device__ __forceinline__ void stage_chunk(const QArgs& A, const QLayer& Ly, in
       }
     }
   }
+  if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
   const uint32_t cbase = smem_u32(cells), zbase = smem_u32(zero);
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
@@ -154,125 +160,125 @@ __device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<U
   }
 }
 
+// Row r of the warp's 32 partial rows ends on lane r (fixed-order butterfly).
+__device__ __forceinline__ float transpose_reduce32(float (&acc)[32], int lane) {
+#pragma unroll
+  for (int m = 16; m >= 1; m >>= 1) {
+    const bool up = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < m; ++i) {
+      const float send = up ? acc[i] : acc[i + m];
+      const float keep = up ? acc[i + m] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  return acc[0];
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// ------------------------------------------------------------------ K3 / K4 persistent kernel
 template <typename E, int UPL, int MT, int HASH, bool GEMV>
 __global__ void __launch_bounds__(kQThreads) k_query_fast(const __grid_constant__ QArgs A) {
   constexpr int TJ = 32 * UPL;
   extern __shared__ __align__(16) uint32_t qsm[];
-  __shared__ int s_last;
-  float* scratch = reinterpret_cast<float*>(qsm);                // GEMV only
-  uint32_t* Rs = qsm + (GEMV ? kScratchWords : 0);
-  uint32_t* zero = Rs + kRB;
-  uint32_t* cells = zero + 32;
+  uint32_t* zero = qsm;
+  uint32_t* cells = qsm + 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
-  const int it0 = (int)(((int64_t)blockIdx.x * A.total_items) / gridDim.x);
-  const int it1 = (int)(((int64_t)(blockIdx.x + 1) * A.total_items) / gridDim.x);
-  int cur_li = -1, cur_chunk = -1;
-  bool waited = false;
+  int li = 0;
+  while (li + 1 < A.n_layers && A.layer[li + 1].cta_begin <= (int)blockIdx.x) ++li;
+  const QLayer& Ly = A.layer[li];
+  const int b = blockIdx.x - Ly.cta_begin;
+  const int chunk = b / Ly.cpc, part = b % Ly.cpc;
+  const int sub0 = (int)(((int64_t)part * Ly.n_sub) / Ly.cpc);
+  const int sub1 = (int)(((int64_t)(part + 1) * Ly.n_sub) / Ly.cpc);
+  const int64_t j0 = (int64_t)chunk * TJ;
+  const int nu = (int)min((int64_t)TJ, A.in - j0);
+
   LaneState<UPL, MT> S;
+  stage_chunk<E, UPL, MT>(A, Ly, j0, nu, cells, zero, S);
   float nx[UPL];
+  if constexpr (GEMV) {
+    pdl_wait();  // x may be written by the previous kernel on the stream
+    if (A.early_trigger) pdl_trigger();
 #pragma unroll
-  for (int v = 0; v < UPL; ++v) nx[v] = 0.f;
-
-  for (int it = it0; it < it1; ++it) {
-    int li = 0;
-    while (li + 1 < A.n_layers && A.layer[li + 1].item_begin <= it) ++li;
-    const QLayer& Ly = A.layer[li];
-    const int local = it - Ly.item_begin;
-    const int chunk = local / Ly.n_rb, rbk = local % Ly.n_rb;
-    const int64_t j0 = (int64_t)chunk * TJ;
-    const int nu = (int)min((int64_t)TJ, A.in - j0);
-    const int64_t r0 = (int64_t)rbk * kRB;
-    const int rows = (int)min((int64_t)kRB, Ly.rows - r0);
-
-    if constexpr (GEMV) {
-      if (it == it1 - 1 && waited) pdl_trigger();  // let the next kernel's prologue start
+    for (int v = 0; v < UPL; ++v) {
+      const int64_t j = j0 + UPL * lane + v;
+      float xv = 0.f;
+      if (UPL * lane + v < nu)
+        xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
+                      : reinterpret_cast<const float*>(A.x)[j];
+      nx[v] = -xv;  // rotr(rho) decodes to -w'
     }
-    __syncthreads();  // previous item is done with cells / Rs
-    if (li != cur_li || chunk != cur_chunk) {
-      stage_chunk<E, UPL, MT>(A, Ly, j0, nu, cells, zero, S);
-      cur_li = li;
-      cur_chunk = chunk;
-      if constexpr (GEMV) {
-        if (!waited) {  // x may be written by the previous kernel on the stream
-          pdl_wait();
-          waited = true;
-        }
-#pragma unroll
-        for (int v = 0; v < UPL; ++v) {
-          const int64_t j = j0 + UPL * lane + v;
-          float xv = 0.f;
-          if (UPL * lane + v < nu)
-            xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
-                          : reinterpret_cast<const float*>(A.x)[j];
-          nx[v] = -xv;  // rotr(rho) decodes to -w'
-        }
-      }
-    }
-    {
-      const int r = threadIdx.x;  // kQThreads == kRB
-      Rs[r] = A.R[Ly.o_begin + r0 + min(r, rows - 1)];
-      if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
-    }
-    __syncthreads();
+  }
+  __syncthreads();
 
-    const int s0 = warp * 32;
+  const uint32_t* Rg = A.R + Ly.o_begin;
+  int sub = sub0 + warp;
+  uint32_t Rnext = 0;
+  if (sub < sub1) Rnext = Rg[min((int64_t)sub * 32 + lane, Ly.rows - 1)];
+  for (; sub < sub1; sub += kQWarps) {
+    const uint32_t Rl = Rnext;
+    if (sub + kQWarps < sub1) Rnext = Rg[min((int64_t)(sub + kQWarps) * 32 + lane, Ly.rows - 1)];
+    const int64_t r0 = (int64_t)sub * 32;  // first local row of the subtile
+    const int nrow = (int)min((int64_t)32, Ly.rows - r0);
     if constexpr (GEMV) {
       float acc[32];
 #pragma unroll
       for (int r = 0; r < 32; ++r) {
-        const uint32_t Rv = Rs[s0 + r];
+        const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
         float a = 0.f;
 #pragma unroll
         for (int v = 0; v < UPL; ++v)
-          a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + s0 + r))), a);
+          a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r))), a);
         acc[r] = a;
       }
-      // transpose through padded shared memory: lane r sums row r over the 32 lanes (fixed order)
-      float* sc = scratch + warp * (32 * 33);
-#pragma unroll
-      for (int r = 0; r < 32; ++r) sc[r * 33 + lane] = acc[r];
-      __syncwarp();
-      float s = 0.f;
-#pragma unroll
-      for (int k = 0; k < 32; ++k) s += sc[lane * 33 + k];
-      if (s0 + lane < rows) Ly.partial[(int64_t)chunk * Ly.rows + r0 + s0 + lane] = s;
-      // ---- deterministic split-K: the CTA completing row block rbk sums its chunks in order
+      const float s = transpose_reduce32(acc, lane);
+      if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = s;
       __threadfence();
-      __syncthreads();
-      if (threadIdx.x == 0) s_last = (atomicAdd(&Ly.counters[rbk], 1u) == (uint32_t)Ly.n_chunks - 1);
-      __syncthreads();
-      if (s_last) {
+      __syncwarp();
+      uint32_t prev = 0;
+      if (lane == 0) prev = atomicAdd(&Ly.counters[sub], 1u);
+      prev = __shfl_sync(0xffffffffu, prev, 0);
+      if (prev == (uint32_t)Ly.n_chunks - 1) {  // this warp completes the subtile: reduce in order
         __threadfence();
-        const int r = threadIdx.x;
-        if (r < rows) {
+        if (lane < nrow) {
+          const float4* p = reinterpret_cast<const float4*>(Ly.partial + (r0 + lane) * Ly.CP);
           float t = 0.f;
-          const float* p = Ly.partial + r0 + r;
-          for (int c = 0; c < Ly.n_chunks; ++c) t += __ldcg(p + (int64_t)c * Ly.rows);
+          int c = 0;
+          for (; c + 32 <= Ly.n_chunks; c += 32) {
+            float4 q[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) q[k] = __ldcg(p + c / 4 + k);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t = t + q[k].x + q[k].y + q[k].z + q[k].w;
+          }
+          for (; c < Ly.n_chunks; c += 4) {
+            const float4 q = __ldcg(p + c / 4);
+            const float w4[4] = {q.x, q.y, q.z, q.w};
+            for (int k = 0; k < 4 && c + k < Ly.n_chunks; ++k) t += w4[k];
+          }
           if (A.y_bf16) {
             const uint32_t bb = __float_as_uint(t);
-            reinterpret_cast<uint16_t*>(Ly.y)[r0 + r] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
+            reinterpret_cast<uint16_t*>(Ly.y)[r0 + lane] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
           } else {
-            reinterpret_cast<float*>(Ly.y)[r0 + r] = t;
+            reinterpret_cast<float*>(Ly.y)[r0 + lane] = t;
           }
         }
-        if (threadIdx.x == 0) Ly.counters[rbk] = 0u;  // leave the workspace zeroed
+        if (lane == 0) Ly.counters[sub] = 0u;  // leave the workspace zeroed for the next call
       }
     } else {
       const bool full_tile = (nu == TJ);
+      E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + j0 + UPL * lane;
 #pragma unroll 4
-      for (int r = 0; r < 32; ++r) {
-        if (s0 + r >= rows) break;
-        const int64_t o = Ly.o_begin + r0 + s0 + r;
-        const uint32_t Rv = Rs[s0 + r];
+      for (int r = 0; r < 32; ++r, dst += Ly.ld_out) {
+        const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
+        if (r >= nrow) continue;
         uint32_t wb[UPL];
 #pragma unroll
-        for (int v = 0; v < UPL; ++v) wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, o)) ^ 0x80000000u;
-        E* dst = reinterpret_cast<E*>(Ly.w_out) + (r0 + s0 + r) * Ly.ld_out + j0 + UPL * lane;
+        for (int v = 0; v < UPL; ++v)
+          wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r)) ^ 0x80000000u;
         if constexpr (sizeof(E) == 2) {
           if (full_tile) {
             if constexpr (UPL == 4) {
@@ -303,8 +309,7 @@ __global__ void __launch_bounds__(kQThreads) k_query_fast(const __grid_constant_
     }
   }
   if constexpr (GEMV) {
-    if (!waited) pdl_wait();
-    pdl_trigger();
+    if (!A.early_trigger) pdl_trigger();
   }
 }
 
@@ -387,74 +392,9 @@ __global__ void k_importance(const void* A, int32_t bf16, int64_t N, int64_t d, 
 // ------------------------------------------------------------------ host side
 bool fast_eligible(const usk_plan* pl) { return pl->gran == USK_GRAN_ROW && pl->g == 1; }
 
-struct Geom {
-  int upl = 0;
-  int maxMN = 0;
-  size_t smem = 0;
-  int items = 0;
-  int grid = 0;
-  std::vector<int> n_chunks, n_rb;
-};
-
-size_t smem_bytes(bool gemv, int upl, int maxMN) {
-  return (gemv ? (size_t)kScratchWords * 4 : 0) + (size_t)kRB * 4 + 128 + (size_t)32 * upl * maxMN * 4;
-}
-
 constexpr size_t kSmemMax = 220 * 1024;
-constexpr size_t kSmemPerSM = 228 * 1024;
 
-// Pick units-per-lane and the persistent grid for a launch covering `layers` (rows each).
-// Larger UPL amortises the per-row work (R(o) load, transpose) over more weights; it must still
-// leave >= 148 items so every SM gets work.
-Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n, bool gemv) {
-  Geom G;
-  for (int k = 0; k < n; ++k) G.maxMN = std::max(G.maxMN, pl->M * pl->layers[layers[k]].max_ncols);
-  const int64_t in = pl->layers[layers[0]].in;
-  auto items_for = [&](int upl) {
-    int it = 0;
-    for (int k = 0; k < n; ++k)
-      it += (int)((in + 32 * upl - 1) / (32 * upl)) * (int)((rows[k] + kRB - 1) / kRB);
-    return it;
-  };
-  int best = 0;
-  for (int upl : {4, 2, 1}) {
-    if (smem_bytes(gemv, upl, G.maxMN) > kSmemMax) continue;
-    best = upl;
-    if (items_for(upl) >= 148) break;
-  }
-  if (!best) return G;
-  G.upl = best;
-  G.smem = smem_bytes(gemv, best, G.maxMN);
-  for (int k = 0; k < n; ++k) {
-    G.n_chunks.push_back((int)((in + 32 * best - 1) / (32 * best)));
-    G.n_rb.push_back((int)((rows[k] + kRB - 1) / kRB));
-    G.items += G.n_chunks.back() * G.n_rb.back();
-  }
-  const int per_sm = std::max<int>(1, std::min<int>(4, (int)(kSmemPerSM / (G.smem + 1024))));
-  const int resident = 148 * std::min(per_sm, 2048 / kQThreads);
-  G.grid = std::min(G.items, resident);
-  return G;
-}
-
-size_t layer_ws_bytes(int n_chunks, int n_rb, int64_t rows) {
-  const size_t p = ((size_t)n_chunks * rows * 4 + 255) / 256 * 256;
-  return p + ((size_t)n_rb * 4 + 255) / 256 * 256;
-}
-
-QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& G) {
-  QArgs A{};
-  A.M = pl->M;
-  A.maxMN = G.maxMN;
-  A.total_items = G.items;
-  A.in = in;
-  A.sketch = sketch;
-  A.ncols = pl->d_ncols;
-  A.offsets = pl->d_offsets;
-  A.ukeys = pl->d_keys;
-  A.R = pl->d_R;
-  A.hc = pl->hc;
-  return A;
-}
+size_t smem_bytes(int upl, int maxMN) { return 128 + (size_t)32 * upl * maxMN * 4; }
 
 template <typename E, int UPL, bool GEMV>
 void* pick_m(int M, int hash) {
@@ -481,21 +421,119 @@ void* pick_fast(int upl, bool gemv, bool bf16, int M, int hash) {
   }
 }
 
-usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl, cudaStream_t st) {
-  // max dynamic smem is raised once per kernel (callers warm up before any graph capture)
+int sm_count() {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                 cudaSuccess)
+      sms = 148;
+  }
+  return sms;
+}
+
+int occupancy(void* kern, size_t smem) {
+  // cached per (kernel, smem); the max-dynamic-smem attribute is raised on first use (callers
+  // warm up before any graph capture)
+  static std::mutex mu;
+  static std::vector<std::pair<std::pair<void*, size_t>, int>> cache;
   static std::vector<void*> raised;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto& e : cache)
+    if (e.first.first == kern && e.first.second == smem) return e.second;
   if (std::find(raised.begin(), raised.end(), kern) == raised.end()) {
-    USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return 1;
+    }
     raised.push_back(kern);
   }
   int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQThreads, smem) != cudaSuccess || occ < 1) occ = 1;
-  int sms = 148;
-  {
-    int dev = 0;
-    if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQThreads, smem) != cudaSuccess || occ < 1) {
+    (void)cudaGetLastError();
+    occ = 1;
   }
-  grid = std::min(grid, sms * occ);  // persistent: every CTA resident
+  cache.push_back({{kern, smem}, occ});
+  return occ;
+}
+
+struct Geom {
+  int upl = 0;
+  int maxMN = 0;
+  size_t smem = 0;
+  int grid = 0;
+  bool one_wave = false;
+  void* kern = nullptr;
+  std::vector<int> n_chunks, n_sub, cpc;
+};
+
+// Units per lane: the largest UPL whose chunks all get a resident CTA (larger UPL amortises the
+// per-row R broadcast and the 32-row transpose over more weights).  USK_UPL overrides (tuning).
+Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n, bool gemv) {
+  Geom G;
+  for (int k = 0; k < n; ++k) G.maxMN = std::max(G.maxMN, pl->M * pl->layers[layers[k]].max_ncols);
+  const int64_t in = pl->layers[layers[0]].in;
+  const bool bf16 = pl->dtype == USK_BF16;
+  static const int forced = [] {
+    const char* e = std::getenv("USK_UPL");
+    return e ? std::atoi(e) : 0;
+  }();
+  int best = 0, best_cap = 0;
+  for (int upl : {4, 2, 1}) {
+    if (forced && upl != forced) continue;
+    const size_t sm = smem_bytes(upl, G.maxMN);
+    if (sm > kSmemMax) continue;
+    void* kern = pick_fast(upl, gemv, bf16, pl->M, pl->hash);
+    const int cap = sm_count() * occupancy(kern, sm);
+    int chunks = 0;
+    for (int k = 0; k < n; ++k) chunks += (int)((in + 32 * upl - 1) / (32 * upl));
+    best = upl;
+    best_cap = cap;
+    G.kern = kern;
+    if (chunks <= cap) break;
+  }
+  if (!best) return G;
+  G.upl = best;
+  G.smem = smem_bytes(best, G.maxMN);
+  int chunks = 0;
+  for (int k = 0; k < n; ++k) {
+    G.n_chunks.push_back((int)((in + 32 * best - 1) / (32 * best)));
+    G.n_sub.push_back((int)((rows[k] + 31) / 32));
+    chunks += G.n_chunks.back();
+  }
+  // CTAs per chunk: fill one resident wave; rows spread evenly (cpc <= subtiles)
+  const int cpc_all = std::max(1, best_cap / std::max(1, chunks));
+  for (int k = 0; k < n; ++k) {
+    G.cpc.push_back(std::max(1, std::min(cpc_all, G.n_sub[k])));
+    G.grid += G.n_chunks[k] * G.cpc[k];
+  }
+  G.one_wave = G.grid <= best_cap;
+  return G;
+}
+
+int partial_stride(int64_t in) { return (int)((((in + 31) / 32) + 3) / 4 * 4); }
+
+size_t layer_ws_bytes(int64_t in, int64_t rows) {
+  const size_t p = ((size_t)rows * partial_stride(in) * 4 + 255) / 256 * 256;
+  return p + ((size_t)((rows + 31) / 32) * 4 + 255) / 256 * 256;
+}
+
+QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& G) {
+  QArgs A{};
+  A.M = pl->M;
+  A.maxMN = G.maxMN;
+  A.in = in;
+  A.sketch = sketch;
+  A.ncols = pl->d_ncols;
+  A.offsets = pl->d_offsets;
+  A.ukeys = pl->d_keys;
+  A.R = pl->d_R;
+  A.hc = pl->hc;
+  A.early_trigger = G.one_wave ? 1 : 0;
+  return A;
+}
+
+usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
   cfg.blockDim = dim3(kQThreads);
@@ -536,12 +574,8 @@ GenQ make_genq(const usk_plan* pl, int32_t l, const void* sketch) {
 size_t gemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* o0, const int64_t* o1,
                                   int n) {
   if (!fast_eligible(pl)) return 256;
-  std::vector<int64_t> rows(n);
-  for (int k = 0; k < n; ++k) rows[k] = o1[k] - o0[k];
-  Geom G = geometry(pl, layers, rows.data(), n, true);
-  if (!G.upl) return 256;
   size_t b = 0;
-  for (int k = 0; k < n; ++k) b += layer_ws_bytes(G.n_chunks[k], G.n_rb[k], rows[k]);
+  for (int k = 0; k < n; ++k) b += layer_ws_bytes(pl->layers[layers[k]].in, o1[k] - o0[k]);
   return std::max<size_t>(b, 256);
 }
 
@@ -562,31 +596,28 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
     A.x_bf16 = x_dtype == USK_BF16;
     A.y_bf16 = y_dtype == USK_BF16;
     char* w = reinterpret_cast<char*>(ws);
-    int item = 0;
+    int cta = 0;
     for (int k = 0; k < n; ++k) {
-      const size_t wsb = layer_ws_bytes(G.n_chunks[k], G.n_rb[k], rows[k]);
-      if (rows[k] == 0) {
-        w += wsb;
-        continue;
+      const size_t wsb = layer_ws_bytes(in, rows[k]);
+      if (rows[k] > 0) {
+        QLayer& Ly = A.layer[A.n_layers++];
+        Ly.unit_base = pl->layers[layers[k]].unit_begin;
+        Ly.o_begin = o0[k];
+        Ly.rows = rows[k];
+        Ly.n_chunks = G.n_chunks[k];
+        Ly.n_sub = G.n_sub[k];
+        Ly.cpc = G.cpc[k];
+        Ly.cta_begin = cta;
+        Ly.CP = partial_stride(in);
+        cta += Ly.n_chunks * Ly.cpc;
+        Ly.y = y[k];
+        Ly.partial = reinterpret_cast<float*>(w);
+        Ly.counters = reinterpret_cast<uint32_t*>(w + ((size_t)rows[k] * Ly.CP * 4 + 255) / 256 * 256);
       }
-      QLayer& Ly = A.layer[A.n_layers++];
-      Ly.unit_base = pl->layers[layers[k]].unit_begin;
-      Ly.o_begin = o0[k];
-      Ly.rows = rows[k];
-      Ly.n_chunks = G.n_chunks[k];
-      Ly.n_rb = G.n_rb[k];
-      Ly.item_begin = item;
-      item += Ly.n_chunks * Ly.n_rb;
-      Ly.y = y[k];
-      Ly.partial = reinterpret_cast<float*>(w);
-      const size_t p = ((size_t)Ly.n_chunks * rows[k] * 4 + 255) / 256 * 256;
-      Ly.counters = reinterpret_cast<uint32_t*>(w + p);
       w += wsb;
     }
     if (!A.n_layers) return USK_OK;
-    A.total_items = item;
-    void* k = pick_fast(G.upl, true, pl->dtype == USK_BF16, pl->M, pl->hash);
-    return launch_q(k, A, std::min(G.grid, item), G.smem, true, st);
+    return launch_q(G.kern, A, cta, G.smem, true, st);
   }
   for (int k = 0; k < n; ++k) {
     if (rows[k] == 0) continue;
@@ -620,12 +651,12 @@ usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l,
     Ly.o_begin = r0;
     Ly.rows = rows;
     Ly.n_chunks = G.n_chunks[0];
-    Ly.n_rb = G.n_rb[0];
-    Ly.item_begin = 0;
+    Ly.n_sub = G.n_sub[0];
+    Ly.cpc = G.cpc[0];
+    Ly.cta_begin = 0;
     Ly.w_out = w_out;
     Ly.ld_out = ld;
-    void* k = pick_fast(G.upl, false, pl->dtype == USK_BF16, pl->M, pl->hash);
-    return launch_q(k, A, G.grid, G.smem, false, st);
+    return launch_q(G.kern, A, G.grid, G.smem, false, st);
   }
   GenQ Q = make_genq(pl, l, sketch);
   const int64_t n = rows * L.in;
