@@ -178,8 +178,18 @@ __device__ __forceinline__ float transpose_reduce32(float (&acc)[32], int lane) 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+#ifndef USK_QUERY_MINB
+#define USK_QUERY_MINB 1
+#endif
+
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
 template <typename E, int UPL, int MT, int HASH, bool GEMV>
-__global__ void __launch_bounds__(kQThreads) k_query_fast(const __grid_constant__ QArgs A) {
+__global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const __grid_constant__ QArgs A) {
   constexpr int TJ = 32 * UPL;
   extern __shared__ __align__(16) uint32_t qsm[];
   uint32_t* zero = qsm;
@@ -189,10 +199,15 @@ __global__ void __launch_bounds__(kQThreads) k_query_fast(const __grid_constant_
   int li = 0;
   while (li + 1 < A.n_layers && A.layer[li + 1].cta_begin <= (int)blockIdx.x) ++li;
   const QLayer& Ly = A.layer[li];
+  // this layer's cpc CTAs are spread over its chunks as evenly as possible:
+  // CTA b belongs to chunk floor(b * n_chunks / cpc); each chunk's CTAs split its subtiles evenly
   const int b = blockIdx.x - Ly.cta_begin;
-  const int chunk = b / Ly.cpc, part = b % Ly.cpc;
-  const int sub0 = (int)(((int64_t)part * Ly.n_sub) / Ly.cpc);
-  const int sub1 = (int)(((int64_t)(part + 1) * Ly.n_sub) / Ly.cpc);
+  const int chunk = (int)(((int64_t)b * Ly.n_chunks) / Ly.cpc);
+  const int first = (int)(((int64_t)chunk * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks);
+  const int nparts = (int)((((int64_t)(chunk + 1) * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks) - first);
+  const int part = b - first;
+  const int sub0 = (int)(((int64_t)part * Ly.n_sub) / nparts);
+  const int sub1 = (int)(((int64_t)(part + 1) * Ly.n_sub) / nparts);
   const int64_t j0 = (int64_t)chunk * TJ;
   const int nu = (int)min((int64_t)TJ, A.in - j0);
 
@@ -236,13 +251,14 @@ __global__ void __launch_bounds__(kQThreads) k_query_fast(const __grid_constant_
       }
       const float s = transpose_reduce32(acc, lane);
       if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = s;
-      __threadfence();
+      // publish the warp's partials (bar.warp.sync orders the lanes' stores before lane 0's
+      // acq_rel atomic, which is cumulative) and learn whether this warp completes the subtile
       __syncwarp();
       uint32_t prev = 0;
-      if (lane == 0) prev = atomicAdd(&Ly.counters[sub], 1u);
+      if (lane == 0) prev = atom_add_acq_rel(&Ly.counters[sub], 1u);
       prev = __shfl_sync(0xffffffffu, prev, 0);
       if (prev == (uint32_t)Ly.n_chunks - 1) {  // this warp completes the subtile: reduce in order
-        __threadfence();
+        __syncwarp();  // orders the other lanes' loads after lane 0's acquire
         if (lane < nrow) {
           const float4* p = reinterpret_cast<const float4*>(Ly.partial + (r0 + lane) * Ly.CP);
           float t = 0.f;
@@ -501,11 +517,14 @@ Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, in
     G.n_sub.push_back((int)((rows[k] + 31) / 32));
     chunks += G.n_chunks.back();
   }
-  // CTAs per chunk: fill one resident wave; rows spread evenly (cpc <= subtiles)
-  const int cpc_all = std::max(1, best_cap / std::max(1, chunks));
+  // CTAs per layer ("cpc" = the layer's CTA count): one resident wave shared in proportion to
+  // the layers' weights, at least one CTA per chunk and at most one per (chunk, subtile)
+  double wsum = 0;
+  for (int k = 0; k < n; ++k) wsum += (double)rows[k] * in;
   for (int k = 0; k < n; ++k) {
-    G.cpc.push_back(std::max(1, std::min(cpc_all, G.n_sub[k])));
-    G.grid += G.n_chunks[k] * G.cpc[k];
+    const int share = (int)((double)best_cap * (double)rows[k] * in / std::max(wsum, 1.0));
+    G.cpc.push_back(std::max(G.n_chunks[k], std::min(share, G.n_chunks[k] * G.n_sub[k])));
+    G.grid += G.cpc[k];
   }
   G.one_wave = G.grid <= best_cap;
   return G;
@@ -609,7 +628,7 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
         Ly.cpc = G.cpc[k];
         Ly.cta_begin = cta;
         Ly.CP = partial_stride(in);
-        cta += Ly.n_chunks * Ly.cpc;
+        cta += Ly.cpc;
         Ly.y = y[k];
         Ly.partial = reinterpret_cast<float*>(w);
         Ly.counters = reinterpret_cast<uint32_t*>(w + ((size_t)rows[k] * Ly.CP * 4 + 255) / 256 * 256);
