@@ -38,6 +38,7 @@ namespace {
 constexpr int kQThreads = 512;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxBatch = 8;
+constexpr int kCellsWordOffset = 32 + 160;  // zero cells + chunk unit offsets (<= 129)
 
 __device__ __forceinline__ uint32_t lds32(uint32_t addr) {
   uint32_t v;
@@ -95,25 +96,59 @@ template <typename E, int UPL, int MT>
 __device__ __forceinline__ void stage_chunk(const QArgs& A, const QLayer& Ly, int64_t j0, int nu, uint32_t* cells,
                                             uint32_t* zero, LaneState<UPL, MT>& S) {
   constexpr int TJ = 32 * UPL;
+  constexpr int VE = 16 / sizeof(E);  // cells per 16-B vector
   const int lane = threadIdx.x & 31;
   const E* sk = reinterpret_cast<const E*>(A.sketch);
+  // The chunk's units are consecutive in the sketch, so their cells form one contiguous range
+  // [c0, c1): read it with coalesced 16-B loads (all issued up front) and scatter each cell to
+  // its bank-private slot.  uoff[ul] = first cell of chunk unit ul, relative to c0.
+  int* uoff = reinterpret_cast<int*>(zero + 32);
+  const int64_t ubase = Ly.unit_base + j0;
+  const int64_t c0 = A.offsets[ubase];
+  for (int ul = threadIdx.x; ul <= nu; ul += kQThreads) uoff[ul] = (int)(A.offsets[ubase + ul] - c0);
+  if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
+  __syncthreads();
   {
-    const int ul = threadIdx.x % TJ;
-    if (ul < nu) {
-      const int64_t u = Ly.unit_base + j0 + ul;
-      const int64_t off = A.offsets[u];
-      const int mn = A.M * A.ncols[u];
-      const int L = ul / UPL, v = ul % UPL;
-      uint32_t* dst = cells + v * 32 * A.maxMN + L;
-#pragma unroll 8
-      for (int k = threadIdx.x / TJ; k < mn; k += kQThreads / TJ) {
-        uint32_t b = (uint32_t)sk[off + k];
-        if (sizeof(E) == 2) b <<= 16;
-        dst[k * 32] = rotl1(b) ^ 1u;
+    const int total = uoff[nu];
+    const int64_t v0 = c0 / VE;                  // first vector
+    const int nvec = (int)((c0 + total + VE - 1) / VE - v0);
+    const uint4* src = reinterpret_cast<const uint4*>(sk) + v0;
+    const int shift = (int)(c0 - v0 * VE);      // cells of the first vector before c0
+    constexpr int kMaxV = 8;
+    for (int q0 = threadIdx.x; q0 < nvec; q0 += kQThreads * kMaxV) {
+      uint4 buf[kMaxV];
+#pragma unroll
+      for (int t = 0; t < kMaxV; ++t) {
+        const int q = q0 + t * kQThreads;
+        if (q < nvec) buf[t] = __ldg(src + q);
+      }
+#pragma unroll
+      for (int t = 0; t < kMaxV; ++t) {
+        const int q = q0 + t * kQThreads;
+        if (q >= nvec) break;
+        const uint32_t w[4] = {buf[t].x, buf[t].y, buf[t].z, buf[t].w};
+        int e = q * VE - shift;  // chunk-relative cell index of the vector's first element
+        // unit containing max(e, 0): binary search over uoff (TJ <= 128 entries)
+        int lo = 0, hi = nu;
+        const int e0 = max(e, 0);
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (uoff[mid] <= e0) lo = mid; else hi = mid;
+        }
+        int ul = lo;
+#pragma unroll
+        for (int s = 0; s < VE; ++s, ++e) {
+          if (e < 0 || e >= total) continue;
+          while (e >= uoff[ul + 1]) ++ul;
+          uint32_t b;
+          if constexpr (sizeof(E) == 2) b = (s & 1) ? (w[s >> 1] & 0xFFFF0000u) : (w[s >> 1] << 16);
+          else b = w[s];
+          const int k = e - uoff[ul];
+          cells[(ul % UPL) * 32 * A.maxMN + k * 32 + ul / UPL] = rotl1(b) ^ 1u;
+        }
       }
     }
   }
-  if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
   const uint32_t cbase = smem_u32(cells), zbase = smem_u32(zero);
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
@@ -193,7 +228,7 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
   constexpr int TJ = 32 * UPL;
   extern __shared__ __align__(16) uint32_t qsm[];
   uint32_t* zero = qsm;
-  uint32_t* cells = qsm + 32;
+  uint32_t* cells = qsm + kCellsWordOffset;  // [zero: 32 words][unit offsets: 160][cells]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 
   int li = 0;
@@ -410,7 +445,7 @@ bool fast_eligible(const usk_plan* pl) { return pl->gran == USK_GRAN_ROW && pl->
 
 constexpr size_t kSmemMax = 220 * 1024;
 
-size_t smem_bytes(int upl, int maxMN) { return 128 + (size_t)32 * upl * maxMN * 4; }
+size_t smem_bytes(int upl, int maxMN) { return kCellsWordOffset * 4 + (size_t)32 * upl * maxMN * 4; }
 
 template <typename E, int UPL, bool GEMV>
 void* pick_m(int M, int hash) {
