@@ -99,56 +99,35 @@ __device__ __forceinline__ void stage_chunk(const QArgs& A, const QLayer& Ly, in
   constexpr int VE = 16 / sizeof(E);  // cells per 16-B vector
   const int lane = threadIdx.x & 31;
   const E* sk = reinterpret_cast<const E*>(A.sketch);
-  // The chunk's units are consecutive in the sketch, so their cells form one contiguous range
-  // [c0, c1): read it with coalesced 16-B loads (all issued up front) and scatter each cell to
-  // its bank-private slot.  uoff[ul] = first cell of chunk unit ul, relative to c0.
-  int* uoff = reinterpret_cast<int*>(zero + 32);
-  const int64_t ubase = Ly.unit_base + j0;
-  const int64_t c0 = A.offsets[ubase];
-  for (int ul = threadIdx.x; ul <= nu; ul += kQThreads) uoff[ul] = (int)(A.offsets[ubase + ul] - c0);
-  if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
-  __syncthreads();
+  // thread t stages cells k = t/TJ + m*(threads/TJ) of chunk unit t % TJ; loads are issued in
+  // batches of 16 before their converts/stores so ~16 round trips overlap per thread
+  (void)VE;
   {
-    const int total = uoff[nu];
-    const int64_t v0 = c0 / VE;                  // first vector
-    const int nvec = (int)((c0 + total + VE - 1) / VE - v0);
-    const uint4* src = reinterpret_cast<const uint4*>(sk) + v0;
-    const int shift = (int)(c0 - v0 * VE);      // cells of the first vector before c0
-    constexpr int kMaxV = 8;
-    for (int q0 = threadIdx.x; q0 < nvec; q0 += kQThreads * kMaxV) {
-      uint4 buf[kMaxV];
+    const int ul = threadIdx.x % TJ;
+    if (ul < nu) {
+      const int64_t u = Ly.unit_base + j0 + ul;
+      const int64_t off = A.offsets[u];
+      const int mn = A.M * A.ncols[u];
+      const int L = ul / UPL, v = ul % UPL;
+      uint32_t* dst = cells + v * 32 * A.maxMN + L;
+      constexpr int KS = kQThreads / TJ;
+      constexpr int B = 16;
+      for (int k0 = threadIdx.x / TJ; k0 < mn; k0 += KS * B) {
+        uint32_t buf[B];
 #pragma unroll
-      for (int t = 0; t < kMaxV; ++t) {
-        const int q = q0 + t * kQThreads;
-        if (q < nvec) buf[t] = __ldg(src + q);
-      }
-#pragma unroll
-      for (int t = 0; t < kMaxV; ++t) {
-        const int q = q0 + t * kQThreads;
-        if (q >= nvec) break;
-        const uint32_t w[4] = {buf[t].x, buf[t].y, buf[t].z, buf[t].w};
-        int e = q * VE - shift;  // chunk-relative cell index of the vector's first element
-        // unit containing max(e, 0): binary search over uoff (TJ <= 128 entries)
-        int lo = 0, hi = nu;
-        const int e0 = max(e, 0);
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (uoff[mid] <= e0) lo = mid; else hi = mid;
+        for (int t = 0; t < B; ++t) {
+          const int k = k0 + t * KS;
+          buf[t] = (k < mn) ? (uint32_t)__ldg(sk + off + k) : 0u;
         }
-        int ul = lo;
 #pragma unroll
-        for (int s = 0; s < VE; ++s, ++e) {
-          if (e < 0 || e >= total) continue;
-          while (e >= uoff[ul + 1]) ++ul;
-          uint32_t b;
-          if constexpr (sizeof(E) == 2) b = (s & 1) ? (w[s >> 1] & 0xFFFF0000u) : (w[s >> 1] << 16);
-          else b = w[s];
-          const int k = e - uoff[ul];
-          cells[(ul % UPL) * 32 * A.maxMN + k * 32 + ul / UPL] = rotl1(b) ^ 1u;
+        for (int t = 0; t < B; ++t) {
+          const int k = k0 + t * KS;
+          if (k < mn) dst[k * 32] = rotl1(sizeof(E) == 2 ? (buf[t] << 16) : buf[t]) ^ 1u;
         }
       }
     }
   }
+  if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
   const uint32_t cbase = smem_u32(cells), zbase = smem_u32(zero);
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
@@ -210,18 +189,56 @@ __device__ __forceinline__ float transpose_reduce32(float (&acc)[32], int lane) 
   return acc[0];
 }
 
+__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
+  uint32_t old;
+  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+
+// Publish a warp's partials of subtile `sub` (bar.warp.sync orders the lanes' stores before lane
+// 0's acq_rel atomic, which is cumulative).  The warp that brings the subtile's count to n_chunks
+// sums the chunks in fixed order (float4 loads of the row-major partials) and writes y.
+__device__ __noinline__ void publish_subtile(const QArgs& A, const QLayer& Ly, int sub, int lane) {
+  __syncwarp();
+  uint32_t prev = 0;
+  if (lane == 0) prev = atom_add_acq_rel(&Ly.counters[sub], 1u);
+  prev = __shfl_sync(0xffffffffu, prev, 0);
+  if (prev != (uint32_t)Ly.n_chunks - 1) return;
+  __syncwarp();  // orders the other lanes' loads after lane 0's acquire
+  const int64_t r0 = (int64_t)sub * 32;
+  const int nrow = (int)min((int64_t)32, Ly.rows - r0);
+  if (lane < nrow) {
+    const float4* p = reinterpret_cast<const float4*>(Ly.partial + (r0 + lane) * Ly.CP);
+    float t = 0.f;
+    int c = 0;
+    for (; c + 32 <= Ly.n_chunks; c += 32) {
+      float4 q[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) q[k] = __ldcg(p + c / 4 + k);
+#pragma unroll
+      for (int k = 0; k < 8; ++k) t = t + q[k].x + q[k].y + q[k].z + q[k].w;
+    }
+    for (; c < Ly.n_chunks; c += 4) {
+      const float4 q = __ldcg(p + c / 4);
+      const float w4[4] = {q.x, q.y, q.z, q.w};
+      for (int k = 0; k < 4 && c + k < Ly.n_chunks; ++k) t += w4[k];
+    }
+    if (A.y_bf16) {
+      const uint32_t bb = __float_as_uint(t);
+      reinterpret_cast<uint16_t*>(Ly.y)[r0 + lane] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
+    } else {
+      reinterpret_cast<float*>(Ly.y)[r0 + lane] = t;
+    }
+  }
+  if (lane == 0) Ly.counters[sub] = 0u;  // leave the workspace zeroed for the next call
+}
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 #ifndef USK_QUERY_MINB
 #define USK_QUERY_MINB 1
 #endif
-
-__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
 
 template <typename E, int UPL, int MT, int HASH, bool GEMV>
 __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const __grid_constant__ QArgs A) {
@@ -265,6 +282,7 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
   __syncthreads();
 
   const uint32_t* Rg = A.R + Ly.o_begin;
+  int pending = -1;  // GEMV: subtile whose partials are written but not yet published
   int sub = sub0 + warp;
   uint32_t Rnext = 0;
   if (sub < sub1) Rnext = Rg[min((int64_t)sub * 32 + lane, Ly.rows - 1)];
@@ -286,39 +304,10 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
       }
       const float s = transpose_reduce32(acc, lane);
       if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = s;
-      // publish the warp's partials (bar.warp.sync orders the lanes' stores before lane 0's
-      // acq_rel atomic, which is cumulative) and learn whether this warp completes the subtile
-      __syncwarp();
-      uint32_t prev = 0;
-      if (lane == 0) prev = atom_add_acq_rel(&Ly.counters[sub], 1u);
-      prev = __shfl_sync(0xffffffffu, prev, 0);
-      if (prev == (uint32_t)Ly.n_chunks - 1) {  // this warp completes the subtile: reduce in order
-        __syncwarp();  // orders the other lanes' loads after lane 0's acquire
-        if (lane < nrow) {
-          const float4* p = reinterpret_cast<const float4*>(Ly.partial + (r0 + lane) * Ly.CP);
-          float t = 0.f;
-          int c = 0;
-          for (; c + 32 <= Ly.n_chunks; c += 32) {
-            float4 q[8];
-#pragma unroll
-            for (int k = 0; k < 8; ++k) q[k] = __ldcg(p + c / 4 + k);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) t = t + q[k].x + q[k].y + q[k].z + q[k].w;
-          }
-          for (; c < Ly.n_chunks; c += 4) {
-            const float4 q = __ldcg(p + c / 4);
-            const float w4[4] = {q.x, q.y, q.z, q.w};
-            for (int k = 0; k < 4 && c + k < Ly.n_chunks; ++k) t += w4[k];
-          }
-          if (A.y_bf16) {
-            const uint32_t bb = __float_as_uint(t);
-            reinterpret_cast<uint16_t*>(Ly.y)[r0 + lane] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
-          } else {
-            reinterpret_cast<float*>(Ly.y)[r0 + lane] = t;
-          }
-        }
-        if (lane == 0) Ly.counters[sub] = 0u;  // leave the workspace zeroed for the next call
-      }
+      // publish the PREVIOUS subtile now: its stores have drained during this subtile's math,
+      // so the release is cheap (software-pipelined split-K publication)
+      if (pending >= 0) publish_subtile(A, Ly, pending, lane);
+      pending = sub;
     } else {
       const bool full_tile = (nu == TJ);
       E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + j0 + UPL * lane;
@@ -360,6 +349,7 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
     }
   }
   if constexpr (GEMV) {
+    if (pending >= 0) publish_subtile(A, Ly, pending, lane);
     if (!A.early_trigger) pdl_trigger();
   }
 }
