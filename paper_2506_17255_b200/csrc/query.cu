@@ -40,10 +40,12 @@ constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxBatch = 8;
 constexpr int kCellsWordOffset = 32 + 160;  // zero cells + chunk unit offsets (<= 129)
 
-__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
+extern __shared__ __align__(16) uint32_t qsm[];  // dynamic shared memory of the query kernels
+
+// 32-bit shared load at a byte offset from qsm: compiles to LDS [R + UR] (base folded), and as
+// an ordinary load it can be scheduled freely around the address arithmetic.
+__device__ __forceinline__ uint32_t lds32(uint32_t off) {
+  return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(qsm) + off);
 }
 
 struct QLayer {
@@ -128,7 +130,7 @@ __device__ __forceinline__ void stage_chunk(const QArgs& A, const QLayer& Ly, in
     }
   }
   if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
-  const uint32_t cbase = smem_u32(cells), zbase = smem_u32(zero);
+  const uint32_t cbase = (uint32_t)((cells - qsm) * 4), zbase = (uint32_t)((zero - qsm) * 4);  // byte offsets
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
     const int ul = UPL * lane + v;
@@ -243,7 +245,6 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 template <typename E, int UPL, int MT, int HASH, bool GEMV>
 __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const __grid_constant__ QArgs A) {
   constexpr int TJ = 32 * UPL;
-  extern __shared__ __align__(16) uint32_t qsm[];
   uint32_t* zero = qsm;
   uint32_t* cells = qsm + kCellsWordOffset;  // [zero: 32 words][unit offsets: 160][cells]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
