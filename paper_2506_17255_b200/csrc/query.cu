@@ -27,10 +27,12 @@
 //     griddepcontrol.wait, overlapping the previous kernel; x is read after it.
 //     usk_linear_batch puts several linears that share x (q|k|v, gate|up) in one launch.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
+#include "ptx.cuh"
 
 namespace usk {
 namespace {
@@ -38,6 +40,7 @@ namespace {
 constexpr int kQThreads = 512;
 constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxBatch = 8;
+constexpr int kSubRows = 16;  // rows per warp work item (subtile)
 constexpr int kCellsWordOffset = 32 + 160;  // zero cells + chunk unit offsets (<= 129)
 
 extern __shared__ __align__(16) uint32_t qsm[];  // dynamic shared memory of the query kernels
@@ -83,7 +86,14 @@ struct QArgs {
   const void* x;
   int32_t x_bf16;
   int32_t y_bf16;
+  unsigned long long* timeline;  // debug only (USK_TIMELINE=1): 4 globaltimer stamps per CTA
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int UPL, int MT>
 struct LaneState {
@@ -98,38 +108,45 @@ template <typename E, int UPL, int MT>
 __device__ __forceinline__ void stage_chunk(const QArgs& A, const QLayer& Ly, int64_t j0, int nu, uint32_t* cells,
                                             uint32_t* zero, LaneState<UPL, MT>& S) {
   constexpr int TJ = 32 * UPL;
-  constexpr int VE = 16 / sizeof(E);  // cells per 16-B vector
+  constexpr int ES = sizeof(E);
   const int lane = threadIdx.x & 31;
-  const E* sk = reinterpret_cast<const E*>(A.sketch);
-  // thread t stages cells k = t/TJ + m*(threads/TJ) of chunk unit t % TJ; loads are issued in
-  // batches of 16 before their converts/stores so ~16 round trips overlap per thread
-  (void)VE;
-  {
-    const int ul = threadIdx.x % TJ;
-    if (ul < nu) {
-      const int64_t u = Ly.unit_base + j0 + ul;
-      const int64_t off = A.offsets[u];
-      const int mn = A.M * A.ncols[u];
-      const int L = ul / UPL, v = ul % UPL;
-      uint32_t* dst = cells + v * 32 * A.maxMN + L;
-      constexpr int KS = kQThreads / TJ;
-      constexpr int B = 16;
-      for (int k0 = threadIdx.x / TJ; k0 < mn; k0 += KS * B) {
-        uint32_t buf[B];
-#pragma unroll
-        for (int t = 0; t < B; ++t) {
-          const int k = k0 + t * KS;
-          buf[t] = (k < mn) ? (uint32_t)__ldg(sk + off + k) : 0u;
-        }
-#pragma unroll
-        for (int t = 0; t < B; ++t) {
-          const int k = k0 + t * KS;
-          if (k < mn) dst[k * 32] = rotl1(sizeof(E) == 2 ? (buf[t] << 16) : buf[t]) ^ 1u;
-        }
-      }
-    }
+  // The chunk's units are consecutive in the sketch, so their cells are one contiguous byte range:
+  // a single TMA bulk copy (cp.async.bulk, mbarrier completion) brings it into a raw shared
+  // buffer; threads then convert shared -> shared into the bank-private rho layout.
+  uint64_t* bar = reinterpret_cast<uint64_t*>(zero + 32);
+  uint32_t* s_shift = zero + 34;
+  unsigned char* raw = reinterpret_cast<unsigned char*>(cells + UPL * 32 * A.maxMN);
+  const int64_t ubase = Ly.unit_base + j0;
+  if (threadIdx.x == 0) {
+    const uint64_t g0 = (uint64_t)A.offsets[ubase] * ES, g1 = (uint64_t)A.offsets[ubase + nu] * ES;
+    const uint64_t a0 = g0 & ~uint64_t(15), a1 = (g1 + 15) & ~uint64_t(15);
+    mbar_init(bar, 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(bar, (uint32_t)(a1 - a0));
+    bulk_g2s(raw, reinterpret_cast<const unsigned char*>(A.sketch) + a0, (uint32_t)(a1 - a0), bar);
+    *s_shift = (uint32_t)(g0 - a0);
+  }
+  const int ul = threadIdx.x % TJ;
+  int64_t u_off = 0;
+  int mn = 0;
+  if (ul < nu) {  // overlaps the copy
+    u_off = A.offsets[ubase + ul] - A.offsets[ubase];
+    mn = A.M * A.ncols[ubase + ul];
   }
   if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
+  __syncthreads();                                 // barrier init + shift visible
+  mbar_wait(bar, 0);
+  {
+    const unsigned char* src = raw + *s_shift + u_off * ES;
+    uint32_t* dst = cells + (ul % UPL) * 32 * A.maxMN + ul / UPL;
+    constexpr int KS = kQThreads / TJ;
+#pragma unroll 4
+    for (int k = threadIdx.x / TJ; k < mn; k += KS) {
+      const uint32_t b = ES == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
+                                 : reinterpret_cast<const uint32_t*>(src)[k];
+      dst[k * 32] = rotl1(b) ^ 1u;
+    }
+  }
   const uint32_t cbase = (uint32_t)((cells - qsm) * 4), zbase = (uint32_t)((zero - qsm) * 4);  // byte offsets
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
@@ -176,10 +193,11 @@ __device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<U
   }
 }
 
-// Row r of the warp's 32 partial rows ends on lane r (fixed-order butterfly).
-__device__ __forceinline__ float transpose_reduce32(float (&acc)[32], int lane) {
+// Row r of the warp's 16 partial rows ends on lanes r and r + 16 (fixed-order butterfly: 4
+// exchange-and-halve stages inside each half-warp, then the two halves are added).
+__device__ __forceinline__ float transpose_reduce16(float (&acc)[16], int lane) {
 #pragma unroll
-  for (int m = 16; m >= 1; m >>= 1) {
+  for (int m = 8; m >= 1; m >>= 1) {
     const bool up = (lane & m) != 0;
 #pragma unroll
     for (int i = 0; i < m; ++i) {
@@ -188,7 +206,7 @@ __device__ __forceinline__ float transpose_reduce32(float (&acc)[32], int lane) 
       acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
     }
   }
-  return acc[0];
+  return acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 16);
 }
 
 __device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
@@ -207,8 +225,8 @@ __device__ __noinline__ void publish_subtile(const QArgs& A, const QLayer& Ly, i
   prev = __shfl_sync(0xffffffffu, prev, 0);
   if (prev != (uint32_t)Ly.n_chunks - 1) return;
   __syncwarp();  // orders the other lanes' loads after lane 0's acquire
-  const int64_t r0 = (int64_t)sub * 32;
-  const int nrow = (int)min((int64_t)32, Ly.rows - r0);
+  const int64_t r0 = (int64_t)sub * kSubRows;
+  const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
   if (lane < nrow) {
     const float4* p = reinterpret_cast<const float4*>(Ly.partial + (r0 + lane) * Ly.CP);
     float t = 0.f;
@@ -264,6 +282,7 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
   const int64_t j0 = (int64_t)chunk * TJ;
   const int nu = (int)min((int64_t)TJ, A.in - j0);
 
+  if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 0] = gtimer();
   LaneState<UPL, MT> S;
   stage_chunk<E, UPL, MT>(A, Ly, j0, nu, cells, zero, S);
   float nx[UPL];
@@ -281,21 +300,23 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
     }
   }
   __syncthreads();
+  if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 1] = gtimer();
 
   const uint32_t* Rg = A.R + Ly.o_begin;
   int pending = -1;  // GEMV: subtile whose partials are written but not yet published
   int sub = sub0 + warp;
   uint32_t Rnext = 0;
-  if (sub < sub1) Rnext = Rg[min((int64_t)sub * 32 + lane, Ly.rows - 1)];
+  const int rl = lane & (kSubRows - 1);  // lanes r and r + 16 both hold R(o0 + r)
+  if (sub < sub1) Rnext = Rg[min((int64_t)sub * kSubRows + rl, Ly.rows - 1)];
   for (; sub < sub1; sub += kQWarps) {
     const uint32_t Rl = Rnext;
-    if (sub + kQWarps < sub1) Rnext = Rg[min((int64_t)(sub + kQWarps) * 32 + lane, Ly.rows - 1)];
-    const int64_t r0 = (int64_t)sub * 32;  // first local row of the subtile
-    const int nrow = (int)min((int64_t)32, Ly.rows - r0);
+    if (sub + kQWarps < sub1) Rnext = Rg[min((int64_t)(sub + kQWarps) * kSubRows + rl, Ly.rows - 1)];
+    const int64_t r0 = (int64_t)sub * kSubRows;  // first local row of the subtile
+    const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
     if constexpr (GEMV) {
-      float acc[32];
+      float acc[kSubRows];
 #pragma unroll
-      for (int r = 0; r < 32; ++r) {
+      for (int r = 0; r < kSubRows; ++r) {
         const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
         float a = 0.f;
 #pragma unroll
@@ -303,7 +324,7 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
           a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r))), a);
         acc[r] = a;
       }
-      const float s = transpose_reduce32(acc, lane);
+      const float s = transpose_reduce16(acc, lane);
       if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = s;
       // publish the PREVIOUS subtile now: its stores have drained during this subtile's math,
       // so the release is cheap (software-pipelined split-K publication)
@@ -313,7 +334,7 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
       const bool full_tile = (nu == TJ);
       E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + j0 + UPL * lane;
 #pragma unroll 4
-      for (int r = 0; r < 32; ++r, dst += Ly.ld_out) {
+      for (int r = 0; r < kSubRows; ++r, dst += Ly.ld_out) {
         const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
         if (r >= nrow) continue;
         uint32_t wb[UPL];
@@ -349,10 +370,12 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
       }
     }
   }
+  if (A.timeline && lane == 0) atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
   if constexpr (GEMV) {
     if (pending >= 0) publish_subtile(A, Ly, pending, lane);
     if (!A.early_trigger) pdl_trigger();
   }
+  if (A.timeline && lane == 0) atomicMax(&A.timeline[blockIdx.x * 4 + 3], gtimer());
 }
 
 // ------------------------------------------------------------------ generic query path
@@ -436,7 +459,10 @@ bool fast_eligible(const usk_plan* pl) { return pl->gran == USK_GRAN_ROW && pl->
 
 constexpr size_t kSmemMax = 220 * 1024;
 
-size_t smem_bytes(int upl, int maxMN) { return kCellsWordOffset * 4 + (size_t)32 * upl * maxMN * 4; }
+// [zero + mbarrier + unit slots][rho cells][raw chunk bytes of the bulk copy (+ alignment slack)]
+size_t smem_bytes(int upl, int maxMN, int es) {
+  return kCellsWordOffset * 4 + (size_t)32 * upl * maxMN * 4 + (size_t)32 * upl * maxMN * es + 48;
+}
 
 template <typename E, int UPL, bool GEMV>
 void* pick_m(int M, int hash) {
@@ -523,7 +549,7 @@ Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, in
   int best = 0, best_cap = 0;
   for (int upl : {4, 2, 1}) {
     if (forced && upl != forced) continue;
-    const size_t sm = smem_bytes(upl, G.maxMN);
+    const size_t sm = smem_bytes(upl, G.maxMN, pl->cell_bytes());
     if (sm > kSmemMax) continue;
     void* kern = pick_fast(upl, gemv, bf16, pl->M, pl->hash);
     const int cap = sm_count() * occupancy(kern, sm);
@@ -536,11 +562,11 @@ Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, in
   }
   if (!best) return G;
   G.upl = best;
-  G.smem = smem_bytes(best, G.maxMN);
+  G.smem = smem_bytes(best, G.maxMN, pl->cell_bytes());
   int chunks = 0;
   for (int k = 0; k < n; ++k) {
     G.n_chunks.push_back((int)((in + 32 * best - 1) / (32 * best)));
-    G.n_sub.push_back((int)((rows[k] + 31) / 32));
+    G.n_sub.push_back((int)((rows[k] + kSubRows - 1) / kSubRows));
     chunks += G.n_chunks.back();
   }
   // CTAs per layer ("cpc" = the layer's CTA count): one resident wave shared in proportion to
@@ -560,7 +586,7 @@ int partial_stride(int64_t in) { return (int)((((in + 31) / 32) + 3) / 4 * 4); }
 
 size_t layer_ws_bytes(int64_t in, int64_t rows) {
   const size_t p = ((size_t)rows * partial_stride(in) * 4 + 255) / 256 * 256;
-  return p + ((size_t)((rows + 31) / 32) * 4 + 255) / 256 * 256;
+  return p + ((size_t)((rows + kSubRows - 1) / kSubRows) * 4 + 255) / 256 * 256;
 }
 
 QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& G) {
@@ -589,8 +615,38 @@ usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  void* args[] = {const_cast<QArgs*>(&A)};
-  USK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+  static const bool timeline = std::getenv("USK_TIMELINE") != nullptr;  // debug / tuning only
+  if (timeline) {
+    static unsigned long long* dbuf = nullptr;
+    if (!dbuf) USK_CUDA(cudaMalloc(&dbuf, sizeof(unsigned long long) * 4 * 8192));
+    QArgs B = A;
+    B.timeline = dbuf;
+    USK_CUDA(cudaMemsetAsync(dbuf, 0, sizeof(unsigned long long) * 4 * grid, st));
+    void* args[] = {&B};
+    USK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+    std::vector<unsigned long long> h(4 * (size_t)grid);
+    USK_CUDA(cudaMemcpyAsync(h.data(), dbuf, h.size() * 8, cudaMemcpyDeviceToHost, st));
+    USK_CUDA(cudaStreamSynchronize(st));
+    unsigned long long t0 = ~0ull, tend = 0;
+    double stage = 0, comp = 0, tail = 0, last_comp = 0;
+    for (int b = 0; b < grid; ++b) {
+      t0 = std::min(t0, h[4 * b]);
+      tend = std::max(tend, h[4 * b + 3]);
+    }
+    for (int b = 0; b < grid; ++b) {
+      stage += (double)(h[4 * b + 1] - h[4 * b]);
+      comp += (double)(h[4 * b + 2] - h[4 * b + 1]);
+      tail += (double)(h[4 * b + 3] - h[4 * b + 2]);
+      last_comp = std::max(last_comp, (double)(h[4 * b + 2] - t0));
+    }
+    std::fprintf(stderr,
+                 "[usk timeline] grid=%d span=%.2fus mean: start_skew? stage=%.2fus compute=%.2fus tail=%.2fus "
+                 "last_compute_end=%.2fus\n",
+                 grid, (tend - t0) / 1e3, stage / grid / 1e3, comp / grid / 1e3, tail / grid / 1e3, last_comp / 1e3);
+  } else {
+    void* args[] = {const_cast<QArgs*>(&A)};
+    USK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+  }
   count_launch();
   return USK_OK;
 }
