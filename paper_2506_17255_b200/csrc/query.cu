@@ -56,15 +56,16 @@ struct QLayer {
   int64_t o_begin;     // first output row
   int64_t rows;        // rows in [o_begin, o_end)
   int32_t n_chunks;    // unit chunks of TJ
-  int32_t n_sub;       // 32-row subtiles
-  int32_t cpc;         // CTAs per chunk
+  int32_t n_sub;       // 16-row subtiles
+  int32_t cpc;         // GEMV: CTAs per chunk; reconstruct: CTAs of the layer
   int32_t cta_begin;   // first CTA of this layer in the launch
   int32_t CP;          // row stride of the partial workspace (>= n_chunks, multiple of 4)
   int32_t pad;
   // gemv
   void* y;
   float* partial;      // [rows][CP]
-  uint32_t* counters;  // [n_sub]
+  uint32_t* counters;  // [n_sub] split-K completion counts
+  uint32_t* work;      // [2 * n_chunks]: per chunk, next subtile to grab and warps finished
   // reconstruct
   void* w_out;
   int64_t ld_out;
@@ -270,15 +271,21 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
   int li = 0;
   while (li + 1 < A.n_layers && A.layer[li + 1].cta_begin <= (int)blockIdx.x) ++li;
   const QLayer& Ly = A.layer[li];
-  // this layer's cpc CTAs are spread over its chunks as evenly as possible:
-  // CTA b belongs to chunk floor(b * n_chunks / cpc); each chunk's CTAs split its subtiles evenly
   const int b = blockIdx.x - Ly.cta_begin;
-  const int chunk = (int)(((int64_t)b * Ly.n_chunks) / Ly.cpc);
-  const int first = (int)(((int64_t)chunk * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks);
-  const int nparts = (int)((((int64_t)(chunk + 1) * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks) - first);
-  const int part = b - first;
-  const int sub0 = (int)(((int64_t)part * Ly.n_sub) / nparts);
-  const int sub1 = (int)(((int64_t)(part + 1) * Ly.n_sub) / nparts);
+  int chunk, sub0 = 0, sub1 = 0;
+  if constexpr (GEMV) {
+    // cpc CTAs per chunk; their warps grab 16-row subtiles dynamically (balanced to one subtile)
+    chunk = b / Ly.cpc;
+  } else {
+    // the layer's cpc CTAs are spread over its chunks as evenly as possible; each chunk's CTAs
+    // split its subtiles evenly (static)
+    chunk = (int)(((int64_t)b * Ly.n_chunks) / Ly.cpc);
+    const int first = (int)(((int64_t)chunk * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks);
+    const int nparts = (int)((((int64_t)(chunk + 1) * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks) - first);
+    const int part = b - first;
+    sub0 = (int)(((int64_t)part * Ly.n_sub) / nparts);
+    sub1 = (int)(((int64_t)(part + 1) * Ly.n_sub) / nparts);
+  }
   const int64_t j0 = (int64_t)chunk * TJ;
   const int nu = (int)min((int64_t)TJ, A.in - j0);
 
@@ -304,13 +311,23 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
 
   const uint32_t* Rg = A.R + Ly.o_begin;
   int pending = -1;  // GEMV: subtile whose partials are written but not yet published
-  int sub = sub0 + warp;
-  uint32_t Rnext = 0;
   const int rl = lane & (kSubRows - 1);  // lanes r and r + 16 both hold R(o0 + r)
-  if (sub < sub1) Rnext = Rg[min((int64_t)sub * kSubRows + rl, Ly.rows - 1)];
-  for (; sub < sub1; sub += kQWarps) {
-    const uint32_t Rl = Rnext;
-    if (sub + kQWarps < sub1) Rnext = Rg[min((int64_t)(sub + kQWarps) * kSubRows + rl, Ly.rows - 1)];
+  uint32_t* grab = GEMV ? Ly.work + 2 * chunk : nullptr;
+  auto next_sub = [&](int cur) -> int {
+    if constexpr (GEMV) {
+      int g = 0;
+      if (lane == 0) g = (int)atomicAdd(grab, 1u);
+      return __shfl_sync(0xffffffffu, g, 0);
+    } else {
+      return cur + kQWarps;
+    }
+  };
+  const int sub_end = GEMV ? Ly.n_sub : sub1;
+  int sub = GEMV ? next_sub(0) : sub0 + warp;
+  uint32_t Rl = 0;
+  if (sub < sub_end) Rl = Rg[min((int64_t)sub * kSubRows + rl, Ly.rows - 1)];
+  while (sub < sub_end) {
+    const int nxt = next_sub(sub);  // issued now, consumed after this subtile's math
     const int64_t r0 = (int64_t)sub * kSubRows;  // first local row of the subtile
     const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
     if constexpr (GEMV) {
@@ -369,10 +386,17 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
         }
       }
     }
+    sub = nxt;
+    if (sub < sub_end) Rl = Rg[min((int64_t)sub * kSubRows + rl, Ly.rows - 1)];
   }
   if (A.timeline && lane == 0) atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
   if constexpr (GEMV) {
     if (pending >= 0) publish_subtile(A, Ly, pending, lane);
+    // the last warp of this chunk to finish resets the chunk's work counters for the next call
+    if (lane == 0 && atomicAdd(grab + 1, 1u) == (uint32_t)Ly.cpc * kQWarps - 1) {
+      grab[0] = 0u;
+      grab[1] = 0u;
+    }
     if (!A.early_trigger) pdl_trigger();
   }
   if (A.timeline && lane == 0) atomicMax(&A.timeline[blockIdx.x * 4 + 3], gtimer());
@@ -575,8 +599,13 @@ Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, in
   for (int k = 0; k < n; ++k) wsum += (double)rows[k] * in;
   for (int k = 0; k < n; ++k) {
     const int share = (int)((double)best_cap * (double)rows[k] * in / std::max(wsum, 1.0));
-    G.cpc.push_back(std::max(G.n_chunks[k], std::min(share, G.n_chunks[k] * G.n_sub[k])));
-    G.grid += G.cpc[k];
+    if (gemv) {  // cpc = CTAs per chunk (equal for every chunk; warps then balance dynamically)
+      G.cpc.push_back(std::max(1, std::min(share / G.n_chunks[k], G.n_sub[k])));
+      G.grid += G.cpc[k] * G.n_chunks[k];
+    } else {     // cpc = CTAs of the layer, spread over its chunks
+      G.cpc.push_back(std::max(G.n_chunks[k], std::min(share, G.n_chunks[k] * G.n_sub[k])));
+      G.grid += G.cpc[k];
+    }
   }
   G.one_wave = G.grid <= best_cap;
   return G;
@@ -584,9 +613,15 @@ Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, in
 
 int partial_stride(int64_t in) { return (int)((((in + 31) / 32) + 3) / 4 * 4); }
 
+// per layer: [partials rows x CP floats][split-K counters per subtile][work counters 2 x chunks]
+size_t layer_ws_counters_off(int64_t in, int64_t rows) {
+  return ((size_t)rows * partial_stride(in) * 4 + 255) / 256 * 256;
+}
+size_t layer_ws_work_off(int64_t in, int64_t rows) {
+  return layer_ws_counters_off(in, rows) + ((size_t)((rows + kSubRows - 1) / kSubRows) * 4 + 255) / 256 * 256;
+}
 size_t layer_ws_bytes(int64_t in, int64_t rows) {
-  const size_t p = ((size_t)rows * partial_stride(in) * 4 + 255) / 256 * 256;
-  return p + ((size_t)((rows + kSubRows - 1) / kSubRows) * 4 + 255) / 256 * 256;
+  return layer_ws_work_off(in, rows) + ((size_t)2 * ((in + 31) / 32) * 4 + 255) / 256 * 256;
 }
 
 QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& G) {
@@ -710,10 +745,11 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
         Ly.cpc = G.cpc[k];
         Ly.cta_begin = cta;
         Ly.CP = partial_stride(in);
-        cta += Ly.cpc;
+        cta += Ly.cpc * Ly.n_chunks;
         Ly.y = y[k];
         Ly.partial = reinterpret_cast<float*>(w);
-        Ly.counters = reinterpret_cast<uint32_t*>(w + ((size_t)rows[k] * Ly.CP * 4 + 255) / 256 * 256);
+        Ly.counters = reinterpret_cast<uint32_t*>(w + layer_ws_counters_off(in, rows[k]));
+        Ly.work = reinterpret_cast<uint32_t*>(w + layer_ws_work_off(in, rows[k]));
       }
       w += wsb;
     }
