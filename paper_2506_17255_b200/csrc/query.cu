@@ -309,7 +309,6 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
   __syncthreads();
   if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 1] = gtimer();
 
-  const uint32_t* Rg = A.R + Ly.o_begin;
   int pending = -1;  // GEMV: subtile whose partials are written but not yet published
   const int rl = lane & (kSubRows - 1);  // lanes r and r + 16 both hold R(o0 + r)
   uint32_t* grab = GEMV ? Ly.work + 2 * chunk : nullptr;
@@ -325,7 +324,9 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
   const int sub_end = GEMV ? Ly.n_sub : sub1;
   int sub = GEMV ? next_sub(0) : sub0 + warp;
   uint32_t Rl = 0;
-  if (sub < sub_end) Rl = Rg[min((int64_t)sub * kSubRows + rl, Ly.rows - 1)];
+  // R(o) = fmix32(o ^ rho): lane r computes its own row's mix (6 integer ops per subtile and
+  // lane, no memory access); SHFL broadcasts it row by row
+  if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
   while (sub < sub_end) {
     const int nxt = next_sub(sub);  // issued now, consumed after this subtile's math
     const int64_t r0 = (int64_t)sub * kSubRows;  // first local row of the subtile
@@ -387,7 +388,7 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
       }
     }
     sub = nxt;
-    if (sub < sub_end) Rl = Rg[min((int64_t)sub * kSubRows + rl, Ly.rows - 1)];
+    if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
   }
   if (A.timeline && lane == 0) atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
   if constexpr (GEMV) {
