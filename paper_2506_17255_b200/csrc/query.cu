@@ -38,7 +38,6 @@ namespace usk {
 namespace {
 
 constexpr int kQThreads = 512;
-constexpr int kQWarps = kQThreads / 32;
 constexpr int kMaxBatch = 8;
 constexpr int kSubRows = 16;  // rows per warp work item (subtile)
 constexpr int kCellsWordOffset = 32 + 160;  // zero cells + chunk unit offsets (<= 129)
@@ -210,48 +209,29 @@ __device__ __forceinline__ float transpose_reduce16(float (&acc)[16], int lane) 
   return acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 16);
 }
 
-__device__ __forceinline__ uint32_t atom_add_acq_rel(uint32_t* p, uint32_t v) {
-  uint32_t old;
-  asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
-  return old;
-}
-
-// Publish a warp's partials of subtile `sub` (bar.warp.sync orders the lanes' stores before lane
-// 0's acq_rel atomic, which is cumulative).  The warp that brings the subtile's count to n_chunks
-// sums the chunks in fixed order (float4 loads of the row-major partials) and writes y.
-__device__ __noinline__ void publish_subtile(const QArgs& A, const QLayer& Ly, int sub, int lane) {
-  __syncwarp();
-  uint32_t prev = 0;
-  if (lane == 0) prev = atom_add_acq_rel(&Ly.counters[sub], 1u);
-  prev = __shfl_sync(0xffffffffu, prev, 0);
-  if (prev != (uint32_t)Ly.n_chunks - 1) return;
-  __syncwarp();  // orders the other lanes' loads after lane 0's acquire
-  const int64_t r0 = (int64_t)sub * kSubRows;
-  const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
-  if (lane < nrow) {
-    const float4* p = reinterpret_cast<const float4*>(Ly.partial + (r0 + lane) * Ly.CP);
-    float t = 0.f;
-    int c = 0;
-    for (; c + 32 <= Ly.n_chunks; c += 32) {
-      float4 q[8];
+// y[r] = sum over chunks (fixed order) of the row-major partials; float4 loads, all issued up front.
+__device__ __forceinline__ void reduce_row(const QArgs& A, const QLayer& Ly, int64_t r) {
+  const float4* p = reinterpret_cast<const float4*>(Ly.partial + r * Ly.CP);
+  float t = 0.f;
+  int c = 0;
+  for (; c + 32 <= Ly.n_chunks; c += 32) {
+    float4 q[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) q[k] = __ldcg(p + c / 4 + k);
+    for (int k = 0; k < 8; ++k) q[k] = __ldcg(p + c / 4 + k);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) t = t + q[k].x + q[k].y + q[k].z + q[k].w;
-    }
-    for (; c < Ly.n_chunks; c += 4) {
-      const float4 q = __ldcg(p + c / 4);
-      const float w4[4] = {q.x, q.y, q.z, q.w};
-      for (int k = 0; k < 4 && c + k < Ly.n_chunks; ++k) t += w4[k];
-    }
-    if (A.y_bf16) {
-      const uint32_t bb = __float_as_uint(t);
-      reinterpret_cast<uint16_t*>(Ly.y)[r0 + lane] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
-    } else {
-      reinterpret_cast<float*>(Ly.y)[r0 + lane] = t;
-    }
+    for (int k = 0; k < 8; ++k) t = t + q[k].x + q[k].y + q[k].z + q[k].w;
   }
-  if (lane == 0) Ly.counters[sub] = 0u;  // leave the workspace zeroed for the next call
+  for (; c < Ly.n_chunks; c += 4) {
+    const float4 q = __ldcg(p + c / 4);
+    const float w4[4] = {q.x, q.y, q.z, q.w};
+    for (int k = 0; k < 4 && c + k < Ly.n_chunks; ++k) t += w4[k];
+  }
+  if (A.y_bf16) {
+    const uint32_t bb = __float_as_uint(t);
+    reinterpret_cast<uint16_t*>(Ly.y)[r] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
+  } else {
+    reinterpret_cast<float*>(Ly.y)[r] = t;
+  }
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -266,23 +246,29 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
   constexpr int TJ = 32 * UPL;
   uint32_t* zero = qsm;
   uint32_t* cells = qsm + kCellsWordOffset;  // [zero: 32 words][unit offsets: 160][cells]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  __shared__ int s_next;  // next subtile of this CTA's range (warps grab dynamically)
+  __shared__ int s_last;
+  const int lane = threadIdx.x & 31;
 
   int li = 0;
   while (li + 1 < A.n_layers && A.layer[li + 1].cta_begin <= (int)blockIdx.x) ++li;
   const QLayer& Ly = A.layer[li];
   const int b = blockIdx.x - Ly.cta_begin;
-  int chunk, sub0 = 0, sub1 = 0;
+  int chunk, part = 0, sub0 = 0, sub1 = 0;
   if constexpr (GEMV) {
-    // cpc CTAs per chunk; their warps grab 16-row subtiles dynamically (balanced to one subtile)
+    // cpc CTAs per chunk; every chunk uses the same row partition (part q covers subtiles
+    // [q n_sub / cpc, (q+1) n_sub / cpc)), so one counter per part collects the chunks
     chunk = b / Ly.cpc;
+    part = b % Ly.cpc;
+    sub0 = (int)(((int64_t)part * Ly.n_sub) / Ly.cpc);
+    sub1 = (int)(((int64_t)(part + 1) * Ly.n_sub) / Ly.cpc);
   } else {
     // the layer's cpc CTAs are spread over its chunks as evenly as possible; each chunk's CTAs
     // split its subtiles evenly (static)
     chunk = (int)(((int64_t)b * Ly.n_chunks) / Ly.cpc);
     const int first = (int)(((int64_t)chunk * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks);
     const int nparts = (int)((((int64_t)(chunk + 1) * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks) - first);
-    const int part = b - first;
+    part = b - first;
     sub0 = (int)(((int64_t)part * Ly.n_sub) / nparts);
     sub1 = (int)(((int64_t)(part + 1) * Ly.n_sub) / nparts);
   }
@@ -306,29 +292,24 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
       nx[v] = -xv;  // rotr(rho) decodes to -w'
     }
   }
+  if (threadIdx.x == 0) s_next = sub0 + 0;
   __syncthreads();
   if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 1] = gtimer();
 
-  int pending = -1;  // GEMV: subtile whose partials are written but not yet published
   const int rl = lane & (kSubRows - 1);  // lanes r and r + 16 both hold R(o0 + r)
-  uint32_t* grab = GEMV ? Ly.work + 2 * chunk : nullptr;
-  auto next_sub = [&](int cur) -> int {
-    if constexpr (GEMV) {
-      int g = 0;
-      if (lane == 0) g = (int)atomicAdd(grab, 1u);
-      return __shfl_sync(0xffffffffu, g, 0);
-    } else {
-      return cur + kQWarps;
-    }
+  auto next_sub = [&]() -> int {
+    int g = 0;
+    if (lane == 0) g = atomicAdd(&s_next, 1);
+    return __shfl_sync(0xffffffffu, g, 0);
   };
-  const int sub_end = GEMV ? Ly.n_sub : sub1;
-  int sub = GEMV ? next_sub(0) : sub0 + warp;
+  const int sub_end = sub1;
+  int sub = next_sub();
   uint32_t Rl = 0;
   // R(o) = fmix32(o ^ rho): lane r computes its own row's mix (6 integer ops per subtile and
   // lane, no memory access); SHFL broadcasts it row by row
   if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
   while (sub < sub_end) {
-    const int nxt = next_sub(sub);  // issued now, consumed after this subtile's math
+    const int nxt = next_sub();  // issued now, consumed after this subtile's math
     const int64_t r0 = (int64_t)sub * kSubRows;  // first local row of the subtile
     const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
     if constexpr (GEMV) {
@@ -344,10 +325,6 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
       }
       const float s = transpose_reduce16(acc, lane);
       if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = s;
-      // publish the PREVIOUS subtile now: its stores have drained during this subtile's math,
-      // so the release is cheap (software-pipelined split-K publication)
-      if (pending >= 0) publish_subtile(A, Ly, pending, lane);
-      pending = sub;
     } else {
       const bool full_tile = (nu == TJ);
       E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + j0 + UPL * lane;
@@ -392,13 +369,19 @@ __global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const 
   }
   if (A.timeline && lane == 0) atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
   if constexpr (GEMV) {
-    if (pending >= 0) publish_subtile(A, Ly, pending, lane);
-    // the last warp of this chunk to finish resets the chunk's work counters for the next call
-    if (lane == 0 && atomicAdd(grab + 1, 1u) == (uint32_t)Ly.cpc * kQWarps - 1) {
-      grab[0] = 0u;
-      grab[1] = 0u;
-    }
+    // ---- split-K: one release per CTA; the CTA that completes row part `part` (the n_chunks-th
+    // arrival) sums its rows' chunk partials in fixed chunk order and writes y
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(&Ly.counters[part], 1u) == (uint32_t)Ly.n_chunks - 1);
+    __syncthreads();
     if (!A.early_trigger) pdl_trigger();
+    if (s_last) {
+      __threadfence();
+      const int64_t ra = (int64_t)sub0 * kSubRows, rb = min((int64_t)sub1 * kSubRows, Ly.rows);
+      for (int64_t r = ra + threadIdx.x; r < rb; r += kQThreads) reduce_row(A, Ly, r);
+      if (threadIdx.x == 0) Ly.counters[part] = 0u;  // leave the workspace zeroed for the next call
+    }
   }
   if (A.timeline && lane == 0) atomicMax(&A.timeline[blockIdx.x * 4 + 3], gtimer());
 }
@@ -675,10 +658,18 @@ usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl,
       tail += (double)(h[4 * b + 3] - h[4 * b + 2]);
       last_comp = std::max(last_comp, (double)(h[4 * b + 2] - t0));
     }
+    double skew = 0, cmin = 1e30, cmax = 0, smax = 0;
+    for (int b = 0; b < grid; ++b) {
+      skew = std::max(skew, (double)(h[4 * b] - t0));
+      cmin = std::min(cmin, (double)(h[4 * b + 2] - h[4 * b + 1]));
+      cmax = std::max(cmax, (double)(h[4 * b + 2] - h[4 * b + 1]));
+      smax = std::max(smax, (double)(h[4 * b + 1] - h[4 * b]));
+    }
     std::fprintf(stderr,
-                 "[usk timeline] grid=%d span=%.2fus mean: start_skew? stage=%.2fus compute=%.2fus tail=%.2fus "
-                 "last_compute_end=%.2fus\n",
-                 grid, (tend - t0) / 1e3, stage / grid / 1e3, comp / grid / 1e3, tail / grid / 1e3, last_comp / 1e3);
+                 "[usk timeline] grid=%d span=%.2fus start_skew_max=%.2fus stage mean/max=%.2f/%.2fus compute "
+                 "mean/min/max=%.2f/%.2f/%.2fus tail=%.2fus last_compute_end=%.2fus\n",
+                 grid, (tend - t0) / 1e3, skew / 1e3, stage / grid / 1e3, smax / 1e3, comp / grid / 1e3, cmin / 1e3,
+                 cmax / 1e3, tail / grid / 1e3, last_comp / 1e3);
   } else {
     void* args[] = {const_cast<QArgs*>(&A)};
     USK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
