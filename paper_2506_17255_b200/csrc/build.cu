@@ -26,7 +26,7 @@ namespace usk {
 namespace {
 
 constexpr int kRO = 32;         // weight rows per stage
-constexpr int kConsumers = 8;   // consumer warps
+constexpr int kConsumers = 16;  // consumer warps (2 rows of every stage each)
 constexpr int kBuildThreads = 32 * (kConsumers + 1);
 constexpr int kMaxTasks = 48;
 constexpr size_t kSmemLimit = 227 * 1024;
@@ -54,10 +54,23 @@ struct BuildArgs {
 };
 
 template <int ES>
-constexpr int stages_for() { return ES == 2 ? 8 : 4; }
+constexpr int stages_for() { return ES == 2 ? 6 : 4; }
 
 template <typename E, int UPL>
 constexpr int stage_bytes() { return kRO * 4 + kRO * 32 * UPL * (int)sizeof(E); }
+
+// kappa-min update of one shared key: plain load, then (only if the candidate is smaller) a
+// predicated red.shared.min -- no branch, and the atomic is rare (a new minimum appears ~H(n)
+// times among n candidates of a bucket).  A stale read can only be larger, so it is safe.
+__device__ __forceinline__ void key_min(const uint32_t* keys, uint32_t smem_keys, uint32_t off, uint32_t kap) {
+  const uint32_t cur = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(keys) + off);
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.lt.u32 p, %1, %2;\n\t"
+      "@p red.shared.min.u32 [%0], %1;\n\t}" ::"r"(smem_keys + off),
+      "r"(kap), "r"(cur)
+      : "memory");
+}
 
 template <typename E, int UPL, int MT, int HASH>
 __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_constant__ BuildArgs A) {
@@ -72,6 +85,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   uint64_t* empty = full + S;
   uint8_t* stages = smem + 128;
   uint32_t* keys = reinterpret_cast<uint32_t*>(stages + S * STAGEB);
+  const uint32_t smem_keys = smem_u32(keys);
 
   const int b = blockIdx.x;
   int ti = 0;
@@ -119,10 +133,10 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
         bulk_g2s(st + kRO * 4 + r * ROWB, W + (o0 + r) * T.in + j0, segb, &full[s]);
     }
   } else {
-    // ---------------- consumers
+    // ---------------- consumers: warp cw takes rows cw and cw + 16 of every stage
     const int cw = warp - 1;
     uint32_t K[UPL], N[UPL];
-    int rb[UPL][MR];
+    uint32_t rb[UPL][MR];  // byte offsets of (unit v, sketch row i) in `keys` for this lane
     bool valid[UPL];
 #pragma unroll
     for (int v = 0; v < UPL; ++v) {
@@ -132,7 +146,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       K[v] = A.ukeys[u];
       N[v] = (uint32_t)A.ncols[u];
 #pragma unroll
-      for (int i = 0; i < MR; ++i) rb[v][i] = v * stride_v + i * (int)N[v] * 32 + lane;
+      for (int i = 0; i < MR; ++i) rb[v][i] = 4u * (uint32_t)(v * stride_v + i * (int)N[v] * 32 + lane);
     }
     uint32_t kmax = 0;
     for (int64_t it = 0; it < n_it; ++it) {
@@ -141,20 +155,35 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       const uint8_t* st = stages + s * STAGEB;
       const int64_t o0 = it * kRO;
       const int rows = (int)min((int64_t)kRO, T.out - o0);
-      for (int r = cw; r < rows; r += kConsumers) {
+#pragma unroll
+      for (int rr = 0; rr < kRO / kConsumers; ++rr) {
+        const int r = cw + rr * kConsumers;
+        if (r >= rows) break;
         const uint32_t Rv = reinterpret_cast<const uint32_t*>(st)[r];
         const uint8_t* row = st + kRO * 4 + r * ROWB;
         uint32_t bits[UPL];
-        if constexpr (ES == 2 && UPL == 2) {
+        if constexpr (ES == 2 && UPL == 4) {
+          const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
+          bits[0] = v2.x << 16;
+          bits[1 % UPL] = v2.x & 0xFFFF0000u;
+          bits[2 % UPL] = v2.y << 16;
+          bits[3 % UPL] = v2.y & 0xFFFF0000u;
+        } else if constexpr (ES == 2 && UPL == 2) {
           const uint32_t v2 = reinterpret_cast<const uint32_t*>(row)[lane];
           bits[0] = v2 << 16;
-          bits[1] = v2 & 0xFFFF0000u;
+          bits[1 % UPL] = v2 & 0xFFFF0000u;
         } else if constexpr (ES == 2) {
           bits[0] = (uint32_t)reinterpret_cast<const uint16_t*>(row)[lane] << 16;
+        } else if constexpr (UPL == 4) {
+          const uint4 v4 = reinterpret_cast<const uint4*>(row)[lane];
+          bits[0] = v4.x;
+          bits[1 % UPL] = v4.y;
+          bits[2 % UPL] = v4.z;
+          bits[3 % UPL] = v4.w;
         } else if constexpr (UPL == 2) {
           const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
           bits[0] = v2.x;
-          bits[1] = v2.y;
+          bits[1 % UPL] = v2.y;
         } else {
           bits[0] = reinterpret_cast<const uint32_t*>(row)[lane];
         }
@@ -170,8 +199,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
             uint32_t idx;
             if constexpr (HASH == USK_HASH_X) idx = __umulhi(h * A.hc.a[i], N[v]);
             else idx = (uint32_t)((o0 + r) % N[v]);
-            volatile uint32_t* c = keys + rb[v][i] + idx * 32;
-            if (kap < *c) atomicMin(const_cast<uint32_t*>(c), kap);
+            key_min(keys, smem_keys, rb[v][i] + (idx << 7), kap);
           }
         }
       }
@@ -277,16 +305,17 @@ __global__ void k_gen_final(void* sketch, int64_t c0, int64_t n) {
 
 // ---------------------------------------------------------------- host side
 int fast_upl(const usk_plan* pl, int32_t l) {
-  // units per lane for the fast kernels, 0 = not eligible
+  // units per lane for the fast kernels, 0 = not eligible: the largest UPL whose key array and
+  // stage ring fit one CTA (one CTA per SM is enough: 17 warps, bulk-copy ring in flight)
   const LayerGeom& L = pl->layers[l];
   if (pl->gran != USK_GRAN_ROW || pl->g != 1) return 0;
   const int es = pl->cell_bytes();
   if ((L.in * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
-  const int S = es == 2 ? 8 : 4;
+  const int S = es == 2 ? 6 : 4;
   auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 4 + kRO * 32 * upl * es) + 32LL * upl * mn * 4; };
-  if (smem(2) <= 120 * 1024) return 2;
-  if (smem(1) <= (int64_t)kSmemLimit) return 1;
+  for (int upl : {4, 2, 1})
+    if (smem(upl) <= (int64_t)kSmemLimit) return upl;
   return 0;
 }
 
@@ -344,9 +373,13 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
     A.maxMN = maxmn;
     usk_status s;
     if (pl->dtype == USK_BF16)
-      s = upl == 2 ? launch_fast_m<uint16_t, 2>(A, tiles, pl->hash, st) : launch_fast_m<uint16_t, 1>(A, tiles, pl->hash, st);
+      s = upl == 4   ? launch_fast_m<uint16_t, 4>(A, tiles, pl->hash, st)
+          : upl == 2 ? launch_fast_m<uint16_t, 2>(A, tiles, pl->hash, st)
+                     : launch_fast_m<uint16_t, 1>(A, tiles, pl->hash, st);
     else
-      s = upl == 2 ? launch_fast_m<uint32_t, 2>(A, tiles, pl->hash, st) : launch_fast_m<uint32_t, 1>(A, tiles, pl->hash, st);
+      s = upl == 4   ? launch_fast_m<uint32_t, 4>(A, tiles, pl->hash, st)
+          : upl == 2 ? launch_fast_m<uint32_t, 2>(A, tiles, pl->hash, st)
+                     : launch_fast_m<uint32_t, 1>(A, tiles, pl->hash, st);
     if (s != USK_OK) return s;
   }
   return USK_OK;
@@ -379,24 +412,21 @@ bool layer_fast_ok(const usk_plan* pl, int32_t l) { return fast_upl(pl, l) != 0;
 
 usk_status launch_build(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
                         void* sketch, cudaStream_t st) {
-  std::vector<std::pair<int32_t, const void*>> g1, g2;
+  std::vector<std::pair<int32_t, const void*>> grp[5];  // by units per lane (1, 2, 4)
   for (int32_t k = 0; k < n; ++k) {
     const int32_t l = layer_ids ? layer_ids[k] : k;
     const int upl = fast_upl(pl, l);
-    if (upl == 2) g2.push_back({l, weights[k]});
-    else if (upl == 1) g1.push_back({l, weights[k]});
-    else {
+    if (upl) {
+      grp[upl].push_back({l, weights[k]});
+    } else {
       usk_status s = pl->dtype == USK_BF16 ? launch_generic_t<2>(pl, l, weights[k], sketch, st)
                                             : launch_generic_t<4>(pl, l, weights[k], sketch, st);
       if (s != USK_OK) return s;
     }
   }
-  if (!g2.empty()) {
-    usk_status s = launch_fast(pl, 2, g2, sketch, st);
-    if (s != USK_OK) return s;
-  }
-  if (!g1.empty()) {
-    usk_status s = launch_fast(pl, 1, g1, sketch, st);
+  for (int upl : {4, 2, 1}) {
+    if (grp[upl].empty()) continue;
+    usk_status s = launch_fast(pl, upl, grp[upl], sketch, st);
     if (s != USK_OK) return s;
   }
   return USK_OK;

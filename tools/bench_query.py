@@ -29,8 +29,20 @@ sk = pl.new_sketch(dev)
 ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, 0, k), dev) for k, (o, i) in enumerate(shapes)]
 usk.build(pl, ws, sk)
 usk.check(pl)
-del ws
 flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+_bt = []
+for _ in range(3):
+    flush.fill_(1)
+    _a, _b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    _a.record()
+    usk.build(pl, ws, sk)
+    _b.record()
+    _b.synchronize()
+    _bt.append(_a.elapsed_time(_b) * 1000.0)
+_nw = sum(o * i for o, i in shapes)
+print(json.dumps({"build_block_us": round(min(_bt), 1), "build_Gw_s": round(_nw / min(_bt) / 1e3, 1),
+                  "build_GB_s": round(_nw * 2 / min(_bt) / 1e3, 1)}))
+del ws
 groups = {"qkv": [0, 1, 2], "o": [3], "gate_up": [4, 5], "down": [6]}
 res = {}
 
