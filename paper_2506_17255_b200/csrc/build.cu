@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   const int stride_v = 32 * A.maxMN;  // words per unit slot
 
   {
-    const int nwords = TJ * A.maxMN;
+    const int nwords = TJ * A.maxMN + 32;  // + one dummy word per lane (ragged tiles)
     uint4* k4 = reinterpret_cast<uint4*>(keys);
     for (int i = threadIdx.x; i < nwords / 4; i += blockDim.x) k4[i] = make_uint4(~0u, ~0u, ~0u, ~0u);
     for (int i = (nwords / 4) * 4 + threadIdx.x; i < nwords; i += blockDim.x) keys[i] = ~0u;
@@ -135,18 +135,22 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   } else {
     // ---------------- consumers: warp cw takes rows cw and cw + 16 of every stage
     const int cw = warp - 1;
-    uint32_t K[UPL], N[UPL];
+    uint32_t K[UPL], N[UPL], vmask[UPL];
     uint32_t rb[UPL][MR];  // byte offsets of (unit v, sketch row i) in `keys` for this lane
-    bool valid[UPL];
 #pragma unroll
     for (int v = 0; v < UPL; ++v) {
       const int ul = UPL * lane + v;
-      valid[v] = ul < nu;
-      const int64_t u = T.unit_base + j0 + (valid[v] ? ul : 0);
+      const bool valid = ul < nu;
+      const int64_t u = T.unit_base + j0 + (valid ? ul : 0);
       K[v] = A.ukeys[u];
-      N[v] = (uint32_t)A.ncols[u];
+      // a missing unit of a ragged tile updates a private dummy word (never written back) with a
+      // zero candidate, so the loop below needs no branch
+      N[v] = valid ? (uint32_t)A.ncols[u] : 1u;
+      vmask[v] = valid ? ~0u : 0u;
 #pragma unroll
-      for (int i = 0; i < MR; ++i) rb[v][i] = 4u * (uint32_t)(v * stride_v + i * (int)N[v] * 32 + lane);
+      for (int i = 0; i < MR; ++i)
+        rb[v][i] = valid ? 4u * (uint32_t)(v * stride_v + i * (int)N[v] * 32 + lane)
+                         : 4u * (uint32_t)(TJ * A.maxMN + lane);
     }
     uint32_t kmax = 0;
     for (int64_t it = 0; it < n_it; ++it) {
@@ -189,8 +193,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
         }
 #pragma unroll
         for (int v = 0; v < UPL; ++v) {
-          if (!valid[v]) continue;
-          const uint32_t kap = rotl1(bits[v]);
+          const uint32_t kap = rotl1(bits[v] & vmask[v]);
           kmax = max(kmax, kap);
           const uint32_t h = Rv ^ K[v];
 #pragma unroll
@@ -313,7 +316,7 @@ int fast_upl(const usk_plan* pl, int32_t l) {
   if ((L.in * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
   const int S = es == 2 ? 6 : 4;
-  auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 4 + kRO * 32 * upl * es) + 32LL * upl * mn * 4; };
+  auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 4 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
   for (int upl : {4, 2, 1})
     if (smem(upl) <= (int64_t)kSmemLimit) return upl;
   return 0;
@@ -322,7 +325,7 @@ int fast_upl(const usk_plan* pl, int32_t l) {
 template <typename E, int UPL, int MT, int HASH>
 usk_status launch_fast_t(BuildArgs& A, int n_ctas, cudaStream_t st) {
   constexpr int S = stages_for<sizeof(E)>();
-  const size_t smem = 128 + (size_t)S * stage_bytes<E, UPL>() + (size_t)32 * UPL * A.maxMN * 4;
+  const size_t smem = 128 + (size_t)S * stage_bytes<E, UPL>() + (size_t)32 * UPL * A.maxMN * 4 + 128;
   auto kern = k_build_fast<E, UPL, MT, HASH>;
   USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<n_ctas, kBuildThreads, smem, st>>>(A);
