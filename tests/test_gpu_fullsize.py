@@ -1,0 +1,187 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py times.
+
+  c2: one Llama-3.2-1B MLP block, M=3, 0.5 bpw, importance-aware (C=4): every sketch byte and
+      the plan arrays vs the oracle; sampled reconstruction rows and GEMV rows.
+  c3: all 112 Llama-3.2-1B linears built in ONE usk_build call with the bench's device-generated
+      weights; sampled units of sampled layers (sketch bytes + reconstructed entries) and sampled
+      GEMV rows of the grouped launches (usk_linear_batch, as timed by bench.py).
+  c4: prefill of the 1B gate projection with 2048 x 8 = 16384 tokens at 0.5 and 0.8 bpw
+      (reconstruct + tcgen05 GEMM), sampled (token, output) entries vs the fp64 oracle.
+  c5: Llama-3-8B-shaped block: plan parity, sampled unit bytes, sampled GEMV rows.
+"""
+import numpy as np
+import pytest
+
+import synth
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+SEED = 0x5EED000000000003
+
+
+@pytest.fixture(scope="module")
+def usk():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2506_17255_b200 import usk as u
+    return u
+
+
+def host_bits(t):
+    return t.cpu().view(torch.int16).numpy().view(np.uint16)
+
+
+def dev_bf16(bits):
+    return torch.from_numpy(np.ascontiguousarray(bits).view(np.int16).copy()).view(torch.bfloat16).cuda()
+
+
+def gemv_err(y, y64, x64, Wr):
+    scale = np.abs(x64)[None, :] @ np.abs(Wr).T
+    return float(np.max(np.abs(y - y64) / np.maximum(scale, 1e-30)))
+
+
+def test_c2_mlp_block_importance(orc, usk):
+    shapes = synth.mlp_block_1b_shapes()
+    Ws = [synth.weights_bf16(o, i, synth.seed_for(2, 0, 4 + k)) for k, (o, i) in enumerate(shapes)]
+    # saliency = Eq. 7 of synthetic calibration activations (oracle fp64 -> fp32, fed to both sides)
+    sal = [orc.importance(synth.activations(512, i, seed=200 + k)).astype(np.float32) for k, (o, i) in enumerate(shapes)]
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, n_classes=4, seed=SEED,
+                             saliency=[torch.from_numpy(s).cuda() for s in sal])
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, saliency=sal, C=4, seed=SEED)
+    for l in range(3):
+        cls, ncols, _, offs = pl.export(l)
+        u0, u1 = opl.layer_units(l)
+        assert np.array_equal(cls, opl.cls[u0:u1]) and np.array_equal(ncols, opl.ncols[u0:u1])
+        assert np.array_equal(offs, opl.offsets[u0:u1 + 1])
+        assert pl.layers[l].achieved_bits <= pl.layers[l].budget_bits
+    sk = pl.new_sketch()
+    usk.build(pl, [dev_bf16(W) for W in Ws], sk)
+    usk.check(pl)
+    osk = orc.build_model(opl, Ws)
+    assert np.array_equal(sk.cpu().numpy().view(np.uint16)[:opl.total_cells], osk)
+    rng = np.random.default_rng(0)
+    for l, (o, i) in enumerate(shapes):
+        Wr = torch.empty((o, i), dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, Wr)
+        rows = rng.choice(o, 24, replace=False)
+        got = host_bits(Wr)[rows]
+        for k, r in enumerate(rows):
+            assert np.array_equal(got[k], orc.reconstruct_rows(opl, osk, l, int(r), int(r) + 1)[0])
+        xb = synth.f32_to_bf16_bits(synth.vector(i, seed=l)[0])
+        y = torch.empty(o, dtype=torch.float32, device="cuda")
+        usk.linear(pl, sk, l, dev_bf16(xb).view(1, -1), y.view(1, -1), usk.new_workspace(pl, l))
+        x64 = synth.bf16_bits_to_f32(xb).astype(np.float64)
+        r0 = int(rng.integers(0, o - 16))
+        y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 16)[0]
+        W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, r0, r0 + 16), orc.BF16).reshape(16, i)
+        assert gemv_err(y.cpu().numpy()[r0:r0 + 16].astype(np.float64), y64, x64, W64) <= 1e-5
+
+
+def _unit_parity(orc, usk, pl, opl, sk, l, W_dev, n_units, rng):
+    """Sampled units of layer l: the oracle builds them from the same (device-generated) weights."""
+    o, i = opl.shapes[l]
+    ts = np.sort(rng.choice(i, n_units, replace=False))
+    Wh = np.zeros((o, i), np.uint16)
+    cols = host_bits(W_dev[:, torch.from_numpy(ts).cuda()].contiguous())
+    Wh[:, ts] = cols
+    osk = np.zeros(opl.total_cells, np.uint16)
+    for t in ts:
+        orc.build_layer(opl, l, Wh, osk, int(t), int(t) + 1)
+    u0, _ = opl.layer_units(l)
+    got = sk.cpu().numpy().view(np.uint16)
+    for t in ts:
+        a, b = opl.offsets[u0 + t], opl.offsets[u0 + t + 1]
+        assert np.array_equal(got[a:b], osk[a:b]), (l, t)
+    # reconstructed entries of those units
+    Wr = torch.empty((o, i), dtype=torch.bfloat16, device="cuda")
+    usk.reconstruct(pl, sk, l, Wr)
+    oj = np.stack([rng.integers(0, o, 256), rng.choice(ts, 256)], 1)
+    want = orc.reconstruct_entries(opl, osk, l, oj)
+    assert np.array_equal(host_bits(Wr)[oj[:, 0], oj[:, 1]].astype(np.uint32), want)
+
+
+def test_c3_full_model_sampled(orc, usk):
+    shapes = synth.llama32_1b_shapes()
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED)
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED)
+    assert pl.info["total_cells"] == opl.total_cells
+    sk = pl.new_sketch()
+    ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, l // 7, l % 7), "cuda") for l, (o, i) in enumerate(shapes)]
+    usk.build(pl, ws, sk)  # one call, as bench.py
+    usk.check(pl)
+    rng = np.random.default_rng(1)
+    sample_layers = [0, 1, 3, 4, 6, 7 * 15 + 2, 7 * 15 + 5]
+    for l in sample_layers:
+        _unit_parity(orc, usk, pl, opl, sk, l, ws[l], 6, rng)
+    # grouped GEMV (bench launch configuration) on sampled rows of two groups: the oracle builds
+    # the full layers from the same weights
+    for g in ([0, 1, 2], [4, 5]):
+        i = shapes[g[0]][1]
+        x = synth.torch_vector(i, 1000 + g[0], "cuda", torch.bfloat16)[0]
+        ys = [torch.empty(shapes[l][0], dtype=torch.float32, device="cuda") for l in g]
+        usk.linear_batch(pl, sk, g, x, ys, usk.new_batch_workspace(pl, g))
+        x64 = synth.bf16_bits_to_f32(host_bits(x)).astype(np.float64)
+        for l, y in zip(g, ys):
+            o = shapes[l][0]
+            osk = np.zeros(opl.total_cells, np.uint16)
+            orc.build_layer(opl, l, host_bits(ws[l]), osk)
+            r0 = int(rng.integers(0, o - 8))
+            y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 8)[0]
+            W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, r0, r0 + 8), orc.BF16).reshape(8, i)
+            assert gemv_err(y.cpu().numpy()[r0:r0 + 8].astype(np.float64), y64, x64, W64) <= 1e-5
+
+
+@pytest.mark.parametrize("bpw", [0.5, 0.8])
+def test_c4_prefill_16384_tokens(orc, usk, bpw):
+    o, i, T = 8192, 2048, 16384
+    W = synth.torch_weights_bf16(o, i, synth.seed_for(4, 0, 4), "cuda")
+    pl = usk.plan_allocation([(o, i)], bpw=bpw, rows=3, seed=SEED)
+    opl = orc.plan([(o, i)], bpw, M=3, dtype=orc.BF16, seed=SEED)
+    sk = pl.new_sketch()
+    usk.build(pl, [W], sk)
+    X = synth.torch_vector(i, 7, "cuda", torch.bfloat16, T=T)
+    Y = torch.empty((T, o), dtype=torch.bfloat16, device="cuda")
+    usk.linear(pl, sk, 0, X, Y, usk.new_workspace(pl, 0, T))
+    osk = np.zeros(opl.total_cells, np.uint16)
+    orc.build_layer(opl, 0, host_bits(W), osk)
+    rng = np.random.default_rng(2)
+    rows = rng.choice(o, 8, replace=False)
+    toks = rng.choice(T, 64, replace=False)
+    Xh = synth.bf16_bits_to_f32(host_bits(X[torch.from_numpy(toks).cuda()])).astype(np.float64)
+    Yh = Y.float().cpu().numpy()
+    for r in rows:
+        y64 = orc.linear_rows(opl, osk, 0, Xh, int(r), int(r) + 1)[:, 0]
+        w64 = orc.value_of(orc.reconstruct_rows(opl, osk, 0, int(r), int(r) + 1), orc.BF16)
+        scale = np.abs(Xh) @ np.abs(w64)
+        err = np.max(np.abs(Yh[toks, r] - y64) / np.maximum(scale, 1e-30))
+        assert err <= 2e-2, err
+
+
+def test_c5_llama8b_block(orc, usk):
+    shapes = synth.llama3_8b_shapes()[:7]
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED)
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED)
+    for l in range(7):
+        _, ncols, _, offs = pl.export(l)
+        u0, u1 = opl.layer_units(l)
+        assert np.array_equal(ncols, opl.ncols[u0:u1]) and np.array_equal(offs, opl.offsets[u0:u1 + 1])
+    sk = pl.new_sketch()
+    ws = [synth.torch_weights_bf16(o, i, synth.seed_for(5, 0, l), "cuda") for l, (o, i) in enumerate(shapes)]
+    usk.build(pl, ws, sk)
+    usk.check(pl)
+    rng = np.random.default_rng(3)
+    for l in (0, 4, 6):
+        _unit_parity(orc, usk, pl, opl, sk, l, ws[l], 4, rng)
+    l = 6  # down [4096, 14336]
+    o, i = shapes[l]
+    x = synth.torch_vector(i, 11, "cuda", torch.bfloat16)
+    y = torch.empty((1, o), dtype=torch.float32, device="cuda")
+    usk.linear(pl, sk, l, x, y, usk.new_workspace(pl, l))
+    osk = np.zeros(opl.total_cells, np.uint16)
+    orc.build_layer(opl, l, host_bits(ws[l]), osk)
+    x64 = synth.bf16_bits_to_f32(host_bits(x)[0]).astype(np.float64)
+    r0 = 1000
+    y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 8)[0]
+    W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, r0, r0 + 8), orc.BF16).reshape(8, i)
+    assert gemv_err(y.cpu().numpy()[0, r0:r0 + 8].astype(np.float64), y64, x64, W64) <= 1e-5

@@ -78,3 +78,21 @@ tot_gemv = sum(v["us"] for k, v in res.items() if k.startswith("gemv"))
 res["gemv_block_us"] = tot_gemv
 res["est_tok_s"] = 1e6 / (tot_gemv * len(shapes) / 7 * (16 if args.model == "1b" else 32))
 print(json.dumps({"env_upl": os.environ.get("USK_UPL"), **{k: (round(v["us"], 2), round(v["Gw_s"], 1)) if isinstance(v, dict) else round(v, 2) for k, v in res.items()}}))
+
+# ---------------- prefill (config 4): usk_linear with T = 2048 x 8 tokens per block-0 linear
+if os.environ.get("USK_PREFILL", "1") == "1":
+    T = 16384
+    pre = {}
+    tot_flop = tot_us = 0.0
+    for l, (o, i) in enumerate(shapes):
+        X = synth.torch_vector(i, 5, dev, torch.bfloat16, T=T)
+        Y = torch.empty((T, o), dtype=torch.bfloat16, device=dev)
+        w = usk.new_workspace(pl, l, T, device=dev)
+        us = timeit(lambda: usk.linear(pl, sk, l, X, Y, w))
+        fl = 2.0 * T * o * i
+        pre[f"prefill_{l}"] = (round(us, 1), round(fl / us / 1e6, 1))  # us, TFLOP/s
+        tot_flop += fl
+        tot_us += us
+        del X, Y, w
+    pre["prefill_block_TFLOPs"] = round(tot_flop / tot_us / 1e6, 1)
+    print(json.dumps(pre))
