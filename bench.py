@@ -162,6 +162,7 @@ def run_reference(args):
 def run_usk(args):
     import torch
     import torch.distributed as dist
+    from paper_2506_17255_b200 import dist as udist
     from paper_2506_17255_b200 import usk
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -180,7 +181,7 @@ def run_usk(args):
     plan = usk.plan_allocation(shapes, bpw=BPW, rows=ROWS, seed=SEED)
     sketch = plan.new_sketch(dev)
     sketch.zero_()
-    owned = [l for l in range(L) if (l // 7) % world == rank]       # blocks round-robin over ranks
+    owned = udist.owned_layers(L, rank, world)  # whole blocks round-robin over ranks
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     # all owned layers in ONE usk_build call (the kernel balances its tiles across waves); the
     # weights (1.95 GB bf16 for all 112 linears) are generated first and freed after the build
@@ -201,19 +202,22 @@ def run_usk(args):
     del ws
     usk.check(plan)
     owned_w = sum(shapes[l][0] * shapes[l][1] for l in owned)
-    if world > 1:
-        cb = 2  # bf16 cells
-        for l in range(L):
-            li = plan.layers[l]
-            src = (l // 7) % world
-            dist.broadcast(sketch[li.cell_begin * cb:(li.cell_begin + li.n_cells) * cb], src=src)
+    replicate_ms = 0.0
+    if world > 1:  # one-time replication of the layer-sharded sketch (deployment step)
+        regions = [(plan.layers[l].cell_begin * 2, (plan.layers[l].cell_begin + plan.layers[l].n_cells) * 2)
+                   for l in range(L)]
         torch.cuda.synchronize()
+        ev0.record()
+        udist.replicate_sketch(sketch, regions, world)
+        ev1.record()
+        torch.cuda.synchronize()
+        replicate_ms = ev0.elapsed_time(ev1)
 
     # ---- decode buffers.  The linears of a block that read the same activation share one
     #      synthetic x (q|k|v: attention input, o, gate|up: MLP input, down), exactly as in a
     #      decode step; y is fp32.  Grouped launches (usk_linear_batch): 4 per block = 64/token.
     def shard(o):
-        return (o * rank) // world, (o * (rank + 1)) // world
+        return udist.output_shard(o, rank, world)
     groups = []
     for b in range(L // 7):
         base = 7 * b
@@ -237,7 +241,7 @@ def run_usk(args):
     def gather(ls):
         if world > 1:
             for l in ls:
-                dist.all_gather_into_tensor(ys_full[l], Yshard[l])
+                udist.allgather_outputs(Yshard[l], ys_full[l])
 
     def step_grouped():
         for gi, g in enumerate(groups):
@@ -254,6 +258,13 @@ def run_usk(args):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def capture(fn):
+        if world > 1 and os.environ.get("USK_BENCH_NCCL_GRAPH") != "1":
+            torch.cuda.synchronize()
+            usk.launch_count(reset=True)
+            with torch.cuda.stream(stream):
+                fn()
+            torch.cuda.synchronize()
+            return None, usk.launch_count(reset=True)  # eager steps (NCCL in graph capture is opt-in)
         torch.cuda.synchronize()
         with torch.cuda.stream(stream):
             for _ in range(2):
@@ -410,7 +421,7 @@ def run_usk(args):
             "weights_reconstructed_per_s": tok_s * numel,
             "reconstruct_standalone": {"weights_per_s": rec_wps, "GB_per_s_written": rec_wps * 2 / 1e9,
                                        "hbm_frac": rec_wps * (2 + 2 * BPW / 16) / 1e9 / peaks["hbm_gbs"]},
-            "build": {"ms": build_ms, "weights_per_s": owned_w / (build_ms * 1e-3),
+            "build": {"ms": build_ms, "replicate_ms": replicate_ms, "weights_per_s": owned_w / (build_ms * 1e-3),
                       "GB_per_s": owned_w * (2 + BPW / 8) / (build_ms * 1e-3) / 1e9},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": gather_peak, "unit": "Gweight/s",
                          "frac": achieved / gather_peak, "traffic": traffic,

@@ -1,0 +1,56 @@
+"""Multi-GPU orchestration of the sketch path (host side; torch.distributed for the plumbing).
+
+SURVEY §8(e) / DESIGN.md "Multi-GPU":
+  * Build: compression units are independent, so layers are sharded over ranks with
+    no data-path collective; every rank computes the (deterministic) plan itself.  A one-time
+    replication (one broadcast per layer region from its owner) gives every rank the full sketch
+    for output-sharded inference.
+  * Decode: each linear's output features are split into contiguous per-rank ranges; each rank
+    runs usk_linear on its range and the fp32 y shards are all-gathered (NCCL on GPUs).
+  * Prefill: replicas (sequences sharded, sketch replicated) -- no collective.
+"""
+from __future__ import annotations
+
+
+def output_shard(out_features: int, rank: int, world: int):
+    """Contiguous output range [o0, o1) of `rank` (sizes differ by at most one row)."""
+    return (out_features * rank) // world, (out_features * (rank + 1)) // world
+
+
+def layer_owner(layer: int, world: int, layers_per_block: int = 7) -> int:
+    """Owner rank of a layer for the sharded build: whole transformer blocks round-robin."""
+    return (layer // layers_per_block) % world
+
+
+def owned_layers(n_layers: int, rank: int, world: int, layers_per_block: int = 7):
+    return [l for l in range(n_layers) if layer_owner(l, world, layers_per_block) == rank]
+
+
+def replicate_sketch(sketch_bytes, layer_regions, world: int, group=None, layers_per_block: int = 7):
+    """Broadcast every layer's byte region [b0, b1) of `sketch_bytes` (a uint8 tensor) from its
+    owner so that all ranks hold the full sketch (one-time deployment step)."""
+    import torch.distributed as dist
+    for l, (b0, b1) in enumerate(layer_regions):
+        if b1 > b0:
+            dist.broadcast(sketch_bytes[b0:b1], src=layer_owner(l, world, layers_per_block), group=group)
+
+
+def allgather_outputs(y_shard, y_full, group=None):
+    """y_full[...] = concatenation over ranks of their y shards (equal-size shards use
+    all_gather_into_tensor; ragged shards fall back to all_gather + copy)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n = y_full.shape[-1]
+    sizes = [output_shard(n, r, world) for r in range(world)]
+    if all(b - a == sizes[0][1] - sizes[0][0] for a, b in sizes):
+        dist.all_gather_into_tensor(y_full, y_shard.contiguous(), group=group)
+        return y_full
+    mx = max(b - a for a, b in sizes)  # pad the ragged shards to one size
+    padded = torch.zeros(mx, dtype=y_shard.dtype, device=y_shard.device)
+    padded[:y_shard.numel()] = y_shard
+    parts = [torch.empty(mx, dtype=y_shard.dtype, device=y_shard.device) for _ in sizes]
+    dist.all_gather(parts, padded, group=group)
+    for (a, b), p in zip(sizes, parts):
+        y_full[a:b] = p[:b - a]
+    return y_full

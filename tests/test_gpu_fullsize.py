@@ -152,7 +152,7 @@ def test_c4_prefill_16384_tokens(orc, usk, bpw):
     Yh = Y.float().cpu().numpy()
     for r in rows:
         y64 = orc.linear_rows(opl, osk, 0, Xh, int(r), int(r) + 1)[:, 0]
-        w64 = orc.value_of(orc.reconstruct_rows(opl, osk, 0, int(r), int(r) + 1), orc.BF16)
+        w64 = orc.value_of(orc.reconstruct_rows(opl, osk, 0, int(r), int(r) + 1), orc.BF16).reshape(i)
         scale = np.abs(Xh) @ np.abs(w64)
         err = np.max(np.abs(Yh[toks, r] - y64) / np.maximum(scale, 1e-30))
         assert err <= 2e-2, err
