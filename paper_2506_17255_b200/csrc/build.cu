@@ -6,13 +6,14 @@
 // atomicMin gives the same bytes for every interleaving.
 //
 // Fast path (ROW granularity, one input dimension per unit -- DESIGN.md L6):
-//   * one CTA per tile of TJ = 32*UPL consecutive units (input dims) of a layer, all outputs;
-//   * warp 0 streams [32 rows x TJ] weight tiles (plus the 32 position mixes R(o)) into an
-//     8-stage shared-memory ring with cp.async.bulk + mbarrier (TMA bulk engine);
-//   * 8 consumer warps: lane L owns units UPL*L .. UPL*L+UPL-1; its keys live in shared memory
-//     at word (v * 32 * maxMN + k * 32 + L), i.e. always in bank L, so the M random bucket
-//     updates of a warp are bank-conflict free;  each update is a plain LDS pre-check and,
-//     only when the candidate is smaller, an ATOMS.MIN (candidates rarely win: ~H(n)/n);
+//   * one CTA per tile of TJ = 32*UPL consecutive units (input dims) of a layer, all outputs
+//     (no cross-CTA merge); a whole model is one launch so tiles balance across waves;
+//   * warp 0 streams [32 rows x TJ] weight tiles (plus the 32 position mixes R(o)) into a
+//     6-stage shared-memory ring with cp.async.bulk + mbarrier (TMA bulk engine);
+//   * 16 consumer warps (2 rows of each stage): lane L owns units UPL*L .. UPL*L+UPL-1; its
+//     keys live in shared memory at word (v * 32 * maxMN + k * 32 + L), i.e. always in bank L,
+//     so the M random bucket updates of a warp are bank-conflict free; each update is an
+//     unconditional red.shared.min (see key_min);
 //   * the CTA then writes its units' cells (states, +Inf for empty) to the sketch.
 // Generic path (LAYER granularity, dims_per_unit > 1, odd shapes, oversize units): keys are
 // kept in place in the sketch buffer (32-bit atomicMin for fp32 cells, 16-bit CAS for bf16),
