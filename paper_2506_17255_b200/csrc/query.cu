@@ -37,7 +37,10 @@
 namespace usk {
 namespace {
 
-constexpr int kQThreads = 512;
+#ifndef USK_QUERY_THREADS
+#define USK_QUERY_THREADS 512
+#endif
+constexpr int kQThreads = USK_QUERY_THREADS;
 constexpr int kMaxBatch = 8;
 constexpr int kSubRows = 16;  // rows per warp work item (subtile)
 constexpr int kCellsWordOffset = 32 + 160;  // zero cells + chunk unit offsets (<= 129)
