@@ -61,11 +61,27 @@ __global__ void k_unit_scores(PlanDev P, int64_t U, double* s_u, int* err) {
   s_u[u] = acc / (double)(j1 - j0);
 }
 
+// warp-aggregated atomics: lanes with equal keys combine first, the group leader does one atomic
+__device__ __forceinline__ void group_max_u64(unsigned long long* dst, unsigned key, unsigned long long v) {
+  const unsigned mask = __match_any_sync(0xffffffffu, key);
+  unsigned long long m = v;
+  for (unsigned b = mask; b; b &= b - 1) m = max(m, __shfl_sync(mask, v, __ffs(b) - 1));
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1) && dst) atomicMax(dst, m);
+}
+
+__device__ __forceinline__ void group_add_u64(unsigned long long* dst, unsigned key, unsigned long long v) {
+  const unsigned mask = __match_any_sync(0xffffffffu, key);
+  unsigned long long sum = 0;
+  for (unsigned b = mask; b; b &= b - 1) sum += __shfl_sync(mask, v, __ffs(b) - 1);
+  if ((threadIdx.x & 31) == (unsigned)(__ffs(mask) - 1) && dst) atomicAdd(dst, sum);
+}
+
 __global__ void k_scope_max(PlanDev P, int64_t U, const double* s_u, unsigned long long* smax) {
-  int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (u >= U) return;
-  int sc = (P.gran == USK_GRAN_ROW) ? find_layer(P.unit_base, P.L, u) : 0;
-  atomicMax(&smax[sc], (unsigned long long)__double_as_longlong(s_u[u]));  // s_u >= 0
+  const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool ok = u < U;
+  const int sc = !ok ? -1 : (P.gran == USK_GRAN_ROW) ? find_layer(P.unit_base, P.L, u) : 0;
+  const unsigned long long v = ok ? (unsigned long long)__double_as_longlong(s_u[u]) : 0ull;  // s_u >= 0
+  group_max_u64(ok ? &smax[sc] : nullptr, (unsigned)sc, v);
 }
 
 __global__ void k_sort_keys(PlanDev P, int64_t U, const double* s_u, const unsigned long long* smax,
@@ -84,17 +100,23 @@ __global__ void k_classes(PlanDev P, int64_t U, const uint64_t* keys_sorted,
                           const uint32_t* vals_sorted, const uint32_t* q, const int64_t* scope_begin,
                           const int64_t* scope_units, uint8_t* cls,
                           unsigned long long* n_c, unsigned long long* W_c) {
-  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (r >= U) return;
-  int sc = (int)(keys_sorted[r] >> 25);
-  uint32_t u = vals_sorted[r];
-  int64_t rank = r - scope_begin[sc];
-  int c = (int)((rank * (int64_t)P.C) / scope_units[sc]);
-  cls[u] = (uint8_t)c;
-  unsigned long long Lu = 1;
-  if (P.gran == USK_GRAN_LAYER) Lu = (unsigned long long)P.numel[u];
-  atomicAdd(&n_c[(int64_t)sc * P.C + c], 1ull);
-  atomicAdd(&W_c[(int64_t)sc * P.C + c], (unsigned long long)q[u] * Lu);
+  const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool ok = r < U;
+  int64_t slot = -1;
+  unsigned long long w = 0;
+  if (ok) {
+    const int sc = (int)(keys_sorted[r] >> 25);
+    const uint32_t u = vals_sorted[r];
+    const int64_t rank = r - scope_begin[sc];
+    const int c = (int)((rank * (int64_t)P.C) / scope_units[sc]);
+    cls[u] = (uint8_t)c;
+    const unsigned long long Lu = (P.gran == USK_GRAN_LAYER) ? (unsigned long long)P.numel[u] : 1ull;
+    slot = (int64_t)sc * P.C + c;
+    w = (unsigned long long)q[u] * Lu;
+  }
+  // consecutive ranks share (scope, class): aggregate inside the warp before the atomics
+  group_add_u64(ok ? &n_c[slot] : nullptr, (unsigned)slot, 1ull);
+  group_add_u64(ok ? &W_c[slot] : nullptr, (unsigned)slot, w);
 }
 
 // One block (one thread) per scope: proportional share, water-filled floor, largest remainder.

@@ -241,7 +241,7 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 #ifndef USK_QUERY_MINB
-#define USK_QUERY_MINB 1
+#define USK_QUERY_MINB 2
 #endif
 
 template <typename E, int UPL, int MT, int HASH, bool GEMV>
