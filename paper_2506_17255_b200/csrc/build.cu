@@ -187,40 +187,18 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
         } else {
           bits[0] = reinterpret_cast<const uint32_t*>(row)[lane];
         }
-        if constexpr (MT > 0 && HASH == USK_HASH_X) {
-          // all UPL x M key loads of the row first (pipelined), then the rare winning updates:
-          // the predicated atomics run with ~2 active lanes instead of 32
-          uint32_t kap[UPL], off[UPL][MR], cur[UPL][MR];
 #pragma unroll
-          for (int v = 0; v < UPL; ++v) {
-            kap[v] = rotl1(bits[v] & vmask[v]);
-            kmax = max(kmax, kap[v]);
-            const uint32_t h = Rv ^ K[v];
+        for (int v = 0; v < UPL; ++v) {
+          const uint32_t kap = rotl1(bits[v] & vmask[v]);
+          kmax = max(kmax, kap);
+          const uint32_t h = Rv ^ K[v];
 #pragma unroll
-            for (int i = 0; i < MR; ++i) {
-              off[v][i] = rb[v][i] + (__umulhi(h * A.hc.a[i], N[v]) << 7);
-              cur[v][i] = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(keys) + off[v][i]);
-            }
-          }
-#pragma unroll
-          for (int v = 0; v < UPL; ++v)
-#pragma unroll
-            for (int i = 0; i < MR; ++i)
-              if (kap[v] < cur[v][i]) key_min(smem_keys, off[v][i], kap[v]);
-        } else {
-#pragma unroll
-          for (int v = 0; v < UPL; ++v) {
-            const uint32_t kap = rotl1(bits[v] & vmask[v]);
-            kmax = max(kmax, kap);
-            const uint32_t h = Rv ^ K[v];
-#pragma unroll
-            for (int i = 0; i < MR; ++i) {
-              if (MT == 0 && i >= M) break;
-              uint32_t idx;
-              if constexpr (HASH == USK_HASH_X) idx = __umulhi(h * A.hc.a[i], N[v]);
-              else idx = (uint32_t)((o0 + r) % N[v]);
-              key_min(smem_keys, rb[v][i] + (idx << 7), kap);
-            }
+          for (int i = 0; i < MR; ++i) {
+            if (MT == 0 && i >= M) break;
+            uint32_t idx;
+            if constexpr (HASH == USK_HASH_X) idx = __umulhi(h * A.hc.a[i], N[v]);
+            else idx = (uint32_t)((o0 + r) % N[v]);
+            key_min(smem_keys, rb[v][i] + (idx << 7), kap);
           }
         }
       }
