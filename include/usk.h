@@ -209,6 +209,17 @@ USK_API const char* usk_last_error(void);
  * (bench evidence for "gpu_launches"). */
 USK_API int64_t usk_launch_count(int32_t reset);
 
+/* Tuning-only kernel trace (active only when the environment variable USK_TRACE is set when the
+ * library first launches a query kernel).  Every sketch-GEMV / reconstruct launch then writes 4
+ * %globaltimer stamps per CTA (start, staged, compute done, exit) into a device ring; launch
+ * slots are assigned when the launch is ISSUED, so a captured CUDA graph rewrites the same slots
+ * on every replay.  usk_trace_read synchronises the device, copies up to cap_stamps stamps
+ * (4 per CTA, launches in issue order) into `stamps` and up to cap_launches grid sizes into
+ * `grids` (host buffers) and returns the number of launches recorded (0 when tracing is off).
+ * usk_trace_reset forgets all slots (call before capturing a new graph). */
+USK_API int32_t usk_trace_read(uint64_t* stamps, int64_t cap_stamps, int32_t* grids, int32_t cap_launches);
+USK_API void usk_trace_reset(void);
+
 #ifdef __cplusplus
 }
 #endif

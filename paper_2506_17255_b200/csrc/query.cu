@@ -42,34 +42,39 @@ namespace {
 #endif
 constexpr int kQThreads = USK_QUERY_THREADS;
 constexpr int kMaxBatch = 8;
-constexpr int kSubRows = 16;  // rows per warp work item (subtile)
+constexpr int kMaxCtas = 256;  // GEMV compute grid (one CTA per SM)
+#ifndef USK_SUB_ROWS
+#define USK_SUB_ROWS 8
+#endif
+constexpr int kSubRows = USK_SUB_ROWS;  // rows per warp work item (subtile): 8 or 16
+static_assert(kSubRows == 8 || kSubRows == 16, "subtile rows");
 constexpr int kCellsWordOffset = 32 + 160;  // zero cells + chunk unit offsets (<= 129)
 
 extern __shared__ __align__(16) uint32_t qsm[];  // dynamic shared memory of the query kernels
 
-// 32-bit shared load at a byte offset from qsm: compiles to LDS [R + UR] (base folded), and as
-// an ordinary load it can be scheduled freely around the address arithmetic.
-__device__ __forceinline__ uint32_t lds32(uint32_t off) {
-  return *reinterpret_cast<const uint32_t*>(reinterpret_cast<const char*>(qsm) + off);
+// 32-bit shared load at a shared-window byte address (ld.shared: no generic -> shared conversion
+// in the inner loop).
+__device__ __forceinline__ uint32_t lds_at(uint32_t saddr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(saddr));
+  return v;
 }
 
 struct QLayer {
   int64_t unit_base;   // global unit id of the layer's first unit
   int64_t o_begin;     // first output row
   int64_t rows;        // rows in [o_begin, o_end)
+  int64_t item_begin;  // GEMV: first work item (chunk-major, subtile-minor) of the layer in the launch
+  int64_t row_begin;   // GEMV: first row of the layer in the launch's reduction order
   int32_t n_chunks;    // unit chunks of TJ
   int32_t n_sub;       // 16-row subtiles
-  int32_t cpc;         // GEMV: CTAs per chunk; reconstruct: CTAs of the layer
-  int32_t cta_begin;   // first CTA of this layer in the launch
-  int32_t CP;          // row stride of the partial workspace (>= n_chunks, multiple of 4)
+  int32_t cpc;         // reconstruct: CTAs of the layer
+  int32_t cta_begin;   // reconstruct: first CTA of this layer in the launch
+  int32_t CP;          // GEMV: row stride of the partial workspace (>= n_chunks, multiple of 4)
   int32_t pad;
-  // gemv
-  void* y;
-  float* partial;      // [rows][CP]
-  uint32_t* counters;  // [n_sub] split-K completion counts
-  uint32_t* work;      // [2 * n_chunks]: per chunk, next subtile to grab and warps finished
-  // reconstruct
-  void* w_out;
+  void* y;             // GEMV output
+  float* partial;      // GEMV: [rows][CP] chunk partials
+  void* w_out;         // reconstruct output
   int64_t ld_out;
 };
 
@@ -77,19 +82,25 @@ struct QArgs {
   QLayer layer[kMaxBatch];
   int32_t n_layers;
   int32_t M;
-  int32_t maxMN;       // smem slot stride (cells) = max over the launch's layers
-  int32_t early_trigger;
-  int64_t in;          // in_features (shared by the batch)
+  int32_t maxMN;        // smem slot stride (cells) = M * maxN
+  int32_t piece_units;  // units per bulk copy when staging a chunk (power of two, <= TJ)
+  int32_t maxN;         // smem stride (cells) between sketch rows of a slot: 1 + max N over the
+                        // launch's units; column maxN - 1 of every row holds rho(+0) (zero column)
+  uint32_t row_bytes;   // 128 * maxN: shared byte distance between sketch rows of a slot
+  int64_t in;           // in_features (shared by the batch)
+  int64_t items;        // GEMV: total work items (chunk, subtile) of the launch
+  int64_t rows;         // GEMV: total output rows of the launch
   const void* sketch;
   const int32_t* ncols;
   const int64_t* offsets;
   const uint32_t* ukeys;
-  const uint32_t* R;
   HashConsts hc;
   const void* x;
   int32_t x_bf16;
   int32_t y_bf16;
-  unsigned long long* timeline;  // debug only (USK_TIMELINE=1): 4 globaltimer stamps per CTA
+  int32_t red_lanes;               // GEMV reduce: lanes per row (power of two <= 32)
+  int32_t cta_item[kMaxCtas + 1];  // GEMV: CTA c computes work items [cta_item[c], cta_item[c + 1])
+  unsigned long long* timeline;  // tuning only (USK_TRACE): 4 globaltimer stamps per CTA
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -100,75 +111,105 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 template <int UPL, int MT>
 struct LaneState {
-  static constexpr int MR = MT > 0 ? MT : 1;
   uint32_t K[UPL], N[UPL];
-  uint32_t rb[UPL][MR];  // shared byte address of (unit v, sketch row i, column 0) for this lane
-  uint32_t rstride[UPL]; // bytes between sketch rows (runtime-M kernels)
+  uint32_t b0[UPL];  // shared-window byte address of (unit v, sketch row 0, column 0) for this
+                     // lane; cell (i, k) is at b0 + 128 * (i * maxN + k)
 };
 
-// Stage one chunk's cells (rho codes, bank-private layout) and set up the lane state.
-template <typename E, int UPL, int MT>
-__device__ __forceinline__ void stage_chunk(const QArgs& A, const QLayer& Ly, int64_t j0, int nu, uint32_t* cells,
-                                            uint32_t* zero, LaneState<UPL, MT>& S) {
-  constexpr int TJ = 32 * UPL;
-  constexpr int ES = sizeof(E);
+// shared memory: [zero cells: 32 words][mbarrier: 2 words][copy shift: 1 word]...[cells @ word
+// kCellsWordOffset: UPL*32*maxMN words][raw bulk-copy buffer: piece_units*maxMN cells + 32 B]
+__device__ __forceinline__ uint64_t* q_bar() { return reinterpret_cast<uint64_t*>(qsm + 32); }
+
+// Lane state of a chunk [ubase, ubase + nu): K_u, N_u and the shared byte address of each of
+// the lane's units (missing units of a ragged chunk point at the zero cells: idx is always 0).
+template <int UPL, int MT>
+__device__ __forceinline__ void lane_setup(const QArgs& A, int64_t ubase, int nu, LaneState<UPL, MT>& S) {
   const int lane = threadIdx.x & 31;
-  // The chunk's units are consecutive in the sketch, so their cells are one contiguous byte range:
-  // a single TMA bulk copy (cp.async.bulk, mbarrier completion) brings it into a raw shared
-  // buffer; threads then convert shared -> shared into the bank-private rho layout.
-  uint64_t* bar = reinterpret_cast<uint64_t*>(zero + 32);
-  uint32_t* s_shift = zero + 34;
-  unsigned char* raw = reinterpret_cast<unsigned char*>(cells + UPL * 32 * A.maxMN);
-  const int64_t ubase = Ly.unit_base + j0;
-  if (threadIdx.x == 0) {
-    const uint64_t g0 = (uint64_t)A.offsets[ubase] * ES, g1 = (uint64_t)A.offsets[ubase + nu] * ES;
-    const uint64_t a0 = g0 & ~uint64_t(15), a1 = (g1 + 15) & ~uint64_t(15);
-    mbar_init(bar, 1);
-    fence_mbar_init();
-    mbar_arrive_expect_tx(bar, (uint32_t)(a1 - a0));
-    bulk_g2s(raw, reinterpret_cast<const unsigned char*>(A.sketch) + a0, (uint32_t)(a1 - a0), bar);
-    *s_shift = (uint32_t)(g0 - a0);
-  }
-  const int ul = threadIdx.x % TJ;
-  int64_t u_off = 0;
-  int mn = 0;
-  if (ul < nu) {  // overlaps the copy
-    u_off = A.offsets[ubase + ul] - A.offsets[ubase];
-    mn = A.M * A.ncols[ubase + ul];
-  }
-  if (threadIdx.x < 32) zero[threadIdx.x] = 1u;  // rho(+0)
-  __syncthreads();                                 // barrier init + shift visible
-  mbar_wait(bar, 0);
-  {
-    const unsigned char* src = raw + *s_shift + u_off * ES;
-    uint32_t* dst = cells + (ul % UPL) * 32 * A.maxMN + ul / UPL;
-    constexpr int KS = kQThreads / TJ;
-#pragma unroll 4
-    for (int k = threadIdx.x / TJ; k < mn; k += KS) {
-      const uint32_t b = ES == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
-                                 : reinterpret_cast<const uint32_t*>(src)[k];
-      dst[k * 32] = rotl1(b) ^ 1u;
-    }
-  }
-  const uint32_t cbase = (uint32_t)((cells - qsm) * 4), zbase = (uint32_t)((zero - qsm) * 4);  // byte offsets
+  const uint32_t cbase = smem_u32(qsm + kCellsWordOffset);
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
     const int ul = UPL * lane + v;
     if (ul < nu) {
-      const int64_t u = Ly.unit_base + j0 + ul;
-      S.K[v] = A.ukeys[u];
-      S.N[v] = (uint32_t)A.ncols[u];
-      const uint32_t b0 = cbase + 4u * (uint32_t)(v * 32 * A.maxMN + lane);
-      S.rstride[v] = S.N[v] * 128u;
-#pragma unroll
-      for (int i = 0; i < LaneState<UPL, MT>::MR; ++i) S.rb[v][i] = b0 + (uint32_t)i * S.rstride[v];
-    } else {
+      S.K[v] = A.ukeys[ubase + ul];
+      S.N[v] = (uint32_t)A.ncols[ubase + ul];
+      S.b0[v] = cbase + 4u * (uint32_t)(v * 32 * A.maxMN + lane);
+    } else {  // missing unit of a ragged chunk: idx is always 0 -> the zero column of every row
       S.K[v] = 0;
-      S.N[v] = 1;  // idx is always 0
-      S.rstride[v] = 0;
-#pragma unroll
-      for (int i = 0; i < LaneState<UPL, MT>::MR; ++i) S.rb[v][i] = zbase + 4u * lane;
+      S.N[v] = 1;
+      S.b0[v] = cbase + 4u * (uint32_t)((A.maxN - 1) * 32 + lane);
     }
+  }
+}
+
+template <typename E, int UPL>
+__device__ __forceinline__ unsigned char* q_raw(const QArgs& A) {
+  return reinterpret_cast<unsigned char*>(qsm + kCellsWordOffset + UPL * 32 * A.maxMN);
+}
+
+// thread 0: bulk copy of the cells of units [ubase + pa, ubase + pa + pn) into the raw buffer
+template <typename E, int UPL>
+__device__ __forceinline__ void stage_issue(const QArgs& A, int64_t ubase, int pa, int pn) {
+  constexpr int ES = sizeof(E);
+  const uint64_t g0 = (uint64_t)A.offsets[ubase + pa] * ES, g1 = (uint64_t)A.offsets[ubase + pa + pn] * ES;
+  const uint64_t a0 = g0 & ~uint64_t(15), a1 = (g1 + 15) & ~uint64_t(15);
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of raw
+  mbar_arrive_expect_tx(q_bar(), (uint32_t)(a1 - a0));
+  bulk_g2s(q_raw<E, UPL>(A), reinterpret_cast<const unsigned char*>(A.sketch) + a0, (uint32_t)(a1 - a0), q_bar());
+  qsm[34] = (uint32_t)(g0 - a0);  // copy shift
+}
+
+// Stage the cells of units [ubase, ubase + nu) (consecutive in the sketch, so contiguous bytes)
+// into the bank-private rho layout: pieces of piece_units units are brought in by one TMA bulk
+// copy each (cp.async.bulk, mbarrier completion) and converted shared -> shared.  The first
+// piece may have been issued already (first_issued; thread 0 called stage_issue).  Ends with a
+// __syncthreads (cells complete, raw buffer free).  The mbarrier phase advances once per piece.
+template <typename E, int UPL>
+__device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int nu, uint32_t& phase,
+                                            bool first_issued) {
+  constexpr int ES = sizeof(E);
+  uint32_t* cells = qsm + kCellsWordOffset;
+  const unsigned char* raw = q_raw<E, UPL>(A);
+  const int pu = A.piece_units;
+  for (int pa = 0; pa < nu; pa += pu) {
+    const int pn = min(pu, nu - pa);
+    if (threadIdx.x == 0 && !(pa == 0 && first_issued)) stage_issue<E, UPL>(A, ubase, pa, pn);
+    const int t = threadIdx.x & (pu - 1);
+    const int ul = pa + t;
+    int64_t u_off = 0;
+    int n = 0;  // N of the thread's unit (0: no unit)
+    if (t < pn) {  // overlaps the copy
+      u_off = A.offsets[ubase + ul] - A.offsets[ubase + pa];
+      n = A.ncols[ubase + ul];
+    }
+    __syncthreads();  // shift visible
+    mbar_wait(q_bar(), phase);
+    phase ^= 1u;
+    const unsigned char* src = raw + qsm[34] + u_off * ES;
+    uint32_t* dst = cells + (ul % UPL) * 32 * A.maxMN + ul / UPL;
+    const int KS = kQThreads / pu;
+    for (int i = 0; i < A.M; ++i, src += n * ES, dst += A.maxN * 32) {  // sketch row i -> slot row i
+#pragma unroll 4
+      for (int k = threadIdx.x / pu; k < n; k += KS) {
+        const uint32_t b = ES == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
+                                   : reinterpret_cast<const uint32_t*>(src)[k];
+        dst[k * 32] = rotl1(b) ^ 1u;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+// kernel prologue shared by the fast kernels: zero column of every slot row, staging mbarrier
+template <int UPL>
+__device__ __forceinline__ void q_prologue(const QArgs& A) {
+  uint32_t* cells = qsm + kCellsWordOffset;
+  for (int e = threadIdx.x; e < UPL * A.M * 32; e += kQThreads) {
+    const int lane = e & 31, vi = e >> 5, v = vi % UPL, i = vi / UPL;
+    cells[v * 32 * A.maxMN + (i * A.maxN + A.maxN - 1) * 32 + lane] = 1u;  // rho(+0)
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(q_bar(), 1);
+    fence_mbar_init();
   }
 }
 
@@ -178,29 +219,30 @@ __device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<U
                                                int64_t o) {
   const uint32_t h = Rv ^ S.K[v];
   if constexpr (MT > 0 && HASH == USK_HASH_X) {
+    // idx_i + i * maxN in one IMAD.HI (the addend), then one LEA to the shared address
     uint32_t m[MT];
 #pragma unroll
-    for (int i = 0; i < MT; ++i) m[i] = lds32(S.rb[v][i] + (__umulhi(h * A.hc.a[i], S.N[v]) << 7));
+    for (int i = 0; i < MT; ++i) m[i] = lds_at(S.b0[v] + ((__umulhi(h * A.hc.a[i], S.N[v]) + i * A.maxN) << 7));
     uint32_t best = m[0];
 #pragma unroll
     for (int i = 1; i < MT; ++i) best = max(best, m[i]);
     return best;
   } else {
-    uint32_t best = 0, base = S.rb[v][0];
+    uint32_t best = 0;
     for (int i = 0; i < A.M; ++i) {
       const uint32_t idx = (HASH == USK_HASH_X) ? __umulhi(h * A.hc.a[i], S.N[v]) : (uint32_t)(o % S.N[v]);
-      best = max(best, lds32(base + (idx << 7)));
-      base += S.rstride[v];
+      best = max(best, lds_at(S.b0[v] + ((idx + i * A.maxN) << 7)));
     }
     return best;
   }
 }
 
-// Row r of the warp's 16 partial rows ends on lanes r and r + 16 (fixed-order butterfly: 4
-// exchange-and-halve stages inside each half-warp, then the two halves are added).
-__device__ __forceinline__ float transpose_reduce16(float (&acc)[16], int lane) {
+// Row r of the warp's kSubRows partial rows ends on the lanes congruent to r mod kSubRows
+// (fixed-order butterfly: log2(kSubRows) exchange-and-halve stages inside each group of kSubRows
+// lanes, then the groups are added).
+__device__ __forceinline__ float transpose_reduce(float (&acc)[kSubRows], int lane) {
 #pragma unroll
-  for (int m = 8; m >= 1; m >>= 1) {
+  for (int m = kSubRows / 2; m >= 1; m >>= 1) {
     const bool up = (lane & m) != 0;
 #pragma unroll
     for (int i = 0; i < m; ++i) {
@@ -209,184 +251,281 @@ __device__ __forceinline__ float transpose_reduce16(float (&acc)[16], int lane) 
       acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
     }
   }
-  return acc[0] + __shfl_xor_sync(0xffffffffu, acc[0], 16);
-}
-
-// y[r] = sum over chunks (fixed order) of the row-major partials; float4 loads, all issued up front.
-__device__ __forceinline__ void reduce_row(const QArgs& A, const QLayer& Ly, int64_t r) {
-  const float4* p = reinterpret_cast<const float4*>(Ly.partial + r * Ly.CP);
-  float t = 0.f;
-  int c = 0;
-  for (; c + 32 <= Ly.n_chunks; c += 32) {
-    float4 q[8];
+  float t = acc[0];
 #pragma unroll
-    for (int k = 0; k < 8; ++k) q[k] = __ldcg(p + c / 4 + k);
-#pragma unroll
-    for (int k = 0; k < 8; ++k) t = t + q[k].x + q[k].y + q[k].z + q[k].w;
-  }
-  for (; c < Ly.n_chunks; c += 4) {
-    const float4 q = __ldcg(p + c / 4);
-    const float w4[4] = {q.x, q.y, q.z, q.w};
-    for (int k = 0; k < 4 && c + k < Ly.n_chunks; ++k) t += w4[k];
-  }
-  if (A.y_bf16) {
-    const uint32_t bb = __float_as_uint(t);
-    reinterpret_cast<uint16_t*>(Ly.y)[r] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
-  } else {
-    reinterpret_cast<float*>(Ly.y)[r] = t;
-  }
+  for (int m = kSubRows; m < 32; m <<= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+  return t;
 }
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 #ifndef USK_QUERY_MINB
-#define USK_QUERY_MINB 2
+#define USK_QUERY_MINB 1
+#endif
+#ifndef USK_GEMV_MAXREG
+#define USK_GEMV_MAXREG 112  // 512 x 112 + 256 x 32 registers: k_gemv_fast + k_gemv_reduce share an SM
 #endif
 
-template <typename E, int UPL, int MT, int HASH, bool GEMV>
-__global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_query_fast(const __grid_constant__ QArgs A) {
+// ------------------------------------------------------------------ K4: sketch-GEMV (decode)
+// Two kernels per call, chained with programmatic dependent launch (no grid barrier):
+//  * k_gemv_fast (one CTA per SM): the launch's work items (layer, chunk, subtile) are laid out
+//    chunk-major and CTA c computes the contiguous range [cta_item[c], cta_item[c+1]) -- the host
+//    balances the ranges, charging every chunk boundary inside a range for its extra staging.
+//    Warps grab the subtiles of a staged chunk dynamically; the next chunk of the range is
+//    prefetched (TMA) under the current one's math.  Chunk partials go to [rows][CP].
+//  * k_gemv_reduce: y[r] = the fixed-order sum of row r's chunk partials.  Its small CTAs fit
+//    beside k_gemv_fast's (register budget 112 + 32 per thread), wait there for the partials
+//    (griddepcontrol.wait), and the NEXT call's k_gemv_fast stages its sketch chunk while they
+//    reduce.
+template <typename E, int UPL, int MT, int HASH>
+__global__ void __maxnreg__(USK_GEMV_MAXREG) k_gemv_fast(const __grid_constant__ QArgs A) {
   constexpr int TJ = 32 * UPL;
-  uint32_t* zero = qsm;
-  uint32_t* cells = qsm + kCellsWordOffset;  // [zero: 32 words][unit offsets: 160][cells]
-  __shared__ int s_next;  // next subtile of this CTA's range (warps grab dynamically)
-  __shared__ int s_last;
+  __shared__ int s_next;  // next subtile of the current segment (warps grab dynamically)
   const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const int64_t s_begin = A.cta_item[c], s_end = A.cta_item[c + 1];
+  if (A.timeline && threadIdx.x == 0) A.timeline[c * 4 + 0] = gtimer();
+  q_prologue<UPL>(A);
+  uint32_t phase = 0;
+  bool waited = false;
+  // a segment = the part of [s_begin, s_end) inside one chunk
+  struct Seg {
+    int li, chunk, sub_a, sub_end, nu;
+    int64_t end, j0, ubase;
+  };
+  auto seg_at = [&](int64_t s) {
+    Seg g;
+    g.li = 0;
+    while (g.li + 1 < A.n_layers && A.layer[g.li + 1].item_begin <= s) ++g.li;
+    const QLayer& L = A.layer[g.li];
+    const int64_t local = s - L.item_begin;
+    g.chunk = (int)(local / L.n_sub);
+    g.sub_a = (int)(local - (int64_t)g.chunk * L.n_sub);
+    g.end = min(s_end, L.item_begin + (int64_t)(g.chunk + 1) * L.n_sub);
+    g.sub_end = g.sub_a + (int)(g.end - s);
+    g.j0 = (int64_t)g.chunk * TJ;
+    g.nu = (int)min((int64_t)TJ, A.in - g.j0);
+    g.ubase = L.unit_base + g.j0;
+    return g;
+  };
+  if (s_begin < s_end) {
+    Seg cur = seg_at(s_begin);
+    if (threadIdx.x == 0) {
+      s_next = cur.sub_a;
+      stage_issue<E, UPL>(A, cur.ubase, 0, min(A.piece_units, cur.nu));  // first piece in flight
+    }
+    bool stamped = false;
+    while (true) {
+      const QLayer& Ly = A.layer[cur.li];
+      LaneState<UPL, MT> S;
+      lane_setup<UPL, MT>(A, cur.ubase, cur.nu, S);  // overlaps the copy
+      stage_units<E, UPL>(A, cur.ubase, cur.nu, phase, true);  // sketch only: before the wait
+      if (!waited) {
+        pdl_wait();     // x may be written by the previous kernel on the stream
+        pdl_trigger();  // every CTA of this grid is running: the next launch may be scheduled
+        waited = true;
+      }
+      float nx[UPL];
+#pragma unroll
+      for (int v = 0; v < UPL; ++v) {
+        const int64_t j = cur.j0 + UPL * lane + v;
+        float xv = 0.f;
+        if (UPL * lane + v < cur.nu)
+          xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
+                        : reinterpret_cast<const float*>(A.x)[j];
+        nx[v] = -xv;  // rotr(rho) decodes to -w'
+      }
+      if (A.timeline && threadIdx.x == 0 && !stamped) A.timeline[c * 4 + 1] = gtimer();
+      stamped = true;
+      // the raw buffer is free: prefetch the next segment's first piece under this one's math
+      const bool more = cur.end < s_end;
+      Seg nxt_seg = cur;
+      if (more) {
+        nxt_seg = seg_at(cur.end);
+        if (threadIdx.x == 0) stage_issue<E, UPL>(A, nxt_seg.ubase, 0, min(A.piece_units, nxt_seg.nu));
+      }
+      const int rl = lane & (kSubRows - 1);  // lanes congruent to r mod kSubRows hold R(o0 + r)
+      auto next_sub = [&]() -> int {
+        int g = 0;
+        if (lane == 0) g = atomicAdd(&s_next, 1);
+        return __shfl_sync(0xffffffffu, g, 0);
+      };
+      const int sub_end = cur.sub_end;
+      const int chunk = cur.chunk;
+      int sub = next_sub();
+      uint32_t Rl = 0;
+      // R(o) = fmix32(o ^ rho): lane r computes its own row's mix; SHFL broadcasts it row by row
+      if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
+      while (sub < sub_end) {
+        const int nxt = next_sub();  // issued now, consumed after this subtile's math
+        const int64_t r0 = (int64_t)sub * kSubRows;
+        const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
+        float acc[kSubRows];
+#pragma unroll
+        for (int r = 0; r < kSubRows; ++r) {
+          const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
+          float a = 0.f;
+#pragma unroll
+          for (int v = 0; v < UPL; ++v)
+            a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r))), a);
+          acc[r] = a;
+        }
+        const float t = transpose_reduce(acc, lane);
+        if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = t;
+        sub = nxt;
+        if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
+      }
+      __syncthreads();  // cells and s_next are reused by the next segment
+      if (!more) break;
+      cur = nxt_seg;
+      if (threadIdx.x == 0) s_next = cur.sub_a;
+    }
+  }
+  if (!waited) {
+    pdl_wait();
+    pdl_trigger();
+  }
+  if (A.timeline && lane == 0) {
+    atomicMax(&A.timeline[c * 4 + 2], gtimer());
+    atomicMax(&A.timeline[c * 4 + 3], gtimer());
+  }
+}
 
+constexpr int kRedThreads = 256;
+
+// y[r] = sum of row r's chunk partials in a fixed order: a group of red_lanes (power of two)
+// lanes per row; lane j sums chunks [4j, 4j + 4) of every 4*red_lanes-chunk stride with one
+// coalesced float4 load each, then an xor butterfly over the group (every lane ends with the same
+// bits, so the result is deterministic).
+__global__ void __launch_bounds__(kRedThreads, 8) k_gemv_reduce(const __grid_constant__ QArgs A) {
+  if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 0] = gtimer();
+  pdl_trigger();  // the next call's compute kernel may be scheduled (it stages before its own wait)
+  pdl_wait();     // all chunk partials written
+  if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 1] = gtimer();
+  const int L = A.red_lanes;
+  const int64_t g = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
+  const int64_t r = g / L;
+  const int j = (int)(g % L);
+  float t = 0.f;
+  int li = 0;
+  if (r < A.rows) {
+    while (li + 1 < A.n_layers && A.layer[li + 1].row_begin <= r) ++li;
+    const QLayer& Ly = A.layer[li];
+    const float4* p = reinterpret_cast<const float4*>(Ly.partial + (r - Ly.row_begin) * Ly.CP);
+    for (int c = 4 * j; c < Ly.n_chunks; c += 4 * L) {
+      const float4 q = __ldcg(p + c / 4);
+      t += q.x;
+      if (c + 1 < Ly.n_chunks) t += q.y;
+      if (c + 2 < Ly.n_chunks) t += q.z;
+      if (c + 3 < Ly.n_chunks) t += q.w;
+    }
+  }
+  for (int m = 1; m < L; m <<= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+  if (r < A.rows && j == 0) {
+    const QLayer& Ly = A.layer[li];
+    const int64_t rr = r - Ly.row_begin;
+    if (A.y_bf16) {
+      const uint32_t bb = __float_as_uint(t);
+      reinterpret_cast<uint16_t*>(Ly.y)[rr] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
+    } else {
+      reinterpret_cast<float*>(Ly.y)[rr] = t;
+    }
+  }
+  if (A.timeline && (threadIdx.x & 31) == 0) {
+    atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
+    atomicMax(&A.timeline[blockIdx.x * 4 + 3], gtimer());
+  }
+}
+
+// ------------------------------------------------------------------ K3: reconstruct (fast path)
+// The layer's cpc CTAs are spread over its chunks as evenly as possible; each chunk's CTAs split
+// its subtiles evenly (static); warps grab subtiles dynamically.  W' rows are written with
+// vector stores (bf16: 4 units per lane -> one 8-byte store).
+template <typename E, int UPL, int MT, int HASH>
+__global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_recon_fast(const __grid_constant__ QArgs A) {
+  constexpr int TJ = 32 * UPL;
+  __shared__ int s_next;
+  const int lane = threadIdx.x & 31;
   int li = 0;
   while (li + 1 < A.n_layers && A.layer[li + 1].cta_begin <= (int)blockIdx.x) ++li;
   const QLayer& Ly = A.layer[li];
   const int b = blockIdx.x - Ly.cta_begin;
-  int chunk, part = 0, sub0 = 0, sub1 = 0;
-  if constexpr (GEMV) {
-    // cpc CTAs per chunk; every chunk uses the same row partition (part q covers subtiles
-    // [q n_sub / cpc, (q+1) n_sub / cpc)), so one counter per part collects the chunks
-    chunk = b / Ly.cpc;
-    part = b % Ly.cpc;
-    sub0 = (int)(((int64_t)part * Ly.n_sub) / Ly.cpc);
-    sub1 = (int)(((int64_t)(part + 1) * Ly.n_sub) / Ly.cpc);
-  } else {
-    // the layer's cpc CTAs are spread over its chunks as evenly as possible; each chunk's CTAs
-    // split its subtiles evenly (static)
-    chunk = (int)(((int64_t)b * Ly.n_chunks) / Ly.cpc);
-    const int first = (int)(((int64_t)chunk * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks);
-    const int nparts = (int)((((int64_t)(chunk + 1) * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks) - first);
-    part = b - first;
-    sub0 = (int)(((int64_t)part * Ly.n_sub) / nparts);
-    sub1 = (int)(((int64_t)(part + 1) * Ly.n_sub) / nparts);
-  }
+  const int chunk = (int)(((int64_t)b * Ly.n_chunks) / Ly.cpc);
+  const int first = (int)(((int64_t)chunk * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks);
+  const int nparts = (int)((((int64_t)(chunk + 1) * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks) - first);
+  const int part = b - first;
+  const int sub0 = (int)(((int64_t)part * Ly.n_sub) / nparts);
+  const int sub_end = (int)(((int64_t)(part + 1) * Ly.n_sub) / nparts);
   const int64_t j0 = (int64_t)chunk * TJ;
   const int nu = (int)min((int64_t)TJ, A.in - j0);
 
   if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 0] = gtimer();
+  q_prologue<UPL>(A);
+  if (threadIdx.x == 0) s_next = sub0;
   LaneState<UPL, MT> S;
-  stage_chunk<E, UPL, MT>(A, Ly, j0, nu, cells, zero, S);
-  float nx[UPL];
-  if constexpr (GEMV) {
-    pdl_wait();  // x may be written by the previous kernel on the stream
-    if (A.early_trigger) pdl_trigger();
-#pragma unroll
-    for (int v = 0; v < UPL; ++v) {
-      const int64_t j = j0 + UPL * lane + v;
-      float xv = 0.f;
-      if (UPL * lane + v < nu)
-        xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
-                      : reinterpret_cast<const float*>(A.x)[j];
-      nx[v] = -xv;  // rotr(rho) decodes to -w'
-    }
-  }
-  if (threadIdx.x == 0) s_next = sub0 + 0;
-  __syncthreads();
+  lane_setup<UPL, MT>(A, Ly.unit_base + j0, nu, S);
+  uint32_t phase = 0;
+  stage_units<E, UPL>(A, Ly.unit_base + j0, nu, phase, false);
   if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 1] = gtimer();
 
-  const int rl = lane & (kSubRows - 1);  // lanes r and r + 16 both hold R(o0 + r)
+  const int rl = lane & (kSubRows - 1);
   auto next_sub = [&]() -> int {
     int g = 0;
     if (lane == 0) g = atomicAdd(&s_next, 1);
     return __shfl_sync(0xffffffffu, g, 0);
   };
-  const int sub_end = sub1;
   int sub = next_sub();
   uint32_t Rl = 0;
-  // R(o) = fmix32(o ^ rho): lane r computes its own row's mix (6 integer ops per subtile and
-  // lane, no memory access); SHFL broadcasts it row by row
   if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
+  const bool full_tile = (nu == TJ);
   while (sub < sub_end) {
-    const int nxt = next_sub();  // issued now, consumed after this subtile's math
-    const int64_t r0 = (int64_t)sub * kSubRows;  // first local row of the subtile
+    const int nxt = next_sub();
+    const int64_t r0 = (int64_t)sub * kSubRows;
     const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
-    if constexpr (GEMV) {
-      float acc[kSubRows];
-#pragma unroll
-      for (int r = 0; r < kSubRows; ++r) {
-        const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
-        float a = 0.f;
-#pragma unroll
-        for (int v = 0; v < UPL; ++v)
-          a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r))), a);
-        acc[r] = a;
-      }
-      const float s = transpose_reduce16(acc, lane);
-      if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = s;
-    } else {
-      const bool full_tile = (nu == TJ);
-      E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + j0 + UPL * lane;
+    E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + j0 + UPL * lane;
 #pragma unroll 4
-      for (int r = 0; r < kSubRows; ++r, dst += Ly.ld_out) {
-        const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
-        if (r >= nrow) continue;
-        uint32_t wb[UPL];
+    for (int r = 0; r < kSubRows; ++r, dst += Ly.ld_out) {
+      const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
+      if (r >= nrow) continue;
+      uint32_t wb[UPL];
 #pragma unroll
-        for (int v = 0; v < UPL; ++v)
-          wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r)) ^ 0x80000000u;
-        if constexpr (sizeof(E) == 2) {
-          if (full_tile) {
-            if constexpr (UPL == 4) {
-              *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(wb[0], wb[1 % UPL], 0x7632),
-                                                          __byte_perm(wb[2 % UPL], wb[3 % UPL], 0x7632));
-            } else if constexpr (UPL == 2) {
-              *reinterpret_cast<uint32_t*>(dst) = __byte_perm(wb[0], wb[1 % UPL], 0x7632);
-            } else {
-              dst[0] = (E)(wb[0] >> 16);
-            }
+      for (int v = 0; v < UPL; ++v)
+        wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r)) ^ 0x80000000u;
+      if constexpr (sizeof(E) == 2) {
+        if (full_tile) {
+          if constexpr (UPL == 4) {
+            *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(wb[0], wb[1 % UPL], 0x7632),
+                                                        __byte_perm(wb[2 % UPL], wb[3 % UPL], 0x7632));
+          } else if constexpr (UPL == 2) {
+            *reinterpret_cast<uint32_t*>(dst) = __byte_perm(wb[0], wb[1 % UPL], 0x7632);
           } else {
-#pragma unroll
-            for (int v = 0; v < UPL; ++v)
-              if (UPL * lane + v < nu) dst[v] = (E)(wb[v] >> 16);
+            dst[0] = (E)(wb[0] >> 16);
           }
         } else {
-          if (full_tile && UPL == 4) {
-            *reinterpret_cast<uint4*>(dst) = make_uint4(wb[0], wb[1 % UPL], wb[2 % UPL], wb[3 % UPL]);
-          } else if (full_tile && UPL == 2) {
-            *reinterpret_cast<uint2*>(dst) = make_uint2(wb[0], wb[1 % UPL]);
-          } else {
 #pragma unroll
-            for (int v = 0; v < UPL; ++v)
-              if (UPL * lane + v < nu) dst[v] = wb[v];
-          }
+          for (int v = 0; v < UPL; ++v)
+            if (UPL * lane + v < nu) dst[v] = (E)(wb[v] >> 16);
+        }
+      } else {
+        if (full_tile && UPL == 4) {
+          *reinterpret_cast<uint4*>(dst) = make_uint4(wb[0], wb[1 % UPL], wb[2 % UPL], wb[3 % UPL]);
+        } else if (full_tile && UPL == 2) {
+          *reinterpret_cast<uint2*>(dst) = make_uint2(wb[0], wb[1 % UPL]);
+        } else {
+#pragma unroll
+          for (int v = 0; v < UPL; ++v)
+            if (UPL * lane + v < nu) dst[v] = wb[v];
         }
       }
     }
     sub = nxt;
     if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
   }
-  if (A.timeline && lane == 0) atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
-  if constexpr (GEMV) {
-    // ---- split-K: one release per CTA; the CTA that completes row part `part` (the n_chunks-th
-    // arrival) sums its rows' chunk partials in fixed chunk order and writes y
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(&Ly.counters[part], 1u) == (uint32_t)Ly.n_chunks - 1);
-    __syncthreads();
-    if (!A.early_trigger) pdl_trigger();
-    if (s_last) {
-      __threadfence();
-      const int64_t ra = (int64_t)sub0 * kSubRows, rb = min((int64_t)sub1 * kSubRows, Ly.rows);
-      for (int64_t r = ra + threadIdx.x; r < rb; r += kQThreads) reduce_row(A, Ly, r);
-      if (threadIdx.x == 0) Ly.counters[part] = 0u;  // leave the workspace zeroed for the next call
-    }
+  if (A.timeline && lane == 0) {
+    atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
+    atomicMax(&A.timeline[blockIdx.x * 4 + 3], gtimer());
   }
-  if (A.timeline && lane == 0) atomicMax(&A.timeline[blockIdx.x * 4 + 3], gtimer());
 }
 
 // ------------------------------------------------------------------ generic query path
@@ -470,19 +609,29 @@ bool fast_eligible(const usk_plan* pl) { return pl->gran == USK_GRAN_ROW && pl->
 
 constexpr size_t kSmemMax = 220 * 1024;
 
-// [zero + mbarrier + unit slots][rho cells][raw chunk bytes of the bulk copy (+ alignment slack)]
-size_t smem_bytes(int upl, int maxMN, int es) {
-  return kCellsWordOffset * 4 + (size_t)32 * upl * maxMN * 4 + (size_t)32 * upl * maxMN * es + 48;
+// [zero + mbarrier + shift][rho cells][raw bulk-copy buffer for `pu` units (+ alignment slack)]
+size_t smem_bytes(int upl, int maxMN, int es, int pu) {
+  return kCellsWordOffset * 4 + (size_t)32 * upl * maxMN * 4 + (size_t)pu * maxMN * es + 48;
 }
 
 template <typename E, int UPL, bool GEMV>
 void* pick_m(int M, int hash) {
-  if (hash == USK_HASH_IDENTITY) return (void*)k_query_fast<E, UPL, 0, USK_HASH_IDENTITY, GEMV>;
-  switch (M) {
-    case 1: return (void*)k_query_fast<E, UPL, 1, USK_HASH_X, GEMV>;
-    case 2: return (void*)k_query_fast<E, UPL, 2, USK_HASH_X, GEMV>;
-    case 3: return (void*)k_query_fast<E, UPL, 3, USK_HASH_X, GEMV>;
-    default: return (void*)k_query_fast<E, UPL, 0, USK_HASH_X, GEMV>;
+  if constexpr (GEMV) {
+    if (hash == USK_HASH_IDENTITY) return (void*)k_gemv_fast<E, UPL, 0, USK_HASH_IDENTITY>;
+    switch (M) {
+      case 1: return (void*)k_gemv_fast<E, UPL, 1, USK_HASH_X>;
+      case 2: return (void*)k_gemv_fast<E, UPL, 2, USK_HASH_X>;
+      case 3: return (void*)k_gemv_fast<E, UPL, 3, USK_HASH_X>;
+      default: return (void*)k_gemv_fast<E, UPL, 0, USK_HASH_X>;
+    }
+  } else {
+    if (hash == USK_HASH_IDENTITY) return (void*)k_recon_fast<E, UPL, 0, USK_HASH_IDENTITY>;
+    switch (M) {
+      case 1: return (void*)k_recon_fast<E, UPL, 1, USK_HASH_X>;
+      case 2: return (void*)k_recon_fast<E, UPL, 2, USK_HASH_X>;
+      case 3: return (void*)k_recon_fast<E, UPL, 3, USK_HASH_X>;
+      default: return (void*)k_recon_fast<E, UPL, 0, USK_HASH_X>;
+    }
   }
 }
 
@@ -523,113 +672,198 @@ int occupancy(void* kern, size_t smem) {
   if (std::find(raised.begin(), raised.end(), kern) == raised.end()) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax) != cudaSuccess) {
       (void)cudaGetLastError();
-      return 1;
+      return 0;
     }
     raised.push_back(kern);
   }
-  int occ = 1;
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQThreads, smem) != cudaSuccess || occ < 1) {
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQThreads, smem) != cudaSuccess) {
     (void)cudaGetLastError();
-    occ = 1;
+    occ = 0;
   }
   cache.push_back({{kern, smem}, occ});
   return occ;
 }
 
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
 struct Geom {
   int upl = 0;
   int maxMN = 0;
+  int pu = 0;  // units per staging bulk copy
   size_t smem = 0;
   int grid = 0;
-  bool one_wave = false;
   void* kern = nullptr;
+  int64_t items = 0;
   std::vector<int> n_chunks, n_sub, cpc;
 };
 
-// Units per lane: the largest UPL whose chunks all get a resident CTA (larger UPL amortises the
-// per-row R broadcast and the 32-row transpose over more weights).  USK_UPL overrides (tuning).
-Geom geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n, bool gemv) {
+// GEMV geometry.  Units per lane: the largest UPL whose CTA fits the shared-memory budget
+// (default 176 KB: leaves room on the SM for a 49 KB CTA of the next launch, which then stages
+// its chunk while this one computes); the raw staging buffer shrinks to pieces of pu units
+// before UPL does.  Grid: one CTA per SM (USK_GEMV_CPS per SM for tuning), never more than one
+// resident wave (the kernel's grid barrier relies on it) nor more than the work items.
+// USK_UPL / USK_GEMV_SMEM_KB / USK_GEMV_CPS override (tuning).
+Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n) {
   Geom G;
-  for (int k = 0; k < n; ++k) G.maxMN = std::max(G.maxMN, pl->M * pl->layers[layers[k]].max_ncols);
+  for (int k = 0; k < n; ++k) G.maxMN = std::max(G.maxMN, pl->M * (pl->layers[layers[k]].max_ncols + 1));
   const int64_t in = pl->layers[layers[0]].in;
   const bool bf16 = pl->dtype == USK_BF16;
-  static const int forced = [] {
-    const char* e = std::getenv("USK_UPL");
-    return e ? std::atoi(e) : 0;
-  }();
-  int best = 0, best_cap = 0;
-  for (int upl : {4, 2, 1}) {
-    if (forced && upl != forced) continue;
-    const size_t sm = smem_bytes(upl, G.maxMN, pl->cell_bytes());
-    if (sm > kSmemMax) continue;
-    void* kern = pick_fast(upl, gemv, bf16, pl->M, pl->hash);
-    const int cap = sm_count() * occupancy(kern, sm);
-    int chunks = 0;
-    for (int k = 0; k < n; ++k) chunks += (int)((in + 32 * upl - 1) / (32 * upl));
-    best = upl;
-    best_cap = cap;
-    G.kern = kern;
-    if (chunks <= cap) break;
-  }
-  if (!best) return G;
-  G.upl = best;
-  G.smem = smem_bytes(best, G.maxMN, pl->cell_bytes());
-  int chunks = 0;
-  for (int k = 0; k < n; ++k) {
-    G.n_chunks.push_back((int)((in + 32 * best - 1) / (32 * best)));
-    G.n_sub.push_back((int)((rows[k] + kSubRows - 1) / kSubRows));
-    chunks += G.n_chunks.back();
-  }
-  // CTAs per layer ("cpc" = the layer's CTA count): one resident wave shared in proportion to
-  // the layers' weights, at least one CTA per chunk and at most one per (chunk, subtile)
-  double wsum = 0;
-  for (int k = 0; k < n; ++k) wsum += (double)rows[k] * in;
-  for (int k = 0; k < n; ++k) {
-    const int share = (int)((double)best_cap * (double)rows[k] * in / std::max(wsum, 1.0));
-    if (gemv) {  // cpc = CTAs per chunk (equal for every chunk; warps then balance dynamically)
-      G.cpc.push_back(std::max(1, std::min(share / G.n_chunks[k], G.n_sub[k])));
-      G.grid += G.cpc[k] * G.n_chunks[k];
-    } else {     // cpc = CTAs of the layer, spread over its chunks
-      G.cpc.push_back(std::max(G.n_chunks[k], std::min(share, G.n_chunks[k] * G.n_sub[k])));
-      G.grid += G.cpc[k];
+  const int es = pl->cell_bytes();
+  static const int forced = env_int("USK_UPL", 0);
+  static const size_t budget = (size_t)env_int("USK_GEMV_SMEM_KB", 192) * 1024;
+  static const int cps = std::max(1, env_int("USK_GEMV_CPS", 1));
+  for (int pass = 0; pass < 2 && !G.upl; ++pass) {  // pass 1: any fit below the hardware limit
+    const size_t cap = pass == 0 ? std::min(budget, kSmemMax) : kSmemMax;
+    for (int upl : {4, 2, 1}) {
+      if (forced && upl != forced) continue;
+      for (int pu = 32 * upl; pu >= 8; pu /= 2) {
+        const size_t sm = smem_bytes(upl, G.maxMN, es, pu);
+        if (sm > cap) continue;
+        void* kern = pick_fast(upl, true, bf16, pl->M, pl->hash);
+        const int occ = occupancy(kern, sm);
+        if (occ < 1) continue;
+        G.upl = upl;
+        G.pu = pu;
+        G.smem = sm;
+        G.kern = kern;
+        G.grid = sm_count() * std::min(occ, cps);
+        break;
+      }
+      if (G.upl) break;
     }
   }
-  G.one_wave = G.grid <= best_cap;
+  if (!G.upl) return G;
+  for (int k = 0; k < n; ++k) {
+    G.n_chunks.push_back((int)((in + 32 * G.upl - 1) / (32 * G.upl)));
+    G.n_sub.push_back((int)((rows[k] + kSubRows - 1) / kSubRows));
+    G.items += (int64_t)G.n_chunks.back() * G.n_sub.back();
+  }
+  G.grid = (int)std::min<int64_t>(G.grid, std::max<int64_t>(G.items, 1));
+  return G;
+}
+
+// Reconstruct geometry: the largest UPL whose chunks all get a resident CTA (larger UPL amortises
+// the per-row R broadcast over more weights); CTAs per layer in proportion to its weights.
+Geom recon_geometry(const usk_plan* pl, int32_t layer, int64_t rows) {
+  Geom G;
+  G.maxMN = pl->M * (pl->layers[layer].max_ncols + 1);
+  const int64_t in = pl->layers[layer].in;
+  const bool bf16 = pl->dtype == USK_BF16;
+  static const int forced = env_int("USK_UPL", 0);
+  int cap = 0;
+  for (int upl : {4, 2, 1}) {
+    if (forced && upl != forced) continue;
+    const size_t sm = smem_bytes(upl, G.maxMN, pl->cell_bytes(), 32 * upl);
+    if (sm > kSmemMax) continue;
+    void* kern = pick_fast(upl, false, bf16, pl->M, pl->hash);
+    const int occ = occupancy(kern, sm);
+    if (occ < 1) continue;
+    G.upl = upl;
+    G.pu = 32 * upl;
+    G.smem = sm;
+    G.kern = kern;
+    cap = sm_count() * occ;
+    if ((in + 32 * upl - 1) / (32 * upl) <= cap) break;
+  }
+  if (!G.upl) return G;
+  G.n_chunks.push_back((int)((in + 32 * G.upl - 1) / (32 * G.upl)));
+  G.n_sub.push_back((int)((rows + kSubRows - 1) / kSubRows));
+  G.cpc.push_back(std::max(G.n_chunks[0], std::min(cap, G.n_chunks[0] * G.n_sub[0])));
+  G.grid = G.cpc[0];
   return G;
 }
 
 int partial_stride(int64_t in) { return (int)((((in + 31) / 32) + 3) / 4 * 4); }
 
-// per layer: [partials rows x CP floats][split-K counters per subtile][work counters 2 x chunks]
-size_t layer_ws_counters_off(int64_t in, int64_t rows) {
-  return ((size_t)rows * partial_stride(in) * 4 + 255) / 256 * 256;
-}
-size_t layer_ws_work_off(int64_t in, int64_t rows) {
-  return layer_ws_counters_off(in, rows) + ((size_t)((rows + kSubRows - 1) / kSubRows) * 4 + 255) / 256 * 256;
-}
-size_t layer_ws_bytes(int64_t in, int64_t rows) {
-  return layer_ws_work_off(in, rows) + ((size_t)2 * ((in + 31) / 32) * 4 + 255) / 256 * 256;
-}
+// per layer: [partials rows x CP floats][256 B control: grid-barrier counters]
+size_t layer_ws_ctrl_off(int64_t in, int64_t rows) { return ((size_t)rows * partial_stride(in) * 4 + 255) / 256 * 256; }
+size_t layer_ws_bytes(int64_t in, int64_t rows) { return layer_ws_ctrl_off(in, rows) + 256; }
 
 QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& G) {
   QArgs A{};
   A.M = pl->M;
   A.maxMN = G.maxMN;
+  A.maxN = G.maxMN / pl->M;
+  A.row_bytes = 128u * (uint32_t)A.maxN;
+  A.piece_units = G.pu;
   A.in = in;
   A.sketch = sketch;
   A.ncols = pl->d_ncols;
   A.offsets = pl->d_offsets;
   A.ukeys = pl->d_keys;
-  A.R = pl->d_R;
   A.hc = pl->hc;
-  A.early_trigger = G.one_wave ? 1 : 0;
   return A;
 }
 
-usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl, cudaStream_t st) {
+// Balanced CTA item ranges for k_gemv_fast.  Every chunk boundary inside a CTA's range costs P
+// items of time (one more chunk staging + warp drain): P = 8 + (slot cells per chunk) / 1024
+// items (fitted to the in-graph traces: ~40 for Llama-1B gate|up chunks, ~16 for the 2048-row
+// layers; USK_SWITCH_ITEMS overrides).  Minimises the largest per-CTA cost over at most
+// `G.grid` CTAs (binary search on the bound, greedy fill).  Fills A.cta_item, returns the grid.
+int partition_items(QArgs& A, const Geom& G) {
+  const int64_t I = A.items;
+  const int cap = (int)std::min<int64_t>(std::min<int64_t>(G.grid, I), kMaxCtas);
+  static const int forced_p = env_int("USK_SWITCH_ITEMS", -1);
+  const int64_t P = forced_p >= 0 ? forced_p : 8 + (int64_t)32 * G.upl * G.maxMN / 1024;
+  auto chunk_end = [&](int64_t s) {
+    int li = 0;
+    while (li + 1 < A.n_layers && A.layer[li + 1].item_begin <= s) ++li;
+    const QLayer& L = A.layer[li];
+    return L.item_begin + ((s - L.item_begin) / L.n_sub + 1) * L.n_sub;
+  };
+  auto fill = [&](int64_t T, bool write) -> int {  // CTAs used (cap + 1: infeasible)
+    int64_t pos = 0;
+    int c = 0;
+    while (pos < I) {
+      if (c >= cap) return cap + 1;
+      if (write) A.cta_item[c] = (int32_t)pos;
+      int64_t budget = T, cur = pos;
+      for (bool first = true; cur < I; first = false) {
+        if (!first && (budget -= P) <= 0) break;
+        const int64_t take = std::min(chunk_end(cur) - cur, budget);
+        cur += take;
+        budget -= take;
+        if (budget <= 0) break;
+      }
+      pos = cur;
+      ++c;
+    }
+    if (write) A.cta_item[c] = (int32_t)I;
+    return c;
+  };
+  int64_t lo = (I + cap - 1) / cap, hi = lo;
+  while (fill(hi, false) > cap) hi *= 2;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (fill(mid, false) <= cap) hi = mid;
+    else lo = mid + 1;
+  }
+  return fill(lo, true);
+}
+
+// USK_TRACE (tuning only): per-CTA %globaltimer stamps of every query launch, slot per issue
+struct Trace {
+  static constexpr int64_t kCap = 1 << 18;  // CTAs
+  std::mutex mu;
+  bool on = std::getenv("USK_TRACE") != nullptr;
+  unsigned long long* d = nullptr;
+  int64_t cursor = 0;
+  std::vector<int> grids;
+};
+Trace& trace() {
+  static Trace T;
+  return T;
+}
+
+usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl, cudaStream_t st,
+                    int threads = kQThreads) {
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
-  cfg.blockDim = dim3(kQThreads);
+  cfg.blockDim = dim3(threads);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -637,46 +871,23 @@ usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl,
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = pdl ? 1 : 0;
-  static const bool timeline = std::getenv("USK_TIMELINE") != nullptr;  // debug / tuning only
-  if (timeline) {
-    static unsigned long long* dbuf = nullptr;
-    if (!dbuf) USK_CUDA(cudaMalloc(&dbuf, sizeof(unsigned long long) * 4 * 8192));
-    QArgs B = A;
-    B.timeline = dbuf;
-    USK_CUDA(cudaMemsetAsync(dbuf, 0, sizeof(unsigned long long) * 4 * grid, st));
-    void* args[] = {&B};
-    USK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
-    std::vector<unsigned long long> h(4 * (size_t)grid);
-    USK_CUDA(cudaMemcpyAsync(h.data(), dbuf, h.size() * 8, cudaMemcpyDeviceToHost, st));
-    USK_CUDA(cudaStreamSynchronize(st));
-    unsigned long long t0 = ~0ull, tend = 0;
-    double stage = 0, comp = 0, tail = 0, last_comp = 0;
-    for (int b = 0; b < grid; ++b) {
-      t0 = std::min(t0, h[4 * b]);
-      tend = std::max(tend, h[4 * b + 3]);
+  QArgs B = A;
+  {
+    Trace& T = trace();
+    std::lock_guard<std::mutex> lock(T.mu);
+    if (T.on) {  // tuning only: stamps into this launch's slot of the ring
+      if (!T.d) {
+        USK_CUDA(cudaMalloc(&T.d, sizeof(unsigned long long) * 4 * Trace::kCap));
+        USK_CUDA(cudaMemset(T.d, 0, sizeof(unsigned long long) * 4 * Trace::kCap));
+      }
+      if (T.cursor + grid > Trace::kCap) T.cursor = 0, T.grids.clear();
+      B.timeline = T.d + 4 * T.cursor;
+      T.cursor += grid;
+      T.grids.push_back(grid);
     }
-    for (int b = 0; b < grid; ++b) {
-      stage += (double)(h[4 * b + 1] - h[4 * b]);
-      comp += (double)(h[4 * b + 2] - h[4 * b + 1]);
-      tail += (double)(h[4 * b + 3] - h[4 * b + 2]);
-      last_comp = std::max(last_comp, (double)(h[4 * b + 2] - t0));
-    }
-    double skew = 0, cmin = 1e30, cmax = 0, smax = 0;
-    for (int b = 0; b < grid; ++b) {
-      skew = std::max(skew, (double)(h[4 * b] - t0));
-      cmin = std::min(cmin, (double)(h[4 * b + 2] - h[4 * b + 1]));
-      cmax = std::max(cmax, (double)(h[4 * b + 2] - h[4 * b + 1]));
-      smax = std::max(smax, (double)(h[4 * b + 1] - h[4 * b]));
-    }
-    std::fprintf(stderr,
-                 "[usk timeline] grid=%d span=%.2fus start_skew_max=%.2fus stage mean/max=%.2f/%.2fus compute "
-                 "mean/min/max=%.2f/%.2f/%.2fus tail=%.2fus last_compute_end=%.2fus\n",
-                 grid, (tend - t0) / 1e3, skew / 1e3, stage / grid / 1e3, smax / 1e3, comp / grid / 1e3, cmin / 1e3,
-                 cmax / 1e3, tail / grid / 1e3, last_comp / 1e3);
-  } else {
-    void* args[] = {const_cast<QArgs*>(&A)};
-    USK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
   }
+  void* args[] = {&B};
+  USK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
   count_launch();
   return USK_OK;
 }
@@ -719,7 +930,7 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
                              void* ws, cudaStream_t st) {
   std::vector<int64_t> rows(n);
   for (int k = 0; k < n; ++k) rows[k] = o1[k] - o0[k];
-  Geom G = fast_eligible(pl) ? geometry(pl, layers, rows.data(), n, true) : Geom{};
+  Geom G = fast_eligible(pl) ? gemv_geometry(pl, layers, rows.data(), n) : Geom{};
   if (G.upl) {
     const int64_t in = pl->layers[layers[0]].in;
     QArgs A = base_args(pl, sketch, in, G);
@@ -727,29 +938,38 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
     A.x_bf16 = x_dtype == USK_BF16;
     A.y_bf16 = y_dtype == USK_BF16;
     char* w = reinterpret_cast<char*>(ws);
-    int cta = 0;
     for (int k = 0; k < n; ++k) {
-      const size_t wsb = layer_ws_bytes(in, rows[k]);
       if (rows[k] > 0) {
         QLayer& Ly = A.layer[A.n_layers++];
         Ly.unit_base = pl->layers[layers[k]].unit_begin;
         Ly.o_begin = o0[k];
         Ly.rows = rows[k];
+        Ly.item_begin = A.items;
+        Ly.row_begin = A.rows;
         Ly.n_chunks = G.n_chunks[k];
         Ly.n_sub = G.n_sub[k];
-        Ly.cpc = G.cpc[k];
-        Ly.cta_begin = cta;
         Ly.CP = partial_stride(in);
-        cta += Ly.cpc * Ly.n_chunks;
         Ly.y = y[k];
         Ly.partial = reinterpret_cast<float*>(w);
-        Ly.counters = reinterpret_cast<uint32_t*>(w + layer_ws_counters_off(in, rows[k]));
-        Ly.work = reinterpret_cast<uint32_t*>(w + layer_ws_work_off(in, rows[k]));
+        A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
+        A.rows += rows[k];
       }
-      w += wsb;
+      w += layer_ws_bytes(in, rows[k]);
     }
     if (!A.n_layers) return USK_OK;
-    return launch_q(G.kern, A, cta, G.smem, true, st);
+    const int grid = partition_items(A, G);
+    A.red_lanes = 1;
+    while (A.red_lanes < 32 && 4 * A.red_lanes < G.n_chunks[0]) A.red_lanes *= 2;
+    usk_status s1 = launch_q(G.kern, A, grid, G.smem, true, st);
+    if (s1 != USK_OK) return s1;
+    static const bool carveout = [] {  // co-reside with k_gemv_fast's max-shared configuration
+      (void)cudaFuncSetAttribute((void*)k_gemv_reduce, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+      (void)cudaGetLastError();
+      return true;
+    }();
+    (void)carveout;
+    return launch_q((void*)k_gemv_reduce, A, (int)((A.rows * A.red_lanes + kRedThreads - 1) / kRedThreads), 0, true,
+                    st, kRedThreads);
   }
   for (int k = 0; k < n; ++k) {
     if (rows[k] == 0) continue;
@@ -775,7 +995,7 @@ usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l,
   if (rows == 0) return USK_OK;
   const int es = pl->cell_bytes();
   const bool aligned = ((ld * es) % 16 == 0) && (reinterpret_cast<uintptr_t>(w_out) % 16 == 0);
-  Geom G = (fast_eligible(pl) && aligned) ? geometry(pl, &l, &rows, 1, false) : Geom{};
+  Geom G = (fast_eligible(pl) && aligned) ? recon_geometry(pl, l, rows) : Geom{};
   if (G.upl) {
     QArgs A = base_args(pl, sketch, L.in, G);
     QLayer& Ly = A.layer[A.n_layers++];
@@ -804,3 +1024,27 @@ usk_status launch_importance(const void* A, int32_t a_dtype, int64_t N, int64_t 
 }
 
 }  // namespace usk
+
+extern "C" {
+
+int32_t usk_trace_read(uint64_t* stamps, int64_t cap_stamps, int32_t* grids, int32_t cap_launches) {
+  usk::Trace& T = usk::trace();
+  std::lock_guard<std::mutex> lock(T.mu);
+  if (!T.on || !T.d) return 0;
+  if (cudaDeviceSynchronize() != cudaSuccess) return 0;
+  const int64_t n = std::min<int64_t>(4 * T.cursor, cap_stamps);
+  if (stamps && n > 0 && cudaMemcpy(stamps, T.d, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
+  const int32_t nl = (int32_t)T.grids.size();
+  for (int32_t k = 0; grids && k < std::min(nl, cap_launches); ++k) grids[k] = T.grids[k];
+  return nl;
+}
+
+void usk_trace_reset(void) {
+  usk::Trace& T = usk::trace();
+  std::lock_guard<std::mutex> lock(T.mu);
+  T.cursor = 0;
+  T.grids.clear();
+  if (T.d) (void)cudaMemset(T.d, 0, sizeof(unsigned long long) * 4 * usk::Trace::kCap);
+}
+
+}  // extern "C"

@@ -77,6 +77,8 @@ def _load():
         "usk_status_string": (ct.c_char_p, [i32]),
         "usk_last_error": (ct.c_char_p, []),
         "usk_launch_count": (i64, [i32]),
+        "usk_trace_read": (i32, [p, i64, p, i32]),
+        "usk_trace_reset": (None, []),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -260,3 +262,21 @@ def check(plan: Plan, stream=None):
 
 def launch_count(reset: bool = False) -> int:
     return int(lib.usk_launch_count(1 if reset else 0))
+
+
+def trace_read(max_launches: int = 4096, max_ctas: int = 1 << 18):
+    """Tuning only (USK_TRACE=1): per launch, an int64 array [grid, 4] of %globaltimer stamps
+    (start, staged, compute done, exit) of every CTA, launches in issue order."""
+    import numpy as np
+    stamps = np.zeros(4 * max_ctas, np.uint64)
+    grids = np.zeros(max_launches, np.int32)
+    n = int(lib.usk_trace_read(stamps.ctypes.data, stamps.size, grids.ctypes.data, max_launches))
+    out, c = [], 0
+    for g in grids[:n]:
+        out.append(stamps[4 * c:4 * (c + int(g))].astype(np.int64).reshape(int(g), 4))
+        c += int(g)
+    return out
+
+
+def trace_reset():
+    lib.usk_trace_reset()
