@@ -346,26 +346,46 @@ def run_usk(args):
     sum_kern = float(kern_ms.sum())
     clk = clocks.summary()
     f_peak = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
-    gather_peak = 148 * 32 * f_peak / ROWS / 1e9          # Gweight/s: M LDS lookups per weight
-    achieved = w_rank / (sum_kern * 1e-3) / 1e9
+    n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
+    # ALU roofline of the sketch query: per 32 weights and SM sub-partition
+    # the USK-X hash needs 3 IMAD (2 clk) + 3 IMAD.HI (4 clk) + 1 FFMA (2 clk) on the FMA pipe =
+    # 20 clk (pipe rates measured by tools/micro/pipes.cu, profiles/r1_micro_pipes.txt)
+    alu_peak = n_sm * 4 * 32 / 20.0 * f_peak / 1e9             # Gweight/s
+    gather_floor = n_sm * 32 * f_peak / ROWS / 1e9             # Gweight/s: M LDS wavefronts per 32 weights
+    # the timed graph holds only the sketch-GEMV launches (k_gemv_fast + k_gemv_reduce per group),
+    # so their achieved rate over the timed region is the step's weights / step time
+    achieved = w_rank / (ms_per_step * 1e-3) / 1e9
     sketch_bytes = plan.info["total_cells"] * 2
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
         traffic = json.load(open(tp)).get("k_gemv_fast_bytes_per_launch")
 
-    # ---- standalone reconstruct throughput (weights reconstructed/s, HBM-bound kernel)
+    # ---- standalone reconstruct throughput (weights reconstructed/s, HBM-bound kernel): the 112
+    #      layer reconstructions into one scratch buffer, captured as one CUDA graph, L2 flushed
     scratch = torch.empty(max(o * i for o, i in shapes), dtype=torch.bfloat16, device=dev)
-    rec_ms = 0.0
-    for l, (o, i) in enumerate(shapes):
-        flush.fill_(1)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda._sleep(20000)
-        a.record()
-        usk.reconstruct(plan, sketch, l, scratch[:o * i].view(o, i))
-        b.record()
+
+    def rec_all():
+        for l, (o, i) in enumerate(shapes):
+            usk.reconstruct(plan, sketch, l, scratch[:o * i].view(o, i), stream=stream)
+
+    with torch.cuda.stream(stream):
+        rec_all()
+    torch.cuda.synchronize()
+    g_rec = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g_rec, stream=stream):
+        rec_all()
+    rec_runs = []
+    for k in range(5):
+        with torch.cuda.stream(stream):
+            flush.fill_(k & 0xFF)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            g_rec.replay()
+            b.record(stream)
         b.synchronize()
-        rec_ms += a.elapsed_time(b)
+        rec_runs.append(a.elapsed_time(b))
+    rec_ms = float(np.median(rec_runs))
     rec_wps = numel / (rec_ms * 1e-3)
 
     # ---- end-to-end through the binding: pinned host x -> device, 112 linears, y -> pinned host
@@ -426,12 +446,14 @@ def run_usk(args):
                                        "hbm_frac": rec_wps * (2 + 2 * BPW / 16) / 1e9 / peaks["hbm_gbs"]},
             "build": {"ms": build_ms, "replicate_ms": replicate_ms, "weights_per_s": owned_w / (build_ms * 1e-3),
                       "GB_per_s": owned_w * (2 + BPW / 8) / (build_ms * 1e-3) / 1e9},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": gather_peak, "unit": "Gweight/s",
-                         "frac": achieved / gather_peak, "traffic": traffic,
-                         "kernel": "k_gemv_fast", "kernel_ms_per_step": sum_kern, "peak_basis": f"M={ROWS} shared-memory lookups per weight at 1 LDS "
-                         f"wavefront/clk/SM x 148 SMs x {f_peak / 1e6:.0f} MHz (DESIGN.md §Rooflines)",
-                         "kernel_share_of_step": sum_kern / ms_per_step,
-                         "hbm_frac": sketch_bytes / (sum_kern * 1e-3) / 1e9 / peaks["hbm_gbs"]},
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gweight/s",
+                         "frac": achieved / alu_peak, "traffic": traffic,
+                         "kernel": "k_gemv_fast (+ k_gemv_reduce): the whole timed graph",
+                         "peak_basis": f"FMA pipe: 20 clk per 32 weights per SMSP (3 IMAD + 3 IMAD.HI + FFMA; "
+                                       f"measured rates) -> 6.4 weight/clk/SM x {n_sm} SMs x {f_peak / 1e6:.0f} MHz",
+                         "lds_gather_floor": gather_floor,
+                         "isolated_launch_ms_per_step": sum_kern,
+                         "hbm_frac": sketch_bytes / (ms_per_step * 1e-3) / 1e9 / peaks["hbm_gbs"]},
             "e2e": {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 2),
                     "d2h_bytes_per_step": int(Yh.numel() * 4)},
             "gpu_launches": int(launches_per_step * args.steps),

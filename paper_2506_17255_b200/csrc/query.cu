@@ -44,7 +44,7 @@ constexpr int kQThreads = USK_QUERY_THREADS;
 constexpr int kMaxBatch = 8;
 constexpr int kMaxCtas = 256;  // GEMV compute grid (one CTA per SM)
 #ifndef USK_SUB_ROWS
-#define USK_SUB_ROWS 8
+#define USK_SUB_ROWS 16
 #endif
 constexpr int kSubRows = USK_SUB_ROWS;  // rows per warp work item (subtile): 8 or 16
 static_assert(kSubRows == 8 || kSubRows == 16, "subtile rows");
@@ -714,7 +714,7 @@ Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* row
   const bool bf16 = pl->dtype == USK_BF16;
   const int es = pl->cell_bytes();
   static const int forced = env_int("USK_UPL", 0);
-  static const size_t budget = (size_t)env_int("USK_GEMV_SMEM_KB", 192) * 1024;
+  static const size_t budget = (size_t)env_int("USK_GEMV_SMEM_KB", 220) * 1024;
   static const int cps = std::max(1, env_int("USK_GEMV_CPS", 1));
   for (int pass = 0; pass < 2 && !G.upl; ++pass) {  // pass 1: any fit below the hardware limit
     const size_t cap = pass == 0 ? std::min(budget, kSmemMax) : kSmemMax;

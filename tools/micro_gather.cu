@@ -4,6 +4,10 @@
 //   full   : LOP3 + 3 x (IMAD, IMAD.HI, LEA, LDS) + VIMNMX3 + SHF + FFMA per weight
 //   hash   : same arithmetic, the "gather" replaced by the address itself (no LDS)
 //   gather : LDS of precomputed-ish addresses (address = LEA of an IADD chain), no multiply
+//   mul16  : 16-bit range reduction ((h*a_i) >> 16) * N >> 16 (IMAD instead of IMAD.HI)
+//   mul16u : mul16 with one per-unit base and the row offset folded in (uniform row stride)
+//   hiaddr : q = mulhi(h*a_i, N*128) + R_vi (uniform row base in the IMAD.HI addend), address =
+//            (q & ~127) | lane*4 (one LOP3): same index as mulhi(h*a_i, N), LEA moved to the ALU
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -46,6 +50,28 @@ __global__ void __launch_bounds__(512) kern(const uint32_t* __restrict__ Rg, flo
           } else {
             m0 = o0; m1 = o1; m2 = o2;
           }
+        } else if (MODE == 3) {
+          const uint32_t o0 = ((((h * a0) >> 16) * N >> 16) << 7) + rb[v][0];
+          const uint32_t o1 = ((((h * a1) >> 16) * N >> 16) << 7) + rb[v][1];
+          const uint32_t o2 = ((((h * a2) >> 16) * N >> 16) << 7) + rb[v][2];
+          m0 = *reinterpret_cast<const uint32_t*>(base + o0);
+          m1 = *reinterpret_cast<const uint32_t*>(base + o1);
+          m2 = *reinterpret_cast<const uint32_t*>(base + o2);
+        } else if (MODE == 4) {
+          const uint32_t o0 = ((((h * a0) >> 16) * N >> 16) << 7) + rb[v][0];
+          const uint32_t o1 = ((((h * a1) >> 16) * N >> 16) + N) << 7;
+          const uint32_t o2 = ((((h * a2) >> 16) * N >> 16) + 2 * N) << 7;
+          m0 = *reinterpret_cast<const uint32_t*>(base + o0);
+          m1 = *reinterpret_cast<const uint32_t*>(base + o1 + rb[v][0]);
+          m2 = *reinterpret_cast<const uint32_t*>(base + o2 + rb[v][0]);
+        } else if (MODE == 5) {
+          const uint32_t N128 = (uint32_t)N << 7, l4 = lane * 4u;
+          const uint32_t q0 = __umulhi(h * a0, N128) + (uint32_t)(v * 32 * 3 * N * 4);
+          const uint32_t q1 = __umulhi(h * a1, N128) + (uint32_t)(v * 32 * 3 * N * 4 + N * 128);
+          const uint32_t q2 = __umulhi(h * a2, N128) + (uint32_t)(v * 32 * 3 * N * 4 + 2 * N * 128);
+          m0 = *reinterpret_cast<const uint32_t*>(base + ((q0 & ~127u) | l4));
+          m1 = *reinterpret_cast<const uint32_t*>(base + ((q1 & ~127u) | l4));
+          m2 = *reinterpret_cast<const uint32_t*>(base + ((q2 & ~127u) | l4));
         } else {
           const uint32_t o = ((h & 63u) << 7);
           m0 = *reinterpret_cast<const uint32_t*>(base + o + rb[v][0]);
@@ -98,6 +124,9 @@ void run(const char* name, int occ_target) {
 }
 
 int main() {
+  run<4, 5>("hiaddr", 4);
+  run<2, 5>("hiaddr", 4);
+  run<4, 3>("mul16", 4);
   run<4, 0>("full", 4);
   run<4, 1>("hash", 4);
   run<4, 2>("gather", 4);
