@@ -4,28 +4,24 @@
 // indices in a batch ... interpreting these intermediate results"):
 //   w'(o, j) = the bonded cell of maximum |.| over rows i < M (ties -> non-negative, L1/L2).
 //
-// Fast path (ROW granularity, one input dimension per unit).
-//   * Each CTA owns one CHUNK of TJ = 32*UPL consecutive units (input dims) of one layer and a
-//     contiguous range of 32-row SUBTILES; the chunk's cells are staged into shared memory once
-//     and reused over the whole row range (a cell is hit by ~out/N rows, so a CTA must cover
-//     many rows for the staging to amortise).  Grid = sum over layers of n_chunks x cpc, with
-//     cpc (CTAs per chunk) chosen so that the grid is one resident wave.
-//   * Lane L owns units UPL*L+v.  Their cells sit in shared memory as rho codes
+// Fast path (ROW granularity, one input dimension per unit), shared by K3 and K4:
+//   * A launch's work items -- (layer, chunk of TJ = 32*UPL consecutive units, 16-row subtile) --
+//     are laid out chunk-major; one CTA per SM computes a host-balanced contiguous item range
+//     (partition_items).  A chunk's cells are one contiguous byte range: TMA bulk copies into a raw
+//     shared buffer, converted shared -> shared into the bank-private rho layout
 //         rho = rotl(bits_hi, 1) ^ 1 = (mag << 1) | (1 - sign)
-//     at byte address  cells + 4*(v*32*maxMN + k*32 + L)  -- always bank L, so the M random
-//     gathers of a warp never conflict.  The Eq. 5 select is an integer max (VIMNMX3 for M=3)
-//     and rotr(rho, 1) is the IEEE pattern of -w', so the GEMV multiplies by -x (exact).
-//     Per weight and lane: 1 LOP3 (R(o) ^ K_u) + M x (IMAD, IMAD.HI, LEA, LDS) + max + SHF + FFMA.
-//   * Missing units of a ragged chunk point at a shared "zero" cell (rho of +0) with x = 0, so
-//     the inner loop has no branches.  R(o) for a subtile is one register per lane (lane r holds
-//     R(o0 + r)), broadcast with SHFL, prefetched one subtile ahead.
-//   * GEMV: per subtile a warp holds 32 row partials per lane; a transpose butterfly leaves row r
-//     on lane r.  Partials go to a row-major [rows][CP] workspace; the warp that completes a
-//     subtile's last chunk (atomic counter per subtile) sums the chunks in fixed order with
-//     float4 loads (deterministic, no float atomics) and writes y.
-//   * Programmatic dependent launch: the chunk is staged (sketch only) before
-//     griddepcontrol.wait, overlapping the previous kernel; x is read after it.
-//     usk_linear_batch puts several linears that share x (q|k|v, gate|up) in one launch.
+//     with cell (i, k) of lane L's unit v at word v*32*maxMN + (i*maxN + k)*32 + L -- always bank L,
+//     so the M random gathers of a warp never conflict.  The Eq. 5 select is an integer max
+//     (VIMNMX3 for M=3) and rotr(rho, 1) is the IEEE pattern of -w', so the GEMV multiplies by -x
+//     (exact).  The next chunk of a CTA's range is prefetched under the current one's math.
+//   * Missing units of a ragged chunk point at the zero column (rho of +0) with x = 0, so the inner
+//     loop has no branches.  R(o) for a subtile is one register per lane, broadcast with SHFL.
+//   * K4 (k_gemv_fast + k_gemv_reduce): per subtile a transpose butterfly leaves one row sum per
+//     lane; chunk partials go to a row-major [rows][CP] workspace and a second, PDL-chained kernel
+//     sums them in fixed order (deterministic, no float atomics).  The sketch is staged before
+//     griddepcontrol.wait; x is read after it.  usk_linear_batch puts several linears that share x
+//     (q|k|v, gate|up) in one call.
+//   * K3 (k_recon_fast): the same skeleton storing W' rows (8-byte stores for bf16, UPL = 4).
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
@@ -68,8 +64,6 @@ struct QLayer {
   int64_t row_begin;   // GEMV: first row of the layer in the launch's reduction order
   int32_t n_chunks;    // unit chunks of TJ
   int32_t n_sub;       // 16-row subtiles
-  int32_t cpc;         // reconstruct: CTAs of the layer
-  int32_t cta_begin;   // reconstruct: first CTA of this layer in the launch
   int32_t CP;          // GEMV: row stride of the partial workspace (>= n_chunks, multiple of 4)
   int32_t pad;
   void* y;             // GEMV output
@@ -267,6 +261,37 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 #define USK_GEMV_MAXREG 112  // 512 x 112 + 256 x 32 registers: k_gemv_fast + k_gemv_reduce share an SM
 #endif
 
+// store the UPL reconstructed weights (bits in the high half for bf16) of lane L's units
+template <typename E, int UPL>
+__device__ __forceinline__ void store_units(E* dst, const uint32_t (&wb)[UPL], bool full_tile, int nu, int lane) {
+  if constexpr (sizeof(E) == 2) {
+    if (full_tile) {
+      if constexpr (UPL == 4) {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(wb[0], wb[1 % UPL], 0x7632),
+                                                    __byte_perm(wb[2 % UPL], wb[3 % UPL], 0x7632));
+      } else if constexpr (UPL == 2) {
+        *reinterpret_cast<uint32_t*>(dst) = __byte_perm(wb[0], wb[1 % UPL], 0x7632);
+      } else {
+        dst[0] = (E)(wb[0] >> 16);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < UPL; ++v)
+        if (UPL * lane + v < nu) dst[v] = (E)(wb[v] >> 16);
+    }
+  } else {
+    if (full_tile && UPL == 4) {
+      *reinterpret_cast<uint4*>(dst) = make_uint4(wb[0], wb[1 % UPL], wb[2 % UPL], wb[3 % UPL]);
+    } else if (full_tile && UPL == 2) {
+      *reinterpret_cast<uint2*>(dst) = make_uint2(wb[0], wb[1 % UPL]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < UPL; ++v)
+        if (UPL * lane + v < nu) dst[v] = wb[v];
+    }
+  }
+}
+
 // ------------------------------------------------------------------ K4: sketch-GEMV (decode)
 // Two kernels per call, chained with programmatic dependent launch (no grid barrier):
 //  * k_gemv_fast (one CTA per SM): the launch's work items (layer, chunk, subtile) are laid out
@@ -278,8 +303,8 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 //    beside k_gemv_fast's (register budget 112 + 32 per thread), wait there for the partials
 //    (griddepcontrol.wait), and the NEXT call's k_gemv_fast stages its sketch chunk while they
 //    reduce.
-template <typename E, int UPL, int MT, int HASH>
-__global__ void __maxnreg__(USK_GEMV_MAXREG) k_gemv_fast(const __grid_constant__ QArgs A) {
+template <typename E, int UPL, int MT, int HASH, bool GEMV>
+__device__ __forceinline__ void query_balanced(const QArgs& A) {
   constexpr int TJ = 32 * UPL;
   __shared__ int s_next;  // next subtile of the current segment (warps grab dynamically)
   const int lane = threadIdx.x & 31;
@@ -331,7 +356,7 @@ __global__ void __maxnreg__(USK_GEMV_MAXREG) k_gemv_fast(const __grid_constant__
       for (int v = 0; v < UPL; ++v) {
         const int64_t j = cur.j0 + UPL * lane + v;
         float xv = 0.f;
-        if (UPL * lane + v < cur.nu)
+        if (GEMV && UPL * lane + v < cur.nu)
           xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
                         : reinterpret_cast<const float*>(A.x)[j];
         nx[v] = -xv;  // rotr(rho) decodes to -w'
@@ -361,18 +386,34 @@ __global__ void __maxnreg__(USK_GEMV_MAXREG) k_gemv_fast(const __grid_constant__
         const int nxt = next_sub();  // issued now, consumed after this subtile's math
         const int64_t r0 = (int64_t)sub * kSubRows;
         const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
-        float acc[kSubRows];
+        if constexpr (GEMV) {
+          float acc[kSubRows];
 #pragma unroll
-        for (int r = 0; r < kSubRows; ++r) {
-          const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
-          float a = 0.f;
+          for (int r = 0; r < kSubRows; ++r) {
+            const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
+            float a = 0.f;
 #pragma unroll
-          for (int v = 0; v < UPL; ++v)
-            a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r))), a);
-          acc[r] = a;
+            for (int v = 0; v < UPL; ++v)
+              a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r))), a);
+            acc[r] = a;
+          }
+          const float t = transpose_reduce(acc, lane);
+          if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = t;
+        } else {
+          // W' rows: lane L writes its UPL units of each row (bf16: one 8-byte store for UPL = 4)
+          const bool full_tile = (cur.nu == TJ);
+          E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + cur.j0 + UPL * lane;
+#pragma unroll 4
+          for (int r = 0; r < kSubRows; ++r, dst += Ly.ld_out) {
+            const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
+            if (r >= nrow) continue;
+            uint32_t wb[UPL];
+#pragma unroll
+            for (int v = 0; v < UPL; ++v)
+              wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r)) ^ 0x80000000u;
+            store_units<E, UPL>(dst, wb, full_tile, cur.nu, lane);
+          }
         }
-        const float t = transpose_reduce(acc, lane);
-        if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = t;
         sub = nxt;
         if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
       }
@@ -390,6 +431,18 @@ __global__ void __maxnreg__(USK_GEMV_MAXREG) k_gemv_fast(const __grid_constant__
     atomicMax(&A.timeline[c * 4 + 2], gtimer());
     atomicMax(&A.timeline[c * 4 + 3], gtimer());
   }
+}
+
+template <typename E, int UPL, int MT, int HASH>
+__global__ void __maxnreg__(USK_GEMV_MAXREG) k_gemv_fast(const __grid_constant__ QArgs A) {
+  query_balanced<E, UPL, MT, HASH, true>(A);
+}
+
+// K3 fast path: the same balanced chunk-major partition, staging and per-subtile select as
+// k_gemv_fast, with W' rows stored instead of multiplied (no x, no reduction).
+template <typename E, int UPL, int MT, int HASH>
+__global__ void __maxnreg__(USK_GEMV_MAXREG) k_recon_fast(const __grid_constant__ QArgs A) {
+  query_balanced<E, UPL, MT, HASH, false>(A);
 }
 
 constexpr int kRedThreads = 256;
@@ -433,96 +486,6 @@ __global__ void __launch_bounds__(kRedThreads, 8) k_gemv_reduce(const __grid_con
     }
   }
   if (A.timeline && (threadIdx.x & 31) == 0) {
-    atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
-    atomicMax(&A.timeline[blockIdx.x * 4 + 3], gtimer());
-  }
-}
-
-// ------------------------------------------------------------------ K3: reconstruct (fast path)
-// The layer's cpc CTAs are spread over its chunks as evenly as possible; each chunk's CTAs split
-// its subtiles evenly (static); warps grab subtiles dynamically.  W' rows are written with
-// vector stores (bf16: 4 units per lane -> one 8-byte store).
-template <typename E, int UPL, int MT, int HASH>
-__global__ void __launch_bounds__(kQThreads, USK_QUERY_MINB) k_recon_fast(const __grid_constant__ QArgs A) {
-  constexpr int TJ = 32 * UPL;
-  __shared__ int s_next;
-  const int lane = threadIdx.x & 31;
-  int li = 0;
-  while (li + 1 < A.n_layers && A.layer[li + 1].cta_begin <= (int)blockIdx.x) ++li;
-  const QLayer& Ly = A.layer[li];
-  const int b = blockIdx.x - Ly.cta_begin;
-  const int chunk = (int)(((int64_t)b * Ly.n_chunks) / Ly.cpc);
-  const int first = (int)(((int64_t)chunk * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks);
-  const int nparts = (int)((((int64_t)(chunk + 1) * Ly.cpc + Ly.n_chunks - 1) / Ly.n_chunks) - first);
-  const int part = b - first;
-  const int sub0 = (int)(((int64_t)part * Ly.n_sub) / nparts);
-  const int sub_end = (int)(((int64_t)(part + 1) * Ly.n_sub) / nparts);
-  const int64_t j0 = (int64_t)chunk * TJ;
-  const int nu = (int)min((int64_t)TJ, A.in - j0);
-
-  if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 0] = gtimer();
-  q_prologue<UPL>(A);
-  if (threadIdx.x == 0) s_next = sub0;
-  LaneState<UPL, MT> S;
-  lane_setup<UPL, MT>(A, Ly.unit_base + j0, nu, S);
-  uint32_t phase = 0;
-  stage_units<E, UPL>(A, Ly.unit_base + j0, nu, phase, false);
-  if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 1] = gtimer();
-
-  const int rl = lane & (kSubRows - 1);
-  auto next_sub = [&]() -> int {
-    int g = 0;
-    if (lane == 0) g = atomicAdd(&s_next, 1);
-    return __shfl_sync(0xffffffffu, g, 0);
-  };
-  int sub = next_sub();
-  uint32_t Rl = 0;
-  if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
-  const bool full_tile = (nu == TJ);
-  while (sub < sub_end) {
-    const int nxt = next_sub();
-    const int64_t r0 = (int64_t)sub * kSubRows;
-    const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
-    E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + j0 + UPL * lane;
-#pragma unroll 4
-    for (int r = 0; r < kSubRows; ++r, dst += Ly.ld_out) {
-      const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
-      if (r >= nrow) continue;
-      uint32_t wb[UPL];
-#pragma unroll
-      for (int v = 0; v < UPL; ++v)
-        wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r)) ^ 0x80000000u;
-      if constexpr (sizeof(E) == 2) {
-        if (full_tile) {
-          if constexpr (UPL == 4) {
-            *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(wb[0], wb[1 % UPL], 0x7632),
-                                                        __byte_perm(wb[2 % UPL], wb[3 % UPL], 0x7632));
-          } else if constexpr (UPL == 2) {
-            *reinterpret_cast<uint32_t*>(dst) = __byte_perm(wb[0], wb[1 % UPL], 0x7632);
-          } else {
-            dst[0] = (E)(wb[0] >> 16);
-          }
-        } else {
-#pragma unroll
-          for (int v = 0; v < UPL; ++v)
-            if (UPL * lane + v < nu) dst[v] = (E)(wb[v] >> 16);
-        }
-      } else {
-        if (full_tile && UPL == 4) {
-          *reinterpret_cast<uint4*>(dst) = make_uint4(wb[0], wb[1 % UPL], wb[2 % UPL], wb[3 % UPL]);
-        } else if (full_tile && UPL == 2) {
-          *reinterpret_cast<uint2*>(dst) = make_uint2(wb[0], wb[1 % UPL]);
-        } else {
-#pragma unroll
-          for (int v = 0; v < UPL; ++v)
-            if (UPL * lane + v < nu) dst[v] = wb[v];
-        }
-      }
-    }
-    sub = nxt;
-    if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
-  }
-  if (A.timeline && lane == 0) {
     atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
     atomicMax(&A.timeline[blockIdx.x * 4 + 3], gtimer());
   }
@@ -698,7 +661,7 @@ struct Geom {
   int grid = 0;
   void* kern = nullptr;
   int64_t items = 0;
-  std::vector<int> n_chunks, n_sub, cpc;
+  std::vector<int> n_chunks, n_sub;
 };
 
 // GEMV geometry.  Units per lane: the largest UPL whose CTA fits the shared-memory budget
@@ -707,7 +670,7 @@ struct Geom {
 // before UPL does.  Grid: one CTA per SM (USK_GEMV_CPS per SM for tuning), never more than one
 // resident wave (the kernel's grid barrier relies on it) nor more than the work items.
 // USK_UPL / USK_GEMV_SMEM_KB / USK_GEMV_CPS override (tuning).
-Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n) {
+Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n, bool gemv = true) {
   Geom G;
   for (int k = 0; k < n; ++k) G.maxMN = std::max(G.maxMN, pl->M * (pl->layers[layers[k]].max_ncols + 1));
   const int64_t in = pl->layers[layers[0]].in;
@@ -723,7 +686,7 @@ Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* row
       for (int pu = 32 * upl; pu >= 8; pu /= 2) {
         const size_t sm = smem_bytes(upl, G.maxMN, es, pu);
         if (sm > cap) continue;
-        void* kern = pick_fast(upl, true, bf16, pl->M, pl->hash);
+        void* kern = pick_fast(upl, gemv, bf16, pl->M, pl->hash);
         const int occ = occupancy(kern, sm);
         if (occ < 1) continue;
         G.upl = upl;
@@ -743,37 +706,6 @@ Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* row
     G.items += (int64_t)G.n_chunks.back() * G.n_sub.back();
   }
   G.grid = (int)std::min<int64_t>(G.grid, std::max<int64_t>(G.items, 1));
-  return G;
-}
-
-// Reconstruct geometry: the largest UPL whose chunks all get a resident CTA (larger UPL amortises
-// the per-row R broadcast over more weights); CTAs per layer in proportion to its weights.
-Geom recon_geometry(const usk_plan* pl, int32_t layer, int64_t rows) {
-  Geom G;
-  G.maxMN = pl->M * (pl->layers[layer].max_ncols + 1);
-  const int64_t in = pl->layers[layer].in;
-  const bool bf16 = pl->dtype == USK_BF16;
-  static const int forced = env_int("USK_UPL", 0);
-  int cap = 0;
-  for (int upl : {4, 2, 1}) {
-    if (forced && upl != forced) continue;
-    const size_t sm = smem_bytes(upl, G.maxMN, pl->cell_bytes(), 32 * upl);
-    if (sm > kSmemMax) continue;
-    void* kern = pick_fast(upl, false, bf16, pl->M, pl->hash);
-    const int occ = occupancy(kern, sm);
-    if (occ < 1) continue;
-    G.upl = upl;
-    G.pu = 32 * upl;
-    G.smem = sm;
-    G.kern = kern;
-    cap = sm_count() * occ;
-    if ((in + 32 * upl - 1) / (32 * upl) <= cap) break;
-  }
-  if (!G.upl) return G;
-  G.n_chunks.push_back((int)((in + 32 * G.upl - 1) / (32 * G.upl)));
-  G.n_sub.push_back((int)((rows + kSubRows - 1) / kSubRows));
-  G.cpc.push_back(std::max(G.n_chunks[0], std::min(cap, G.n_chunks[0] * G.n_sub[0])));
-  G.grid = G.cpc[0];
   return G;
 }
 
@@ -995,20 +927,21 @@ usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l,
   if (rows == 0) return USK_OK;
   const int es = pl->cell_bytes();
   const bool aligned = ((ld * es) % 16 == 0) && (reinterpret_cast<uintptr_t>(w_out) % 16 == 0);
-  Geom G = (fast_eligible(pl) && aligned) ? recon_geometry(pl, l, rows) : Geom{};
+  Geom G = (fast_eligible(pl) && aligned) ? gemv_geometry(pl, &l, &rows, 1, false) : Geom{};
   if (G.upl) {
     QArgs A = base_args(pl, sketch, L.in, G);
     QLayer& Ly = A.layer[A.n_layers++];
     Ly.unit_base = L.unit_begin;
     Ly.o_begin = r0;
     Ly.rows = rows;
+    Ly.item_begin = 0;
     Ly.n_chunks = G.n_chunks[0];
     Ly.n_sub = G.n_sub[0];
-    Ly.cpc = G.cpc[0];
-    Ly.cta_begin = 0;
     Ly.w_out = w_out;
     Ly.ld_out = ld;
-    return launch_q(G.kern, A, G.grid, G.smem, false, st);
+    A.items = (int64_t)Ly.n_chunks * Ly.n_sub;
+    A.rows = rows;
+    return launch_q(G.kern, A, partition_items(A, G), G.smem, false, st);
   }
   GenQ Q = make_genq(pl, l, sketch);
   const int64_t n = rows * L.in;
