@@ -7,17 +7,21 @@
 // into the B-tile producer (CUDA-core reconstruction would be 2-3x slower than the MMA at
 // 128-256-token reuse).
 //
-// Structure (one CTA per 128 x 256 output tile, 256 threads):
+// Structure: persistent, one CTA (256 threads) per SM walks 128 x 256 output tiles
+// (tile = blockIdx.x + k * gridDim.x, m fastest within groups of 8 n-blocks for L2 reuse):
 //   warp 0      TMA producer: A tile [128 x 64] + B tile [256 x 64] per stage, SWIZZLE_128B,
-//               4-stage ring guarded by full/empty mbarriers;
-//   warp 1      MMA issuer (one elected lane): 4 x tcgen05.mma (K = 16 each) per stage,
-//               tcgen05.commit -> empty[stage]; final commit -> tmem_full;
-//   warp 2      TMEM allocator (256 fp32 columns = the 128 x 256 accumulator);
-//   warps 4..7  epilogue: tcgen05.ld 32x32b (warp w reads TMEM lanes 32*(w%4)..+31 = its 32
-//               output rows), convert, store.
+//               4-stage ring guarded by full/empty mbarriers, flowing across tiles;
+//   warp 1      MMA issuer (one elected lane): 4 x tcgen05.mma (K = 16 each) per stage into one of
+//               TWO TMEM accumulators (tile parity), tcgen05.commit -> empty[stage]; after a
+//               tile's last stage, commit -> acc_full[parity];
+//   warp 2      TMEM allocator (512 fp32 columns = 2 x the 128 x 256 accumulator);
+//   warps 4..7  epilogue: wait acc_full[parity], tcgen05.ld 32x32b (warp w reads TMEM lanes
+//               32*(w%4)..+31 = its 32 output rows), convert, store, then release the accumulator
+//               (acc_empty[parity]) -- so the epilogue of tile i overlaps the MMAs of tile i+1.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <mutex>
 
 #include "common.cuh"
@@ -32,7 +36,7 @@ constexpr int kGemmThreads = 256;
 constexpr uint32_t kABytes = BM * BK * 2;  // 16 KB
 constexpr uint32_t kBBytes = BN * BK * 2;  // 32 KB
 constexpr uint32_t kStageBytes = kABytes + kBBytes;
-constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kTmemCols = 512;  // two 128 x 256 fp32 accumulators
 constexpr size_t kGemmSmem = 1024 /*align slack*/ + kStages * kStageBytes + 256 /*barriers*/;
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
@@ -98,6 +102,17 @@ struct GemmArgs {
   int64_t ldy;
 };
 
+// tile index -> (m block, n block): groups of kGroupN n-blocks, m fastest inside a group
+constexpr int kGroupN = 8;
+__device__ __forceinline__ void tile_coords(int64_t t, int mblocks, int nblocks, int& mb, int& nb) {
+  const int64_t per_group = (int64_t)mblocks * kGroupN;
+  const int g = (int)(t / per_group);
+  const int64_t r = t - (int64_t)g * per_group;
+  const int gw = min(kGroupN, nblocks - g * kGroupN);  // n-blocks in this group
+  mb = (int)(r / gw);
+  nb = g * kGroupN + (int)(r % gw);
+}
+
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
               const __grid_constant__ GemmArgs G) {
@@ -107,12 +122,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint8_t* sB = gsm + kStages * kABytes;               // kStages x 32 KB
   uint64_t* full = reinterpret_cast<uint64_t*>(gsm + kStages * kStageBytes);
   uint64_t* empty = full + kStages;
-  uint64_t* tmem_full = empty + kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+  uint64_t* acc_full = empty + kStages;   // [2]
+  uint64_t* acc_empty = acc_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM;
-  const int n0 = blockIdx.y * BN;
+  const int mblocks = (int)((G.T + BM - 1) / BM), nblocks = (int)((G.N + BN - 1) / BN);
+  const int64_t tiles = (int64_t)mblocks * nblocks;
   const int nkb = (int)((G.K + BK - 1) / BK);
 
   if (warp == 0 && lane == 0) {
@@ -120,7 +136,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(tmem_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
+    }
     fence_mbar_init();
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
@@ -138,73 +157,97 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % kStages;
-        if (kb >= kStages) mbar_wait(&empty[s], (uint32_t)((kb / kStages) - 1) & 1u);
-        mbar_arrive_expect_tx(&full[s], kStageBytes);
-        tma_load_2d(sA + s * kABytes, &mapA, &full[s], kb * BK, m0);
-        tma_load_2d(sB + s * kBBytes, &mapB, &full[s], kb * BK, n0);
+      int64_t it = 0;  // global stage counter across tiles
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        int mb, nb;
+        tile_coords(t, mblocks, nblocks, mb, nb);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = (int)(it % kStages);
+          if (it >= kStages) mbar_wait(&empty[s], (uint32_t)((it / kStages) - 1) & 1u);
+          mbar_arrive_expect_tx(&full[s], kStageBytes);
+          tma_load_2d(sA + s * kABytes, &mapA, &full[s], kb * BK, mb * BM);
+          tma_load_2d(sB + s * kBBytes, &mapB, &full[s], kb * BK, nb * BN);
+        }
       }
     }
   } else if (warp == 1) {
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % kStages;
-      mbar_wait(&full[s], (uint32_t)(kb / kStages) & 1u);
+    int64_t it = 0;
+    int local = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int b = local & 1;
+      if (local >= 2) mbar_wait(&acc_empty[b], (uint32_t)((local >> 1) - 1) & 1u);  // epilogue drained it
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      if (lane == 0) {
+      const uint32_t acc = tmem + (uint32_t)(b * BN);
+      for (int kb = 0; kb < nkb; ++kb, ++it) {
+        const int s = (int)(it % kStages);
+        mbar_wait(&full[s], (uint32_t)(it / kStages) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (lane == 0) {
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k) {
-          const uint64_t da = smem_desc_sw128(sA + s * kABytes + k * 32);
-          const uint64_t db = smem_desc_sw128(sB + s * kBBytes + k * 32);
-          mma_bf16(tmem, da, db, (kb | k) != 0);
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t da = smem_desc_sw128(sA + s * kABytes + k * 32);
+            const uint64_t db = smem_desc_sw128(sB + s * kBBytes + k * 32);
+            mma_bf16(acc, da, db, (kb | k) != 0);
+          }
+          mma_commit(&empty[s]);
+          if (kb == nkb - 1) mma_commit(&acc_full[b]);
         }
-        mma_commit(&empty[s]);
-        if (kb == nkb - 1) mma_commit(tmem_full);
+        __syncwarp();
       }
-      __syncwarp();
     }
   } else if (warp >= 4) {
     const int q = warp & 3;  // TMEM lane quarter this warp may access
-    mbar_wait(tmem_full, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const int64_t row = (int64_t)m0 + q * 32 + lane;
+    int local = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
+      const int b = local & 1;
+      int mb, nb;
+      tile_coords(t, mblocks, nblocks, mb, nb);
+      mbar_wait(&acc_full[b], (uint32_t)(local >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row = (int64_t)mb * BM + q * 32 + lane;
+      const int64_t n0 = (int64_t)nb * BN;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 32) {
-      uint32_t r[32];
-      tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)c0, r);
-      if (row >= G.T) continue;
-      const int64_t col = (int64_t)n0 + c0;
-      if (col >= G.N) continue;
-      const int nvalid = (int)min((int64_t)32, G.N - col);
-      if (G.y_bf16) {
-        uint16_t* dst = reinterpret_cast<uint16_t*>(G.Y) + row * G.ldy + col;
-        if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c0), r);
+        if (row >= G.T) continue;
+        const int64_t col = n0 + c0;
+        if (col >= G.N) continue;
+        const int nvalid = (int)min((int64_t)32, G.N - col);
+        if (G.y_bf16) {
+          uint16_t* dst = reinterpret_cast<uint16_t*>(G.Y) + row * G.ldy + col;
+          if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
-          for (int v = 0; v < 4; ++v) {
-            uint4 pk;
-            pk.x = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 0])) |
-                   ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 1])) << 16);
-            pk.y = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 2])) |
-                   ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 3])) << 16);
-            pk.z = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 4])) |
-                   ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 5])) << 16);
-            pk.w = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 6])) |
-                   ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 7])) << 16);
-            reinterpret_cast<uint4*>(dst)[v] = pk;
+            for (int v = 0; v < 4; ++v) {
+              uint4 pk;
+              pk.x = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 0])) |
+                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 1])) << 16);
+              pk.y = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 2])) |
+                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 3])) << 16);
+              pk.z = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 4])) |
+                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 5])) << 16);
+              pk.w = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 6])) |
+                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 7])) << 16);
+              reinterpret_cast<uint4*>(dst)[v] = pk;
+            }
+          } else {
+            for (int v = 0; v < nvalid; ++v) dst[v] = f32_to_bf16_rne(__uint_as_float(r[v]));
           }
         } else {
-          for (int v = 0; v < nvalid; ++v) dst[v] = f32_to_bf16_rne(__uint_as_float(r[v]));
-        }
-      } else {
-        float* dst = reinterpret_cast<float*>(G.Y) + row * G.ldy + col;
-        if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+          float* dst = reinterpret_cast<float*>(G.Y) + row * G.ldy + col;
+          if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
-          for (int v = 0; v < 8; ++v)
-            reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
-        } else {
-          for (int v = 0; v < nvalid; ++v) dst[v] = __uint_as_float(r[v]);
+            for (int v = 0; v < 8; ++v)
+              reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+          } else {
+            for (int v = 0; v < nvalid; ++v) dst[v] = __uint_as_float(r[v]);
+          }
         }
       }
+      // all of this warp's TMEM reads of accumulator b are complete (tcgen05.wait::ld in tmem_ld32)
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -256,8 +299,15 @@ usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dty
   std::call_once(attr_once, [] {
     cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
   });
-  dim3 grid((unsigned)((T + BM - 1) / BM), (unsigned)((n_out + BN - 1) / BN));
-  k_gemm_tc<<<grid, kGemmThreads, kGemmSmem, st>>>(ma, mb, G);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
+                                                 cudaSuccess)
+      sms = 148;
+  }
+  const int64_t tiles = ((T + BM - 1) / BM) * ((n_out + BN - 1) / BN);
+  k_gemm_tc<<<(unsigned)std::min<int64_t>(tiles, sms), kGemmThreads, kGemmSmem, st>>>(ma, mb, G);
   USK_LAUNCHED("k_gemm_tc");
   return USK_OK;
 }
