@@ -8,6 +8,8 @@
 //   mul16u : mul16 with one per-unit base and the row offset folded in (uniform row stride)
 //   hiaddr : q = mulhi(h*a_i, N*128) + R_vi (uniform row base in the IMAD.HI addend), address =
 //            (q & ~127) | lane*4 (one LOP3): same index as mulhi(h*a_i, N), LEA moved to the ALU
+//   oraddr : power-of-two aligned (unit, row) regions: address = base_vi_lane | (idx << 7)
+//            (SHF + LOP3 on the ALU pipe instead of an IMAD/LEA)
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -23,7 +25,8 @@ __global__ void __launch_bounds__(512) kern(const uint32_t* __restrict__ Rg, flo
   float nx[UPL];
   for (int v = 0; v < UPL; ++v) {
     K[v] = 0x12345u * (v + 1) + lane;
-    for (int i = 0; i < 3; ++i) rb[v][i] = 4u * (uint32_t)(v * 32 * 3 * N + i * N * 32 + lane);
+    for (int i = 0; i < 3; ++i)
+      rb[v][i] = MODE == 6 ? (((uint32_t)(v * 3 + i) << 14) | (4u * lane)) : 4u * (uint32_t)(v * 32 * 3 * N + i * N * 32 + lane);
     nx[v] = 1.0f + v;
   }
   const char* base = reinterpret_cast<const char*>(sm);
@@ -64,6 +67,20 @@ __global__ void __launch_bounds__(512) kern(const uint32_t* __restrict__ Rg, flo
           m0 = *reinterpret_cast<const uint32_t*>(base + o0);
           m1 = *reinterpret_cast<const uint32_t*>(base + o1 + rb[v][0]);
           m2 = *reinterpret_cast<const uint32_t*>(base + o2 + rb[v][0]);
+        } else if (MODE == 6) {
+          // regions of 16 KB: base(v, i) = (v * 3 + i) << 14, lane * 4 in the low bits
+          const uint32_t i0 = __umulhi(h * a0, N), i1 = __umulhi(h * a1, N), i2 = __umulhi(h * a2, N);
+          uint32_t s0, s1, s2;
+          asm("shl.b32 %0, %1, 7;" : "=r"(s0) : "r"(i0));
+          asm("shl.b32 %0, %1, 7;" : "=r"(s1) : "r"(i1));
+          asm("shl.b32 %0, %1, 7;" : "=r"(s2) : "r"(i2));
+          uint32_t o0, o1, o2;
+          asm("or.b32 %0, %1, %2;" : "=r"(o0) : "r"(s0), "r"(rb[v][0]));
+          asm("or.b32 %0, %1, %2;" : "=r"(o1) : "r"(s1), "r"(rb[v][1]));
+          asm("or.b32 %0, %1, %2;" : "=r"(o2) : "r"(s2), "r"(rb[v][2]));
+          m0 = *reinterpret_cast<const uint32_t*>(base + o0);
+          m1 = *reinterpret_cast<const uint32_t*>(base + o1);
+          m2 = *reinterpret_cast<const uint32_t*>(base + o2);
         } else if (MODE == 5) {
           const uint32_t N128 = (uint32_t)N << 7, l4 = lane * 4u;
           const uint32_t q0 = __umulhi(h * a0, N128) + (uint32_t)(v * 32 * 3 * N * 4);
@@ -92,7 +109,7 @@ __global__ void __launch_bounds__(512) kern(const uint32_t* __restrict__ Rg, flo
 template <int UPL, int MODE>
 void run(const char* name, int occ_target) {
   const int N = 85;
-  const size_t smem = (size_t)UPL * 32 * 3 * N * 4;
+  const size_t smem = MODE == 6 ? (size_t)UPL * 3 * 16384 : (size_t)UPL * 32 * 3 * N * 4;
   cudaFuncSetAttribute(kern<UPL, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern<UPL, MODE>, 512, smem);
@@ -124,8 +141,8 @@ void run(const char* name, int occ_target) {
 }
 
 int main() {
-  run<4, 5>("hiaddr", 4);
-  run<2, 5>("hiaddr", 4);
+  run<4, 6>("oraddr", 4);
+  run<2, 6>("oraddr", 4);
   run<4, 3>("mul16", 4);
   run<4, 0>("full", 4);
   run<4, 1>("hash", 4);
