@@ -70,7 +70,15 @@ def lib():
         L.uo_allocate.restype = i32
         L.uo_allocate.argtypes = [i64, p, p, i64, i32, i32, i32, p, p]
         L.uo_plan.restype = i32
-        L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, p, p, p, p, p]
+        L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, i32, i32, p, p, p, p, p]
+        L.uo_quantize.restype = i32
+        L.uo_quantize.argtypes = [i32, p, i64, i32, i32, p, p]
+        L.uo_dequantize.restype = i32
+        L.uo_dequantize.argtypes = [i32, p, p, i64, p]
+        L.uo_pack_codes.restype = i32
+        L.uo_pack_codes.argtypes = [i32, p, i64, p]
+        L.uo_f32_to_bf16_rne.restype = u32
+        L.uo_f32_to_bf16_rne.argtypes = [u32]
         L.uo_build_units.restype = i32
         L.uo_build_units.argtypes = [i32, p, i64, i64, i32, i32, i32, i64, i64, p, p, i32, i32, u64, p]
         L.uo_reconstruct_rows.restype = i32
@@ -199,11 +207,14 @@ class Plan:
     ncols: np.ndarray       # [U]
     offsets: np.ndarray     # [U+1] cells
     acct: np.ndarray        # [L, 4] budget bits, class-map bits, T, achieved bits
+    state_bits: int = 0     # 0: raw states in the weight dtype; 4 / 8: stacked quantisation
+    group: int = 128        # cells per quantisation group (layers start at multiples of it)
     extra: dict = field(default_factory=dict)
 
     @property
     def total_cells(self) -> int:
-        return int(self.offsets[-1])
+        end = int(self.offsets[-1])
+        return end if not self.state_bits else -(-end // self.group) * self.group
 
     def layer_units(self, l):
         return int(self.unit_base[l]), int(self.unit_base[l + 1])
@@ -214,7 +225,7 @@ class Plan:
 
 
 def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None, min_cols=1,
-         hash_kind=HASH_X, seed=0) -> Plan:
+         hash_kind=HASH_X, seed=0, state_bits=0, group=128) -> Plan:
     L = len(shapes)
     outf = np.array([s[0] for s in shapes], dtype=np.int64)
     inf = np.array([s[1] for s in shapes], dtype=np.int64)
@@ -233,11 +244,11 @@ def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None
     acct = np.zeros(4 * L, dtype=np.int64)
     st = lib().uo_plan(L, _ptr(outf), _ptr(inf), dtype,
                        ct.cast(sal_ptrs, ct.c_void_p) if sal_ptrs is not None else None,
-                       float(bpw), M, gran, g, C, min_cols, _ptr(unit_base), _ptr(cls), _ptr(ncols),
-                       _ptr(offsets), _ptr(acct))
+                       float(bpw), M, gran, g, C, min_cols, state_bits, group, _ptr(unit_base), _ptr(cls),
+                       _ptr(ncols), _ptr(offsets), _ptr(acct))
     _check(st, "plan")
     return Plan(list(map(tuple, zip(outf.tolist(), inf.tolist()))), dtype, M, gran, g, C, min_cols, hash_kind,
-                seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4))
+                seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4), state_bits, group)
 
 
 def _np_dtype(dtype):
@@ -260,43 +271,118 @@ def build_layer(pl: Plan, l: int, W: np.ndarray, sketch: np.ndarray, t_begin=0, 
                                 _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(sketch)), "build_units")
 
 
-def build_model(pl: Plan, weights) -> np.ndarray:
-    sketch = np.zeros(pl.total_cells, dtype=_np_dtype(pl.dtype))
-    for l, W in enumerate(weights):
-        build_layer(pl, l, W, sketch)
-    return sketch
+@dataclass
+class QSketch:
+    """A quantised sketch (state_bits 4 / 8): int8 codes per cell, fp32 scales per group, the
+    packed code bytes as stored, and the dequantised fp32 cells (bit patterns) used for
+    retrieval."""
+    codes: np.ndarray       # int8 [total_cells]
+    scales: np.ndarray      # float32 [total_cells / group]
+    packed: np.ndarray      # uint8 code storage
+    deq: np.ndarray         # uint32 fp32 bits [total_cells]
+    raw: np.ndarray         # the raw (pre-quantisation) states, weight dtype
 
 
-def reconstruct_rows(pl: Plan, sketch: np.ndarray, l: int, o_begin=0, o_end=None) -> np.ndarray:
+def inf_bits(dtype):
+    return 0x7F80 if dtype == BF16 else 0x7F800000
+
+
+def quantize(dtype, raw: np.ndarray, q: int, G: int):
+    """SPEC quant: per-group fp32 absmax scale, round-half-away codes; (codes int8, scales f32)."""
+    raw = np.ascontiguousarray(raw, dtype=_np_dtype(dtype))
+    n = len(raw)
+    codes = np.zeros(n, dtype=np.int8)
+    scales = np.zeros(n // G, dtype=np.float32)
+    _check(lib().uo_quantize(dtype, _ptr(raw), n, q, G, _ptr(codes), _ptr(scales)), "quantize")
+    return codes, scales
+
+
+def dequantize(codes: np.ndarray, scales: np.ndarray, G: int) -> np.ndarray:
+    """fp32 bits of fl32(code * scale) per cell."""
+    codes = np.ascontiguousarray(codes, dtype=np.int8)
+    scales = np.ascontiguousarray(scales, dtype=np.float32)
+    out = np.zeros(len(codes), dtype=np.uint32)
+    _check(lib().uo_dequantize(G, _ptr(codes), _ptr(scales), len(codes), _ptr(out)), "dequantize")
+    return out
+
+
+def pack_codes(q: int, codes: np.ndarray) -> np.ndarray:
+    codes = np.ascontiguousarray(codes, dtype=np.int8)
+    out = np.zeros(len(codes) * q // 8, dtype=np.uint8)
+    _check(lib().uo_pack_codes(q, _ptr(codes), len(codes), _ptr(out)), "pack_codes")
+    return out
+
+
+def f32_to_bf16_rne(bits: np.ndarray) -> np.ndarray:
+    L = lib()
+    return np.array([L.uo_f32_to_bf16_rne(int(b)) for b in np.asarray(bits).ravel()],
+                    dtype=np.uint16).reshape(np.shape(bits))
+
+
+def build_model(pl: Plan, weights, layers=None):
+    """Raw plans: the sketch cells (uint16 / uint32).  Quantised plans: a QSketch (raw states
+    built into a +Inf-initialised buffer, then quantised per group)."""
+    layers = range(len(weights)) if layers is None else layers
+    if not pl.state_bits:
+        sketch = np.zeros(pl.total_cells, dtype=_np_dtype(pl.dtype))
+        for l, W in zip(layers, weights):
+            build_layer(pl, l, W, sketch)
+        return sketch
+    raw = np.full(pl.total_cells, inf_bits(pl.dtype), dtype=_np_dtype(pl.dtype))
+    for l, W in zip(layers, weights):
+        build_layer(pl, l, W, raw)
+    codes, scales = quantize(pl.dtype, raw, pl.state_bits, pl.group)
+    return QSketch(codes, scales, pack_codes(pl.state_bits, codes), dequantize(codes, scales, pl.group), raw)
+
+
+def _retrieval_view(pl: Plan, sketch):
+    """(dtype, cells) on which Eq. 5 runs: raw cells, or the dequantised fp32 cells."""
+    if isinstance(sketch, QSketch):
+        return F32, sketch.deq
+    return pl.dtype, sketch
+
+
+def _to_plan_dtype(pl: Plan, sketch, bits: np.ndarray) -> np.ndarray:
+    if isinstance(sketch, QSketch) and pl.dtype == BF16:
+        return f32_to_bf16_rne(bits)
+    return bits
+
+
+def reconstruct_rows(pl: Plan, sketch, l: int, o_begin=0, o_end=None) -> np.ndarray:
+    """W' rows in the plan dtype (quantised plans: the dequantised value, RNE to bf16)."""
     out, inn = pl.shapes[l]
     o_end = out if o_end is None else o_end
     ncols, offs = pl.layer_slices(l)
-    res = np.zeros((o_end - o_begin, inn), dtype=_np_dtype(pl.dtype))
-    _check(lib().uo_reconstruct_rows(pl.dtype, _ptr(sketch), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs),
+    dt, cells = _retrieval_view(pl, sketch)
+    res = np.zeros((o_end - o_begin, inn), dtype=_np_dtype(dt))
+    _check(lib().uo_reconstruct_rows(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs),
                                      pl.M, pl.hash_kind, pl.seed, o_begin, o_end, _ptr(res)), "reconstruct_rows")
-    return res
+    return _to_plan_dtype(pl, sketch, res)
 
 
-def reconstruct_entries(pl: Plan, sketch: np.ndarray, l: int, oj: np.ndarray) -> np.ndarray:
+def reconstruct_entries(pl: Plan, sketch, l: int, oj: np.ndarray) -> np.ndarray:
     out, inn = pl.shapes[l]
     ncols, offs = pl.layer_slices(l)
+    dt, cells = _retrieval_view(pl, sketch)
     oj = np.ascontiguousarray(oj, dtype=np.int64)
     res = np.zeros(len(oj), dtype=np.uint32)
-    _check(lib().uo_reconstruct_entries(pl.dtype, _ptr(sketch), out, inn, l, pl.gran, pl.g, _ptr(ncols),
+    _check(lib().uo_reconstruct_entries(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols),
                                         _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(oj), len(oj), _ptr(res)),
            "reconstruct_entries")
-    return res
+    return _to_plan_dtype(pl, sketch, res).astype(np.uint32)
 
 
-def linear_rows(pl: Plan, sketch: np.ndarray, l: int, x: np.ndarray, o_begin=0, o_end=None) -> np.ndarray:
-    """fp64 y[T, o_end-o_begin] = x[T, in] @ W'[o_begin:o_end]^T."""
+def linear_rows(pl: Plan, sketch, l: int, x: np.ndarray, o_begin=0, o_end=None) -> np.ndarray:
+    """fp64 y[T, o_end-o_begin] = x[T, in] @ W'[o_begin:o_end]^T (quantised plans: W' = the
+    dequantised fp32 values, not rounded to the weight dtype)."""
     out, inn = pl.shapes[l]
     o_end = out if o_end is None else o_end
     x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
     T = x.shape[0]
     ncols, offs = pl.layer_slices(l)
+    dt, cells = _retrieval_view(pl, sketch)
     y = np.zeros((T, o_end - o_begin), dtype=np.float64)
-    _check(lib().uo_linear_rows(pl.dtype, _ptr(sketch), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs), pl.M,
+    _check(lib().uo_linear_rows(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs), pl.M,
                                 pl.hash_kind, pl.seed, _ptr(x), T, o_begin, o_end, _ptr(y)), "linear_rows")
     return y
 

@@ -25,6 +25,9 @@
  *       remainder order are our reading (L9/L10): "parity unpinned" for those.
  *   uo_importance -- pinned (SPEC Eq. 7 examples, constant activations).
  *   uo_linear_rows -- pinned (numpy fp64 matmul of the oracle-verified W').
+ *   uo_quantize / uo_dequantize / uo_pack_codes / uo_f32_to_bf16_rne (stacked state
+ *       quantisation) -- pinned (SPEC quant worked examples, round-trip error
+ *       bound <= scale/2, code range, unoccupied -> 0, torch's bf16 RNE conversion).
  */
 #include <math.h>
 #include <stdint.h>
@@ -109,6 +112,9 @@ static double uo_value(int32_t dtype, uint32_t bits) {
 }
 
 static uint32_t uo_inf_bits(int32_t dtype) { return dtype == UO_BF16 ? 0x7F80u : 0x7F800000u; }
+static uint32_t uo_load_bits(int32_t dtype, const void* base, int64_t idx) {
+  return dtype == UO_BF16 ? (uint32_t)((const uint16_t*)base)[idx] : ((const uint32_t*)base)[idx];
+}
 
 /* Eq. 4: S[i,I_i] = (Abs(S[i,I_i]) > Abs(X)) ? X : S[i,I_i].
  * Tie |X| == |S| with opposite signs: prefer the non-negative value (L2,
@@ -356,14 +362,24 @@ static int32_t uo_ceil_log2(int32_t C) {
   return b;
 }
 
+/* Stacked state quantisation (q = 4 or 8 bits per state; PAPER.md:348-350,
+ * Table 1 "+ q4"/"+ q8"): states are stored as codes in groups of G consecutive cells of a
+ * layer with one fp32 scale per group.  Each layer's cells start at a multiple of G (layers are
+ * padded; padding cells are unoccupied), so a layer stores ceil(cells/G) groups of q*G + 32 bits
+ * (DESIGN.md ledger L25).  ROW scope: T = floor((budget - meta) / (q*G + 32)) * G; LAYER scope:
+ * T = (floor(budget / (q*G + 32)) - n_layers) * G (one partial group per layer). */
+static int64_t uo_align_up(int64_t x, int64_t a) { return ((x + a - 1) / a) * a; }
+
 int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32_t dtype,
                 const float* const* sal, double bpw, int32_t M, int32_t gran, int32_t g, int32_t C,
-                int32_t min_cols, int64_t* unit_base, uint8_t* cls, int32_t* ncols,
+                int32_t min_cols, int32_t q, int32_t G, int64_t* unit_base, uint8_t* cls, int32_t* ncols,
                 int64_t* offsets, int64_t* layer_acct) {
   int32_t l;
   int64_t U = 0, u;
   int32_t state_bits = (dtype == UO_BF16) ? 16 : 32;
   if (n_layers < 1 || M < 1 || M > 8 || C < 1 || C > 255 || min_cols < 1) return UO_EINVAL;
+  if (q != 0 && q != 4 && q != 8) return UO_EINVAL;
+  if (q != 0 && (G < 32 || G % 32 != 0)) return UO_EINVAL;
   if (!(bpw > 0.0) || !isfinite(bpw)) return UO_EINVAL;
   if (dtype != UO_F32 && dtype != UO_BF16) return UO_EINVAL;
   if (gran != UO_GRAN_ROW && gran != UO_GRAN_LAYER) return UO_EINVAL;
@@ -391,7 +407,7 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       int32_t st;
       int64_t achieved = meta;
       if (budget < meta) return UO_EBUDGET;
-      T = (budget - meta) / state_bits;
+      T = (q == 0) ? (budget - meta) / state_bits : ((budget - meta) / ((int64_t)q * G + 32)) * G;
       s_u = (double*)malloc(sizeof(double) * (size_t)Ul);
       L_u = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)Ul);
       for (t = 0; t < Ul; t++) {
@@ -412,7 +428,11 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       free(s_u);
       free(L_u);
       if (st != UO_OK) return st;
-      for (t = 0; t < Ul; t++) achieved += (int64_t)M * ncols[unit_base[l] + t] * state_bits;
+      {
+        int64_t cells = 0;
+        for (t = 0; t < Ul; t++) cells += (int64_t)M * ncols[unit_base[l] + t];
+        achieved += (q == 0) ? cells * state_bits : ((cells + G - 1) / G) * ((int64_t)q * G + 32);
+      }
       layer_acct[4 * l + 0] = budget;
       layer_acct[4 * l + 1] = meta;
       layer_acct[4 * l + 2] = T;
@@ -440,7 +460,12 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       numel += outf[l] * inf[l];
     }
     budget = (int64_t)floor(bpw * (double)numel);
-    T = budget / state_bits;
+    if (q == 0) {
+      T = budget / state_bits;
+    } else {
+      int64_t ng = budget / ((int64_t)q * G + 32) - n_layers;
+      T = (ng > 0 ? ng : 0) * G;
+    }
     st = uo_allocate(n_layers, s_u, L_u, T, C, M, min_cols, cls, ncols);
     free(s_u);
     free(L_u);
@@ -449,13 +474,89 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       layer_acct[4 * l + 0] = (l == 0) ? budget : 0;
       layer_acct[4 * l + 1] = 0;
       layer_acct[4 * l + 2] = (l == 0) ? T : 0;
-      layer_acct[4 * l + 3] = (int64_t)M * ncols[l] * state_bits;
+      layer_acct[4 * l + 3] = (q == 0) ? (int64_t)M * ncols[l] * state_bits
+                                       : (((int64_t)M * ncols[l] + G - 1) / G) * ((int64_t)q * G + 32);
     }
   }
+  /* offsets: exclusive prefix sum of M * N_u in (layer, t) order; with q, each layer starts at
+   * a multiple of G */
   offsets[0] = 0;
-  for (u = 0; u < U; u++) offsets[u + 1] = offsets[u] + (int64_t)M * ncols[u];
+  for (l = 0; l < n_layers; l++) {
+    if (q != 0) offsets[unit_base[l]] = uo_align_up(offsets[unit_base[l]], G);
+    for (u = unit_base[l]; u < unit_base[l + 1]; u++) offsets[u + 1] = offsets[u] + (int64_t)M * ncols[u];
+  }
   return UO_OK;
 }
+
+/* ------------------------------------------------------------------------------------
+ * Stacked state quantisation, per group of G cells (SPEC.md quant module: "scale = max|value|
+ * over occupied cells of g divided by the max code magnitude (127 for 8-bit, 7 for 4-bit);
+ * codes = round(value/scale) clamped; unoccupied cells coded 0; all-zero groups get scale 0";
+ * rounding half away from zero, SPEC "DESIGN DECISIONS").  Arithmetic in fp32 (the scale is
+ * stored as fp32; DESIGN.md ledger L25): scale = fl32(absmax / qmax), code = roundf(fl32(v /
+ * scale)) clamped to [-qmax, qmax].  A cell is occupied iff its raw state is finite (empty
+ * cells hold +Inf).  raw: n cells (n a multiple of G) of the dtype; codes: one
+ * int8 per cell (unpacked); scales: n / G floats.
+ * ------------------------------------------------------------------------------------ */
+int32_t uo_quantize(int32_t dtype, const void* raw, int64_t n, int32_t q, int32_t G, int8_t* codes,
+                    float* scales) {
+  int64_t gi, c;
+  const float qmax = (q == 4) ? 7.0f : 127.0f;
+  if ((q != 4 && q != 8) || G < 1 || n % G != 0) return UO_EINVAL;
+  for (gi = 0; gi < n / G; gi++) {
+    float absmax = 0.0f, scale;
+    for (c = gi * G; c < (gi + 1) * G; c++) {
+      const float v = (float)uo_value(dtype, uo_load_bits(dtype, raw, c));
+      if (isfinite(v) && fabsf(v) > absmax) absmax = fabsf(v);
+    }
+    scale = absmax / qmax;
+    scales[gi] = scale;
+    for (c = gi * G; c < (gi + 1) * G; c++) {
+      const float v = (float)uo_value(dtype, uo_load_bits(dtype, raw, c));
+      float r = 0.0f;
+      if (isfinite(v) && scale > 0.0f) {
+        r = roundf(v / scale);
+        if (r > qmax) r = qmax;
+        if (r < -qmax) r = -qmax;
+      }
+      codes[c] = (int8_t)r;
+    }
+  }
+  return UO_OK;
+}
+
+/* value = fl32(code * scale) (SPEC.md quant module "value = code x group scale"), returned as
+ * fp32 bit patterns: the quantised sketch is then an fp32 sketch for retrieval (Eq. 5). */
+int32_t uo_dequantize(int32_t G, const int8_t* codes, const float* scales, int64_t n, uint32_t* f32_bits) {
+  int64_t c;
+  if (G < 1) return UO_EINVAL;
+  for (c = 0; c < n; c++) {
+    const float v = (float)codes[c] * scales[c / G];
+    memcpy(&f32_bits[c], &v, 4);
+  }
+  return UO_OK;
+}
+
+/* storage of the codes: q = 8 -> one byte (two's complement) per cell; q = 4 -> two cells per
+ * byte, the even cell in the low nibble (SPEC "4-bit codes packed two per byte, little-end
+ * nibble first"). */
+int32_t uo_pack_codes(int32_t q, const int8_t* codes, int64_t n, uint8_t* out) {
+  int64_t c;
+  if (q == 8) {
+    for (c = 0; c < n; c++) out[c] = (uint8_t)codes[c];
+  } else if (q == 4) {
+    if (n % 2) return UO_EINVAL;
+    for (c = 0; c < n / 2; c++)
+      out[c] = (uint8_t)(((uint8_t)codes[2 * c] & 0xFu) | (((uint8_t)codes[2 * c + 1] & 0xFu) << 4));
+  } else {
+    return UO_EINVAL;
+  }
+  return UO_OK;
+}
+
+/* fp32 -> bf16, round to nearest even (finite values): the reconstruction of a quantised bf16
+ * plan (the dequantised fp32 value rounded to the weight dtype). */
+uint32_t uo_f32_to_bf16_rne(uint32_t b) { return (b + 0x7FFFu + ((b >> 16) & 1u)) >> 16; }
 
 /* ------------------------------------------------------------------------------------
  * Layer-level build / reconstruct / linear over a unit range of one layer.
