@@ -83,6 +83,11 @@ typedef struct {
   int32_t hash;          /* usk_hash */
   int32_t dtype;         /* usk_dtype of weights == dtype of sketch states (L3) */
   uint64_t seed;         /* hash seed ("fixing random seed in hash functions") */
+  int32_t state_bits;    /* 0: raw states in the weight dtype; 4 or 8: stacked state quantisation
+                            (Table 1 "+ q4"/"+ q8"): codes of
+                            state_bits bits, one fp32 absmax scale per group_size cells of a layer,
+                            round half away from zero; DESIGN.md ledger L25 */
+  int32_t group_size;    /* cells per scale group (power of two >= 32; 0 = 128); quantised plans only */
 } usk_params;
 
 typedef struct usk_plan usk_plan;
@@ -97,7 +102,14 @@ typedef struct {
   int64_t sketch_bytes;   /* bytes the caller must allocate for the sketch (cells + tail pad) */
   int64_t numel;          /* weights covered */
   int64_t budget_bits;    /* sum of floor(bpw * numel) over budget scopes */
-  int64_t achieved_bits;  /* states * state bits + charged class-map bits (<= budget_bits) */
+  int64_t achieved_bits;  /* states * state bits + charged class-map bits (<= budget_bits);
+                             quantised: sum over layers of ceil(cells/G) * (q*G + 32) + class map */
+  int32_t state_bits;     /* 0 (raw), 4 or 8 */
+  int32_t group_size;     /* quantised plans: cells per scale group */
+  int64_t n_groups;       /* quantised plans: total_cells / group_size (layers start at multiples
+                             of group_size, total_cells includes the padding) */
+  int64_t scales_offset;  /* quantised plans: byte offset of the fp32 scales in the sketch buffer;
+                             the codes (packed, cell c at bit c*state_bits) start at byte 0 */
 } usk_plan_info;
 
 typedef struct {

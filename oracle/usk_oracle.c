@@ -379,7 +379,7 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
   int32_t state_bits = (dtype == UO_BF16) ? 16 : 32;
   if (n_layers < 1 || M < 1 || M > 8 || C < 1 || C > 255 || min_cols < 1) return UO_EINVAL;
   if (q != 0 && q != 4 && q != 8) return UO_EINVAL;
-  if (q != 0 && (G < 32 || G % 32 != 0)) return UO_EINVAL;
+  if (q != 0 && (G < 32 || (G & (G - 1)) != 0)) return UO_EINVAL; /* power of two >= 32 */
   if (!(bpw > 0.0) || !isfinite(bpw)) return UO_EINVAL;
   if (dtype != UO_F32 && dtype != UO_BF16) return UO_EINVAL;
   if (gran != UO_GRAN_ROW && gran != UO_GRAN_LAYER) return UO_EINVAL;

@@ -88,6 +88,10 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   if (P.dtype != USK_F32 && P.dtype != USK_BF16) return fail(USK_EINVAL, "dtype");
   if (P.min_cols < 1) return fail(USK_EINVAL, "min_cols must be >= 1");
   if (P.n_classes < 0 || P.n_classes > 64) return fail(USK_EINVAL, "n_classes must be in [0, 64]");
+  if (P.state_bits != 0 && P.state_bits != 4 && P.state_bits != 8) return fail(USK_EINVAL, "state_bits must be 0, 4 or 8");
+  const int32_t qG = P.group_size ? P.group_size : 128;
+  if (P.state_bits && (qG < 32 || (qG & (qG - 1)) != 0))
+    return fail(USK_EINVAL, "group_size must be a power of two >= 32");
   const int g = P.granularity == USK_GRAN_ROW ? P.dims_per_unit : 1;
   if (P.granularity == USK_GRAN_ROW && g < 1) return fail(USK_EINVAL, "dims_per_unit must be >= 1");
   for (int l = 0; l < n_layers; ++l) {
@@ -110,6 +114,8 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   pl->dtype = P.dtype;
   pl->bpw = P.bpw;
   pl->seed = P.seed;
+  pl->q = P.state_bits;
+  pl->G = P.state_bits ? qG : 128;
   const int state_bits = P.dtype == USK_BF16 ? 16 : 32;
   pl->hc.rho = (uint32_t)splitmix64(P.seed);
   for (int i = 0; i < 8; ++i) pl->hc.a[i] = ((uint32_t)splitmix64(P.seed + 0x100ull + (uint64_t)i)) | 1u;
@@ -142,13 +148,16 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
       }
       L.budget_bits = budget;
       L.meta_bits = meta;
-      L.cells_T = (budget - meta) / state_bits;
+      // quantised: ceil(cells/G) groups of q*G code bits + one fp32 scale (layers G-aligned)
+      L.cells_T = pl->q ? ((budget - meta) / ((int64_t)pl->q * pl->G + 32)) * pl->G : (budget - meta) / state_bits;
       pl->budget_bits += budget;
     }
   } else {
     const int64_t budget = (int64_t)std::floor(P.bpw * (double)numel_all);
     pl->layers[0].budget_bits = budget;
-    pl->layers[0].cells_T = budget / state_bits;
+    // quantised: one partial group per layer is reserved (each layer starts a new group)
+    pl->layers[0].cells_T =
+        pl->q ? std::max<int64_t>(0, budget / ((int64_t)pl->q * pl->G + 32) - n_layers) * pl->G : budget / state_bits;
     pl->budget_bits = budget;
   }
   cudaStream_t st = (cudaStream_t)stream;
@@ -170,7 +179,28 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
     free_plan(pl);
     return s;
   }
-  pl->total_cells = pl->h_offsets[U];
+  if (pl->q) {
+    // each layer's cells start at a multiple of G (groups never straddle layers, so
+    // layer-sharded builds quantise independently): shift the prefix-scan offsets on the host
+    int64_t shift = 0;
+    for (int l = 0; l < n_layers; ++l) {
+      const int64_t u0 = pl->layers[l].unit_begin, u1 = u0 + pl->layers[l].n_units;
+      const int64_t start = pl->h_offsets[u0] + shift;
+      shift += (start + pl->G - 1) / pl->G * pl->G - start;
+      for (int64_t u = u0; u < u1; ++u) pl->h_offsets[u] += shift;
+    }
+    pl->h_offsets[U] += shift;
+    e = cudaMemcpy(pl->d_offsets, pl->h_offsets.data(), sizeof(int64_t) * (U + 1), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) {
+      free_plan(pl);
+      return cuda_fail(e, "usk_plan_allocation: offsets upload");
+    }
+  }
+  pl->total_cells = pl->q ? (pl->h_offsets[U] + pl->G - 1) / pl->G * pl->G : pl->h_offsets[U];
+  if (pl->q) {
+    pl->n_groups = pl->total_cells / pl->G;
+    pl->scales_off = (pl->code_bytes() + 255) / 256 * 256;
+  }
   pl->achieved_bits = 0;
   for (int l = 0; l < n_layers; ++l) {
     LayerGeom& L = pl->layers[l];
@@ -179,7 +209,8 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
     int32_t mx = 0;
     for (int64_t u = L.unit_begin; u < L.unit_begin + L.n_units; ++u) mx = std::max(mx, pl->h_ncols[u]);
     L.max_ncols = mx;
-    L.achieved_bits = L.n_cells * state_bits + L.meta_bits;
+    L.achieved_bits = pl->q ? (L.n_cells + pl->G - 1) / pl->G * ((int64_t)pl->q * pl->G + 32) + L.meta_bits
+                            : L.n_cells * state_bits + L.meta_bits;
     pl->achieved_bits += L.achieved_bits;
   }
   *plan_out = pl;
@@ -194,8 +225,12 @@ usk_status usk_plan_query(const usk_plan* pl, usk_plan_info* out) {
   out->dtype = pl->dtype;
   out->n_units = pl->U;
   out->total_cells = pl->total_cells;
-  const int64_t bytes = pl->total_cells * pl->cell_bytes();
+  const int64_t bytes = pl->q ? pl->scales_off + pl->n_groups * 4 : pl->total_cells * pl->cell_bytes();
   out->sketch_bytes = ((bytes + 255) / 256) * 256 + 256;
+  out->state_bits = pl->q;
+  out->group_size = pl->q ? pl->G : 0;
+  out->n_groups = pl->n_groups;
+  out->scales_offset = pl->scales_off;
   out->numel = pl->numel;
   out->budget_bits = pl->budget_bits;
   out->achieved_bits = pl->achieved_bits;

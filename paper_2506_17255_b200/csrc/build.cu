@@ -302,6 +302,52 @@ __global__ void k_gen_final(void* sketch, int64_t c0, int64_t n) {
   }
 }
 
+// ---------------------------------------------------------------- stacked state quantisation
+// (scheme: SPEC.md quant module, DESIGN.md ledger L25)
+template <int ES>
+__global__ void k_fill_inf(void* raw, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (ES == 2) reinterpret_cast<uint16_t*>(raw)[i] = 0x7F80;  // empty = +Inf
+  else reinterpret_cast<uint32_t*>(raw)[i] = 0x7F800000u;
+}
+
+// One warp per group of G cells (cell c = g*G + j, lane j mod 32): scale = fl32(absmax / qmax)
+// over occupied (finite) cells, code = clamp(roundf(fl32(v / scale)), +-qmax) (round half away
+// from zero), unoccupied cells and zero scales -> code 0.  Codes are stored packed: q = 8 one
+// byte per cell, q = 4 two per byte with the even cell in the low nibble; scales as fp32.
+template <int ES, int Q>
+__global__ void k_quantize(const void* raw, int64_t g0, int64_t g1, int G, uint8_t* codes, float* scales) {
+  const int64_t g = g0 + (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (g >= g1) return;  // uniform per warp
+  const float qmax = Q == 4 ? 7.f : 127.f;
+  auto value = [&](int64_t c) {
+    return ES == 2 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(raw)[c] << 16)
+                   : __uint_as_float(reinterpret_cast<const uint32_t*>(raw)[c]);
+  };
+  uint32_t amax = 0;  // bit pattern of max |v| (order-preserving for non-negative floats)
+  for (int j = lane; j < G; j += 32) {
+    const float v = value(g * G + j);
+    if (isfinite(v)) amax = max(amax, __float_as_uint(fabsf(v)));
+  }
+  amax = __reduce_max_sync(0xffffffffu, amax);
+  const float scale = __fdiv_rn(__uint_as_float(amax), qmax);
+  if (lane == 0) scales[g] = scale;
+  for (int j = lane; j < G; j += 32) {  // G % 32 == 0: every lane runs the same trip count
+    const float v = value(g * G + j);
+    int code = 0;
+    if (isfinite(v) && scale > 0.f) code = (int)fminf(fmaxf(roundf(__fdiv_rn(v, scale)), -qmax), qmax);
+    const int64_t c = g * G + j;
+    if constexpr (Q == 8) {
+      codes[c] = (uint8_t)(int8_t)code;
+    } else {
+      const int hi = __shfl_down_sync(0xffffffffu, code, 1);
+      if ((lane & 1) == 0) codes[c >> 1] = (uint8_t)((code & 0xF) | ((hi & 0xF) << 4));
+    }
+  }
+}
+
 // ---------------------------------------------------------------- host side
 int fast_upl(const usk_plan* pl, int32_t l) {
   // units per lane for the fast kernels, 0 = not eligible: the largest UPL whose key array and
@@ -409,8 +455,8 @@ usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* 
 
 bool layer_fast_ok(const usk_plan* pl, int32_t l) { return fast_upl(pl, l) != 0; }
 
-usk_status launch_build(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
-                        void* sketch, cudaStream_t st) {
+static usk_status launch_build_raw(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids,
+                                   int32_t n, void* sketch, cudaStream_t st) {
   std::vector<std::pair<int32_t, const void*>> grp[5];  // by units per lane (1, 2, 4)
   for (int32_t k = 0; k < n; ++k) {
     const int32_t l = layer_ids ? layer_ids[k] : k;
@@ -429,6 +475,44 @@ usk_status launch_build(const usk_plan* pl, const void* const* weights, const in
     if (s != USK_OK) return s;
   }
   return USK_OK;
+}
+
+// Quantised plans (L25): raw states are built into a stream-ordered temporary buffer
+// with the plan's (G-aligned) cell offsets, then quantised group by group into the sketch:
+// codes at byte 0, fp32 scales at scales_off.  Groups never straddle layers, so a layer-sharded
+// build quantises exactly the groups of its layers.
+usk_status launch_build(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
+                        void* sketch, cudaStream_t st) {
+  if (!pl->q) return launch_build_raw(pl, weights, layer_ids, n, sketch, st);
+  const int es = pl->cell_bytes();
+  void* raw = nullptr;
+  USK_CUDA(cudaMallocAsync(&raw, (size_t)pl->total_cells * es + 256, st));
+  const unsigned fb = (unsigned)((pl->total_cells + 255) / 256);
+  if (es == 2) k_fill_inf<2><<<fb, 256, 0, st>>>(raw, pl->total_cells);
+  else k_fill_inf<4><<<fb, 256, 0, st>>>(raw, pl->total_cells);
+  USK_LAUNCHED("k_fill_inf");
+  usk_status s = launch_build_raw(pl, weights, layer_ids, n, raw, st);
+  uint8_t* codes = reinterpret_cast<uint8_t*>(sketch);
+  float* scales = reinterpret_cast<float*>(reinterpret_cast<char*>(sketch) + pl->scales_off);
+  for (int32_t k = 0; k < n && s == USK_OK; ++k) {
+    const LayerGeom& L = pl->layers[layer_ids ? layer_ids[k] : k];
+    const int64_t g0 = L.cell_begin / pl->G, g1 = (L.cell_begin + L.n_cells + pl->G - 1) / pl->G;
+    if (g1 <= g0) continue;
+    const unsigned blocks = (unsigned)((g1 - g0 + 7) / 8);  // 8 warps (groups) per block
+    if (es == 2) {
+      if (pl->q == 4) k_quantize<2, 4><<<blocks, 256, 0, st>>>(raw, g0, g1, pl->G, codes, scales);
+      else k_quantize<2, 8><<<blocks, 256, 0, st>>>(raw, g0, g1, pl->G, codes, scales);
+    } else {
+      if (pl->q == 4) k_quantize<4, 4><<<blocks, 256, 0, st>>>(raw, g0, g1, pl->G, codes, scales);
+      else k_quantize<4, 8><<<blocks, 256, 0, st>>>(raw, g0, g1, pl->G, codes, scales);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) s = cuda_fail(e, "k_quantize");
+    else count_launch();
+  }
+  cudaError_t e = cudaFreeAsync(raw, st);
+  if (s == USK_OK && e != cudaSuccess) s = cuda_fail(e, "usk_build: cudaFreeAsync");
+  return s;
 }
 
 }  // namespace usk

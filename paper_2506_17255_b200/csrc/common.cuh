@@ -102,7 +102,12 @@ struct usk_plan {
   uint32_t* d_R = nullptr;     // R(o) = fmix32(o ^ rho), o < max_out (g = 1 positions)
   int* d_err = nullptr;        // sticky device error flag
   int device = 0;
-  int cell_bytes() const { return dtype == USK_BF16 ? 2 : 4; }
+  // stacked state quantisation (L25): q = 0 (raw states) or 4 / 8 bits
+  int32_t q = 0, G = 128;
+  int64_t n_groups = 0;       // total_cells / G (quantised)
+  int64_t scales_off = 0;     // byte offset of the fp32 group scales in the sketch (quantised)
+  int cell_bytes() const { return dtype == USK_BF16 ? 2 : 4; }  // raw state bytes
+  int64_t code_bytes() const { return (total_cells * q + 7) / 8; }
 };
 
 namespace usk {

@@ -93,6 +93,9 @@ struct QArgs {
   int32_t x_bf16;
   int32_t y_bf16;
   int32_t red_lanes;               // GEMV reduce: lanes per row (power of two <= 32)
+  int32_t g_shift;                 // quantised plans: log2(group size)
+  int32_t sbuf_off;                // quantised plans: byte offset of the staged scales from the raw buffer
+  const float* scales;             // quantised plans: fp32 group scales (in the sketch buffer)
   int32_t cta_item[kMaxCtas + 1];  // GEMV: CTA c computes work items [cta_item[c], cta_item[c + 1])
   unsigned long long* timeline;  // tuning only (USK_TRACE): 4 globaltimer stamps per CTA
 };
@@ -140,16 +143,31 @@ __device__ __forceinline__ unsigned char* q_raw(const QArgs& A) {
   return reinterpret_cast<unsigned char*>(qsm + kCellsWordOffset + UPL * 32 * A.maxMN);
 }
 
-// thread 0: bulk copy of the cells of units [ubase + pa, ubase + pa + pn) into the raw buffer
-template <typename E, int UPL>
+// thread 0: bulk copy of the cells of units [ubase + pa, ubase + pa + pn) into the raw buffer.
+// Quantised plans (QB = 4 / 8 bits, L25): the cells' packed codes into the raw buffer and
+// their groups' fp32 scales into the scale buffer, both on the same mbarrier.
+template <typename E, int UPL, int QB>
 __device__ __forceinline__ void stage_issue(const QArgs& A, int64_t ubase, int pa, int pn) {
   constexpr int ES = sizeof(E);
-  const uint64_t g0 = (uint64_t)A.offsets[ubase + pa] * ES, g1 = (uint64_t)A.offsets[ubase + pa + pn] * ES;
-  const uint64_t a0 = g0 & ~uint64_t(15), a1 = (g1 + 15) & ~uint64_t(15);
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // earlier generic reads of raw
-  mbar_arrive_expect_tx(q_bar(), (uint32_t)(a1 - a0));
-  bulk_g2s(q_raw<E, UPL>(A), reinterpret_cast<const unsigned char*>(A.sketch) + a0, (uint32_t)(a1 - a0), q_bar());
-  qsm[34] = (uint32_t)(g0 - a0);  // copy shift
+  if constexpr (QB == 0) {
+    const uint64_t g0 = (uint64_t)A.offsets[ubase + pa] * ES, g1 = (uint64_t)A.offsets[ubase + pa + pn] * ES;
+    const uint64_t a0 = g0 & ~uint64_t(15), a1 = (g1 + 15) & ~uint64_t(15);
+    mbar_arrive_expect_tx(q_bar(), (uint32_t)(a1 - a0));
+    bulk_g2s(q_raw<E, UPL>(A), reinterpret_cast<const unsigned char*>(A.sketch) + a0, (uint32_t)(a1 - a0), q_bar());
+    qsm[34] = (uint32_t)(g0 - a0);  // copy shift
+  } else {
+    const int64_t c0 = A.offsets[ubase + pa], c1 = A.offsets[ubase + pa + pn];
+    const uint64_t a0 = ((uint64_t)c0 * QB / 8) & ~uint64_t(15), a1 = (((uint64_t)c1 * QB + 7) / 8 + 15) & ~uint64_t(15);
+    const uint64_t s0 = ((uint64_t)(c0 >> A.g_shift) * 4) & ~uint64_t(15);
+    const uint64_t s1 = ((uint64_t)(((c1 - 1) >> A.g_shift) + 1) * 4 + 15) & ~uint64_t(15);
+    mbar_arrive_expect_tx(q_bar(), (uint32_t)((a1 - a0) + (s1 - s0)));
+    bulk_g2s(q_raw<E, UPL>(A), reinterpret_cast<const unsigned char*>(A.sketch) + a0, (uint32_t)(a1 - a0), q_bar());
+    bulk_g2s(q_raw<E, UPL>(A) + A.sbuf_off, reinterpret_cast<const unsigned char*>(A.scales) + s0, (uint32_t)(s1 - s0),
+             q_bar());
+    reinterpret_cast<uint64_t*>(qsm + 34)[0] = a0;      // byte of code storage at raw[0]
+    reinterpret_cast<uint64_t*>(qsm + 36)[0] = s0 / 4;  // group of scale buffer entry 0
+  }
 }
 
 // Stage the cells of units [ubase, ubase + nu) (consecutive in the sketch, so contiguous bytes)
@@ -157,7 +175,9 @@ __device__ __forceinline__ void stage_issue(const QArgs& A, int64_t ubase, int p
 // copy each (cp.async.bulk, mbarrier completion) and converted shared -> shared.  The first
 // piece may have been issued already (first_issued; thread 0 called stage_issue).  Ends with a
 // __syncthreads (cells complete, raw buffer free).  The mbarrier phase advances once per piece.
-template <typename E, int UPL>
+// Quantised plans convert each cell to its dequantised value fl32(code * scale) first, so the
+// query loop is the same for every plan (the rho of an fp32 value).
+template <typename E, int UPL, int QB>
 __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int nu, uint32_t& phase,
                                             bool first_issued) {
   constexpr int ES = sizeof(E);
@@ -166,27 +186,50 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
   const int pu = A.piece_units;
   for (int pa = 0; pa < nu; pa += pu) {
     const int pn = min(pu, nu - pa);
-    if (threadIdx.x == 0 && !(pa == 0 && first_issued)) stage_issue<E, UPL>(A, ubase, pa, pn);
+    if (threadIdx.x == 0 && !(pa == 0 && first_issued)) stage_issue<E, UPL, QB>(A, ubase, pa, pn);
     const int t = threadIdx.x & (pu - 1);
     const int ul = pa + t;
-    int64_t u_off = 0;
+    int64_t u_off = 0, cu = 0;
     int n = 0;  // N of the thread's unit (0: no unit)
     if (t < pn) {  // overlaps the copy
-      u_off = A.offsets[ubase + ul] - A.offsets[ubase + pa];
+      cu = A.offsets[ubase + ul];
+      u_off = cu - A.offsets[ubase + pa];
       n = A.ncols[ubase + ul];
     }
     __syncthreads();  // shift visible
     mbar_wait(q_bar(), phase);
     phase ^= 1u;
-    const unsigned char* src = raw + qsm[34] + u_off * ES;
     uint32_t* dst = cells + (ul % UPL) * 32 * A.maxMN + ul / UPL;
     const int KS = kQThreads / pu;
-    for (int i = 0; i < A.M; ++i, src += n * ES, dst += A.maxN * 32) {  // sketch row i -> slot row i
+    if constexpr (QB == 0) {
+      const unsigned char* src = raw + qsm[34] + u_off * ES;
+      for (int i = 0; i < A.M; ++i, src += n * ES, dst += A.maxN * 32) {  // sketch row i -> slot row i
 #pragma unroll 4
-      for (int k = threadIdx.x / pu; k < n; k += KS) {
-        const uint32_t b = ES == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
-                                   : reinterpret_cast<const uint32_t*>(src)[k];
-        dst[k * 32] = rotl1(b) ^ 1u;
+        for (int k = threadIdx.x / pu; k < n; k += KS) {
+          const uint32_t b = ES == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
+                                     : reinterpret_cast<const uint32_t*>(src)[k];
+          dst[k * 32] = rotl1(b) ^ 1u;
+        }
+      }
+    } else {
+      const uint64_t a0 = reinterpret_cast<const uint64_t*>(qsm + 34)[0];
+      const uint64_t sg0 = reinterpret_cast<const uint64_t*>(qsm + 36)[0];
+      const float* sb = reinterpret_cast<const float*>(raw + A.sbuf_off);
+      for (int i = 0; i < A.M; ++i, dst += A.maxN * 32) {
+#pragma unroll 4
+        for (int k = threadIdx.x / pu; k < n; k += KS) {
+          const int64_t c = cu + (int64_t)i * n + k;  // global cell
+          int code;
+          if constexpr (QB == 8) {
+            code = (int)(int8_t)raw[(uint64_t)c - a0];
+          } else {
+            const uint32_t byte = raw[((uint64_t)c >> 1) - a0];
+            code = (int)((byte >> ((c & 1) * 4)) & 0xFu);
+            code = (code ^ 8) - 8;  // sign-extend the nibble
+          }
+          const float v = __fmul_rn((float)code, sb[((uint64_t)c >> A.g_shift) - sg0]);
+          dst[k * 32] = rotl1(__float_as_uint(v)) ^ 1u;
+        }
       }
     }
     __syncthreads();
@@ -261,9 +304,15 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 #define USK_GEMV_MAXREG 112  // 512 x 112 + 256 x 32 registers: k_gemv_fast + k_gemv_reduce share an SM
 #endif
 
-// store the UPL reconstructed weights (bits in the high half for bf16) of lane L's units
-template <typename E, int UPL>
-__device__ __forceinline__ void store_units(E* dst, const uint32_t (&wb)[UPL], bool full_tile, int nu, int lane) {
+// store the UPL reconstructed weights (fp32 bit patterns; raw bf16 plans: bf16 bits in the high
+// half, exact) of lane L's units.  RNE: quantised plans round the fp32 dequantised value to bf16
+// (round to nearest even, L25); raw bf16 plans take the high half as it is.
+template <typename E, int UPL, bool RNE>
+__device__ __forceinline__ void store_units(E* dst, uint32_t (&wb)[UPL], bool full_tile, int nu, int lane) {
+  if constexpr (sizeof(E) == 2 && RNE) {
+#pragma unroll
+    for (int v = 0; v < UPL; ++v) wb[v] = wb[v] + 0x7FFFu + ((wb[v] >> 16) & 1u);
+  }
   if constexpr (sizeof(E) == 2) {
     if (full_tile) {
       if constexpr (UPL == 4) {
@@ -303,7 +352,7 @@ __device__ __forceinline__ void store_units(E* dst, const uint32_t (&wb)[UPL], b
 //    beside k_gemv_fast's (register budget 112 + 32 per thread), wait there for the partials
 //    (griddepcontrol.wait), and the NEXT call's k_gemv_fast stages its sketch chunk while they
 //    reduce.
-template <typename E, int UPL, int MT, int HASH, bool GEMV>
+template <typename E, int UPL, int MT, int HASH, bool GEMV, int QB>
 __device__ __forceinline__ void query_balanced(const QArgs& A) {
   constexpr int TJ = 32 * UPL;
   __shared__ int s_next;  // next subtile of the current segment (warps grab dynamically)
@@ -338,14 +387,14 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
     Seg cur = seg_at(s_begin);
     if (threadIdx.x == 0) {
       s_next = cur.sub_a;
-      stage_issue<E, UPL>(A, cur.ubase, 0, min(A.piece_units, cur.nu));  // first piece in flight
+      stage_issue<E, UPL, QB>(A, cur.ubase, 0, min(A.piece_units, cur.nu));  // first piece in flight
     }
     bool stamped = false;
     while (true) {
       const QLayer& Ly = A.layer[cur.li];
       LaneState<UPL, MT> S;
       lane_setup<UPL, MT>(A, cur.ubase, cur.nu, S);  // overlaps the copy
-      stage_units<E, UPL>(A, cur.ubase, cur.nu, phase, true);  // sketch only: before the wait
+      stage_units<E, UPL, QB>(A, cur.ubase, cur.nu, phase, true);  // sketch only: before the wait
       if (!waited) {
         pdl_wait();     // x may be written by the previous kernel on the stream
         pdl_trigger();  // every CTA of this grid is running: the next launch may be scheduled
@@ -368,7 +417,7 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
       Seg nxt_seg = cur;
       if (more) {
         nxt_seg = seg_at(cur.end);
-        if (threadIdx.x == 0) stage_issue<E, UPL>(A, nxt_seg.ubase, 0, min(A.piece_units, nxt_seg.nu));
+        if (threadIdx.x == 0) stage_issue<E, UPL, QB>(A, nxt_seg.ubase, 0, min(A.piece_units, nxt_seg.nu));
       }
       const int rl = lane & (kSubRows - 1);  // lanes congruent to r mod kSubRows hold R(o0 + r)
       auto next_sub = [&]() -> int {
@@ -411,7 +460,7 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
 #pragma unroll
             for (int v = 0; v < UPL; ++v)
               wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r)) ^ 0x80000000u;
-            store_units<E, UPL>(dst, wb, full_tile, cur.nu, lane);
+            store_units<E, UPL, QB != 0>(dst, wb, full_tile, cur.nu, lane);
           }
         }
         sub = nxt;
@@ -433,16 +482,16 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
   }
 }
 
-template <typename E, int UPL, int MT, int HASH>
+template <typename E, int UPL, int MT, int HASH, int QB>
 __global__ void __maxnreg__(USK_GEMV_MAXREG) k_gemv_fast(const __grid_constant__ QArgs A) {
-  query_balanced<E, UPL, MT, HASH, true>(A);
+  query_balanced<E, UPL, MT, HASH, true, QB>(A);
 }
 
 // K3 fast path: the same balanced chunk-major partition, staging and per-subtile select as
 // k_gemv_fast, with W' rows stored instead of multiplied (no x, no reduction).
-template <typename E, int UPL, int MT, int HASH>
+template <typename E, int UPL, int MT, int HASH, int QB>
 __global__ void __maxnreg__(USK_GEMV_MAXREG) k_recon_fast(const __grid_constant__ QArgs A) {
-  query_balanced<E, UPL, MT, HASH, false>(A);
+  query_balanced<E, UPL, MT, HASH, false, QB>(A);
 }
 
 constexpr int kRedThreads = 256;
@@ -500,7 +549,25 @@ struct GenQ {
   HashConsts hc;
   int64_t unit_base, out, in;
   int32_t M, gran, g, hash, es;
+  int32_t q, g_shift;     // quantised plans (L25)
+  const float* scales;
 };
+
+// cell value as fp32 bits (raw bf16: bits << 16; quantised: fl32(code * scale))
+__device__ __forceinline__ uint32_t gen_cell_bits(const GenQ& Q, int64_t c) {
+  if (Q.q == 0)
+    return Q.es == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(Q.sketch)[c] << 16)
+                     : reinterpret_cast<const uint32_t*>(Q.sketch)[c];
+  const uint8_t* codes = reinterpret_cast<const uint8_t*>(Q.sketch);
+  int code;
+  if (Q.q == 8) {
+    code = (int)(int8_t)codes[c];
+  } else {
+    code = (int)((codes[c >> 1] >> ((c & 1) * 4)) & 0xFu);
+    code = (code ^ 8) - 8;
+  }
+  return __float_as_uint(__fmul_rn((float)code, Q.scales[c >> Q.g_shift]));
+}
 
 __device__ __forceinline__ uint32_t gen_weight_bits_hi(const GenQ& Q, int64_t o, int64_t j) {
   int64_t t, p;
@@ -514,9 +581,7 @@ __device__ __forceinline__ uint32_t gen_weight_bits_hi(const GenQ& Q, int64_t o,
   for (int i = 0; i < Q.M; ++i) {
     const uint32_t idx = Q.hash == USK_HASH_X ? __umulhi(h * Q.hc.a[i], N) : (uint32_t)(p % N);
     const int64_t c = off + (int64_t)i * N + idx;
-    uint32_t b = Q.es == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(Q.sketch)[c] << 16)
-                           : reinterpret_cast<const uint32_t*>(Q.sketch)[c];
-    best = max(best, rotl1(b) ^ 1u);
+    best = max(best, rotl1(gen_cell_bits(Q, c)) ^ 1u);
   }
   return rotr1(best) ^ 0x80000000u;
 }
@@ -525,7 +590,8 @@ __global__ void k_reconstruct_gen(GenQ Q, int64_t o0, int64_t o1, void* w_out, i
   const int64_t n = (o1 - o0) * Q.in;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / Q.in, j = e - r * Q.in;
-    const uint32_t b = gen_weight_bits_hi(Q, o0 + r, j);
+    uint32_t b = gen_weight_bits_hi(Q, o0 + r, j);
+    if (Q.es == 2 && Q.q) b = b + 0x7FFFu + ((b >> 16) & 1u);  // quantised: RNE to bf16
     if (Q.es == 2) reinterpret_cast<uint16_t*>(w_out)[r * ld + j] = (uint16_t)(b >> 16);
     else reinterpret_cast<uint32_t*>(w_out)[r * ld + j] = b;
   }
@@ -572,44 +638,80 @@ bool fast_eligible(const usk_plan* pl) { return pl->gran == USK_GRAN_ROW && pl->
 
 constexpr size_t kSmemMax = 220 * 1024;
 
-// [zero + mbarrier + shift][rho cells][raw bulk-copy buffer for `pu` units (+ alignment slack)]
-size_t smem_bytes(int upl, int maxMN, int es, int pu) {
-  return kCellsWordOffset * 4 + (size_t)32 * upl * maxMN * 4 + (size_t)pu * maxMN * es + 48;
+// raw staging bytes of `pu` units: cell bytes (raw plans) or packed codes (quantised, q bits);
+// the staged scales follow at a 16-B aligned offset (quantised plans)
+size_t raw_bytes(int maxMN, int es, int q, int pu) {
+  return q ? ((size_t)pu * maxMN * q + 7) / 8 + 48 : (size_t)pu * maxMN * es + 48;
+}
+size_t sbuf_bytes(int maxMN, int q, int g_shift, int pu) {
+  return q ? ((((size_t)pu * maxMN) >> g_shift) + 3) * 4 + 32 : 0;
 }
 
-template <typename E, int UPL, bool GEMV>
+// [zero + mbarrier + copy bases][rho cells][raw bulk-copy buffer for `pu` units][scales]
+size_t smem_bytes(int upl, int maxMN, int es, int pu, int q = 0, int g_shift = 7) {
+  return kCellsWordOffset * 4 + (size_t)32 * upl * maxMN * 4 + (raw_bytes(maxMN, es, q, pu) + 15) / 16 * 16 +
+         sbuf_bytes(maxMN, q, g_shift, pu);
+}
+
+template <typename E, int UPL, bool GEMV, int QB>
 void* pick_m(int M, int hash) {
   if constexpr (GEMV) {
-    if (hash == USK_HASH_IDENTITY) return (void*)k_gemv_fast<E, UPL, 0, USK_HASH_IDENTITY>;
-    switch (M) {
-      case 1: return (void*)k_gemv_fast<E, UPL, 1, USK_HASH_X>;
-      case 2: return (void*)k_gemv_fast<E, UPL, 2, USK_HASH_X>;
-      case 3: return (void*)k_gemv_fast<E, UPL, 3, USK_HASH_X>;
-      default: return (void*)k_gemv_fast<E, UPL, 0, USK_HASH_X>;
+    if (hash == USK_HASH_IDENTITY) return (void*)k_gemv_fast<E, UPL, 0, USK_HASH_IDENTITY, QB>;
+    if constexpr (QB == 0) {
+      switch (M) {
+        case 1: return (void*)k_gemv_fast<E, UPL, 1, USK_HASH_X, QB>;
+        case 2: return (void*)k_gemv_fast<E, UPL, 2, USK_HASH_X, QB>;
+        default: break;
+      }
     }
+    return M == 3 ? (void*)k_gemv_fast<E, UPL, 3, USK_HASH_X, QB> : (void*)k_gemv_fast<E, UPL, 0, USK_HASH_X, QB>;
   } else {
-    if (hash == USK_HASH_IDENTITY) return (void*)k_recon_fast<E, UPL, 0, USK_HASH_IDENTITY>;
-    switch (M) {
-      case 1: return (void*)k_recon_fast<E, UPL, 1, USK_HASH_X>;
-      case 2: return (void*)k_recon_fast<E, UPL, 2, USK_HASH_X>;
-      case 3: return (void*)k_recon_fast<E, UPL, 3, USK_HASH_X>;
-      default: return (void*)k_recon_fast<E, UPL, 0, USK_HASH_X>;
+    if (hash == USK_HASH_IDENTITY) return (void*)k_recon_fast<E, UPL, 0, USK_HASH_IDENTITY, QB>;
+    if constexpr (QB == 0) {
+      switch (M) {
+        case 1: return (void*)k_recon_fast<E, UPL, 1, USK_HASH_X, QB>;
+        case 2: return (void*)k_recon_fast<E, UPL, 2, USK_HASH_X, QB>;
+        default: break;
+      }
     }
+    return M == 3 ? (void*)k_recon_fast<E, UPL, 3, USK_HASH_X, QB> : (void*)k_recon_fast<E, UPL, 0, USK_HASH_X, QB>;
   }
+}
+
+// quantised plans: the GEMV does not depend on the weight dtype (dequantised fp32 values, fp32 y),
+// so only one E is instantiated for it; the reconstruct stores in the weight dtype
+template <int UPL, int QB>
+void* pick_q(bool gemv, bool bf16, int M, int hash) {
+  if (gemv) {
+    if constexpr (QB == 0)
+      return bf16 ? pick_m<uint16_t, UPL, true, 0>(M, hash) : pick_m<uint32_t, UPL, true, 0>(M, hash);
+    else
+      return pick_m<uint32_t, UPL, true, QB>(M, hash);
+  }
+  return bf16 ? pick_m<uint16_t, UPL, false, QB>(M, hash) : pick_m<uint32_t, UPL, false, QB>(M, hash);
 }
 
 template <int UPL>
-void* pick_upl(bool gemv, bool bf16, int M, int hash) {
-  if (gemv) return bf16 ? pick_m<uint16_t, UPL, true>(M, hash) : pick_m<uint32_t, UPL, true>(M, hash);
-  return bf16 ? pick_m<uint16_t, UPL, false>(M, hash) : pick_m<uint32_t, UPL, false>(M, hash);
+void* pick_upl(bool gemv, bool bf16, int M, int hash, int q) {
+  switch (q) {
+    case 4: return pick_q<UPL, 4>(gemv, bf16, M, hash);
+    case 8: return pick_q<UPL, 8>(gemv, bf16, M, hash);
+    default: return pick_q<UPL, 0>(gemv, bf16, M, hash);
+  }
 }
 
-void* pick_fast(int upl, bool gemv, bool bf16, int M, int hash) {
+void* pick_fast(int upl, bool gemv, bool bf16, int M, int hash, int q) {
   switch (upl) {
-    case 4: return pick_upl<4>(gemv, bf16, M, hash);
-    case 2: return pick_upl<2>(gemv, bf16, M, hash);
-    default: return pick_upl<1>(gemv, bf16, M, hash);
+    case 4: return pick_upl<4>(gemv, bf16, M, hash, q);
+    case 2: return pick_upl<2>(gemv, bf16, M, hash, q);
+    default: return pick_upl<1>(gemv, bf16, M, hash, q);
   }
+}
+
+int ilog2(int v) {
+  int r = 0;
+  while ((1 << r) < v) ++r;
+  return r;
 }
 
 int sm_count() {
@@ -664,11 +766,9 @@ struct Geom {
   std::vector<int> n_chunks, n_sub;
 };
 
-// GEMV geometry.  Units per lane: the largest UPL whose CTA fits the shared-memory budget
-// (default 176 KB: leaves room on the SM for a 49 KB CTA of the next launch, which then stages
-// its chunk while this one computes); the raw staging buffer shrinks to pieces of pu units
-// before UPL does.  Grid: one CTA per SM (USK_GEMV_CPS per SM for tuning), never more than one
-// resident wave (the kernel's grid barrier relies on it) nor more than the work items.
+// Query geometry (K3 and K4).  Units per lane: the largest UPL whose CTA fits the shared-memory
+// budget (default 220 KB); the raw staging buffer shrinks to pieces of pu units before UPL does.
+// Grid: one CTA per SM (USK_GEMV_CPS per SM for tuning), never more than the work items.
 // USK_UPL / USK_GEMV_SMEM_KB / USK_GEMV_CPS override (tuning).
 Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n, bool gemv = true) {
   Geom G;
@@ -684,9 +784,9 @@ Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* row
     for (int upl : {4, 2, 1}) {
       if (forced && upl != forced) continue;
       for (int pu = 32 * upl; pu >= 8; pu /= 2) {
-        const size_t sm = smem_bytes(upl, G.maxMN, es, pu);
+        const size_t sm = smem_bytes(upl, G.maxMN, es, pu, pl->q, ilog2(pl->G));
         if (sm > cap) continue;
-        void* kern = pick_fast(upl, gemv, bf16, pl->M, pl->hash);
+        void* kern = pick_fast(upl, gemv, bf16, pl->M, pl->hash, pl->q);
         const int occ = occupancy(kern, sm);
         if (occ < 1) continue;
         G.upl = upl;
@@ -728,6 +828,11 @@ QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& 
   A.offsets = pl->d_offsets;
   A.ukeys = pl->d_keys;
   A.hc = pl->hc;
+  if (pl->q) {
+    A.g_shift = ilog2(pl->G);
+    A.sbuf_off = (int32_t)((raw_bytes(G.maxMN, pl->cell_bytes(), pl->q, G.pu) + 15) / 16 * 16);
+    A.scales = reinterpret_cast<const float*>(reinterpret_cast<const char*>(sketch) + pl->scales_off);
+  }
   return A;
 }
 
@@ -840,6 +945,9 @@ GenQ make_genq(const usk_plan* pl, int32_t l, const void* sketch) {
   Q.g = pl->g;
   Q.hash = pl->hash;
   Q.es = pl->cell_bytes();
+  Q.q = pl->q;
+  Q.g_shift = ilog2(pl->G);
+  Q.scales = pl->q ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(sketch) + pl->scales_off) : nullptr;
   return Q;
 }
 

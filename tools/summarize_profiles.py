@@ -18,6 +18,7 @@ import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(ROOT, "tools"))
+sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 
@@ -36,11 +37,12 @@ def json_line(path):
 # ---- bench lines
 bl = json_line(os.path.join(OUT, "bench_full.log"))
 rl = json_line(os.path.join(OUT, "bench_ref.log")) if os.path.exists(os.path.join(OUT, "bench_ref.log")) else None
-with open(os.path.join(PROF, f"{args.tag}_bench.jsonl"), "a") as f:
-    if bl:
-        f.write(bl + "\n")
-    if rl:
-        f.write(rl + "\n")
+bp = os.path.join(PROF, f"{args.tag}_bench.jsonl")
+have = open(bp).read().splitlines() if os.path.exists(bp) else []
+with open(bp, "a") as f:
+    for line in (bl, rl):
+        if line and line not in have:
+            f.write(line + "\n")
 
 # ---- launch list
 import launches  # noqa: E402
@@ -88,12 +90,10 @@ with open(os.path.join(PROF, f"{args.tag}_ncu_full_summary.txt"), "w") as f:
 # ---- traffic.json: DRAM bytes per k_gemv_fast launch (MB in the raw page) vs algorithmic
 if gemv_bytes:
     # algorithmic bytes of the 4 grouped calls of block 0: the block's sketch cells (bf16) + x + y
+    import oracle  # noqa: E402  (CPU plan: same cell counts as the GPU plan, tests/test_gpu_parity)
     import synth  # noqa: E402
-    sys.path.insert(0, ROOT)
-    from paper_2506_17255_b200 import usk  # noqa: E402
     shapes = synth.llama_block(2048, 512, 8192)
-    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=0x5EED000000000003)
-    cells = pl.info["total_cells"]
+    cells = oracle.plan(shapes, 0.5, M=3, dtype=oracle.BF16, seed=0x5EED000000000003).total_cells
     xy = sum(2 * i + 4 * o for o, i in shapes)
     alg = (2 * cells + xy) / 4
     json.dump({"k_gemv_fast_bytes_per_launch": sum(gemv_bytes) / len(gemv_bytes),
