@@ -422,6 +422,38 @@ def run_usk(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
+    # ---- the paper's own 0.5-bpw point: a 1/8-rate sketch of 4-bit states (Table 1 "+ q4",
+    #      SURVEY 8(f1)): same workload and grouping, q4 plan (G = 128), measured the same way
+    q4 = None
+    if world == 1 and not args.no_q4:
+        del g_rec, g2
+        torch.cuda.empty_cache()
+        qplan = usk.plan_allocation(shapes, bpw=BPW, rows=ROWS, seed=SEED, state_bits=4, group_size=128)
+        qsk = qplan.new_sketch(dev)
+        wq = [synth.torch_weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, l // 7, l % 7), dev)
+              for l in range(L)]
+        usk.build(qplan, wq, qsk)
+        torch.cuda.synchronize()
+        ev0.record()
+        usk.build(qplan, wq, qsk)
+        ev1.record()
+        torch.cuda.synchronize()
+        qbuild_ms = ev0.elapsed_time(ev1)
+        del wq
+        usk.check(qplan)
+        ws_q = [usk.new_batch_workspace(qplan, g, device=dev) for g in groups]
+
+        def step_q():
+            for gi, g in enumerate(groups):
+                usk.linear_batch(qplan, qsk, g, xg[gi], [ys_full[l] for l in g], ws_q[gi])
+
+        gq, lq = capture(step_q)
+        qms = time_steps(gq, step_q, max(20, args.steps // 4), args.warmup)
+        q4 = {"tokens_per_s": 1000.0 / qms, "ms_per_step": qms, "state_bits": 4, "group_size": 128,
+              "sketch_MB": qplan.sketch_bytes / 1e6, "cells": qplan.info["total_cells"],
+              "achieved_bpw": qplan.info["achieved_bits"] / qplan.info["numel"], "build_ms": qbuild_ms,
+              "launches_per_step": lq}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_decode_sample(shapes, host_block0_weights(shapes), budget_s=args.cpu_budget)
@@ -461,6 +493,8 @@ def run_usk(args):
         }
         if cpu is not None:
             line["cpu_baseline"] = cpu
+        if q4 is not None:
+            line["paper_point_q4"] = q4
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -475,6 +509,7 @@ def main():
     ap.add_argument("--impl", default="usk", choices=["usk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--no-q4", action="store_true", help="skip the q4-state (paper 0.5-bpw point) extra")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
