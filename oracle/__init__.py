@@ -77,6 +77,8 @@ def lib():
         L.uo_dequantize.argtypes = [i32, p, p, i64, p]
         L.uo_pack_codes.restype = i32
         L.uo_pack_codes.argtypes = [i32, p, i64, p]
+        L.uo_aggregate_grad.restype = i32
+        L.uo_aggregate_grad.argtypes = [p, i64, i64, i32, i32, i32, i64, p, p, i32, i32, u64, p]
         L.uo_f32_to_bf16_rne.restype = u32
         L.uo_f32_to_bf16_rne.argtypes = [u32]
         L.uo_build_units.restype = i32
@@ -385,6 +387,20 @@ def linear_rows(pl: Plan, sketch, l: int, x: np.ndarray, o_begin=0, o_end=None) 
     _check(lib().uo_linear_rows(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs), pl.M,
                                 pl.hash_kind, pl.seed, _ptr(x), T, o_begin, o_end, _ptr(y)), "linear_rows")
     return y
+
+
+def aggregate_grad(pl: Plan, l: int, grad: np.ndarray) -> np.ndarray:
+    """Aggregated-gradient baseline (Figure 4a): per cell of layer l, the 2^-48 fixed-point sum of
+    the gradients of the weights mapped to it in each sketch row (ledger L26).  grad: [out, in]
+    values (any float dtype, exact in fp64)."""
+    out, inn = pl.shapes[l]
+    ncols, offs = pl.layer_slices(l)
+    g = np.ascontiguousarray(grad, dtype=np.float64)
+    assert g.shape == (out, inn)
+    res = np.zeros(int(offs[-1] - offs[0]), dtype=np.float32)
+    _check(lib().uo_aggregate_grad(_ptr(g), out, inn, l, pl.gran, pl.g, len(ncols), _ptr(ncols), _ptr(offs), pl.M,
+                                   pl.hash_kind, pl.seed, _ptr(res)), "aggregate_grad")
+    return res
 
 
 def peak_memory(layer_bytes, sketch_bytes) -> int:

@@ -25,6 +25,9 @@
  *       remainder order are our reading (L9/L10): "parity unpinned" for those.
  *   uo_importance -- pinned (SPEC Eq. 7 examples, constant activations).
  *   uo_linear_rows -- pinned (numpy fp64 matmul of the oracle-verified W').
+ *   uo_aggregate_grad (aggregated-gradient baseline) -- pinned (SPEC example
+ *       0.1 + -0.3 -> -0.2, the exact fp64 sum within the fixed-point resolution, injective
+ *       mapping = identity, central finite differences of a shared-parameter loss).
  *   uo_quantize / uo_dequantize / uo_pack_codes / uo_f32_to_bf16_rne (stacked state
  *       quantisation) -- pinned (SPEC quant worked examples, round-trip error
  *       bound <= scale/2, code range, unoccupied -> 0, torch's bf16 RNE conversion).
@@ -686,6 +689,39 @@ int32_t uo_linear_rows(int32_t dtype, const void* sketch, int64_t out, int64_t i
     }
   }
   free(wrow);
+  return UO_OK;
+}
+
+/* Aggregated-gradient baseline ("estimate the gradient of trainable parameters by
+ * aggregating gradients from corresponding original weights", Figure 4a; SPEC aggregated_backward:
+ * shared_grad[s] = sum of the member gradients mapped to s).  Every weight (o, j) adds its
+ * gradient g to the cell (u, i, idx_i(u, p)) of each sketch row i.  The sum is defined in 2^-48
+ * fixed point so that it does not depend on the summation order (DESIGN.md ledger L26):
+ *   q(g) = rint(g * 2^48) (int64, ties to even), S = sum q (int64), cell_grad = fl32(fl64(S) * 2^-48).
+ * grad: [out, in] doubles (exact values of the fp32 / bf16 gradient); cell_grad: the layer's
+ * cells (offsets relative to offsets[0]). */
+int32_t uo_aggregate_grad(const double* grad, int64_t out, int64_t in, int32_t layer, int32_t gran,
+                          int32_t g, int64_t n_units, const int32_t* ncols, const int64_t* offsets,
+                          int32_t M, int32_t hash_kind, uint64_t seed, float* cell_grad) {
+  int64_t t, o, j, c;
+  const int64_t n_cells = offsets[n_units] - offsets[0];
+  int64_t* acc = (int64_t*)calloc((size_t)(n_cells > 0 ? n_cells : 1), sizeof(int64_t));
+  for (t = 0; t < n_units; t++) {
+    int64_t j0, j1;
+    uo_unit_span(gran, g, in, t, &j0, &j1);
+    for (o = 0; o < out; o++)
+      for (j = j0; j < j1; j++) {
+        const uint32_t p = (uint32_t)((j - j0) * out + o);
+        const int64_t q = llrint(grad[o * in + j] * 281474976710656.0); /* 2^48 */
+        int32_t i;
+        for (i = 0; i < M; i++) {
+          const uint32_t idx = uo_hash_index(hash_kind, seed, (uint32_t)layer, (uint32_t)t, i, p, (uint32_t)ncols[t]);
+          acc[offsets[t] - offsets[0] + (int64_t)i * ncols[t] + idx] += q;
+        }
+      }
+  }
+  for (c = 0; c < n_cells; c++) cell_grad[c] = (float)((double)acc[c] * (1.0 / 281474976710656.0));
+  free(acc);
   return UO_OK;
 }
 
