@@ -208,6 +208,22 @@ USK_API usk_status usk_linear_batch(const usk_plan* plan, const void* sketch, co
                                     void* const* y, int32_t y_dtype, void* workspace,
                                     size_t workspace_bytes, usk_stream stream);
 
+/* Aggregated-gradient baseline of finetuning (§3.3, Figure 4a; SPEC.md
+ * aggregated_backward): the gradient of a shared sketch state is the sum of the gradients of the
+ * weights mapped to it.  For every weight (o, j) of `layer` and every sketch row i,
+ *   cell_grad[c_i(o, j) - cell_begin] += grad[o, j],
+ * summed in 2^-48 fixed point (q = rint(g * 2^48) as int64, result fl32(fl64(sum) * 2^-48)), so the
+ * result does not depend on the summation order (DESIGN.md ledger L26; |sum| < 2^15).
+ *   grad: device [out, in] row-major of grad_dtype (USK_F32 / USK_BF16); cell_grad: device
+ *   float[n_cells of the layer]; workspace: device, >= usk_aggregate_grad_workspace_bytes, 16-B
+ *   aligned, zero-filled before first use -- every call leaves it zero-filled.
+ * Raw-state plans only (USK_EUNSUPPORTED for state_bits != 0).  The STE alternative (identity
+ * backward through build + reconstruct) needs no kernel of its own. */
+USK_API size_t usk_aggregate_grad_workspace_bytes(const usk_plan* plan, int32_t layer);
+USK_API usk_status usk_aggregate_grad(const usk_plan* plan, int32_t layer, const void* grad, int32_t grad_dtype,
+                                      float* cell_grad, void* workspace, size_t workspace_bytes,
+                                      usk_stream stream);
+
 /* Synchronises `stream`, returns and clears the plan's sticky device error (USK_ENONFINITE),
  * or USK_ECUDA on a CUDA error, else USK_OK. */
 USK_API usk_status usk_check(const usk_plan* plan, usk_stream stream);

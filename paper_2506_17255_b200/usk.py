@@ -80,6 +80,8 @@ def _load():
         "usk_status_string": (ct.c_char_p, [i32]),
         "usk_last_error": (ct.c_char_p, []),
         "usk_launch_count": (i64, [i32]),
+        "usk_aggregate_grad_workspace_bytes": (ct.c_size_t, [p, i32]),
+        "usk_aggregate_grad": (i32, [p, i32, p, i32, p, p, ct.c_size_t, p]),
         "usk_trace_read": (i32, [p, i64, p, i32]),
         "usk_trace_reset": (None, []),
     }
@@ -258,6 +260,18 @@ def linear_batch(plan: Plan, sketch, layers, x, ys, workspace, ranges=None, stre
 def importance(A, out, stream=None):
     """Eq. 7: out[j] = mean_k A[k, j]^2 (A [N, d] bf16/fp32 CUDA, out float32 [d])."""
     _check(lib.usk_importance(_ptr(A), _dtype_code(A), A.shape[0], A.shape[1], _ptr(out), _stream(stream)))
+
+
+def aggregate_grad(plan: Plan, layer: int, grad, cell_grad, workspace=None, stream=None):
+    """usk_aggregate_grad: cell_grad[c] = fixed-point sum of grad over the weights mapped to cell c
+    (aggregated-gradient baseline, Figure 4a).  cell_grad: float32 CUDA tensor [n_cells of layer]."""
+    import torch
+    if workspace is None:
+        workspace = torch.zeros(int(lib.usk_aggregate_grad_workspace_bytes(plan.handle, layer)), dtype=torch.uint8,
+                                device=grad.device)
+    _check(lib.usk_aggregate_grad(plan.handle, layer, _ptr(grad), _dtype_code(grad), _ptr(cell_grad), _ptr(workspace),
+                                  workspace.numel(), _stream(stream)))
+    return cell_grad
 
 
 def check(plan: Plan, stream=None):
