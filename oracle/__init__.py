@@ -22,6 +22,7 @@ SRC = os.path.join(HERE, "usk_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
 
 F32, BF16 = 0, 1
+ABSMAXMIN, ABSMINMAX, COUNTMIN = 0, 1, 2
 HASH_X, HASH_IDENTITY = 0, 1
 GRAN_ROW, GRAN_LAYER = 0, 1
 OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE = 0, 1, 2, 3, 4
@@ -82,13 +83,19 @@ def lib():
         L.uo_f32_to_bf16_rne.restype = u32
         L.uo_f32_to_bf16_rne.argtypes = [u32]
         L.uo_build_units.restype = i32
-        L.uo_build_units.argtypes = [i32, p, i64, i64, i32, i32, i32, i64, i64, p, p, i32, i32, u64, p]
+        L.uo_build_units.argtypes = [i32, p, i64, i64, i32, i32, i32, i64, i64, p, p, i32, i32, u64, p, i32]
         L.uo_reconstruct_rows.restype = i32
-        L.uo_reconstruct_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, i64, i64, p]
+        L.uo_reconstruct_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, i64, i64, p, i32]
         L.uo_reconstruct_entries.restype = i32
-        L.uo_reconstruct_entries.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, p, i64, p]
+        L.uo_reconstruct_entries.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, p, i64, p, i32]
         L.uo_linear_rows.restype = i32
-        L.uo_linear_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, p, i64, i64, i64, p]
+        L.uo_linear_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, p, i64, i64, i64, p, i32]
+        L.uo_retrieve_v.restype = u32
+        L.uo_retrieve_v.argtypes = [i32, i32, p, i32]
+        L.uo_sketch_unit_v.restype = i32
+        L.uo_sketch_unit_v.argtypes = [i32, i32, p, p, i64, i32, u64, u32, u32, i32, u32, p]
+        L.uo_stats.restype = i32
+        L.uo_stats.argtypes = [i32, p, p, i64, i64, i32, i32, i32, i64, p, p, i32, i32, u64, p]
         L.uo_peak_memory.restype = i64
         L.uo_peak_memory.argtypes = [p, p, i32]
     return _lib
@@ -211,6 +218,7 @@ class Plan:
     acct: np.ndarray        # [L, 4] budget bits, class-map bits, T, achieved bits
     state_bits: int = 0     # 0: raw states in the weight dtype; 4 / 8: stacked quantisation
     group: int = 128        # cells per quantisation group (layers start at multiples of it)
+    variant: int = 0        # ABSMAXMIN (the paper's sketch), ABSMINMAX, COUNTMIN (App. C.2)
     extra: dict = field(default_factory=dict)
 
     @property
@@ -227,7 +235,7 @@ class Plan:
 
 
 def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None, min_cols=1,
-         hash_kind=HASH_X, seed=0, state_bits=0, group=128) -> Plan:
+         hash_kind=HASH_X, seed=0, state_bits=0, group=128, variant=ABSMAXMIN) -> Plan:
     L = len(shapes)
     outf = np.array([s[0] for s in shapes], dtype=np.int64)
     inf = np.array([s[1] for s in shapes], dtype=np.int64)
@@ -250,7 +258,7 @@ def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None
                        _ptr(ncols), _ptr(offsets), _ptr(acct))
     _check(st, "plan")
     return Plan(list(map(tuple, zip(outf.tolist(), inf.tolist()))), dtype, M, gran, g, C, min_cols, hash_kind,
-                seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4), state_bits, group)
+                seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4), state_bits, group, variant)
 
 
 def _np_dtype(dtype):
@@ -270,7 +278,7 @@ def build_layer(pl: Plan, l: int, W: np.ndarray, sketch: np.ndarray, t_begin=0, 
     ncols, offs = pl.layer_slices(l)
     assert sketch.dtype == _np_dtype(pl.dtype) and sketch.flags["C_CONTIGUOUS"]
     _check(lib().uo_build_units(pl.dtype, _ptr(W), out, inn, l, pl.gran, pl.g, t_begin, t_end, _ptr(ncols),
-                                _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(sketch)), "build_units")
+                                _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(sketch), pl.variant), "build_units")
 
 
 @dataclass
@@ -358,7 +366,8 @@ def reconstruct_rows(pl: Plan, sketch, l: int, o_begin=0, o_end=None) -> np.ndar
     dt, cells = _retrieval_view(pl, sketch)
     res = np.zeros((o_end - o_begin, inn), dtype=_np_dtype(dt))
     _check(lib().uo_reconstruct_rows(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs),
-                                     pl.M, pl.hash_kind, pl.seed, o_begin, o_end, _ptr(res)), "reconstruct_rows")
+                                     pl.M, pl.hash_kind, pl.seed, o_begin, o_end, _ptr(res), pl.variant),
+           "reconstruct_rows")
     return _to_plan_dtype(pl, sketch, res)
 
 
@@ -369,8 +378,8 @@ def reconstruct_entries(pl: Plan, sketch, l: int, oj: np.ndarray) -> np.ndarray:
     oj = np.ascontiguousarray(oj, dtype=np.int64)
     res = np.zeros(len(oj), dtype=np.uint32)
     _check(lib().uo_reconstruct_entries(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols),
-                                        _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(oj), len(oj), _ptr(res)),
-           "reconstruct_entries")
+                                        _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(oj), len(oj), _ptr(res),
+                                        pl.variant), "reconstruct_entries")
     return _to_plan_dtype(pl, sketch, res).astype(np.uint32)
 
 
@@ -385,7 +394,7 @@ def linear_rows(pl: Plan, sketch, l: int, x: np.ndarray, o_begin=0, o_end=None) 
     dt, cells = _retrieval_view(pl, sketch)
     y = np.zeros((T, o_end - o_begin), dtype=np.float64)
     _check(lib().uo_linear_rows(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs), pl.M,
-                                pl.hash_kind, pl.seed, _ptr(x), T, o_begin, o_end, _ptr(y)), "linear_rows")
+                                pl.hash_kind, pl.seed, _ptr(x), T, o_begin, o_end, _ptr(y), pl.variant), "linear_rows")
     return y
 
 
@@ -401,6 +410,25 @@ def aggregate_grad(pl: Plan, l: int, grad: np.ndarray) -> np.ndarray:
     _check(lib().uo_aggregate_grad(_ptr(g), out, inn, l, pl.gran, pl.g, len(ncols), _ptr(ncols), _ptr(offs), pl.M,
                                    pl.hash_kind, pl.seed, _ptr(res)), "aggregate_grad")
     return res
+
+
+STATS_KEYS = ("weights", "untouched", "sign_errors", "zero_weights", "rel_exact", "rel_lt_1e-3", "rel_1e-3",
+              "rel_1e-2", "rel_1e-1", "rel_1", "rel_ge_10", "cells", "unoccupied")
+
+
+def stats(pl: Plan, l: int, W: np.ndarray, Wp: np.ndarray) -> dict:
+    """Compression report of layer l (ledger L27): counts keyed by STATS_KEYS."""
+    out, inn = pl.shapes[l]
+    ncols, offs = pl.layer_slices(l)
+    W = np.ascontiguousarray(W, dtype=_np_dtype(pl.dtype) if pl.dtype == BF16 else np.float32)
+    Wp = np.ascontiguousarray(Wp)
+    if pl.dtype == F32:
+        W = W.view(np.uint32)
+        Wp = Wp.view(np.uint32) if Wp.dtype != np.uint32 else Wp
+    counts = np.zeros(13, dtype=np.int64)
+    _check(lib().uo_stats(pl.dtype, _ptr(W), _ptr(Wp), out, inn, l, pl.gran, pl.g, len(ncols), _ptr(ncols), _ptr(offs),
+                          pl.M, pl.hash_kind, pl.seed, _ptr(counts)), "stats")
+    return dict(zip(STATS_KEYS, counts.tolist()))
 
 
 def peak_memory(layer_bytes, sketch_bytes) -> int:

@@ -53,6 +53,11 @@
 #define UO_GRAN_ROW 0
 #define UO_GRAN_LAYER 1
 
+/* sketch variants (Appendix C.2) */
+#define UO_ABSMAXMIN 0 /* the paper's sketch: keep min |.|, retrieve max |.| */
+#define UO_ABSMINMAX 1 /* "changes the order of the min and max operations" */
+#define UO_COUNTMIN 2  /* "adding the current weight ... retrieves ... minimum absolute value" */
+
 /* ------------------------------------------------------------------------------------
  * Hash family "USK-X" (paper Eq. 3, PAPER.md:239-243:
  * I = H(Addr(w)) with independent H_0..H_{M-1}; Addr(w) is the natural, storage-free
@@ -143,6 +148,36 @@ uint32_t uo_retrieve(int32_t dtype, const uint32_t* bonded, int32_t M) {
 }
 
 static int uo_finite(int32_t dtype, uint32_t bits) { return isfinite(uo_value(dtype, bits)); }
+/* Variants (Appendix C.2; DESIGN.md ledger L27).  AbsMinMax keeps the colliding
+ * weight of MAXIMUM |.| (cells start at +0, ties -> non-negative) and retrieves the bonded cell of
+ * MINIMUM |.| (ties -> non-negative).  CountMin cells hold the sum of their weights (2^-48 fixed
+ * point, as the aggregated gradient, L26, rounded to the weight dtype) and retrieve like AbsMinMax. */
+static uint32_t uo_update_absminmax(int32_t dtype, uint32_t cell, uint32_t x) {
+  double s = uo_value(dtype, cell), v = uo_value(dtype, x);
+  if (fabs(v) > fabs(s)) return x;
+  if (fabs(s) == fabs(v) && signbit(s) && !signbit(v)) return x;
+  return cell;
+}
+
+uint32_t uo_retrieve_v(int32_t variant, int32_t dtype, const uint32_t* bonded, int32_t M) {
+  uint32_t best = bonded[0];
+  int32_t i;
+  if (variant == UO_ABSMAXMIN) return uo_retrieve(dtype, bonded, M);
+  for (i = 1; i < M; i++) {
+    double b = uo_value(dtype, best), c = uo_value(dtype, bonded[i]);
+    if (fabs(c) < fabs(b) || (fabs(c) == fabs(b) && signbit(b) && !signbit(c))) best = bonded[i];
+  }
+  return best;
+}
+
+/* fp32 -> weight dtype bits (bf16: round to nearest even) */
+static uint32_t uo_from_float(int32_t dtype, float f) {
+  uint32_t b;
+  memcpy(&b, &f, 4);
+  return dtype == UO_BF16 ? (b + 0x7FFFu + ((b >> 16) & 1u)) >> 16 : b;
+}
+
+
 
 /* One compression unit ("S in AbsMaxMin is initialized as inf";
  * select Eq. 3, update Eq. 4).  Inserts the n (position, weight) pairs in the order
@@ -165,6 +200,38 @@ int32_t uo_sketch_unit(int32_t dtype, const uint32_t* w_bits, const uint32_t* po
       *cell = uo_update(dtype, *cell, w_bits[k]);
     }
   }
+  return UO_OK;
+}
+
+/* one unit under a variant (cells as in uo_sketch_unit) */
+int32_t uo_sketch_unit_v(int32_t variant, int32_t dtype, const uint32_t* w_bits, const uint32_t* pos, int64_t n,
+                         int32_t hash_kind, uint64_t seed, uint32_t layer, uint32_t t, int32_t M, uint32_t N,
+                         uint32_t* cells) {
+  int64_t k, c;
+  int32_t i;
+  int64_t* acc;
+  if (variant == UO_ABSMAXMIN) return uo_sketch_unit(dtype, w_bits, pos, n, hash_kind, seed, layer, t, M, N, cells);
+  if (M < 1 || N < 1) return UO_EINVAL;
+  for (k = 0; k < n; k++)
+    if (!uo_finite(dtype, w_bits[k])) return UO_ENONFINITE;
+  if (variant == UO_ABSMINMAX) {
+    for (c = 0; c < (int64_t)M * N; c++) cells[c] = 0u; /* +0 */
+    for (k = 0; k < n; k++)
+      for (i = 0; i < M; i++) {
+        uint32_t* cell = &cells[(int64_t)i * N + uo_hash_index(hash_kind, seed, layer, t, i, pos[k], N)];
+        *cell = uo_update_absminmax(dtype, *cell, w_bits[k]);
+      }
+    return UO_OK;
+  }
+  if (variant != UO_COUNTMIN) return UO_EINVAL;
+  acc = (int64_t*)calloc((size_t)M * N, sizeof(int64_t));
+  for (k = 0; k < n; k++) {
+    const int64_t q = llrint(uo_value(dtype, w_bits[k]) * 281474976710656.0); /* 2^48 */
+    for (i = 0; i < M; i++) acc[(int64_t)i * N + uo_hash_index(hash_kind, seed, layer, t, i, pos[k], N)] += q;
+  }
+  for (c = 0; c < (int64_t)M * N; c++)
+    cells[c] = uo_from_float(dtype, (float)((double)acc[c] * (1.0 / 281474976710656.0)));
+  free(acc);
   return UO_OK;
 }
 
@@ -592,7 +659,7 @@ static void uo_unit_span(int32_t gran, int32_t g, int64_t in, int64_t t, int64_t
 int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, int32_t layer,
                        int32_t gran, int32_t g, int64_t t_begin, int64_t t_end,
                        const int32_t* ncols, const int64_t* offsets, int32_t M, int32_t hash_kind,
-                       uint64_t seed, void* sketch) {
+                       uint64_t seed, void* sketch, int32_t variant) {
   int64_t t;
   for (t = t_begin; t < t_end; t++) {
     int64_t j0, j1, j, o, n, k = 0;
@@ -610,8 +677,8 @@ int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, in
         pos[k] = (uint32_t)((j - j0) * out + o);
         k++;
       }
-    st = uo_sketch_unit(dtype, wb, pos, n, hash_kind, seed, (uint32_t)layer, (uint32_t)t, M,
-                        (uint32_t)ncols[t], cells);
+    st = uo_sketch_unit_v(variant, dtype, wb, pos, n, hash_kind, seed, (uint32_t)layer, (uint32_t)t, M,
+                          (uint32_t)ncols[t], cells);
     if (st == UO_OK)
       for (c = 0; c < (int64_t)M * ncols[t]; c++) uo_store(dtype, sketch, offsets[t] + c, cells[c]);
     free(wb);
@@ -625,7 +692,7 @@ int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, in
 static uint32_t uo_weight_at(int32_t dtype, const void* sketch, int64_t out, int64_t in,
                              int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
                              const int64_t* offsets, int32_t M, int32_t hash_kind, uint64_t seed,
-                             int64_t o, int64_t j) {
+                             int64_t o, int64_t j, int32_t variant) {
   int64_t t = (gran == UO_GRAN_ROW) ? j / g : 0;
   int64_t j0 = (gran == UO_GRAN_ROW) ? t * g : 0;
   uint32_t p = (uint32_t)((j - j0) * out + o);
@@ -637,21 +704,21 @@ static uint32_t uo_weight_at(int32_t dtype, const void* sketch, int64_t out, int
     bonded[i] = uo_load(dtype, sketch,
                         offsets[t] + (int64_t)i * N +
                             uo_hash_index(hash_kind, seed, (uint32_t)layer, (uint32_t)t, i, p, N));
-  return uo_retrieve(dtype, bonded, M);
+  return uo_retrieve_v(variant, dtype, bonded, M);
 }
 
 /* W'[o, j] for o in [o_begin, o_end), all j; w_out is [(o_end-o_begin), in] raw bits. */
 int32_t uo_reconstruct_rows(int32_t dtype, const void* sketch, int64_t out, int64_t in,
                             int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
                             const int64_t* offsets, int32_t M, int32_t hash_kind, uint64_t seed,
-                            int64_t o_begin, int64_t o_end, void* w_out) {
+                            int64_t o_begin, int64_t o_end, void* w_out, int32_t variant) {
   int64_t o, j;
   if (o_begin < 0 || o_end > out || o_begin > o_end) return UO_ESHAPE;
   for (o = o_begin; o < o_end; o++)
     for (j = 0; j < in; j++)
       uo_store(dtype, w_out, (o - o_begin) * in + j,
                uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets, M, hash_kind,
-                            seed, o, j));
+                            seed, o, j, variant));
   return UO_OK;
 }
 
@@ -659,11 +726,11 @@ int32_t uo_reconstruct_rows(int32_t dtype, const void* sketch, int64_t out, int6
 int32_t uo_reconstruct_entries(int32_t dtype, const void* sketch, int64_t out, int64_t in,
                                int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
                                const int64_t* offsets, int32_t M, int32_t hash_kind, uint64_t seed,
-                               const int64_t* oj, int64_t n, uint32_t* out_bits) {
+                               const int64_t* oj, int64_t n, uint32_t* out_bits, int32_t variant) {
   int64_t k;
   for (k = 0; k < n; k++)
     out_bits[k] = uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets, M, hash_kind,
-                               seed, oj[2 * k], oj[2 * k + 1]);
+                               seed, oj[2 * k], oj[2 * k + 1], variant);
   return UO_OK;
 }
 
@@ -673,7 +740,7 @@ int32_t uo_reconstruct_entries(int32_t dtype, const void* sketch, int64_t out, i
 int32_t uo_linear_rows(int32_t dtype, const void* sketch, int64_t out, int64_t in, int32_t layer,
                        int32_t gran, int32_t g, const int32_t* ncols, const int64_t* offsets,
                        int32_t M, int32_t hash_kind, uint64_t seed, const double* x, int64_t T,
-                       int64_t o_begin, int64_t o_end, double* y) {
+                       int64_t o_begin, int64_t o_end, double* y, int32_t variant) {
   int64_t o, j, tok;
   double* wrow;
   if (o_begin < 0 || o_end > out || o_begin > o_end) return UO_ESHAPE;
@@ -681,7 +748,7 @@ int32_t uo_linear_rows(int32_t dtype, const void* sketch, int64_t out, int64_t i
   for (o = o_begin; o < o_end; o++) {
     for (j = 0; j < in; j++)
       wrow[j] = uo_value(dtype, uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets,
-                                             M, hash_kind, seed, o, j));
+                                             M, hash_kind, seed, o, j, variant));
     for (tok = 0; tok < T; tok++) {
       double s = 0.0;
       for (j = 0; j < in; j++) s += x[tok * in + j] * wrow[j];
@@ -722,6 +789,59 @@ int32_t uo_aggregate_grad(const double* grad, int64_t out, int64_t in, int32_t l
   }
   for (c = 0; c < n_cells; c++) cell_grad[c] = (float)((double)acc[c] * (1.0 / 281474976710656.0));
   free(acc);
+  return UO_OK;
+}
+
+/* Compression report (SPEC stats: "relative error per element = |w - w'| / |w| (w = 0 counted
+ * separately); sign error when sign(w') != sign(w) and both nonzero"; untouched = bit-exact
+ * preservation, Table 3 unoccupied states).  counts (int64[13]):
+ *   0 weights, 1 untouched (w' bits == w bits), 2 sign errors, 3 zero weights (w == 0),
+ *   4..10 relative-error histogram of the nonzero weights, r = fl32(fl32(|w - w'|) / |w|) in fp32
+ *   (DESIGN.md ledger L27): [r == 0], (0, 1e-3), [1e-3, 1e-2), [1e-2, 0.1), [0.1, 1), [1, 10),
+ *   [10, inf); 11 cells of the layer, 12 unoccupied cells (no weight maps to them).
+ * W, Wp: [out, in] raw bits of the weight dtype (Wp = the reconstruction). */
+int32_t uo_stats(int32_t dtype, const void* W, const void* Wp, int64_t out, int64_t in, int32_t layer,
+                 int32_t gran, int32_t g, int64_t n_units, const int32_t* ncols, const int64_t* offsets,
+                 int32_t M, int32_t hash_kind, uint64_t seed, int64_t* counts) {
+  static const float edges[5] = {1e-3f, 1e-2f, 1e-1f, 1.0f, 10.0f};
+  int64_t e, t, o, j, c;
+  const int64_t n_cells = offsets[n_units] - offsets[0];
+  int32_t* occ = (int32_t*)calloc((size_t)(n_cells > 0 ? n_cells : 1), sizeof(int32_t));
+  for (c = 0; c < 13; c++) counts[c] = 0;
+  for (e = 0; e < out * in; e++) {
+    const uint32_t wb = uo_load_bits(dtype, W, e), pb = uo_load_bits(dtype, Wp, e);
+    const float w = (float)uo_value(dtype, wb), wp = (float)uo_value(dtype, pb);
+    counts[0]++;
+    if (wb == pb) counts[1]++;
+    if (w != 0.0f && wp != 0.0f && (signbit(w) != signbit(wp))) counts[2]++;
+    if (w == 0.0f) {
+      counts[3]++;
+    } else {
+      const float d = fabsf(w - wp);
+      const float r = d / fabsf(w);
+      int b = 0;
+      if (r > 0.0f) {
+        b = 1;
+        while (b <= 5 && r >= edges[b - 1]) b++;
+      }
+      counts[4 + b]++;
+    }
+  }
+  for (t = 0; t < n_units; t++) {
+    int64_t j0, j1;
+    uo_unit_span(gran, g, in, t, &j0, &j1);
+    for (o = 0; o < out; o++)
+      for (j = j0; j < j1; j++) {
+        const uint32_t p = (uint32_t)((j - j0) * out + o);
+        int32_t i;
+        for (i = 0; i < M; i++)
+          occ[offsets[t] - offsets[0] + (int64_t)i * ncols[t] +
+              uo_hash_index(hash_kind, seed, (uint32_t)layer, (uint32_t)t, i, p, (uint32_t)ncols[t])]++;
+      }
+  }
+  counts[11] = n_cells;
+  for (c = 0; c < n_cells; c++) counts[12] += occ[c] == 0;
+  free(occ);
   return UO_OK;
 }
 
