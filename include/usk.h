@@ -65,6 +65,12 @@ typedef enum { USK_GRAN_ROW = 0, USK_GRAN_LAYER = 1 } usk_granularity;
  * tests only). */
 typedef enum { USK_HASH_X = 0, USK_HASH_IDENTITY = 1 } usk_hash;
 
+/* Sketch variant (Appendix C.2): USK_ABSMAXMIN = the paper's sketch (keep the
+ * min |.|, retrieve the max |.|); USK_ABSMINMAX = the order of min and max swapped (cells start at
+ * +0); USK_COUNTMIN = cells hold the sum of their weights (2^-48 fixed point, ledger L26/L27),
+ * retrieve the min |.|.  Ties prefer the non-negative value in every variant. */
+typedef enum { USK_ABSMAXMIN = 0, USK_ABSMINMAX = 1, USK_COUNTMIN = 2 } usk_variant;
+
 /* One linear layer, PyTorch layout: weight is row-major [out_features, in_features]. */
 typedef struct {
   int64_t out_features;
@@ -88,6 +94,8 @@ typedef struct {
                             state_bits bits, one fp32 absmax scale per group_size cells of a layer,
                             round half away from zero; DESIGN.md ledger L25 */
   int32_t group_size;    /* cells per scale group (power of two >= 32; 0 = 128); quantised plans only */
+  int32_t variant;       /* usk_variant: the sketch (Appendix C.2; L27).
+                            The comparison variants run on the generic kernels, raw states only. */
 } usk_params;
 
 typedef struct usk_plan usk_plan;
@@ -223,6 +231,20 @@ USK_API size_t usk_aggregate_grad_workspace_bytes(const usk_plan* plan, int32_t 
 USK_API usk_status usk_aggregate_grad(const usk_plan* plan, int32_t layer, const void* grad, int32_t grad_dtype,
                                       float* cell_grad, void* workspace, size_t workspace_bytes,
                                       usk_stream stream);
+
+/* Compression report of one layer (SPEC stats; untouched weights PAPER.md:616-619; Table 3
+ * unoccupied states), computed on the device from the original weights and the sketch:
+ *   counts (device int64[USK_STATS_N]) receives, for the layer's weights w and reconstructions w':
+ *   [0] weights, [1] untouched (w' bits == w bits), [2] sign errors (both nonzero, signs differ),
+ *   [3] zero weights, [4..10] histogram of r = fl32(fl32(|w - w'|) / |w|) over nonzero w:
+ *   r == 0, (0, 1e-3), [1e-3, 1e-2), [1e-2, 0.1), [0.1, 1), [1, 10), [10, inf);
+ *   [11] cells of the layer, [12] unoccupied cells (no weight of the layer maps to them).
+ *   W: device [out, in] of the plan dtype; workspace: device, >= usk_stats_workspace_bytes,
+ *   zero-filled before first use, left zero-filled.  Integer counts: deterministic. */
+#define USK_STATS_N 13
+USK_API size_t usk_stats_workspace_bytes(const usk_plan* plan, int32_t layer);
+USK_API usk_status usk_stats(const usk_plan* plan, const void* sketch, int32_t layer, const void* W, int64_t* counts,
+                             void* workspace, size_t workspace_bytes, usk_stream stream);
 
 /* Synchronises `stream`, returns and clears the plan's sticky device error (USK_ENONFINITE),
  * or USK_ECUDA on a CUDA error, else USK_OK. */

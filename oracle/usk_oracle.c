@@ -813,7 +813,7 @@ int32_t uo_stats(int32_t dtype, const void* W, const void* Wp, int64_t out, int6
     const float w = (float)uo_value(dtype, wb), wp = (float)uo_value(dtype, pb);
     counts[0]++;
     if (wb == pb) counts[1]++;
-    if (w != 0.0f && wp != 0.0f && (signbit(w) != signbit(wp))) counts[2]++;
+    if (w != 0.0f && wp != 0.0f && (signbit(w) != 0) != (signbit(wp) != 0)) counts[2]++;
     if (w == 0.0f) {
       counts[3]++;
     } else {

@@ -90,6 +90,8 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   if (P.n_classes < 0 || P.n_classes > 64) return fail(USK_EINVAL, "n_classes must be in [0, 64]");
   if (P.state_bits != 0 && P.state_bits != 4 && P.state_bits != 8) return fail(USK_EINVAL, "state_bits must be 0, 4 or 8");
   const int32_t qG = P.group_size ? P.group_size : 128;
+  if (P.variant < USK_ABSMAXMIN || P.variant > USK_COUNTMIN) return fail(USK_EINVAL, "variant");
+  if (P.variant != USK_ABSMAXMIN && P.state_bits) return fail(USK_EUNSUPPORTED, "variants use raw states");
   if (P.state_bits && (qG < 32 || (qG & (qG - 1)) != 0))
     return fail(USK_EINVAL, "group_size must be a power of two >= 32");
   const int g = P.granularity == USK_GRAN_ROW ? P.dims_per_unit : 1;
@@ -111,6 +113,7 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   pl->C = P.n_classes > 0 ? P.n_classes : (saliency ? 4 : 1);
   pl->min_cols = P.min_cols;
   pl->hash = P.hash;
+  pl->variant = P.variant;
   pl->dtype = P.dtype;
   pl->bpw = P.bpw;
   pl->seed = P.seed;

@@ -348,12 +348,94 @@ __global__ void k_quantize(const void* raw, int64_t g0, int64_t g1, int G, uint8
   }
 }
 
+// ---------------------------------------------------------------- comparison variants
+// (Appendix C.2; DESIGN.md ledger L27).  AbsMinMax keeps the max |.| per cell:
+// keys rho = kappa ^ 1 = (mag << 1) | (1 - sign) (max rho = max |.|, ties -> non-negative), cells
+// start at rho(+0) = 1.  bf16 cells hold the 16-bit rho16 = rotl16(bits, 1) ^ 1 (in-word CAS max).
+__device__ __forceinline__ void cas_max16(uint16_t* cell, uint32_t key16) {
+  uint32_t* word = reinterpret_cast<uint32_t*>(reinterpret_cast<uintptr_t>(cell) & ~uintptr_t(3));
+  const int sh = (reinterpret_cast<uintptr_t>(cell) & 2) ? 16 : 0;
+  uint32_t old = *reinterpret_cast<volatile uint32_t*>(word);
+  for (;;) {
+    const uint32_t cur = (old >> sh) & 0xFFFFu;
+    if (key16 <= cur) return;
+    const uint32_t nw = (old & ~(0xFFFFu << sh)) | (key16 << sh);
+    const uint32_t prev = atomicCAS(word, old, nw);
+    if (prev == old) return;
+    old = prev;
+  }
+}
+
+template <int ES>
+__global__ void k_amx_init(void* sketch, int64_t c0, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (ES == 2) reinterpret_cast<uint16_t*>(sketch)[c0 + i] = 1;  // rho16(+0)
+  else reinterpret_cast<uint32_t*>(sketch)[c0 + i] = 1u;         // rho(+0)
+}
+
+template <int ES, int HASH>
+__global__ void k_amx_scatter(GenLayer G, const void* W, int32_t layer_M, HashConsts hc, const int32_t* ncols,
+                              const int64_t* offsets, const uint32_t* ukeys, void* sketch, int* err) {
+  const int64_t n = G.out * G.in;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = e / G.in, j = e - o * G.in;
+    int64_t t, p;
+    if (G.gran == USK_GRAN_ROW) { t = j / G.g; p = (j - t * G.g) * G.out + o; }
+    else { t = 0; p = j * G.out + o; }
+    const int64_t u = G.unit_base + t;
+    const uint32_t N = (uint32_t)ncols[u];
+    const int64_t off = offsets[u];
+    const uint32_t bhi = (ES == 2) ? ((uint32_t)reinterpret_cast<const uint16_t*>(W)[e] << 16)
+                                   : reinterpret_cast<const uint32_t*>(W)[e];
+    const uint32_t kap = rotl1(bhi);
+    if (kap >= 0xFF000000u) atomicOr(err, 1);
+    const uint32_t rho = kap ^ 1u;
+    const uint32_t h = fmix32((uint32_t)p ^ hc.rho) ^ ukeys[u];
+    for (int i = 0; i < layer_M; ++i) {
+      const uint32_t idx = (HASH == USK_HASH_X) ? __umulhi(h * hc.a[i], N) : (uint32_t)(p % N);
+      const int64_t c = off + (int64_t)i * N + idx;
+      if (ES == 2) {
+        cas_max16(reinterpret_cast<uint16_t*>(sketch) + c, (rho >> 16) | (rho & 1u));
+      } else {
+        uint32_t* cell = reinterpret_cast<uint32_t*>(sketch) + c;
+        if (rho > *reinterpret_cast<volatile uint32_t*>(cell)) atomicMax(cell, rho);
+      }
+    }
+  }
+}
+
+template <int ES>
+__global__ void k_amx_final(void* sketch, int64_t c0, int64_t n) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  if (ES == 2) {
+    uint16_t* c = reinterpret_cast<uint16_t*>(sketch) + c0 + i;
+    const uint32_t k = *c ^ 1u;  // kappa16 = (mag << 1) | sign
+    *c = (uint16_t)((k >> 1) | ((k & 1u) << 15));
+  } else {
+    uint32_t* c = reinterpret_cast<uint32_t*>(sketch) + c0 + i;
+    *c = rotr1(*c ^ 1u);
+  }
+}
+
+// CountMin cells: fl32(fl64(S) * 2^-48) of the fixed-point sums, in the weight dtype (bf16: RNE)
+template <int ES>
+__global__ void k_cm_final(const unsigned long long* acc, int64_t n, void* sketch, int64_t c0) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float v = __double2float_rn(__ll2double_rn((long long)acc[i]) * (1.0 / 281474976710656.0));
+  const uint32_t b = __float_as_uint(v);
+  if (ES == 2) reinterpret_cast<uint16_t*>(sketch)[c0 + i] = (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+  else reinterpret_cast<uint32_t*>(sketch)[c0 + i] = b;
+}
+
 // ---------------------------------------------------------------- host side
 int fast_upl(const usk_plan* pl, int32_t l) {
   // units per lane for the fast kernels, 0 = not eligible: the largest UPL whose key array and
   // stage ring fit one CTA (one CTA per SM is enough: 17 warps, bulk-copy ring in flight)
   const LayerGeom& L = pl->layers[l];
-  if (pl->gran != USK_GRAN_ROW || pl->g != 1) return 0;
+  if (pl->gran != USK_GRAN_ROW || pl->g != 1 || pl->variant != USK_ABSMAXMIN) return 0;
   const int es = pl->cell_bytes();
   if ((L.in * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
@@ -435,6 +517,38 @@ usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* 
   const LayerGeom& L = pl->layers[l];
   GenLayer G{L.out, L.in, L.unit_begin, L.cell_begin, L.n_cells, pl->gran, pl->g};
   const int T = 256;
+  const unsigned cb = (unsigned)((std::max<int64_t>(L.n_cells, 1) + T - 1) / T);
+  if (pl->variant == USK_COUNTMIN) {
+    unsigned long long* acc = nullptr;
+    USK_CUDA(cudaMallocAsync(&acc, (size_t)std::max<int64_t>(L.n_cells, 1) * 8, st));
+    USK_CUDA(cudaMemsetAsync(acc, 0, (size_t)std::max<int64_t>(L.n_cells, 1) * 8, st));
+    usk_status s = launch_fixed_accumulate(pl, l, W, pl->dtype, acc, pl->d_err, st);
+    if (s == USK_OK && L.n_cells > 0) {
+      k_cm_final<ES><<<cb, T, 0, st>>>(acc, L.n_cells, sketch, L.cell_begin);
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) s = cuda_fail(e, "k_cm_final");
+      else count_launch();
+    }
+    cudaError_t e = cudaFreeAsync(acc, st);
+    if (s == USK_OK && e != cudaSuccess) s = cuda_fail(e, "cudaFreeAsync");
+    return s;
+  }
+  if (pl->variant == USK_ABSMINMAX) {
+    k_amx_init<ES><<<cb, T, 0, st>>>(sketch, L.cell_begin, L.n_cells);
+    USK_LAUNCHED("k_amx_init");
+    const int64_t n = L.out * L.in;
+    const unsigned blocks = (unsigned)std::min<int64_t>((n + T - 1) / T, 148 * 16);
+    if (pl->hash == USK_HASH_X)
+      k_amx_scatter<ES, USK_HASH_X><<<blocks, T, 0, st>>>(G, W, pl->M, pl->hc, pl->d_ncols, pl->d_offsets, pl->d_keys,
+                                                          sketch, pl->d_err);
+    else
+      k_amx_scatter<ES, USK_HASH_IDENTITY><<<blocks, T, 0, st>>>(G, W, pl->M, pl->hc, pl->d_ncols, pl->d_offsets,
+                                                                 pl->d_keys, sketch, pl->d_err);
+    USK_LAUNCHED("k_amx_scatter");
+    k_amx_final<ES><<<cb, T, 0, st>>>(sketch, L.cell_begin, L.n_cells);
+    USK_LAUNCHED("k_amx_final");
+    return USK_OK;
+  }
   k_gen_init<ES><<<(unsigned)((L.n_cells + T - 1) / T), T, 0, st>>>(sketch, L.cell_begin, L.n_cells);
   USK_LAUNCHED("k_gen_init");
   const int64_t n = L.out * L.in;

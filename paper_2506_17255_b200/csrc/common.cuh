@@ -106,6 +106,7 @@ struct usk_plan {
   int device = 0;
   // stacked state quantisation (L25): q = 0 (raw states) or 4 / 8 bits
   int32_t q = 0, G = 128;
+  int32_t variant = 0;        // usk_variant (comparison variants: generic kernels only)
   int64_t n_groups = 0;       // total_cells / G (quantised)
   int64_t scales_off = 0;     // byte offset of the fp32 group scales in the sketch (quantised)
   int cell_bytes() const { return dtype == USK_BF16 ? 2 : 4; }  // raw state bytes
@@ -132,5 +133,7 @@ usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dty
 usk_status launch_importance(const void* A, int32_t a_dtype, int64_t N, int64_t d, float* I,
                              cudaStream_t st);
 usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStream_t st);
+usk_status launch_fixed_accumulate(const usk_plan* pl, int32_t l, const void* vals, int32_t dtype,
+                                   unsigned long long* acc, int* err, cudaStream_t st);
 bool layer_fast_ok(const usk_plan* pl, int32_t layer);
 }  // namespace usk

@@ -22,6 +22,7 @@ struct AggArgs {
   const uint32_t* ukeys;
   HashConsts hc;
   unsigned long long* acc;
+  int* err;  // non-NULL: flag non-finite values (CountMin build)
 };
 
 __global__ void k_aggregate(AggArgs A) {
@@ -36,6 +37,7 @@ __global__ void k_aggregate(AggArgs A) {
     const int64_t base = A.offsets[u] - A.cell_begin;
     const float gv = A.bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.grad)[e] << 16)
                             : reinterpret_cast<const float*>(A.grad)[e];
+    if (A.err && !isfinite(gv)) atomicOr(A.err, 1);
     const long long q = __double2ll_rn((double)gv * kFix);
     if (q == 0) continue;
     const uint32_t h = fmix32((uint32_t)p ^ A.hc.rho) ^ A.ukeys[u];
@@ -59,14 +61,27 @@ size_t aggregate_workspace_bytes(const usk_plan* pl, int32_t l) {
   return (size_t)std::max<int64_t>(pl->layers[l].n_cells, 1) * 8;
 }
 
-usk_status launch_aggregate(const usk_plan* pl, int32_t l, const void* grad, int32_t grad_dtype, float* cell_grad,
-                            void* ws, cudaStream_t st) {
+// acc[c - cell_begin] += 2^-48 fixed point of vals (o, j) for every sketch row's cell of layer l
+usk_status launch_fixed_accumulate(const usk_plan* pl, int32_t l, const void* vals, int32_t dtype,
+                                   unsigned long long* acc, int* err, cudaStream_t st) {
   const LayerGeom& L = pl->layers[l];
-  AggArgs A{grad, grad_dtype == USK_BF16, L.out, L.in, L.unit_begin, L.cell_begin, pl->M, pl->gran, pl->g,
-            pl->hash, pl->d_ncols, pl->d_offsets, pl->d_keys, pl->hc, reinterpret_cast<unsigned long long*>(ws)};
+  AggArgs A{vals, dtype == USK_BF16, L.out, L.in, L.unit_begin, L.cell_begin, pl->M, pl->gran, pl->g,
+            pl->hash, pl->d_ncols, pl->d_offsets, pl->d_keys, pl->hc, acc, err};
   const int64_t n = L.out * L.in;
   k_aggregate<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, st>>>(A);
   USK_LAUNCHED("k_aggregate");
+  return USK_OK;
+}
+
+usk_status launch_aggregate(const usk_plan* pl, int32_t l, const void* grad, int32_t grad_dtype, float* cell_grad,
+                            void* ws, cudaStream_t st) {
+  const LayerGeom& L = pl->layers[l];
+  usk_status s = launch_fixed_accumulate(pl, l, grad, grad_dtype, reinterpret_cast<unsigned long long*>(ws), nullptr,
+                                         st);
+  if (s != USK_OK) return s;
+  struct {
+    unsigned long long* acc;
+  } A{reinterpret_cast<unsigned long long*>(ws)};
   if (L.n_cells > 0) {
     k_agg_finish<<<(unsigned)((L.n_cells + 255) / 256), 256, 0, st>>>(A.acc, L.n_cells, cell_grad);
     USK_LAUNCHED("k_agg_finish");

@@ -551,6 +551,7 @@ struct GenQ {
   int32_t M, gran, g, hash, es;
   int32_t q, g_shift;     // quantised plans (L25)
   const float* scales;
+  int32_t variant;        // usk_variant (L27)
 };
 
 // cell value as fp32 bits (raw bf16: bits << 16; quantised: fl32(code * scale))
@@ -577,6 +578,15 @@ __device__ __forceinline__ uint32_t gen_weight_bits_hi(const GenQ& Q, int64_t o,
   const uint32_t N = (uint32_t)Q.ncols[u];
   const int64_t off = Q.offsets[u];
   const uint32_t h = fmix32((uint32_t)p ^ Q.hc.rho) ^ Q.ukeys[u];
+  if (Q.variant != USK_ABSMAXMIN) {
+    // AbsMinMax / CountMin: the bonded cell of MINIMUM |.|, ties -> non-negative = min kappa
+    uint32_t best = 0xFFFFFFFFu;
+    for (int i = 0; i < Q.M; ++i) {
+      const uint32_t idx = Q.hash == USK_HASH_X ? __umulhi(h * Q.hc.a[i], N) : (uint32_t)(p % N);
+      best = min(best, rotl1(gen_cell_bits(Q, off + (int64_t)i * N + idx)));
+    }
+    return rotr1(best);
+  }
   uint32_t best = 0;
   for (int i = 0; i < Q.M; ++i) {
     const uint32_t idx = Q.hash == USK_HASH_X ? __umulhi(h * Q.hc.a[i], N) : (uint32_t)(p % N);
@@ -620,6 +630,69 @@ __global__ void k_gemv_gen(GenQ Q, int64_t o0, int64_t o1, const void* x, int32_
   }
 }
 
+// ------------------------------------------------------------------ K7: compression report
+// (SPEC stats; DESIGN.md ledger L27).  Integer counts with integer atomics: deterministic.
+__global__ void k_stats_weights(GenQ Q, const void* W, unsigned long long* counts, int32_t* occ) {
+  __shared__ unsigned int sc[11];
+  if (threadIdx.x < 11) sc[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t n = Q.out * Q.in;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t o = e / Q.in, j = e - o * Q.in;
+    uint32_t pb = gen_weight_bits_hi(Q, o, j);  // w' (fp32 bits; bf16 in the high half)
+    if (Q.es == 2 && Q.q) pb = pb + 0x7FFFu + ((pb >> 16) & 1u);
+    uint32_t wb;
+    if (Q.es == 2) {
+      wb = (uint32_t)reinterpret_cast<const uint16_t*>(W)[e] << 16;
+      pb &= 0xFFFF0000u;
+    } else {
+      wb = reinterpret_cast<const uint32_t*>(W)[e];
+    }
+    const float w = __uint_as_float(wb), wp = __uint_as_float(pb);
+    atomicAdd(&sc[0], 1u);
+    if (wb == pb) atomicAdd(&sc[1], 1u);
+    if (w != 0.f && wp != 0.f && ((wb ^ pb) & 0x80000000u)) atomicAdd(&sc[2], 1u);
+    if (w == 0.f) {
+      atomicAdd(&sc[3], 1u);
+    } else {
+      const float r = __fdiv_rn(fabsf(__fsub_rn(w, wp)), fabsf(w));
+      int b = 0;
+      if (r > 0.f) b = r < 1e-3f ? 1 : r < 1e-2f ? 2 : r < 1e-1f ? 3 : r < 1.f ? 4 : r < 10.f ? 5 : 6;
+      atomicAdd(&sc[4 + b], 1u);
+    }
+    // occupancy: one count per sketch row
+    int64_t t, p;
+    if (Q.gran == USK_GRAN_ROW) { t = j / Q.g; p = (j - t * Q.g) * Q.out + o; }
+    else { t = 0; p = j * Q.out + o; }
+    const int64_t u = Q.unit_base + t;
+    const uint32_t N = (uint32_t)Q.ncols[u];
+    const uint32_t h = fmix32((uint32_t)p ^ Q.hc.rho) ^ Q.ukeys[u];
+    const int64_t base = Q.offsets[u] - Q.offsets[Q.unit_base];
+    for (int i = 0; i < Q.M; ++i) {
+      const uint32_t idx = Q.hash == USK_HASH_X ? __umulhi(h * Q.hc.a[i], N) : (uint32_t)(p % N);
+      atomicAdd(&occ[base + (int64_t)i * N + idx], 1);
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 11 && sc[threadIdx.x]) atomicAdd(&counts[threadIdx.x], (unsigned long long)sc[threadIdx.x]);
+}
+
+__global__ void k_stats_cells(int32_t* occ, int64_t n, unsigned long long* counts) {
+  __shared__ unsigned int z;
+  if (threadIdx.x == 0) z = 0;
+  __syncthreads();
+  const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (c < n) {
+    if (occ[c] == 0) atomicAdd(&z, 1u);
+    occ[c] = 0;  // leave the workspace zeroed
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (z) atomicAdd(&counts[12], (unsigned long long)z);
+    if (blockIdx.x == 0) atomicAdd(&counts[11], (unsigned long long)n);
+  }
+}
+
 // ------------------------------------------------------------------ K6: importance (Eq. 7)
 __global__ void k_importance(const void* A, int32_t bf16, int64_t N, int64_t d, float* I) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -634,7 +707,9 @@ __global__ void k_importance(const void* A, int32_t bf16, int64_t N, int64_t d, 
 }
 
 // ------------------------------------------------------------------ host side
-bool fast_eligible(const usk_plan* pl) { return pl->gran == USK_GRAN_ROW && pl->g == 1; }
+bool fast_eligible(const usk_plan* pl) {
+  return pl->gran == USK_GRAN_ROW && pl->g == 1 && pl->variant == USK_ABSMAXMIN;
+}
 
 constexpr size_t kSmemMax = 220 * 1024;
 
@@ -948,6 +1023,7 @@ GenQ make_genq(const usk_plan* pl, int32_t l, const void* sketch) {
   Q.q = pl->q;
   Q.g_shift = ilog2(pl->G);
   Q.scales = pl->q ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(sketch) + pl->scales_off) : nullptr;
+  Q.variant = pl->variant;
   return Q;
 }
 
@@ -1058,6 +1134,26 @@ usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l,
   return USK_OK;
 }
 
+size_t stats_workspace_bytes(const usk_plan* pl, int32_t l) {
+  return (size_t)std::max<int64_t>(pl->layers[l].n_cells, 1) * 4;
+}
+
+usk_status launch_stats(const usk_plan* pl, const void* sketch, int32_t l, const void* W, int64_t* counts, void* ws,
+                        cudaStream_t st) {
+  const LayerGeom& L = pl->layers[l];
+  GenQ Q = make_genq(pl, l, sketch);
+  unsigned long long* c = reinterpret_cast<unsigned long long*>(counts);
+  USK_CUDA(cudaMemsetAsync(counts, 0, sizeof(int64_t) * USK_STATS_N, st));
+  const int64_t n = L.out * L.in;
+  k_stats_weights<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(Q, W, c,
+                                                                                           reinterpret_cast<int32_t*>(ws));
+  USK_LAUNCHED("k_stats_weights");
+  k_stats_cells<<<(unsigned)((std::max<int64_t>(L.n_cells, 1) + 255) / 256), 256, 0, st>>>(
+      reinterpret_cast<int32_t*>(ws), L.n_cells, c);
+  USK_LAUNCHED("k_stats_cells");
+  return USK_OK;
+}
+
 usk_status launch_importance(const void* A, int32_t a_dtype, int64_t N, int64_t d, float* I, cudaStream_t st) {
   k_importance<<<(unsigned)((d + 255) / 256), 256, 0, st>>>(A, a_dtype == USK_BF16, N, d, I);
   USK_LAUNCHED("k_importance");
@@ -1067,6 +1163,19 @@ usk_status launch_importance(const void* A, int32_t a_dtype, int64_t N, int64_t 
 }  // namespace usk
 
 extern "C" {
+
+size_t usk_stats_workspace_bytes(const usk_plan* pl, int32_t layer) {
+  if (!pl || layer < 0 || layer >= pl->n_layers) return 0;
+  return usk::stats_workspace_bytes(pl, layer);
+}
+
+usk_status usk_stats(const usk_plan* pl, const void* sketch, int32_t layer, const void* W, int64_t* counts,
+                     void* workspace, size_t workspace_bytes, usk_stream stream) {
+  if (!pl || !sketch || !W || !counts || !workspace) return usk::fail(USK_EINVAL, "usk_stats: null pointer");
+  if (layer < 0 || layer >= pl->n_layers) return usk::fail(USK_ESHAPE, "usk_stats: layer out of range");
+  if (workspace_bytes < usk::stats_workspace_bytes(pl, layer)) return usk::fail(USK_ESHAPE, "usk_stats: workspace");
+  return usk::launch_stats(pl, sketch, layer, W, counts, workspace, (cudaStream_t)stream);
+}
 
 int32_t usk_trace_read(uint64_t* stamps, int64_t cap_stamps, int32_t* grids, int32_t cap_launches) {
   usk::Trace& T = usk::trace();

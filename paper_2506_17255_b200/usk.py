@@ -18,6 +18,9 @@ OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE, ECUDA, EUNSUPPORTED = range(7)
 F32, BF16 = 0, 1
 GRAN = {"row": 0, "layer": 1}
 HASH = {"x": 0, "identity": 1}
+VARIANT = {"absmaxmin": 0, "absminmax": 1, "countmin": 2}
+STATS_KEYS = ("weights", "untouched", "sign_errors", "zero_weights", "rel_exact", "rel_lt_1e-3", "rel_1e-3",
+              "rel_1e-2", "rel_1e-1", "rel_1", "rel_ge_10", "cells", "unoccupied")
 DTYPE = {"f32": F32, "fp32": F32, "float32": F32, "bf16": BF16, "bfloat16": BF16}
 
 
@@ -39,7 +42,7 @@ class _Params(ct.Structure):
     _fields_ = [("bpw", ct.c_double), ("rows", ct.c_int32), ("granularity", ct.c_int32),
                 ("dims_per_unit", ct.c_int32), ("n_classes", ct.c_int32), ("min_cols", ct.c_int32),
                 ("hash", ct.c_int32), ("dtype", ct.c_int32), ("seed", ct.c_uint64), ("state_bits", ct.c_int32),
-                ("group_size", ct.c_int32)]
+                ("group_size", ct.c_int32), ("variant", ct.c_int32)]
 
 
 class _PlanInfo(ct.Structure):
@@ -81,6 +84,8 @@ def _load():
         "usk_last_error": (ct.c_char_p, []),
         "usk_launch_count": (i64, [i32]),
         "usk_aggregate_grad_workspace_bytes": (ct.c_size_t, [p, i32]),
+        "usk_stats_workspace_bytes": (ct.c_size_t, [p, i32]),
+        "usk_stats": (i32, [p, p, i32, p, p, p, ct.c_size_t, p]),
         "usk_aggregate_grad": (i32, [p, i32, p, i32, p, p, ct.c_size_t, p]),
         "usk_trace_read": (i32, [p, i64, p, i32]),
         "usk_trace_reset": (None, []),
@@ -180,13 +185,14 @@ class Plan:
 
 def plan_allocation(shapes, *, bpw: float, rows: int = 3, granularity: str = "row", dims_per_unit: int = 1,
                     n_classes: int = 0, min_cols: int = 1, hash: str = "x", dtype: str = "bf16", seed: int = 0,
-                    saliency=None, state_bits: int = 0, group_size: int = 0, stream=None) -> Plan:
+                    saliency=None, state_bits: int = 0, group_size: int = 0, variant: str = "absmaxmin",
+                    stream=None) -> Plan:
     """usk_plan_allocation. saliency: None or list of (None | float32 CUDA tensor [in_features]).
     state_bits 4 / 8: stacked state quantisation with group_size cells per scale (0 = 128)."""
     n = len(shapes)
     arr = (_Shape * n)(*[_Shape(int(o), int(i)) for (o, i) in shapes])
     prm = _Params(float(bpw), rows, GRAN[granularity], dims_per_unit, n_classes, min_cols, HASH[hash],
-                  DTYPE[dtype], seed & (2**64 - 1), state_bits, group_size)
+                  DTYPE[dtype], seed & (2**64 - 1), state_bits, group_size, VARIANT[variant])
     sal = ct.c_void_p(0)
     keep = None
     if saliency is not None:
@@ -272,6 +278,15 @@ def aggregate_grad(plan: Plan, layer: int, grad, cell_grad, workspace=None, stre
     _check(lib.usk_aggregate_grad(plan.handle, layer, _ptr(grad), _dtype_code(grad), _ptr(cell_grad), _ptr(workspace),
                                   workspace.numel(), _stream(stream)))
     return cell_grad
+
+
+def stats(plan: Plan, sketch, layer: int, W, stream=None) -> dict:
+    """usk_stats: the compression report of `layer` (counts keyed by STATS_KEYS)."""
+    import torch
+    counts = torch.zeros(13, dtype=torch.int64, device=W.device)
+    ws = torch.zeros(int(lib.usk_stats_workspace_bytes(plan.handle, layer)), dtype=torch.uint8, device=W.device)
+    _check(lib.usk_stats(plan.handle, _ptr(sketch), layer, _ptr(W), _ptr(counts), _ptr(ws), ws.numel(), _stream(stream)))
+    return dict(zip(STATS_KEYS, counts.cpu().tolist()))
 
 
 def check(plan: Plan, stream=None):
