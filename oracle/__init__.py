@@ -71,7 +71,9 @@ def lib():
         L.uo_allocate.restype = i32
         L.uo_allocate.argtypes = [i64, p, p, i64, i32, i32, i32, p, p]
         L.uo_plan.restype = i32
-        L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, i32, i32, p, p, p, p, p]
+        L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, i32, i32, p, p, p, p, p, p]
+        L.uo_layer_cells.restype = i32
+        L.uo_layer_cells.argtypes = [i32, p, p, p, i32, i32, i64, p]
         L.uo_quantize.restype = i32
         L.uo_quantize.argtypes = [i32, p, i64, i32, i32, p, p]
         L.uo_dequantize.restype = i32
@@ -235,7 +237,7 @@ class Plan:
 
 
 def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None, min_cols=1,
-         hash_kind=HASH_X, seed=0, state_bits=0, group=128, variant=ABSMAXMIN) -> Plan:
+         hash_kind=HASH_X, seed=0, state_bits=0, group=128, variant=ABSMAXMIN, layer_importance=None) -> Plan:
     L = len(shapes)
     outf = np.array([s[0] for s in shapes], dtype=np.int64)
     inf = np.array([s[1] for s in shapes], dtype=np.int64)
@@ -252,13 +254,25 @@ def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None
     ncols = np.zeros(max(U, 1), dtype=np.int32)
     offsets = np.zeros(max(U, 1) + 1, dtype=np.int64)
     acct = np.zeros(4 * L, dtype=np.int64)
+    limp = None if layer_importance is None else np.ascontiguousarray(layer_importance, dtype=np.float64)
     st = lib().uo_plan(L, _ptr(outf), _ptr(inf), dtype,
                        ct.cast(sal_ptrs, ct.c_void_p) if sal_ptrs is not None else None,
-                       float(bpw), M, gran, g, C, min_cols, state_bits, group, _ptr(unit_base), _ptr(cls),
+                       float(bpw), M, gran, g, C, min_cols, state_bits, group,
+                       None if limp is None else _ptr(limp), _ptr(unit_base), _ptr(cls),
                        _ptr(ncols), _ptr(offsets), _ptr(acct))
     _check(st, "plan")
     return Plan(list(map(tuple, zip(outf.tolist(), inf.tolist()))), dtype, M, gran, g, C, min_cols, hash_kind,
                 seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4), state_bits, group, variant)
+
+
+def layer_cells(importance, numel, units, M, min_cols, T) -> np.ndarray:
+    """First level of the two-level allocation (ledger L28): cells per layer."""
+    imp = np.ascontiguousarray(importance, dtype=np.float64)
+    n = np.ascontiguousarray(numel, dtype=np.int64)
+    u = np.ascontiguousarray(units, dtype=np.int64)
+    out = np.zeros(len(imp), dtype=np.int64)
+    _check(lib().uo_layer_cells(len(imp), _ptr(imp), _ptr(n), _ptr(u), M, min_cols, T, _ptr(out)), "layer_cells")
+    return out
 
 
 def _np_dtype(dtype):

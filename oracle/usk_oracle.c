@@ -440,13 +440,77 @@ static int32_t uo_ceil_log2(int32_t C) {
  * T = (floor(budget / (q*G + 32)) - n_layers) * G (one partial group per layer). */
 static int64_t uo_align_up(int64_t x, int64_t a) { return ((x + a - 1) / a) * a; }
 
+/* Two-level (layer x row) allocation ("Front-end layers are more
+ * important ... the degradation extent can serve as an important metric"; DESIGN.md ledger L28):
+ * the model's cells T are shared among layers in proportion to q_l * numel_l, q_l the layer
+ * importance in 2^24 fixed point (as L8), each layer floored at U_l * M * min_cols cells
+ * (water-filled), the leftover cells by largest remainder (frac desc, l asc).  Exact integer
+ * arithmetic (u128); T_l out. */
+int32_t uo_layer_cells(int32_t L, const double* imp, const int64_t* numel, const int64_t* Ul, int32_t M,
+                       int32_t min_cols, int64_t T, int64_t* T_l) {
+  int32_t l;
+  double smax = 0.0;
+  uo_u128 w[256], num[256], den[256];
+  int active[256];
+  int64_t floor_sum = 0, left;
+  uo_rem_item rem[256];
+  int32_t n_rem = 0, k;
+  if (L < 1 || L > 256) return UO_EINVAL;
+  for (l = 0; l < L; l++) {
+    if (!(imp[l] >= 0.0) || !isfinite(imp[l])) return UO_EINVAL;
+    if (imp[l] > smax) smax = imp[l];
+  }
+  for (l = 0; l < L; l++) {
+    const uint64_t ql = (smax > 0.0) ? (uint64_t)floor((imp[l] / smax) * 16777216.0) : 1u;
+    w[l] = (uo_u128)ql * (uo_u128)numel[l];
+    floor_sum += Ul[l] * (int64_t)M * (int64_t)min_cols;
+    active[l] = 1;
+  }
+  if (floor_sum > T) return UO_EBUDGET;
+  for (;;) {
+    uo_u128 Wa = 0;
+    int64_t Ta = T;
+    int changed = 0;
+    for (l = 0; l < L; l++) {
+      if (active[l]) Wa += w[l];
+      else Ta -= Ul[l] * (int64_t)M * (int64_t)min_cols;
+    }
+    for (l = 0; l < L; l++) {
+      if (!active[l]) continue;
+      num[l] = (uo_u128)Ta * w[l];
+      den[l] = Wa;
+      T_l[l] = (Wa == 0) ? 0 : (int64_t)(num[l] / den[l]);
+      if (T_l[l] < Ul[l] * (int64_t)M * (int64_t)min_cols) {
+        active[l] = 0;
+        changed = 1;
+      }
+    }
+    if (!changed) break;
+  }
+  left = T;
+  for (l = 0; l < L; l++) {
+    if (!active[l]) T_l[l] = Ul[l] * (int64_t)M * (int64_t)min_cols;
+    left -= T_l[l];
+  }
+  for (l = 0; l < L; l++) {
+    if (!active[l] || den[l] == 0) continue;
+    rem[n_rem].key = (uint64_t)(((num[l] % den[l]) << 32) / den[l]);
+    rem[n_rem].c = l;
+    n_rem++;
+  }
+  qsort(rem, (size_t)n_rem, sizeof(uo_rem_item), uo_rem_cmp);
+  for (k = 0; k < n_rem && left > 0; k++, left--) T_l[rem[k].c] += 1;
+  return UO_OK;
+}
+
 int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32_t dtype,
                 const float* const* sal, double bpw, int32_t M, int32_t gran, int32_t g, int32_t C,
-                int32_t min_cols, int32_t q, int32_t G, int64_t* unit_base, uint8_t* cls, int32_t* ncols,
-                int64_t* offsets, int64_t* layer_acct) {
+                int32_t min_cols, int32_t q, int32_t G, const double* layer_imp, int64_t* unit_base,
+                uint8_t* cls, int32_t* ncols, int64_t* offsets, int64_t* layer_acct) {
   int32_t l;
   int64_t U = 0, u;
   int32_t state_bits = (dtype == UO_BF16) ? 16 : 32;
+  int64_t two_T[256];
   if (n_layers < 1 || M < 1 || M > 8 || C < 1 || C > 255 || min_cols < 1) return UO_EINVAL;
   if (q != 0 && q != 4 && q != 8) return UO_EINVAL;
   if (q != 0 && (G < 32 || (G & (G - 1)) != 0)) return UO_EINVAL; /* power of two >= 32 */
@@ -465,6 +529,23 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
   }
   unit_base[n_layers] = U;
 
+  if (layer_imp) {
+    /* two-level: one model budget, split over layers first (raw states, ROW units) */
+    int64_t numel_l[256], Ul_l[256], budget = 0, meta_sum = 0, numel_all = 0;
+    int32_t st;
+    if (gran != UO_GRAN_ROW || q != 0 || n_layers > 256) return UO_EINVAL;
+    for (l = 0; l < n_layers; l++) {
+      numel_l[l] = outf[l] * inf[l];
+      Ul_l[l] = inf[l] / g;
+      numel_all += numel_l[l];
+      meta_sum += (C > 1) ? Ul_l[l] * (int64_t)uo_ceil_log2(C) : 0;
+    }
+    budget = (int64_t)floor(bpw * (double)numel_all);
+    if (budget < meta_sum) return UO_EBUDGET;
+    st = uo_layer_cells(n_layers, layer_imp, numel_l, Ul_l, M, min_cols, (budget - meta_sum) / state_bits, two_T);
+    if (st != UO_OK) return st;
+  }
+
   if (gran == UO_GRAN_ROW) {
     for (l = 0; l < n_layers; l++) {
       int64_t Ul = inf[l] / g, t, j;
@@ -476,6 +557,7 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       uint64_t* L_u;
       int32_t st;
       int64_t achieved = meta;
+      if (layer_imp) budget = two_T[l] * state_bits + meta; /* the layer's share of the model budget */
       if (budget < meta) return UO_EBUDGET;
       T = (q == 0) ? (budget - meta) / state_bits : ((budget - meta) / ((int64_t)q * G + 32)) * G;
       s_u = (double*)malloc(sizeof(double) * (size_t)Ul);
