@@ -96,6 +96,12 @@ typedef struct {
   int32_t group_size;    /* cells per scale group (power of two >= 32; 0 = 128); quantised plans only */
   int32_t variant;       /* usk_variant: the sketch (Appendix C.2; L27).
                             The comparison variants run on the generic kernels, raw states only. */
+  const double* layer_importance; /* host [n_layers] >= 0, or NULL.  Non-NULL (ROW granularity, raw
+                            states): two-level allocation -- one model budget floor(bpw * numel),
+                            split over layers in proportion to importance_l * numel_l (2^24 fixed
+                            point, water-filled floors U_l * M * min_cols, largest remainder), then
+                            the row allocation inside each layer (L28).
+                            NULL: every layer is its own budget scope. */
 } usk_params;
 
 typedef struct usk_plan usk_plan;

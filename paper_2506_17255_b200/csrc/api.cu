@@ -32,6 +32,55 @@ static int ceil_log2(int c) {
   return b;
 }
 
+// First level of the two-level allocation (L28): cells per layer from the layer
+// importance, exact integer arithmetic (u128); false when the floors exceed T.
+static bool layer_cells(int L, const double* imp, const std::vector<int64_t>& numel, const std::vector<int64_t>& Ul,
+                        int M, int min_cols, int64_t T, std::vector<int64_t>& Tl) {
+  typedef unsigned __int128 u128;
+  double smax = 0.0;
+  for (int l = 0; l < L; ++l) smax = std::max(smax, imp[l]);
+  std::vector<u128> w(L), num(L, 0), den(L, 0);
+  std::vector<int> active(L, 1);
+  std::vector<int64_t> fl(L);
+  int64_t floor_sum = 0;
+  for (int l = 0; l < L; ++l) {
+    const uint64_t q = smax > 0.0 ? (uint64_t)std::floor((imp[l] / smax) * 16777216.0) : 1u;
+    w[l] = (u128)q * (u128)numel[l];
+    fl[l] = Ul[l] * M * (int64_t)min_cols;
+    floor_sum += fl[l];
+  }
+  if (floor_sum > T) return false;
+  Tl.assign(L, 0);
+  for (bool changed = true; changed;) {
+    changed = false;
+    u128 Wa = 0;
+    int64_t Ta = T;
+    for (int l = 0; l < L; ++l) {
+      if (active[l]) Wa += w[l];
+      else Ta -= fl[l];
+    }
+    for (int l = 0; l < L; ++l) {
+      if (!active[l]) continue;
+      num[l] = (u128)Ta * w[l];
+      den[l] = Wa;
+      Tl[l] = Wa == 0 ? 0 : (int64_t)(num[l] / den[l]);
+      if (Tl[l] < fl[l]) active[l] = 0, changed = true;
+    }
+  }
+  int64_t left = T;
+  std::vector<std::pair<uint64_t, int>> rem;
+  for (int l = 0; l < L; ++l) {
+    if (!active[l]) Tl[l] = fl[l];
+    left -= Tl[l];
+    if (active[l] && den[l] != 0) rem.push_back({(uint64_t)(((num[l] % den[l]) << 32) / den[l]), l});
+  }
+  std::sort(rem.begin(), rem.end(), [](const std::pair<uint64_t, int>& a, const std::pair<uint64_t, int>& b) {
+    return a.first != b.first ? a.first > b.first : a.second < b.second;
+  });
+  for (size_t k = 0; k < rem.size() && left > 0; ++k, --left) Tl[rem[k].second] += 1;
+  return true;
+}
+
 static void free_plan(usk_plan* p) {
   if (!p) return;
   void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R, p->d_err};
@@ -91,6 +140,13 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   if (P.state_bits != 0 && P.state_bits != 4 && P.state_bits != 8) return fail(USK_EINVAL, "state_bits must be 0, 4 or 8");
   const int32_t qG = P.group_size ? P.group_size : 128;
   if (P.variant < USK_ABSMAXMIN || P.variant > USK_COUNTMIN) return fail(USK_EINVAL, "variant");
+  if (P.layer_importance) {
+    if (P.granularity != USK_GRAN_ROW || P.state_bits)
+      return fail(USK_EINVAL, "layer_importance: ROW granularity with raw states only");
+    for (int l = 0; l < n_layers; ++l)
+      if (!(P.layer_importance[l] >= 0.0) || !std::isfinite(P.layer_importance[l]))
+        return fail(USK_EINVAL, "layer_importance must be finite and >= 0");
+  }
   if (P.variant != USK_ABSMAXMIN && P.state_bits) return fail(USK_EUNSUPPORTED, "variants use raw states");
   if (P.state_bits && (qG < 32 || (qG & (qG - 1)) != 0))
     return fail(USK_EINVAL, "group_size must be a power of two >= 32");
@@ -140,11 +196,28 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   }
   pl->U = U;
   pl->numel = numel_all;
+  std::vector<int64_t> two_T;
+  if (P.layer_importance) {  // two-level: one model budget split over the layers first (L28)
+    std::vector<int64_t> numel(n_layers), Ul(n_layers);
+    int64_t meta_sum = 0;
+    for (int l = 0; l < n_layers; ++l) {
+      numel[l] = pl->layers[l].out * pl->layers[l].in;
+      Ul[l] = pl->layers[l].n_units;
+      meta_sum += pl->C > 1 ? Ul[l] * ceil_log2(pl->C) : 0;
+    }
+    const int64_t budget = (int64_t)std::floor(P.bpw * (double)numel_all);
+    if (budget < meta_sum || !layer_cells(n_layers, P.layer_importance, numel, Ul, pl->M, pl->min_cols,
+                                          (budget - meta_sum) / state_bits, two_T)) {
+      free_plan(pl);
+      return fail(USK_EBUDGET, "two-level allocation: the layer floors exceed the model budget");
+    }
+  }
   if (P.granularity == USK_GRAN_ROW) {
     for (int l = 0; l < n_layers; ++l) {
       LayerGeom& L = pl->layers[l];
-      const int64_t budget = (int64_t)std::floor(P.bpw * (double)(L.out * L.in));
       const int64_t meta = pl->C > 1 ? L.n_units * ceil_log2(pl->C) : 0;
+      const int64_t budget =
+          P.layer_importance ? two_T[l] * state_bits + meta : (int64_t)std::floor(P.bpw * (double)(L.out * L.in));
       if (budget < meta) {
         free_plan(pl);
         return fail(USK_EBUDGET, "budget smaller than the class map of layer " + std::to_string(l));
@@ -155,6 +228,7 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
       L.cells_T = pl->q ? ((budget - meta) / ((int64_t)pl->q * pl->G + 32)) * pl->G : (budget - meta) / state_bits;
       pl->budget_bits += budget;
     }
+    if (P.layer_importance) pl->budget_bits = (int64_t)std::floor(P.bpw * (double)numel_all);  // one model scope
   } else {
     const int64_t budget = (int64_t)std::floor(P.bpw * (double)numel_all);
     pl->layers[0].budget_bits = budget;

@@ -163,3 +163,21 @@ def test_quantised_paper_point_full_layer_sampled(orc, usk):
     usk.reconstruct(pl, sk, 0, Wr)
     got = w_bits(Wr, "bf16")[oj[:, 0], oj[:, 1]]
     np.testing.assert_array_equal(got, want)
+
+
+def test_two_level_allocation_plan_parity(orc, usk):
+    # SURVEY 8(f4) two-level (layer x row) allocation: the device plan equals the oracle's, with
+    # saliency-driven classes inside each layer (ledger L28)
+    shapes = [(256, 128), (128, 256), (512, 128), (64, 64)]
+    imp = [4.0, 1.5, 2.0, 0.25]
+    rng = np.random.default_rng(4)
+    sal = [rng.gamma(1.0, 1.0, i).astype(np.float32) for o, i in shapes]
+    pl = usk.plan_allocation(shapes, bpw=1.0, rows=3, dtype="bf16", seed=6, layer_importance=imp,
+                             saliency=[torch.from_numpy(s).cuda() for s in sal])
+    opl = orc.plan(shapes, 1.0, M=3, dtype=orc.BF16, seed=6, layer_importance=np.array(imp), saliency=sal)
+    assert_plan_equal(pl, opl)
+    W = make_weights(shapes, "bf16", 2)
+    sk = pl.new_sketch()
+    usk.build(pl, [to_dev(w, "bf16") for w in W], sk)
+    osk = orc.build_model(opl, W)
+    np.testing.assert_array_equal(sk.cpu().numpy().view(np.uint16)[:opl.total_cells], osk)
