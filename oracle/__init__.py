@@ -71,7 +71,9 @@ def lib():
         L.uo_allocate.restype = i32
         L.uo_allocate.argtypes = [i64, p, p, i64, i32, i32, i32, p, p]
         L.uo_plan.restype = i32
-        L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, i32, i32, p, p, p, p, p, p]
+        L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, i32, i32, p, i64, p, p, p, p, p]
+        L.uo_topk.restype = i32
+        L.uo_topk.argtypes = [i32, p, i64, i64, p, p]
         L.uo_layer_cells.restype = i32
         L.uo_layer_cells.argtypes = [i32, p, p, p, i32, i32, i64, p]
         L.uo_quantize.restype = i32
@@ -85,7 +87,7 @@ def lib():
         L.uo_f32_to_bf16_rne.restype = u32
         L.uo_f32_to_bf16_rne.argtypes = [u32]
         L.uo_build_units.restype = i32
-        L.uo_build_units.argtypes = [i32, p, i64, i64, i32, i32, i32, i64, i64, p, p, i32, i32, u64, p, i32]
+        L.uo_build_units.argtypes = [i32, p, i64, i64, i32, i32, i32, i64, i64, p, p, i32, i32, u64, p, i32, p]
         L.uo_reconstruct_rows.restype = i32
         L.uo_reconstruct_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, i64, i64, p, i32]
         L.uo_reconstruct_entries.restype = i32
@@ -221,6 +223,7 @@ class Plan:
     state_bits: int = 0     # 0: raw states in the weight dtype; 4 / 8: stacked quantisation
     group: int = 128        # cells per quantisation group (layers start at multiples of it)
     variant: int = 0        # ABSMAXMIN (the paper's sketch), ABSMINMAX, COUNTMIN (App. C.2)
+    topk: int = 0           # Top-K outliers per layer stored apart (App. A)
     extra: dict = field(default_factory=dict)
 
     @property
@@ -237,7 +240,8 @@ class Plan:
 
 
 def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None, min_cols=1,
-         hash_kind=HASH_X, seed=0, state_bits=0, group=128, variant=ABSMAXMIN, layer_importance=None) -> Plan:
+         hash_kind=HASH_X, seed=0, state_bits=0, group=128, variant=ABSMAXMIN, layer_importance=None,
+         topk=0) -> Plan:
     L = len(shapes)
     outf = np.array([s[0] for s in shapes], dtype=np.int64)
     inf = np.array([s[1] for s in shapes], dtype=np.int64)
@@ -258,11 +262,12 @@ def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None
     st = lib().uo_plan(L, _ptr(outf), _ptr(inf), dtype,
                        ct.cast(sal_ptrs, ct.c_void_p) if sal_ptrs is not None else None,
                        float(bpw), M, gran, g, C, min_cols, state_bits, group,
-                       None if limp is None else _ptr(limp), _ptr(unit_base), _ptr(cls),
+                       None if limp is None else _ptr(limp), int(topk), _ptr(unit_base), _ptr(cls),
                        _ptr(ncols), _ptr(offsets), _ptr(acct))
     _check(st, "plan")
     return Plan(list(map(tuple, zip(outf.tolist(), inf.tolist()))), dtype, M, gran, g, C, min_cols, hash_kind,
-                seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4), state_bits, group, variant)
+                seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4), state_bits, group, variant,
+                int(topk))
 
 
 def layer_cells(importance, numel, units, M, min_cols, T) -> np.ndarray:
@@ -279,9 +284,10 @@ def _np_dtype(dtype):
     return np.uint16 if dtype == BF16 else np.uint32
 
 
-def build_layer(pl: Plan, l: int, W: np.ndarray, sketch: np.ndarray, t_begin=0, t_end=None):
+def build_layer(pl: Plan, l: int, W: np.ndarray, sketch: np.ndarray, t_begin=0, t_end=None, exclude=None):
     """Build units [t_begin, t_end) of layer l from W ([out,in] raw bits: uint16 bf16 / float32)
-    into the model sketch (raw cells, uint16 or uint32)."""
+    into the model sketch (raw cells, uint16 or uint32).  exclude: optional [out, in] bool mask of
+    weights kept out of the sketch (Top-K outliers)."""
     out, inn = pl.shapes[l]
     u0, u1 = pl.layer_units(l)
     t_end = (u1 - u0) if t_end is None else t_end
@@ -291,8 +297,30 @@ def build_layer(pl: Plan, l: int, W: np.ndarray, sketch: np.ndarray, t_begin=0, 
     assert W.shape == (out, inn)
     ncols, offs = pl.layer_slices(l)
     assert sketch.dtype == _np_dtype(pl.dtype) and sketch.flags["C_CONTIGUOUS"]
+    ex = None if exclude is None else np.ascontiguousarray(exclude, dtype=np.uint8)
     _check(lib().uo_build_units(pl.dtype, _ptr(W), out, inn, l, pl.gran, pl.g, t_begin, t_end, _ptr(ncols),
-                                _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(sketch), pl.variant), "build_units")
+                                _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(sketch), pl.variant,
+                                None if ex is None else _ptr(ex)), "build_units")
+
+
+def topk(dtype, W: np.ndarray, K: int):
+    """Top-K outliers of W (App. A): flat indices (ascending) and raw bits of the K weights of
+    largest |w| (ties -> smaller flat index)."""
+    Wb = np.ascontiguousarray(W, dtype=_np_dtype(dtype)) if dtype == BF16 else \
+        np.ascontiguousarray(W, dtype=np.float32).view(np.uint32)
+    n = Wb.size
+    idx = np.zeros(max(K, 1), dtype=np.int64)
+    vals = np.zeros(max(K, 1), dtype=np.uint32)
+    _check(lib().uo_topk(dtype, _ptr(Wb), n, K, _ptr(idx), _ptr(vals)), "topk")
+    return idx[:K], vals[:K]
+
+
+@dataclass
+class TSketch:
+    """A sketch with Top-K outlier side tables: raw cells + per layer (flat indices, raw bits)."""
+    cells: np.ndarray
+    idx: list
+    vals: list
 
 
 @dataclass
@@ -347,6 +375,16 @@ def build_model(pl: Plan, weights, layers=None):
     """Raw plans: the sketch cells (uint16 / uint32).  Quantised plans: a QSketch (raw states
     built into a +Inf-initialised buffer, then quantised per group)."""
     layers = range(len(weights)) if layers is None else layers
+    if pl.topk:
+        cells = np.zeros(pl.total_cells, dtype=_np_dtype(pl.dtype))
+        idx, vals = [None] * len(pl.shapes), [None] * len(pl.shapes)
+        for l, W in zip(layers, weights):
+            out, inn = pl.shapes[l]
+            idx[l], vals[l] = topk(pl.dtype, W, min(pl.topk, out * inn))
+            mask = np.zeros(out * inn, dtype=bool)
+            mask[idx[l]] = True
+            build_layer(pl, l, W, cells, exclude=mask.reshape(out, inn))
+        return TSketch(cells, idx, vals)
     if not pl.state_bits:
         sketch = np.zeros(pl.total_cells, dtype=_np_dtype(pl.dtype))
         for l, W in zip(layers, weights):
@@ -363,6 +401,8 @@ def _retrieval_view(pl: Plan, sketch):
     """(dtype, cells) on which Eq. 5 runs: raw cells, or the dequantised fp32 cells."""
     if isinstance(sketch, QSketch):
         return F32, sketch.deq
+    if isinstance(sketch, TSketch):
+        return pl.dtype, sketch.cells
     return pl.dtype, sketch
 
 
@@ -382,6 +422,10 @@ def reconstruct_rows(pl: Plan, sketch, l: int, o_begin=0, o_end=None) -> np.ndar
     _check(lib().uo_reconstruct_rows(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs),
                                      pl.M, pl.hash_kind, pl.seed, o_begin, o_end, _ptr(res), pl.variant),
            "reconstruct_rows")
+    if isinstance(sketch, TSketch):  # outliers keep their value (App. A)
+        o_idx, j_idx = sketch.idx[l] // inn, sketch.idx[l] % inn
+        sel = (o_idx >= o_begin) & (o_idx < o_end)
+        res[o_idx[sel] - o_begin, j_idx[sel]] = sketch.vals[l][sel]
     return _to_plan_dtype(pl, sketch, res)
 
 
@@ -394,6 +438,11 @@ def reconstruct_entries(pl: Plan, sketch, l: int, oj: np.ndarray) -> np.ndarray:
     _check(lib().uo_reconstruct_entries(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols),
                                         _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(oj), len(oj), _ptr(res),
                                         pl.variant), "reconstruct_entries")
+    if isinstance(sketch, TSketch):
+        flat = oj[:, 0] * inn + oj[:, 1]
+        pos = np.searchsorted(sketch.idx[l], flat)
+        hit = (pos < len(sketch.idx[l])) & (sketch.idx[l][np.minimum(pos, len(sketch.idx[l]) - 1)] == flat)
+        res[hit] = sketch.vals[l][pos[hit]]
     return _to_plan_dtype(pl, sketch, res).astype(np.uint32)
 
 
@@ -404,6 +453,8 @@ def linear_rows(pl: Plan, sketch, l: int, x: np.ndarray, o_begin=0, o_end=None) 
     o_end = out if o_end is None else o_end
     x = np.ascontiguousarray(np.atleast_2d(x), dtype=np.float64)
     T = x.shape[0]
+    if isinstance(sketch, TSketch):  # fp64 matmul of the overlaid W' (uo_linear_rows is pinned to it)
+        return x @ value_of(reconstruct_rows(pl, sketch, l, o_begin, o_end), pl.dtype).T
     ncols, offs = pl.layer_slices(l)
     dt, cells = _retrieval_view(pl, sketch)
     y = np.zeros((T, o_end - o_begin), dtype=np.float64)

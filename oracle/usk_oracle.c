@@ -505,7 +505,7 @@ int32_t uo_layer_cells(int32_t L, const double* imp, const int64_t* numel, const
 
 int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32_t dtype,
                 const float* const* sal, double bpw, int32_t M, int32_t gran, int32_t g, int32_t C,
-                int32_t min_cols, int32_t q, int32_t G, const double* layer_imp, int64_t* unit_base,
+                int32_t min_cols, int32_t q, int32_t G, const double* layer_imp, int64_t topk, int64_t* unit_base,
                 uint8_t* cls, int32_t* ncols, int64_t* offsets, int64_t* layer_acct) {
   int32_t l;
   int64_t U = 0, u;
@@ -529,6 +529,7 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
   }
   unit_base[n_layers] = U;
 
+  if (topk < 0 || (topk > 0 && (gran != UO_GRAN_ROW || q != 0))) return UO_EINVAL;
   if (layer_imp) {
     /* two-level: one model budget, split over layers first (raw states, ROW units) */
     int64_t numel_l[256], Ul_l[256], budget = 0, meta_sum = 0, numel_all = 0;
@@ -557,9 +558,15 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       uint64_t* L_u;
       int32_t st;
       int64_t achieved = meta;
+      /* Top-K outliers (App. A): K = min(topk, numel) weights of the layer stored apart as
+       * (32-bit flat index, state) pairs, charged to the layer (ledger L29) */
+      const int64_t K = topk < numel ? topk : numel;
+      const int64_t side = K * (32 + (int64_t)state_bits);
       if (layer_imp) budget = two_T[l] * state_bits + meta; /* the layer's share of the model budget */
-      if (budget < meta) return UO_EBUDGET;
-      T = (q == 0) ? (budget - meta) / state_bits : ((budget - meta) / ((int64_t)q * G + 32)) * G;
+      if (budget < meta + side) return UO_EBUDGET;
+      achieved += side;
+      T = (q == 0) ? (budget - meta - side) / state_bits
+                   : ((budget - meta - side) / ((int64_t)q * G + 32)) * G;
       s_u = (double*)malloc(sizeof(double) * (size_t)Ul);
       L_u = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)Ul);
       for (t = 0; t < Ul; t++) {
@@ -741,7 +748,7 @@ static void uo_unit_span(int32_t gran, int32_t g, int64_t in, int64_t t, int64_t
 int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, int32_t layer,
                        int32_t gran, int32_t g, int64_t t_begin, int64_t t_end,
                        const int32_t* ncols, const int64_t* offsets, int32_t M, int32_t hash_kind,
-                       uint64_t seed, void* sketch, int32_t variant) {
+                       uint64_t seed, void* sketch, int32_t variant, const uint8_t* exclude) {
   int64_t t;
   for (t = t_begin; t < t_end; t++) {
     int64_t j0, j1, j, o, n, k = 0;
@@ -755,11 +762,12 @@ int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, in
     cells = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)M * (size_t)ncols[t]);
     for (o = 0; o < out; o++) /* stream W in its row-major order */
       for (j = j0; j < j1; j++) {
+        if (exclude && exclude[o * in + j]) continue; /* Top-K outliers are stored apart */
         wb[k] = uo_load(dtype, W, o * in + j);
         pos[k] = (uint32_t)((j - j0) * out + o);
         k++;
       }
-    st = uo_sketch_unit_v(variant, dtype, wb, pos, n, hash_kind, seed, (uint32_t)layer, (uint32_t)t, M,
+    st = uo_sketch_unit_v(variant, dtype, wb, pos, k, hash_kind, seed, (uint32_t)layer, (uint32_t)t, M,
                           (uint32_t)ncols[t], cells);
     if (st == UO_OK)
       for (c = 0; c < (int64_t)M * ncols[t]; c++) uo_store(dtype, sketch, offsets[t] + c, cells[c]);
@@ -924,6 +932,40 @@ int32_t uo_stats(int32_t dtype, const void* W, const void* Wp, int64_t out, int6
   counts[11] = n_cells;
   for (c = 0; c < n_cells; c++) counts[12] += occ[c] == 0;
   free(occ);
+  return UO_OK;
+}
+
+/* Top-K outliers (Appendix A: "considers weights with top-k large absolute
+ * values as important ones, stores them independently, and keeps their value untouched"):
+ * the K weights of largest |w| (ties -> smaller flat index o*in + j), returned as flat indices in
+ * ascending order with their raw bits.  Plain selection: K passes over the weights. */
+int32_t uo_topk(int32_t dtype, const void* W, int64_t n, int64_t K, int64_t* idx, uint32_t* vals) {
+  uint8_t* taken;
+  int64_t k, e, c = 0;
+  if (K < 0 || K > n) return UO_EINVAL;
+  taken = (uint8_t*)calloc((size_t)(n > 0 ? n : 1), 1);
+  for (k = 0; k < K; k++) {
+    int64_t best = -1;
+    double bv = -1.0;
+    for (e = 0; e < n; e++) {
+      double a;
+      if (taken[e]) continue;
+      a = fabs(uo_value(dtype, uo_load_bits(dtype, W, e)));
+      if (a > bv) {
+        bv = a;
+        best = e;
+      }
+    }
+    if (best < 0) break; /* only non-finite weights left (the build rejects them) */
+    taken[best] = 1;
+  }
+  for (e = 0; e < n; e++)
+    if (taken[e]) {
+      idx[c] = e;
+      vals[c] = uo_load_bits(dtype, W, e);
+      c++;
+    }
+  free(taken);
   return UO_OK;
 }
 
