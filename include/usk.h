@@ -102,6 +102,12 @@ typedef struct {
                             point, water-filled floors U_l * M * min_cols, largest remainder), then
                             the row allocation inside each layer (L28).
                             NULL: every layer is its own budget scope. */
+  int64_t topk;          /* Top-K outliers per layer (App. A): the min(topk, numel)
+                            weights of largest |w| (ties -> smaller flat index o*in + j) are kept
+                            exactly in a side table of (int32 flat index, state) pairs charged to
+                            the layer budget (32 + state bits each), left out of the sketch, and
+                            overlaid on every retrieval (L29).  ROW granularity, raw
+                            states, AbsMaxMin only; 0 = none. */
 } usk_params;
 
 typedef struct usk_plan usk_plan;
@@ -124,6 +130,7 @@ typedef struct {
                              of group_size, total_cells includes the padding) */
   int64_t scales_offset;  /* quantised plans: byte offset of the fp32 scales in the sketch buffer;
                              the codes (packed, cell c at bit c*state_bits) start at byte 0 */
+  int64_t topk;           /* Top-K outliers per layer (0 = none) */
 } usk_plan_info;
 
 typedef struct {
@@ -136,7 +143,11 @@ typedef struct {
   int64_t budget_bits;    /* ROW: floor(bpw * numel_l); LAYER: model budget on layer 0, else 0 */
   int64_t meta_bits;      /* charged class-map bits (ROW with C > 1: U_l * ceil(log2 C)) */
   int64_t cells_T;        /* cells available to the scope (ROW per layer; LAYER on layer 0) */
-  int64_t achieved_bits;  /* states of this layer * state bits + meta_bits */
+  int64_t achieved_bits;  /* states of this layer * state bits + meta_bits (+ outlier side table) */
+  int64_t n_outliers;     /* Top-K: outliers of this layer (min(topk, numel)) */
+  int64_t outlier_offset; /* Top-K: byte offset in the sketch of the layer's side table: n_outliers
+                             int32 flat indices (ascending), then at the next 16-B boundary their
+                             states in the plan dtype */
 } usk_layer_info;
 
 /* Importance metric, Eq. 7: I[j] = (1/N) sum_k A[k, j]^2.

@@ -140,6 +140,9 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   if (P.state_bits != 0 && P.state_bits != 4 && P.state_bits != 8) return fail(USK_EINVAL, "state_bits must be 0, 4 or 8");
   const int32_t qG = P.group_size ? P.group_size : 128;
   if (P.variant < USK_ABSMAXMIN || P.variant > USK_COUNTMIN) return fail(USK_EINVAL, "variant");
+  if (P.topk < 0) return fail(USK_EINVAL, "topk must be >= 0");
+  if (P.topk > 0 && (P.granularity != USK_GRAN_ROW || P.state_bits || P.variant != USK_ABSMAXMIN))
+    return fail(USK_EINVAL, "topk: ROW granularity, raw states and AbsMaxMin only");
   if (P.layer_importance) {
     if (P.granularity != USK_GRAN_ROW || P.state_bits)
       return fail(USK_EINVAL, "layer_importance: ROW granularity with raw states only");
@@ -170,6 +173,7 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   pl->min_cols = P.min_cols;
   pl->hash = P.hash;
   pl->variant = P.variant;
+  pl->topk = P.topk;
   pl->dtype = P.dtype;
   pl->bpw = P.bpw;
   pl->seed = P.seed;
@@ -224,8 +228,16 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
       }
       L.budget_bits = budget;
       L.meta_bits = meta;
+      // Top-K outliers: (int32 index, state) pairs charged to the layer (L29)
+      L.n_out = std::min<int64_t>(pl->topk, L.out * L.in);
+      const int64_t side = L.n_out * (32 + state_bits);
+      if (budget < meta + side) {
+        free_plan(pl);
+        return fail(USK_EBUDGET, "Top-K side table exceeds the budget of layer " + std::to_string(l));
+      }
       // quantised: ceil(cells/G) groups of q*G code bits + one fp32 scale (layers G-aligned)
-      L.cells_T = pl->q ? ((budget - meta) / ((int64_t)pl->q * pl->G + 32)) * pl->G : (budget - meta) / state_bits;
+      L.cells_T = pl->q ? ((budget - meta - side) / ((int64_t)pl->q * pl->G + 32)) * pl->G
+                        : (budget - meta - side) / state_bits;
       pl->budget_bits += budget;
     }
     if (P.layer_importance) pl->budget_bits = (int64_t)std::floor(P.bpw * (double)numel_all);  // one model scope
@@ -278,6 +290,15 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
     pl->n_groups = pl->total_cells / pl->G;
     pl->scales_off = (pl->code_bytes() + 255) / 256 * 256;
   }
+  if (pl->topk) {  // side tables after the cells, layer by layer (16-B aligned pieces)
+    int64_t off = (pl->total_cells * pl->cell_bytes() + 255) / 256 * 256;
+    for (int l = 0; l < n_layers; ++l) {
+      LayerGeom& L = pl->layers[l];
+      L.out_off = off;
+      off += (L.n_out * 4 + 15) / 16 * 16 + (L.n_out * pl->cell_bytes() + 15) / 16 * 16;
+    }
+    pl->side_bytes = off - (pl->total_cells * pl->cell_bytes() + 255) / 256 * 256;
+  }
   pl->achieved_bits = 0;
   for (int l = 0; l < n_layers; ++l) {
     LayerGeom& L = pl->layers[l];
@@ -287,7 +308,7 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
     for (int64_t u = L.unit_begin; u < L.unit_begin + L.n_units; ++u) mx = std::max(mx, pl->h_ncols[u]);
     L.max_ncols = mx;
     L.achieved_bits = pl->q ? (L.n_cells + pl->G - 1) / pl->G * ((int64_t)pl->q * pl->G + 32) + L.meta_bits
-                            : L.n_cells * state_bits + L.meta_bits;
+                            : L.n_cells * state_bits + L.meta_bits + L.n_out * (32 + state_bits);
     pl->achieved_bits += L.achieved_bits;
   }
   *plan_out = pl;
@@ -302,12 +323,14 @@ usk_status usk_plan_query(const usk_plan* pl, usk_plan_info* out) {
   out->dtype = pl->dtype;
   out->n_units = pl->U;
   out->total_cells = pl->total_cells;
-  const int64_t bytes = pl->q ? pl->scales_off + pl->n_groups * 4 : pl->total_cells * pl->cell_bytes();
+  const int64_t bytes = pl->q ? pl->scales_off + pl->n_groups * 4
+                              : (pl->total_cells * pl->cell_bytes() + 255) / 256 * 256 + pl->side_bytes;
   out->sketch_bytes = ((bytes + 255) / 256) * 256 + 256;
   out->state_bits = pl->q;
   out->group_size = pl->q ? pl->G : 0;
   out->n_groups = pl->n_groups;
   out->scales_offset = pl->scales_off;
+  out->topk = pl->topk;
   out->numel = pl->numel;
   out->budget_bits = pl->budget_bits;
   out->achieved_bits = pl->achieved_bits;
@@ -318,8 +341,8 @@ usk_status usk_plan_layer(const usk_plan* pl, int32_t layer, usk_layer_info* out
   if (!pl || !out) return fail(USK_EINVAL, "usk_plan_layer: null");
   if (layer < 0 || layer >= pl->n_layers) return fail(USK_ESHAPE, "usk_plan_layer: layer out of range");
   const LayerGeom& L = pl->layers[layer];
-  *out = usk_layer_info{L.out, L.in, L.unit_begin, L.n_units, L.cell_begin, L.n_cells,
-                        L.budget_bits, L.meta_bits, L.cells_T, L.achieved_bits};
+  *out = usk_layer_info{L.out,         L.in,        L.unit_begin, L.n_units,       L.cell_begin, L.n_cells,
+                        L.budget_bits, L.meta_bits, L.cells_T,    L.achieved_bits, L.n_out,      L.out_off};
   return USK_OK;
 }
 

@@ -20,6 +20,8 @@
 // then converted to states.
 #include <algorithm>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "common.cuh"
 #include "ptx.cuh"
 
@@ -52,6 +54,7 @@ struct BuildArgs {
   const uint32_t* R;
   void* sketch;
   int* err;
+  uint32_t kap_max;  // largest accepted weight key: 0xFEFFFFFF (finite), 0xFF000000 (+Inf = excluded outlier)
 };
 
 template <int ES>
@@ -205,7 +208,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
     }
-    if (kmax >= 0xFF000000u) atomicOr(A.err, 1);  // NaN / Inf weight (USK_ENONFINITE)
+    if (kmax > A.kap_max) atomicOr(A.err, 1);  // NaN / Inf weight (USK_ENONFINITE)
   }
   __syncthreads();
 
@@ -258,7 +261,7 @@ __device__ __forceinline__ void cas_min16(uint16_t* cell, uint32_t key16) {
 template <int ES, int HASH>
 __global__ void k_gen_scatter(GenLayer G, const void* W, int32_t layer_M, HashConsts hc,
                               const int32_t* ncols, const int64_t* offsets, const uint32_t* ukeys,
-                              void* sketch, int* err) {
+                              void* sketch, int* err, uint32_t kap_max) {
   const int64_t n = G.out * G.in;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -272,7 +275,7 @@ __global__ void k_gen_scatter(GenLayer G, const void* W, int32_t layer_M, HashCo
     uint32_t bhi = (ES == 2) ? ((uint32_t)reinterpret_cast<const uint16_t*>(W)[e] << 16)
                              : reinterpret_cast<const uint32_t*>(W)[e];
     const uint32_t kap = rotl1(bhi);
-    if (kap >= 0xFF000000u) atomicOr(err, 1);
+    if (kap > kap_max) atomicOr(err, 1);
     const uint32_t h = fmix32((uint32_t)p ^ hc.rho) ^ ukeys[u];
     for (int i = 0; i < layer_M; ++i) {
       const uint32_t idx = (HASH == USK_HASH_X) ? __umulhi(h * hc.a[i], N) : (uint32_t)(p % N);
@@ -430,6 +433,47 @@ __global__ void k_cm_final(const unsigned long long* acc, int64_t n, void* sketc
   else reinterpret_cast<uint32_t*>(sketch)[c0 + i] = b;
 }
 
+// ---------------------------------------------------------------- Top-K outliers
+// (Appendix A; DESIGN.md ledger L29).  Selection key of weight e:
+// (|w| bits << 32) | (2^32 - 1 - e): a descending sort ranks by |w|, ties -> smaller index.
+__global__ void k_topk_keys(const void* W, int32_t es, int64_t n, unsigned long long* keys, int* err) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  uint32_t mag;
+  if (es == 2) {
+    const uint32_t b = reinterpret_cast<const uint16_t*>(W)[e];
+    if ((b & 0x7F80u) == 0x7F80u) atomicOr(err, 1);
+    mag = b & 0x7FFFu;
+  } else {
+    const uint32_t b = reinterpret_cast<const uint32_t*>(W)[e];
+    if ((b & 0x7F800000u) == 0x7F800000u) atomicOr(err, 1);
+    mag = b & 0x7FFFFFFFu;
+  }
+  keys[e] = ((unsigned long long)mag << 32) | (unsigned long long)(0xFFFFFFFFu - (uint32_t)e);
+}
+
+__global__ void k_topk_take(const unsigned long long* sorted, int64_t K, uint32_t* idx) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k < K) idx[k] = 0xFFFFFFFFu - (uint32_t)(sorted[k] & 0xFFFFFFFFull);
+}
+
+// side table (ascending flat indices, their states) + the outlier marked +Inf (= excluded) in
+// the build copy of W
+__global__ void k_topk_finish(const uint32_t* idx, int64_t K, const void* W, int32_t es, int32_t* tab_idx,
+                              void* tab_vals, void* Wb) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= K) return;
+  const uint32_t e = idx[k];
+  tab_idx[k] = (int32_t)e;
+  if (es == 2) {
+    reinterpret_cast<uint16_t*>(tab_vals)[k] = reinterpret_cast<const uint16_t*>(W)[e];
+    reinterpret_cast<uint16_t*>(Wb)[e] = 0x7F80;
+  } else {
+    reinterpret_cast<uint32_t*>(tab_vals)[k] = reinterpret_cast<const uint32_t*>(W)[e];
+    reinterpret_cast<uint32_t*>(Wb)[e] = 0x7F800000u;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 int fast_upl(const usk_plan* pl, int32_t l) {
   // units per lane for the fast kernels, 0 = not eligible: the largest UPL whose key array and
@@ -469,7 +513,7 @@ usk_status launch_fast_m(BuildArgs& A, int n_ctas, int hash, cudaStream_t st) {
 }
 
 usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_t, const void*>>& group,
-                       void* sketch, cudaStream_t st) {
+                       void* sketch, cudaStream_t st, uint32_t kap_max) {
   // longest tasks first (largest out) so the big CTAs start in the first wave
   std::stable_sort(group.begin(), group.end(), [&](auto& a, auto& b) {
     return pl->layers[a.first].out > pl->layers[b.first].out;
@@ -484,6 +528,7 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
     A.R = pl->d_R;
     A.sketch = sketch;
     A.err = pl->d_err;
+    A.kap_max = kap_max;
     int tiles = 0, maxmn = 1;
     const int TJ = 32 * upl;
     for (size_t k = g0; k < std::min(group.size(), g0 + kMaxTasks); ++k) {
@@ -513,7 +558,8 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
 }
 
 template <int ES>
-usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* sketch, cudaStream_t st) {
+usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* sketch, cudaStream_t st,
+                            uint32_t kap_max = 0xFEFFFFFFu) {
   const LayerGeom& L = pl->layers[l];
   GenLayer G{L.out, L.in, L.unit_begin, L.cell_begin, L.n_cells, pl->gran, pl->g};
   const int T = 256;
@@ -555,10 +601,10 @@ usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* 
   const unsigned blocks = (unsigned)std::min<int64_t>((n + T - 1) / T, 148 * 16);
   if (pl->hash == USK_HASH_X)
     k_gen_scatter<ES, USK_HASH_X><<<blocks, T, 0, st>>>(G, W, pl->M, pl->hc, pl->d_ncols, pl->d_offsets, pl->d_keys,
-                                                        sketch, pl->d_err);
+                                                        sketch, pl->d_err, kap_max);
   else
     k_gen_scatter<ES, USK_HASH_IDENTITY><<<blocks, T, 0, st>>>(G, W, pl->M, pl->hc, pl->d_ncols, pl->d_offsets,
-                                                               pl->d_keys, sketch, pl->d_err);
+                                                               pl->d_keys, sketch, pl->d_err, kap_max);
   USK_LAUNCHED("k_gen_scatter");
   k_gen_final<ES><<<(unsigned)((L.n_cells + T - 1) / T), T, 0, st>>>(sketch, L.cell_begin, L.n_cells);
   USK_LAUNCHED("k_gen_final");
@@ -570,7 +616,7 @@ usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* 
 bool layer_fast_ok(const usk_plan* pl, int32_t l) { return fast_upl(pl, l) != 0; }
 
 static usk_status launch_build_raw(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids,
-                                   int32_t n, void* sketch, cudaStream_t st) {
+                                   int32_t n, void* sketch, cudaStream_t st, uint32_t kap_max = 0xFEFFFFFFu) {
   std::vector<std::pair<int32_t, const void*>> grp[5];  // by units per lane (1, 2, 4)
   for (int32_t k = 0; k < n; ++k) {
     const int32_t l = layer_ids ? layer_ids[k] : k;
@@ -578,14 +624,14 @@ static usk_status launch_build_raw(const usk_plan* pl, const void* const* weight
     if (upl) {
       grp[upl].push_back({l, weights[k]});
     } else {
-      usk_status s = pl->dtype == USK_BF16 ? launch_generic_t<2>(pl, l, weights[k], sketch, st)
-                                            : launch_generic_t<4>(pl, l, weights[k], sketch, st);
+      usk_status s = pl->dtype == USK_BF16 ? launch_generic_t<2>(pl, l, weights[k], sketch, st, kap_max)
+                                            : launch_generic_t<4>(pl, l, weights[k], sketch, st, kap_max);
       if (s != USK_OK) return s;
     }
   }
   for (int upl : {4, 2, 1}) {
     if (grp[upl].empty()) continue;
-    usk_status s = launch_fast(pl, upl, grp[upl], sketch, st);
+    usk_status s = launch_fast(pl, upl, grp[upl], sketch, st, kap_max);
     if (s != USK_OK) return s;
   }
   return USK_OK;
@@ -595,8 +641,68 @@ static usk_status launch_build_raw(const usk_plan* pl, const void* const* weight
 // with the plan's (G-aligned) cell offsets, then quantised group by group into the sketch:
 // codes at byte 0, fp32 scales at scales_off.  Groups never straddle layers, so a layer-sharded
 // build quantises exactly the groups of its layers.
+// Top-K plans (L29): per built layer, a device top-K selection (CUB radix sort of the
+// selection keys) writes the side table, and a copy of W with the outliers set to +Inf (a key no
+// finite weight loses to, so they never enter a cell) is sketched instead of W.
+static usk_status launch_build_topk(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids,
+                                    int32_t n, void* sketch, cudaStream_t st) {
+  const int es = pl->cell_bytes();
+  std::vector<void*> temps;
+  std::vector<const void*> wb(n);
+  usk_status s = USK_OK;
+  auto cuda_ok = [&](cudaError_t e, const char* what) {
+    if (e != cudaSuccess && s == USK_OK) s = cuda_fail(e, what);
+    return s == USK_OK;
+  };
+  for (int32_t k = 0; k < n && s == USK_OK; ++k) {
+    const LayerGeom& L = pl->layers[layer_ids ? layer_ids[k] : k];
+    const int64_t ne = L.out * L.in, K = L.n_out;
+    wb[k] = weights[k];
+    if (K == 0) continue;
+    void *Wc = nullptr, *keys = nullptr, *keys2 = nullptr, *idx = nullptr, *idx2 = nullptr, *tmp = nullptr;
+    size_t tb1 = 0, tb2 = 0;
+    if (!cuda_ok(cudaMallocAsync(&Wc, (size_t)ne * es, st), "cudaMallocAsync")) break;
+    temps.push_back(Wc);
+    cuda_ok(cudaMemcpyAsync(Wc, weights[k], (size_t)ne * es, cudaMemcpyDeviceToDevice, st), "cudaMemcpyAsync");
+    cuda_ok(cudaMallocAsync(&keys, (size_t)ne * 8, st), "cudaMallocAsync");
+    cuda_ok(cudaMallocAsync(&keys2, (size_t)ne * 8, st), "cudaMallocAsync");
+    cuda_ok(cudaMallocAsync(&idx, (size_t)K * 4, st), "cudaMallocAsync");
+    cuda_ok(cudaMallocAsync(&idx2, (size_t)K * 4, st), "cudaMallocAsync");
+    cuda_ok(cub::DeviceRadixSort::SortKeysDescending(nullptr, tb1, (unsigned long long*)keys,
+                                                     (unsigned long long*)keys2, (int)ne, 0, 64, st), "cub");
+    cuda_ok(cub::DeviceRadixSort::SortKeys(nullptr, tb2, (uint32_t*)idx, (uint32_t*)idx2, (int)K, 0, 32, st), "cub");
+    cuda_ok(cudaMallocAsync(&tmp, std::max(tb1, tb2), st), "cudaMallocAsync");
+    if (s != USK_OK) break;
+    k_topk_keys<<<(unsigned)((ne + 255) / 256), 256, 0, st>>>(weights[k], es, ne, (unsigned long long*)keys,
+                                                             pl->d_err);
+    cuda_ok(cudaGetLastError(), "k_topk_keys");
+    count_launch();
+    cuda_ok(cub::DeviceRadixSort::SortKeysDescending(tmp, tb1, (unsigned long long*)keys, (unsigned long long*)keys2,
+                                                     (int)ne, 0, 64, st), "cub sort");
+    count_launch();
+    k_topk_take<<<(unsigned)((K + 255) / 256), 256, 0, st>>>((unsigned long long*)keys2, K, (uint32_t*)idx);
+    cuda_ok(cudaGetLastError(), "k_topk_take");
+    count_launch();
+    cuda_ok(cub::DeviceRadixSort::SortKeys(tmp, tb2, (uint32_t*)idx, (uint32_t*)idx2, (int)K, 0, 32, st), "cub sort");
+    count_launch();
+    char* tab = reinterpret_cast<char*>(sketch) + L.out_off;
+    k_topk_finish<<<(unsigned)((K + 255) / 256), 256, 0, st>>>((uint32_t*)idx2, K, weights[k], es,
+                                                               reinterpret_cast<int32_t*>(tab),
+                                                               tab + (K * 4 + 15) / 16 * 16, Wc);
+    cuda_ok(cudaGetLastError(), "k_topk_finish");
+    count_launch();
+    void* frees[] = {keys, keys2, idx, idx2, tmp};
+    for (void* f : frees) cuda_ok(cudaFreeAsync(f, st), "cudaFreeAsync");
+    wb[k] = Wc;
+  }
+  if (s == USK_OK) s = launch_build_raw(pl, wb.data(), layer_ids, n, sketch, st, 0xFF000000u);
+  for (void* t : temps) cudaFreeAsync(t, st);
+  return s;
+}
+
 usk_status launch_build(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
                         void* sketch, cudaStream_t st) {
+  if (pl->topk) return launch_build_topk(pl, weights, layer_ids, n, sketch, st);
   if (!pl->q) return launch_build_raw(pl, weights, layer_ids, n, sketch, st);
   const int es = pl->cell_bytes();
   void* raw = nullptr;

@@ -80,6 +80,8 @@ struct LayerGeom {
   int64_t budget_bits, meta_bits, cells_T, achieved_bits;
   int32_t max_ncols;  // max N over the layer's units
   int32_t scope;      // budget scope id
+  int64_t n_out = 0;  // Top-K outliers of the layer (L29)
+  int64_t out_off = 0;  // byte offset of the layer's side table in the sketch (indices, then states)
 };
 
 }  // namespace usk
@@ -107,6 +109,8 @@ struct usk_plan {
   // stacked state quantisation (L25): q = 0 (raw states) or 4 / 8 bits
   int32_t q = 0, G = 128;
   int32_t variant = 0;        // usk_variant (comparison variants: generic kernels only)
+  int64_t topk = 0;           // Top-K outliers per layer (0 = none)
+  int64_t side_bytes = 0;     // bytes of all outlier side tables (after the cells)
   int64_t n_groups = 0;       // total_cells / G (quantised)
   int64_t scales_off = 0;     // byte offset of the fp32 group scales in the sketch (quantised)
   int cell_bytes() const { return dtype == USK_BF16 ? 2 : 4; }  // raw state bytes

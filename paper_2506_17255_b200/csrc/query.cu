@@ -70,6 +70,10 @@ struct QLayer {
   float* partial;      // GEMV: [rows][CP] chunk partials
   void* w_out;         // reconstruct output
   int64_t ld_out;
+  const int32_t* oidx; // Top-K side table: ascending flat indices o*in + j (global rows), or NULL
+  const void* ovals;   //   their states (plan dtype)
+  int64_t n_out;
+  int64_t out_rows;    // out_features of the layer (flat index stride is `in`)
 };
 
 struct QArgs {
@@ -96,6 +100,7 @@ struct QArgs {
   int32_t g_shift;                 // quantised plans: log2(group size)
   int32_t sbuf_off;                // quantised plans: byte offset of the staged scales from the raw buffer
   const float* scales;             // quantised plans: fp32 group scales (in the sketch buffer)
+  int32_t es;                      // bytes of a raw state (Top-K side-table values)
   int32_t cta_item[kMaxCtas + 1];  // GEMV: CTA c computes work items [cta_item[c], cta_item[c + 1])
   unsigned long long* timeline;  // tuning only (USK_TRACE): 4 globaltimer stamps per CTA
 };
@@ -494,6 +499,44 @@ __global__ void __maxnreg__(USK_GEMV_MAXREG) k_recon_fast(const __grid_constant_
   query_balanced<E, UPL, MT, HASH, false, QB>(A);
 }
 
+// Top-K (L29): [lo, hi) of the side-table entries of global row o
+__device__ __forceinline__ void outlier_range(const int32_t* idx, int64_t n, int64_t o, int64_t in, int64_t& lo,
+                                              int64_t& hi) {
+  auto lower = [&](int64_t key) {
+    int64_t a = 0, b = n;
+    while (a < b) {
+      const int64_t m = (a + b) >> 1;
+      if ((int64_t)(uint32_t)idx[m] < key) a = m + 1;
+      else b = m;
+    }
+    return a;
+  };
+  lo = lower(o * in);
+  hi = lower((o + 1) * in);
+}
+
+__device__ __forceinline__ float state_value(const void* vals, int32_t es, int64_t k) {
+  return es == 2 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(vals)[k] << 16)
+                 : __uint_as_float(reinterpret_cast<const uint32_t*>(vals)[k]);
+}
+
+// the sketch's w'(o, j) of a fast-path layout (ROW units, g = 1, raw states): unit j, position o
+__device__ __forceinline__ float sketch_value_row(const QArgs& A, const QLayer& Ly, int64_t o, int64_t j) {
+  const int64_t u = Ly.unit_base + j;
+  const uint32_t N = (uint32_t)A.ncols[u];
+  const int64_t off = A.offsets[u];
+  const uint32_t h = fmix32((uint32_t)o ^ A.hc.rho) ^ A.ukeys[u];
+  uint32_t best = 0;
+  for (int i = 0; i < A.M; ++i) {
+    const uint32_t idx = __umulhi(h * A.hc.a[i], N);
+    const int64_t c = off + (int64_t)i * N + idx;
+    const uint32_t b = A.es == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(A.sketch)[c] << 16)
+                                 : reinterpret_cast<const uint32_t*>(A.sketch)[c];
+    best = max(best, rotl1(b) ^ 1u);
+  }
+  return __uint_as_float(rotr1(best) ^ 0x80000000u);
+}
+
 constexpr int kRedThreads = 256;
 
 // y[r] = sum of row r's chunk partials in a fixed order: a group of red_lanes (power of two)
@@ -527,6 +570,19 @@ __global__ void __launch_bounds__(kRedThreads, 8) k_gemv_reduce(const __grid_con
   if (r < A.rows && j == 0) {
     const QLayer& Ly = A.layer[li];
     const int64_t rr = r - Ly.row_begin;
+    if (Ly.n_out) {  // Top-K: outliers contribute x_j * (w - w'_sketch) on top, in index order
+      const int64_t o = Ly.o_begin + rr;
+      int64_t lo, hi;
+      outlier_range(Ly.oidx, Ly.n_out, o, A.in, lo, hi);
+      float corr = 0.f;
+      for (int64_t k = lo; k < hi; ++k) {
+        const int64_t jj = (int64_t)(uint32_t)Ly.oidx[k] - o * A.in;
+        const float xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[jj] << 16)
+                                  : reinterpret_cast<const float*>(A.x)[jj];
+        corr = fmaf(xv, state_value(Ly.ovals, A.es, k) - sketch_value_row(A, Ly, o, jj), corr);
+      }
+      t += corr;
+    }
     if (A.y_bf16) {
       const uint32_t bb = __float_as_uint(t);
       reinterpret_cast<uint16_t*>(Ly.y)[rr] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
@@ -552,6 +608,9 @@ struct GenQ {
   int32_t q, g_shift;     // quantised plans (L25)
   const float* scales;
   int32_t variant;        // usk_variant (L27)
+  const int32_t* oidx;    // Top-K side table, or NULL
+  const void* ovals;
+  int64_t n_out;
 };
 
 // cell value as fp32 bits (raw bf16: bits << 16; quantised: fl32(code * scale))
@@ -607,6 +666,18 @@ __global__ void k_reconstruct_gen(GenQ Q, int64_t o0, int64_t o1, void* w_out, i
   }
 }
 
+// Top-K overlay of the reconstruction (L29): rows [o0, o1) of w_out (ld) get the
+// outliers' exact states
+__global__ void k_overlay(const int32_t* idx, const void* vals, int64_t n, int32_t es, int64_t in, int64_t o0,
+                          int64_t o1, void* w_out, int64_t ld) {
+  const int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const int64_t e = (int64_t)(uint32_t)idx[k], o = e / in, j = e - o * in;
+  if (o < o0 || o >= o1) return;
+  if (es == 2) reinterpret_cast<uint16_t*>(w_out)[(o - o0) * ld + j] = reinterpret_cast<const uint16_t*>(vals)[k];
+  else reinterpret_cast<uint32_t*>(w_out)[(o - o0) * ld + j] = reinterpret_cast<const uint32_t*>(vals)[k];
+}
+
 // one warp per output row, lanes over j, fixed-order warp reduction
 __global__ void k_gemv_gen(GenQ Q, int64_t o0, int64_t o1, const void* x, int32_t x_bf16, void* y, int32_t y_bf16) {
   const int64_t r = blockIdx.x * (int64_t)(blockDim.x / 32) + (threadIdx.x >> 5);
@@ -620,6 +691,19 @@ __global__ void k_gemv_gen(GenQ Q, int64_t o0, int64_t o1, const void* x, int32_
     s = fmaf(xv, w, s);
   }
   for (int m = 16; m >= 1; m >>= 1) s += __shfl_xor_sync(0xffffffffu, s, m);
+  if (lane == 0 && Q.n_out) {  // Top-K: outliers contribute x_j * (w - w'_sketch), in index order
+    const int64_t o = o0 + r;
+    int64_t lo, hi;
+    outlier_range(Q.oidx, Q.n_out, o, Q.in, lo, hi);
+    float corr = 0.f;
+    for (int64_t k = lo; k < hi; ++k) {
+      const int64_t jj = (int64_t)(uint32_t)Q.oidx[k] - o * Q.in;
+      const float xv = x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(x)[jj] << 16)
+                              : reinterpret_cast<const float*>(x)[jj];
+      corr = fmaf(xv, state_value(Q.ovals, Q.es, k) - __uint_as_float(gen_weight_bits_hi(Q, o, jj)), corr);
+    }
+    s += corr;
+  }
   if (lane == 0) {
     if (y_bf16) {
       const uint32_t b = __float_as_uint(s);
@@ -641,6 +725,12 @@ __global__ void k_stats_weights(GenQ Q, const void* W, unsigned long long* count
     const int64_t o = e / Q.in, j = e - o * Q.in;
     uint32_t pb = gen_weight_bits_hi(Q, o, j);  // w' (fp32 bits; bf16 in the high half)
     if (Q.es == 2 && Q.q) pb = pb + 0x7FFFu + ((pb >> 16) & 1u);
+    if (Q.n_out) {  // Top-K: outliers keep their value
+      int64_t lo, hi;
+      outlier_range(Q.oidx, Q.n_out, o, Q.in, lo, hi);
+      for (int64_t k = lo; k < hi; ++k)
+        if ((int64_t)(uint32_t)Q.oidx[k] == e) pb = __float_as_uint(state_value(Q.ovals, Q.es, k));
+    }
     uint32_t wb;
     if (Q.es == 2) {
       wb = (uint32_t)reinterpret_cast<const uint16_t*>(W)[e] << 16;
@@ -890,8 +980,20 @@ int partial_stride(int64_t in) { return (int)((((in + 31) / 32) + 3) / 4 * 4); }
 size_t layer_ws_ctrl_off(int64_t in, int64_t rows) { return ((size_t)rows * partial_stride(in) * 4 + 255) / 256 * 256; }
 size_t layer_ws_bytes(int64_t in, int64_t rows) { return layer_ws_ctrl_off(in, rows) + 256; }
 
+// Top-K side table of layer l (L29) into a launch layer
+void set_outliers(const usk_plan* pl, int32_t l, const void* sketch, QLayer& Ly) {
+  const LayerGeom& L = pl->layers[l];
+  Ly.n_out = L.n_out;
+  Ly.out_rows = L.out;
+  if (!L.n_out) return;
+  const char* tab = reinterpret_cast<const char*>(sketch) + L.out_off;
+  Ly.oidx = reinterpret_cast<const int32_t*>(tab);
+  Ly.ovals = tab + (L.n_out * 4 + 15) / 16 * 16;
+}
+
 QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& G) {
   QArgs A{};
+  A.es = pl->cell_bytes();
   A.M = pl->M;
   A.maxMN = G.maxMN;
   A.maxN = G.maxMN / pl->M;
@@ -1024,6 +1126,12 @@ GenQ make_genq(const usk_plan* pl, int32_t l, const void* sketch) {
   Q.g_shift = ilog2(pl->G);
   Q.scales = pl->q ? reinterpret_cast<const float*>(reinterpret_cast<const char*>(sketch) + pl->scales_off) : nullptr;
   Q.variant = pl->variant;
+  Q.n_out = L.n_out;
+  if (L.n_out) {
+    const char* tab = reinterpret_cast<const char*>(sketch) + L.out_off;
+    Q.oidx = reinterpret_cast<const int32_t*>(tab);
+    Q.ovals = tab + (L.n_out * 4 + 15) / 16 * 16;
+  }
   return Q;
 }
 
@@ -1067,6 +1175,7 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
         Ly.CP = partial_stride(in);
         Ly.y = y[k];
         Ly.partial = reinterpret_cast<float*>(w);
+        set_outliers(pl, layers[k], sketch, Ly);
         A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
         A.rows += rows[k];
       }
@@ -1125,12 +1234,21 @@ usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l,
     Ly.ld_out = ld;
     A.items = (int64_t)Ly.n_chunks * Ly.n_sub;
     A.rows = rows;
-    return launch_q(G.kern, A, partition_items(A, G), G.smem, false, st);
+    usk_status s = launch_q(G.kern, A, partition_items(A, G), G.smem, false, st);
+    if (s != USK_OK) return s;
+  } else {
+    GenQ Q = make_genq(pl, l, sketch);
+    const int64_t n = rows * L.in;
+    k_reconstruct_gen<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(Q, r0, r1, w_out, ld);
+    USK_LAUNCHED("k_reconstruct_gen");
   }
-  GenQ Q = make_genq(pl, l, sketch);
-  const int64_t n = rows * L.in;
-  k_reconstruct_gen<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, st>>>(Q, r0, r1, w_out, ld);
-  USK_LAUNCHED("k_reconstruct_gen");
+  if (L.n_out) {  // Top-K: the outliers keep their value (L29)
+    const char* tab = reinterpret_cast<const char*>(sketch) + L.out_off;
+    k_overlay<<<(unsigned)((L.n_out + 255) / 256), 256, 0, st>>>(reinterpret_cast<const int32_t*>(tab),
+                                                                 tab + (L.n_out * 4 + 15) / 16 * 16, L.n_out,
+                                                                 pl->cell_bytes(), L.in, r0, r1, w_out, ld);
+    USK_LAUNCHED("k_overlay");
+  }
   return USK_OK;
 }
 
