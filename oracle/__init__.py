@@ -50,12 +50,16 @@ def lib():
         L.uo_splitmix64.argtypes = [u64]
         L.uo_fmix32.restype = u32
         L.uo_fmix32.argtypes = [u32]
-        L.uo_row_multiplier.restype = u32
-        L.uo_row_multiplier.argtypes = [u64, i32]
+        L.uo_row_salt.restype = u32
+        L.uo_row_salt.argtypes = [u64, i32]
+        L.uo_row_key_salt.restype = u32
+        L.uo_row_key_salt.argtypes = [u64, i32]
+        L.uo_hash_word.restype = u32
+        L.uo_hash_word.argtypes = [u64, u32, u32, i32, u32]
         L.uo_unit_key.restype = u32
         L.uo_unit_key.argtypes = [u64, u32, u32]
         L.uo_position_mix.restype = u32
-        L.uo_position_mix.argtypes = [u64, u32]
+        L.uo_position_mix.argtypes = [u64, i32, u32]
         L.uo_hash_index.restype = u32
         L.uo_hash_index.argtypes = [i32, u64, u32, u32, i32, u32, u32]
         L.uo_update.restype = u32

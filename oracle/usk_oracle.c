@@ -81,9 +81,14 @@ uint32_t uo_fmix32(uint32_t h) {
   return h;
 }
 
-/* a_i: per sketch row multiplier (odd) */
-uint32_t uo_row_multiplier(uint64_t seed, int32_t row) {
-  return ((uint32_t)uo_splitmix64(seed + 0x100ull + (uint64_t)row)) | 1u;
+/* rho_i: per sketch row position salt */
+uint32_t uo_row_salt(uint64_t seed, int32_t row) {
+  return (uint32_t)uo_splitmix64(seed + 0x200ull + (uint64_t)row);
+}
+
+/* kappa_i: per sketch row key salt */
+uint32_t uo_row_key_salt(uint64_t seed, int32_t row) {
+  return (uint32_t)uo_splitmix64(seed + 0x300ull + (uint64_t)row);
 }
 
 /* K_u: per compression unit u = (layer l, unit t) */
@@ -92,20 +97,26 @@ uint32_t uo_unit_key(uint64_t seed, uint32_t layer, uint32_t t) {
   return (uint32_t)uo_splitmix64(seed ^ uo_splitmix64(lt));
 }
 
-/* R(p): per position, shared by all rows */
-uint32_t uo_position_mix(uint64_t seed, uint32_t p) {
-  uint32_t rho = (uint32_t)uo_splitmix64(seed);
-  return uo_fmix32(p ^ rho);
+/* R_i(p) = fmix32(p ^ rho_i): per position and row, shared by every unit */
+uint32_t uo_position_mix(uint64_t seed, int32_t row, uint32_t p) {
+  return uo_fmix32(p ^ uo_row_salt(seed, row));
 }
 
-/* idx_i(u, p) in [0, ncols) */
+/* h_i(u, p) = R_i(p) ^ fmix32(K_u ^ kappa_i) */
+uint32_t uo_hash_word(uint64_t seed, uint32_t layer, uint32_t t, int32_t row, uint32_t p) {
+  return uo_position_mix(seed, row, p) ^ uo_fmix32(uo_unit_key(seed, layer, t) ^ uo_row_key_salt(seed, row));
+}
+
+/* idx_i(u, p) in [0, ncols):
+ *   short units (ncols <= 2^16): floor((h mod 2^23) * ncols / 2^23)
+ *   long units:                  floor(h * ncols / 2^32) */
 uint32_t uo_hash_index(int32_t kind, uint64_t seed, uint32_t layer, uint32_t t, int32_t row,
                        uint32_t p, uint32_t ncols) {
   if (kind == UO_HASH_IDENTITY) return p % ncols; /* SPEC.md:54 test_hash: flat_index mod columns */
   {
-    uint32_t h = uo_position_mix(seed, p) ^ uo_unit_key(seed, layer, t);
-    uint32_t m = h * uo_row_multiplier(seed, row); /* wraps mod 2^32 */
-    return (uint32_t)(((uint64_t)m * (uint64_t)ncols) >> 32);
+    uint32_t h = uo_hash_word(seed, layer, t, row, p);
+    if (ncols <= 65536u) return (uint32_t)(((uint64_t)(h & 0x7FFFFFu) * (uint64_t)ncols) >> 23);
+    return (uint32_t)(((uint64_t)h * (uint64_t)ncols) >> 32);
   }
 }
 

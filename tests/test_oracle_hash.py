@@ -30,11 +30,13 @@ def fmix32(h):
 
 
 def usk_x(seed, layer, t, row, p, N):
-    rho = splitmix64(seed) & M32
+    rho = splitmix64((seed + 0x200 + row) & M64) & M32
+    kap = splitmix64((seed + 0x300 + row) & M64) & M32
     K = splitmix64(seed ^ splitmix64((layer << 32) | t)) & M32
-    a = (splitmix64((seed + 0x100 + row) & M64) & M32) | 1
-    h = fmix32(p ^ rho) ^ K
-    return (((h * a) & M32) * N) >> 32
+    h = fmix32(p ^ rho) ^ fmix32(K ^ kap)
+    if N <= 1 << 16:
+        return ((h % (1 << 23)) * N) // (1 << 23)
+    return (h * N) // (1 << 32)
 
 
 def test_contract_second_implementation(orc):
@@ -43,7 +45,7 @@ def test_contract_second_implementation(orc):
         seed = int(rng.integers(0, 2**63)) * 2 + int(rng.integers(0, 2))
         layer, t = int(rng.integers(0, 300)), int(rng.integers(0, 20000))
         row, p = int(rng.integers(0, 8)), int(rng.integers(0, 2**32))
-        N = int(rng.integers(1, 2**31))
+        N = int(rng.integers(1, 2**31)) if rng.integers(0, 2) else int(rng.integers(1, 2**16 + 2))
         assert orc.hash_index(0, seed, layer, t, row, p, N) == usk_x(seed, layer, t, row, p, N)
         assert orc.hash_index(1, seed, layer, t, row, p, N) == p % N
 
@@ -62,3 +64,20 @@ def test_rows_independent_of_M(orc):
     c2 = orc.sketch_unit(w.view(np.uint32), pos, 2, 37, seed=4)
     c5 = orc.sketch_unit(w.view(np.uint32), pos, 5, 37, seed=4)
     np.testing.assert_array_equal(c5[:2], c2)
+
+
+def test_short_unit_float_form(orc):
+    """The fast GPU kernels evaluate the short-unit range reduction as one fp32 fused multiply-add
+    rounded toward zero: RZ((1 + k/2^23) * N + (2^23 - N + off)) = 2^23 + off + floor(k N / 2^23)
+    whenever off + N < 2^23 (exact product, single rounding).  Check that identity against the
+    integer contract with numpy's float32 arithmetic emulated exactly in Python fractions."""
+    from fractions import Fraction
+    rng = np.random.default_rng(5)
+    for _ in range(2000):
+        k = int(rng.integers(0, 1 << 23))
+        N = int(rng.integers(1, 1 << 16))
+        off = int(rng.integers(0, (1 << 23) - N))
+        exact = Fraction((1 << 23) + k, 1 << 23) * N + ((1 << 23) - N + off)
+        rz = exact.numerator // exact.denominator  # values in [2^23, 2^24): fp32 ulp is 1
+        assert (1 << 23) <= rz < (1 << 24)
+        assert rz - (1 << 23) - off == (k * N) >> 23
