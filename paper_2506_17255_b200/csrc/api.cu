@@ -83,7 +83,7 @@ static bool layer_cells(int L, const double* imp, const std::vector<int64_t>& nu
 
 static void free_plan(usk_plan* p) {
   if (!p) return;
-  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R, p->d_err};
+  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_err};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete p;
@@ -180,8 +180,10 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   pl->q = P.state_bits;
   pl->G = P.state_bits ? qG : 128;
   const int state_bits = P.dtype == USK_BF16 ? 16 : 32;
-  pl->hc.rho = (uint32_t)splitmix64(P.seed);
-  for (int i = 0; i < 8; ++i) pl->hc.a[i] = ((uint32_t)splitmix64(P.seed + 0x100ull + (uint64_t)i)) | 1u;
+  for (int i = 0; i < 8; ++i) {  // per-row salts
+    pl->hc.rho[i] = (uint32_t)splitmix64(P.seed + 0x200ull + (uint64_t)i);
+    pl->hc.kap[i] = (uint32_t)splitmix64(P.seed + 0x300ull + (uint64_t)i);
+  }
   cudaGetDevice(&pl->device);
 
   pl->layers.resize(n_layers);
@@ -256,7 +258,6 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   e = e ? e : cudaMalloc(&pl->d_nrows, (size_t)U);
   e = e ? e : cudaMalloc(&pl->d_offsets, sizeof(int64_t) * (U + 1));
   e = e ? e : cudaMalloc(&pl->d_keys, sizeof(uint32_t) * U);
-  e = e ? e : cudaMalloc(&pl->d_R, sizeof(uint32_t) * (pl->max_out + 64));
   e = e ? e : cudaMalloc(&pl->d_err, sizeof(int));
   if (e != cudaSuccess) {
     free_plan(pl);

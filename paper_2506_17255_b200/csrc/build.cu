@@ -8,12 +8,14 @@
 // Fast path (ROW granularity, one input dimension per unit -- DESIGN.md L6):
 //   * one CTA per tile of TJ = 32*UPL consecutive units (input dims) of a layer, all outputs
 //     (no cross-CTA merge); a whole model is one launch so tiles balance across waves;
-//   * warp 0 streams [32 rows x TJ] weight tiles (plus the 32 position mixes R(o)) into a
-//     6-stage shared-memory ring with cp.async.bulk + mbarrier (TMA bulk engine);
+//   * warp 0 streams [32 rows x TJ] weight tiles into a 6-stage shared-memory ring with
+//     cp.async.bulk + mbarrier (TMA bulk engine);
 //   * 16 consumer warps (2 rows of each stage): lane L owns units UPL*L .. UPL*L+UPL-1; its
 //     keys live in shared memory at word (v * 32 * maxMN + k * 32 + L), i.e. always in bank L,
 //     so the M random bucket updates of a warp are bank-conflict free; each update is an
-//     unconditional red.shared.min (see key_min);
+//     unconditional red.shared.min (see key_min).  Per weight row o the warp's lane i computes the
+//     position mix R_i(o) and SHFL broadcasts it; the short-unit index and the
+//     key's shared address come from one FFMA.RZ + one IMAD (short_fma_bits);
 //   * the CTA then writes its units' cells (states, +Inf for empty) to the sketch.
 // Generic path (LAYER granularity, dims_per_unit > 1, odd shapes, oversize units): keys are
 // kept in place in the sketch buffer (32-bit atomicMin for fp32 cells, 16-bit CAS for bf16),
@@ -51,7 +53,6 @@ struct BuildArgs {
   const int32_t* ncols;
   const int64_t* offsets;
   const uint32_t* ukeys;
-  const uint32_t* R;
   void* sketch;
   int* err;
   uint32_t kap_max;  // largest accepted weight key: 0xFEFFFFFF (finite), 0xFF000000 (+Inf = excluded outlier)
@@ -61,14 +62,14 @@ template <int ES>
 constexpr int stages_for() { return ES == 2 ? 6 : 4; }
 
 template <typename E, int UPL>
-constexpr int stage_bytes() { return kRO * 4 + kRO * 32 * UPL * (int)sizeof(E); }
+constexpr int stage_bytes() { return kRO * 32 * UPL * (int)sizeof(E); }
 
 // kappa-min update of one shared key: an unconditional red.shared.min (no return value).  A
 // plain-load pre-check would skip most atomics, but ptxas turns the predicated atomic into a branch
 // per gather (serialising the gathers); measured on B200 the unconditional form is ~10% faster
 // for the full Llama-3.2-1B build.
-__device__ __forceinline__ void key_min(uint32_t smem_keys, uint32_t off, uint32_t kap) {
-  asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(smem_keys + off), "r"(kap) : "memory");
+__device__ __forceinline__ void key_min(uint32_t saddr, uint32_t kap) {
+  asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(saddr), "r"(kap) : "memory");
 }
 
 template <typename E, int UPL, int MT, int HASH>
@@ -113,7 +114,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   __syncthreads();
 
   if (warp == 0) {
-    // ---------------- producer: bulk-copy weight row segments + R(o) into the ring
+    // ---------------- producer: bulk-copy weight row segments into the ring
     const E* W = reinterpret_cast<const E*>(T.W);
     const uint32_t segb = (uint32_t)nu * ES;
     for (int64_t it = 0; it < n_it; ++it) {
@@ -121,21 +122,22 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       if (it >= S) mbar_wait(&empty[s], (uint32_t)((it / S) - 1) & 1u);
       const int64_t o0 = it * kRO;
       const int rows = (int)min((int64_t)kRO, T.out - o0);
-      const uint32_t rbytes = (uint32_t)((rows + 3) & ~3) * 4u;
       uint8_t* st = stages + s * STAGEB;
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&full[s], rbytes + (uint32_t)rows * segb);
-        bulk_g2s(st, A.R + o0, rbytes, &full[s]);
-      }
+      if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)rows * segb);
       __syncwarp();
       for (int r = lane; r < rows; r += 32)
-        bulk_g2s(st + kRO * 4 + r * ROWB, W + (o0 + r) * T.in + j0, segb, &full[s]);
+        bulk_g2s(st + r * ROWB, W + (o0 + r) * T.in + j0, segb, &full[s]);
     }
   } else {
     // ---------------- consumers: warp cw takes rows cw and cw + 16 of every stage
     const int cw = warp - 1;
+    constexpr bool FAST = MT > 0 && HASH == USK_HASH_X;  // short-unit FFMA.RZ form
+    constexpr int KR = FAST ? MT : 1;
     uint32_t K[UPL], N[UPL], vmask[UPL];
-    uint32_t rb[UPL][MR];  // byte offsets of (unit v, sketch row i) in `keys` for this lane
+    uint32_t rb[UPL][FAST ? 1 : MR];  // generic: byte offsets of (unit v, sketch row i) for this lane
+    uint32_t fk[UPL][KR], cb[UPL][KR];  // fast: FFMA key and addend of (unit v, sketch row i)
+    float Nf[UPL];
+    const uint32_t kbase = smem_keys + 4u * (uint32_t)lane - 0x80000000u;  // (0x4B000000 << 7) wraps to 2^31
 #pragma unroll
     for (int v = 0; v < UPL; ++v) {
       const int ul = UPL * lane + v;
@@ -145,11 +147,20 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       // a missing unit of a ragged tile updates a private dummy word (never written back) with a
       // zero candidate, so the loop below needs no branch
       N[v] = valid ? (uint32_t)A.ncols[u] : 1u;
+      Nf[v] = (float)N[v];
       vmask[v] = valid ? ~0u : 0u;
+      if constexpr (FAST) {
 #pragma unroll
-      for (int i = 0; i < MR; ++i)
-        rb[v][i] = valid ? 4u * (uint32_t)(v * stride_v + i * (int)N[v] * 32 + lane)
-                         : 4u * (uint32_t)(TJ * A.maxMN + lane);
+        for (int i = 0; i < MT; ++i) {
+          fk[v][i] = short_fkey(row_key(K[v], A.hc.kap[i]));
+          cb[v][i] = short_cbits(N[v], valid ? (uint32_t)(v * A.maxMN + i * (int)N[v]) : (uint32_t)(UPL * A.maxMN));
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < MR; ++i)
+          rb[v][i] = valid ? 4u * (uint32_t)(v * stride_v + i * (int)N[v] * 32 + lane)
+                           : 4u * (uint32_t)(TJ * A.maxMN + lane);
+      }
     }
     uint32_t kmax = 0;
     for (int64_t it = 0; it < n_it; ++it) {
@@ -162,8 +173,9 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       for (int rr = 0; rr < kRO / kConsumers; ++rr) {
         const int r = cw + rr * kConsumers;
         if (r >= rows) break;
-        const uint32_t Rv = reinterpret_cast<const uint32_t*>(st)[r];
-        const uint8_t* row = st + kRO * 4 + r * ROWB;
+        const uint32_t o = (uint32_t)(o0 + r);
+        const uint32_t Rl = fmix32(o ^ A.hc.rho[lane & 7]);  // lane i: R_i(o)
+        const uint8_t* row = st + r * ROWB;
         uint32_t bits[UPL];
         if constexpr (ES == 2 && UPL == 4) {
           const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
@@ -190,18 +202,31 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
         } else {
           bits[0] = reinterpret_cast<const uint32_t*>(row)[lane];
         }
+        if constexpr (FAST) {
+          uint32_t R23[MT];
 #pragma unroll
-        for (int v = 0; v < UPL; ++v) {
-          const uint32_t kap = rotl1(bits[v] & vmask[v]);
-          kmax = max(kmax, kap);
-          const uint32_t h = Rv ^ K[v];
+          for (int i = 0; i < MT; ++i) R23[i] = __shfl_sync(0xffffffffu, Rl, i) & 0x7FFFFFu;
 #pragma unroll
-          for (int i = 0; i < MR; ++i) {
-            if (MT == 0 && i >= M) break;
-            uint32_t idx;
-            if constexpr (HASH == USK_HASH_X) idx = __umulhi(h * A.hc.a[i], N[v]);
-            else idx = (uint32_t)((o0 + r) % N[v]);
-            key_min(smem_keys, rb[v][i] + (idx << 7), kap);
+          for (int v = 0; v < UPL; ++v) {
+            const uint32_t kap = rotl1(bits[v] & vmask[v]);
+            kmax = max(kmax, kap);
+#pragma unroll
+            for (int i = 0; i < MT; ++i) key_min(short_fma_bits(R23[i], fk[v][i], Nf[v], cb[v][i]) * 128u + kbase, kap);
+          }
+        } else {
+#pragma unroll
+          for (int v = 0; v < UPL; ++v) {
+            const uint32_t kap = rotl1(bits[v] & vmask[v]);
+            kmax = max(kmax, kap);
+#pragma unroll
+            for (int i = 0; i < MR; ++i) {
+              if (MT == 0 && i >= M) break;
+              const uint32_t Ri = __shfl_sync(0xffffffffu, Rl, i);
+              uint32_t idx;
+              if constexpr (HASH == USK_HASH_X) idx = hash_reduce(Ri ^ row_key(K[v], A.hc.kap[i]), N[v]);
+              else idx = o % N[v];
+              key_min(smem_keys + rb[v][i] + (idx << 7), kap);
+            }
           }
         }
       }
@@ -276,9 +301,9 @@ __global__ void k_gen_scatter(GenLayer G, const void* W, int32_t layer_M, HashCo
                              : reinterpret_cast<const uint32_t*>(W)[e];
     const uint32_t kap = rotl1(bhi);
     if (kap > kap_max) atomicOr(err, 1);
-    const uint32_t h = fmix32((uint32_t)p ^ hc.rho) ^ ukeys[u];
+    const uint32_t Ku = ukeys[u];
     for (int i = 0; i < layer_M; ++i) {
-      const uint32_t idx = (HASH == USK_HASH_X) ? __umulhi(h * hc.a[i], N) : (uint32_t)(p % N);
+      const uint32_t idx = (HASH == USK_HASH_X) ? hash_index_x(hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
       const int64_t c = off + (int64_t)i * N + idx;
       if (ES == 2) {
         cas_min16(reinterpret_cast<uint16_t*>(sketch) + c, (kap >> 16) | (kap & 1u));  // kappa16 = (mag << 1) | s
@@ -394,9 +419,9 @@ __global__ void k_amx_scatter(GenLayer G, const void* W, int32_t layer_M, HashCo
     const uint32_t kap = rotl1(bhi);
     if (kap >= 0xFF000000u) atomicOr(err, 1);
     const uint32_t rho = kap ^ 1u;
-    const uint32_t h = fmix32((uint32_t)p ^ hc.rho) ^ ukeys[u];
+    const uint32_t Ku = ukeys[u];
     for (int i = 0; i < layer_M; ++i) {
-      const uint32_t idx = (HASH == USK_HASH_X) ? __umulhi(h * hc.a[i], N) : (uint32_t)(p % N);
+      const uint32_t idx = (HASH == USK_HASH_X) ? hash_index_x(hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
       const int64_t c = off + (int64_t)i * N + idx;
       if (ES == 2) {
         cas_max16(reinterpret_cast<uint16_t*>(sketch) + c, (rho >> 16) | (rho & 1u));
@@ -484,7 +509,7 @@ int fast_upl(const usk_plan* pl, int32_t l) {
   if ((L.in * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
   const int S = es == 2 ? 6 : 4;
-  auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 4 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
+  auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
   for (int upl : {4, 2, 1})
     if (smem(upl) <= (int64_t)kSmemLimit) return upl;
   return 0;
@@ -525,7 +550,6 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
     A.ncols = pl->d_ncols;
     A.offsets = pl->d_offsets;
     A.ukeys = pl->d_keys;
-    A.R = pl->d_R;
     A.sketch = sketch;
     A.err = pl->d_err;
     A.kap_max = kap_max;

@@ -5,6 +5,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstring>
 
 #include <string>
 #include <vector>
@@ -33,10 +34,13 @@ void count_launch(int n = 1);
   } while (0)
 
 // ----------------------------------------------------------------------------- hash contract
-// USK-X (Eq. 3).  Host-side constants:
-//   rho = (u32) splitmix64(seed); a_i = (u32) splitmix64(seed + 0x100 + i) | 1;
-//   K_u = (u32) splitmix64(seed ^ splitmix64((l << 32) | t)).
-// Device side per weight:  idx_i = mulhi32((fmix32(p ^ rho) ^ K_u) * a_i, N_u).
+// USK-X (DESIGN.md 2.2 "Hash contract"; Eq. 3).  Host-side constants per
+// sketch row i: rho_i = (u32) splitmix64(seed + 0x200 + i), kappa_i = (u32) splitmix64(seed + 0x300 + i);
+// per unit K_u = (u32) splitmix64(seed ^ splitmix64((l << 32) | t)).  Per weight:
+//   h_i = fmix32(p ^ rho_i) ^ fmix32(K_u ^ kappa_i)
+//   idx_i = ((h_i mod 2^23) * N_u) >> 23 (N_u <= 2^16), else (h_i * N_u) >> 32.
+// The fast kernels evaluate the short-unit reduction as one fp32 FMA rounded toward zero (see
+// short_fma_bits); everything else calls hash_word / hash_reduce.
 __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
   uint64_t z = x;
@@ -55,9 +59,47 @@ __host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
 }
 
 struct HashConsts {
-  uint32_t rho;
-  uint32_t a[8];
+  uint32_t rho[8];  // position salts rho_i
+  uint32_t kap[8];  // unit-key salts kappa_i
 };
+
+constexpr uint32_t kShortUnitMax = 65536;  // N_u <= 2^16: 23-bit short-unit reduction
+
+__host__ __device__ __forceinline__ uint32_t row_key(uint32_t Ku, uint32_t kap_i) { return fmix32(Ku ^ kap_i); }
+
+__host__ __device__ __forceinline__ uint32_t hash_word(const HashConsts& hc, uint32_t p, uint32_t Ku, int i) {
+  return fmix32(p ^ hc.rho[i]) ^ row_key(Ku, hc.kap[i]);
+}
+
+__host__ __device__ __forceinline__ uint32_t hash_reduce(uint32_t h, uint32_t N) {
+  return N <= kShortUnitMax ? (uint32_t)(((uint64_t)(h & 0x7FFFFFu) * N) >> 23)
+                            : (uint32_t)(((uint64_t)h * N) >> 32);
+}
+
+__host__ __device__ __forceinline__ uint32_t hash_index_x(const HashConsts& hc, uint32_t p, uint32_t Ku, int i,
+                                                          uint32_t N) {
+  return hash_reduce(hash_word(hc, p, Ku, i), N);
+}
+
+// Short-unit reduction in one FFMA.RZ: with f = as_float(0x3F800000 | k) =
+// 1 + k / 2^23 and C = 2^23 - N + off (off + N < 2^23), the exact f * N + C lies in [2^23, 2^24)
+// where the fp32 ulp is 1, so rounding toward zero gives 2^23 + off + floor(k N / 2^23): the bit
+// pattern 0x4B000000 + off + idx.  fkey = 0x3F800000 | (row key mod 2^23); R23 = R_i mod 2^23.
+__device__ __forceinline__ uint32_t short_fma_bits(uint32_t R23, uint32_t fkey, float Nf, uint32_t Cbits) {
+  return __float_as_uint(__fmaf_rz(__uint_as_float(R23 ^ fkey), Nf, __uint_as_float(Cbits)));
+}
+__host__ __device__ __forceinline__ uint32_t short_fkey(uint32_t rowkey) { return 0x3F800000u | (rowkey & 0x7FFFFFu); }
+__host__ __device__ __forceinline__ uint32_t short_cbits(uint32_t N, uint32_t off) {
+  // 2^23 - N + off as fp32 bits (an integer below 2^24: exact)
+  const float c = (float)(int32_t)(8388608u - N + off);
+#ifdef __CUDA_ARCH__
+  return __float_as_uint(c);
+#else
+  uint32_t b;
+  std::memcpy(&b, &c, 4);
+  return b;
+#endif
+}
 
 // Key encodings on 32-bit words (weights held with their bits in the HIGH position: bf16
 // bits << 16, fp32 bits as-is).  With mag = magnitude bits and s = sign bit:
@@ -103,7 +145,6 @@ struct usk_plan {
   uint8_t* d_nrows = nullptr;
   int64_t* d_offsets = nullptr;
   uint32_t* d_keys = nullptr;  // K_u per unit
-  uint32_t* d_R = nullptr;     // R(o) = fmix32(o ^ rho), o < max_out (g = 1 positions)
   int* d_err = nullptr;        // sticky device error flag
   int device = 0;
   // stacked state quantisation (L25): q = 0 (raw states) or 4 / 8 bits

@@ -40,9 +40,9 @@ __global__ void k_aggregate(AggArgs A) {
     if (A.err && !isfinite(gv)) atomicOr(A.err, 1);
     const long long q = __double2ll_rn((double)gv * kFix);
     if (q == 0) continue;
-    const uint32_t h = fmix32((uint32_t)p ^ A.hc.rho) ^ A.ukeys[u];
+    const uint32_t Ku = A.ukeys[u];
     for (int i = 0; i < A.M; ++i) {
-      const uint32_t idx = A.hash == USK_HASH_X ? __umulhi(h * A.hc.a[i], N) : (uint32_t)(p % N);
+      const uint32_t idx = A.hash == USK_HASH_X ? hash_index_x(A.hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
       atomicAdd(&A.acc[base + (int64_t)i * N + idx], (unsigned long long)q);  // two's complement sum
     }
   }

@@ -266,11 +266,6 @@ __global__ void k_scan_last(const int64_t* in, int64_t U, int64_t* out) {
   out[U] = out[U - 1] + in[U - 1];
 }
 
-__global__ void k_R_table(uint32_t rho, int64_t n, uint32_t* R) {
-  int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (o < n) R[o] = fmix32((uint32_t)o ^ rho);
-}
-
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 template <class T>
@@ -384,8 +379,6 @@ usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStr
   USK_LAUNCHED("k_scan_apply");
   k_scan_last<<<1, 1, 0, st>>>(d_sizes, U, pl->d_offsets);
   USK_LAUNCHED("k_scan_last");
-  k_R_table<<<blocks_for(pl->max_out, T256), T256, 0, st>>>(pl->hc.rho, pl->max_out, pl->d_R);
-  USK_LAUNCHED("k_R_table");
 
   int h_err = 0;
   pl->h_ncols.resize(U);

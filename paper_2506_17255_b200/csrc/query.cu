@@ -15,7 +15,10 @@
 //     (VIMNMX3 for M=3) and rotr(rho, 1) is the IEEE pattern of -w', so the GEMV multiplies by -x
 //     (exact).  The next chunk of a CTA's range is prefetched under the current one's math.
 //   * Missing units of a ragged chunk point at the zero column (rho of +0) with x = 0, so the inner
-//     loop has no branches.  R(o) for a subtile is one register per lane, broadcast with SHFL.
+//     loop has no branches.  Hash: per subtile, lanes r < 16 write the position
+//     mixes R_i(o0 + r) mod 2^23 of their row to a per-warp shared table (one 16-B broadcast load
+//     per row); per weight and sketch row one LOP3 (R_i ^ key), one FFMA.RZ (short-unit index +
+//     slot offset, exact) and one IMAD (x128 + lane base) give the bank-private shared address.
 //   * K4 (k_gemv_fast + k_gemv_reduce): per subtile a transpose butterfly leaves one row sum per
 //     lane; chunk partials go to a row-major [rows][CP] workspace and a second, PDL-chained kernel
 //     sums them in fixed order (deterministic, no float atomics).  The sketch is staged before
@@ -44,7 +47,9 @@ constexpr int kMaxCtas = 256;  // GEMV compute grid (one CTA per SM)
 #endif
 constexpr int kSubRows = USK_SUB_ROWS;  // rows per warp work item (subtile): 8 or 16
 static_assert(kSubRows == 8 || kSubRows == 16, "subtile rows");
-constexpr int kCellsWordOffset = 32 + 160;  // zero cells + chunk unit offsets (<= 129)
+constexpr int kRTabWordOffset = 32 + 160;  // zero cells + chunk unit offsets (<= 129)
+constexpr int kRTabWords = (kQThreads / 32) * kSubRows * 4;  // per warp: kSubRows x {R_0, R_1, R_2, 0}
+constexpr int kCellsWordOffset = kRTabWordOffset + kRTabWords;
 
 extern __shared__ __align__(16) uint32_t qsm[];  // dynamic shared memory of the query kernels
 
@@ -111,27 +116,38 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
-template <int UPL, int MT>
+template <int MT, int HASH>
+constexpr bool fast_hash() { return MT > 0 && HASH == USK_HASH_X; }
+
+template <int UPL, int MT, int HASH>
 struct LaneState {
-  uint32_t K[UPL], N[UPL];
-  uint32_t b0[UPL];  // shared-window byte address of (unit v, sketch row 0, column 0) for this
-                     // lane; cell (i, k) is at b0 + 128 * (i * maxN + k)
+  static constexpr int KR = fast_hash<MT, HASH>() ? MT : 1;
+  // generic (M > 3, identity hash): unit key, N and the shared-window byte address of (unit v,
+  // sketch row 0, column 0) for this lane; cell (i, k) is at b0 + 128 * (i * maxN + k)
+  uint32_t K[UPL], N[UPL], b0[UPL];
+  // fast: FFMA key and addend of (unit v, sketch row i); address = bits * 128 + B
+  uint32_t fk[UPL][KR], cb[UPL][KR];
+  float Nf[UPL];
+  uint32_t B;
 };
 
-// shared memory: [zero cells: 32 words][mbarrier: 2 words][copy shift: 1 word]...[cells @ word
-// kCellsWordOffset: UPL*32*maxMN words][raw bulk-copy buffer: piece_units*maxMN cells + 32 B]
+// shared memory: [zero cells: 32 words][mbarrier: 2 words][copy shift: 1 word]...[per-warp R tables
+// @ word kRTabWordOffset][cells @ word kCellsWordOffset: UPL*32*maxMN words][raw bulk-copy buffer:
+// piece_units*maxMN cells + 32 B]
 __device__ __forceinline__ uint64_t* q_bar() { return reinterpret_cast<uint64_t*>(qsm + 32); }
 
-// Lane state of a chunk [ubase, ubase + nu): K_u, N_u and the shared byte address of each of
-// the lane's units (missing units of a ragged chunk point at the zero cells: idx is always 0).
-template <int UPL, int MT>
-__device__ __forceinline__ void lane_setup(const QArgs& A, int64_t ubase, int nu, LaneState<UPL, MT>& S) {
+// Lane state of a chunk [ubase, ubase + nu): keys, N_u and the shared addresses of each of the
+// lane's units (missing units of a ragged chunk point at the zero cells: idx is always 0).
+template <int UPL, int MT, int HASH>
+__device__ __forceinline__ void lane_setup(const QArgs& A, int64_t ubase, int nu, LaneState<UPL, MT, HASH>& S) {
   const int lane = threadIdx.x & 31;
   const uint32_t cbase = smem_u32(qsm + kCellsWordOffset);
+  S.B = cbase + 4u * (uint32_t)lane - 0x80000000u;  // (0x4B000000 << 7) wraps to 2^31
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
     const int ul = UPL * lane + v;
-    if (ul < nu) {
+    const bool valid = ul < nu;
+    if (valid) {
       S.K[v] = A.ukeys[ubase + ul];
       S.N[v] = (uint32_t)A.ncols[ubase + ul];
       S.b0[v] = cbase + 4u * (uint32_t)(v * 32 * A.maxMN + lane);
@@ -139,6 +155,14 @@ __device__ __forceinline__ void lane_setup(const QArgs& A, int64_t ubase, int nu
       S.K[v] = 0;
       S.N[v] = 1;
       S.b0[v] = cbase + 4u * (uint32_t)((A.maxN - 1) * 32 + lane);
+    }
+    S.Nf[v] = (float)S.N[v];
+    if constexpr (fast_hash<MT, HASH>()) {
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        S.fk[v][i] = short_fkey(row_key(S.K[v], A.hc.kap[i]));
+        S.cb[v][i] = short_cbits(S.N[v], valid ? (uint32_t)(v * A.maxMN + i * A.maxN) : (uint32_t)(i * A.maxN + A.maxN - 1));
+      }
     }
   }
 }
@@ -255,16 +279,15 @@ __device__ __forceinline__ void q_prologue(const QArgs& A) {
   }
 }
 
-// rho code of w'(o, unit v) for this lane
+// rho code of w'(o, unit v) for this lane; R = the row's position mixes R_i(o) mod 2^23 (fast hash)
 template <int UPL, int MT, int HASH>
-__device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<UPL, MT>& S, int v, uint32_t Rv,
+__device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<UPL, MT, HASH>& S, int v, const uint4& R,
                                                int64_t o) {
-  const uint32_t h = Rv ^ S.K[v];
-  if constexpr (MT > 0 && HASH == USK_HASH_X) {
-    // idx_i + i * maxN in one IMAD.HI (the addend), then one LEA to the shared address
+  if constexpr (fast_hash<MT, HASH>()) {
+    const uint32_t Ri[3] = {R.x, R.y, R.z};
     uint32_t m[MT];
 #pragma unroll
-    for (int i = 0; i < MT; ++i) m[i] = lds_at(S.b0[v] + ((__umulhi(h * A.hc.a[i], S.N[v]) + i * A.maxN) << 7));
+    for (int i = 0; i < MT; ++i) m[i] = lds_at(short_fma_bits(Ri[i], S.fk[v][i], S.Nf[v], S.cb[v][i]) * 128u + S.B);
     uint32_t best = m[0];
 #pragma unroll
     for (int i = 1; i < MT; ++i) best = max(best, m[i]);
@@ -272,11 +295,36 @@ __device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<U
   } else {
     uint32_t best = 0;
     for (int i = 0; i < A.M; ++i) {
-      const uint32_t idx = (HASH == USK_HASH_X) ? __umulhi(h * A.hc.a[i], S.N[v]) : (uint32_t)(o % S.N[v]);
+      const uint32_t idx = (HASH == USK_HASH_X) ? hash_index_x(A.hc, (uint32_t)o, S.K[v], i, S.N[v])
+                                                : (uint32_t)(o % S.N[v]);
       best = max(best, lds_at(S.b0[v] + ((idx + i * A.maxN) << 7)));
     }
     return best;
   }
+}
+
+// per-warp table of the subtile rows' position mixes: lane r < kSubRows writes row r's
+// {R_0, R_1, R_2} mod 2^23 (rows past the layer repeat its last row)
+template <int MT, int HASH>
+__device__ __forceinline__ void fill_rtab(const QArgs& A, uint32_t rtab, int64_t o_first, int64_t o_last, int lane) {
+  if constexpr (fast_hash<MT, HASH>()) {
+    __syncwarp();  // the previous subtile's reads are done
+    if (lane < kSubRows) {
+      const uint32_t o = (uint32_t)min(o_first + lane, o_last);
+      const uint32_t r0 = fmix32(o ^ A.hc.rho[0]) & 0x7FFFFFu;
+      const uint32_t r1 = MT > 1 ? fmix32(o ^ A.hc.rho[1]) & 0x7FFFFFu : 0u;
+      const uint32_t r2 = MT > 2 ? fmix32(o ^ A.hc.rho[2]) & 0x7FFFFFu : 0u;
+      asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rtab + 16u * lane), "r"(r0), "r"(r1), "r"(r2),
+                   "r"(0u) : "memory");
+    }
+    __syncwarp();
+  }
+}
+
+__device__ __forceinline__ uint4 lds_rtab(uint32_t a) {
+  uint4 q;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(a));
+  return q;
 }
 
 // Row r of the warp's kSubRows partial rows ends on the lanes congruent to r mod kSubRows
@@ -397,8 +445,8 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
     bool stamped = false;
     while (true) {
       const QLayer& Ly = A.layer[cur.li];
-      LaneState<UPL, MT> S;
-      lane_setup<UPL, MT>(A, cur.ubase, cur.nu, S);  // overlaps the copy
+      LaneState<UPL, MT, HASH> S;
+      lane_setup<UPL, MT, HASH>(A, cur.ubase, cur.nu, S);  // overlaps the copy
       stage_units<E, UPL, QB>(A, cur.ubase, cur.nu, phase, true);  // sketch only: before the wait
       if (!waited) {
         pdl_wait();     // x may be written by the previous kernel on the stream
@@ -424,7 +472,6 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
         nxt_seg = seg_at(cur.end);
         if (threadIdx.x == 0) stage_issue<E, UPL, QB>(A, nxt_seg.ubase, 0, min(A.piece_units, nxt_seg.nu));
       }
-      const int rl = lane & (kSubRows - 1);  // lanes congruent to r mod kSubRows hold R(o0 + r)
       auto next_sub = [&]() -> int {
         int g = 0;
         if (lane == 0) g = atomicAdd(&s_next, 1);
@@ -432,10 +479,9 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
       };
       const int sub_end = cur.sub_end;
       const int chunk = cur.chunk;
+      const uint32_t rtab = smem_u32(qsm + kRTabWordOffset) + (uint32_t)(threadIdx.x >> 5) * (kSubRows * 16u);
       int sub = next_sub();
-      uint32_t Rl = 0;
-      // R(o) = fmix32(o ^ rho): lane r computes its own row's mix; SHFL broadcasts it row by row
-      if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
+      if (sub < sub_end) fill_rtab<MT, HASH>(A, rtab, Ly.o_begin + (int64_t)sub * kSubRows, Ly.o_begin + Ly.rows - 1, lane);
       while (sub < sub_end) {
         const int nxt = next_sub();  // issued now, consumed after this subtile's math
         const int64_t r0 = (int64_t)sub * kSubRows;
@@ -444,7 +490,8 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
           float acc[kSubRows];
 #pragma unroll
           for (int r = 0; r < kSubRows; ++r) {
-            const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
+            uint4 Rv = make_uint4(0, 0, 0, 0);
+            if constexpr (fast_hash<MT, HASH>()) Rv = lds_rtab(rtab + 16u * r);
             float a = 0.f;
 #pragma unroll
             for (int v = 0; v < UPL; ++v)
@@ -459,8 +506,9 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
           E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + cur.j0 + UPL * lane;
 #pragma unroll 4
           for (int r = 0; r < kSubRows; ++r, dst += Ly.ld_out) {
-            const uint32_t Rv = __shfl_sync(0xffffffffu, Rl, r);
             if (r >= nrow) continue;
+            uint4 Rv = make_uint4(0, 0, 0, 0);
+            if constexpr (fast_hash<MT, HASH>()) Rv = lds_rtab(rtab + 16u * r);
             uint32_t wb[UPL];
 #pragma unroll
             for (int v = 0; v < UPL; ++v)
@@ -469,7 +517,7 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
           }
         }
         sub = nxt;
-        if (sub < sub_end) Rl = fmix32((uint32_t)(Ly.o_begin + min((int64_t)sub * kSubRows + rl, Ly.rows - 1)) ^ A.hc.rho);
+        if (sub < sub_end) fill_rtab<MT, HASH>(A, rtab, Ly.o_begin + (int64_t)sub * kSubRows, Ly.o_begin + Ly.rows - 1, lane);
       }
       __syncthreads();  // cells and s_next are reused by the next segment
       if (!more) break;
@@ -525,10 +573,10 @@ __device__ __forceinline__ float sketch_value_row(const QArgs& A, const QLayer& 
   const int64_t u = Ly.unit_base + j;
   const uint32_t N = (uint32_t)A.ncols[u];
   const int64_t off = A.offsets[u];
-  const uint32_t h = fmix32((uint32_t)o ^ A.hc.rho) ^ A.ukeys[u];
+  const uint32_t Ku = A.ukeys[u];
   uint32_t best = 0;
   for (int i = 0; i < A.M; ++i) {
-    const uint32_t idx = __umulhi(h * A.hc.a[i], N);
+    const uint32_t idx = hash_index_x(A.hc, (uint32_t)o, Ku, i, N);
     const int64_t c = off + (int64_t)i * N + idx;
     const uint32_t b = A.es == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(A.sketch)[c] << 16)
                                  : reinterpret_cast<const uint32_t*>(A.sketch)[c];
@@ -636,19 +684,19 @@ __device__ __forceinline__ uint32_t gen_weight_bits_hi(const GenQ& Q, int64_t o,
   const int64_t u = Q.unit_base + t;
   const uint32_t N = (uint32_t)Q.ncols[u];
   const int64_t off = Q.offsets[u];
-  const uint32_t h = fmix32((uint32_t)p ^ Q.hc.rho) ^ Q.ukeys[u];
+  const uint32_t Ku = Q.ukeys[u];
   if (Q.variant != USK_ABSMAXMIN) {
     // AbsMinMax / CountMin: the bonded cell of MINIMUM |.|, ties -> non-negative = min kappa
     uint32_t best = 0xFFFFFFFFu;
     for (int i = 0; i < Q.M; ++i) {
-      const uint32_t idx = Q.hash == USK_HASH_X ? __umulhi(h * Q.hc.a[i], N) : (uint32_t)(p % N);
+      const uint32_t idx = Q.hash == USK_HASH_X ? hash_index_x(Q.hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
       best = min(best, rotl1(gen_cell_bits(Q, off + (int64_t)i * N + idx)));
     }
     return rotr1(best);
   }
   uint32_t best = 0;
   for (int i = 0; i < Q.M; ++i) {
-    const uint32_t idx = Q.hash == USK_HASH_X ? __umulhi(h * Q.hc.a[i], N) : (uint32_t)(p % N);
+    const uint32_t idx = Q.hash == USK_HASH_X ? hash_index_x(Q.hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
     const int64_t c = off + (int64_t)i * N + idx;
     best = max(best, rotl1(gen_cell_bits(Q, c)) ^ 1u);
   }
@@ -756,10 +804,10 @@ __global__ void k_stats_weights(GenQ Q, const void* W, unsigned long long* count
     else { t = 0; p = j * Q.out + o; }
     const int64_t u = Q.unit_base + t;
     const uint32_t N = (uint32_t)Q.ncols[u];
-    const uint32_t h = fmix32((uint32_t)p ^ Q.hc.rho) ^ Q.ukeys[u];
+    const uint32_t Ku = Q.ukeys[u];
     const int64_t base = Q.offsets[u] - Q.offsets[Q.unit_base];
     for (int i = 0; i < Q.M; ++i) {
-      const uint32_t idx = Q.hash == USK_HASH_X ? __umulhi(h * Q.hc.a[i], N) : (uint32_t)(p % N);
+      const uint32_t idx = Q.hash == USK_HASH_X ? hash_index_x(Q.hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
       atomicAdd(&occ[base + (int64_t)i * N + idx], 1);
     }
   }
