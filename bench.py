@@ -347,10 +347,12 @@ def run_usk(args):
     clk = clocks.summary()
     f_peak = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    # ALU roofline of the sketch query: per 32 weights and SM sub-partition
-    # the USK-X hash needs 3 IMAD (2 clk) + 3 IMAD.HI (4 clk) + 1 FFMA (2 clk) on the FMA pipe =
-    # 20 clk (pipe rates measured by tools/micro/pipes.cu, profiles/r1_micro_pipes.txt)
-    alu_peak = n_sm * 4 * 32 / 20.0 * f_peak / 1e9             # Gweight/s
+    # ALU roofline of the sketch query: per 32 weights and SM sub-partition the query
+    # issues 3 x (LOP3 + FFMA.RZ + IMAD + LDS) + VIMNMX3 + SHF + FFMA = 15 warp instructions at one
+    # per clock (the FMA pipe needs <= 14 clk, the ALU pipe 10 clk at the rates measured by
+    # tools/micro/pipes.cu, profiles/r1_micro_pipes.txt), so issue binds
+    ISSUE = 15.0
+    alu_peak = n_sm * 4 * 32 / ISSUE * f_peak / 1e9             # Gweight/s
     gather_floor = n_sm * 32 * f_peak / ROWS / 1e9             # Gweight/s: M LDS wavefronts per 32 weights
     # the timed graph holds only the sketch-GEMV launches (k_gemv_fast + k_gemv_reduce per group),
     # so their achieved rate over the timed region is the step's weights / step time
@@ -481,8 +483,9 @@ def run_usk(args):
             "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gweight/s",
                          "frac": achieved / alu_peak, "traffic": traffic,
                          "kernel": "k_gemv_fast (+ k_gemv_reduce): the whole timed graph",
-                         "peak_basis": f"FMA pipe: 20 clk per 32 weights per SMSP (3 IMAD + 3 IMAD.HI + FFMA; "
-                                       f"measured rates) -> 6.4 weight/clk/SM x {n_sm} SMs x {f_peak / 1e6:.0f} MHz",
+                         "peak_basis": f"instruction issue: 15 warp-instructions per 32 weights per SMSP "
+                                       f"(3 x (LOP3 + FFMA.RZ + IMAD + LDS) + VIMNMX3 + SHF + FFMA), 1 issue/clk "
+                                       f"-> {128 / ISSUE:.2f} weight/clk/SM x {n_sm} SMs x {f_peak / 1e6:.0f} MHz",
                          "lds_gather_floor": gather_floor,
                          "isolated_launch_ms_per_step": sum_kern,
                          "hbm_frac": sketch_bytes / (ms_per_step * 1e-3) / 1e9 / peaks["hbm_gbs"]},

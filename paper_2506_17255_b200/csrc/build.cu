@@ -137,7 +137,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
     uint32_t rb[UPL][FAST ? 1 : MR];  // generic: byte offsets of (unit v, sketch row i) for this lane
     uint32_t fk[UPL][KR], cb[UPL][KR];  // fast: FFMA key and addend of (unit v, sketch row i)
     float Nf[UPL];
-    const uint32_t kbase = smem_keys + 4u * (uint32_t)lane - 0x80000000u;  // (0x4B000000 << 7) wraps to 2^31
+    const uint32_t kbase = smem_keys + 4u * (uint32_t)lane;  // (0x4C000000 << 7) wraps to 0
 #pragma unroll
     for (int v = 0; v < UPL; ++v) {
       const int ul = UPL * lane + v;
@@ -147,7 +147,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       // a missing unit of a ragged tile updates a private dummy word (never written back) with a
       // zero candidate, so the loop below needs no branch
       N[v] = valid ? (uint32_t)A.ncols[u] : 1u;
-      Nf[v] = (float)N[v];
+      Nf[v] = (float)(4u * N[v]);
       vmask[v] = valid ? ~0u : 0u;
       if constexpr (FAST) {
 #pragma unroll

@@ -82,16 +82,18 @@ __host__ __device__ __forceinline__ uint32_t hash_index_x(const HashConsts& hc, 
 }
 
 // Short-unit reduction in one FFMA.RZ: with f = as_float(0x3F800000 | k) =
-// 1 + k / 2^23 and C = 2^23 - N + off (off + N < 2^23), the exact f * N + C lies in [2^23, 2^24)
-// where the fp32 ulp is 1, so rounding toward zero gives 2^23 + off + floor(k N / 2^23): the bit
-// pattern 0x4B000000 + off + idx.  fkey = 0x3F800000 | (row key mod 2^23); R23 = R_i mod 2^23.
-__device__ __forceinline__ uint32_t short_fma_bits(uint32_t R23, uint32_t fkey, float Nf, uint32_t Cbits) {
-  return __float_as_uint(__fmaf_rz(__uint_as_float(R23 ^ fkey), Nf, __uint_as_float(Cbits)));
+// 1 + k / 2^23 and C = 2^25 - 4N + 4 off (off + N < 2^23), the exact f * 4N + C = 2^25 + 4 (off +
+// k N / 2^23) lies in [2^25, 2^26) where the fp32 ulp is 4, so rounding toward zero gives
+// 2^25 + 4 (off + floor(k N / 2^23)): the bit pattern 0x4C000000 + off + idx.  Biased exponent 152
+// is a multiple of 4, so bits * 128 = (off + idx) * 128 mod 2^32: one IMAD to the shared address.
+// fkey = 0x3F800000 | (row key mod 2^23); R23 = R_i mod 2^23; N4 = (float) 4N.
+__device__ __forceinline__ uint32_t short_fma_bits(uint32_t R23, uint32_t fkey, float N4, uint32_t Cbits) {
+  return __float_as_uint(__fmaf_rz(__uint_as_float(R23 ^ fkey), N4, __uint_as_float(Cbits)));
 }
 __host__ __device__ __forceinline__ uint32_t short_fkey(uint32_t rowkey) { return 0x3F800000u | (rowkey & 0x7FFFFFu); }
 __host__ __device__ __forceinline__ uint32_t short_cbits(uint32_t N, uint32_t off) {
-  // 2^23 - N + off as fp32 bits (an integer below 2^24: exact)
-  const float c = (float)(int32_t)(8388608u - N + off);
+  // 2^25 - 4N + 4 off as fp32 bits (a multiple of 4 below 2^26: exact)
+  const float c = (float)(int32_t)(33554432u - 4u * N + 4u * off);
 #ifdef __CUDA_ARCH__
   return __float_as_uint(c);
 #else

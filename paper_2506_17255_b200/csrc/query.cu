@@ -142,7 +142,7 @@ template <int UPL, int MT, int HASH>
 __device__ __forceinline__ void lane_setup(const QArgs& A, int64_t ubase, int nu, LaneState<UPL, MT, HASH>& S) {
   const int lane = threadIdx.x & 31;
   const uint32_t cbase = smem_u32(qsm + kCellsWordOffset);
-  S.B = cbase + 4u * (uint32_t)lane - 0x80000000u;  // (0x4B000000 << 7) wraps to 2^31
+  S.B = cbase + 4u * (uint32_t)lane;  // (0x4C000000 << 7) wraps to 0
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
     const int ul = UPL * lane + v;
@@ -156,7 +156,7 @@ __device__ __forceinline__ void lane_setup(const QArgs& A, int64_t ubase, int nu
       S.N[v] = 1;
       S.b0[v] = cbase + 4u * (uint32_t)((A.maxN - 1) * 32 + lane);
     }
-    S.Nf[v] = (float)S.N[v];
+    S.Nf[v] = (float)(4u * S.N[v]);
     if constexpr (fast_hash<MT, HASH>()) {
 #pragma unroll
       for (int i = 0; i < MT; ++i) {

@@ -68,16 +68,20 @@ def test_rows_independent_of_M(orc):
 
 def test_short_unit_float_form(orc):
     """The fast GPU kernels evaluate the short-unit range reduction as one fp32 fused multiply-add
-    rounded toward zero: RZ((1 + k/2^23) * N + (2^23 - N + off)) = 2^23 + off + floor(k N / 2^23)
-    whenever off + N < 2^23 (exact product, single rounding).  Check that identity against the
-    integer contract with numpy's float32 arithmetic emulated exactly in Python fractions."""
+    rounded toward zero: with f = 1 + k/2^23,
+    RZ(f * 4N + (2^25 - 4N + 4 off)) = 2^25 + 4 (off + floor(k N / 2^23)) whenever off + N < 2^23
+    (exact product, one rounding; the result lies in [2^25, 2^26) where the fp32 ulp is 4), so the
+    bit pattern is 0x4C000000 + off + idx.  Check that identity against the integer contract with the
+    rounding done exactly in Python fractions."""
     from fractions import Fraction
     rng = np.random.default_rng(5)
-    for _ in range(2000):
+    for _ in range(3000):
         k = int(rng.integers(0, 1 << 23))
         N = int(rng.integers(1, 1 << 16))
         off = int(rng.integers(0, (1 << 23) - N))
-        exact = Fraction((1 << 23) + k, 1 << 23) * N + ((1 << 23) - N + off)
-        rz = exact.numerator // exact.denominator  # values in [2^23, 2^24): fp32 ulp is 1
-        assert (1 << 23) <= rz < (1 << 24)
-        assert rz - (1 << 23) - off == (k * N) >> 23
+        exact = Fraction((1 << 23) + k, 1 << 23) * (4 * N) + ((1 << 25) - 4 * N + 4 * off)
+        rz = (exact.numerator // exact.denominator) // 4 * 4  # toward zero to a multiple of the ulp 4
+        assert (1 << 25) <= rz < (1 << 26)
+        bits = (152 << 23) + (rz - (1 << 25)) // 4
+        assert bits - 0x4C000000 - off == (k * N) >> 23
+        assert (bits * 128) % (1 << 32) == ((off + ((k * N) >> 23)) * 128) % (1 << 32)
