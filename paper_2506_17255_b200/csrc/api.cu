@@ -83,7 +83,7 @@ static bool layer_cells(int L, const double* imp, const std::vector<int64_t>& nu
 
 static void free_plan(usk_plan* p) {
   if (!p) return;
-  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_err};
+  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R4, p->d_err};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete p;
@@ -258,6 +258,7 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   e = e ? e : cudaMalloc(&pl->d_nrows, (size_t)U);
   e = e ? e : cudaMalloc(&pl->d_offsets, sizeof(int64_t) * (U + 1));
   e = e ? e : cudaMalloc(&pl->d_keys, sizeof(uint32_t) * U);
+  e = e ? e : cudaMalloc(&pl->d_R4, sizeof(uint4) * (pl->max_out + 32));
   e = e ? e : cudaMalloc(&pl->d_err, sizeof(int));
   if (e != cudaSuccess) {
     free_plan(pl);

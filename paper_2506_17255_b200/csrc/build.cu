@@ -53,6 +53,7 @@ struct BuildArgs {
   const int32_t* ncols;
   const int64_t* offsets;
   const uint32_t* ukeys;
+  const uint4* R4;  // {R_0, R_1, R_2} mod 2^23 per output row (fast hash, M <= 3)
   void* sketch;
   int* err;
   uint32_t kap_max;  // largest accepted weight key: 0xFEFFFFFF (finite), 0xFF000000 (+Inf = excluded outlier)
@@ -62,7 +63,7 @@ template <int ES>
 constexpr int stages_for() { return ES == 2 ? 6 : 4; }
 
 template <typename E, int UPL>
-constexpr int stage_bytes() { return kRO * 32 * UPL * (int)sizeof(E); }
+constexpr int stage_bytes() { return kRO * 16 + kRO * 32 * UPL * (int)sizeof(E); }
 
 // kappa-min update of one shared key: an unconditional red.shared.min (no return value).  A
 // plain-load pre-check would skip most atomics, but ptxas turns the predicated atomic into a branch
@@ -123,10 +124,13 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       const int64_t o0 = it * kRO;
       const int rows = (int)min((int64_t)kRO, T.out - o0);
       uint8_t* st = stages + s * STAGEB;
-      if (lane == 0) mbar_arrive_expect_tx(&full[s], (uint32_t)rows * segb);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&full[s], (uint32_t)rows * (16u + segb));
+        bulk_g2s(st, A.R4 + o0, (uint32_t)rows * 16u, &full[s]);  // the rows' position mixes
+      }
       __syncwarp();
       for (int r = lane; r < rows; r += 32)
-        bulk_g2s(st + r * ROWB, W + (o0 + r) * T.in + j0, segb, &full[s]);
+        bulk_g2s(st + kRO * 16 + r * ROWB, W + (o0 + r) * T.in + j0, segb, &full[s]);
     }
   } else {
     // ---------------- consumers: warp cw takes rows cw and cw + 16 of every stage
@@ -174,8 +178,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
         const int r = cw + rr * kConsumers;
         if (r >= rows) break;
         const uint32_t o = (uint32_t)(o0 + r);
-        const uint32_t Rl = fmix32(o ^ A.hc.rho[lane & 7]);  // lane i: R_i(o)
-        const uint8_t* row = st + r * ROWB;
+        const uint8_t* row = st + kRO * 16 + r * ROWB;
         uint32_t bits[UPL];
         if constexpr (ES == 2 && UPL == 4) {
           const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
@@ -203,9 +206,8 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
           bits[0] = reinterpret_cast<const uint32_t*>(row)[lane];
         }
         if constexpr (FAST) {
-          uint32_t R23[MT];
-#pragma unroll
-          for (int i = 0; i < MT; ++i) R23[i] = __shfl_sync(0xffffffffu, Rl, i) & 0x7FFFFFu;
+          const uint4 R4 = reinterpret_cast<const uint4*>(st)[r];  // broadcast shared load
+          const uint32_t R23[3] = {R4.x, R4.y, R4.z};
 #pragma unroll
           for (int v = 0; v < UPL; ++v) {
             const uint32_t kap = rotl1(bits[v] & vmask[v]);
@@ -221,9 +223,8 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
 #pragma unroll
             for (int i = 0; i < MR; ++i) {
               if (MT == 0 && i >= M) break;
-              const uint32_t Ri = __shfl_sync(0xffffffffu, Rl, i);
               uint32_t idx;
-              if constexpr (HASH == USK_HASH_X) idx = hash_reduce(Ri ^ row_key(K[v], A.hc.kap[i]), N[v]);
+              if constexpr (HASH == USK_HASH_X) idx = hash_index_x(A.hc, o, K[v], i, N[v]);
               else idx = o % N[v];
               key_min(smem_keys + rb[v][i] + (idx << 7), kap);
             }
@@ -509,7 +510,7 @@ int fast_upl(const usk_plan* pl, int32_t l) {
   if ((L.in * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
   const int S = es == 2 ? 6 : 4;
-  auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
+  auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 16 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
   for (int upl : {4, 2, 1})
     if (smem(upl) <= (int64_t)kSmemLimit) return upl;
   return 0;
@@ -550,6 +551,7 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
     A.ncols = pl->d_ncols;
     A.offsets = pl->d_offsets;
     A.ukeys = pl->d_keys;
+    A.R4 = pl->d_R4;
     A.sketch = sketch;
     A.err = pl->d_err;
     A.kap_max = kap_max;

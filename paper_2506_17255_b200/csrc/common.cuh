@@ -147,6 +147,7 @@ struct usk_plan {
   uint8_t* d_nrows = nullptr;
   int64_t* d_offsets = nullptr;
   uint32_t* d_keys = nullptr;  // K_u per unit
+  uint4* d_R4 = nullptr;       // {R_0, R_1, R_2} mod 2^23 per output row o < max_out (build bulk copies)
   int* d_err = nullptr;        // sticky device error flag
   int device = 0;
   // stacked state quantisation (L25): q = 0 (raw states) or 4 / 8 bits

@@ -266,6 +266,16 @@ __global__ void k_scan_last(const int64_t* in, int64_t U, int64_t* out) {
   out[U] = out[U - 1] + in[U - 1];
 }
 
+// position mixes of the g = 1 layouts for the build's bulk copies: per output row o,
+// {R_0, R_1, R_2} mod 2^23 and 0 (16 B, so a stage of rows is one contiguous copy)
+__global__ void k_R4_table(HashConsts hc, int64_t n, uint4* R4) {
+  const int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (o >= n) return;
+  const uint32_t p = (uint32_t)o;
+  R4[o] = make_uint4(fmix32(p ^ hc.rho[0]) & 0x7FFFFFu, fmix32(p ^ hc.rho[1]) & 0x7FFFFFu,
+                     fmix32(p ^ hc.rho[2]) & 0x7FFFFFu, 0u);
+}
+
 inline unsigned blocks_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
 template <class T>
@@ -379,6 +389,8 @@ usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStr
   USK_LAUNCHED("k_scan_apply");
   k_scan_last<<<1, 1, 0, st>>>(d_sizes, U, pl->d_offsets);
   USK_LAUNCHED("k_scan_last");
+  k_R4_table<<<blocks_for(pl->max_out, T256), T256, 0, st>>>(pl->hc, pl->max_out, pl->d_R4);
+  USK_LAUNCHED("k_R4_table");
 
   int h_err = 0;
   pl->h_ncols.resize(U);

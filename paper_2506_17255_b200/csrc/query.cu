@@ -594,31 +594,39 @@ constexpr int kRedThreads = 256;
 __global__ void __launch_bounds__(kRedThreads, 8) k_gemv_reduce(const __grid_constant__ QArgs A) {
   if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 0] = gtimer();
   pdl_trigger();  // the next call's compute kernel may be scheduled (it stages before its own wait)
-  pdl_wait();     // all chunk partials written
-  if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 1] = gtimer();
+  // every kernel-parameter read happens before the wait: a first touch of a parameter line misses
+  // the SM's constant cache (~1 us), which would otherwise sit on the critical path
   const int L = A.red_lanes;
   const int64_t g = (int64_t)blockIdx.x * kRedThreads + threadIdx.x;
   const int64_t r = g / L;
   const int j = (int)(g % L);
-  float t = 0.f;
   int li = 0;
-  if (r < A.rows) {
+  if (r < A.rows)
     while (li + 1 < A.n_layers && A.layer[li + 1].row_begin <= r) ++li;
-    const QLayer& Ly = A.layer[li];
-    const float4* p = reinterpret_cast<const float4*>(Ly.partial + (r - Ly.row_begin) * Ly.CP);
-    for (int c = 4 * j; c < Ly.n_chunks; c += 4 * L) {
+  const QLayer& Ly = A.layer[li];
+  const int64_t rr = r - Ly.row_begin;
+  const int nch = Ly.n_chunks;
+  const float4* p = reinterpret_cast<const float4*>(Ly.partial + rr * Ly.CP);
+  void* const yp = Ly.y;
+  const int64_t n_out = Ly.n_out;
+  const bool y_bf16 = A.y_bf16 != 0;
+  unsigned long long* const tl = A.timeline;
+  asm volatile("" ::"l"(p), "l"(yp), "l"(n_out), "r"(nch), "r"((int)y_bf16), "l"(tl) : "memory");
+  pdl_wait();     // all chunk partials written
+  if (tl && threadIdx.x == 0) tl[blockIdx.x * 4 + 1] = gtimer();
+  float t = 0.f;
+  if (r < A.rows) {
+    for (int c = 4 * j; c < nch; c += 4 * L) {
       const float4 q = __ldcg(p + c / 4);
       t += q.x;
-      if (c + 1 < Ly.n_chunks) t += q.y;
-      if (c + 2 < Ly.n_chunks) t += q.z;
-      if (c + 3 < Ly.n_chunks) t += q.w;
+      if (c + 1 < nch) t += q.y;
+      if (c + 2 < nch) t += q.z;
+      if (c + 3 < nch) t += q.w;
     }
   }
   for (int m = 1; m < L; m <<= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
   if (r < A.rows && j == 0) {
-    const QLayer& Ly = A.layer[li];
-    const int64_t rr = r - Ly.row_begin;
-    if (Ly.n_out) {  // Top-K: outliers contribute x_j * (w - w'_sketch) on top, in index order
+    if (n_out) {  // Top-K: outliers contribute x_j * (w - w'_sketch) on top, in index order
       const int64_t o = Ly.o_begin + rr;
       int64_t lo, hi;
       outlier_range(Ly.oidx, Ly.n_out, o, A.in, lo, hi);
@@ -631,16 +639,16 @@ __global__ void __launch_bounds__(kRedThreads, 8) k_gemv_reduce(const __grid_con
       }
       t += corr;
     }
-    if (A.y_bf16) {
+    if (y_bf16) {
       const uint32_t bb = __float_as_uint(t);
-      reinterpret_cast<uint16_t*>(Ly.y)[rr] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
+      reinterpret_cast<uint16_t*>(yp)[rr] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
     } else {
-      reinterpret_cast<float*>(Ly.y)[rr] = t;
+      reinterpret_cast<float*>(yp)[rr] = t;
     }
   }
-  if (A.timeline && (threadIdx.x & 31) == 0) {
-    atomicMax(&A.timeline[blockIdx.x * 4 + 2], gtimer());
-    atomicMax(&A.timeline[blockIdx.x * 4 + 3], gtimer());
+  if (tl && (threadIdx.x & 31) == 0) {
+    atomicMax(&tl[blockIdx.x * 4 + 2], gtimer());
+    atomicMax(&tl[blockIdx.x * 4 + 3], gtimer());
   }
 }
 
