@@ -1,4 +1,10 @@
-// float-range-reduction hash micro: per weight per row: k = R_i ^ Kf (LOP3), a = FFMA.RZ(f, N, C), addr, LDS
+// tools/micro/fhash.cu -- ceiling of the decode inner loop under the v2 hash contract (
+// tuning aid, not product).  Per weight and sketch row: f = R_i ^ fkey (LOP3), q = FFMA.RZ(f, 4N, C)
+// (bits 0x4C000000 + off + idx), address = q * 128 + lane base (IMAD), LDS; then VIMNMX3 + SHF + FFMA.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o fh tools/micro/fhash.cu && ./fh
+// MODE 0: the v1 contract (IMAD + IMAD.HI + LEA per row); 1: v2 with 3 SHFL per row for R_i;
+// 2: v2 with one LDS.128 broadcast of {R_0, R_1, R_2} per row (the product kernel's form);
+// 3: as 2 with row 2's address from a LOP3 mask (C scaled by 128); 4: as 2 with LEA addresses.
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -25,13 +31,13 @@ __global__ void __launch_bounds__(512, 1) kern(const uint32_t* __restrict__ Rg, 
   for (int v = 0; v < UPL; ++v) {
     K[v] = 0x12345u * (v + 1) + lane;
     const uint32_t vb = (uint32_t)(v * 32 * 3 * (N + 1));
-    B[v] = smb + 4u * (vb + lane) - 0x80000000u;
+    B[v] = smb + 4u * (vb + lane);
     for (int i = 0; i < 3; ++i) {
       Kf[v][i] = ((K[v] * (i + 7)) & 0x7FFFFFu) | 0x3F800000u;
-      C[v][i] = __float_as_uint((float)(8388608 - N + i * (N + 1)));
+      C[v][i] = __float_as_uint((float)(33554432 - 4 * N + 4 * i * (N + 1)));
       B2[v][i] = smb + 4u * (vb + i * (N + 1) * 32);  // for the 128N form: C' = region byte offset
     }
-    Nf[v] = (float)N;
+    Nf[v] = (float)(4 * N);
     Nf128[v] = (float)(128 * N);
     nx[v] = 1.0f + v;
   }
@@ -75,7 +81,8 @@ __global__ void __launch_bounds__(512, 1) kern(const uint32_t* __restrict__ Rg, 
           const uint32_t q0 = __float_as_uint(__fmaf_rz(f0, Nf[v], __uint_as_float(C[v][0])));
           const uint32_t q1 = __float_as_uint(__fmaf_rz(f1, Nf[v], __uint_as_float(C[v][1])));
           if (MODE == 3) {
-            const uint32_t q2 = __float_as_uint(__fmaf_rz(f2, Nf128[v], __uint_as_float(0x4B000000u | B2[v][2])));
+            // 128N scaling at exponent 150 (ulp 1): mantissa = B2 + floor(128 k N / 2^23); mask to the row
+            const uint32_t q2 = __float_as_uint(__fmaf_rz(f2, Nf128[v], __uint_as_float(0x4B000000u | (B2[v][2] - 128u * N))));
             m0 = lds(imad(q0, 128u, B[v]));
             m1 = lds(imad(q1, 128u, B[v]));
             m2 = lds((q2 & 0x7FFF80u) | l4);
