@@ -31,9 +31,11 @@ OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE = 0, 1, 2, 3, 4
 def build(force: bool = False) -> str:
     """Compile the oracle with gcc (no fast-math, no FP contraction)."""
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < os.path.getmtime(SRC):
+        tmp = f"{LIB}.{os.getpid()}.tmp"  # concurrent builders (pytest -n) each rename atomically
         subprocess.check_call(
             ["gcc", "-std=c99", "-O2", "-fno-fast-math", "-ffp-contract=off", "-fPIC", "-shared",
-             "-Wall", "-o", LIB, SRC, "-lm"])
+             "-Wall", "-o", tmp, SRC, "-lm"])
+        os.replace(tmp, LIB)
     return LIB
 
 
@@ -73,9 +75,9 @@ def lib():
         L.uo_importance.restype = i32
         L.uo_importance.argtypes = [p, i64, i64, p]
         L.uo_allocate.restype = i32
-        L.uo_allocate.argtypes = [i64, p, p, i64, i32, i32, i32, p, p]
+        L.uo_allocate.argtypes = [i64, p, p, i64, i32, p, i32, p, p]
         L.uo_plan.restype = i32
-        L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, i32, i32, p, i64, p, p, p, p, p]
+        L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, i32, i32, p, i64, p, p, p, p, p, p, p]
         L.uo_topk.restype = i32
         L.uo_topk.argtypes = [i32, p, i64, i64, p, p]
         L.uo_layer_cells.restype = i32
@@ -87,23 +89,23 @@ def lib():
         L.uo_pack_codes.restype = i32
         L.uo_pack_codes.argtypes = [i32, p, i64, p]
         L.uo_aggregate_grad.restype = i32
-        L.uo_aggregate_grad.argtypes = [p, i64, i64, i32, i32, i32, i64, p, p, i32, i32, u64, p]
+        L.uo_aggregate_grad.argtypes = [p, i64, i64, i32, i32, i32, i64, p, p, p, i32, u64, p]
         L.uo_f32_to_bf16_rne.restype = u32
         L.uo_f32_to_bf16_rne.argtypes = [u32]
         L.uo_build_units.restype = i32
-        L.uo_build_units.argtypes = [i32, p, i64, i64, i32, i32, i32, i64, i64, p, p, i32, i32, u64, p, i32, p]
+        L.uo_build_units.argtypes = [i32, p, i64, i64, i32, i32, i32, i64, i64, p, p, p, i32, u64, p, i32, p]
         L.uo_reconstruct_rows.restype = i32
-        L.uo_reconstruct_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, i64, i64, p, i32]
+        L.uo_reconstruct_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, p, i32, u64, i64, i64, p, i32]
         L.uo_reconstruct_entries.restype = i32
-        L.uo_reconstruct_entries.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, p, i64, p, i32]
+        L.uo_reconstruct_entries.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, p, i32, u64, p, i64, p, i32]
         L.uo_linear_rows.restype = i32
-        L.uo_linear_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, i32, i32, u64, p, i64, i64, i64, p, i32]
+        L.uo_linear_rows.argtypes = [i32, p, i64, i64, i32, i32, i32, p, p, p, i32, u64, p, i64, i64, i64, p, i32]
         L.uo_retrieve_v.restype = u32
         L.uo_retrieve_v.argtypes = [i32, i32, p, i32]
         L.uo_sketch_unit_v.restype = i32
         L.uo_sketch_unit_v.argtypes = [i32, i32, p, p, i64, i32, u64, u32, u32, i32, u32, p]
         L.uo_stats.restype = i32
-        L.uo_stats.argtypes = [i32, p, p, i64, i64, i32, i32, i32, i64, p, p, i32, i32, u64, p]
+        L.uo_stats.argtypes = [i32, p, p, i64, i64, i32, i32, i32, i64, p, p, p, i32, u64, p]
         L.uo_peak_memory.restype = i64
         L.uo_peak_memory.argtypes = [p, p, i32]
     return _lib
@@ -196,14 +198,17 @@ def importance(A: np.ndarray) -> np.ndarray:
 
 
 def allocate(scores, T, C=None, M=1, min_cols=1, lengths=None):
-    """Per-unit columns for unit scores under a budget of T cells (C defaults to U)."""
+    """Per-unit columns for unit scores under a budget of T cells (C defaults to U).  M: the sketch
+    rows of every class, or a sequence of C per-class row counts (ledger L30)."""
     s = np.ascontiguousarray(scores, dtype=np.float64)
     U = len(s)
     C = U if C is None else C
+    Mc = np.full(C, M, dtype=np.int32) if np.isscalar(M) else np.ascontiguousarray(M, dtype=np.int32)
+    assert len(Mc) == C
     L_u = np.ones(U, dtype=np.uint64) if lengths is None else np.ascontiguousarray(lengths, dtype=np.uint64)
     cls = np.zeros(U, dtype=np.uint8)
     ncols = np.zeros(U, dtype=np.int32)
-    _check(lib().uo_allocate(U, _ptr(s), _ptr(L_u), T, C, M, min_cols, _ptr(cls), _ptr(ncols)), "allocate")
+    _check(lib().uo_allocate(U, _ptr(s), _ptr(L_u), T, C, _ptr(Mc), min_cols, _ptr(cls), _ptr(ncols)), "allocate")
     return ncols, cls
 
 
@@ -228,6 +233,8 @@ class Plan:
     group: int = 128        # cells per quantisation group (layers start at multiples of it)
     variant: int = 0        # ABSMAXMIN (the paper's sketch), ABSMINMAX, COUNTMIN (App. C.2)
     topk: int = 0           # Top-K outliers per layer stored apart (App. A)
+    nrows: np.ndarray = None  # [U] sketch rows per unit (its class's; ledger L30)
+    class_rows: tuple = None  # per-class rows, or None (every class has M)
     extra: dict = field(default_factory=dict)
 
     @property
@@ -240,12 +247,13 @@ class Plan:
 
     def layer_slices(self, l):
         u0, u1 = self.layer_units(l)
-        return (np.ascontiguousarray(self.ncols[u0:u1]), np.ascontiguousarray(self.offsets[u0:u1 + 1]))
+        return (np.ascontiguousarray(self.ncols[u0:u1]), np.ascontiguousarray(self.offsets[u0:u1 + 1]),
+                np.ascontiguousarray(self.nrows[u0:u1]))
 
 
 def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None, min_cols=1,
          hash_kind=HASH_X, seed=0, state_bits=0, group=128, variant=ABSMAXMIN, layer_importance=None,
-         topk=0) -> Plan:
+         topk=0, class_rows=None) -> Plan:
     L = len(shapes)
     outf = np.array([s[0] for s in shapes], dtype=np.int64)
     inf = np.array([s[1] for s in shapes], dtype=np.int64)
@@ -263,15 +271,21 @@ def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None
     offsets = np.zeros(max(U, 1) + 1, dtype=np.int64)
     acct = np.zeros(4 * L, dtype=np.int64)
     limp = None if layer_importance is None else np.ascontiguousarray(layer_importance, dtype=np.float64)
+    crows = None
+    if class_rows is not None:
+        crows = np.ascontiguousarray(class_rows, dtype=np.int32)
+        if len(crows) != C:
+            raise OracleError(EINVAL, "plan: class_rows needs one row count per class")
+    nrows = np.zeros(max(U, 1), dtype=np.uint8)
     st = lib().uo_plan(L, _ptr(outf), _ptr(inf), dtype,
                        ct.cast(sal_ptrs, ct.c_void_p) if sal_ptrs is not None else None,
                        float(bpw), M, gran, g, C, min_cols, state_bits, group,
-                       None if limp is None else _ptr(limp), int(topk), _ptr(unit_base), _ptr(cls),
-                       _ptr(ncols), _ptr(offsets), _ptr(acct))
+                       None if limp is None else _ptr(limp), int(topk), None if crows is None else _ptr(crows),
+                       _ptr(unit_base), _ptr(cls), _ptr(ncols), _ptr(nrows), _ptr(offsets), _ptr(acct))
     _check(st, "plan")
     return Plan(list(map(tuple, zip(outf.tolist(), inf.tolist()))), dtype, M, gran, g, C, min_cols, hash_kind,
                 seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4), state_bits, group, variant,
-                int(topk))
+                int(topk), nrows[:U], None if crows is None else tuple(int(v) for v in crows))
 
 
 def layer_cells(importance, numel, units, M, min_cols, T) -> np.ndarray:
@@ -299,11 +313,11 @@ def build_layer(pl: Plan, l: int, W: np.ndarray, sketch: np.ndarray, t_begin=0, 
     if pl.dtype == F32:
         W = W.astype(np.float32, copy=False)
     assert W.shape == (out, inn)
-    ncols, offs = pl.layer_slices(l)
+    ncols, offs, nrows = pl.layer_slices(l)
     assert sketch.dtype == _np_dtype(pl.dtype) and sketch.flags["C_CONTIGUOUS"]
     ex = None if exclude is None else np.ascontiguousarray(exclude, dtype=np.uint8)
     _check(lib().uo_build_units(pl.dtype, _ptr(W), out, inn, l, pl.gran, pl.g, t_begin, t_end, _ptr(ncols),
-                                _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(sketch), pl.variant,
+                                _ptr(offs), _ptr(nrows), pl.hash_kind, pl.seed, _ptr(sketch), pl.variant,
                                 None if ex is None else _ptr(ex)), "build_units")
 
 
@@ -420,11 +434,11 @@ def reconstruct_rows(pl: Plan, sketch, l: int, o_begin=0, o_end=None) -> np.ndar
     """W' rows in the plan dtype (quantised plans: the dequantised value, RNE to bf16)."""
     out, inn = pl.shapes[l]
     o_end = out if o_end is None else o_end
-    ncols, offs = pl.layer_slices(l)
+    ncols, offs, nrows = pl.layer_slices(l)
     dt, cells = _retrieval_view(pl, sketch)
     res = np.zeros((o_end - o_begin, inn), dtype=_np_dtype(dt))
     _check(lib().uo_reconstruct_rows(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs),
-                                     pl.M, pl.hash_kind, pl.seed, o_begin, o_end, _ptr(res), pl.variant),
+                                     _ptr(nrows), pl.hash_kind, pl.seed, o_begin, o_end, _ptr(res), pl.variant),
            "reconstruct_rows")
     if isinstance(sketch, TSketch):  # outliers keep their value (App. A)
         o_idx, j_idx = sketch.idx[l] // inn, sketch.idx[l] % inn
@@ -435,12 +449,12 @@ def reconstruct_rows(pl: Plan, sketch, l: int, o_begin=0, o_end=None) -> np.ndar
 
 def reconstruct_entries(pl: Plan, sketch, l: int, oj: np.ndarray) -> np.ndarray:
     out, inn = pl.shapes[l]
-    ncols, offs = pl.layer_slices(l)
+    ncols, offs, nrows = pl.layer_slices(l)
     dt, cells = _retrieval_view(pl, sketch)
     oj = np.ascontiguousarray(oj, dtype=np.int64)
     res = np.zeros(len(oj), dtype=np.uint32)
     _check(lib().uo_reconstruct_entries(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols),
-                                        _ptr(offs), pl.M, pl.hash_kind, pl.seed, _ptr(oj), len(oj), _ptr(res),
+                                        _ptr(offs), _ptr(nrows), pl.hash_kind, pl.seed, _ptr(oj), len(oj), _ptr(res),
                                         pl.variant), "reconstruct_entries")
     if isinstance(sketch, TSketch):
         flat = oj[:, 0] * inn + oj[:, 1]
@@ -459,10 +473,10 @@ def linear_rows(pl: Plan, sketch, l: int, x: np.ndarray, o_begin=0, o_end=None) 
     T = x.shape[0]
     if isinstance(sketch, TSketch):  # fp64 matmul of the overlaid W' (uo_linear_rows is pinned to it)
         return x @ value_of(reconstruct_rows(pl, sketch, l, o_begin, o_end), pl.dtype).T
-    ncols, offs = pl.layer_slices(l)
+    ncols, offs, nrows = pl.layer_slices(l)
     dt, cells = _retrieval_view(pl, sketch)
     y = np.zeros((T, o_end - o_begin), dtype=np.float64)
-    _check(lib().uo_linear_rows(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs), pl.M,
+    _check(lib().uo_linear_rows(dt, _ptr(cells), out, inn, l, pl.gran, pl.g, _ptr(ncols), _ptr(offs), _ptr(nrows),
                                 pl.hash_kind, pl.seed, _ptr(x), T, o_begin, o_end, _ptr(y), pl.variant), "linear_rows")
     return y
 
@@ -472,11 +486,11 @@ def aggregate_grad(pl: Plan, l: int, grad: np.ndarray) -> np.ndarray:
     the gradients of the weights mapped to it in each sketch row (ledger L26).  grad: [out, in]
     values (any float dtype, exact in fp64)."""
     out, inn = pl.shapes[l]
-    ncols, offs = pl.layer_slices(l)
+    ncols, offs, nrows = pl.layer_slices(l)
     g = np.ascontiguousarray(grad, dtype=np.float64)
     assert g.shape == (out, inn)
     res = np.zeros(int(offs[-1] - offs[0]), dtype=np.float32)
-    _check(lib().uo_aggregate_grad(_ptr(g), out, inn, l, pl.gran, pl.g, len(ncols), _ptr(ncols), _ptr(offs), pl.M,
+    _check(lib().uo_aggregate_grad(_ptr(g), out, inn, l, pl.gran, pl.g, len(ncols), _ptr(ncols), _ptr(offs), _ptr(nrows),
                                    pl.hash_kind, pl.seed, _ptr(res)), "aggregate_grad")
     return res
 
@@ -488,7 +502,7 @@ STATS_KEYS = ("weights", "untouched", "sign_errors", "zero_weights", "rel_exact"
 def stats(pl: Plan, l: int, W: np.ndarray, Wp: np.ndarray) -> dict:
     """Compression report of layer l (ledger L27): counts keyed by STATS_KEYS."""
     out, inn = pl.shapes[l]
-    ncols, offs = pl.layer_slices(l)
+    ncols, offs, nrows = pl.layer_slices(l)
     W = np.ascontiguousarray(W, dtype=_np_dtype(pl.dtype) if pl.dtype == BF16 else np.float32)
     Wp = np.ascontiguousarray(Wp)
     if pl.dtype == F32:
@@ -496,7 +510,7 @@ def stats(pl: Plan, l: int, W: np.ndarray, Wp: np.ndarray) -> dict:
         Wp = Wp.view(np.uint32) if Wp.dtype != np.uint32 else Wp
     counts = np.zeros(13, dtype=np.int64)
     _check(lib().uo_stats(pl.dtype, _ptr(W), _ptr(Wp), out, inn, l, pl.gran, pl.g, len(ncols), _ptr(ncols), _ptr(offs),
-                          pl.M, pl.hash_kind, pl.seed, _ptr(counts)), "stats")
+                          _ptr(nrows), pl.hash_kind, pl.seed, _ptr(counts)), "stats")
     return dict(zip(STATS_KEYS, counts.tolist()))
 
 

@@ -23,6 +23,9 @@
  *   uo_allocate / uo_plan -- pinned (SPEC allocation examples, conservation, monotonicity,
  *       scale invariance, bpw accounting vs Table 1 arithmetic); class boundaries and the
  *       remainder order are our reading (L9/L10): "parity unpinned" for those.
+ *   per-class sketch rows (uo_plan class_rows, uo_allocate Mc, ledger L30) --
+ *       pinned (hand-worked allocation, reduction to the uniform plan, conservation, the set-based
+ *       enumerator per unit incl. LAYER units, Appendix B's untouched closed form per class).
  *   uo_importance -- pinned (SPEC Eq. 7 examples, constant activations).
  *   uo_linear_rows -- pinned (numpy fp64 matmul of the oracle-verified W').
  *   uo_aggregate_grad (aggregated-gradient baseline) -- pinned (SPEC example
@@ -315,10 +318,11 @@ static int uo_rem_cmp(const void* a, const void* b) {
 }
 
 /* s_u: unit scores (>= 0, finite); L_u: unit lengths (weights per unit; pass 1 for a
- * common length); T: cells available; C classes; M rows; min_cols floor.
- * Outputs: cls[U], ncols[U]. */
+ * common length); T: cells available; C classes; Mc[c]: sketch rows of class c (ledger L30: the
+ * class's share of the cells is split into Mc[c] rows of N_c columns, so x_c = T W_c / (W n_c
+ * Mc[c])); min_cols floor.  Outputs: cls[U], ncols[U]. */
 int32_t uo_allocate(int64_t U, const double* s_u, const uint64_t* L_u, int64_t T, int32_t C,
-                    int32_t M, int32_t min_cols, uint8_t* cls, int32_t* ncols) {
+                    const int32_t* Mc, int32_t min_cols, uint8_t* cls, int32_t* ncols) {
   int64_t u, r;
   int32_t c;
   double s_max = 0.0;
@@ -330,7 +334,9 @@ int32_t uo_allocate(int64_t U, const double* s_u, const uint64_t* L_u, int64_t T
   int64_t N_c[256];
   uo_u128 num_c[256], den_c[256];
   if (U < 1) return UO_ESHAPE;
-  if (C < 1 || C > 255 || M < 1 || M > 8 || min_cols < 1 || T < 0) return UO_EINVAL;
+  if (C < 1 || C > 255 || min_cols < 1 || T < 0) return UO_EINVAL;
+  for (c = 0; c < C; c++)
+    if (Mc[c] < 1 || Mc[c] > 8) return UO_EINVAL;
   q = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)U);
   items = (uo_rank_item*)malloc(sizeof(uo_rank_item) * (size_t)U);
   for (u = 0; u < U; u++) {
@@ -363,7 +369,7 @@ int32_t uo_allocate(int64_t U, const double* s_u, const uint64_t* L_u, int64_t T
   /* feasibility of the floor */
   {
     int64_t floor_cells = 0;
-    for (c = 0; c < C; c++) floor_cells += n_c[c] * (int64_t)M * (int64_t)min_cols;
+    for (c = 0; c < C; c++) floor_cells += n_c[c] * (int64_t)Mc[c] * (int64_t)min_cols;
     if (floor_cells > T) {
       free(q);
       free(items);
@@ -381,12 +387,12 @@ int32_t uo_allocate(int64_t U, const double* s_u, const uint64_t* L_u, int64_t T
       if (active[c])
         Wa += W_c[c];
       else
-        Ta -= n_c[c] * (int64_t)M * (int64_t)min_cols;
+        Ta -= n_c[c] * (int64_t)Mc[c] * (int64_t)min_cols;
     }
     for (c = 0; c < C; c++) {
       if (!active[c]) continue;
       num_c[c] = (uo_u128)Ta * W_c[c];
-      den_c[c] = Wa * (uo_u128)n_c[c] * (uo_u128)M;
+      den_c[c] = Wa * (uo_u128)n_c[c] * (uo_u128)Mc[c];
       N_c[c] = (den_c[c] == 0) ? 0 : (int64_t)(num_c[c] / den_c[c]);
       if (N_c[c] < min_cols) {
         active[c] = 0;
@@ -402,7 +408,7 @@ int32_t uo_allocate(int64_t U, const double* s_u, const uint64_t* L_u, int64_t T
     int64_t left = T;
     uo_rem_item rem[256];
     int32_t n_rem = 0, k;
-    for (c = 0; c < C; c++) left -= n_c[c] * (int64_t)M * N_c[c];
+    for (c = 0; c < C; c++) left -= n_c[c] * (int64_t)Mc[c] * N_c[c];
     for (c = 0; c < C; c++) {
       if (!active[c]) continue;
       rem[n_rem].key = (uint64_t)(((num_c[c] % den_c[c]) << 32) / den_c[c]);
@@ -412,7 +418,7 @@ int32_t uo_allocate(int64_t U, const double* s_u, const uint64_t* L_u, int64_t T
     qsort(rem, (size_t)n_rem, sizeof(uo_rem_item), uo_rem_cmp);
     for (k = 0; k < n_rem; k++) {
       int32_t cc = rem[k].c;
-      int64_t need = n_c[cc] * (int64_t)M;
+      int64_t need = n_c[cc] * (int64_t)Mc[cc];
       if (need <= left) {
         N_c[cc] += 1;
         left -= need;
@@ -516,13 +522,20 @@ int32_t uo_layer_cells(int32_t L, const double* imp, const int64_t* numel, const
 
 int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32_t dtype,
                 const float* const* sal, double bpw, int32_t M, int32_t gran, int32_t g, int32_t C,
-                int32_t min_cols, int32_t q, int32_t G, const double* layer_imp, int64_t topk, int64_t* unit_base,
-                uint8_t* cls, int32_t* ncols, int64_t* offsets, int64_t* layer_acct) {
-  int32_t l;
+                int32_t min_cols, int32_t q, int32_t G, const double* layer_imp, int64_t topk,
+                const int32_t* class_rows, int64_t* unit_base, uint8_t* cls, int32_t* ncols, uint8_t* nrows,
+                int64_t* offsets, int64_t* layer_acct) {
+  int32_t l, c;
   int64_t U = 0, u;
   int32_t state_bits = (dtype == UO_BF16) ? 16 : 32;
   int64_t two_T[256];
+  int32_t Mc[256]; /* rows per class: class_rows (ledger L30), or M for every class */
   if (n_layers < 1 || M < 1 || M > 8 || C < 1 || C > 255 || min_cols < 1) return UO_EINVAL;
+  for (c = 0; c < C; c++) {
+    Mc[c] = class_rows ? class_rows[c] : M;
+    if (Mc[c] < 1 || Mc[c] > 8) return UO_EINVAL;
+  }
+  if (class_rows && layer_imp) return UO_EINVAL; /* two-level floors assume one row count */
   if (q != 0 && q != 4 && q != 8) return UO_EINVAL;
   if (q != 0 && (G < 32 || (G & (G - 1)) != 0)) return UO_EINVAL; /* power of two >= 32 */
   if (!(bpw > 0.0) || !isfinite(bpw)) return UO_EINVAL;
@@ -594,13 +607,13 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
         s_u[t] = s / (double)g;
         L_u[t] = 1; /* common unit length within a layer */
       }
-      st = uo_allocate(Ul, s_u, L_u, T, C, M, min_cols, cls + unit_base[l], ncols + unit_base[l]);
+      st = uo_allocate(Ul, s_u, L_u, T, C, Mc, min_cols, cls + unit_base[l], ncols + unit_base[l]);
       free(s_u);
       free(L_u);
       if (st != UO_OK) return st;
       {
         int64_t cells = 0;
-        for (t = 0; t < Ul; t++) cells += (int64_t)M * ncols[unit_base[l] + t];
+        for (t = 0; t < Ul; t++) cells += (int64_t)Mc[cls[unit_base[l] + t]] * ncols[unit_base[l] + t];
         achieved += (q == 0) ? cells * state_bits : ((cells + G - 1) / G) * ((int64_t)q * G + 32);
       }
       layer_acct[4 * l + 0] = budget;
@@ -636,7 +649,7 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       int64_t ng = budget / ((int64_t)q * G + 32) - n_layers;
       T = (ng > 0 ? ng : 0) * G;
     }
-    st = uo_allocate(n_layers, s_u, L_u, T, C, M, min_cols, cls, ncols);
+    st = uo_allocate(n_layers, s_u, L_u, T, C, Mc, min_cols, cls, ncols);
     free(s_u);
     free(L_u);
     if (st != UO_OK) return st;
@@ -644,16 +657,17 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       layer_acct[4 * l + 0] = (l == 0) ? budget : 0;
       layer_acct[4 * l + 1] = 0;
       layer_acct[4 * l + 2] = (l == 0) ? T : 0;
-      layer_acct[4 * l + 3] = (q == 0) ? (int64_t)M * ncols[l] * state_bits
-                                       : (((int64_t)M * ncols[l] + G - 1) / G) * ((int64_t)q * G + 32);
+      layer_acct[4 * l + 3] = (q == 0) ? (int64_t)Mc[cls[l]] * ncols[l] * state_bits
+                                       : (((int64_t)Mc[cls[l]] * ncols[l] + G - 1) / G) * ((int64_t)q * G + 32);
     }
   }
-  /* offsets: exclusive prefix sum of M * N_u in (layer, t) order; with q, each layer starts at
-   * a multiple of G */
+  /* offsets: exclusive prefix sum of M_u * N_u in (layer, t) order (M_u = the rows of the unit's
+   * class); with q, each layer starts at a multiple of G */
+  for (u = 0; u < U; u++) nrows[u] = (uint8_t)Mc[cls[u]];
   offsets[0] = 0;
   for (l = 0; l < n_layers; l++) {
     if (q != 0) offsets[unit_base[l]] = uo_align_up(offsets[unit_base[l]], G);
-    for (u = unit_base[l]; u < unit_base[l + 1]; u++) offsets[u + 1] = offsets[u] + (int64_t)M * ncols[u];
+    for (u = unit_base[l]; u < unit_base[l + 1]; u++) offsets[u + 1] = offsets[u] + (int64_t)nrows[u] * ncols[u];
   }
   return UO_OK;
 }
@@ -758,10 +772,11 @@ static void uo_unit_span(int32_t gran, int32_t g, int64_t in, int64_t t, int64_t
 
 int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, int32_t layer,
                        int32_t gran, int32_t g, int64_t t_begin, int64_t t_end,
-                       const int32_t* ncols, const int64_t* offsets, int32_t M, int32_t hash_kind,
+                       const int32_t* ncols, const int64_t* offsets, const uint8_t* nrows, int32_t hash_kind,
                        uint64_t seed, void* sketch, int32_t variant, const uint8_t* exclude) {
   int64_t t;
   for (t = t_begin; t < t_end; t++) {
+    const int32_t M = nrows[t]; /* the unit's sketch rows (its class's, ledger L30) */
     int64_t j0, j1, j, o, n, k = 0;
     uint32_t *wb, *pos, *cells;
     int32_t st;
@@ -792,9 +807,10 @@ int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, in
 
 static uint32_t uo_weight_at(int32_t dtype, const void* sketch, int64_t out, int64_t in,
                              int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
-                             const int64_t* offsets, int32_t M, int32_t hash_kind, uint64_t seed,
+                             const int64_t* offsets, const uint8_t* nrows, int32_t hash_kind, uint64_t seed,
                              int64_t o, int64_t j, int32_t variant) {
   int64_t t = (gran == UO_GRAN_ROW) ? j / g : 0;
+  const int32_t M = nrows[t];
   int64_t j0 = (gran == UO_GRAN_ROW) ? t * g : 0;
   uint32_t p = (uint32_t)((j - j0) * out + o);
   uint32_t N = (uint32_t)ncols[t];
@@ -811,14 +827,14 @@ static uint32_t uo_weight_at(int32_t dtype, const void* sketch, int64_t out, int
 /* W'[o, j] for o in [o_begin, o_end), all j; w_out is [(o_end-o_begin), in] raw bits. */
 int32_t uo_reconstruct_rows(int32_t dtype, const void* sketch, int64_t out, int64_t in,
                             int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
-                            const int64_t* offsets, int32_t M, int32_t hash_kind, uint64_t seed,
+                            const int64_t* offsets, const uint8_t* nrows, int32_t hash_kind, uint64_t seed,
                             int64_t o_begin, int64_t o_end, void* w_out, int32_t variant) {
   int64_t o, j;
   if (o_begin < 0 || o_end > out || o_begin > o_end) return UO_ESHAPE;
   for (o = o_begin; o < o_end; o++)
     for (j = 0; j < in; j++)
       uo_store(dtype, w_out, (o - o_begin) * in + j,
-               uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets, M, hash_kind,
+               uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets, nrows, hash_kind,
                             seed, o, j, variant));
   return UO_OK;
 }
@@ -826,11 +842,11 @@ int32_t uo_reconstruct_rows(int32_t dtype, const void* sketch, int64_t out, int6
 /* W'[o, j] for an explicit list of (o, j) pairs (sampled parity at full size). */
 int32_t uo_reconstruct_entries(int32_t dtype, const void* sketch, int64_t out, int64_t in,
                                int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
-                               const int64_t* offsets, int32_t M, int32_t hash_kind, uint64_t seed,
+                               const int64_t* offsets, const uint8_t* nrows, int32_t hash_kind, uint64_t seed,
                                const int64_t* oj, int64_t n, uint32_t* out_bits, int32_t variant) {
   int64_t k;
   for (k = 0; k < n; k++)
-    out_bits[k] = uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets, M, hash_kind,
+    out_bits[k] = uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets, nrows, hash_kind,
                                seed, oj[2 * k], oj[2 * k + 1], variant);
   return UO_OK;
 }
@@ -840,7 +856,7 @@ int32_t uo_reconstruct_entries(int32_t dtype, const void* sketch, int64_t out, i
  * x: [T, in] doubles; y: [T, o_end - o_begin]. */
 int32_t uo_linear_rows(int32_t dtype, const void* sketch, int64_t out, int64_t in, int32_t layer,
                        int32_t gran, int32_t g, const int32_t* ncols, const int64_t* offsets,
-                       int32_t M, int32_t hash_kind, uint64_t seed, const double* x, int64_t T,
+                       const uint8_t* nrows, int32_t hash_kind, uint64_t seed, const double* x, int64_t T,
                        int64_t o_begin, int64_t o_end, double* y, int32_t variant) {
   int64_t o, j, tok;
   double* wrow;
@@ -849,7 +865,7 @@ int32_t uo_linear_rows(int32_t dtype, const void* sketch, int64_t out, int64_t i
   for (o = o_begin; o < o_end; o++) {
     for (j = 0; j < in; j++)
       wrow[j] = uo_value(dtype, uo_weight_at(dtype, sketch, out, in, layer, gran, g, ncols, offsets,
-                                             M, hash_kind, seed, o, j, variant));
+                                             nrows, hash_kind, seed, o, j, variant));
     for (tok = 0; tok < T; tok++) {
       double s = 0.0;
       for (j = 0; j < in; j++) s += x[tok * in + j] * wrow[j];
@@ -870,7 +886,7 @@ int32_t uo_linear_rows(int32_t dtype, const void* sketch, int64_t out, int64_t i
  * cells (offsets relative to offsets[0]). */
 int32_t uo_aggregate_grad(const double* grad, int64_t out, int64_t in, int32_t layer, int32_t gran,
                           int32_t g, int64_t n_units, const int32_t* ncols, const int64_t* offsets,
-                          int32_t M, int32_t hash_kind, uint64_t seed, float* cell_grad) {
+                          const uint8_t* nrows, int32_t hash_kind, uint64_t seed, float* cell_grad) {
   int64_t t, o, j, c;
   const int64_t n_cells = offsets[n_units] - offsets[0];
   int64_t* acc = (int64_t*)calloc((size_t)(n_cells > 0 ? n_cells : 1), sizeof(int64_t));
@@ -882,7 +898,7 @@ int32_t uo_aggregate_grad(const double* grad, int64_t out, int64_t in, int32_t l
         const uint32_t p = (uint32_t)((j - j0) * out + o);
         const int64_t q = llrint(grad[o * in + j] * 281474976710656.0); /* 2^48 */
         int32_t i;
-        for (i = 0; i < M; i++) {
+        for (i = 0; i < nrows[t]; i++) {
           const uint32_t idx = uo_hash_index(hash_kind, seed, (uint32_t)layer, (uint32_t)t, i, p, (uint32_t)ncols[t]);
           acc[offsets[t] - offsets[0] + (int64_t)i * ncols[t] + idx] += q;
         }
@@ -903,7 +919,7 @@ int32_t uo_aggregate_grad(const double* grad, int64_t out, int64_t in, int32_t l
  * W, Wp: [out, in] raw bits of the weight dtype (Wp = the reconstruction). */
 int32_t uo_stats(int32_t dtype, const void* W, const void* Wp, int64_t out, int64_t in, int32_t layer,
                  int32_t gran, int32_t g, int64_t n_units, const int32_t* ncols, const int64_t* offsets,
-                 int32_t M, int32_t hash_kind, uint64_t seed, int64_t* counts) {
+                 const uint8_t* nrows, int32_t hash_kind, uint64_t seed, int64_t* counts) {
   static const float edges[5] = {1e-3f, 1e-2f, 1e-1f, 1.0f, 10.0f};
   int64_t e, t, o, j, c;
   const int64_t n_cells = offsets[n_units] - offsets[0];
@@ -935,7 +951,7 @@ int32_t uo_stats(int32_t dtype, const void* W, const void* Wp, int64_t out, int6
       for (j = j0; j < j1; j++) {
         const uint32_t p = (uint32_t)((j - j0) * out + o);
         int32_t i;
-        for (i = 0; i < M; i++)
+        for (i = 0; i < nrows[t]; i++)
           occ[offsets[t] - offsets[0] + (int64_t)i * ncols[t] +
               uo_hash_index(hash_kind, seed, (uint32_t)layer, (uint32_t)t, i, p, (uint32_t)ncols[t])]++;
       }

@@ -77,7 +77,7 @@ def assert_plan_equal(pl, opl):
         np.testing.assert_array_equal(cls, opl.cls[u0:u1])
         np.testing.assert_array_equal(ncols, opl.ncols[u0:u1])
         np.testing.assert_array_equal(offs, opl.offsets[u0:u1 + 1])
-        assert (nrows == opl.M).all()
+        np.testing.assert_array_equal(nrows, opl.nrows[u0:u1])
         li = pl.layers[l]
         assert li.budget_bits == opl.acct[l, 0] and li.meta_bits == opl.acct[l, 1]
         if opl.gran == 0:
