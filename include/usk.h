@@ -108,6 +108,14 @@ typedef struct {
                             the layer budget (32 + state bits each), left out of the sketch, and
                             overlaid on every retrieval (L29).  ROW granularity, raw
                             states, AbsMaxMin only; 0 = none. */
+  const int32_t* class_rows; /* host [n_classes] sketch rows per importance class, each in [1, 8], or
+                            NULL (every class has `rows`).  The north star's "salient weights more
+                            rows or buckets" (categories PAPER.md:523-528; DESIGN.md
+                            L30): class c's share of the cells (proportional to its importance, as
+                            without class_rows) is laid out as class_rows[c] rows of N_c columns,
+                            x_c = T W_c / (W n_c class_rows[c]).  Unit u has M_u = class_rows[cls_u]
+                            rows (usk_plan_export nrows); usk_plan_info.rows = max_c class_rows[c].
+                            AbsMaxMin only; not with layer_importance. */
 } usk_params;
 
 typedef struct usk_plan usk_plan;

@@ -151,6 +151,17 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
         return fail(USK_EINVAL, "layer_importance must be finite and >= 0");
   }
   if (P.variant != USK_ABSMAXMIN && P.state_bits) return fail(USK_EUNSUPPORTED, "variants use raw states");
+  const int32_t n_cls = P.n_classes > 0 ? P.n_classes : (saliency ? 4 : 1);
+  int32_t max_rows = P.rows;
+  if (P.class_rows) {  // per-class sketch rows (ledger L30)
+    if (P.layer_importance) return fail(USK_EINVAL, "class_rows: not with layer_importance");
+    if (P.variant != USK_ABSMAXMIN) return fail(USK_EINVAL, "class_rows: AbsMaxMin only");
+    max_rows = 0;
+    for (int c = 0; c < n_cls; ++c) {
+      if (P.class_rows[c] < 1 || P.class_rows[c] > 8) return fail(USK_EINVAL, "class_rows must be in [1, 8]");
+      max_rows = std::max(max_rows, P.class_rows[c]);
+    }
+  }
   if (P.state_bits && (qG < 32 || (qG & (qG - 1)) != 0))
     return fail(USK_EINVAL, "group_size must be a power of two >= 32");
   const int g = P.granularity == USK_GRAN_ROW ? P.dims_per_unit : 1;
@@ -166,10 +177,12 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   usk_plan* pl = new (std::nothrow) usk_plan();
   if (!pl) return fail(USK_ECUDA, "out of host memory");
   pl->n_layers = n_layers;
-  pl->M = P.rows;
+  pl->M = max_rows;
+  pl->Mc.assign(n_cls, P.rows);
+  if (P.class_rows) pl->Mc.assign(P.class_rows, P.class_rows + n_cls);
   pl->gran = P.granularity;
   pl->g = g;
-  pl->C = P.n_classes > 0 ? P.n_classes : (saliency ? 4 : 1);
+  pl->C = n_cls;
   pl->min_cols = P.min_cols;
   pl->hash = P.hash;
   pl->variant = P.variant;

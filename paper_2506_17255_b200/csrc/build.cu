@@ -51,6 +51,7 @@ struct BuildArgs {
   int32_t maxMN;
   HashConsts hc;
   const int32_t* ncols;
+  const uint8_t* nrows;  // M_u per unit (ledger L30: per-class rows; slot rows >= M_u are scratch)
   const int64_t* offsets;
   const uint32_t* ukeys;
   const uint4* R4;  // {R_0, R_1, R_2} mod 2^23 per output row (fast hash, M <= 3)
@@ -245,7 +246,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
     const int ul = UPL * lane + v;
     if (ul >= nu) continue;
     const int64_t u = T.unit_base + j0 + ul;
-    const int mn = M * A.ncols[u];
+    const int mn = (int)A.nrows[u] * A.ncols[u];  // the unit's own rows (<= M)
     const int64_t off = A.offsets[u];
     for (int k = warp; k < mn; k += kConsumers + 1) {
       const uint32_t key = keys[v * stride_v + k * 32 + lane];
@@ -285,7 +286,7 @@ __device__ __forceinline__ void cas_min16(uint16_t* cell, uint32_t key16) {
 }
 
 template <int ES, int HASH>
-__global__ void k_gen_scatter(GenLayer G, const void* W, int32_t layer_M, HashConsts hc,
+__global__ void k_gen_scatter(GenLayer G, const void* W, const uint8_t* nrows, HashConsts hc,
                               const int32_t* ncols, const int64_t* offsets, const uint32_t* ukeys,
                               void* sketch, int* err, uint32_t kap_max) {
   const int64_t n = G.out * G.in;
@@ -303,7 +304,8 @@ __global__ void k_gen_scatter(GenLayer G, const void* W, int32_t layer_M, HashCo
     const uint32_t kap = rotl1(bhi);
     if (kap > kap_max) atomicOr(err, 1);
     const uint32_t Ku = ukeys[u];
-    for (int i = 0; i < layer_M; ++i) {
+    const int Mu = nrows[u];  // the unit's rows (ledger L30)
+    for (int i = 0; i < Mu; ++i) {
       const uint32_t idx = (HASH == USK_HASH_X) ? hash_index_x(hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
       const int64_t c = off + (int64_t)i * N + idx;
       if (ES == 2) {
@@ -549,6 +551,7 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
     A.M = pl->M;
     A.hc = pl->hc;
     A.ncols = pl->d_ncols;
+    A.nrows = pl->d_nrows;
     A.offsets = pl->d_offsets;
     A.ukeys = pl->d_keys;
     A.R4 = pl->d_R4;
@@ -626,10 +629,10 @@ usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* 
   const int64_t n = L.out * L.in;
   const unsigned blocks = (unsigned)std::min<int64_t>((n + T - 1) / T, 148 * 16);
   if (pl->hash == USK_HASH_X)
-    k_gen_scatter<ES, USK_HASH_X><<<blocks, T, 0, st>>>(G, W, pl->M, pl->hc, pl->d_ncols, pl->d_offsets, pl->d_keys,
+    k_gen_scatter<ES, USK_HASH_X><<<blocks, T, 0, st>>>(G, W, pl->d_nrows, pl->hc, pl->d_ncols, pl->d_offsets, pl->d_keys,
                                                         sketch, pl->d_err, kap_max);
   else
-    k_gen_scatter<ES, USK_HASH_IDENTITY><<<blocks, T, 0, st>>>(G, W, pl->M, pl->hc, pl->d_ncols, pl->d_offsets,
+    k_gen_scatter<ES, USK_HASH_IDENTITY><<<blocks, T, 0, st>>>(G, W, pl->d_nrows, pl->hc, pl->d_ncols, pl->d_offsets,
                                                                pl->d_keys, sketch, pl->d_err, kap_max);
   USK_LAUNCHED("k_gen_scatter");
   k_gen_final<ES><<<(unsigned)((L.n_cells + T - 1) / T), T, 0, st>>>(sketch, L.cell_begin, L.n_cells);

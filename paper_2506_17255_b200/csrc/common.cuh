@@ -153,6 +153,7 @@ struct usk_plan {
   // stacked state quantisation (L25): q = 0 (raw states) or 4 / 8 bits
   int32_t q = 0, G = 128;
   int32_t variant = 0;        // usk_variant (comparison variants: generic kernels only)
+  std::vector<int32_t> Mc;    // sketch rows per class (ledger L30); M = max over the classes
   int64_t topk = 0;           // Top-K outliers per layer (0 = none)
   int64_t side_bytes = 0;     // bytes of all outlier side tables (after the cells)
   int64_t n_groups = 0;       // total_cells / G (quantised)

@@ -18,6 +18,7 @@ struct AggArgs {
   int64_t out, in, unit_base, cell_begin;
   int32_t M, gran, g, hash;
   const int32_t* ncols;
+  const uint8_t* nrows;  // M_u per unit (ledger L30)
   const int64_t* offsets;
   const uint32_t* ukeys;
   HashConsts hc;
@@ -41,7 +42,8 @@ __global__ void k_aggregate(AggArgs A) {
     const long long q = __double2ll_rn((double)gv * kFix);
     if (q == 0) continue;
     const uint32_t Ku = A.ukeys[u];
-    for (int i = 0; i < A.M; ++i) {
+    const int Mu = A.nrows[u];
+    for (int i = 0; i < Mu; ++i) {
       const uint32_t idx = A.hash == USK_HASH_X ? hash_index_x(A.hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
       atomicAdd(&A.acc[base + (int64_t)i * N + idx], (unsigned long long)q);  // two's complement sum
     }
@@ -66,7 +68,7 @@ usk_status launch_fixed_accumulate(const usk_plan* pl, int32_t l, const void* va
                                    unsigned long long* acc, int* err, cudaStream_t st) {
   const LayerGeom& L = pl->layers[l];
   AggArgs A{vals, dtype == USK_BF16, L.out, L.in, L.unit_begin, L.cell_begin, pl->M, pl->gran, pl->g,
-            pl->hash, pl->d_ncols, pl->d_offsets, pl->d_keys, pl->hc, acc, err};
+            pl->hash, pl->d_ncols, pl->d_nrows, pl->d_offsets, pl->d_keys, pl->hc, acc, err};
   const int64_t n = L.out * L.in;
   k_aggregate<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, st>>>(A);
   USK_LAUNCHED("k_aggregate");

@@ -9,9 +9,10 @@
 //   k_sort_keys     q_u = floor(s_u / s_max * 2^24); key = (scope << 25) | (2^24 - q_u)
 //   cub radix sort  stable: rank by (q desc, u asc) inside each scope
 //   k_classes       class = floor(rank * C / U_scope); n_c, W_c = sum q_u L_u (u64 atomics, exact)
-//   k_geometry      per scope: N_c = max(min_cols, floor(T W_c / (W n_c M))) with water-filling
+//   k_geometry      per scope: N_c = max(min_cols, floor(T W_c / (W n_c M_c))) with water-filling
 //                   and largest remainder (unsigned __int128)            (one thread / scope)
-//   k_unit_sizes    ncols, nrows, per-unit hash key K_u, size = M * N
+//                   M_c = the class's sketch rows (usk_params.class_rows, ledger L30; else M)
+//   k_unit_sizes    ncols, nrows = M_c, per-unit hash key K_u, size = M_c * N
 //   k_scan_*        device-wide exclusive prefix scan of sizes -> unit offsets
 #include <cub/device/device_radix_sort.cuh>
 
@@ -26,6 +27,11 @@ namespace {
 constexpr int kErrNonFinite = 1;
 constexpr int kErrBudget = 2;
 constexpr int kErrInval = 4;
+
+constexpr int kMaxClasses = 64;
+struct ClassRows {
+  int32_t m[kMaxClasses];  // sketch rows per class
+};
 
 struct PlanDev {
   const int64_t* unit_base;   // [L+1]
@@ -120,8 +126,7 @@ __global__ void k_classes(PlanDev P, int64_t U, const uint64_t* keys_sorted,
 }
 
 // One block (one thread) per scope: proportional share, water-filled floor, largest remainder.
-constexpr int kMaxClasses = 64;
-__global__ void k_geometry(int32_t C, int32_t M, int32_t min_cols, const int64_t* T_scope,
+__global__ void k_geometry(int32_t C, ClassRows Mc, int32_t min_cols, const int64_t* T_scope,
                            const unsigned long long* n_c, const unsigned long long* W_c, int32_t* N_c,
                            int* err) {
   typedef unsigned __int128 u128;
@@ -136,7 +141,7 @@ __global__ void k_geometry(int32_t C, int32_t M, int32_t min_cols, const int64_t
   int32_t* N = N_c + (int64_t)sc * C;
   const int64_t T = T_scope[sc];
   int64_t floor_cells = 0;
-  for (int c = 0; c < C; ++c) floor_cells += (int64_t)n[c] * M * min_cols;
+  for (int c = 0; c < C; ++c) floor_cells += (int64_t)n[c] * Mc.m[c] * min_cols;
   if (floor_cells > T) {
     atomicOr(err, kErrBudget);
     for (int c = 0; c < C; ++c) N[c] = min_cols;
@@ -149,12 +154,12 @@ __global__ void k_geometry(int32_t C, int32_t M, int32_t min_cols, const int64_t
     bool changed = false;
     for (int c = 0; c < C; ++c) {
       if (n[c] == 0) continue;
-      if (active[c]) Wa += W[c]; else Ta -= (int64_t)n[c] * M * min_cols;
+      if (active[c]) Wa += W[c]; else Ta -= (int64_t)n[c] * Mc.m[c] * min_cols;
     }
     for (int c = 0; c < C; ++c) {
       if (!active[c]) continue;
       num[c] = (u128)Ta * W[c];
-      den[c] = Wa * (u128)n[c] * (u128)M;
+      den[c] = Wa * (u128)n[c] * (u128)Mc.m[c];
       Nv[c] = den[c] == 0 ? 0 : (int64_t)(num[c] / den[c]);
       if (Nv[c] < min_cols) { active[c] = false; changed = true; }
     }
@@ -162,7 +167,7 @@ __global__ void k_geometry(int32_t C, int32_t M, int32_t min_cols, const int64_t
   }
   for (int c = 0; c < C; ++c) if (!active[c]) Nv[c] = min_cols;
   int64_t left = T;
-  for (int c = 0; c < C; ++c) left -= (int64_t)n[c] * M * Nv[c];
+  for (int c = 0; c < C; ++c) left -= (int64_t)n[c] * Mc.m[c] * Nv[c];
   // remainder order: (floor(frac * 2^32) desc, c asc), by repeated selection (C <= 64)
   for (int c = 0; c < C; ++c) {
     key[c] = active[c] ? (uint64_t)(((num[c] % den[c]) << 32) / den[c]) : 0;
@@ -174,13 +179,13 @@ __global__ void k_geometry(int32_t C, int32_t M, int32_t min_cols, const int64_t
       if (!done[c] && (best < 0 || key[c] > key[best])) best = c;
     if (best < 0) break;
     done[best] = true;
-    int64_t need = (int64_t)n[best] * M;
+    int64_t need = (int64_t)n[best] * Mc.m[best];
     if (need <= left) { Nv[best] += 1; left -= need; }
   }
   for (int c = 0; c < C; ++c) N[c] = (int32_t)Nv[c];
 }
 
-__global__ void k_unit_sizes(PlanDev P, int64_t U, uint64_t seed, const uint8_t* cls,
+__global__ void k_unit_sizes(PlanDev P, ClassRows Mc, int64_t U, uint64_t seed, const uint8_t* cls,
                              const int32_t* N_c, int32_t* ncols, uint8_t* nrows, uint32_t* ukeys,
                              int64_t* sizes) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -190,8 +195,9 @@ __global__ void k_unit_sizes(PlanDev P, int64_t U, uint64_t seed, const uint8_t*
   int64_t t = (P.gran == USK_GRAN_ROW) ? u - P.unit_base[l] : 0;
   int32_t N = N_c[(int64_t)sc * P.C + cls[u]];
   ncols[u] = N;
-  nrows[u] = (uint8_t)P.M;
-  sizes[u] = (int64_t)P.M * N;
+  const int32_t m = Mc.m[cls[u]];
+  nrows[u] = (uint8_t)m;
+  sizes[u] = (int64_t)m * N;
   ukeys[u] = (uint32_t)splitmix64(seed ^ splitmix64(((uint64_t)(uint32_t)l << 32) | (uint64_t)t));
 }
 
@@ -375,10 +381,12 @@ usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStr
   k_classes<<<blocks_for(U, T256), T256, 0, st>>>(P, U, d_keys2, d_vals2, d_q, d_sbegin, d_sunits, pl->d_cls,
                                                   d_nc, d_Wc);
   USK_LAUNCHED("k_classes");
-  k_geometry<<<(unsigned)n_scopes, 32, 0, st>>>(C, pl->M, pl->min_cols, d_T, d_nc, d_Wc, d_Nc,
+  ClassRows Mc{};
+  for (int c = 0; c < C && c < kMaxClasses; ++c) Mc.m[c] = pl->Mc[c];
+  k_geometry<<<(unsigned)n_scopes, 32, 0, st>>>(C, Mc, pl->min_cols, d_T, d_nc, d_Wc, d_Nc,
                                                       pl->d_err);
   USK_LAUNCHED("k_geometry");
-  k_unit_sizes<<<blocks_for(U, T256), T256, 0, st>>>(P, U, pl->seed, pl->d_cls, d_Nc, pl->d_ncols, pl->d_nrows,
+  k_unit_sizes<<<blocks_for(U, T256), T256, 0, st>>>(P, Mc, U, pl->seed, pl->d_cls, d_Nc, pl->d_ncols, pl->d_nrows,
                                                      pl->d_keys, d_sizes);
   USK_LAUNCHED("k_unit_sizes");
   k_scan_tiles<<<(unsigned)n_tiles, kScanThreads, 0, st>>>(d_sizes, U, d_tiles);

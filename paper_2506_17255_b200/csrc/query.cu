@@ -95,6 +95,7 @@ struct QArgs {
   int64_t rows;         // GEMV: total output rows of the launch
   const void* sketch;
   const int32_t* ncols;
+  const uint8_t* nrows;  // M_u per unit (<= M; ledger L30): staged rows >= M_u hold rho = 0 (neutral)
   const int64_t* offsets;
   const uint32_t* ukeys;
   HashConsts hc;
@@ -220,10 +221,12 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
     const int ul = pa + t;
     int64_t u_off = 0, cu = 0;
     int n = 0;  // N of the thread's unit (0: no unit)
+    int m = 0;  // M_u of the thread's unit: slot rows >= m get rho = 0, the identity of the max
     if (t < pn) {  // overlaps the copy
       cu = A.offsets[ubase + ul];
       u_off = cu - A.offsets[ubase + pa];
       n = A.ncols[ubase + ul];
+      m = A.nrows[ubase + ul];
     }
     __syncthreads();  // shift visible
     mbar_wait(q_bar(), phase);
@@ -233,6 +236,10 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
     if constexpr (QB == 0) {
       const unsigned char* src = raw + qsm[34] + u_off * ES;
       for (int i = 0; i < A.M; ++i, src += n * ES, dst += A.maxN * 32) {  // sketch row i -> slot row i
+        if (i >= m) {
+          for (int k = threadIdx.x / pu; k < n; k += KS) dst[k * 32] = 0u;
+          continue;
+        }
 #pragma unroll 4
         for (int k = threadIdx.x / pu; k < n; k += KS) {
           const uint32_t b = ES == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
@@ -245,6 +252,10 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
       const uint64_t sg0 = reinterpret_cast<const uint64_t*>(qsm + 36)[0];
       const float* sb = reinterpret_cast<const float*>(raw + A.sbuf_off);
       for (int i = 0; i < A.M; ++i, dst += A.maxN * 32) {
+        if (i >= m) {
+          for (int k = threadIdx.x / pu; k < n; k += KS) dst[k * 32] = 0u;
+          continue;
+        }
 #pragma unroll 4
         for (int k = threadIdx.x / pu; k < n; k += KS) {
           const int64_t c = cu + (int64_t)i * n + k;  // global cell
@@ -574,8 +585,9 @@ __device__ __forceinline__ float sketch_value_row(const QArgs& A, const QLayer& 
   const uint32_t N = (uint32_t)A.ncols[u];
   const int64_t off = A.offsets[u];
   const uint32_t Ku = A.ukeys[u];
+  const int Mu = A.nrows[u];
   uint32_t best = 0;
-  for (int i = 0; i < A.M; ++i) {
+  for (int i = 0; i < Mu; ++i) {
     const uint32_t idx = hash_index_x(A.hc, (uint32_t)o, Ku, i, N);
     const int64_t c = off + (int64_t)i * N + idx;
     const uint32_t b = A.es == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(A.sketch)[c] << 16)
@@ -656,6 +668,7 @@ __global__ void __launch_bounds__(kRedThreads, 8) k_gemv_reduce(const __grid_con
 struct GenQ {
   const void* sketch;
   const int32_t* ncols;
+  const uint8_t* nrows;   // M_u per unit (ledger L30)
   const int64_t* offsets;
   const uint32_t* ukeys;
   HashConsts hc;
@@ -693,17 +706,18 @@ __device__ __forceinline__ uint32_t gen_weight_bits_hi(const GenQ& Q, int64_t o,
   const uint32_t N = (uint32_t)Q.ncols[u];
   const int64_t off = Q.offsets[u];
   const uint32_t Ku = Q.ukeys[u];
+  const int Mu = Q.nrows[u];
   if (Q.variant != USK_ABSMAXMIN) {
     // AbsMinMax / CountMin: the bonded cell of MINIMUM |.|, ties -> non-negative = min kappa
     uint32_t best = 0xFFFFFFFFu;
-    for (int i = 0; i < Q.M; ++i) {
+    for (int i = 0; i < Mu; ++i) {
       const uint32_t idx = Q.hash == USK_HASH_X ? hash_index_x(Q.hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
       best = min(best, rotl1(gen_cell_bits(Q, off + (int64_t)i * N + idx)));
     }
     return rotr1(best);
   }
   uint32_t best = 0;
-  for (int i = 0; i < Q.M; ++i) {
+  for (int i = 0; i < Mu; ++i) {
     const uint32_t idx = Q.hash == USK_HASH_X ? hash_index_x(Q.hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
     const int64_t c = off + (int64_t)i * N + idx;
     best = max(best, rotl1(gen_cell_bits(Q, c)) ^ 1u);
@@ -814,7 +828,7 @@ __global__ void k_stats_weights(GenQ Q, const void* W, unsigned long long* count
     const uint32_t N = (uint32_t)Q.ncols[u];
     const uint32_t Ku = Q.ukeys[u];
     const int64_t base = Q.offsets[u] - Q.offsets[Q.unit_base];
-    for (int i = 0; i < Q.M; ++i) {
+    for (int i = 0; i < (int)Q.nrows[u]; ++i) {
       const uint32_t idx = Q.hash == USK_HASH_X ? hash_index_x(Q.hc, (uint32_t)p, Ku, i, N) : (uint32_t)(p % N);
       atomicAdd(&occ[base + (int64_t)i * N + idx], 1);
     }
@@ -1058,6 +1072,7 @@ QArgs base_args(const usk_plan* pl, const void* sketch, int64_t in, const Geom& 
   A.in = in;
   A.sketch = sketch;
   A.ncols = pl->d_ncols;
+  A.nrows = pl->d_nrows;
   A.offsets = pl->d_offsets;
   A.ukeys = pl->d_keys;
   A.hc = pl->hc;
@@ -1167,6 +1182,7 @@ GenQ make_genq(const usk_plan* pl, int32_t l, const void* sketch) {
   GenQ Q{};
   Q.sketch = sketch;
   Q.ncols = pl->d_ncols;
+  Q.nrows = pl->d_nrows;
   Q.offsets = pl->d_offsets;
   Q.ukeys = pl->d_keys;
   Q.hc = pl->hc;

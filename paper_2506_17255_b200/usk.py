@@ -43,7 +43,7 @@ class _Params(ct.Structure):
                 ("dims_per_unit", ct.c_int32), ("n_classes", ct.c_int32), ("min_cols", ct.c_int32),
                 ("hash", ct.c_int32), ("dtype", ct.c_int32), ("seed", ct.c_uint64), ("state_bits", ct.c_int32),
                 ("group_size", ct.c_int32), ("variant", ct.c_int32), ("layer_importance", ct.c_void_p),
-                ("topk", ct.c_int64)]
+                ("topk", ct.c_int64), ("class_rows", ct.c_void_p)]
 
 
 class _PlanInfo(ct.Structure):
@@ -189,17 +189,25 @@ class Plan:
 def plan_allocation(shapes, *, bpw: float, rows: int = 3, granularity: str = "row", dims_per_unit: int = 1,
                     n_classes: int = 0, min_cols: int = 1, hash: str = "x", dtype: str = "bf16", seed: int = 0,
                     saliency=None, state_bits: int = 0, group_size: int = 0, variant: str = "absmaxmin",
-                    layer_importance=None, topk: int = 0, stream=None) -> Plan:
+                    layer_importance=None, topk: int = 0, class_rows=None, stream=None) -> Plan:
     """usk_plan_allocation. saliency: None or list of (None | float32 CUDA tensor [in_features]).
-    state_bits 4 / 8: stacked state quantisation with group_size cells per scale (0 = 128)."""
+    state_bits 4 / 8: stacked state quantisation with group_size cells per scale (0 = 128).
+    class_rows: None or the sketch rows of each importance class (ledger L30)."""
     n = len(shapes)
     arr = (_Shape * n)(*[_Shape(int(o), int(i)) for (o, i) in shapes])
     prm = _Params(float(bpw), rows, GRAN[granularity], dims_per_unit, n_classes, min_cols, HASH[hash],
-                  DTYPE[dtype], seed & (2**64 - 1), state_bits, group_size, VARIANT[variant], None, int(topk))
+                  DTYPE[dtype], seed & (2**64 - 1), state_bits, group_size, VARIANT[variant], None, int(topk), None)
     limp = None
     if layer_importance is not None:  # host doubles, kept alive for the call
         limp = (ct.c_double * n)(*[float(v) for v in layer_importance])
         prm.layer_importance = ct.cast(limp, ct.c_void_p)
+    crows = None
+    if class_rows is not None:  # host int32 [n_classes], kept alive for the call
+        n_cls = n_classes if n_classes > 0 else (4 if saliency is not None else 1)
+        if len(class_rows) != n_cls:
+            raise UskError(1, f"class_rows needs one row count per class ({n_cls})")
+        crows = (ct.c_int32 * len(class_rows))(*[int(v) for v in class_rows])
+        prm.class_rows = ct.cast(crows, ct.c_void_p)
     sal = ct.c_void_p(0)
     keep = None
     if saliency is not None:
