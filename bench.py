@@ -424,37 +424,47 @@ def run_usk(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_ms = float(t.item())
 
-    # ---- the paper's own 0.5-bpw point: a 1/8-rate sketch of 4-bit states (Table 1 "+ q4",
-    #      SURVEY 8(f1)): same workload and grouping, q4 plan (G = 128), measured the same way
-    q4 = None
+    # ---- extra plans on the same workload and grouping, measured the same way:
+    #      * the paper's own 0.5-bpw point: a 1/8-rate sketch of 4-bit states (Table 1 "+ q4",
+    #        SURVEY 8(f1)), q4 plan (G = 128);
+    #      * importance-aware allocation with per-class rows (ledger L30): C = 4
+    #        saliency classes (synth recipe), class rows (3, 3, 2, 2)
+    def extra_point(**kw):
+        xplan = usk.plan_allocation(shapes, bpw=BPW, rows=ROWS, seed=SEED, **kw)
+        xsk = xplan.new_sketch(dev)
+        wq = [synth.torch_weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, l // 7, l % 7), dev)
+              for l in range(L)]
+        usk.build(xplan, wq, xsk)
+        torch.cuda.synchronize()
+        ev0.record()
+        usk.build(xplan, wq, xsk)
+        ev1.record()
+        torch.cuda.synchronize()
+        xbuild_ms = ev0.elapsed_time(ev1)
+        del wq
+        usk.check(xplan)
+        ws_x = [usk.new_batch_workspace(xplan, g, device=dev) for g in groups]
+
+        def step_x():
+            for gi, g in enumerate(groups):
+                usk.linear_batch(xplan, xsk, g, xg[gi], [ys_full[l] for l in g], ws_x[gi])
+
+        gx, lx = capture(step_x)
+        xms = time_steps(gx, step_x, max(20, args.steps // 4), args.warmup)
+        return {"tokens_per_s": 1000.0 / xms, "ms_per_step": xms, "sketch_MB": xplan.sketch_bytes / 1e6,
+                "cells": xplan.info["total_cells"], "achieved_bpw": xplan.info["achieved_bits"] / xplan.info["numel"],
+                "build_ms": xbuild_ms, "launches_per_step": lx}
+
+    q4 = cls = None
     if world == 1 and not args.no_q4:
         del g_rec, g2
         torch.cuda.empty_cache()
-        qplan = usk.plan_allocation(shapes, bpw=BPW, rows=ROWS, seed=SEED, state_bits=4, group_size=128)
-        qsk = qplan.new_sketch(dev)
-        wq = [synth.torch_weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, l // 7, l % 7), dev)
-              for l in range(L)]
-        usk.build(qplan, wq, qsk)
-        torch.cuda.synchronize()
-        ev0.record()
-        usk.build(qplan, wq, qsk)
-        ev1.record()
-        torch.cuda.synchronize()
-        qbuild_ms = ev0.elapsed_time(ev1)
-        del wq
-        usk.check(qplan)
-        ws_q = [usk.new_batch_workspace(qplan, g, device=dev) for g in groups]
-
-        def step_q():
-            for gi, g in enumerate(groups):
-                usk.linear_batch(qplan, qsk, g, xg[gi], [ys_full[l] for l in g], ws_q[gi])
-
-        gq, lq = capture(step_q)
-        qms = time_steps(gq, step_q, max(20, args.steps // 4), args.warmup)
-        q4 = {"tokens_per_s": 1000.0 / qms, "ms_per_step": qms, "state_bits": 4, "group_size": 128,
-              "sketch_MB": qplan.sketch_bytes / 1e6, "cells": qplan.info["total_cells"],
-              "achieved_bpw": qplan.info["achieved_bits"] / qplan.info["numel"], "build_ms": qbuild_ms,
-              "launches_per_step": lq}
+        q4 = extra_point(state_bits=4, group_size=128)
+        q4.update({"state_bits": 4, "group_size": 128})
+        torch.cuda.empty_cache()
+        sal = [torch.from_numpy(synth.saliency_like(i, 500 + l)).to(dev) for l, (o, i) in enumerate(shapes)]
+        cls = extra_point(saliency=sal, n_classes=4, class_rows=(3, 3, 2, 2))
+        cls.update({"n_classes": 4, "class_rows": [3, 3, 2, 2], "saliency": "synth.saliency_like (log-normal, 1% of dims x400)"})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -498,6 +508,8 @@ def run_usk(args):
             line["cpu_baseline"] = cpu
         if q4 is not None:
             line["paper_point_q4"] = q4
+        if cls is not None:
+            line["importance_classes_rows"] = cls
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
