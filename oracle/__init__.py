@@ -24,7 +24,7 @@ LIB = os.path.join(HERE, "liboracle.so")
 F32, BF16 = 0, 1
 ABSMAXMIN, ABSMINMAX, COUNTMIN = 0, 1, 2
 HASH_X, HASH_IDENTITY = 0, 1
-GRAN_ROW, GRAN_LAYER = 0, 1
+GRAN_ROW, GRAN_LAYER, GRAN_OUTROW = 0, 1, 2
 OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE = 0, 1, 2, 3, 4
 
 
@@ -258,13 +258,13 @@ def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None
     outf = np.array([s[0] for s in shapes], dtype=np.int64)
     inf = np.array([s[1] for s in shapes], dtype=np.int64)
     if C is None:
-        C = 4 if saliency is not None else 1
+        C = 4 if saliency is not None and gran != GRAN_OUTROW else 1
     sal_arrays = None
     sal_ptrs = None
     if saliency is not None:
         sal_arrays = [None if s is None else np.ascontiguousarray(s, dtype=np.float32) for s in saliency]
         sal_ptrs = (ct.c_void_p * L)(*[None if a is None else a.ctypes.data for a in sal_arrays])
-    U = int(np.sum(inf // g)) if gran == GRAN_ROW else L
+    U = int(np.sum(inf // g)) if gran == GRAN_ROW else int(np.sum(outf)) if gran == GRAN_OUTROW else L
     unit_base = np.zeros(L + 1, dtype=np.int64)
     cls = np.zeros(max(U, 1), dtype=np.uint8)
     ncols = np.zeros(max(U, 1), dtype=np.int32)

@@ -26,6 +26,8 @@
  *   per-class sketch rows (uo_plan class_rows, uo_allocate Mc, ledger L30) --
  *       pinned (hand-worked allocation, reduction to the uniform plan, conservation, the set-based
  *       enumerator per unit incl. LAYER units, Appendix B's untouched closed form per class).
+ *   output-row units (UO_GRAN_OUTROW, ledger L31) -- pinned (byte-identical to
+ *       input-dim units of W^T, set-based enumerator per unit, accounting, untouched closed form).
  *   uo_importance -- pinned (SPEC Eq. 7 examples, constant activations).
  *   uo_linear_rows -- pinned (numpy fp64 matmul of the oracle-verified W').
  *   uo_aggregate_grad (aggregated-gradient baseline) -- pinned (SPEC example
@@ -55,6 +57,7 @@
 
 #define UO_GRAN_ROW 0
 #define UO_GRAN_LAYER 1
+#define UO_GRAN_OUTROW 2 /* one unit per OUTPUT row o of W [out, in], positions p = j (ledger L31) */
 
 /* sketch variants (Appendix C.2) */
 #define UO_ABSMAXMIN 0 /* the paper's sketch: keep min |.|, retrieve max |.| */
@@ -540,7 +543,10 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
   if (q != 0 && (G < 32 || (G & (G - 1)) != 0)) return UO_EINVAL; /* power of two >= 32 */
   if (!(bpw > 0.0) || !isfinite(bpw)) return UO_EINVAL;
   if (dtype != UO_F32 && dtype != UO_BF16) return UO_EINVAL;
-  if (gran != UO_GRAN_ROW && gran != UO_GRAN_LAYER) return UO_EINVAL;
+  if (gran != UO_GRAN_ROW && gran != UO_GRAN_LAYER && gran != UO_GRAN_OUTROW) return UO_EINVAL;
+  /* output-row units (L31): every unit of a layer has the same score (the saliency is per input
+   * dim, so a row's mean is the layer's mean): one class, one unit per row */
+  if (gran == UO_GRAN_OUTROW && (C != 1 || g != 1)) return UO_EINVAL;
   for (l = 0; l < n_layers; l++) {
     if (outf[l] < 1 || inf[l] < 1) return UO_ESHAPE;
     if (outf[l] * inf[l] > 0xFFFFFFFFll) return UO_ESHAPE; /* positions are 32-bit */
@@ -549,19 +555,19 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
   /* units */
   for (l = 0; l < n_layers; l++) {
     unit_base[l] = U;
-    U += (gran == UO_GRAN_ROW) ? inf[l] / g : 1;
+    U += (gran == UO_GRAN_ROW) ? inf[l] / g : (gran == UO_GRAN_OUTROW) ? outf[l] : 1;
   }
   unit_base[n_layers] = U;
 
-  if (topk < 0 || (topk > 0 && (gran != UO_GRAN_ROW || q != 0))) return UO_EINVAL;
+  if (topk < 0 || (topk > 0 && (gran == UO_GRAN_LAYER || q != 0))) return UO_EINVAL;
   if (layer_imp) {
     /* two-level: one model budget, split over layers first (raw states, ROW units) */
     int64_t numel_l[256], Ul_l[256], budget = 0, meta_sum = 0, numel_all = 0;
     int32_t st;
-    if (gran != UO_GRAN_ROW || q != 0 || n_layers > 256) return UO_EINVAL;
+    if (gran == UO_GRAN_LAYER || q != 0 || n_layers > 256) return UO_EINVAL;
     for (l = 0; l < n_layers; l++) {
       numel_l[l] = outf[l] * inf[l];
-      Ul_l[l] = inf[l] / g;
+      Ul_l[l] = (gran == UO_GRAN_OUTROW) ? outf[l] : inf[l] / g;
       numel_all += numel_l[l];
       meta_sum += (C > 1) ? Ul_l[l] * (int64_t)uo_ceil_log2(C) : 0;
     }
@@ -571,9 +577,9 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
     if (st != UO_OK) return st;
   }
 
-  if (gran == UO_GRAN_ROW) {
+  if (gran != UO_GRAN_LAYER) {
     for (l = 0; l < n_layers; l++) {
-      int64_t Ul = inf[l] / g, t, j;
+      int64_t Ul = (gran == UO_GRAN_OUTROW) ? outf[l] : inf[l] / g, t, j;
       int64_t numel = outf[l] * inf[l];
       int64_t budget = (int64_t)floor(bpw * (double)numel);
       int64_t meta = (C > 1) ? Ul * (int64_t)uo_ceil_log2(C) : 0;
@@ -595,7 +601,8 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       L_u = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)Ul);
       for (t = 0; t < Ul; t++) {
         double s = 0.0;
-        for (j = t * g; j < (t + 1) * g; j++) {
+        const int64_t ja = (gran == UO_GRAN_OUTROW) ? 0 : t * g, jb = (gran == UO_GRAN_OUTROW) ? inf[l] : (t + 1) * g;
+        for (j = ja; j < jb; j++) {
           double v = sal && sal[l] ? (double)sal[l][j] : 1.0;
           if (!(v >= 0.0) || !isfinite(v)) {
             free(s_u);
@@ -604,7 +611,7 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
           }
           s += v;
         }
-        s_u[t] = s / (double)g;
+        s_u[t] = s / (double)(jb - ja);
         L_u[t] = 1; /* common unit length within a layer */
       }
       st = uo_allocate(Ul, s_u, L_u, T, C, Mc, min_cols, cls + unit_base[l], ncols + unit_base[l]);
@@ -760,14 +767,32 @@ static void uo_store(int32_t dtype, void* base, int64_t idx, uint32_t bits) {
     ((uint32_t*)base)[idx] = bits;
 }
 
-static void uo_unit_span(int32_t gran, int32_t g, int64_t in, int64_t t, int64_t* j0, int64_t* j1) {
+/* The weights (o, j) of unit t: o in [o0, o1), j in [j0, j1) (ledgers L6/L31). */
+static void uo_unit_span(int32_t gran, int32_t g, int64_t out, int64_t in, int64_t t, int64_t* o0, int64_t* o1,
+                         int64_t* j0, int64_t* j1) {
+  *o0 = 0;
+  *o1 = out;
+  *j0 = 0;
+  *j1 = in;
   if (gran == UO_GRAN_ROW) {
     *j0 = t * g;
     *j1 = (t + 1) * g;
-  } else {
-    *j0 = 0;
-    *j1 = in;
+  } else if (gran == UO_GRAN_OUTROW) {
+    *o0 = t;
+    *o1 = t + 1;
   }
+}
+
+/* position p of weight (o, j) inside its unit t (the hash input, Eq. 3 "Addr(w)"):
+ * ROW: (j - t g) out + o;  LAYER: j out + o;  OUTROW: j */
+static uint32_t uo_unit_pos(int32_t gran, int32_t g, int64_t out, int64_t t, int64_t o, int64_t j) {
+  if (gran == UO_GRAN_OUTROW) return (uint32_t)j;
+  if (gran == UO_GRAN_ROW) return (uint32_t)((j - t * g) * out + o);
+  return (uint32_t)(j * out + o);
+}
+
+static int64_t uo_unit_of(int32_t gran, int32_t g, int64_t o, int64_t j) {
+  return gran == UO_GRAN_ROW ? j / g : gran == UO_GRAN_OUTROW ? o : 0;
 }
 
 int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, int32_t layer,
@@ -777,20 +802,20 @@ int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, in
   int64_t t;
   for (t = t_begin; t < t_end; t++) {
     const int32_t M = nrows[t]; /* the unit's sketch rows (its class's, ledger L30) */
-    int64_t j0, j1, j, o, n, k = 0;
+    int64_t o0, o1, j0, j1, j, o, n, k = 0;
     uint32_t *wb, *pos, *cells;
     int32_t st;
     int64_t c;
-    uo_unit_span(gran, g, in, t, &j0, &j1);
-    n = (j1 - j0) * out;
+    uo_unit_span(gran, g, out, in, t, &o0, &o1, &j0, &j1);
+    n = (j1 - j0) * (o1 - o0);
     wb = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)n);
     pos = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)n);
     cells = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)M * (size_t)ncols[t]);
-    for (o = 0; o < out; o++) /* stream W in its row-major order */
+    for (o = o0; o < o1; o++) /* stream W in its row-major order */
       for (j = j0; j < j1; j++) {
         if (exclude && exclude[o * in + j]) continue; /* Top-K outliers are stored apart */
         wb[k] = uo_load(dtype, W, o * in + j);
-        pos[k] = (uint32_t)((j - j0) * out + o);
+        pos[k] = uo_unit_pos(gran, g, out, t, o, j);
         k++;
       }
     st = uo_sketch_unit_v(variant, dtype, wb, pos, k, hash_kind, seed, (uint32_t)layer, (uint32_t)t, M,
@@ -809,10 +834,9 @@ static uint32_t uo_weight_at(int32_t dtype, const void* sketch, int64_t out, int
                              int32_t layer, int32_t gran, int32_t g, const int32_t* ncols,
                              const int64_t* offsets, const uint8_t* nrows, int32_t hash_kind, uint64_t seed,
                              int64_t o, int64_t j, int32_t variant) {
-  int64_t t = (gran == UO_GRAN_ROW) ? j / g : 0;
+  int64_t t = uo_unit_of(gran, g, o, j);
   const int32_t M = nrows[t];
-  int64_t j0 = (gran == UO_GRAN_ROW) ? t * g : 0;
-  uint32_t p = (uint32_t)((j - j0) * out + o);
+  uint32_t p = uo_unit_pos(gran, g, out, t, o, j);
   uint32_t N = (uint32_t)ncols[t];
   uint32_t bonded[8];
   int32_t i;
@@ -891,11 +915,11 @@ int32_t uo_aggregate_grad(const double* grad, int64_t out, int64_t in, int32_t l
   const int64_t n_cells = offsets[n_units] - offsets[0];
   int64_t* acc = (int64_t*)calloc((size_t)(n_cells > 0 ? n_cells : 1), sizeof(int64_t));
   for (t = 0; t < n_units; t++) {
-    int64_t j0, j1;
-    uo_unit_span(gran, g, in, t, &j0, &j1);
-    for (o = 0; o < out; o++)
+    int64_t o0, o1, j0, j1;
+    uo_unit_span(gran, g, out, in, t, &o0, &o1, &j0, &j1);
+    for (o = o0; o < o1; o++)
       for (j = j0; j < j1; j++) {
-        const uint32_t p = (uint32_t)((j - j0) * out + o);
+        const uint32_t p = uo_unit_pos(gran, g, out, t, o, j);
         const int64_t q = llrint(grad[o * in + j] * 281474976710656.0); /* 2^48 */
         int32_t i;
         for (i = 0; i < nrows[t]; i++) {
@@ -945,11 +969,11 @@ int32_t uo_stats(int32_t dtype, const void* W, const void* Wp, int64_t out, int6
     }
   }
   for (t = 0; t < n_units; t++) {
-    int64_t j0, j1;
-    uo_unit_span(gran, g, in, t, &j0, &j1);
-    for (o = 0; o < out; o++)
+    int64_t o0, o1, j0, j1;
+    uo_unit_span(gran, g, out, in, t, &o0, &o1, &j0, &j1);
+    for (o = o0; o < o1; o++)
       for (j = j0; j < j1; j++) {
-        const uint32_t p = (uint32_t)((j - j0) * out + o);
+        const uint32_t p = uo_unit_pos(gran, g, out, t, o, j);
         int32_t i;
         for (i = 0; i < nrows[t]; i++)
           occ[offsets[t] - offsets[0] + (int64_t)i * ncols[t] +
