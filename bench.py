@@ -455,7 +455,7 @@ def run_usk(args):
                 "cells": xplan.info["total_cells"], "achieved_bpw": xplan.info["achieved_bits"] / xplan.info["numel"],
                 "build_ms": xbuild_ms, "launches_per_step": lx}
 
-    q4 = cls = None
+    q4 = cls = orow = None
     if world == 1 and not args.no_q4:
         del g_rec, g2
         torch.cuda.empty_cache()
@@ -465,6 +465,9 @@ def run_usk(args):
         sal = [torch.from_numpy(synth.saliency_like(i, 500 + l)).to(dev) for l, (o, i) in enumerate(shapes)]
         cls = extra_point(saliency=sal, n_classes=4, class_rows=(3, 3, 2, 2))
         cls.update({"n_classes": 4, "class_rows": [3, 3, 2, 2], "saliency": "synth.saliency_like (log-normal, 1% of dims x400)"})
+        torch.cuda.empty_cache()
+        orow = extra_point(granularity="outrow")
+        orow.update({"granularity": "outrow (one unit per output row, ledger L31)"})
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -510,6 +513,8 @@ def run_usk(args):
             line["paper_point_q4"] = q4
         if cls is not None:
             line["importance_classes_rows"] = cls
+        if orow is not None:
+            line["output_row_units"] = orow
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -57,8 +57,12 @@ typedef enum {
 typedef enum { USK_F32 = 0, USK_BF16 = 1 } usk_dtype;
 
 /* Sketch-space granularity: ROW = one sketch per input dimension of a
- * weight matrix (per `dims_per_unit` input dims; L6/L7); LAYER = one per matrix. */
-typedef enum { USK_GRAN_ROW = 0, USK_GRAN_LAYER = 1 } usk_granularity;
+ * weight matrix (per `dims_per_unit` input dims; L6/L7); LAYER = one per matrix;
+ * OUTROW = one per OUTPUT row o of the [out, in] matrix, positions p = j ("each row
+ * of the weight matrix corresponds to an independent AbsMaxMin sketch instance"; L31).
+ * OUTROW units all carry the layer's mean saliency, so they form one class (n_classes 0 or 1);
+ * dims_per_unit must be 1.  Its decode runs one kernel per call (no cross-CTA reduction). */
+typedef enum { USK_GRAN_ROW = 0, USK_GRAN_LAYER = 1, USK_GRAN_OUTROW = 2 } usk_granularity;
 
 /* Hash family (Eq. 3; contract in DESIGN.md "Hash contract"):
  * USK_HASH_X = our independent multiply-high family; USK_HASH_IDENTITY = p mod N (SPEC.md:54,

@@ -132,7 +132,10 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   const usk_params& P = *params;
   if (!(P.bpw > 0.0) || !std::isfinite(P.bpw)) return fail(USK_EINVAL, "bpw must be finite and > 0");
   if (P.rows < 1 || P.rows > 8) return fail(USK_EINVAL, "rows must be in [1, 8]");
-  if (P.granularity != USK_GRAN_ROW && P.granularity != USK_GRAN_LAYER) return fail(USK_EINVAL, "granularity");
+  if (P.granularity != USK_GRAN_ROW && P.granularity != USK_GRAN_LAYER && P.granularity != USK_GRAN_OUTROW)
+    return fail(USK_EINVAL, "granularity");
+  if (P.granularity == USK_GRAN_OUTROW && (P.n_classes > 1 || P.dims_per_unit != 1))
+    return fail(USK_EINVAL, "OUTROW units form one class (n_classes 0 or 1) with dims_per_unit 1");
   if (P.hash != USK_HASH_X && P.hash != USK_HASH_IDENTITY) return fail(USK_EINVAL, "hash");
   if (P.dtype != USK_F32 && P.dtype != USK_BF16) return fail(USK_EINVAL, "dtype");
   if (P.min_cols < 1) return fail(USK_EINVAL, "min_cols must be >= 1");
@@ -144,14 +147,14 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   if (P.topk > 0 && (P.granularity != USK_GRAN_ROW || P.state_bits || P.variant != USK_ABSMAXMIN))
     return fail(USK_EINVAL, "topk: ROW granularity, raw states and AbsMaxMin only");
   if (P.layer_importance) {
-    if (P.granularity != USK_GRAN_ROW || P.state_bits)
+    if (P.granularity == USK_GRAN_LAYER || P.state_bits)
       return fail(USK_EINVAL, "layer_importance: ROW granularity with raw states only");
     for (int l = 0; l < n_layers; ++l)
       if (!(P.layer_importance[l] >= 0.0) || !std::isfinite(P.layer_importance[l]))
         return fail(USK_EINVAL, "layer_importance must be finite and >= 0");
   }
   if (P.variant != USK_ABSMAXMIN && P.state_bits) return fail(USK_EUNSUPPORTED, "variants use raw states");
-  const int32_t n_cls = P.n_classes > 0 ? P.n_classes : (saliency ? 4 : 1);
+  const int32_t n_cls = P.n_classes > 0 ? P.n_classes : (saliency && P.granularity != USK_GRAN_OUTROW ? 4 : 1);
   int32_t max_rows = P.rows;
   if (P.class_rows) {  // per-class sketch rows (ledger L30)
     if (P.layer_importance) return fail(USK_EINVAL, "class_rows: not with layer_importance");
@@ -207,11 +210,12 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
     L.out = layers[l].out_features;
     L.in = layers[l].in_features;
     L.unit_begin = U;
-    L.n_units = P.granularity == USK_GRAN_ROW ? L.in / g : 1;
-    L.scope = P.granularity == USK_GRAN_ROW ? l : 0;
+    L.n_units = P.granularity == USK_GRAN_ROW ? L.in / g : P.granularity == USK_GRAN_OUTROW ? L.out : 1;
+    L.scope = P.granularity != USK_GRAN_LAYER ? l : 0;
     U += L.n_units;
     numel_all += L.out * L.in;
     pl->max_out = std::max<int64_t>(pl->max_out, L.out);
+    pl->max_pos = std::max<int64_t>(pl->max_pos, std::max(L.out, L.in));
   }
   pl->U = U;
   pl->numel = numel_all;
@@ -231,7 +235,7 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
       return fail(USK_EBUDGET, "two-level allocation: the layer floors exceed the model budget");
     }
   }
-  if (P.granularity == USK_GRAN_ROW) {
+  if (P.granularity != USK_GRAN_LAYER) {
     for (int l = 0; l < n_layers; ++l) {
       LayerGeom& L = pl->layers[l];
       const int64_t meta = pl->C > 1 ? L.n_units * ceil_log2(pl->C) : 0;
@@ -271,7 +275,7 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   e = e ? e : cudaMalloc(&pl->d_nrows, (size_t)U);
   e = e ? e : cudaMalloc(&pl->d_offsets, sizeof(int64_t) * (U + 1));
   e = e ? e : cudaMalloc(&pl->d_keys, sizeof(uint32_t) * U);
-  e = e ? e : cudaMalloc(&pl->d_R4, sizeof(uint4) * (pl->max_out + 32));
+  e = e ? e : cudaMalloc(&pl->d_R4, sizeof(uint4) * (pl->max_pos + 32));
   e = e ? e : cudaMalloc(&pl->d_err, sizeof(int));
   if (e != cudaSuccess) {
     free_plan(pl);

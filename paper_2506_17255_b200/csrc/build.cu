@@ -294,8 +294,7 @@ __global__ void k_gen_scatter(GenLayer G, const void* W, const uint8_t* nrows, H
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = e / G.in, j = e - o * G.in;
     int64_t t, p;
-    if (G.gran == USK_GRAN_ROW) { t = j / G.g; p = (j - t * G.g) * G.out + o; }
-    else { t = 0; p = j * G.out + o; }
+    unit_pos(G.gran, G.g, G.out, o, j, t, p);
     const int64_t u = G.unit_base + t;
     const uint32_t N = (uint32_t)ncols[u];
     const int64_t off = offsets[u];
@@ -412,8 +411,7 @@ __global__ void k_amx_scatter(GenLayer G, const void* W, int32_t layer_M, HashCo
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = e / G.in, j = e - o * G.in;
     int64_t t, p;
-    if (G.gran == USK_GRAN_ROW) { t = j / G.g; p = (j - t * G.g) * G.out + o; }
-    else { t = 0; p = j * G.out + o; }
+    unit_pos(G.gran, G.g, G.out, o, j, t, p);
     const int64_t u = G.unit_base + t;
     const uint32_t N = (uint32_t)ncols[u];
     const int64_t off = offsets[u];

@@ -49,6 +49,15 @@ __host__ __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   return z ^ (z >> 31);
 }
 
+// unit t (within its layer) and position p of weight (o, j) (L6/L31):
+// ROW: t = j / g, p = (j - t g) out + o;  LAYER: t = 0, p = j out + o;  OUTROW: t = o, p = j
+__host__ __device__ __forceinline__ void unit_pos(int32_t gran, int32_t g, int64_t out, int64_t o, int64_t j,
+                                                  int64_t& t, int64_t& p) {
+  if (gran == USK_GRAN_ROW) { t = j / g; p = (j - t * g) * out + o; }
+  else if (gran == USK_GRAN_OUTROW) { t = o; p = j; }
+  else { t = 0; p = j * out + o; }
+}
+
 __host__ __device__ __forceinline__ uint32_t fmix32(uint32_t h) {
   h ^= h >> 16;
   h *= 0x85EBCA6Bu;
@@ -136,6 +145,7 @@ struct usk_plan {
   uint64_t seed = 0;
   int64_t U = 0, total_cells = 0, numel = 0, budget_bits = 0, achieved_bits = 0;
   int64_t max_out = 0;
+  int64_t max_pos = 0;  // positions covered by d_R4: max over layers of max(out, in) (ROW: p = o, OUTROW: p = j)
   usk::HashConsts hc{};
   std::vector<usk::LayerGeom> layers;
   std::vector<int32_t> h_ncols;    // [U]
@@ -147,7 +157,7 @@ struct usk_plan {
   uint8_t* d_nrows = nullptr;
   int64_t* d_offsets = nullptr;
   uint32_t* d_keys = nullptr;  // K_u per unit
-  uint4* d_R4 = nullptr;       // {R_0, R_1, R_2} mod 2^23 per output row o < max_out (build bulk copies)
+  uint4* d_R4 = nullptr;       // {R_0, R_1, R_2} mod 2^23 per position p < max_pos (build bulk copies, K4o)
   int* d_err = nullptr;        // sticky device error flag
   int device = 0;
   // stacked state quantisation (L25): q = 0 (raw states) or 4 / 8 bits
@@ -185,4 +195,8 @@ usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStr
 usk_status launch_fixed_accumulate(const usk_plan* pl, int32_t l, const void* vals, int32_t dtype,
                                    unsigned long long* acc, int* err, cudaStream_t st);
 bool layer_fast_ok(const usk_plan* pl, int32_t layer);
+bool outrow_fast_ok(const usk_plan* pl, const int32_t* layers, int n);
+usk_status launch_gemv_outrow(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
+                              const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
+                              cudaStream_t st);
 }  // namespace usk

@@ -31,8 +31,7 @@ __global__ void k_aggregate(AggArgs A) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t o = e / A.in, j = e - o * A.in;
     int64_t t, p;
-    if (A.gran == USK_GRAN_ROW) { t = j / A.g; p = (j - t * A.g) * A.out + o; }
-    else { t = 0; p = j * A.out + o; }
+    unit_pos(A.gran, A.g, A.out, o, j, t, p);
     const int64_t u = A.unit_base + t;
     const uint32_t N = (uint32_t)A.ncols[u];
     const int64_t base = A.offsets[u] - A.cell_begin;

@@ -85,7 +85,7 @@ __device__ __forceinline__ void group_add_u64(unsigned long long* dst, unsigned 
 __global__ void k_scope_max(PlanDev P, int64_t U, const double* s_u, unsigned long long* smax) {
   const int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const bool ok = u < U;
-  const int sc = !ok ? -1 : (P.gran == USK_GRAN_ROW) ? find_layer(P.unit_base, P.L, u) : 0;
+  const int sc = !ok ? -1 : (P.gran != USK_GRAN_LAYER) ? find_layer(P.unit_base, P.L, u) : 0;
   const unsigned long long v = ok ? (unsigned long long)__double_as_longlong(s_u[u]) : 0ull;  // s_u >= 0
   group_max_u64(ok ? &smax[sc] : nullptr, (unsigned)sc, v);
 }
@@ -94,7 +94,7 @@ __global__ void k_sort_keys(PlanDev P, int64_t U, const double* s_u, const unsig
                             uint32_t* q, uint64_t* keys, uint32_t* vals) {
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= U) return;
-  int sc = (P.gran == USK_GRAN_ROW) ? find_layer(P.unit_base, P.L, u) : 0;
+  int sc = (P.gran != USK_GRAN_LAYER) ? find_layer(P.unit_base, P.L, u) : 0;
   double mx = __longlong_as_double((long long)smax[sc]);
   uint32_t qu = (mx > 0.0) ? (uint32_t)floor((s_u[u] / mx) * 16777216.0) : 1u;
   q[u] = qu;
@@ -191,8 +191,8 @@ __global__ void k_unit_sizes(PlanDev P, ClassRows Mc, int64_t U, uint64_t seed, 
   int64_t u = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (u >= U) return;
   int l = find_layer(P.unit_base, P.L, u);
-  int sc = (P.gran == USK_GRAN_ROW) ? l : 0;
-  int64_t t = (P.gran == USK_GRAN_ROW) ? u - P.unit_base[l] : 0;
+  int sc = (P.gran != USK_GRAN_LAYER) ? l : 0;
+  int64_t t = (P.gran != USK_GRAN_LAYER) ? u - P.unit_base[l] : 0;
   int32_t N = N_c[(int64_t)sc * P.C + cls[u]];
   ncols[u] = N;
   const int32_t m = Mc.m[cls[u]];
@@ -295,7 +295,7 @@ usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStr
   const int32_t L = pl->n_layers;
   const int64_t U = pl->U;
   const int32_t C = pl->C;
-  const int32_t n_scopes = (pl->gran == USK_GRAN_ROW) ? L : 1;
+  const int32_t n_scopes = (pl->gran != USK_GRAN_LAYER) ? L : 1;
 
   std::vector<int64_t> h_unit_base(L + 1), h_in(L), h_numel(L), h_T(n_scopes), h_sbegin(n_scopes),
       h_sunits(n_scopes);
@@ -306,7 +306,7 @@ usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStr
   }
   h_unit_base[L] = U;
   for (int s = 0; s < n_scopes; ++s) {
-    if (pl->gran == USK_GRAN_ROW) {
+    if (pl->gran != USK_GRAN_LAYER) {
       h_T[s] = pl->layers[s].cells_T;
       h_sbegin[s] = pl->layers[s].unit_begin;
       h_sunits[s] = pl->layers[s].n_units;
@@ -397,7 +397,7 @@ usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStr
   USK_LAUNCHED("k_scan_apply");
   k_scan_last<<<1, 1, 0, st>>>(d_sizes, U, pl->d_offsets);
   USK_LAUNCHED("k_scan_last");
-  k_R4_table<<<blocks_for(pl->max_out, T256), T256, 0, st>>>(pl->hc, pl->max_out, pl->d_R4);
+  k_R4_table<<<blocks_for(pl->max_pos, T256), T256, 0, st>>>(pl->hc, pl->max_pos, pl->d_R4);
   USK_LAUNCHED("k_R4_table");
 
   int h_err = 0;

@@ -700,8 +700,7 @@ __device__ __forceinline__ uint32_t gen_cell_bits(const GenQ& Q, int64_t c) {
 
 __device__ __forceinline__ uint32_t gen_weight_bits_hi(const GenQ& Q, int64_t o, int64_t j) {
   int64_t t, p;
-  if (Q.gran == USK_GRAN_ROW) { t = j / Q.g; p = (j - t * Q.g) * Q.out + o; }
-  else { t = 0; p = j * Q.out + o; }
+  unit_pos(Q.gran, Q.g, Q.out, o, j, t, p);
   const int64_t u = Q.unit_base + t;
   const uint32_t N = (uint32_t)Q.ncols[u];
   const int64_t off = Q.offsets[u];
@@ -822,8 +821,7 @@ __global__ void k_stats_weights(GenQ Q, const void* W, unsigned long long* count
     }
     // occupancy: one count per sketch row
     int64_t t, p;
-    if (Q.gran == USK_GRAN_ROW) { t = j / Q.g; p = (j - t * Q.g) * Q.out + o; }
-    else { t = 0; p = j * Q.out + o; }
+    unit_pos(Q.gran, Q.g, Q.out, o, j, t, p);
     const int64_t u = Q.unit_base + t;
     const uint32_t N = (uint32_t)Q.ncols[u];
     const uint32_t Ku = Q.ukeys[u];
@@ -1224,6 +1222,8 @@ size_t gemv_workspace_bytes(const usk_plan* pl, int32_t l, int64_t o0, int64_t o
 usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
                              const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
                              void* ws, cudaStream_t st) {
+  if (outrow_fast_ok(pl, layers, n))  // output-row units: one kernel, no split-K (outrow.cu)
+    return launch_gemv_outrow(pl, sketch, layers, o0, o1, n, x, x_dtype, y, y_dtype, st);
   std::vector<int64_t> rows(n);
   for (int k = 0; k < n; ++k) rows[k] = o1[k] - o0[k];
   Geom G = fast_eligible(pl) ? gemv_geometry(pl, layers, rows.data(), n) : Geom{};

@@ -16,7 +16,7 @@ LIB_PATH = os.path.join(HERE, "libusk.so")
 
 OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE, ECUDA, EUNSUPPORTED = range(7)
 F32, BF16 = 0, 1
-GRAN = {"row": 0, "layer": 1}
+GRAN = {"row": 0, "layer": 1, "outrow": 2}
 HASH = {"x": 0, "identity": 1}
 VARIANT = {"absmaxmin": 0, "absminmax": 1, "countmin": 2}
 STATS_KEYS = ("weights", "untouched", "sign_errors", "zero_weights", "rel_exact", "rel_lt_1e-3", "rel_1e-3",
@@ -203,7 +203,7 @@ def plan_allocation(shapes, *, bpw: float, rows: int = 3, granularity: str = "ro
         prm.layer_importance = ct.cast(limp, ct.c_void_p)
     crows = None
     if class_rows is not None:  # host int32 [n_classes], kept alive for the call
-        n_cls = n_classes if n_classes > 0 else (4 if saliency is not None else 1)
+        n_cls = n_classes if n_classes > 0 else (4 if saliency is not None and granularity != "outrow" else 1)
         if len(class_rows) != n_cls:
             raise UskError(1, f"class_rows needs one row count per class ({n_cls})")
         crows = (ct.c_int32 * len(class_rows))(*[int(v) for v in class_rows])

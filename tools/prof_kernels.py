@@ -21,10 +21,11 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--bpw", type=float, default=0.5)
 ap.add_argument("--prefill", action="store_true")
+ap.add_argument("--gran", default="row")
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 shapes = synth.llama_block(2048, 512, 8192)
-pl = usk.plan_allocation(shapes, bpw=args.bpw, rows=3, seed=0x5EED000000000003)
+pl = usk.plan_allocation(shapes, bpw=args.bpw, rows=3, seed=0x5EED000000000003, granularity=args.gran)
 sk = pl.new_sketch(dev)
 ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, 0, k), dev) for k, (o, i) in enumerate(shapes)]
 torch.cuda.synchronize()
