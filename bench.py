@@ -469,6 +469,55 @@ def run_usk(args):
         orow = extra_point(granularity="outrow")
         orow.update({"granularity": "outrow (one unit per output row, ledger L31)"})
 
+    # ---- BASELINE config 5 at N = 1: Llama-3-8B-shaped linears (224, 6.98 G weights, 13.96 GB bf16)
+    #      at 0.5 bpw -- the build of all layers in one call, and the batch-1 decode token as 128
+    #      grouped calls in one CUDA graph (the 436 MB sketch exceeds L2: it streams from HBM)
+    c5 = None
+    if world == 1 and not args.no_8b:
+        torch.cuda.empty_cache()
+        shapes8 = synth.llama3_8b_shapes()
+        L8 = len(shapes8)
+        plan8 = usk.plan_allocation(shapes8, bpw=BPW, rows=ROWS, seed=SEED)
+        sk8 = plan8.new_sketch(dev)
+        w8 = [synth.torch_weights_bf16(o, i, synth.seed_for(5, l // 7, l % 7), dev) for l, (o, i) in enumerate(shapes8)]
+        usk.build(plan8, w8, sk8)
+        bt = []
+        for _ in range(3):
+            flush.fill_(3)
+            torch.cuda.synchronize()
+            ev0.record()
+            usk.build(plan8, w8, sk8)
+            ev1.record()
+            torch.cuda.synchronize()
+            bt.append(ev0.elapsed_time(ev1))
+        b8_ms = float(np.median(bt))
+        del w8
+        torch.cuda.empty_cache()
+        usk.check(plan8)
+        groups8 = []
+        for blk in range(L8 // 7):
+            base = 7 * blk
+            groups8 += [[base, base + 1, base + 2], [base + 3], [base + 4, base + 5], [base + 6]]
+        x8 = [synth.torch_vector(shapes8[g[0]][1], 2000 + gi, dev, torch.bfloat16)[0] for gi, g in enumerate(groups8)]
+        y8 = [torch.empty(o, dtype=torch.float32, device=dev) for o, i in shapes8]
+        ws8 = [usk.new_batch_workspace(plan8, g, device=dev) for g in groups8]
+
+        def step8():
+            for gi, g in enumerate(groups8):
+                usk.linear_batch(plan8, sk8, g, x8[gi], [y8[l] for l in g], ws8[gi])
+
+        g8, l8 = capture(step8)
+        ms8 = time_steps(g8, step8, max(20, args.steps // 4), args.warmup)
+        n8 = sum(o * i for o, i in shapes8)
+        c5 = {"workload": "c5 at N=1: Llama-3-8B-shaped 224 linears, 0.5 bpw, M=3",
+              "decode_tokens_per_s": 1000.0 / ms8, "decode_ms_per_step": ms8,
+              "decode_weights_per_s": n8 * 1000.0 / ms8, "launches_per_step": l8,
+              "build_ms": b8_ms, "build_GB_per_s": n8 * (2 + BPW / 8) / (b8_ms * 1e-3) / 1e9,
+              "build_hbm_frac": n8 * (2 + BPW / 8) / (b8_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
+              "sketch_MB": plan8.sketch_bytes / 1e6, "weights": n8}
+        del sk8, plan8, ws8, y8, x8, g8
+        torch.cuda.empty_cache()
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cpu = oracle_decode_sample(shapes, host_block0_weights(shapes), budget_s=args.cpu_budget)
@@ -515,6 +564,8 @@ def run_usk(args):
             line["importance_classes_rows"] = cls
         if orow is not None:
             line["output_row_units"] = orow
+        if c5 is not None:
+            line["llama3_8b_n1"] = c5
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -529,7 +580,8 @@ def main():
     ap.add_argument("--impl", default="usk", choices=["usk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
-    ap.add_argument("--no-q4", action="store_true", help="skip the q4-state (paper 0.5-bpw point) extra")
+    ap.add_argument("--no-q4", action="store_true", help="skip the extra plans (q4 states, classes, output-row units)")
+    ap.add_argument("--no-8b", action="store_true", help="skip the Llama-3-8B (config 5) build + decode at N=1")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
