@@ -51,9 +51,10 @@ d = launches.summarise(os.path.join(OUT, "launches_bench.csv"))
 tot = sum(sum(v) for v in d.values())
 with open(os.path.join(PROF, f"{args.tag}_launches_bench.txt"), "w") as f:
     f.write("# ncu --metrics gpu__time_duration.sum --clock-control none of `python bench.py --steps 3 --warmup 3 "
-            "--no-cpu-baseline` (whole process: plan, 4 builds, warm-up + timed decode graphs, per-linear graphs,\n"
-            "# isolated per-call timing, 112 reconstructs, e2e).  Per-launch times are cold-cache and serialised by "
-            "ncu; the shares, not the absolutes, compare with the bench.\n")
+            "--no-cpu-baseline` (whole process: plans, builds, warm-up + timed decode graphs, per-linear graphs,\n"
+            "# isolated per-call timing, 112 reconstructs, e2e, then the extra plans: q4 states, importance classes\n"
+            "# with per-class rows, output-row units, Llama-3-8B at N=1).  Per-launch times are cold-cache and\n"
+            "# serialised by ncu; the shares, not the absolutes, compare with the bench.\n")
     f.write(f"{'kernel':36s} {'n':>5s} {'mean_us':>10s} {'total_us':>11s} {'share':>6s}\n")
     for k, v in d.items():
         f.write(f"{k:36s} {len(v):5d} {sum(v) / len(v):10.2f} {sum(v):11.2f} {sum(v) / tot:6.1%}\n")
