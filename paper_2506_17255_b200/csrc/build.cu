@@ -21,6 +21,7 @@
 // kept in place in the sketch buffer (32-bit atomicMin for fp32 cells, 16-bit CAS for bf16),
 // then converted to states.
 #include <algorithm>
+#include <type_traits>
 
 #include <cub/device/device_radix_sort.cuh>
 
@@ -505,9 +506,11 @@ int fast_upl(const usk_plan* pl, int32_t l) {
   // units per lane for the fast kernels, 0 = not eligible: the largest UPL whose key array and
   // stage ring fit one CTA (one CTA per SM is enough: 17 warps, bulk-copy ring in flight)
   const LayerGeom& L = pl->layers[l];
-  if (pl->gran != USK_GRAN_ROW || pl->g != 1 || pl->variant != USK_ABSMAXMIN) return 0;
+  // output-row units (L31) build as input-dim units of W^T (the same sketch bytes, L31)
+  const bool outrow = pl->gran == USK_GRAN_OUTROW;
+  if ((pl->gran != USK_GRAN_ROW && !outrow) || pl->g != 1 || pl->variant != USK_ABSMAXMIN) return 0;
   const int es = pl->cell_bytes();
-  if ((L.in * es) % 16 != 0) return 0;
+  if (((outrow ? L.out : L.in) * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
   const int S = es == 2 ? 6 : 4;
   auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 16 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
@@ -562,11 +565,12 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
       const LayerGeom& L = pl->layers[group[k].first];
       BuildTask& t = A.task[A.n_tasks++];
       t.W = group[k].second;
-      t.out = L.out;
-      t.in = L.in;
+      const bool outrow = pl->gran == USK_GRAN_OUTROW;  // W is W^T [in, out] here
+      t.out = outrow ? L.in : L.out;
+      t.in = outrow ? L.out : L.in;
       t.unit_base = L.unit_begin;
       t.tile_begin = tiles;
-      tiles += (int)((L.in + TJ - 1) / TJ);
+      tiles += (int)((t.in + TJ - 1) / TJ);
       maxmn = std::max(maxmn, pl->M * L.max_ncols);
     }
     A.maxMN = maxmn;
@@ -642,26 +646,80 @@ usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* 
 
 bool layer_fast_ok(const usk_plan* pl, int32_t l) { return fast_upl(pl, l) != 0; }
 
+// W^T of a row-major [rows, cols] matrix of ES-byte elements (32 x 32 tiles through shared memory)
+template <int ES>
+__global__ void k_transpose(const void* src, void* dst, int64_t rows, int64_t cols) {
+  using T = typename std::conditional<ES == 2, uint16_t, uint32_t>::type;
+  __shared__ T tile[32][33];
+  const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
+  const T* S = reinterpret_cast<const T*>(src);
+  T* D = reinterpret_cast<T*>(dst);
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t r = r0 + i, c = c0 + threadIdx.x;
+    if (r < rows && c < cols) tile[i][threadIdx.x] = S[r * cols + c];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += blockDim.y) {
+    const int64_t c = c0 + i, r = r0 + threadIdx.x;
+    if (r < rows && c < cols) D[c * rows + r] = tile[threadIdx.x][i];
+  }
+}
+
 static usk_status launch_build_raw(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids,
                                    int32_t n, void* sketch, cudaStream_t st, uint32_t kap_max = 0xFEFFFFFFu) {
   std::vector<std::pair<int32_t, const void*>> grp[5];  // by units per lane (1, 2, 4)
+  std::vector<std::pair<int32_t, const void*>> tgrp[5];  // output-row units: built from W^T
   for (int32_t k = 0; k < n; ++k) {
     const int32_t l = layer_ids ? layer_ids[k] : k;
     const int upl = fast_upl(pl, l);
     if (upl) {
-      grp[upl].push_back({l, weights[k]});
+      (pl->gran == USK_GRAN_OUTROW ? tgrp : grp)[upl].push_back({l, weights[k]});
     } else {
       usk_status s = pl->dtype == USK_BF16 ? launch_generic_t<2>(pl, l, weights[k], sketch, st, kap_max)
                                             : launch_generic_t<4>(pl, l, weights[k], sketch, st, kap_max);
       if (s != USK_OK) return s;
     }
   }
+  usk_status s = USK_OK;
   for (int upl : {4, 2, 1}) {
-    if (grp[upl].empty()) continue;
-    usk_status s = launch_fast(pl, upl, grp[upl], sketch, st, kap_max);
-    if (s != USK_OK) return s;
+    if (grp[upl].empty() || s != USK_OK) continue;
+    s = launch_fast(pl, upl, grp[upl], sketch, st, kap_max);
   }
-  return USK_OK;
+  // output-row units (L31): transpose batches of layers (<= 64 MB, or one layer) into a stream-ordered
+  // scratch buffer and build them as input-dim units of W^T; stream order serialises the batches
+  const int es = pl->cell_bytes();
+  const size_t cap = (size_t)64 << 20;
+  for (int upl : {4, 2, 1}) {
+    auto& tg = tgrp[upl];
+    for (size_t a = 0; a < tg.size() && s == USK_OK;) {
+      size_t b = a, bytes = 0;
+      while (b < tg.size()) {
+        const LayerGeom& L = pl->layers[tg[b].first];
+        const size_t lb = ((size_t)(L.out * L.in * es) + 255) / 256 * 256;
+        if (b > a && bytes + lb > cap) break;
+        bytes += lb;
+        ++b;
+      }
+      char* wt = nullptr;
+      USK_CUDA(cudaMallocAsync(&wt, bytes, st));
+      std::vector<std::pair<int32_t, const void*>> batch;
+      size_t off = 0;
+      for (size_t k = a; k < b; ++k) {
+        const LayerGeom& L = pl->layers[tg[k].first];
+        const dim3 grid((unsigned)((L.in + 31) / 32), (unsigned)((L.out + 31) / 32));
+        if (es == 2) k_transpose<2><<<grid, dim3(32, 8), 0, st>>>(tg[k].second, wt + off, L.out, L.in);
+        else k_transpose<4><<<grid, dim3(32, 8), 0, st>>>(tg[k].second, wt + off, L.out, L.in);
+        USK_LAUNCHED("k_transpose");
+        batch.push_back({tg[k].first, wt + off});
+        off += ((size_t)(L.out * L.in * es) + 255) / 256 * 256;
+      }
+      s = launch_fast(pl, upl, batch, sketch, st, kap_max);
+      cudaError_t e = cudaFreeAsync(wt, st);
+      if (s == USK_OK && e != cudaSuccess) s = cuda_fail(e, "usk_build: cudaFreeAsync");
+      a = b;
+    }
+  }
+  return s;
 }
 
 // Quantised plans (L25): raw states are built into a stream-ordered temporary buffer
