@@ -20,7 +20,11 @@
 // Generic path (LAYER granularity, dims_per_unit > 1, odd shapes, oversize units): keys are
 // kept in place in the sketch buffer (32-bit atomicMin for fp32 cells, 16-bit CAS for bf16),
 // then converted to states.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <mutex>
 #include <type_traits>
 
 #include <cub/device/device_radix_sort.cuh>
@@ -37,7 +41,8 @@ constexpr int kBuildThreads = 32 * (kConsumers + 1);
 constexpr int kMaxTasks = 48;
 constexpr size_t kSmemLimit = 227 * 1024;
 
-struct BuildTask {
+struct alignas(64) BuildTask {
+  CUtensorMap map;     // W as a 2-D tensor [out rows, in cols], box = 32 rows x TJ units (TMA tiles)
   const void* W;
   int64_t out, in;
   int64_t unit_base;   // global unit id of the layer's first unit
@@ -118,21 +123,23 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
 
   if (warp == 0) {
     // ---------------- producer: bulk-copy weight row segments into the ring
-    const E* W = reinterpret_cast<const E*>(T.W);
-    const uint32_t segb = (uint32_t)nu * ES;
-    for (int64_t it = 0; it < n_it; ++it) {
-      const int s = (int)(it % S);
-      if (it >= S) mbar_wait(&empty[s], (uint32_t)((it / S) - 1) & 1u);
-      const int64_t o0 = it * kRO;
-      const int rows = (int)min((int64_t)kRO, T.out - o0);
-      uint8_t* st = stages + s * STAGEB;
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&full[s], (uint32_t)rows * (16u + segb));
+    // one 2-D TMA tile per stage (32 rows x TJ units; rows past `out` and units past `in` are
+    // zero-filled) plus one bulk copy of the rows' position mixes
+    if (lane == 0) {
+      for (int64_t it = 0; it < n_it; ++it) {
+        const int s = (int)(it % S);
+        if (it >= S) mbar_wait(&empty[s], (uint32_t)((it / S) - 1) & 1u);
+        const int64_t o0 = it * kRO;
+        const int rows = (int)min((int64_t)kRO, T.out - o0);
+        uint8_t* st = stages + s * STAGEB;
+        mbar_arrive_expect_tx(&full[s], (uint32_t)rows * 16u + (uint32_t)(kRO * ROWB));
         bulk_g2s(st, A.R4 + o0, (uint32_t)rows * 16u, &full[s]);  // the rows' position mixes
+        asm volatile(
+            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+                smem_u32(st + kRO * 16)),
+            "l"(reinterpret_cast<uint64_t>(&T.map)), "r"((int)j0), "r"((int)o0), "r"(smem_u32(&full[s]))
+            : "memory");
       }
-      __syncwarp();
-      for (int r = lane; r < rows; r += 32)
-        bulk_g2s(st + kRO * 16 + r * ROWB, W + (o0 + r) * T.in + j0, segb, &full[s]);
     }
   } else {
     // ---------------- consumers: warp cw takes rows cw and cw + 16 of every stage
@@ -502,6 +509,32 @@ __global__ void k_topk_finish(const uint32_t* idx, int64_t K, const void* W, int
 }
 
 // ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// W [rows, cols] row-major of es-byte elements; box = 32 rows x tj columns, no swizzle, zero fill
+bool make_w_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int es, int tj) {
+  auto fn = encode_tiled();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)cols * es};
+  cuuint32_t box[2] = {(cuuint32_t)tj, (cuuint32_t)kRO};
+  cuuint32_t estr[2] = {1, 1};
+  return fn(m, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
+            dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int fast_upl(const usk_plan* pl, int32_t l) {
   // units per lane for the fast kernels, 0 = not eligible: the largest UPL whose key array and
   // stage ring fit one CTA (one CTA per SM is enough: 17 warps, bulk-copy ring in flight)
@@ -565,6 +598,9 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
       const LayerGeom& L = pl->layers[group[k].first];
       BuildTask& t = A.task[A.n_tasks++];
       t.W = group[k].second;
+      const bool outrow_t = pl->gran == USK_GRAN_OUTROW;
+      if (!make_w_map(&t.map, t.W, outrow_t ? L.in : L.out, outrow_t ? L.out : L.in, pl->cell_bytes(), TJ))
+        return fail(USK_ECUDA, "usk_build: cuTensorMapEncodeTiled failed");
       const bool outrow = pl->gran == USK_GRAN_OUTROW;  // W is W^T [in, out] here
       t.out = outrow ? L.in : L.out;
       t.in = outrow ? L.out : L.in;
