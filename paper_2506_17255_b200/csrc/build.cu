@@ -146,7 +146,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
     const int cw = warp - 1;
     constexpr bool FAST = MT > 0 && HASH == USK_HASH_X;  // short-unit FFMA.RZ form
     constexpr int KR = FAST ? MT : 1;
-    uint32_t K[UPL], N[UPL], vmask[UPL];
+    uint32_t K[UPL], N[UPL];
     uint32_t rb[UPL][FAST ? 1 : MR];  // generic: byte offsets of (unit v, sketch row i) for this lane
     uint32_t fk[UPL][KR], cb[UPL][KR];  // fast: FFMA key and addend of (unit v, sketch row i)
     float Nf[UPL];
@@ -161,7 +161,6 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       // zero candidate, so the loop below needs no branch
       N[v] = valid ? (uint32_t)A.ncols[u] : 1u;
       Nf[v] = (float)(4u * N[v]);
-      vmask[v] = valid ? ~0u : 0u;
       if constexpr (FAST) {
 #pragma unroll
         for (int i = 0; i < MT; ++i) {
@@ -176,9 +175,10 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       }
     }
     uint32_t kmax = 0;
+    int s = 0;
+    uint32_t ph = 0;
     for (int64_t it = 0; it < n_it; ++it) {
-      const int s = (int)(it % S);
-      mbar_wait(&full[s], (uint32_t)(it / S) & 1u);
+      mbar_wait(&full[s], ph);
       const uint8_t* st = stages + s * STAGEB;
       const int64_t o0 = it * kRO;
       const int rows = (int)min((int64_t)kRO, T.out - o0);
@@ -219,7 +219,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
           const uint32_t R23[3] = {R4.x, R4.y, R4.z};
 #pragma unroll
           for (int v = 0; v < UPL; ++v) {
-            const uint32_t kap = rotl1(bits[v] & vmask[v]);
+            const uint32_t kap = rotl1(bits[v]);  // missing units: zero-filled by the tensor copy
             kmax = max(kmax, kap);
 #pragma unroll
             for (int i = 0; i < MT; ++i) key_min(short_fma_bits(R23[i], fk[v][i], Nf[v], cb[v][i]) * 128u + kbase, kap);
@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
         } else {
 #pragma unroll
           for (int v = 0; v < UPL; ++v) {
-            const uint32_t kap = rotl1(bits[v] & vmask[v]);
+            const uint32_t kap = rotl1(bits[v]);  // missing units: zero-filled by the tensor copy
             kmax = max(kmax, kap);
 #pragma unroll
             for (int i = 0; i < MR; ++i) {
@@ -242,6 +242,10 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++s == S) {
+        s = 0;
+        ph ^= 1u;
+      }
     }
     if (kmax > A.kap_max) atomicOr(A.err, 1);  // NaN / Inf weight (USK_ENONFINITE)
   }
