@@ -35,7 +35,10 @@
 namespace usk {
 namespace {
 
-constexpr int kRO = 32;         // weight rows per stage
+#ifndef USK_BUILD_ROWS
+#define USK_BUILD_ROWS 64
+#endif
+constexpr int kRO = USK_BUILD_ROWS;  // weight rows per stage (each consumer warp takes kRO / 16 of them)
 constexpr int kConsumers = 16;  // consumer warps (2 rows of every stage each)
 constexpr int kBuildThreads = 32 * (kConsumers + 1);
 constexpr int kMaxTasks = 48;
@@ -67,7 +70,7 @@ struct BuildArgs {
 };
 
 template <int ES>
-constexpr int stages_for() { return ES == 2 ? 6 : 4; }
+constexpr int stages_for() { return (ES == 2 ? 6 : 4) * 32 / kRO; }
 
 template <typename E, int UPL>
 constexpr int stage_bytes() { return kRO * 16 + kRO * 32 * UPL * (int)sizeof(E); }
@@ -549,7 +552,7 @@ int fast_upl(const usk_plan* pl, int32_t l) {
   const int es = pl->cell_bytes();
   if (((outrow ? L.out : L.in) * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
-  const int S = es == 2 ? 6 : 4;
+  const int S = (es == 2 ? 6 : 4) * 32 / kRO;
   auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 16 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
   for (int upl : {4, 2, 1})
     if (smem(upl) <= (int64_t)kSmemLimit) return upl;
