@@ -36,6 +36,9 @@
 namespace usk {
 namespace {
 
+#ifndef USK_QUERY_LOPADDR
+#define USK_QUERY_LOPADDR 1
+#endif
 #ifndef USK_QUERY_THREADS
 #define USK_QUERY_THREADS 512
 #endif
@@ -130,7 +133,21 @@ struct LaneState {
   uint32_t fk[UPL][KR], cb[UPL][KR];
   float Nf[UPL];
   uint32_t B;
+#if USK_QUERY_LOPADDR
+  // M = 3: sketch row 2 takes its address from an ALU-pipe LOP3 instead of an FMA-pipe IMAD (the two
+  // pipes then carry 6 + 6 of the 15 instructions per 32 weights): FFMA.RZ(f, 128 N, 2^23 + B2 - 128 N)
+  // rounds to 2^23 + B2 + floor(128 k N / 2^23) (ulp 1), and masking its mantissa to bits 7..22 leaves
+  // B2 + 128 idx; cb[v][2] holds those addend bits, B2 = the 128-aligned byte address of the slot row
+  float Nf128[UPL];
+  uint32_t L4;  // 4 * lane (the cells start 128-B aligned)
+#endif
 };
+
+// the rho cells start at a 128-B aligned shared address (row 2's LOP3 address keeps the lane bits)
+__device__ __forceinline__ uint32_t* q_cells() {
+  const uint32_t a = smem_u32(qsm + kCellsWordOffset);
+  return qsm + kCellsWordOffset + ((128u - (a & 127u)) & 127u) / 4u;
+}
 
 // shared memory: [zero cells: 32 words][mbarrier: 2 words][copy shift: 1 word]...[per-warp R tables
 // @ word kRTabWordOffset][cells @ word kCellsWordOffset: UPL*32*maxMN words][raw bulk-copy buffer:
@@ -142,8 +159,11 @@ __device__ __forceinline__ uint64_t* q_bar() { return reinterpret_cast<uint64_t*
 template <int UPL, int MT, int HASH>
 __device__ __forceinline__ void lane_setup(const QArgs& A, int64_t ubase, int nu, LaneState<UPL, MT, HASH>& S) {
   const int lane = threadIdx.x & 31;
-  const uint32_t cbase = smem_u32(qsm + kCellsWordOffset);
+  const uint32_t cbase = smem_u32(q_cells());
   S.B = cbase + 4u * (uint32_t)lane;  // (0x4C000000 << 7) wraps to 0
+#if USK_QUERY_LOPADDR
+  S.L4 = 4u * (uint32_t)lane;
+#endif
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
     const int ul = UPL * lane + v;
@@ -164,13 +184,20 @@ __device__ __forceinline__ void lane_setup(const QArgs& A, int64_t ubase, int nu
         S.fk[v][i] = short_fkey(row_key(S.K[v], A.hc.kap[i]));
         S.cb[v][i] = short_cbits(S.N[v], valid ? (uint32_t)(v * A.maxMN + i * A.maxN) : (uint32_t)(i * A.maxN + A.maxN - 1));
       }
+#if USK_QUERY_LOPADDR
+      if constexpr (MT == 3) {
+        const uint32_t off2 = valid ? (uint32_t)(v * A.maxMN + 2 * A.maxN) : (uint32_t)(3 * A.maxN - 1);
+        S.Nf128[v] = (float)(128u * S.N[v]);
+        S.cb[v][2] = __float_as_uint((float)(8388608u + cbase + 128u * off2 - 128u * S.N[v]));  // exact (< 2^24)
+      }
+#endif
     }
   }
 }
 
 template <typename E, int UPL>
 __device__ __forceinline__ unsigned char* q_raw(const QArgs& A) {
-  return reinterpret_cast<unsigned char*>(qsm + kCellsWordOffset + UPL * 32 * A.maxMN);
+  return reinterpret_cast<unsigned char*>(q_cells() + UPL * 32 * A.maxMN);
 }
 
 // thread 0: bulk copy of the cells of units [ubase + pa, ubase + pa + pn) into the raw buffer.
@@ -211,7 +238,7 @@ template <typename E, int UPL, int QB>
 __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int nu, uint32_t& phase,
                                             bool first_issued) {
   constexpr int ES = sizeof(E);
-  uint32_t* cells = qsm + kCellsWordOffset;
+  uint32_t* cells = q_cells();
   const unsigned char* raw = q_raw<E, UPL>(A);
   const int pu = A.piece_units;
   for (int pa = 0; pa < nu; pa += pu) {
@@ -279,7 +306,7 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
 // kernel prologue shared by the fast kernels: zero column of every slot row, staging mbarrier
 template <int UPL>
 __device__ __forceinline__ void q_prologue(const QArgs& A) {
-  uint32_t* cells = qsm + kCellsWordOffset;
+  uint32_t* cells = q_cells();
   for (int e = threadIdx.x; e < UPL * A.M * 32; e += kQThreads) {
     const int lane = e & 31, vi = e >> 5, v = vi % UPL, i = vi / UPL;
     cells[v * 32 * A.maxMN + (i * A.maxN + A.maxN - 1) * 32 + lane] = 1u;  // rho(+0)
@@ -297,8 +324,19 @@ __device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<U
   if constexpr (fast_hash<MT, HASH>()) {
     const uint32_t Ri[3] = {R.x, R.y, R.z};
     uint32_t m[MT];
+#if USK_QUERY_LOPADDR
+    if constexpr (MT == 3) {
+      m[0] = lds_at(short_fma_bits(Ri[0], S.fk[v][0], S.Nf[v], S.cb[v][0]) * 128u + S.B);
+      m[1] = lds_at(short_fma_bits(Ri[1], S.fk[v][1], S.Nf[v], S.cb[v][1]) * 128u + S.B);
+      uint32_t a2;  // (bits & 0x7FFF80) | lane bits: one LOP3
+      asm("lop3.b32 %0, %1, 0x7FFF80, %2, 0xEA;" : "=r"(a2) : "r"(short_fma_bits(Ri[2], S.fk[v][2], S.Nf128[v], S.cb[v][2])), "r"(S.L4));
+      m[2] = lds_at(a2);
+    } else
+#endif
+    {
 #pragma unroll
-    for (int i = 0; i < MT; ++i) m[i] = lds_at(short_fma_bits(Ri[i], S.fk[v][i], S.Nf[v], S.cb[v][i]) * 128u + S.B);
+      for (int i = 0; i < MT; ++i) m[i] = lds_at(short_fma_bits(Ri[i], S.fk[v][i], S.Nf[v], S.cb[v][i]) * 128u + S.B);
+    }
     uint32_t best = m[0];
 #pragma unroll
     for (int i = 1; i < MT; ++i) best = max(best, m[i]);
@@ -882,7 +920,7 @@ size_t sbuf_bytes(int maxMN, int q, int g_shift, int pu) {
 
 // [zero + mbarrier + copy bases][rho cells][raw bulk-copy buffer for `pu` units][scales]
 size_t smem_bytes(int upl, int maxMN, int es, int pu, int q = 0, int g_shift = 7) {
-  return kCellsWordOffset * 4 + (size_t)32 * upl * maxMN * 4 + (raw_bytes(maxMN, es, q, pu) + 15) / 16 * 16 +
+  return kCellsWordOffset * 4 + 128 + (size_t)32 * upl * maxMN * 4 + (raw_bytes(maxMN, es, q, pu) + 15) / 16 * 16 +
          sbuf_bytes(maxMN, q, g_shift, pu);
 }
 
