@@ -10,6 +10,7 @@ cp -r bench.py synth oracle include tools "$D"/
 mkdir -p "$D/paper_2506_17255_b200"
 cp -r paper_2506_17255_b200/*.py paper_2506_17255_b200/csrc "$D/paper_2506_17255_b200/"
 [ -n "$VARIANT_QUERY" ] && cp "$VARIANT_QUERY" "$D/paper_2506_17255_b200/csrc/query.cu"
+[ -n "$VARIANT_BUILD" ] && cp "$VARIANT_BUILD" "$D/paper_2506_17255_b200/csrc/build.cu"
 cp oracle/liboracle.so "$D/oracle/" 2>/dev/null || true
 USK_NVCC_FLAGS="$*" python "$D/paper_2506_17255_b200/build.py" > "$D/build.log" 2>&1 || { tail -20 "$D/build.log"; exit 1; }
 rm -rf "$D/paper_2506_17255_b200/build"
