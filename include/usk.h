@@ -10,9 +10,10 @@
  *   - Plain pointers and sizes only.  "device" = CUDA device memory of the current device;
  *     "host" = ordinary host memory.  Every large buffer is CALLER-OWNED.
  *   - The plan is an opaque, library-owned, immutable handle (usk_plan_destroy frees it).
- *   - usk_build / usk_reconstruct / usk_linear never allocate, are asynchronous on `stream`
- *     (NULL = legacy default stream) and may run concurrently on different streams with one
- *     plan.  usk_plan_allocation synchronises `stream` once (launch geometry lives on host).
+ *   - usk_reconstruct / usk_linear never allocate; usk_build / usk_build_rows take only
+ *     stream-ordered temporaries (cudaMallocAsync: the raw states of quantised plans, the
+ *     transposed weights of output-row units).  All are asynchronous on `stream` (NULL = legacy
+ *     default stream) and may run concurrently on different streams with one plan.  usk_plan_allocation synchronises `stream` once (launch geometry lives on host).
  *   - Return USK_OK (0) or an error code; no exception or abort crosses the ABI.  A one-line
  *     diagnostic of the last failure on the calling thread is in usk_last_error().
  *   - Results are a pure function of the inputs: sketch bytes and reconstructions do not
@@ -203,6 +204,18 @@ USK_API usk_status usk_plan_export(const usk_plan* plan, int32_t layer, uint8_t*
  * Non-finite weights set the plan's sticky flag (usk_check -> USK_ENONFINITE). */
 USK_API usk_status usk_build(const usk_plan* plan, const void* const* weights, const int32_t* layer_ids,
                      int32_t n, void* sketch, usk_stream stream);
+
+/* Row-sharded build of OUTPUT-ROW units (USK_GRAN_OUTROW, L31; SURVEY 8(f4) "disjoint
+ * per-rank sketch shards"): writes only the cells of the units of output rows [row_begin, row_end)
+ * of `layer` -- byte-identical to those usk_build writes -- so the ranks of an output-sharded
+ * deployment each build and keep just their own rows, with no sketch replication.
+ *   weight_rows: device, the rows [row_begin, row_end) of the layer's [out, in] matrix (row-major,
+ *                leading dimension in_features; rows outside the range are not needed), 16-B aligned.
+ * USK_EINVAL unless the plan is OUTROW with raw states (quantisation groups span rows); USK_ESHAPE
+ * for a bad layer / row range; USK_EUNSUPPORTED when the layer is not eligible for the fast build
+ * (AbsMaxMin, in_features * state bytes a multiple of 16, slots within shared memory). */
+USK_API usk_status usk_build_rows(const usk_plan* plan, int32_t layer, int64_t row_begin, int64_t row_end,
+                          const void* weight_rows, void* sketch, usk_stream stream);
 
 /* Reconstruction / decompression (Eq. 5; §3.1):
  *   w'(o, j) = the bonded cell of maximum |.| over the M rows (ties -> non-negative, L1/L2).

@@ -380,6 +380,18 @@ usk_status usk_plan_export(const usk_plan* pl, int32_t layer, uint8_t* cls, int3
   return USK_OK;
 }
 
+usk_status usk_build_rows(const usk_plan* pl, int32_t layer, int64_t row_begin, int64_t row_end,
+                          const void* weight_rows, void* sketch, usk_stream stream) {
+  if (!pl || !weight_rows || !sketch) return fail(USK_EINVAL, "usk_build_rows: null pointer");
+  if (!aligned16(sketch) || !aligned16(weight_rows)) return fail(USK_EINVAL, "usk_build_rows: 16-B alignment");
+  if (pl->gran != USK_GRAN_OUTROW || pl->q) return fail(USK_EINVAL, "usk_build_rows: OUTROW plans with raw states");
+  if (layer < 0 || layer >= pl->n_layers) return fail(USK_ESHAPE, "usk_build_rows: layer out of range");
+  if (row_begin < 0 || row_end > pl->layers[layer].out || row_begin > row_end)
+    return fail(USK_ESHAPE, "usk_build_rows: row range outside [0, out)");
+  if (row_begin == row_end) return USK_OK;
+  return launch_build_rows(pl, layer, row_begin, row_end, weight_rows, sketch, (cudaStream_t)stream);
+}
+
 usk_status usk_build(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
                      void* sketch, usk_stream stream) {
   if (!pl || !weights || !sketch) return fail(USK_EINVAL, "usk_build: null pointer");

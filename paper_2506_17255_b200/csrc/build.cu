@@ -530,11 +530,11 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
 }
 
 // W [rows, cols] row-major of es-byte elements; box = 32 rows x tj columns, no swizzle, zero fill
-bool make_w_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int es, int tj) {
+bool make_w_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int es, int tj, int64_t ld = 0) {
   auto fn = encode_tiled();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
-  cuuint64_t strides[1] = {(cuuint64_t)cols * es};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld ? ld : cols) * es};
   cuuint32_t box[2] = {(cuuint32_t)tj, (cuuint32_t)kRO};
   cuuint32_t estr[2] = {1, 1};
   return fn(m, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
@@ -542,15 +542,16 @@ bool make_w_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, in
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-int fast_upl(const usk_plan* pl, int32_t l) {
+int fast_upl(const usk_plan* pl, int32_t l, bool pitch_ok = false) {
   // units per lane for the fast kernels, 0 = not eligible: the largest UPL whose key array and
-  // stage ring fit one CTA (one CTA per SM is enough: 17 warps, bulk-copy ring in flight)
+  // stage ring fit one CTA (one CTA per SM is enough: 17 warps, bulk-copy ring in flight).
+  // pitch_ok: the caller pads the row pitch itself (row-sharded output-row builds)
   const LayerGeom& L = pl->layers[l];
   // output-row units (L31) build as input-dim units of W^T (the same sketch bytes, L31)
   const bool outrow = pl->gran == USK_GRAN_OUTROW;
   if ((pl->gran != USK_GRAN_ROW && !outrow) || pl->g != 1 || pl->variant != USK_ABSMAXMIN) return 0;
   const int es = pl->cell_bytes();
-  if (((outrow ? L.out : L.in) * es) % 16 != 0) return 0;
+  if (!pitch_ok && ((outrow ? L.out : L.in) * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
   const int S = (es == 2 ? 6 : 4) * 32 / kRO;
   auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 16 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
@@ -691,7 +692,7 @@ bool layer_fast_ok(const usk_plan* pl, int32_t l) { return fast_upl(pl, l) != 0;
 
 // W^T of a row-major [rows, cols] matrix of ES-byte elements (32 x 32 tiles through shared memory)
 template <int ES>
-__global__ void k_transpose(const void* src, void* dst, int64_t rows, int64_t cols) {
+__global__ void k_transpose(const void* src, void* dst, int64_t rows, int64_t cols, int64_t ld_dst) {
   using T = typename std::conditional<ES == 2, uint16_t, uint32_t>::type;
   __shared__ T tile[32][33];
   const int64_t c0 = (int64_t)blockIdx.x * 32, r0 = (int64_t)blockIdx.y * 32;
@@ -704,7 +705,7 @@ __global__ void k_transpose(const void* src, void* dst, int64_t rows, int64_t co
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
     const int64_t c = c0 + i, r = r0 + threadIdx.x;
-    if (r < rows && c < cols) D[c * rows + r] = tile[threadIdx.x][i];
+    if (r < rows && c < cols) D[c * ld_dst + r] = tile[threadIdx.x][i];
   }
 }
 
@@ -750,8 +751,8 @@ static usk_status launch_build_raw(const usk_plan* pl, const void* const* weight
       for (size_t k = a; k < b; ++k) {
         const LayerGeom& L = pl->layers[tg[k].first];
         const dim3 grid((unsigned)((L.in + 31) / 32), (unsigned)((L.out + 31) / 32));
-        if (es == 2) k_transpose<2><<<grid, dim3(32, 8), 0, st>>>(tg[k].second, wt + off, L.out, L.in);
-        else k_transpose<4><<<grid, dim3(32, 8), 0, st>>>(tg[k].second, wt + off, L.out, L.in);
+        if (es == 2) k_transpose<2><<<grid, dim3(32, 8), 0, st>>>(tg[k].second, wt + off, L.out, L.in, L.out);
+        else k_transpose<4><<<grid, dim3(32, 8), 0, st>>>(tg[k].second, wt + off, L.out, L.in, L.out);
         USK_LAUNCHED("k_transpose");
         batch.push_back({tg[k].first, wt + off});
         off += ((size_t)(L.out * L.in * es) + 255) / 256 * 256;
@@ -825,6 +826,56 @@ static usk_status launch_build_topk(const usk_plan* pl, const void* const* weigh
   }
   if (s == USK_OK) s = launch_build_raw(pl, wb.data(), layer_ids, n, sketch, st, 0xFF000000u);
   for (void* t : temps) cudaFreeAsync(t, st);
+  return s;
+}
+
+usk_status launch_build_rows(const usk_plan* pl, int32_t l, int64_t r0, int64_t r1, const void* w_rows, void* sketch,
+                             cudaStream_t st) {
+  const int upl = fast_upl(pl, l, true);
+  if (!upl) return fail(USK_EUNSUPPORTED, "usk_build_rows: layer not eligible for the fast build");
+  const LayerGeom& L = pl->layers[l];
+  const int es = pl->cell_bytes();
+  const int64_t rows = r1 - r0;
+  const int64_t ld = (rows * es + 15) / 16 * 16 / es;  // W^T row pitch: 16-B multiple for the tensor map
+  char* wt = nullptr;
+  USK_CUDA(cudaMallocAsync(&wt, (size_t)(L.in * ld * es), st));
+  const dim3 grid((unsigned)((L.in + 31) / 32), (unsigned)((rows + 31) / 32));
+  if (es == 2) k_transpose<2><<<grid, dim3(32, 8), 0, st>>>(w_rows, wt, rows, L.in, ld);
+  else k_transpose<4><<<grid, dim3(32, 8), 0, st>>>(w_rows, wt, rows, L.in, ld);
+  USK_LAUNCHED("k_transpose");
+  // one task: W^T [in, rows] -- its columns are the units unit_begin + r0 .. unit_begin + r1 - 1
+  BuildArgs A{};
+  A.M = pl->M;
+  A.hc = pl->hc;
+  A.ncols = pl->d_ncols;
+  A.nrows = pl->d_nrows;
+  A.offsets = pl->d_offsets;
+  A.ukeys = pl->d_keys;
+  A.R4 = pl->d_R4;
+  A.sketch = sketch;
+  A.err = pl->d_err;
+  A.kap_max = 0xFEFFFFFFu;
+  A.maxMN = std::max(1, pl->M * L.max_ncols);
+  const int TJ = 32 * upl;
+  BuildTask& t = A.task[A.n_tasks++];
+  t.W = wt;
+  t.out = L.in;
+  t.in = rows;
+  t.unit_base = L.unit_begin + r0;
+  t.tile_begin = 0;
+  usk_status s = USK_OK;
+  if (!make_w_map(&t.map, wt, L.in, rows, es, TJ, ld)) s = fail(USK_ECUDA, "usk_build_rows: cuTensorMapEncodeTiled failed");
+  const int tiles = (int)((rows + TJ - 1) / TJ);
+  if (s == USK_OK) {
+    if (pl->dtype == USK_BF16)
+      s = upl == 4 ? launch_fast_m<uint16_t, 4>(A, tiles, pl->hash, st)
+          : upl == 2 ? launch_fast_m<uint16_t, 2>(A, tiles, pl->hash, st) : launch_fast_m<uint16_t, 1>(A, tiles, pl->hash, st);
+    else
+      s = upl == 4 ? launch_fast_m<uint32_t, 4>(A, tiles, pl->hash, st)
+          : upl == 2 ? launch_fast_m<uint32_t, 2>(A, tiles, pl->hash, st) : launch_fast_m<uint32_t, 1>(A, tiles, pl->hash, st);
+  }
+  cudaError_t e = cudaFreeAsync(wt, st);
+  if (s == USK_OK && e != cudaSuccess) s = cuda_fail(e, "usk_build_rows: cudaFreeAsync");
   return s;
 }
 

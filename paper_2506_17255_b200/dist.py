@@ -7,6 +7,9 @@ SURVEY §8(e) / DESIGN.md "Multi-GPU":
     for output-sharded inference.
   * Decode: each linear's output features are split into contiguous per-rank ranges; each rank
     runs usk_linear on its range and the fp32 y shards are all-gathered (NCCL on GPUs).
+  * Output-row units (L31): each rank builds just the units of its own output rows
+    (build_output_shard, usk_build_rows) and decodes that range -- disjoint sketch shards, no
+    replication; the y shards are all-gathered as above.
   * Prefill: replicas (sequences sharded, sketch replicated) -- no collective.
 """
 from __future__ import annotations
@@ -24,6 +27,17 @@ def layer_owner(layer: int, world: int, layers_per_block: int = 7) -> int:
 
 def owned_layers(n_layers: int, rank: int, world: int, layers_per_block: int = 7):
     return [l for l in range(n_layers) if layer_owner(l, world, layers_per_block) == rank]
+
+
+def build_output_shard(usk, plan, layer: int, w_full_or_rows, sketch, rank: int, world: int, rows_only=False,
+                       stream=None):
+    """Output-row units (L31): rank `rank` builds only the units of its output shard of
+    `layer` (disjoint per-rank sketch regions: no replication step).  w_full_or_rows: the layer's
+    full [out, in] weight, or (rows_only=True) just this rank's rows."""
+    o0, o1 = output_shard(plan.layers[layer].out_features, rank, world)
+    w_rows = w_full_or_rows if rows_only else w_full_or_rows[o0:o1]
+    usk.build_rows(plan, layer, o0, o1, w_rows, sketch, stream=stream)
+    return o0, o1
 
 
 def replicate_sketch(sketch_bytes, layer_regions, world: int, group=None, layers_per_block: int = 7):

@@ -74,6 +74,7 @@ def _load():
         "usk_plan_layer": (i32, [p, i32, ct.POINTER(_LayerInfo)]),
         "usk_plan_export": (i32, [p, i32, p, p, p, p]),
         "usk_build": (i32, [p, p, p, i32, p, p]),
+        "usk_build_rows": (i32, [p, i32, i64, i64, p, p, p]),
         "usk_reconstruct": (i32, [p, p, i32, i64, i64, p, i64, p]),
         "usk_linear_workspace_bytes": (ct.c_size_t, [p, i32, i64, i64, i64]),
         "usk_linear": (i32, [p, p, i32, p, i32, i64, p, i32, i64, i64, p, ct.c_size_t, p]),
@@ -223,6 +224,12 @@ def build(plan: Plan, weights, sketch, layer_ids=None, stream=None):
     wp = (ct.c_void_p * n)(*[w.data_ptr() for w in weights])
     ids = None if layer_ids is None else (ct.c_int32 * n)(*layer_ids)
     _check(lib.usk_build(plan.handle, wp, ids, n, _ptr(sketch), _stream(stream)))
+
+
+def build_rows(plan: Plan, layer: int, row_begin: int, row_end: int, w_rows, sketch, stream=None):
+    """usk_build_rows (output-row units): build only the units of rows [row_begin, row_end) of `layer`
+    from w_rows = those rows of its [out, in] weight (a rank's shard)."""
+    _check(lib.usk_build_rows(plan.handle, layer, row_begin, row_end, _ptr(w_rows), _ptr(sketch), _stream(stream)))
 
 
 def reconstruct(plan: Plan, sketch, layer: int, w_out, row_begin: int = 0, row_end=None, stream=None):

@@ -94,3 +94,68 @@ def test_shard_helpers():
     owned = [udist.owned_layers(224, r, 8) for r in range(8)]
     assert sorted(l for o in owned for l in o) == list(range(224))
     assert all(len(o) == 28 for o in owned)
+
+
+def _worker_outrow(rank, world, port, shapes, q):
+    """Output-row units (L31): every rank builds only the units of its own output rows
+    (disjoint sketch regions, no replication) and decodes that range; y shards are all-gathered."""
+    import oracle
+    from paper_2506_17255_b200 import dist as udist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        opl = oracle.plan(shapes, 2.0, M=3, dtype=oracle.BF16, gran=oracle.GRAN_OUTROW, seed=13)
+        ys, owned_cells = [], []
+        sk = np.full(opl.total_cells, 0xABCD, np.uint16)      # cells of other ranks' rows stay garbage
+        for l, (o, i) in enumerate(shapes):
+            o0, o1 = udist.output_shard(o, rank, world)
+            W = synth.weights_bf16(o, i, 60 + l)
+            oracle.build_layer(opl, l, W, sk, t_begin=o0, t_end=o1)   # units = rows [o0, o1)
+            u0, _ = opl.layer_units(l)
+            owned_cells.append((int(opl.offsets[u0 + o0]), int(opl.offsets[u0 + o1])))
+            x = synth.vector(i, seed=l)[0].astype(np.float64)
+            y_shard = torch.from_numpy(oracle.linear_rows(opl, sk, l, x, o0, o1)[0])
+            y = torch.zeros(o, dtype=torch.float64)
+            udist.allgather_outputs(y_shard, y)
+            ys.append(y.numpy())
+        parts = [sk[a:b].copy() for a, b in owned_cells]
+        if rank == 0:
+            q.put(("ys", ys))
+        q.put((rank, owned_cells, parts))
+    except Exception as e:
+        q.put(("error", repr(e)))
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+def test_outrow_disjoint_shards_gloo(orc):
+    shapes = [(64, 96), (47, 64), (70, 32)]
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_outrow, args=(r, world, port, shapes, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=120) for _ in range(world + 1)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert not any(g[0] == "error" for g in got), got
+    opl = orc.plan(shapes, 2.0, M=3, dtype=orc.BF16, gran=orc.GRAN_OUTROW, seed=13)
+    ref = orc.build_model(opl, [synth.weights_bf16(o, i, 60 + l) for l, (o, i) in enumerate(shapes)])
+    ys = next(g[1] for g in got if g[0] == "ys")
+    covered = np.zeros(opl.total_cells, bool)
+    for g in got:
+        if g[0] in ("ys", "error"):
+            continue
+        for (a, b), part in zip(g[1], g[2]):
+            np.testing.assert_array_equal(part, ref[a:b])       # each rank's own cells = the full build's
+            assert not covered[a:b].any()                       # disjoint
+            covered[a:b] = True
+    assert covered.all()                                        # the shards tile the whole sketch
+    for l, (o, i) in enumerate(shapes):
+        x = synth.vector(i, seed=l)[0].astype(np.float64)
+        np.testing.assert_array_equal(ys[l], orc.linear_rows(opl, ref, l, x)[0])

@@ -144,3 +144,49 @@ def test_outrow_errors(usk):
         usk.plan_allocation([(64, 64)], bpw=2.0, granularity="outrow", dims_per_unit=2)
     with pytest.raises(usk.UskError):
         usk.plan_allocation([(64, 64)], bpw=2.0, granularity="outrow", topk=4)
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_outrow_row_sharded_build_and_decode(orc, usk, world):
+    """usk_build_rows: each 'rank' (run one after another on this GPU -- no rank waits on another)
+    builds only its output shard from only its rows; the union of the shards is byte-identical to
+    the full build and the oracle, and each rank's decode of its range from a sketch holding ONLY
+    its own units equals the full call's rows bit for bit (no replication step)."""
+    from paper_2506_17255_b200 import dist as udist
+    shapes = [(200, 2048), (130, 8192), (96, 264)]
+    pl, opl, sk, osk, Ws, dW = _both(orc, usk, shapes, "bf16", 0.5, 3, "x")
+    full = sketch_cells(sk, pl, "bf16").copy()
+    np.testing.assert_array_equal(full, osk)
+    union = pl.new_sketch()
+    union.fill_(0x33)
+    for r in range(world):
+        own = pl.new_sketch()
+        own.fill_(0x44)                                            # this rank's sketch: only its units
+        for l, (o, i) in enumerate(shapes):
+            o0, o1 = udist.output_shard(o, r, world)
+            rows_only = dW[l][o0:o1].contiguous()                 # the rank holds only its rows
+            udist.build_output_shard(usk, pl, l, rows_only, own, r, world, rows_only=True)
+            udist.build_output_shard(usk, pl, l, dW[l], union, r, world)
+            x = synth.torch_vector(i, 30 + l, "cuda", torch.bfloat16)
+            y_full = torch.empty(o, dtype=torch.float32, device="cuda")
+            usk.linear(pl, sk, l, x.view(1, -1), y_full.view(1, -1), usk.new_workspace(pl, l))
+            y_sh = torch.empty(o1 - o0, dtype=torch.float32, device="cuda")
+            usk.linear(pl, own, l, x.view(1, -1), y_sh.view(1, -1), usk.new_workspace(pl, l, 1, o0, o1),
+                       out_begin=o0, out_end=o1)
+            assert torch.equal(y_sh, y_full[o0:o1])
+        usk.check(pl)
+    np.testing.assert_array_equal(sketch_cells(union, pl, "bf16"), full)
+
+
+def test_build_rows_errors(usk):
+    pl = usk.plan_allocation([(64, 64)], bpw=2.0)                  # input-dim units
+    sk = pl.new_sketch()
+    w = torch.zeros((64, 64), dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(usk.UskError):
+        usk.build_rows(pl, 0, 0, 32, w, sk)
+    po = usk.plan_allocation([(64, 64)], bpw=2.0, granularity="outrow")
+    so = po.new_sketch()
+    with pytest.raises(usk.UskError):
+        usk.build_rows(po, 0, 10, 70, w, so)                       # rows past out
+    with pytest.raises(usk.UskError):
+        usk.build_rows(po, 1, 0, 8, w, so)                         # layer out of range
