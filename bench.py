@@ -144,7 +144,7 @@ def run_reference(args):
     else:
         getw = lambda l: synth.weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, 0, l))
     per_step = []
-    budget = max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    budget = args.ref_step_s if args.ref_step_s else max(2.0, 60.0 / max(1, args.steps + args.warmup))
     for k in range(args.warmup + args.steps):
         r = oracle_decode_sample(shapes, getw, budget_s=budget)
         if k >= args.warmup:
@@ -152,7 +152,7 @@ def run_reference(args):
     v = float(np.mean([r["value"] for r in per_step]))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 / v, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": "c3: Llama-3.2-1B 112 linears, batch-1 decode, 0.5 bpw, M=3, bf16 weights",
                        "bpw": BPW, "rows": ROWS},
             "cpu_baseline": {**{k: per_step[-1][k] for k in ("kind", "cores", "sample")}, "value": v, "unit": UNIT},
@@ -580,6 +580,7 @@ def main():
     ap.add_argument("--impl", default="usk", choices=["usk", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-step-s", type=float, default=None, help="--impl reference: oracle seconds per step")
     ap.add_argument("--no-q4", action="store_true", help="skip the extra plans (q4 states, classes, output-row units)")
     ap.add_argument("--no-8b", action="store_true", help="skip the Llama-3-8B (config 5) build + decode at N=1")
     args = ap.parse_args()
