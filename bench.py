@@ -469,6 +469,58 @@ def run_usk(args):
         orow = extra_point(granularity="outrow")
         orow.update({"granularity": "outrow (one unit per output row, ledger L31)"})
 
+    # ---- BASELINE config 4: Llama-3.2-1B prefill, 2048 tokens x batch 8 (T = 16384) through all 112
+    #      linears in model order (usk_linear T > 1: K3 reconstruct into the workspace + the tcgen05
+    #      GEMM K5), at 0.5 bpw (the decode plan) and 0.8 bpw; X/Y (268 MB each) exceed L2
+    c4 = None
+    if world == 1 and not args.no_prefill:
+        torch.cuda.empty_cache()
+        T = 16384
+        Xp = synth.torch_vector(8192, 77, dev, torch.bfloat16, T=T)           # [T, 8192], sliced per layer
+        Yp = torch.empty((T, 8192), dtype=torch.bfloat16, device=dev)
+        ws_p = torch.zeros(max(usk.linear_workspace_bytes(plan, l, T) for l in range(L)), dtype=torch.uint8,
+                           device=dev)
+
+        def prefill_pass(pl_, sk_):
+            for l, (o, i) in enumerate(shapes):
+                usk.linear(pl_, sk_, l, Xp[:, :i], Yp[:, :o], ws_p, stream=stream)
+
+        def time_pass(pl_, sk_, reps=3):
+            with torch.cuda.stream(stream):
+                prefill_pass(pl_, sk_)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            with torch.cuda.stream(stream):
+                a.record(stream)
+                for _ in range(reps):
+                    prefill_pass(pl_, sk_)
+                b.record(stream)
+            b.synchronize()
+            return a.elapsed_time(b) / reps
+
+        flop = 2.0 * T * numel
+        ms05 = time_pass(plan, sketch)
+        plan08 = usk.plan_allocation(shapes, bpw=0.8, rows=ROWS, seed=SEED)
+        sk08 = plan08.new_sketch(dev)
+        w8_ = [synth.torch_weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, l // 7, l % 7), dev)
+               for l in range(L)]
+        usk.build(plan08, w8_, sk08)
+        del w8_
+        usk.check(plan08)
+        ms08 = time_pass(plan08, sk08)
+        pk, pk_s = peaks.get("bf16_tflops", 1666.6), peaks.get("bf16_tflops_sustained", 1352.0)
+        c4 = {"workload": "c4: Llama-3.2-1B prefill, 2048 tokens x batch 8 (T = 16384), all 112 linears, M=3",
+              "bpw_0.5": {"ms_per_pass": ms05, "TFLOP_per_s": flop / (ms05 * 1e-3) / 1e12,
+                          "frac_of_bf16_sustained": flop / (ms05 * 1e-3) / 1e12 / pk_s,
+                          "frac_of_bf16_burst": flop / (ms05 * 1e-3) / 1e12 / pk},
+              "bpw_0.8": {"ms_per_pass": ms08, "TFLOP_per_s": flop / (ms08 * 1e-3) / 1e12,
+                          "frac_of_bf16_sustained": flop / (ms08 * 1e-3) / 1e12 / pk_s,
+                          "frac_of_bf16_burst": flop / (ms08 * 1e-3) / 1e12 / pk},
+              "flop_per_pass": flop, "peak_basis": "MEASURED_PEAKS.json bf16 (torch 8192^3): sustained for a "
+                                                   "25 ms pass, burst shown beside"}
+        del Xp, Yp, ws_p, sk08, plan08
+        torch.cuda.empty_cache()
+
     # ---- BASELINE config 5 at N = 1: Llama-3-8B-shaped linears (224, 6.98 G weights, 13.96 GB bf16)
     #      at 0.5 bpw -- the build of all layers in one call, and the batch-1 decode token as 128
     #      grouped calls in one CUDA graph (the 436 MB sketch exceeds L2: it streams from HBM)
@@ -566,6 +618,8 @@ def run_usk(args):
             line["output_row_units"] = orow
         if c5 is not None:
             line["llama3_8b_n1"] = c5
+        if c4 is not None:
+            line["prefill_c4"] = c4
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -583,6 +637,7 @@ def main():
     ap.add_argument("--ref-step-s", type=float, default=None, help="--impl reference: oracle seconds per step")
     ap.add_argument("--no-q4", action="store_true", help="skip the extra plans (q4 states, classes, output-row units)")
     ap.add_argument("--no-8b", action="store_true", help="skip the Llama-3-8B (config 5) build + decode at N=1")
+    ap.add_argument("--no-prefill", action="store_true", help="skip the config-4 prefill passes")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
