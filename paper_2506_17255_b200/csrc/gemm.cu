@@ -18,10 +18,17 @@
 //   warps 4..7  epilogue: wait acc_full[parity], tcgen05.ld 32x32b (warp w reads TMEM lanes
 //               32*(w%4)..+31 = its 32 output rows), convert, store, then release the accumulator
 //               (acc_empty[parity]) -- so the epilogue of tile i overlaps the MMAs of tile i+1.
+//
+// The default launch is the CTA-pair form of the same pipeline, k_gemm_tc2 (cta_group::2, 256 x 256
+// tiles per cluster of two, 6 stages of 32 KB per CTA; see its comment).  USK_GEMM_1SM=1 selects
+// the 1-CTA kernel above (A/B only).  Measured on one B200, Llama-3.2-1B block at T = 16384: 1.760
+// vs 1.876 ms per block (tools/prefill_split.py); ncu on the gate GEMM: tensor pipe 84 % of active
+// cycles, shared-memory pipe 77 %, SM clock 1.48 GHz under the power cap (profiles/r1_gemm2_ncu.txt).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -258,6 +265,219 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+// ---------------------------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a 256 x 256 tile with
+// one tcgen05.mma (M = 256) issued by the leader CTA (rank 0).  CTA r stages A rows
+// [256 m + 128 r, +128) and B rows [256 n + 128 r, +128) of each 64-wide K block (16 + 16 KB per
+// stage), so each SM fills and the MMA reads half the B bytes of the 1-CTA kernel per flop: the
+// 1-CTA 128 x 256 tile needs ~134 B/clk of shared-memory bandwidth per SM at the tensor peak (TMA
+// writes + MMA operand reads), over the 128 B/clk an SM has; the pair needs ~90.
+//   * full[s] lives in the leader: both CTAs' TMA loads (.cta_group::2) complete their bytes on it;
+//     the leader posts the 64 KB expectation.
+//   * the leader's commits are multicast to both CTAs: empty[s] (each CTA's producer reuses its own
+//     half of stage s) and acc_full[b] (each CTA's epilogue drains its own TMEM: rows 128 r + lane).
+//   * acc_empty[b] lives in the leader and counts the 8 epilogue warps of the pair.
+constexpr int kStages2 = 6;
+constexpr uint32_t kHalfBytes = 128 * BK * 2;        // 16 KB: one CTA's half of A or of B
+constexpr uint32_t kStageBytes2 = 2 * kHalfBytes;     // per CTA
+constexpr size_t kGemmSmem2 = 1024 + kStages2 * kStageBytes2 + 256;
+// kind::f16, D = F32, A = B = BF16, K-major, M = 256 (pair), N = 256
+constexpr uint32_t kIdesc2 = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                             ((uint32_t)(256 >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t map_rank(const void* p, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint32_t leader_bar, int c0,
+                                                 int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(leader_bar)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(a), "l"(b), "r"(kIdesc2), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm_tc2(const __grid_constant__ CUtensorMap mapA, const __grid_constant__ CUtensorMap mapB,
+               const __grid_constant__ GemmArgs G) {
+  extern __shared__ uint8_t gsm_raw[];
+  uint8_t* gsm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sA = gsm;                                   // kStages2 x 16 KB
+  uint8_t* sB = gsm + kStages2 * kHalfBytes;           // kStages2 x 16 KB
+  uint64_t* full = reinterpret_cast<uint64_t*>(gsm + kStages2 * kStageBytes2);
+  uint64_t* empty = full + kStages2;
+  uint64_t* acc_full = empty + kStages2;  // [2]
+  uint64_t* acc_empty = acc_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int mblocks = (int)((G.T + BM - 1) / BM), nblocks = (int)((G.N + BN - 1) / BN);
+  const int mpairs = (mblocks + 1) / 2;
+  const int64_t tiles = (int64_t)mpairs * nblocks;
+  const int64_t pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int nkb = (int)((G.K + BK - 1) / BK);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kStages2; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);  // the 4 epilogue warps of each CTA of the pair
+    }
+    fence_mbar_init();
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapA)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&mapB)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(kTmemCols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / complete_tx
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int64_t it = 0;
+      for (int64_t t = pair; t < tiles; t += npairs) {
+        int mp, nb;
+        tile_coords(t, mpairs, nblocks, mp, nb);
+        const int arow = mp * 2 * BM + (int)rank * BM;
+        const int brow = nb * BN + (int)rank * 128;
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = (int)(it % kStages2);
+          if (it >= kStages2) mbar_wait(&empty[s], (uint32_t)((it / kStages2) - 1) & 1u);
+          if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * kStageBytes2);
+          const uint32_t lbar = map_rank(&full[s], 0);
+          tma_load_2d_pair(sA + s * kHalfBytes, &mapA, lbar, kb * BK, arow);
+          tma_load_2d_pair(sB + s * kHalfBytes, &mapB, lbar, kb * BK, brow);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      int64_t it = 0;
+      int local = 0;
+      for (int64_t t = pair; t < tiles; t += npairs, ++local) {
+        const int b = local & 1;
+        if (local >= 2) mbar_wait(&acc_empty[b], (uint32_t)((local >> 1) - 1) & 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t acc = tmem + (uint32_t)(b * BN);
+        for (int kb = 0; kb < nkb; ++kb, ++it) {
+          const int s = (int)(it % kStages2);
+          mbar_wait(&full[s], (uint32_t)(it / kStages2) & 1u);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (lane == 0) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k) {
+              const uint64_t da = smem_desc_sw128(sA + s * kHalfBytes + k * 32);
+              const uint64_t db = smem_desc_sw128(sB + s * kHalfBytes + k * 32);
+              mma_bf16_pair(acc, da, db, (kb | k) != 0);
+            }
+            mma_commit_pair(&empty[s]);
+            if (kb == nkb - 1) mma_commit_pair(&acc_full[b]);
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const uint32_t leader_acc_empty[2] = {map_rank(&acc_empty[0], 0), map_rank(&acc_empty[1], 0)};
+    int local = 0;
+    for (int64_t t = pair; t < tiles; t += npairs, ++local) {
+      const int b = local & 1;
+      int mp, nb;
+      tile_coords(t, mpairs, nblocks, mp, nb);
+      mbar_wait(&acc_full[b], (uint32_t)(local >> 1) & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int64_t row = (int64_t)mp * 2 * BM + (int64_t)rank * BM + q * 32 + lane;
+      const int64_t n0 = (int64_t)nb * BN;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(b * BN + c0), r);
+        if (row >= G.T) continue;
+        const int64_t col = n0 + c0;
+        if (col >= G.N) continue;
+        const int nvalid = (int)min((int64_t)32, G.N - col);
+        if (G.y_bf16) {
+          uint16_t* dst = reinterpret_cast<uint16_t*>(G.Y) + row * G.ldy + col;
+          if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+              uint4 pk;
+              pk.x = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 0])) |
+                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 1])) << 16);
+              pk.y = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 2])) |
+                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 3])) << 16);
+              pk.z = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 4])) |
+                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 5])) << 16);
+              pk.w = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 6])) |
+                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 7])) << 16);
+              reinterpret_cast<uint4*>(dst)[v] = pk;
+            }
+          } else {
+            for (int v = 0; v < nvalid; ++v) dst[v] = f32_to_bf16_rne(__uint_as_float(r[v]));
+          }
+        } else {
+          float* dst = reinterpret_cast<float*>(G.Y) + row * G.ldy + col;
+          if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v)
+              reinterpret_cast<uint4*>(dst)[v] = make_uint4(r[4 * v], r[4 * v + 1], r[4 * v + 2], r[4 * v + 3]);
+          } else {
+            for (int v = 0; v < nvalid; ++v) dst[v] = __uint_as_float(r[v]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive_remote(leader_acc_empty[b]);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  cluster_sync_all();  // no remote arrive or MMA operand read targets a CTA that has exited
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
   static std::once_flag once;
@@ -291,10 +511,45 @@ usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dty
     return fail(USK_EUNSUPPORTED, "tcgen05 path needs in_features % 8 == 0 (16-B TMA row pitch)");
   if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(W) & 15))
     return fail(USK_EINVAL, "tcgen05 path needs 16-B aligned operands");
+  static const bool one_sm = [] {
+    const char* e = std::getenv("USK_GEMM_1SM");
+    return e && e[0] == '1';
+  }();
   CUtensorMap ma, mb;
-  if (!make_map(&ma, X, T, K, BM) || !make_map(&mb, W, n_out, K, BN))
+  if (!make_map(&ma, X, T, K, BM) || !make_map(&mb, W, n_out, K, one_sm ? BN : 128))
     return fail(USK_ECUDA, "cuTensorMapEncodeTiled failed");
   GemmArgs G{Y, y_dtype == USK_BF16, T, n_out, K, n_out};
+  static int sms2 = 0;
+  if (!sms2) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev) !=
+                                                 cudaSuccess)
+      sms2 = 148;
+  }
+  if (!one_sm) {
+    static std::once_flag attr2_once;
+    std::call_once(attr2_once, [] {
+      cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem2);
+    });
+    const int64_t mpairs = ((T + BM - 1) / BM + 1) / 2;
+    const int64_t ptiles = mpairs * ((n_out + BN - 1) / BN);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(2 * std::min<int64_t>(ptiles, sms2 / 2)));
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = kGemmSmem2;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm_tc2, ma, mb, G);
+    if (e != cudaSuccess) return fail(USK_ECUDA, cudaGetErrorString(e));
+    USK_LAUNCHED("k_gemm_tc2");
+    return USK_OK;
+  }
   static std::once_flag attr_once;
   std::call_once(attr_once, [] {
     cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
