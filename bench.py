@@ -246,13 +246,19 @@ def run_usk(args):
             for l in ls:
                 udist.allgather_outputs(Yshard[l], ys_full[l])
 
+    def warm():
+        if args.prefetch:  # opt-in: the step reads the whole sketch (60 MB < L2) from HBM once, up front
+            usk.prefetch_l2(plan, sketch)
+
     def step_grouped():
+        warm()
         for gi, g in enumerate(groups):
             usk.linear_batch(plan, sketch, g, xg[gi], [out_of(l) for l in g], ws_group[gi],
                              ranges=[ranges[l] for l in g])
             gather(g)
 
     def step_single():
+        warm()
         for l in range(L):
             usk.linear(plan, sketch, l, x_of_layer[l].view(1, -1), out_of(l).view(1, -1), ws_layer[l], *ranges[l])
             gather([l])
@@ -638,6 +644,8 @@ def main():
     ap.add_argument("--no-q4", action="store_true", help="skip the extra plans (q4 states, classes, output-row units)")
     ap.add_argument("--no-8b", action="store_true", help="skip the Llama-3-8B (config 5) build + decode at N=1")
     ap.add_argument("--no-prefill", action="store_true", help="skip the config-4 prefill passes")
+    ap.add_argument("--prefetch", action="store_true",
+                    help="start each decode step with usk_prefetch_l2 of the whole sketch (measured: no gain)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -225,6 +225,17 @@ USK_API usk_status usk_reconstruct(const usk_plan* plan, const void* sketch, int
                            int64_t row_begin, int64_t row_end, void* w_out, int64_t ld_out,
                            usk_stream stream);
 
+/* L2 warm-up of the sketch bytes of layers [layer_begin, layer_end) (cells, or codes + group
+ * scales of a quantised plan, and their Top-K side tables): bulk L2 prefetches issued by a small
+ * grid launched with programmatic dependent launch, so it overlaps the running kernel; the
+ * following usk_linear calls then stage their chunks from L2 instead of HBM.  A pure performance
+ * hint: no results change.  Stream-ordered after the previous work on `stream` (the kernel waits
+ * for its predecessor before it completes).  Use it where the sketch region fits L2 (126 MB on
+ * B200), e.g. once per decode token for a 1B model (60 MB), or one block ahead for larger ones.
+ *   USK_ESHAPE for a layer range outside [0, n_layers); USK_EINVAL for null pointers. */
+USK_API usk_status usk_prefetch_l2(const usk_plan* plan, const void* sketch, int32_t layer_begin,
+                                   int32_t layer_end, usk_stream stream);
+
 /* Workspace bytes usk_linear needs for (layer, T, output range).  0 on invalid arguments. */
 USK_API size_t usk_linear_workspace_bytes(const usk_plan* plan, int32_t layer, int64_t T,
                                   int64_t out_begin, int64_t out_end);

@@ -420,6 +420,14 @@ usk_status usk_reconstruct(const usk_plan* pl, const void* sketch, int32_t layer
   return launch_reconstruct(pl, sketch, layer, row_begin, row_end, w_out, ld_out, (cudaStream_t)stream);
 }
 
+usk_status usk_prefetch_l2(const usk_plan* pl, const void* sketch, int32_t layer_begin, int32_t layer_end,
+                           usk_stream stream) {
+  if (!pl || !sketch) return fail(USK_EINVAL, "usk_prefetch_l2: null pointer");
+  if (layer_begin < 0 || layer_end > pl->n_layers || layer_begin > layer_end)
+    return fail(USK_ESHAPE, "usk_prefetch_l2: layer range outside [0, n_layers)");
+  return launch_prefetch(pl, sketch, layer_begin, layer_end, (cudaStream_t)stream);
+}
+
 size_t usk_linear_workspace_bytes(const usk_plan* pl, int32_t layer, int64_t T, int64_t out_begin,
                                   int64_t out_end) {
   if (!pl || layer < 0 || layer >= pl->n_layers || T < 1) return 0;

@@ -176,6 +176,7 @@ namespace usk {
 // launchers (defined in the .cu files)
 usk_status launch_build(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids,
                         int32_t n, void* sketch, cudaStream_t st);
+usk_status launch_prefetch(const usk_plan* pl, const void* sketch, int32_t a, int32_t b, cudaStream_t st);
 usk_status launch_build_rows(const usk_plan* pl, int32_t l, int64_t r0, int64_t r1, const void* w_rows, void* sketch,
                              cudaStream_t st);
 usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t layer, int64_t r0,

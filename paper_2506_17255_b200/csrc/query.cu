@@ -1180,6 +1180,49 @@ Trace& trace() {
   return T;
 }
 
+// L2 warm-up (usk_prefetch_l2): up to 8 byte ranges; CTA c issues bulk L2 prefetches for its
+// 1/grid slice of each (16-B granules), triggers the next launch at once, and waits for its own
+// predecessor only after issuing (so stream order is kept transitively).  No data is returned.
+struct PfRanges {
+  const char* base[8];
+  int64_t bytes[8];
+  int32_t n;
+};
+
+__global__ void k_prefetch_l2(const __grid_constant__ PfRanges R) {
+  if (threadIdx.x == 0)
+    for (int r = 0; r < R.n; ++r) {
+      const int64_t granules = R.bytes[r] >> 4;
+      const int64_t per = (granules + gridDim.x - 1) / gridDim.x;
+      const int64_t g0 = (int64_t)blockIdx.x * per, g1 = min(granules, g0 + per);
+      for (int64_t g = g0; g < g1; g += 2048) {  // 32 KB per request
+        const uint32_t n = (uint32_t)(min(g1 - g, (int64_t)2048) << 4);
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(R.base[r] + (g << 4)), "r"(n) : "memory");
+      }
+    }
+  pdl_trigger();
+  pdl_wait();
+}
+
+usk_status launch_prefetch_l2(const PfRanges& R, cudaStream_t st) {
+  int64_t total = 0;
+  for (int r = 0; r < R.n; ++r) total += R.bytes[r];
+  if (total < 16) return USK_OK;
+  const int grid = (int)std::min<int64_t>(sm_count(), (total + (256 << 10) - 1) / (256 << 10));
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3(32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  USK_CUDA(cudaLaunchKernelEx(&cfg, k_prefetch_l2, R));
+  count_launch();
+  return USK_OK;
+}
+
 usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl, cudaStream_t st,
                     int threads = kQThreads) {
   cudaLaunchConfig_t cfg{};
@@ -1244,6 +1287,41 @@ GenQ make_genq(const usk_plan* pl, int32_t l, const void* sketch) {
 }
 
 }  // namespace
+
+// usk_prefetch_l2: the sketch bytes of layers [a, b) -- raw cells, or the packed codes and the
+// group scales of a quantised plan, plus the layers' Top-K side tables -- and the plan's per-unit
+// metadata the query kernels read before their first cell (offsets, N_u, M_u, keys, classes)
+usk_status launch_prefetch(const usk_plan* pl, const void* sketch, int32_t a, int32_t b, cudaStream_t st) {
+  if (a >= b) return USK_OK;
+  const LayerGeom& La = pl->layers[a];
+  const LayerGeom& Lb = pl->layers[b - 1];
+  const int64_t c0 = La.cell_begin, c1 = Lb.cell_begin + Lb.n_cells;
+  const int64_t u0 = La.unit_begin, u1 = Lb.unit_begin + Lb.n_units;
+  PfRanges R{};
+  auto add = [&](const void* base, int64_t lo, int64_t hi) {
+    lo &= ~int64_t(15);
+    hi = (hi + 15) & ~int64_t(15);
+    if (hi > lo && R.n < 8) {
+      R.base[R.n] = reinterpret_cast<const char*>(base) + lo;
+      R.bytes[R.n++] = hi - lo;
+    }
+  };
+  if (pl->q == 0) {
+    add(sketch, c0 * pl->cell_bytes(), c1 * pl->cell_bytes());
+  } else {
+    add(sketch, c0 * pl->q / 8, (c1 * pl->q + 7) / 8);
+    add(sketch, pl->scales_off + c0 / pl->G * 4, pl->scales_off + (c1 + pl->G - 1) / pl->G * 4);
+  }
+  if (pl->side_bytes > 0 && La.n_out > 0) add(sketch, La.out_off, Lb.out_off + Lb.n_out * (4 + pl->cell_bytes()));
+  // metadata arrays are allocated in whole 16-B granules? round inward at their ends to stay inside
+  auto add_in = [&](const void* base, int64_t lo, int64_t hi) { add(base, lo, hi & ~int64_t(15)); };
+  add_in(pl->d_offsets, u0 * 8, (u1 + 1) * 8);
+  add_in(pl->d_ncols, u0 * 4, u1 * 4);
+  add_in(pl->d_keys, u0 * 4, u1 * 4);
+  add_in(pl->d_nrows, u0, u1);
+  add_in(pl->d_cls, u0, u1);
+  return launch_prefetch_l2(R, st);
+}
 
 size_t gemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* o0, const int64_t* o1,
                                   int n) {

@@ -76,6 +76,7 @@ def _load():
         "usk_build": (i32, [p, p, p, i32, p, p]),
         "usk_build_rows": (i32, [p, i32, i64, i64, p, p, p]),
         "usk_reconstruct": (i32, [p, p, i32, i64, i64, p, i64, p]),
+        "usk_prefetch_l2": (i32, [p, p, i32, i32, p]),
         "usk_linear_workspace_bytes": (ct.c_size_t, [p, i32, i64, i64, i64]),
         "usk_linear": (i32, [p, p, i32, p, i32, i64, p, i32, i64, i64, p, ct.c_size_t, p]),
         "usk_linear_batch_workspace_bytes": (ct.c_size_t, [p, p, p, i32]),
@@ -236,6 +237,12 @@ def reconstruct(plan: Plan, sketch, layer: int, w_out, row_begin: int = 0, row_e
     row_end = plan.layers[layer].out_features if row_end is None else row_end
     _check(lib.usk_reconstruct(plan.handle, _ptr(sketch), layer, row_begin, row_end, _ptr(w_out), w_out.stride(0),
                                _stream(stream)))
+
+
+def prefetch_l2(plan: Plan, sketch, layer_begin: int = 0, layer_end=None, stream=None):
+    """Warm the sketch bytes of layers [layer_begin, layer_end) into L2 (usk_prefetch_l2)."""
+    layer_end = len(plan.layers) if layer_end is None else layer_end
+    _check(lib.usk_prefetch_l2(plan.handle, _ptr(sketch), layer_begin, layer_end, _stream(stream)))
 
 
 def linear_workspace_bytes(plan: Plan, layer: int, T: int = 1, out_begin: int = 0, out_end=None) -> int:

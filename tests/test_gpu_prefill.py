@@ -62,3 +62,33 @@ def test_prefill_output_shard(orc, usk):
     part = torch.empty((T, o - 100), dtype=torch.float32, device="cuda")
     usk.linear(pl, sk, 0, x, part, usk.new_workspace(pl, 0, T, 100, o), out_begin=100, out_end=o)
     assert torch.equal(part, full[:, 100:])
+
+
+def test_prefetch_l2_is_a_pure_hint(usk):
+    """usk_prefetch_l2 changes no result (decode and prefill bit-equal with and without it) and
+    rejects a layer range outside [0, n_layers)."""
+    shapes = [(512, 256), (256, 512)]
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=5)
+    sk = pl.new_sketch()
+    usk.build(pl, [_bf16_dev(synth.weights_bf16(o, i, seed=o)) for o, i in shapes], sk)
+    outs = []
+    for pf in (False, True):
+        if pf:
+            usk.prefetch_l2(pl, sk)
+            usk.prefetch_l2(pl, sk, 1, 2)
+            usk.prefetch_l2(pl, sk, 1, 1)  # empty range: no launch
+        ys = []
+        for l, (o, i) in enumerate(shapes):
+            for T in (1, 100):
+                x = _bf16_dev(synth.f32_to_bf16_bits(synth.vector(i, seed=l, T=T)))
+                y = torch.empty((T, o), dtype=torch.float32, device="cuda")
+                usk.linear(pl, sk, l, x, y, usk.new_workspace(pl, l, T))
+                ys.append(y)
+        torch.cuda.synchronize()
+        outs.append(ys)
+    for a, b in zip(*outs):
+        assert torch.equal(a, b)
+    with pytest.raises(usk.UskError):
+        usk.prefetch_l2(pl, sk, 0, 3)
+    with pytest.raises(usk.UskError):
+        usk.prefetch_l2(pl, sk, 2, 1)
