@@ -244,7 +244,10 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
   for (int pa = 0; pa < nu; pa += pu) {
     const int pn = min(pu, nu - pa);
     if (threadIdx.x == 0 && !(pa == 0 && first_issued)) stage_issue<E, UPL, QB>(A, ubase, pa, pn);
-    const int t = threadIdx.x & (pu - 1);
+    // thread -> unit of the piece: for pu >= 32 a warp's 32 lanes take units pu/32 apart, so their
+    // cells land in distinct owner lanes ul / UPL (banks) -- conflict-free stores for pu = 32 * UPL
+    const int tt = threadIdx.x & (pu - 1);
+    const int t = pu >= 32 ? (tt & 31) * (pu >> 5) + (tt >> 5) : tt;
     const int ul = pa + t;
     int64_t u_off = 0, cu = 0;
     int n = 0;  // N of the thread's unit (0: no unit)
