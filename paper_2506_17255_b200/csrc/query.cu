@@ -270,7 +270,7 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
           for (int k = threadIdx.x / pu; k < n; k += KS) dst[k * 32] = 0u;
           continue;
         }
-#pragma unroll 4
+#pragma unroll 2
         for (int k = threadIdx.x / pu; k < n; k += KS) {
           const uint32_t b = ES == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
                                      : reinterpret_cast<const uint32_t*>(src)[k];
