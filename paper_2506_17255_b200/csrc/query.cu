@@ -123,6 +123,32 @@ __device__ __forceinline__ unsigned long long gtimer() {
 template <int MT, int HASH>
 constexpr bool fast_hash() { return MT > 0 && HASH == USK_HASH_X; }
 
+// Raw bf16 plans stage "key|value" cell words: the high half is the 16-bit retrieve key
+// rho16 = rotl16(b, 1) ^ 1 = (mag << 1) | (1 - sign), the low half the state's bf16 bits b.  An
+// unsigned max over words is decided by the keys (equal keys = equal bits), so the Eq. 5 select
+// is one VIMNMX3 and the selected word's low half IS w' in bf16: the GEMV multiplies it directly
+// (fma.rn.f32.bf16, exact product and one rounding, the same bits as an fp32 FFMA of the
+// widened operands) and the reconstruction stores it as it is.  fp32 and quantised plans keep
+// 32-bit rho words (rotl(bits, 1) ^ 1; rotr(rho, 1) = bits of -w').
+template <typename E, int QB>
+constexpr bool kv_cells() { return sizeof(E) == 2 && QB == 0; }
+
+__device__ __forceinline__ uint32_t kv_word(uint32_t b16) {
+  return ((((b16 << 1) | (b16 >> 15)) & 0xFFFFu) ^ 1u) << 16 | b16;
+}
+
+// c + bf16(xb) * bf16(low half of w): one FHFMA.BF16
+__device__ __forceinline__ float fma_bf16_lo(uint32_t xb, uint32_t w, float c) {
+  float d;
+  asm("{.reg .b16 wl, wh, xl, xh;\n\t"
+      "mov.b32 {wl, wh}, %2;\n\t"
+      "mov.b32 {xl, xh}, %1;\n\t"
+      "fma.rn.f32.bf16 %0, xl, wl, %3;}"
+      : "=f"(d)
+      : "r"(xb), "r"(w), "f"(c));
+  return d;
+}
+
 template <int UPL, int MT, int HASH>
 struct LaneState {
   static constexpr int KR = fast_hash<MT, HASH>() ? MT : 1;
@@ -272,9 +298,11 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
         }
 #pragma unroll 2
         for (int k = threadIdx.x / pu; k < n; k += KS) {
-          const uint32_t b = ES == 2 ? ((uint32_t)reinterpret_cast<const uint16_t*>(src)[k] << 16)
-                                     : reinterpret_cast<const uint32_t*>(src)[k];
-          dst[k * 32] = rotl1(b) ^ 1u;
+          if constexpr (ES == 2) {
+            dst[k * 32] = kv_word(reinterpret_cast<const uint16_t*>(src)[k]);
+          } else {
+            dst[k * 32] = rotl1(reinterpret_cast<const uint32_t*>(src)[k]) ^ 1u;
+          }
         }
       }
     } else {
@@ -307,12 +335,12 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
 }
 
 // kernel prologue shared by the fast kernels: zero column of every slot row, staging mbarrier
-template <int UPL>
+template <int UPL, bool KV>
 __device__ __forceinline__ void q_prologue(const QArgs& A) {
   uint32_t* cells = q_cells();
   for (int e = threadIdx.x; e < UPL * A.M * 32; e += kQThreads) {
     const int lane = e & 31, vi = e >> 5, v = vi % UPL, i = vi / UPL;
-    cells[v * 32 * A.maxMN + (i * A.maxN + A.maxN - 1) * 32 + lane] = 1u;  // rho(+0)
+    cells[v * 32 * A.maxMN + (i * A.maxN + A.maxN - 1) * 32 + lane] = KV ? 0x00010000u : 1u;  // +0
   }
   if (threadIdx.x == 0) {
     mbar_init(q_bar(), 1);
@@ -412,8 +440,25 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 // store the UPL reconstructed weights (fp32 bit patterns; raw bf16 plans: bf16 bits in the high
 // half, exact) of lane L's units.  RNE: quantised plans round the fp32 dequantised value to bf16
 // (round to nearest even, L25); raw bf16 plans take the high half as it is.
-template <typename E, int UPL, bool RNE>
+template <typename E, int UPL, bool RNE, bool LO = false>
 __device__ __forceinline__ void store_units(E* dst, uint32_t (&wb)[UPL], bool full_tile, int nu, int lane) {
+  if constexpr (LO) {  // key|value words: the bf16 bits are the low halves
+    if (full_tile) {
+      if constexpr (UPL == 4) {
+        *reinterpret_cast<uint2*>(dst) = make_uint2(__byte_perm(wb[0], wb[1 % UPL], 0x5410),
+                                                    __byte_perm(wb[2 % UPL], wb[3 % UPL], 0x5410));
+      } else if constexpr (UPL == 2) {
+        *reinterpret_cast<uint32_t*>(dst) = __byte_perm(wb[0], wb[1 % UPL], 0x5410);
+      } else {
+        dst[0] = (E)(wb[0] & 0xFFFFu);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < UPL; ++v)
+        if (UPL * lane + v < nu) dst[v] = (E)(wb[v] & 0xFFFFu);
+    }
+    return;
+  }
   if constexpr (sizeof(E) == 2 && RNE) {
 #pragma unroll
     for (int v = 0; v < UPL; ++v) wb[v] = wb[v] + 0x7FFFu + ((wb[v] >> 16) & 1u);
@@ -457,15 +502,16 @@ __device__ __forceinline__ void store_units(E* dst, uint32_t (&wb)[UPL], bool fu
 //    beside k_gemv_fast's (register budget 112 + 32 per thread), wait there for the partials
 //    (griddepcontrol.wait), and the NEXT call's k_gemv_fast stages its sketch chunk while they
 //    reduce.
-template <typename E, int UPL, int MT, int HASH, bool GEMV, int QB>
+template <typename E, int UPL, int MT, int HASH, bool GEMV, int QB, bool XB>
 __device__ __forceinline__ void query_balanced(const QArgs& A) {
   constexpr int TJ = 32 * UPL;
+  constexpr bool KV = kv_cells<E, QB>();
   __shared__ int s_next;  // next subtile of the current segment (warps grab dynamically)
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x;
   const int64_t s_begin = A.cta_item[c], s_end = A.cta_item[c + 1];
   if (A.timeline && threadIdx.x == 0) A.timeline[c * 4 + 0] = gtimer();
-  q_prologue<UPL>(A);
+  q_prologue<UPL, KV>(A);
   uint32_t phase = 0;
   bool waited = false;
   // a segment = the part of [s_begin, s_end) inside one chunk
@@ -505,15 +551,22 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
         pdl_trigger();  // every CTA of this grid is running: the next launch may be scheduled
         waited = true;
       }
-      float nx[UPL];
+      float nx[UPL];    // rho words: -x (rotr(rho) decodes to -w'); key|value words: x
+      uint32_t xb[UPL];  // XB: x as bf16 bits (fma.rn.f32.bf16 operand)
 #pragma unroll
       for (int v = 0; v < UPL; ++v) {
         const int64_t j = cur.j0 + UPL * lane + v;
         float xv = 0.f;
-        if (GEMV && UPL * lane + v < cur.nu)
-          xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
-                        : reinterpret_cast<const float*>(A.x)[j];
-        nx[v] = -xv;  // rotr(rho) decodes to -w'
+        xb[v] = 0u;
+        if (GEMV && UPL * lane + v < cur.nu) {
+          if constexpr (XB) {
+            xb[v] = reinterpret_cast<const uint16_t*>(A.x)[j];
+          } else {
+            xv = A.x_bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.x)[j] << 16)
+                          : reinterpret_cast<const float*>(A.x)[j];
+          }
+        }
+        nx[v] = KV ? xv : -xv;
       }
       if (A.timeline && threadIdx.x == 0 && !stamped) A.timeline[c * 4 + 1] = gtimer();
       stamped = true;
@@ -546,8 +599,12 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
             if constexpr (fast_hash<MT, HASH>()) Rv = lds_rtab(rtab + 16u * r);
             float a = 0.f;
 #pragma unroll
-            for (int v = 0; v < UPL; ++v)
-              a = fmaf(nx[v], __uint_as_float(rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r))), a);
+            for (int v = 0; v < UPL; ++v) {
+              const uint32_t wsel = select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r);
+              if constexpr (KV && XB) a = fma_bf16_lo(xb[v], wsel, a);
+              else if constexpr (KV) a = fmaf(nx[v], __uint_as_float(wsel << 16), a);
+              else a = fmaf(nx[v], __uint_as_float(rotr1(wsel)), a);
+            }
             acc[r] = a;
           }
           const float t = transpose_reduce(acc, lane);
@@ -563,9 +620,11 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
             if constexpr (fast_hash<MT, HASH>()) Rv = lds_rtab(rtab + 16u * r);
             uint32_t wb[UPL];
 #pragma unroll
-            for (int v = 0; v < UPL; ++v)
-              wb[v] = rotr1(select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r)) ^ 0x80000000u;
-            store_units<E, UPL, QB != 0>(dst, wb, full_tile, cur.nu, lane);
+            for (int v = 0; v < UPL; ++v) {
+              const uint32_t wsel = select_rho<UPL, MT, HASH>(A, S, v, Rv, Ly.o_begin + r0 + r);
+              wb[v] = KV ? wsel : rotr1(wsel) ^ 0x80000000u;  // key|value: bf16 in the low half
+            }
+            store_units<E, UPL, QB != 0, KV>(dst, wb, full_tile, cur.nu, lane);
           }
         }
         sub = nxt;
@@ -587,16 +646,16 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
   }
 }
 
-template <typename E, int UPL, int MT, int HASH, int QB>
+template <typename E, int UPL, int MT, int HASH, int QB, bool XB>
 __global__ void __maxnreg__(USK_GEMV_MAXREG) k_gemv_fast(const __grid_constant__ QArgs A) {
-  query_balanced<E, UPL, MT, HASH, true, QB>(A);
+  query_balanced<E, UPL, MT, HASH, true, QB, XB>(A);
 }
 
 // K3 fast path: the same balanced chunk-major partition, staging and per-subtile select as
 // k_gemv_fast, with W' rows stored instead of multiplied (no x, no reduction).
 template <typename E, int UPL, int MT, int HASH, int QB>
 __global__ void __maxnreg__(USK_GEMV_MAXREG) k_recon_fast(const __grid_constant__ QArgs A) {
-  query_balanced<E, UPL, MT, HASH, false, QB>(A);
+  query_balanced<E, UPL, MT, HASH, false, QB, false>(A);
 }
 
 // Top-K (L29): [lo, hi) of the side-table entries of global row o
@@ -927,18 +986,18 @@ size_t smem_bytes(int upl, int maxMN, int es, int pu, int q = 0, int g_shift = 7
          sbuf_bytes(maxMN, q, g_shift, pu);
 }
 
-template <typename E, int UPL, bool GEMV, int QB>
+template <typename E, int UPL, bool GEMV, int QB, bool XB = false>
 void* pick_m(int M, int hash) {
   if constexpr (GEMV) {
-    if (hash == USK_HASH_IDENTITY) return (void*)k_gemv_fast<E, UPL, 0, USK_HASH_IDENTITY, QB>;
+    if (hash == USK_HASH_IDENTITY) return (void*)k_gemv_fast<E, UPL, 0, USK_HASH_IDENTITY, QB, XB>;
     if constexpr (QB == 0) {
       switch (M) {
-        case 1: return (void*)k_gemv_fast<E, UPL, 1, USK_HASH_X, QB>;
-        case 2: return (void*)k_gemv_fast<E, UPL, 2, USK_HASH_X, QB>;
+        case 1: return (void*)k_gemv_fast<E, UPL, 1, USK_HASH_X, QB, XB>;
+        case 2: return (void*)k_gemv_fast<E, UPL, 2, USK_HASH_X, QB, XB>;
         default: break;
       }
     }
-    return M == 3 ? (void*)k_gemv_fast<E, UPL, 3, USK_HASH_X, QB> : (void*)k_gemv_fast<E, UPL, 0, USK_HASH_X, QB>;
+    return M == 3 ? (void*)k_gemv_fast<E, UPL, 3, USK_HASH_X, QB, XB> : (void*)k_gemv_fast<E, UPL, 0, USK_HASH_X, QB, XB>;
   } else {
     if (hash == USK_HASH_IDENTITY) return (void*)k_recon_fast<E, UPL, 0, USK_HASH_IDENTITY, QB>;
     if constexpr (QB == 0) {
@@ -953,32 +1012,35 @@ void* pick_m(int M, int hash) {
 }
 
 // quantised plans: the GEMV does not depend on the weight dtype (dequantised fp32 values, fp32 y),
-// so only one E is instantiated for it; the reconstruct stores in the weight dtype
+// so only one E is instantiated for it; the reconstruct stores in the weight dtype.  Raw bf16 GEMVs
+// with bf16 x multiply the key|value cells with fma.rn.f32.bf16 (XB).
 template <int UPL, int QB>
-void* pick_q(bool gemv, bool bf16, int M, int hash) {
+void* pick_q(bool gemv, bool bf16, bool xbf16, int M, int hash) {
   if (gemv) {
-    if constexpr (QB == 0)
-      return bf16 ? pick_m<uint16_t, UPL, true, 0>(M, hash) : pick_m<uint32_t, UPL, true, 0>(M, hash);
-    else
+    if constexpr (QB == 0) {
+      if (!bf16) return pick_m<uint32_t, UPL, true, 0>(M, hash);
+      return xbf16 ? pick_m<uint16_t, UPL, true, 0, true>(M, hash) : pick_m<uint16_t, UPL, true, 0, false>(M, hash);
+    } else {
       return pick_m<uint32_t, UPL, true, QB>(M, hash);
+    }
   }
   return bf16 ? pick_m<uint16_t, UPL, false, QB>(M, hash) : pick_m<uint32_t, UPL, false, QB>(M, hash);
 }
 
 template <int UPL>
-void* pick_upl(bool gemv, bool bf16, int M, int hash, int q) {
+void* pick_upl(bool gemv, bool bf16, bool xbf16, int M, int hash, int q) {
   switch (q) {
-    case 4: return pick_q<UPL, 4>(gemv, bf16, M, hash);
-    case 8: return pick_q<UPL, 8>(gemv, bf16, M, hash);
-    default: return pick_q<UPL, 0>(gemv, bf16, M, hash);
+    case 4: return pick_q<UPL, 4>(gemv, bf16, xbf16, M, hash);
+    case 8: return pick_q<UPL, 8>(gemv, bf16, xbf16, M, hash);
+    default: return pick_q<UPL, 0>(gemv, bf16, xbf16, M, hash);
   }
 }
 
-void* pick_fast(int upl, bool gemv, bool bf16, int M, int hash, int q) {
+void* pick_fast(int upl, bool gemv, bool bf16, bool xbf16, int M, int hash, int q) {
   switch (upl) {
-    case 4: return pick_upl<4>(gemv, bf16, M, hash, q);
-    case 2: return pick_upl<2>(gemv, bf16, M, hash, q);
-    default: return pick_upl<1>(gemv, bf16, M, hash, q);
+    case 4: return pick_upl<4>(gemv, bf16, xbf16, M, hash, q);
+    case 2: return pick_upl<2>(gemv, bf16, xbf16, M, hash, q);
+    default: return pick_upl<1>(gemv, bf16, xbf16, M, hash, q);
   }
 }
 
@@ -1044,7 +1106,8 @@ struct Geom {
 // budget (default 220 KB); the raw staging buffer shrinks to pieces of pu units before UPL does.
 // Grid: one CTA per SM (USK_GEMV_CPS per SM for tuning), never more than the work items.
 // USK_UPL / USK_GEMV_SMEM_KB / USK_GEMV_CPS override (tuning).
-Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n, bool gemv = true) {
+Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* rows, int n, bool gemv = true,
+                   bool xbf16 = false) {
   Geom G;
   for (int k = 0; k < n; ++k) G.maxMN = std::max(G.maxMN, pl->M * (pl->layers[layers[k]].max_ncols + 1));
   const int64_t in = pl->layers[layers[0]].in;
@@ -1060,7 +1123,7 @@ Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* row
       for (int pu = 32 * upl; pu >= 8; pu /= 2) {
         const size_t sm = smem_bytes(upl, G.maxMN, es, pu, pl->q, ilog2(pl->G));
         if (sm > cap) continue;
-        void* kern = pick_fast(upl, gemv, bf16, pl->M, pl->hash, pl->q);
+        void* kern = pick_fast(upl, gemv, bf16, xbf16, pl->M, pl->hash, pl->q);
         const int occ = occupancy(kern, sm);
         if (occ < 1) continue;
         G.upl = upl;
@@ -1345,7 +1408,7 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
     return launch_gemv_outrow(pl, sketch, layers, o0, o1, n, x, x_dtype, y, y_dtype, st);
   std::vector<int64_t> rows(n);
   for (int k = 0; k < n; ++k) rows[k] = o1[k] - o0[k];
-  Geom G = fast_eligible(pl) ? gemv_geometry(pl, layers, rows.data(), n) : Geom{};
+  Geom G = fast_eligible(pl) ? gemv_geometry(pl, layers, rows.data(), n, true, x_dtype == USK_BF16) : Geom{};
   if (G.upl) {
     const int64_t in = pl->layers[layers[0]].in;
     QArgs A = base_args(pl, sketch, in, G);
