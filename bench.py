@@ -253,6 +253,8 @@ def run_usk(args):
     def step_grouped():
         warm()
         for gi, g in enumerate(groups):
+            if args.prefetch_next and gi + 1 < len(groups):  # L2 hint: the next group's sketch + metadata
+                usk.prefetch_l2(plan, sketch, groups[gi + 1][0], groups[gi + 1][-1] + 1)
             usk.linear_batch(plan, sketch, g, xg[gi], [out_of(l) for l in g], ws_group[gi],
                              ranges=[ranges[l] for l in g])
             gather(g)
@@ -644,6 +646,8 @@ def main():
     ap.add_argument("--no-q4", action="store_true", help="skip the extra plans (q4 states, classes, output-row units)")
     ap.add_argument("--no-8b", action="store_true", help="skip the Llama-3-8B (config 5) build + decode at N=1")
     ap.add_argument("--no-prefill", action="store_true", help="skip the config-4 prefill passes")
+    ap.add_argument("--prefetch-next", action="store_true",
+                    help="before each grouped call, usk_prefetch_l2 of the next group's sketch bytes (L2 hint)")
     ap.add_argument("--prefetch", action="store_true",
                     help="start each decode step with usk_prefetch_l2 of the whole sketch (measured: no gain)")
     args = ap.parse_args()

@@ -26,6 +26,7 @@
 //     (q|k|v, gate|up) in one call.
 //   * K3 (k_recon_fast): the same skeleton storing W' rows (8-byte stores for bf16, UPL = 4).
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -45,13 +46,18 @@ namespace {
 constexpr int kQThreads = USK_QUERY_THREADS;
 constexpr int kMaxBatch = 8;
 constexpr int kMaxCtas = 256;  // GEMV compute grid (one CTA per SM)
+// USK_TRACE stamps per CTA: start, staged (first segment: + wait + x), compute done, exit; first bulk
+// copy issued, first piece landed, first segment converted, griddepcontrol.wait returned
+constexpr int kTS = 8;
 #ifndef USK_SUB_ROWS
 #define USK_SUB_ROWS 16
 #endif
-constexpr int kSubRows = USK_SUB_ROWS;  // rows per warp work item (subtile): 8 or 16
+constexpr int kSubRows = USK_SUB_ROWS;  // rows per warp work item (subtile) of the default kernels: 8 or 16
 static_assert(kSubRows == 8 || kSubRows == 16, "subtile rows");
+// The raw-bf16 GEMV is also built with 8-row subtiles: the host picks them for calls whose 16-row
+// items would leave the last round of a CTA's warps mostly idle (q|k|v, down of Llama-3.2-1B).
 constexpr int kRTabWordOffset = 32 + 160;  // zero cells + chunk unit offsets (<= 129)
-constexpr int kRTabWords = (kQThreads / 32) * kSubRows * 4;  // per warp: kSubRows x {R_0, R_1, R_2, 0}
+constexpr int kRTabWords = (kQThreads / 32) * 16 * 4;  // per warp: up to 16 rows x {R_0, R_1, R_2, 0}
 constexpr int kCellsWordOffset = kRTabWordOffset + kRTabWords;
 
 extern __shared__ __align__(16) uint32_t qsm[];  // dynamic shared memory of the query kernels
@@ -111,7 +117,12 @@ struct QArgs {
   const float* scales;             // quantised plans: fp32 group scales (in the sketch buffer)
   int32_t es;                      // bytes of a raw state (Top-K side-table values)
   int32_t cta_item[kMaxCtas + 1];  // GEMV: CTA c computes work items [cta_item[c], cta_item[c + 1])
-  unsigned long long* timeline;  // tuning only (USK_TRACE): 4 globaltimer stamps per CTA
+  // raw plans: CTA c's first bulk copy, precomputed on the host from the plan's unit offsets (no
+  // dependent global load before it): 16-B aligned sketch byte offset | copy shift (low 4 bits), bytes
+  int32_t first_ok;
+  uint64_t first_a0s[kMaxCtas];
+  uint32_t first_bytes[kMaxCtas];
+  unsigned long long* timeline;  // tuning only (USK_TRACE): kTS globaltimer stamps per CTA
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -262,7 +273,7 @@ __device__ __forceinline__ void stage_issue(const QArgs& A, int64_t ubase, int p
 // query loop is the same for every plan (the rho of an fp32 value).
 template <typename E, int UPL, int QB>
 __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int nu, uint32_t& phase,
-                                            bool first_issued) {
+                                            bool first_issued, unsigned long long* landed = nullptr) {
   constexpr int ES = sizeof(E);
   uint32_t* cells = q_cells();
   const unsigned char* raw = q_raw<E, UPL>(A);
@@ -287,6 +298,7 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
     __syncthreads();  // shift visible
     mbar_wait(q_bar(), phase);
     phase ^= 1u;
+    if (landed && pa == 0 && threadIdx.x == 0) *landed = gtimer();
     uint32_t* dst = cells + (ul % UPL) * 32 * A.maxMN + ul / UPL;
     const int KS = kQThreads / pu;
     if constexpr (QB == 0) {
@@ -336,13 +348,13 @@ __device__ __forceinline__ void stage_units(const QArgs& A, int64_t ubase, int n
 
 // kernel prologue shared by the fast kernels: zero column of every slot row, staging mbarrier
 template <int UPL, bool KV>
-__device__ __forceinline__ void q_prologue(const QArgs& A) {
+__device__ __forceinline__ void q_prologue(const QArgs& A, bool init_bar = true) {
   uint32_t* cells = q_cells();
   for (int e = threadIdx.x; e < UPL * A.M * 32; e += kQThreads) {
     const int lane = e & 31, vi = e >> 5, v = vi % UPL, i = vi / UPL;
     cells[v * 32 * A.maxMN + (i * A.maxN + A.maxN - 1) * 32 + lane] = KV ? 0x00010000u : 1u;  // +0
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && init_bar) {
     mbar_init(q_bar(), 1);
     fence_mbar_init();
   }
@@ -385,11 +397,11 @@ __device__ __forceinline__ uint32_t select_rho(const QArgs& A, const LaneState<U
 
 // per-warp table of the subtile rows' position mixes: lane r < kSubRows writes row r's
 // {R_0, R_1, R_2} mod 2^23 (rows past the layer repeat its last row)
-template <int MT, int HASH>
+template <int MT, int HASH, int SR>
 __device__ __forceinline__ void fill_rtab(const QArgs& A, uint32_t rtab, int64_t o_first, int64_t o_last, int lane) {
   if constexpr (fast_hash<MT, HASH>()) {
     __syncwarp();  // the previous subtile's reads are done
-    if (lane < kSubRows) {
+    if (lane < SR) {
       const uint32_t o = (uint32_t)min(o_first + lane, o_last);
       const uint32_t r0 = fmix32(o ^ A.hc.rho[0]) & 0x7FFFFFu;
       const uint32_t r1 = MT > 1 ? fmix32(o ^ A.hc.rho[1]) & 0x7FFFFFu : 0u;
@@ -410,9 +422,10 @@ __device__ __forceinline__ uint4 lds_rtab(uint32_t a) {
 // Row r of the warp's kSubRows partial rows ends on the lanes congruent to r mod kSubRows
 // (fixed-order butterfly: log2(kSubRows) exchange-and-halve stages inside each group of kSubRows
 // lanes, then the groups are added).
-__device__ __forceinline__ float transpose_reduce(float (&acc)[kSubRows], int lane) {
+template <int SR>
+__device__ __forceinline__ float transpose_reduce(float (&acc)[SR], int lane) {
 #pragma unroll
-  for (int m = kSubRows / 2; m >= 1; m >>= 1) {
+  for (int m = SR / 2; m >= 1; m >>= 1) {
     const bool up = (lane & m) != 0;
 #pragma unroll
     for (int i = 0; i < m; ++i) {
@@ -423,7 +436,7 @@ __device__ __forceinline__ float transpose_reduce(float (&acc)[kSubRows], int la
   }
   float t = acc[0];
 #pragma unroll
-  for (int m = kSubRows; m < 32; m <<= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+  for (int m = SR; m < 32; m <<= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
   return t;
 }
 
@@ -502,7 +515,7 @@ __device__ __forceinline__ void store_units(E* dst, uint32_t (&wb)[UPL], bool fu
 //    beside k_gemv_fast's (register budget 112 + 32 per thread), wait there for the partials
 //    (griddepcontrol.wait), and the NEXT call's k_gemv_fast stages its sketch chunk while they
 //    reduce.
-template <typename E, int UPL, int MT, int HASH, bool GEMV, int QB, bool XB>
+template <typename E, int UPL, int MT, int HASH, bool GEMV, int QB, bool XB, int SR = kSubRows>
 __device__ __forceinline__ void query_balanced(const QArgs& A) {
   constexpr int TJ = 32 * UPL;
   constexpr bool KV = kv_cells<E, QB>();
@@ -510,8 +523,18 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x;
   const int64_t s_begin = A.cta_item[c], s_end = A.cta_item[c + 1];
-  if (A.timeline && threadIdx.x == 0) A.timeline[c * 4 + 0] = gtimer();
-  q_prologue<UPL, KV>(A);
+  if (A.timeline && threadIdx.x == 0) A.timeline[c * kTS + 0] = gtimer();
+  const bool pre = QB == 0 && A.first_ok && s_begin < s_end;
+  if (pre && threadIdx.x == 0) {  // first piece in flight before anything else
+    const uint64_t a0s = A.first_a0s[c];
+    const uint32_t bytes = A.first_bytes[c];
+    mbar_init(q_bar(), 1);
+    fence_mbar_init();
+    mbar_arrive_expect_tx(q_bar(), bytes);
+    bulk_g2s(q_raw<E, UPL>(A), reinterpret_cast<const unsigned char*>(A.sketch) + (a0s & ~uint64_t(15)), bytes, q_bar());
+    qsm[34] = (uint32_t)(a0s & 15u);  // copy shift
+  }
+  q_prologue<UPL, KV>(A, !pre);
   uint32_t phase = 0;
   bool waited = false;
   // a segment = the part of [s_begin, s_end) inside one chunk
@@ -538,17 +561,21 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
     Seg cur = seg_at(s_begin);
     if (threadIdx.x == 0) {
       s_next = cur.sub_a;
-      stage_issue<E, UPL, QB>(A, cur.ubase, 0, min(A.piece_units, cur.nu));  // first piece in flight
+      if (!pre) stage_issue<E, UPL, QB>(A, cur.ubase, 0, min(A.piece_units, cur.nu));  // first piece in flight
+      if (A.timeline) A.timeline[c * kTS + 4] = gtimer();
     }
     bool stamped = false;
     while (true) {
       const QLayer& Ly = A.layer[cur.li];
       LaneState<UPL, MT, HASH> S;
       lane_setup<UPL, MT, HASH>(A, cur.ubase, cur.nu, S);  // overlaps the copy
-      stage_units<E, UPL, QB>(A, cur.ubase, cur.nu, phase, true);  // sketch only: before the wait
+      stage_units<E, UPL, QB>(A, cur.ubase, cur.nu, phase, true,
+                              (A.timeline && !waited) ? A.timeline + c * kTS + 5 : nullptr);  // sketch only: before the wait
       if (!waited) {
+        if (A.timeline && threadIdx.x == 0) A.timeline[c * kTS + 6] = gtimer();
         pdl_wait();     // x may be written by the previous kernel on the stream
         pdl_trigger();  // every CTA of this grid is running: the next launch may be scheduled
+        if (A.timeline && threadIdx.x == 0) A.timeline[c * kTS + 7] = gtimer();
         waited = true;
       }
       float nx[UPL];    // rho words: -x (rotr(rho) decodes to -w'); key|value words: x
@@ -568,7 +595,7 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
         }
         nx[v] = KV ? xv : -xv;
       }
-      if (A.timeline && threadIdx.x == 0 && !stamped) A.timeline[c * 4 + 1] = gtimer();
+      if (A.timeline && threadIdx.x == 0 && !stamped) A.timeline[c * kTS + 1] = gtimer();
       stamped = true;
       // the raw buffer is free: prefetch the next segment's first piece under this one's math
       const bool more = cur.end < s_end;
@@ -584,17 +611,17 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
       };
       const int sub_end = cur.sub_end;
       const int chunk = cur.chunk;
-      const uint32_t rtab = smem_u32(qsm + kRTabWordOffset) + (uint32_t)(threadIdx.x >> 5) * (kSubRows * 16u);
+      const uint32_t rtab = smem_u32(qsm + kRTabWordOffset) + (uint32_t)(threadIdx.x >> 5) * (16u * 16u);
       int sub = next_sub();
-      if (sub < sub_end) fill_rtab<MT, HASH>(A, rtab, Ly.o_begin + (int64_t)sub * kSubRows, Ly.o_begin + Ly.rows - 1, lane);
+      if (sub < sub_end) fill_rtab<MT, HASH, SR>(A, rtab, Ly.o_begin + (int64_t)sub * SR, Ly.o_begin + Ly.rows - 1, lane);
       while (sub < sub_end) {
         const int nxt = next_sub();  // issued now, consumed after this subtile's math
-        const int64_t r0 = (int64_t)sub * kSubRows;
-        const int nrow = (int)min((int64_t)kSubRows, Ly.rows - r0);
+        const int64_t r0 = (int64_t)sub * SR;
+        const int nrow = (int)min((int64_t)SR, Ly.rows - r0);
         if constexpr (GEMV) {
-          float acc[kSubRows];
+          float acc[SR];
 #pragma unroll
-          for (int r = 0; r < kSubRows; ++r) {
+          for (int r = 0; r < SR; ++r) {
             uint4 Rv = make_uint4(0, 0, 0, 0);
             if constexpr (fast_hash<MT, HASH>()) Rv = lds_rtab(rtab + 16u * r);
             float a = 0.f;
@@ -607,14 +634,14 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
             }
             acc[r] = a;
           }
-          const float t = transpose_reduce(acc, lane);
+          const float t = transpose_reduce<SR>(acc, lane);
           if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = t;
         } else {
           // W' rows: lane L writes its UPL units of each row (bf16: one 8-byte store for UPL = 4)
           const bool full_tile = (cur.nu == TJ);
           E* dst = reinterpret_cast<E*>(Ly.w_out) + r0 * Ly.ld_out + cur.j0 + UPL * lane;
 #pragma unroll 4
-          for (int r = 0; r < kSubRows; ++r, dst += Ly.ld_out) {
+          for (int r = 0; r < SR; ++r, dst += Ly.ld_out) {
             if (r >= nrow) continue;
             uint4 Rv = make_uint4(0, 0, 0, 0);
             if constexpr (fast_hash<MT, HASH>()) Rv = lds_rtab(rtab + 16u * r);
@@ -628,7 +655,7 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
           }
         }
         sub = nxt;
-        if (sub < sub_end) fill_rtab<MT, HASH>(A, rtab, Ly.o_begin + (int64_t)sub * kSubRows, Ly.o_begin + Ly.rows - 1, lane);
+        if (sub < sub_end) fill_rtab<MT, HASH, SR>(A, rtab, Ly.o_begin + (int64_t)sub * SR, Ly.o_begin + Ly.rows - 1, lane);
       }
       __syncthreads();  // cells and s_next are reused by the next segment
       if (!more) break;
@@ -641,14 +668,14 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
     pdl_trigger();
   }
   if (A.timeline && lane == 0) {
-    atomicMax(&A.timeline[c * 4 + 2], gtimer());
-    atomicMax(&A.timeline[c * 4 + 3], gtimer());
+    atomicMax(&A.timeline[c * kTS + 2], gtimer());
+    atomicMax(&A.timeline[c * kTS + 3], gtimer());
   }
 }
 
-template <typename E, int UPL, int MT, int HASH, int QB, bool XB>
+template <typename E, int UPL, int MT, int HASH, int QB, bool XB, int SR = kSubRows>
 __global__ void __maxnreg__(USK_GEMV_MAXREG) k_gemv_fast(const __grid_constant__ QArgs A) {
-  query_balanced<E, UPL, MT, HASH, true, QB, XB>(A);
+  query_balanced<E, UPL, MT, HASH, true, QB, XB, SR>(A);
 }
 
 // K3 fast path: the same balanced chunk-major partition, staging and per-subtile select as
@@ -704,7 +731,7 @@ constexpr int kRedThreads = 256;
 // coalesced float4 load each, then an xor butterfly over the group (every lane ends with the same
 // bits, so the result is deterministic).
 __global__ void __launch_bounds__(kRedThreads, 8) k_gemv_reduce(const __grid_constant__ QArgs A) {
-  if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * 4 + 0] = gtimer();
+  if (A.timeline && threadIdx.x == 0) A.timeline[blockIdx.x * kTS + 0] = gtimer();
   pdl_trigger();  // the next call's compute kernel may be scheduled (it stages before its own wait)
   // every kernel-parameter read happens before the wait: a first touch of a parameter line misses
   // the SM's constant cache (~1 us), which would otherwise sit on the critical path
@@ -725,7 +752,7 @@ __global__ void __launch_bounds__(kRedThreads, 8) k_gemv_reduce(const __grid_con
   unsigned long long* const tl = A.timeline;
   asm volatile("" ::"l"(p), "l"(yp), "l"(n_out), "r"(nch), "r"((int)y_bf16), "l"(tl) : "memory");
   pdl_wait();     // all chunk partials written
-  if (tl && threadIdx.x == 0) tl[blockIdx.x * 4 + 1] = gtimer();
+  if (tl && threadIdx.x == 0) tl[blockIdx.x * kTS + 1] = gtimer();
   float t = 0.f;
   if (r < A.rows) {
     for (int c = 4 * j; c < nch; c += 4 * L) {
@@ -759,8 +786,8 @@ __global__ void __launch_bounds__(kRedThreads, 8) k_gemv_reduce(const __grid_con
     }
   }
   if (tl && (threadIdx.x & 31) == 0) {
-    atomicMax(&tl[blockIdx.x * 4 + 2], gtimer());
-    atomicMax(&tl[blockIdx.x * 4 + 3], gtimer());
+    atomicMax(&tl[blockIdx.x * kTS + 2], gtimer());
+    atomicMax(&tl[blockIdx.x * kTS + 3], gtimer());
   }
 }
 
@@ -1093,6 +1120,7 @@ int env_int(const char* name, int dflt) {
 
 struct Geom {
   int upl = 0;
+  int sub = kSubRows;  // rows per subtile item
   int maxMN = 0;
   int pu = 0;  // units per staging bulk copy
   size_t smem = 0;
@@ -1137,9 +1165,36 @@ Geom gemv_geometry(const usk_plan* pl, const int32_t* layers, const int64_t* row
     }
   }
   if (!G.upl) return G;
+  // 8-row subtiles (raw bf16 GEMV with bf16 x, M = 3): when a CTA's share of 16-row items ends in a
+  // mostly idle round of its 16 warps.  Estimated CTA time = rounds x item time, the 8-row loop
+  // costing ~15 % more per weight in the product (in-graph trace: Llama-3.2-1B down, 3.5 items per
+  // warp at 16 rows, mean compute 13.8 vs 12.8 us with 8 rows; the loop alone: 1792 vs 1898 G w/s).
+  static const int forced_sub = env_int("USK_SUB", 0);
+  auto items_at = [&](int sub) {
+    int64_t it = 0;
+    for (int k = 0; k < n; ++k) it += ((in + 32 * G.upl - 1) / (32 * G.upl)) * ((rows[k] + sub - 1) / sub);
+    return it;
+  };
+  if (gemv && xbf16 && pl->dtype == USK_BF16 && pl->q == 0 && pl->M == 3 && pl->hash == USK_HASH_X && kSubRows == 16) {
+    const int warps = kQThreads / 32;
+    auto est = [&](int sub) {
+      const int64_t it = items_at(sub);
+      const int64_t ctas = std::min<int64_t>(G.grid, it);
+      const double per = (double)it / (double)ctas;
+      return std::ceil(per / warps) * sub * (sub == 8 ? 1.15 : 1.0);
+    };
+    const int want = forced_sub ? forced_sub : (est(8) < est(16) ? 8 : 16);
+    if (want == 8 && G.upl == 4) {
+      void* k8 = (void*)k_gemv_fast<uint16_t, 4, 3, USK_HASH_X, 0, true, 8>;
+      if (occupancy(k8, G.smem) >= 1) {
+        G.sub = 8;
+        G.kern = k8;
+      }
+    }
+  }
   for (int k = 0; k < n; ++k) {
     G.n_chunks.push_back((int)((in + 32 * G.upl - 1) / (32 * G.upl)));
-    G.n_sub.push_back((int)((rows[k] + kSubRows - 1) / kSubRows));
+    G.n_sub.push_back((int)((rows[k] + G.sub - 1) / G.sub));
     G.items += (int64_t)G.n_chunks.back() * G.n_sub.back();
   }
   G.grid = (int)std::min<int64_t>(G.grid, std::max<int64_t>(G.items, 1));
@@ -1195,7 +1250,7 @@ int partition_items(QArgs& A, const Geom& G) {
   const int64_t I = A.items;
   const int cap = (int)std::min<int64_t>(std::min<int64_t>(G.grid, I), kMaxCtas);
   static const int forced_p = env_int("USK_SWITCH_ITEMS", -1);
-  const int64_t P = forced_p >= 0 ? forced_p : 8 + (int64_t)32 * G.upl * G.maxMN / 1024;
+  const int64_t P = (forced_p >= 0 ? forced_p : 8 + (int64_t)32 * G.upl * G.maxMN / 1024) * 16 / G.sub;  // in items
   auto chunk_end = [&](int64_t s) {
     int li = 0;
     while (li + 1 < A.n_layers && A.layer[li + 1].item_begin <= s) ++li;
@@ -1230,6 +1285,36 @@ int partition_items(QArgs& A, const Geom& G) {
     else lo = mid + 1;
   }
   return fill(lo, true);
+}
+
+// Raw plans: each CTA's first bulk copy (the first piece of the chunk at cta_item[c]) from the
+// host copy of the unit offsets, the same bytes stage_issue would compute on the device.
+void first_copies(const usk_plan* pl, QArgs& A, const Geom& G, int grid) {
+  A.first_ok = 0;
+  if (pl->q != 0) return;
+  const int es = pl->cell_bytes();
+  const int TJ = 32 * G.upl;
+  for (int c = 0; c < grid; ++c) {
+    const int64_t s = A.cta_item[c];
+    if (s >= A.cta_item[c + 1]) {
+      A.first_a0s[c] = 0;
+      A.first_bytes[c] = 0;
+      continue;
+    }
+    int li = 0;
+    while (li + 1 < A.n_layers && A.layer[li + 1].item_begin <= s) ++li;
+    const QLayer& L = A.layer[li];
+    const int64_t chunk = (s - L.item_begin) / L.n_sub;
+    const int64_t j0 = chunk * TJ;
+    const int nu = (int)std::min<int64_t>(TJ, A.in - j0);
+    const int pn = std::min(G.pu, nu);
+    const int64_t ub = L.unit_base + j0;
+    const uint64_t g0 = (uint64_t)pl->h_offsets[ub] * es, g1 = (uint64_t)pl->h_offsets[ub + pn] * es;
+    const uint64_t a0 = g0 & ~uint64_t(15), a1 = (g1 + 15) & ~uint64_t(15);
+    A.first_a0s[c] = a0 | (g0 - a0);
+    A.first_bytes[c] = (uint32_t)(a1 - a0);
+  }
+  A.first_ok = 1;
 }
 
 // USK_TRACE (tuning only): per-CTA %globaltimer stamps of every query launch, slot per issue
@@ -1307,11 +1392,11 @@ usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl,
     std::lock_guard<std::mutex> lock(T.mu);
     if (T.on) {  // tuning only: stamps into this launch's slot of the ring
       if (!T.d) {
-        USK_CUDA(cudaMalloc(&T.d, sizeof(unsigned long long) * 4 * Trace::kCap));
-        USK_CUDA(cudaMemset(T.d, 0, sizeof(unsigned long long) * 4 * Trace::kCap));
+        USK_CUDA(cudaMalloc(&T.d, sizeof(unsigned long long) * kTS * Trace::kCap));
+        USK_CUDA(cudaMemset(T.d, 0, sizeof(unsigned long long) * kTS * Trace::kCap));
       }
       if (T.cursor + grid > Trace::kCap) T.cursor = 0, T.grids.clear();
-      B.timeline = T.d + 4 * T.cursor;
+      B.timeline = T.d + kTS * T.cursor;
       T.cursor += grid;
       T.grids.push_back(grid);
     }
@@ -1437,6 +1522,7 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
     }
     if (!A.n_layers) return USK_OK;
     const int grid = partition_items(A, G);
+    first_copies(pl, A, G, grid);
     A.red_lanes = 1;
     while (A.red_lanes < 32 && 4 * A.red_lanes < G.n_chunks[0]) A.red_lanes *= 2;
     usk_status s1 = launch_q(G.kern, A, grid, G.smem, true, st);
@@ -1488,7 +1574,9 @@ usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l,
     Ly.ld_out = ld;
     A.items = (int64_t)Ly.n_chunks * Ly.n_sub;
     A.rows = rows;
-    usk_status s = launch_q(G.kern, A, partition_items(A, G), G.smem, false, st);
+    const int grid = partition_items(A, G);
+    first_copies(pl, A, G, grid);
+    usk_status s = launch_q(G.kern, A, grid, G.smem, false, st);
     if (s != USK_OK) return s;
   } else {
     GenQ Q = make_genq(pl, l, sketch);
@@ -1554,7 +1642,7 @@ int32_t usk_trace_read(uint64_t* stamps, int64_t cap_stamps, int32_t* grids, int
   std::lock_guard<std::mutex> lock(T.mu);
   if (!T.on || !T.d) return 0;
   if (cudaDeviceSynchronize() != cudaSuccess) return 0;
-  const int64_t n = std::min<int64_t>(4 * T.cursor, cap_stamps);
+  const int64_t n = std::min<int64_t>(usk::kTS * T.cursor, cap_stamps);
   if (stamps && n > 0 && cudaMemcpy(stamps, T.d, n * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return 0;
   const int32_t nl = (int32_t)T.grids.size();
   for (int32_t k = 0; grids && k < std::min(nl, cap_launches); ++k) grids[k] = T.grids[k];
@@ -1566,7 +1654,7 @@ void usk_trace_reset(void) {
   std::lock_guard<std::mutex> lock(T.mu);
   T.cursor = 0;
   T.grids.clear();
-  if (T.d) (void)cudaMemset(T.d, 0, sizeof(unsigned long long) * 4 * usk::Trace::kCap);
+  if (T.d) (void)cudaMemset(T.d, 0, sizeof(unsigned long long) * usk::kTS * usk::Trace::kCap);
 }
 
 }  // extern "C"

@@ -327,15 +327,16 @@ def launch_count(reset: bool = False) -> int:
 
 
 def trace_read(max_launches: int = 4096, max_ctas: int = 1 << 18):
-    """Tuning only (USK_TRACE=1): per launch, an int64 array [grid, 4] of %globaltimer stamps
-    (start, staged, compute done, exit) of every CTA, launches in issue order."""
+    """Tuning only (USK_TRACE=1): per launch, an int64 array [grid, 8] of %globaltimer stamps of
+    every CTA (start, staged, compute done, exit; query kernels also: first bulk copy issued, first
+    piece landed, first segment converted, griddepcontrol.wait returned), launches in issue order."""
     import numpy as np
-    stamps = np.zeros(4 * max_ctas, np.uint64)
+    stamps = np.zeros(8 * max_ctas, np.uint64)
     grids = np.zeros(max_launches, np.int32)
     n = int(lib.usk_trace_read(stamps.ctypes.data, stamps.size, grids.ctypes.data, max_launches))
     out, c = [], 0
     for g in grids[:n]:
-        out.append(stamps[4 * c:4 * (c + int(g))].astype(np.int64).reshape(int(g), 4))
+        out.append(stamps[8 * c:8 * (c + int(g))].astype(np.int64).reshape(int(g), 8))
         c += int(g)
     return out
 

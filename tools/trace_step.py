@@ -107,6 +107,34 @@ overl = sum(min(0.0, r["gap"]) for r in rows)
 comp = sum(r["comp"] for r in rows)
 print(f"sum spans {spans:.1f} us, sum gaps {gaps:.1f} us (overlap {overl:.1f}), sum mean-compute {comp:.1f} us, "
       f"step {step_us:.1f} us")
+# critical path per grouped call: previous reduce end -> first CTA past its wait (release + x load),
+# CTA compute starts spread (staging exposed after the release), compute (first start -> last compute
+# end), last compute end -> this call's reduce end (the reduce hop)
+if per == 2:
+    cp = {"release": [], "start_spread": [], "compute": [], "hop": [], "comp_mean": []}
+    sub = {"issue": [], "land": [], "convert": [], "wait": [], "x": []}  # mean per-CTA stage phases
+    for g in range(1, len(groups)):
+        tc, trd, tprev = tr[2 * g], tr[2 * g + 1], tr[2 * g - 1]
+        r_prev = int(tprev[:, 3].max())
+        sg = tc[:, 1].astype(np.int64)
+        cd = tc[:, 2].astype(np.int64)
+        cp["release"].append((sg.min() - r_prev) / 1e3)
+        cp["start_spread"].append((sg.max() - sg.min()) / 1e3)
+        cp["compute"].append((cd.max() - sg.max()) / 1e3)
+        cp["comp_mean"].append(float((cd - sg).mean()) / 1e3)
+        cp["hop"].append((int(trd[:, 3].max()) - cd.max()) / 1e3)
+        st0, iss, lnd, cvt, wtd = (tc[:, c].astype(np.int64) for c in (0, 4, 5, 6, 7))
+        sub["issue"].append(float((iss - st0).mean()) / 1e3)
+        sub["land"].append(float((lnd - iss).mean()) / 1e3)
+        sub["convert"].append(float((cvt - lnd).mean()) / 1e3)
+        sub["wait"].append(float((wtd - cvt).mean()) / 1e3)
+        sub["x"].append(float((sg - wtd).mean()) / 1e3)
+    print("critical path per call (us, mean over calls 1..):", " ".join(f"{k}={np.mean(v):.2f}" for k, v in cp.items()))
+    for kd in ("qkv", "o", "gate_up", "down"):
+        idx = [g - 1 for g in range(1, len(groups)) if groups and kinds[2 * g] == kd]
+        print(f"  {kd:8s}", " ".join(f"{k}={np.mean([v[i] for i in idx]):.2f}" for k, v in cp.items()),
+              f"sum={np.mean([cp['release'][i] + cp['start_spread'][i] + cp['compute'][i] + cp['hop'][i] for i in idx]):.2f}")
+        print(f"  {'':8s} stage phases (CTA mean):", " ".join(f"{k}={np.mean([v[i] for i in idx]):.2f}" for k, v in sub.items()))
 if args.npz:
     np.savez(args.npz, **{f"l{k}": t for k, t in enumerate(tr)}, kinds=np.array(kinds))
 if args.csv:
