@@ -35,6 +35,8 @@ struct Args {
   int work_ns;
   int mode;
   const unsigned* rep;  // graph replay counter (epoch base)
+  unsigned long long* ts;  // [148][4] globaltimer stamps of this call: start, work done, arrived, exit
+  int fence;               // blk: 0 atom.acq_rel, 1 threadfence + relaxed atomicAdd, 2 no fence (timing only)
 };
 
 __global__ void __launch_bounds__(512, 1) kc(const __grid_constant__ Args A) {
@@ -44,6 +46,7 @@ __global__ void __launch_bounds__(512, 1) kc(const __grid_constant__ Args A) {
   pdl_trigger();
   const float xv = A.x[threadIdx.x & 255];
   const unsigned long long t0 = gt();
+  if (threadIdx.x == 0) A.ts[blockIdx.x * 4 + 0] = t0;
   while (gt() - t0 < (unsigned long long)A.work_ns) {
   }
   // this CTA's partials: rows r with r % gridDim == blockIdx, all kPart slots (stand-in for chunk partials)
@@ -74,10 +77,20 @@ __global__ void __launch_bounds__(512, 1) kc(const __grid_constant__ Args A) {
     __shared__ unsigned last;
     __syncthreads();
     if (threadIdx.x == 0) {
+      A.ts[blockIdx.x * 4 + 1] = gt();
       unsigned prev;
-      asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(A.ctr + blk) : "memory");
+      if (A.fence == 0) {
+        asm volatile("atom.add.acq_rel.gpu.u32 %0, [%1], 1;" : "=r"(prev) : "l"(A.ctr + blk) : "memory");
+      } else if (A.fence == 1) {
+        __threadfence();
+        prev = atomicAdd(A.ctr + blk, 1u);
+        __threadfence();
+      } else {
+        prev = atomicAdd(A.ctr + blk, 1u);
+      }
       last = (prev == (unsigned)nc - 1);
       if (last) A.ctr[blk] = 0;
+      A.ts[blockIdx.x * 4 + 2] = gt();
     }
     __syncthreads();
     if (last) {
@@ -92,6 +105,8 @@ __global__ void __launch_bounds__(512, 1) kc(const __grid_constant__ Args A) {
         A.y[r] = s;
       }
     }
+    __syncthreads();
+    if (threadIdx.x == 0) A.ts[blockIdx.x * 4 + 3] = gt();
   } else if (A.mode == 5) {
     const unsigned ep = *A.rep + 1u;
     const int nblk = (gridDim.x + kPart - 1) / kPart, blk = blockIdx.x / kPart, slot = blockIdx.x % kPart;
@@ -183,16 +198,19 @@ int main() {
   cudaMalloc(&ctr, kCalls * 64 * 4);
   cudaStream_t st;
   cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking);
-  const char* names[] = {"pair", "none", "last", "gbar", "blk", "poll"};
+  const char* names[] = {"pair", "none", "last", "gbar", "blk", "poll", "blk-tf", "blk-nofence"};
+  unsigned long long* ts;
+  cudaMalloc(&ts, (size_t)kCalls * 148 * 4 * 8);
   for (int work : {0, 5000}) {
-    for (int mode : {0, 1, 4, 5}) {
+    for (int mode : {0, 1, 4, 6, 7}) {
       cudaGraph_t g;
       cudaStreamBeginCapture(st, cudaStreamCaptureModeGlobal);
       kzero<<<kCalls, 64, 0, st>>>(ctr, kCalls * 64);
       kbump<<<1, 1, 0, st>>>(rep);
       for (int c = 0; c < kCalls; ++c) {
+        const int m = mode >= 6 ? 4 : mode;
         Args A{c ? y + (size_t)(c - 1) * kRows : x, part + (size_t)c * kRows * kPart * 2, y + (size_t)c * kRows, ctr + 64 * c,
-               work, mode, rep};
+               work, m, rep, ts + (size_t)c * 148 * 4, mode == 6 ? 1 : mode == 7 ? 2 : 0};
         launch((void*)kc, dim3(148), dim3(512), smem, st, A);
         if (mode == 0) launch((void*)kr, dim3(kRows / 256), dim3(256), 0, st, A);
       }
@@ -213,8 +231,29 @@ int main() {
       cudaEventSynchronize(b);
       float ms;
       cudaEventElapsedTime(&ms, a, b);
-      printf("%-5s work=%5d ns: %.2f us per call (%s)\n", names[mode], work, ms * 1e3 / reps / kCalls,
+      printf("%-11s work=%5d ns: %.2f us per call (%s)\n", names[mode], work, ms * 1e3 / reps / kCalls,
              cudaGetErrorString(cudaGetLastError()));
+      if (mode >= 4) {  // breakdown from the last replay's stamps (calls 1..63)
+        static unsigned long long h[kCalls * 148 * 4];
+        cudaMemcpy(h, ts, sizeof(h), cudaMemcpyDeviceToHost);
+        double work_to_arr = 0, arr = 0, red = 0, gap = 0;
+        int n = 0;
+        for (int c = 1; c < kCalls; ++c) {
+          unsigned long long s0 = ~0ull, wmax = 0, amax = 0, emax = 0, prev_e = 0;
+          for (int b = 0; b < 148; ++b) {
+            const unsigned long long* t = h + ((size_t)c * 148 + b) * 4;
+            s0 = t[0] < s0 ? t[0] : s0;
+            wmax = t[1] > wmax ? t[1] : wmax;
+            amax = t[2] > amax ? t[2] : amax;
+            emax = t[3] > emax ? t[3] : emax;
+            const unsigned long long* tp = h + ((size_t)(c - 1) * 148 + b) * 4;
+            prev_e = tp[3] > prev_e ? tp[3] : prev_e;
+          }
+          work_to_arr += 0; arr += (double)(amax - wmax); red += (double)(emax - amax); gap += (double)(s0 - prev_e); ++n;
+        }
+        printf("    breakdown (us): last work-done -> last arrival %.2f, -> last exit stamp %.2f, prev exit -> next start %.2f\n",
+               arr / n / 1e3, red / n / 1e3, gap / n / 1e3);
+      }
       cudaGraphExecDestroy(ge);
       cudaGraphDestroy(g);
     }
