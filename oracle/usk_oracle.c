@@ -820,6 +820,13 @@ int32_t uo_build_units(int32_t dtype, const void* W, int64_t out, int64_t in, in
       }
     st = uo_sketch_unit_v(variant, dtype, wb, pos, k, hash_kind, seed, (uint32_t)layer, (uint32_t)t, M,
                           (uint32_t)ncols[t], cells);
+    /* Top-K plans (ledger L29): a cell that no remaining (non-outlier) weight maps to holds +0, not
+     * the +Inf sentinel.  No non-outlier weight ever retrieves it (each of its bonded cells holds
+     * at least its own weight), the reconstruction overlays the outliers, and the GEMV's outlier
+     * correction x (w - w'_sketch) then reads a finite w'_sketch (+Inf would give Inf - Inf). */
+    if (st == UO_OK && exclude)
+      for (c = 0; c < (int64_t)M * ncols[t]; c++)
+        if (cells[c] == uo_inf_bits(dtype)) cells[c] = 0u;
     if (st == UO_OK)
       for (c = 0; c < (int64_t)M * ncols[t]; c++) uo_store(dtype, sketch, offsets[t] + c, cells[c]);
     free(wb);

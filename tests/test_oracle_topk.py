@@ -32,8 +32,9 @@ def test_outliers_excluded_from_the_sketch_and_exact(orc):
         N, off = int(pl.ncols[t]), int(pl.offsets[t])
         keep = [p for p in range(o) if p * i + t not in flat]
         cells = orc.sketch_unit(W[keep, t].astype(np.uint32), np.array(keep), M, N, dtype=orc.BF16, seed=12,
-                                t=t)
-        np.testing.assert_array_equal(ts.cells[off:off + M * N], cells.ravel().astype(np.uint16))
+                                t=t).ravel().astype(np.uint16)
+        cells[cells == 0x7F80] = 0  # ledger L29: cells no remaining weight maps to hold +0, not +Inf
+        np.testing.assert_array_equal(ts.cells[off:off + M * N], cells)
     Wp = orc.reconstruct_rows(pl, ts, 0)
     np.testing.assert_array_equal(Wp.ravel()[ts.idx[0]], ts.vals[0])  # untouched
     # linear over the overlaid W'
@@ -72,3 +73,25 @@ def test_topk_reduces_relative_error(orc):
         res[k] = (int(pl.acct[0, 2]), np.mean(np.abs(w - Wp)[nz] / np.abs(w[nz])), np.mean(np.abs(w - Wp)))
     assert res[0][0] == res[K][0]  # equal sketch cells
     assert res[K][1] < res[0][1] and res[K][2] < res[0][2], res
+
+
+def test_topk_sketch_values_finite_at_outliers(orc):
+    # ledger L29: at 16 bpw a layer's cells outnumber its weights, so some cells receive only
+    # outliers; they hold +0, and the sketch value w'_sketch at every outlier position (which the
+    # GEMV correction x (w - w'_sketch) reads) is finite.  Without outliers no cell is +0-by-rule.
+    o, i, M, K = 64, 64, 3, 64
+    W = synth.weights_bf16(o, i, 9)
+    pl = orc.plan([(o, i)], 16.0, M=M, dtype=orc.BF16, seed=3, topk=K)
+    ts = orc.build_model(pl, [W])
+    assert not np.any(ts.cells[:int(pl.offsets[-1])] == 0x7F80)  # no +Inf state left
+    flat = ts.idx[0]
+    for e in flat.tolist():
+        oo, jj = divmod(e, i)
+        N, off = int(pl.ncols[jj]), int(pl.offsets[jj])
+        idx = orc.hash_indices(orc.HASH_X, 3, 0, jj, M, [oo], N)[:, 0]
+        vals = [orc.value_of(np.array([ts.cells[off + r * N + int(c)]], np.uint16), orc.BF16)[0]
+                for r, c in enumerate(idx)]
+        assert all(np.isfinite(v) for v in vals)
+    x = synth.vector(i, seed=2)[0].astype(np.float64)
+    y = orc.linear_rows(pl, ts, 0, x)[0]
+    assert np.all(np.isfinite(y))
