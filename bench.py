@@ -484,14 +484,18 @@ def run_usk(args):
     if world == 1 and not args.no_prefill:
         torch.cuda.empty_cache()
         T = 16384
-        Xp = synth.torch_vector(8192, 77, dev, torch.bfloat16, T=T)           # [T, 8192], sliced per layer
-        Yp = torch.empty((T, 8192), dtype=torch.bfloat16, device=dev)
+        Xp = synth.torch_vector(8192, 77, dev, torch.bfloat16, T=T).reshape(-1)  # T x 8192 bf16 N(0,1)
+        Yp = torch.empty(T * 8192, dtype=torch.bfloat16, device=dev)
+        # dense row-major [T, in] / [T, out] per layer width (usk_linear's T > 1 layout; the binding
+        # rejects strided views)
+        Xw = {i: Xp[:T * i].view(T, i) for i in {i for _, i in shapes}}
+        Yw = {o: Yp[:T * o].view(T, o) for o in {o for o, _ in shapes}}
         ws_p = torch.zeros(max(usk.linear_workspace_bytes(plan, l, T) for l in range(L)), dtype=torch.uint8,
                            device=dev)
 
         def prefill_pass(pl_, sk_):
             for l, (o, i) in enumerate(shapes):
-                usk.linear(pl_, sk_, l, Xp[:, :i], Yp[:, :o], ws_p, stream=stream)
+                usk.linear(pl_, sk_, l, Xw[i], Yw[o], ws_p, stream=stream)
 
         def time_pass(pl_, sk_, reps=3):
             with torch.cuda.stream(stream):
@@ -526,7 +530,7 @@ def run_usk(args):
                           "frac_of_bf16_burst": flop / (ms08 * 1e-3) / 1e12 / pk},
               "flop_per_pass": flop, "peak_basis": "MEASURED_PEAKS.json bf16 (torch 8192^3): sustained for a "
                                                    "25 ms pass, burst shown beside"}
-        del Xp, Yp, ws_p, sk08, plan08
+        del Xp, Yp, Xw, Yw, ws_p, sk08, plan08
         torch.cuda.empty_cache()
 
     # ---- BASELINE config 5 at N = 1: Llama-3-8B-shaped linears (224, 6.98 G weights, 13.96 GB bf16)

@@ -21,7 +21,7 @@
  *     (order independence); usk_linear is deterministic for fixed inputs.
  *
  * Citations: PAPER.md:<line> (section / equation).  Readings where the paper is silent are
- * listed in DESIGN.md ("ledger" L1..L24) and referenced below.
+ * listed in DESIGN.md ("ledger" L1..L31) and referenced below.
  */
 #ifndef USK_H
 #define USK_H
@@ -52,7 +52,10 @@ typedef enum {
   USK_ENONFINITE = 4,   /* the build saw NaN or +-Inf (sticky; reported by usk_check) --
                            +Inf is the empty-cell sentinel (L4) */
   USK_ECUDA = 5,        /* CUDA launch / runtime failure (text in usk_last_error) */
-  USK_EUNSUPPORTED = 6  /* valid request with no kernel (e.g. T > 1 with fp32 weights) */
+  USK_EUNSUPPORTED = 6, /* valid request with no kernel (e.g. T > 1 with fp32 weights) */
+  USK_ERANGE = 7        /* a value of |v| >= 2^15 entered a 2^-48 fixed-point sum (CountMin build,
+                           usk_aggregate_grad; L26/L27): the affected sums saturated
+                           (sticky; reported by usk_check) */
 } usk_status;
 
 typedef enum { USK_F32 = 0, USK_BF16 = 1 } usk_dtype;
@@ -65,9 +68,11 @@ typedef enum { USK_F32 = 0, USK_BF16 = 1 } usk_dtype;
  * dims_per_unit must be 1.  Its decode runs one kernel per call (no cross-CTA reduction). */
 typedef enum { USK_GRAN_ROW = 0, USK_GRAN_LAYER = 1, USK_GRAN_OUTROW = 2 } usk_granularity;
 
-/* Hash family (Eq. 3; contract in DESIGN.md "Hash contract"):
- * USK_HASH_X = our independent multiply-high family; USK_HASH_IDENTITY = p mod N (SPEC.md:54,
- * tests only). */
+/* Hash family (Eq. 3; contract in DESIGN.md 2.2 "Hash contract USK-X"):
+ * USK_HASH_X = per-row salted position mix fmix32(p ^ rho_i) XOR per-unit key fmix32(K_u ^ kappa_i),
+ * reduced to [0, N_u) by the top 23 bits times N_u (short units, N_u <= 2^16; exact as one fp32
+ * FMA.RZ on the device) or a 32-bit multiply-high (long units); USK_HASH_IDENTITY = p mod N
+ * (tests only). */
 typedef enum { USK_HASH_X = 0, USK_HASH_IDENTITY = 1 } usk_hash;
 
 /* Sketch variant (Appendix C.2): USK_ABSMAXMIN = the paper's sketch (keep the

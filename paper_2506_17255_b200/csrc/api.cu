@@ -2,8 +2,11 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
+#include <tuple>
 
 #include "common.cuh"
 
@@ -23,6 +26,39 @@ usk_status cuda_fail(cudaError_t e, const char* what) {
   return USK_ECUDA;
 }
 void count_launch(int n) { g_launches += n; }
+
+// Function attributes apply to the CURRENT device's context: cache them per (device, kernel,
+// value), under a lock (concurrent calls on several streams and devices are allowed, usk.h).
+static std::mutex g_attr_mu;
+cudaError_t ensure_func_attr(const void* kern, int attr, int value) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  static std::map<std::tuple<int, const void*, int, int>, cudaError_t> done;
+  const auto key = std::make_tuple(dev, kern, attr, value);
+  auto it = done.find(key);
+  if (it != done.end()) return it->second;
+  e = cudaFuncSetAttribute(kern, (cudaFuncAttribute)attr, value);
+  if (e != cudaSuccess) (void)cudaGetLastError();
+  done[key] = e;
+  return e;
+}
+int device_sm_count() {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+  std::lock_guard<std::mutex> lock(g_attr_mu);
+  static std::map<int, int> sms;
+  auto it = sms.find(dev);
+  if (it != sms.end()) return it->second;
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+    (void)cudaGetLastError();
+    n = 148;
+  }
+  sms[dev] = n;
+  return n;
+}
 
 static bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
@@ -104,6 +140,7 @@ const char* usk_status_string(usk_status s) {
     case USK_ENONFINITE: return "USK_ENONFINITE";
     case USK_ECUDA: return "USK_ECUDA";
     case USK_EUNSUPPORTED: return "USK_EUNSUPPORTED";
+    case USK_ERANGE: return "USK_ERANGE";
   }
   return "USK_UNKNOWN";
 }
@@ -519,7 +556,8 @@ usk_status usk_check(const usk_plan* pl, usk_stream stream) {
   USK_CUDA(cudaMemcpy(&h, pl->d_err, sizeof(int), cudaMemcpyDeviceToHost));
   if (h) {
     USK_CUDA(cudaMemset(pl->d_err, 0, sizeof(int)));
-    return fail(USK_ENONFINITE, "the build saw NaN or Inf weights");
+    if (h & 1) return fail(USK_ENONFINITE, "a build or aggregation saw NaN or Inf values");
+    return fail(USK_ERANGE, "a value of |v| >= 2^15 reached the 2^-48 fixed-point sums (CountMin / usk_aggregate_grad)");
   }
   return USK_OK;
 }

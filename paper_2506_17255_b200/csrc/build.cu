@@ -265,7 +265,10 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
     const int64_t off = A.offsets[u];
     for (int k = warp; k < mn; k += kConsumers + 1) {
       const uint32_t key = keys[v * stride_v + k * 32 + lane];
-      const uint32_t b32 = (key == ~0u) ? 0x7F800000u : rotr1(key);
+      // empty = +Inf; Top-K builds (kap_max accepts the +Inf of excluded outliers):
+      // a cell that only outliers (or nothing) map to holds +0 (DESIGN.md ledger L29)
+      const uint32_t b32 = (A.kap_max >= 0xFF000000u && key >= 0xFF000000u) ? 0u
+                           : (key == ~0u) ? 0x7F800000u : rotr1(key);
       if constexpr (ES == 2) out[off + k] = (uint16_t)(b32 >> 16);
       else out[off + k] = b32;
     }
@@ -332,18 +335,21 @@ __global__ void k_gen_scatter(GenLayer G, const void* W, const uint8_t* nrows, H
   }
 }
 
+// keys -> states; empty = +Inf; zero_outlier_only (Top-K builds, DESIGN.md ledger
+// L29): a cell whose min key is that of +Inf (only excluded outliers) or empty holds +0
 template <int ES>
-__global__ void k_gen_final(void* sketch, int64_t c0, int64_t n) {
+__global__ void k_gen_final(void* sketch, int64_t c0, int64_t n, int zero_outlier_only) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   if (ES == 2) {
     uint16_t* c = reinterpret_cast<uint16_t*>(sketch) + c0 + i;
     const uint32_t k = *c;
-    *c = (k == 0xFFFFu) ? (uint16_t)0x7F80 : (uint16_t)((k >> 1) | ((k & 1u) << 15));
+    *c = (zero_outlier_only && k >= 0xFF00u) ? (uint16_t)0
+         : (k == 0xFFFFu) ? (uint16_t)0x7F80 : (uint16_t)((k >> 1) | ((k & 1u) << 15));
   } else {
     uint32_t* c = reinterpret_cast<uint32_t*>(sketch) + c0 + i;
     const uint32_t k = *c;
-    *c = (k == 0xFFFFFFFFu) ? 0x7F800000u : ((k >> 1) | ((k & 1u) << 31));
+    *c = (zero_outlier_only && k >= 0xFF000000u) ? 0u : (k == 0xFFFFFFFFu) ? 0x7F800000u : ((k >> 1) | ((k & 1u) << 31));
   }
 }
 
@@ -565,7 +571,7 @@ usk_status launch_fast_t(BuildArgs& A, int n_ctas, cudaStream_t st) {
   constexpr int S = stages_for<sizeof(E)>();
   const size_t smem = 128 + (size_t)S * stage_bytes<E, UPL>() + (size_t)32 * UPL * A.maxMN * 4 + 128;
   auto kern = k_build_fast<E, UPL, MT, HASH>;
-  USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  USK_CUDA(ensure_smem((const void*)kern, 227 * 1024));  // one limit per (device, kernel): the opt-in maximum
   kern<<<n_ctas, kBuildThreads, smem, st>>>(A);
   USK_LAUNCHED("k_build_fast");
   return USK_OK;
@@ -681,7 +687,8 @@ usk_status launch_generic_t(const usk_plan* pl, int32_t l, const void* W, void* 
     k_gen_scatter<ES, USK_HASH_IDENTITY><<<blocks, T, 0, st>>>(G, W, pl->d_nrows, pl->hc, pl->d_ncols, pl->d_offsets,
                                                                pl->d_keys, sketch, pl->d_err, kap_max);
   USK_LAUNCHED("k_gen_scatter");
-  k_gen_final<ES><<<(unsigned)((L.n_cells + T - 1) / T), T, 0, st>>>(sketch, L.cell_begin, L.n_cells);
+  k_gen_final<ES><<<(unsigned)((L.n_cells + T - 1) / T), T, 0, st>>>(sketch, L.cell_begin, L.n_cells,
+                                                                     kap_max >= 0xFF000000u ? 1 : 0);
   USK_LAUNCHED("k_gen_final");
   return USK_OK;
 }

@@ -19,6 +19,12 @@ void set_error(const std::string& msg);
 usk_status fail(usk_status st, const std::string& msg);
 usk_status cuda_fail(cudaError_t e, const char* what);
 void count_launch(int n = 1);
+// cudaFuncSetAttribute once per (current device, kernel, attribute, value); thread-safe
+cudaError_t ensure_func_attr(const void* kern, int attr, int value);
+inline cudaError_t ensure_smem(const void* kern, int bytes) {
+  return ensure_func_attr(kern, (int)cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+}
+int device_sm_count();  // SM count of the current device (cached per device)
 
 #define USK_CUDA(call)                                              \
   do {                                                              \

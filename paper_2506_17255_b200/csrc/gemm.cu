@@ -519,18 +519,9 @@ usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dty
   if (!make_map(&ma, X, T, K, BM) || !make_map(&mb, W, n_out, K, one_sm ? BN : 128))
     return fail(USK_ECUDA, "cuTensorMapEncodeTiled failed");
   GemmArgs G{Y, y_dtype == USK_BF16, T, n_out, K, n_out};
-  static int sms2 = 0;
-  if (!sms2) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms2, cudaDevAttrMultiProcessorCount, dev) !=
-                                                 cudaSuccess)
-      sms2 = 148;
-  }
+  const int sms2 = device_sm_count();
   if (!one_sm) {
-    static std::once_flag attr2_once;
-    std::call_once(attr2_once, [] {
-      cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem2);
-    });
+    USK_CUDA(ensure_smem((const void*)k_gemm_tc2, (int)kGemmSmem2));
     const int64_t mpairs = ((T + BM - 1) / BM + 1) / 2;
     const int64_t ptiles = mpairs * ((n_out + BN - 1) / BN);
     cudaLaunchConfig_t cfg = {};
@@ -550,17 +541,8 @@ usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dty
     USK_LAUNCHED("k_gemm_tc2");
     return USK_OK;
   }
-  static std::once_flag attr_once;
-  std::call_once(attr_once, [] {
-    cudaFuncSetAttribute(k_gemm_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGemmSmem);
-  });
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
-                                                 cudaSuccess)
-      sms = 148;
-  }
+  USK_CUDA(ensure_smem((const void*)k_gemm_tc, (int)kGemmSmem));
+  const int sms = device_sm_count();
   const int64_t tiles = ((T + BM - 1) / BM) * ((n_out + BN - 1) / BN);
   k_gemm_tc<<<(unsigned)std::min<int64_t>(tiles, sms), kGemmThreads, kGemmSmem, st>>>(ma, mb, G);
   USK_LAUNCHED("k_gemm_tc");

@@ -23,7 +23,7 @@ struct AggArgs {
   const uint32_t* ukeys;
   HashConsts hc;
   unsigned long long* acc;
-  int* err;  // non-NULL: flag non-finite values (CountMin build)
+  int* err;  // sticky flag: bit 0 non-finite value, bit 1 |value| >= 2^15 (outside the 2^-48 fixed point)
 };
 
 __global__ void k_aggregate(AggArgs A) {
@@ -37,7 +37,11 @@ __global__ void k_aggregate(AggArgs A) {
     const int64_t base = A.offsets[u] - A.cell_begin;
     const float gv = A.bf16 ? __uint_as_float((uint32_t)reinterpret_cast<const uint16_t*>(A.grad)[e] << 16)
                             : reinterpret_cast<const float*>(A.grad)[e];
-    if (A.err && !isfinite(gv)) atomicOr(A.err, 1);
+    if (!isfinite(gv)) {  // q would saturate: flag it and leave it out of the sums
+      atomicOr(A.err, 1);
+      continue;
+    }
+    if (fabsf(gv) >= 32768.0f) atomicOr(A.err, 2);  // |q| >= 2^63: saturated, the sums are wrong
     const long long q = __double2ll_rn((double)gv * kFix);
     if (q == 0) continue;
     const uint32_t Ku = A.ukeys[u];
@@ -77,7 +81,7 @@ usk_status launch_fixed_accumulate(const usk_plan* pl, int32_t l, const void* va
 usk_status launch_aggregate(const usk_plan* pl, int32_t l, const void* grad, int32_t grad_dtype, float* cell_grad,
                             void* ws, cudaStream_t st) {
   const LayerGeom& L = pl->layers[l];
-  usk_status s = launch_fixed_accumulate(pl, l, grad, grad_dtype, reinterpret_cast<unsigned long long*>(ws), nullptr,
+  usk_status s = launch_fixed_accumulate(pl, l, grad, grad_dtype, reinterpret_cast<unsigned long long*>(ws), pl->d_err,
                                          st);
   if (s != USK_OK) return s;
   struct {

@@ -314,11 +314,7 @@ usk_status launch_gemv_outrow(const usk_plan* pl, const void* sketch, const int3
   };
   kern = bf16 ? (xb ? pick(uint16_t{}, uint16_t{}) : pick(uint16_t{}, float{}))
               : (xb ? pick(uint32_t{}, uint16_t{}) : pick(uint32_t{}, float{}));
-  static std::vector<void*> raised;
-  if (std::find(raised.begin(), raised.end(), kern) == raised.end()) {
-    USK_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-    raised.push_back(kern);
-  }
+  USK_CUDA(ensure_smem(kern, 200 * 1024));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)blocks);
   cfg.blockDim = dim3(kORSlices * RB);

@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 #include "ptx.cuh"
@@ -419,24 +420,36 @@ __device__ __forceinline__ uint4 lds_rtab(uint32_t a) {
   return q;
 }
 
-// Row r of the warp's kSubRows partial rows ends on the lanes congruent to r mod kSubRows
-// (fixed-order butterfly: log2(kSubRows) exchange-and-halve stages inside each group of kSubRows
-// lanes, then the groups are added).
+// Row sums of a subtile: acc[r] is this lane's partial of row r.  Every row is summed over the 32
+// lanes by ONE fixed tree whatever the subtile height: lane bits 3, 2, 1, 0, then 4, each stage
+// adding the partial of the lane across that bit (fp addition commutes, so the two lanes of a pair
+// agree).  16-row subtiles: exchange-and-halve stages on lane bits 3..0 (row bit 3..0), then bit 4;
+// 8-row subtiles: exchange stages on lane bits 3, 2, 1 (row bits 2, 1, 0), then bits 0 and 4.  So a
+// row's bits do not depend on the subtile height (a per-launch choice), its position in the
+// subtile, the output range, the batch or the GPU count (bit-identical shards).
+// Returns the sum of row sub_row<SR>(lane) (replicated over the lanes that share it).
+template <int SR>
+__device__ __forceinline__ int sub_row(int lane) { return SR == 16 ? (lane & 15) : ((lane >> 1) & 7); }
+template <int SR>
+__device__ __forceinline__ bool row_writer(int lane) { return SR == 16 ? lane < 16 : (lane & 17) == 0; }
+
 template <int SR>
 __device__ __forceinline__ float transpose_reduce(float (&acc)[SR], int lane) {
+  static_assert(SR == 8 || SR == 16, "subtile rows");
+  constexpr int LS = SR == 16 ? 1 : 2;  // lane distance of row bit b: LS << b
 #pragma unroll
   for (int m = SR / 2; m >= 1; m >>= 1) {
-    const bool up = (lane & m) != 0;
+    const bool up = (lane & (LS * m)) != 0;
 #pragma unroll
     for (int i = 0; i < m; ++i) {
       const float send = up ? acc[i] : acc[i + m];
       const float keep = up ? acc[i + m] : acc[i];
-      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, LS * m);
     }
   }
   float t = acc[0];
-#pragma unroll
-  for (int m = SR; m < 32; m <<= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+  if constexpr (SR == 8) t += __shfl_xor_sync(0xffffffffu, t, 1);
+  t += __shfl_xor_sync(0xffffffffu, t, 16);
   return t;
 }
 
@@ -635,7 +648,12 @@ __device__ __forceinline__ void query_balanced(const QArgs& A) {
             acc[r] = a;
           }
           const float t = transpose_reduce<SR>(acc, lane);
-          if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = t;
+          if constexpr (SR == 16) {
+            if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + chunk] = t;
+          } else {
+            const int rr = sub_row<SR>(lane);
+            if (row_writer<SR>(lane) && rr < nrow) Ly.partial[(r0 + rr) * Ly.CP + chunk] = t;
+          }
         } else {
           // W' rows: lane L writes its UPL units of each row (bf16: one 8-byte store for UPL = 4)
           const bool full_tile = (cur.nu == TJ);
@@ -1077,39 +1095,32 @@ int ilog2(int v) {
   return r;
 }
 
-int sm_count() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) !=
-                                                 cudaSuccess)
-      sms = 148;
-  }
-  return sms;
-}
+int sm_count() { return device_sm_count(); }
 
 int occupancy(void* kern, size_t smem) {
-  // cached per (kernel, smem); the max-dynamic-smem attribute is raised on first use (callers
-  // warm up before any graph capture)
+  // cached per (device, kernel, smem); the max-dynamic-smem attribute is raised per device on first
+  // use (callers warm up before any graph capture)
   static std::mutex mu;
-  static std::vector<std::pair<std::pair<void*, size_t>, int>> cache;
-  static std::vector<void*> raised;
-  std::lock_guard<std::mutex> lock(mu);
-  for (auto& e : cache)
-    if (e.first.first == kern && e.first.second == smem) return e.second;
-  if (std::find(raised.begin(), raised.end(), kern) == raised.end()) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax) != cudaSuccess) {
-      (void)cudaGetLastError();
-      return 0;
-    }
-    raised.push_back(kern);
+  static std::vector<std::pair<std::tuple<int, void*, size_t>, int>> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
   }
+  const auto key = std::make_tuple(dev, kern, smem);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : cache)
+      if (e.first == key) return e.second;
+  }
+  if (ensure_smem(kern, (int)kSmemMax) != cudaSuccess) return 0;
   int occ = 0;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kQThreads, smem) != cudaSuccess) {
     (void)cudaGetLastError();
     occ = 0;
   }
-  cache.push_back({{kern, smem}, occ});
+  std::lock_guard<std::mutex> lock(mu);
+  cache.push_back({key, occ});
   return occ;
 }
 
@@ -1527,12 +1538,8 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
     while (A.red_lanes < 32 && 4 * A.red_lanes < G.n_chunks[0]) A.red_lanes *= 2;
     usk_status s1 = launch_q(G.kern, A, grid, G.smem, true, st);
     if (s1 != USK_OK) return s1;
-    static const bool carveout = [] {  // co-reside with k_gemv_fast's max-shared configuration
-      (void)cudaFuncSetAttribute((void*)k_gemv_reduce, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-      (void)cudaGetLastError();
-      return true;
-    }();
-    (void)carveout;
+    // co-reside with k_gemv_fast's max-shared configuration (a hint: a failure is not an error)
+    (void)ensure_func_attr((const void*)k_gemv_reduce, (int)cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     return launch_q((void*)k_gemv_reduce, A, (int)((A.rows * A.red_lanes + kRedThreads - 1) / kRedThreads), 0, true,
                     st, kRedThreads);
   }

@@ -51,9 +51,12 @@ def replicate_sketch(sketch_bytes, layer_regions, world: int, group=None, layers
 
 def allgather_outputs(y_shard, y_full, group=None):
     """y_full[...] = concatenation over ranks of their y shards (equal-size shards use
-    all_gather_into_tensor; ragged shards fall back to all_gather + copy)."""
+    all_gather_into_tensor; ragged shards fall back to all_gather + copy).  Batch-1 decode only:
+    y_shard and y_full are 1-D (one token)."""
     import torch
     import torch.distributed as dist
+    if y_shard.dim() != 1 or y_full.dim() != 1:
+        raise ValueError("allgather_outputs: 1-D (T = 1) shards only")
     world = dist.get_world_size(group)
     n = y_full.shape[-1]
     sizes = [output_shard(n, r, world) for r in range(world)]

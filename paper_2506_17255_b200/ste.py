@@ -22,8 +22,8 @@ class FakeCompress(torch.autograd.Function):
 
     @staticmethod
     def forward(ctx, W, plan, layer, sketch):
-        usk.build(plan, [W.detach()], sketch, layer_ids=[layer])
-        Wp = torch.empty_like(W)
+        usk.build(plan, [W.detach().contiguous()], sketch, layer_ids=[layer])
+        Wp = torch.empty(W.shape, dtype=W.dtype, device=W.device)  # dense row-major, whatever W's strides
         usk.reconstruct(plan, sketch, layer, Wp)
         return Wp
 

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libusk.so")
 
-OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE, ECUDA, EUNSUPPORTED = range(7)
+OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE, ECUDA, EUNSUPPORTED, ERANGE = range(8)
 F32, BF16 = 0, 1
 GRAN = {"row": 0, "layer": 1, "outrow": 2}
 HASH = {"x": 0, "identity": 1}
@@ -31,7 +31,7 @@ class UskError(RuntimeError):
 
 
 _STATUS = {0: "USK_OK", 1: "USK_EINVAL", 2: "USK_ESHAPE", 3: "USK_EBUDGET", 4: "USK_ENONFINITE", 5: "USK_ECUDA",
-           6: "USK_EUNSUPPORTED"}
+           6: "USK_EUNSUPPORTED", 7: "USK_ERANGE"}
 
 
 class _Shape(ct.Structure):
@@ -119,6 +119,20 @@ def _stream(stream):
 
 def _ptr(t):
     return ct.c_void_p(t.data_ptr()) if t is not None else ct.c_void_p(0)
+
+
+def _need(t, what: str, shape=None, dtype=None, contiguous: bool = True):
+    """Argument marshalling guard: the C ABI takes raw pointers with an implied dense row-major
+    layout, so a strided view or a wrong dtype would be silently reinterpreted."""
+    import torch
+    if contiguous and not t.is_contiguous():
+        raise UskError(EINVAL, f"{what}: tensor must be contiguous (got strides {tuple(t.stride())})")
+    if dtype is not None:
+        want = torch.bfloat16 if dtype == BF16 else torch.float32
+        if t.dtype != want:
+            raise UskError(EINVAL, f"{what}: dtype {t.dtype}, the plan needs {want}")
+    if shape is not None and tuple(t.shape) != tuple(shape):
+        raise UskError(ESHAPE, f"{what}: shape {tuple(t.shape)}, expected {tuple(shape)}")
 
 
 def _dtype_code(t) -> int:
@@ -222,6 +236,10 @@ def plan_allocation(shapes, *, bpw: float, rows: int = 3, granularity: str = "ro
 
 def build(plan: Plan, weights, sketch, layer_ids=None, stream=None):
     n = len(weights)
+    for k, w in enumerate(weights):
+        l = k if layer_ids is None else layer_ids[k]
+        if 0 <= l < len(plan.shapes):
+            _need(w, f"build: weights[{k}]", plan.shapes[l], plan.dtype)
     wp = (ct.c_void_p * n)(*[w.data_ptr() for w in weights])
     ids = None if layer_ids is None else (ct.c_int32 * n)(*layer_ids)
     _check(lib.usk_build(plan.handle, wp, ids, n, _ptr(sketch), _stream(stream)))
@@ -230,11 +248,18 @@ def build(plan: Plan, weights, sketch, layer_ids=None, stream=None):
 def build_rows(plan: Plan, layer: int, row_begin: int, row_end: int, w_rows, sketch, stream=None):
     """usk_build_rows (output-row units): build only the units of rows [row_begin, row_end) of `layer`
     from w_rows = those rows of its [out, in] weight (a rank's shard)."""
+    if 0 <= layer < len(plan.shapes):
+        _need(w_rows, "build_rows: w_rows", (row_end - row_begin, plan.shapes[layer][1]), plan.dtype)
     _check(lib.usk_build_rows(plan.handle, layer, row_begin, row_end, _ptr(w_rows), _ptr(sketch), _stream(stream)))
 
 
 def reconstruct(plan: Plan, sketch, layer: int, w_out, row_begin: int = 0, row_end=None, stream=None):
     row_end = plan.layers[layer].out_features if row_end is None else row_end
+    _need(w_out, "reconstruct: w_out", dtype=plan.dtype, contiguous=False)
+    if w_out.dim() != 2 or w_out.stride(1) != 1 or w_out.shape[0] < row_end - row_begin \
+            or w_out.shape[1] < plan.shapes[layer][1]:
+        raise UskError(ESHAPE, f"reconstruct: w_out must be [>= {row_end - row_begin}, {plan.shapes[layer][1]}] with "
+                               f"unit column stride (got {tuple(w_out.shape)}, strides {tuple(w_out.stride())})")
     _check(lib.usk_reconstruct(plan.handle, _ptr(sketch), layer, row_begin, row_end, _ptr(w_out), w_out.stride(0),
                                _stream(stream)))
 
@@ -260,6 +285,10 @@ def linear(plan: Plan, sketch, layer: int, x, y, workspace, out_begin: int = 0, 
     """y[T, out_end-out_begin] = x[T, in] @ W'[out_begin:out_end]^T (x, y contiguous CUDA tensors)."""
     out_end = plan.layers[layer].out_features if out_end is None else out_end
     T = x.shape[0] if x.dim() == 2 else 1
+    if 0 <= layer < len(plan.shapes):
+        _need(x, "linear: x", (T, plan.shapes[layer][1]) if x.dim() == 2 else (plan.shapes[layer][1],))
+        _need(y, "linear: y", (T, out_end - out_begin) if y.dim() == 2 else (out_end - out_begin,))
+    _need(workspace, "linear: workspace")
     _check(lib.usk_linear(plan.handle, _ptr(sketch), layer, _ptr(x), _dtype_code(x), T, _ptr(y), _dtype_code(y),
                           out_begin, out_end, _ptr(workspace), workspace.numel() * workspace.element_size(),
                           _stream(stream)))
@@ -286,6 +315,16 @@ def new_batch_workspace(plan: Plan, layers, ranges=None, device=None):
 def linear_batch(plan: Plan, sketch, layers, x, ys, workspace, ranges=None, stream=None):
     """One launch for several T=1 sketch-GEMVs sharing x: ys[k] = x @ W'_{layers[k]}[range_k]^T."""
     n, ids, rg = _batch_args(layers, ranges)
+    if len(ys) != n:
+        raise UskError(ESHAPE, f"linear_batch: {len(ys)} outputs for {n} layers")
+    _need(x, "linear_batch: x")
+    for k, (l, y) in enumerate(zip(layers, ys)):
+        if 0 <= l < len(plan.shapes):
+            r = (0, plan.shapes[l][0]) if ranges is None else ranges[k]
+            _need(y, f"linear_batch: ys[{k}]")
+            if y.numel() != r[1] - r[0]:
+                raise UskError(ESHAPE, f"linear_batch: ys[{k}] has {y.numel()} elements, range needs {r[1] - r[0]}")
+    _need(workspace, "linear_batch: workspace")
     yp = (ct.c_void_p * n)(*[y.data_ptr() for y in ys])
     _check(lib.usk_linear_batch(plan.handle, _ptr(sketch), ids, rg, n, _ptr(x), _dtype_code(x), yp,
                                 _dtype_code(ys[0]), _ptr(workspace), workspace.numel() * workspace.element_size(),
@@ -294,6 +333,8 @@ def linear_batch(plan: Plan, sketch, layers, x, ys, workspace, ranges=None, stre
 
 def importance(A, out, stream=None):
     """Eq. 7: out[j] = mean_k A[k, j]^2 (A [N, d] bf16/fp32 CUDA, out float32 [d])."""
+    _need(A, "importance: A")
+    _need(out, "importance: out", (A.shape[1],), F32)
     _check(lib.usk_importance(_ptr(A), _dtype_code(A), A.shape[0], A.shape[1], _ptr(out), _stream(stream)))
 
 
@@ -301,6 +342,9 @@ def aggregate_grad(plan: Plan, layer: int, grad, cell_grad, workspace=None, stre
     """usk_aggregate_grad: cell_grad[c] = fixed-point sum of grad over the weights mapped to cell c
     (aggregated-gradient baseline, Figure 4a).  cell_grad: float32 CUDA tensor [n_cells of layer]."""
     import torch
+    if 0 <= layer < len(plan.shapes):
+        _need(grad, "aggregate_grad: grad", plan.shapes[layer])
+        _need(cell_grad, "aggregate_grad: cell_grad", (plan.layers[layer].n_cells,), F32)
     if workspace is None:
         workspace = torch.zeros(int(lib.usk_aggregate_grad_workspace_bytes(plan.handle, layer)), dtype=torch.uint8,
                                 device=grad.device)
@@ -312,6 +356,8 @@ def aggregate_grad(plan: Plan, layer: int, grad, cell_grad, workspace=None, stre
 def stats(plan: Plan, sketch, layer: int, W, stream=None) -> dict:
     """usk_stats: the compression report of `layer` (counts keyed by STATS_KEYS)."""
     import torch
+    if 0 <= layer < len(plan.shapes):
+        _need(W, "stats: W", plan.shapes[layer], plan.dtype)
     counts = torch.zeros(13, dtype=torch.int64, device=W.device)
     ws = torch.zeros(int(lib.usk_stats_workspace_bytes(plan.handle, layer)), dtype=torch.uint8, device=W.device)
     _check(lib.usk_stats(plan.handle, _ptr(sketch), layer, _ptr(W), _ptr(counts), _ptr(ws), ws.numel(), _stream(stream)))

@@ -114,9 +114,10 @@ def test_c3_full_model_sampled(orc, usk):
     sample_layers = [0, 1, 3, 4, 6, 7 * 15 + 2, 7 * 15 + 5]
     for l in sample_layers:
         _unit_parity(orc, usk, pl, opl, sk, l, ws[l], 6, rng)
-    # grouped GEMV (bench launch configuration) on sampled rows of two groups: the oracle builds
-    # the full layers from the same weights
-    for g in ([0, 1, 2], [4, 5]):
+    # grouped GEMV (bench launch configuration) on sampled rows of every group kind (q|k|v, o,
+    # gate|up, down; the 8-row-subtile kernel runs q|k|v): the oracle builds the full layers from
+    # the same weights
+    for g in ([0, 1, 2], [3], [4, 5], [6]):
         i = shapes[g[0]][1]
         x = synth.torch_vector(i, 1000 + g[0], "cuda", torch.bfloat16)[0]
         ys = [torch.empty(shapes[l][0], dtype=torch.float32, device="cuda") for l in g]
@@ -132,10 +133,14 @@ def test_c3_full_model_sampled(orc, usk):
             assert gemv_err(y.cpu().numpy()[r0:r0 + 8].astype(np.float64), y64, x64, W64) <= 1e-5
 
 
-@pytest.mark.parametrize("bpw", [0.5, 0.8])
-def test_c4_prefill_16384_tokens(orc, usk, bpw):
-    o, i, T = 8192, 2048, 16384
-    W = synth.torch_weights_bf16(o, i, synth.seed_for(4, 0, 4), "cuda")
+@pytest.mark.parametrize("bpw,k", [(0.5, 4), (0.8, 4), (0.5, 6), (0.5, 1)], ids=["gate-0.5", "gate-0.8", "down-0.5",
+                                                                                 "k-0.5"])
+def test_c4_prefill_16384_tokens(orc, usk, bpw, k):
+    # every distinct GEMM geometry the config-4 bench pass times: gate/up [8192, 2048], down
+    # [2048, 8192] (K = 8192: 128 K-blocks), k/v [512, 2048] (N = 512); q/o share gate's K
+    o, i = synth.llama_block(2048, 512, 8192)[k]
+    T = 16384
+    W = synth.torch_weights_bf16(o, i, synth.seed_for(4, 0, k), "cuda")
     pl = usk.plan_allocation([(o, i)], bpw=bpw, rows=3, seed=SEED)
     opl = orc.plan([(o, i)], bpw, M=3, dtype=orc.BF16, seed=SEED)
     sk = pl.new_sketch()
@@ -185,3 +190,28 @@ def test_c5_llama8b_block(orc, usk):
     y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 8)[0]
     W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, r0, r0 + 8), orc.BF16).reshape(8, i)
     assert gemv_err(y.cpu().numpy()[0, r0:r0 + 8].astype(np.float64), y64, x64, W64) <= 1e-5
+
+
+def test_q4_gemv_gate_up_batch(orc, usk):
+    # the paper's 0.5-bpw point (q4 states, G = 128; bench.py paper_point_q4) at the Llama-3.2-1B
+    # gate|up geometry through usk_linear_batch, the launch the bench times (UPL = 1 slots)
+    shapes = [(8192, 2048), (8192, 2048)]
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, state_bits=4, group_size=128)
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED, state_bits=4, group=128)
+    ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, 0, 4 + l), "cuda") for l, (o, i) in enumerate(shapes)]
+    sk = pl.new_sketch()
+    usk.build(pl, ws, sk)
+    usk.check(pl)
+    osk = orc.build_model(opl, [host_bits(w) for w in ws])
+    nb = pl.info["total_cells"] * 4 // 8
+    assert np.array_equal(sk.cpu().numpy()[:nb], osk.packed)
+    x = synth.torch_vector(2048, 1004, "cuda", torch.bfloat16)[0]
+    ys = [torch.empty(8192, dtype=torch.float32, device="cuda") for _ in shapes]
+    usk.linear_batch(pl, sk, [0, 1], x, ys, usk.new_batch_workspace(pl, [0, 1]))
+    x64 = synth.bf16_bits_to_f32(host_bits(x)).astype(np.float64)
+    rng = np.random.default_rng(8)
+    for l, y in enumerate(ys):
+        r0 = int(rng.integers(0, 8192 - 8))
+        y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 8)[0]
+        Wdq = orc.linear_rows(opl, osk, l, np.eye(2048), r0, r0 + 8).T  # fp32-dequantised W' rows
+        assert gemv_err(y.cpu().numpy()[r0:r0 + 8].astype(np.float64), y64, x64, Wdq) <= 1e-5

@@ -113,3 +113,36 @@ def test_topk_full_layer_selection(orc, usk):
     want_idx, want_vals = orc.topk(orc.BF16, W, 64)
     np.testing.assert_array_equal(idx.astype(np.int64), want_idx)
     np.testing.assert_array_equal(vals.astype(np.uint32), want_vals)
+
+
+@pytest.mark.parametrize("bpw,g", [(8.0, 1), (12.0, 1), (16.0, 1), (16.0, 2)])
+def test_topk_high_bpw_finite(orc, usk, bpw, g):
+    # ledger L29 (round 2): at 8-16 bpw some cells receive only outliers; they hold +0, so the GEMV's
+    # outlier correction x (w - w'_sketch) stays finite (an +Inf state gave Inf - Inf = NaN)
+    o, i, K = 512, 256, 96
+    Ws = make_weights([(o, i)], "bf16", 31)
+    pl = usk.plan_allocation([(o, i)], bpw=bpw, rows=3, dims_per_unit=g, dtype="bf16", seed=77, topk=K)
+    opl = orc.plan([(o, i)], bpw, M=3, dtype=orc.BF16, g=g, seed=77, topk=K)
+    sk = pl.new_sketch()
+    usk.build(pl, [to_dev(Ws[0], "bf16")], sk)
+    usk.check(pl)
+    ts = orc.build_model(opl, Ws)
+    np.testing.assert_array_equal(sketch_cells(sk, pl, "bf16"), ts.cells)
+    assert not np.any(ts.cells == 0x7F80)
+    want = orc.reconstruct_rows(opl, ts, 0)
+    Wv = orc.value_of(want, orc.BF16)
+    for xdt in ("f32", "bf16"):
+        xv = synth.vector(i, seed=5)[0]
+        if xdt == "bf16":
+            xb = synth.f32_to_bf16_bits(xv)
+            x = torch.from_numpy(xb.view(np.int16).copy()).view(torch.bfloat16).cuda()
+            xv = synth.bf16_bits_to_f32(xb)
+        else:
+            x = torch.from_numpy(xv.astype(np.float32)).cuda()
+        y = torch.empty(o, dtype=torch.float32, device="cuda")
+        usk.linear(pl, sk, 0, x.view(1, -1), y.view(1, -1), usk.new_workspace(pl, 0))
+        yh = y.cpu().numpy().astype(np.float64)
+        assert np.all(np.isfinite(yh))
+        x64 = xv.astype(np.float64)
+        err = np.abs(yh - Wv @ x64) / np.maximum(np.abs(Wv) @ np.abs(x64), 1e-30)
+        assert err.max() <= 1e-5, (xdt, err.max())

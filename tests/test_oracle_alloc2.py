@@ -59,3 +59,19 @@ def test_two_level_plan_front_layers_get_more(orc):
     np.testing.assert_array_equal(pl.acct[:, 2], T_all)
     with pytest.raises(orc.OracleError):
         orc.plan(shapes, bpw, M=3, layer_importance=imp, gran=orc.GRAN_LAYER)
+
+
+def test_two_level_hand_worked_example(orc):
+    # Worked by hand from ledger L28 (no code):  two [8, 4] fp32 layers, M = 1, C = 1 (no class map),
+    # layer importance [1, 3], 16 bpw -> model budget 16 * 64 = 1024 bits -> T = 32 cells.
+    #   q = floor((imp / 3) * 2^24) = [5592405, 16777216];  W = 32 * (5592405 + 16777216) = 32 * 22369621
+    #   x_0 = 32 * 5592405 / 22369621 = 7.99999946...,  x_1 = 32 * 16777216 / 22369621 = 24.0000005...
+    #   floors [7, 24] (above the U_l M min_cols = 4 floors), 1 cell left -> the larger fraction
+    #   (layer 0, 0.99999946 vs 0.0000005) -> T_l = [8, 24];  rows inside a layer: 4 units of one
+    #   class -> N = 2 and N = 6 columns per unit; achieved 8 * 32 + 24 * 32 = 1024 bits.
+    Tl = orc.layer_cells(np.array([1.0, 3.0]), np.array([32, 32]), np.array([4, 4]), 1, 1, 32)
+    np.testing.assert_array_equal(Tl, [8, 24])
+    pl = orc.plan([(8, 4), (8, 4)], 16.0, M=1, dtype=orc.F32, seed=1, layer_importance=np.array([1.0, 3.0]))
+    np.testing.assert_array_equal(pl.acct[:, 2], [8, 24])
+    np.testing.assert_array_equal(pl.ncols, [2, 2, 2, 2, 6, 6, 6, 6])
+    assert int(pl.acct[:, 3].sum()) == 1024

@@ -31,8 +31,8 @@ ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, 0, k), dev) for k, (o, i)
 usk.build(pl, ws, sk)
 usk.check(pl)
 T = args.T
-X = synth.torch_vector(8192, 5, dev, torch.bfloat16, T=T)
-Y = torch.empty((T, 8192), dtype=torch.bfloat16, device=dev)
+X = synth.torch_vector(8192, 5, dev, torch.bfloat16, T=T).reshape(-1)  # dense [T, in] views per width below
+Y = torch.empty(T * 8192, dtype=torch.bfloat16, device=dev)
 wsp = torch.zeros(max(usk.linear_workspace_bytes(pl, l, T) for l in range(7)), dtype=torch.uint8, device=dev)
 scratch = torch.empty(8192 * 8192, dtype=torch.bfloat16, device=dev)
 stream = torch.cuda.Stream(device=dev)
@@ -60,9 +60,10 @@ tot = {"linear": 0.0, "recon": 0.0, "cublas": 0.0}
 for l, (o, i) in enumerate(shapes):
     Wd = scratch[: o * i].view(o, i)
     usk.reconstruct(pl, sk, l, Wd)
-    ms_lin = timed(lambda: usk.linear(pl, sk, l, X[:, :i], Y[:, :o], wsp, stream=stream))
+    Xl, Yl = X[:T * i].view(T, i), Y[:T * o].view(T, o)
+    ms_lin = timed(lambda: usk.linear(pl, sk, l, Xl, Yl, wsp, stream=stream))
     ms_rec = timed(lambda: usk.reconstruct(pl, sk, l, Wd, stream=stream))
-    Xc = X[:, :i].contiguous()
+    Xc = Xl
     Yc = torch.empty((T, o), dtype=torch.bfloat16, device=dev)
     ms_cub = timed(lambda: torch.matmul(Xc, Wd.t(), out=Yc))
     del Xc, Yc
