@@ -9,8 +9,12 @@ flushed (256 MB write) before every timed step, so the 60.8 MB sketch is re-read
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl usk|reference]
 
-N > 1 (torchrun, one rank per GPU, NCCL): every linear's output features are sharded over the
-ranks and the fp32 y shards are all-gathered with NCCL after each linear (strong scaling).
+N > 1 (one rank per GPU, NCCL): `--gpus N` spawns the N ranks itself (torch.distributed.run on
+127.0.0.1) unless it already runs under a launcher, whose WORLD_SIZE must equal N.  Every linear's
+output features are sharded over the ranks; the y shards of a grouped call (q|k|v, o, gate|up,
+down) land in one contiguous per-rank buffer and are all-gathered with ONE NCCL collective per call
+(64 per token), captured in the step's CUDA graph (strong scaling).  --dist-selftest runs the same
+launcher and host logic on CPU (gloo) with synthetic shard outputs: the CPU test of the N > 1 path.
 --impl reference times the CPU oracle (oracle/, plain C) on a bounded sample of the same
 workload, on rank 0 only.
 """
@@ -96,10 +100,24 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU oracle leg
-def oracle_decode_sample(shapes, weights_for_layer, budget_s=12.0):
-    """Time the CPU oracle's fp64 sketch-GEMV (reconstruct-on-the-fly + FMA, oracle/usk_oracle.c)
-    on a bounded sample: the 7 linears of block 0, output rows in round-robin until ~budget_s of
-    oracle compute has run.  Returns tokens/s extrapolated by weights/s over all 112 linears."""
+def _cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_decode_sample(shapes, weights_for_layer, budget_s=12.0, threads=1, rows_per_call=32):
+    """Time the CPU oracle's fp64 sketch-GEMV (reconstruct-on-the-fly + FMA, oracle/usk_oracle.c, as
+    it stands) on a bounded sample: the 7 linears of block 0, output rows in round-robin until
+    ~budget_s of wall time has run.  threads > 1: that many host threads call the oracle at once on
+    disjoint row slices (ctypes releases the GIL during each C call; OpenMP-free, every core busy).
+    Returns tokens/s extrapolated by weights/s over all 112 linears."""
+    import concurrent.futures as cf
+
     import oracle
     blk = shapes[:7]
     opl = oracle.plan(blk, BPW, M=ROWS, dtype=oracle.BF16, seed=SEED)
@@ -107,20 +125,31 @@ def oracle_decode_sample(shapes, weights_for_layer, budget_s=12.0):
     for l in range(7):
         oracle.build_layer(opl, l, weights_for_layer(l), sk)
     xs = [synth.vector(i, seed=1000 + l)[0].astype(np.float64) for l, (o, i) in enumerate(blk)]
-    done_w, spent, row = 0, 0.0, 0
-    while spent < budget_s:
-        for l, (o, i) in enumerate(blk):
-            r0 = (row * 8) % o
-            t0 = time.perf_counter()
-            oracle.linear_rows(opl, sk, l, xs[l], r0, r0 + 8)
-            spent += time.perf_counter() - t0
-            done_w += 8 * i
-        row += 1
+    RS = rows_per_call  # output rows per oracle call
+
+    def worker(k):
+        done, row = 0, k
+        t_end = time.perf_counter() + budget_s
+        while time.perf_counter() < t_end:
+            for l, (o, i) in enumerate(blk):
+                r0 = (row * RS) % o
+                oracle.linear_rows(opl, sk, l, xs[l], r0, r0 + RS)
+                done += RS * i
+            row += threads
+        return done
+
+    t0 = time.perf_counter()
+    with cf.ThreadPoolExecutor(max_workers=threads) as ex:
+        done_w = sum(ex.map(worker, range(threads)))
+    spent = time.perf_counter() - t0
     wps = done_w / spent
     total_w = sum(o * i for o, i in shapes)
-    return {"value": wps / total_w, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"oracle fp64 sketch-GEMV of {done_w} weights (8-row slices of the 7 block-0 linears, "
-                      f"{spent:.1f} s single-threaded), extrapolated to the 112-linear token by weights/s",
+    return {"value": wps / total_w, "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"oracle fp64 sketch-GEMV of {done_w} weights ({RS}-row slices of the 7 block-0 linears, "
+                      f"{spent:.1f} s wall on {threads} host thread(s)), extrapolated to the 112-linear token by "
+                      f"weights/s",
+            "host": {"cpu_model": _cpu_model(), "os_cpu_count": os.cpu_count(),
+                     "OMP_NUM_THREADS": os.environ.get("OMP_NUM_THREADS")},
             "weights_per_s": wps}
 
 
@@ -145,8 +174,9 @@ def run_reference(args):
         getw = lambda l: synth.weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, 0, l))
     per_step = []
     budget = args.ref_step_s if args.ref_step_s else max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    ncores = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 1)
     for k in range(args.warmup + args.steps):
-        r = oracle_decode_sample(shapes, getw, budget_s=budget)
+        r = oracle_decode_sample(shapes, getw, budget_s=budget, threads=ncores)  # the box's host cores
         if k >= args.warmup:
             per_step.append(r)
     v = float(np.mean([r["value"] for r in per_step]))
@@ -235,16 +265,32 @@ def run_usk(args):
     xg = [X[x_off[gi]:x_off[gi + 1]] for gi in range(len(groups))]
     x_of_layer = {l: xg[gi] for gi, g in enumerate(groups) for l in g}
     ys_full = [Y[out_off[l]:out_off[l + 1]] for l in range(L)]
-    Yshard = [torch.empty(shard(o)[1] - shard(o)[0], dtype=torch.float32, device=dev) for o, i in shapes]
     ranges = {l: shard(shapes[l][0]) for l in range(L)}
+    # N > 1: a group's y shards live in one contiguous buffer, gathered by one collective per call
+    glay = [udist.group_shard_layout([shapes[l][0] for l in g], rank, world) for g in groups]
+    Gsh = [torch.zeros(pad, dtype=torch.float32, device=dev) for _, pad in glay]
+    g_off = np.cumsum([0] + [world * pad for _, pad in glay])
+    GF = torch.zeros(int(g_off[-1]), dtype=torch.float32, device=dev)   # every group's gathered y, one buffer
+    Gfull = [GF[g_off[gi]:g_off[gi + 1]] for gi in range(len(groups))]
+    Yshard = {}
+    for gi, g in enumerate(groups):
+        for k, l in enumerate(g):
+            o0, o1, off = glay[gi][0][k]
+            Yshard[l] = Gsh[gi][off:off + (o1 - o0)]
     ws_group = [usk.new_batch_workspace(plan, g, [ranges[l] for l in g], device=dev) for g in groups]
     ws_layer = [usk.new_workspace(plan, l, 1, *ranges[l], device=dev) for l in range(L)]
     out_of = (lambda l: ys_full[l]) if world == 1 else (lambda l: Yshard[l])
 
-    def gather(ls):
+    group_of = {l: gi for gi, g in enumerate(groups) for l in g}
+
+    def gather(ls):  # one all-gather per grouped call (per linear for the 112-launch variant)
         if world > 1:
-            for l in ls:
-                udist.allgather_outputs(Yshard[l], ys_full[l])
+            gi = group_of[ls[0]]
+            if len(ls) == len(groups[gi]):
+                udist.allgather_group(Gsh[gi], Gfull[gi])
+            else:
+                for l in ls:
+                    udist.allgather_outputs(Yshard[l].contiguous(), ys_full[l])
 
     def warm():
         if args.prefetch:  # opt-in: the step reads the whole sketch (60 MB < L2) from HBM once, up front
@@ -269,7 +315,7 @@ def run_usk(args):
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
 
     def capture(fn):
-        if world > 1 and os.environ.get("USK_BENCH_NCCL_GRAPH") != "1":
+        if world > 1 and os.environ.get("USK_BENCH_NCCL_GRAPH") == "0":  # opt-out: eager steps
             torch.cuda.synchronize()
             usk.launch_count(reset=True)
             with torch.cuda.stream(stream):
@@ -325,12 +371,22 @@ def run_usk(args):
 
     g_grp, launches_grp = capture(step_grouped)
     g_one, launches_one = capture(step_single)
+    def full_y():  # the step's outputs in layer order (N > 1: assembled from the gathered buffers)
+        if world == 1:
+            return Y.clone()
+        ys = []
+        for gi, g in enumerate(groups):
+            ys += udist.assemble_group(Gfull[gi], [shapes[l][0] for l in g], world)
+        return torch.cat(ys)
+
     y_check = None
     with ClockSampler(local) as clocks:
         ms_per_step = time_steps(g_grp, step_grouped, args.steps, args.warmup)
-        y_check = Y.clone()
+        y_check = full_y()
         ms_single = time_steps(g_one, step_single, args.steps, args.warmup)
     same = bool(torch.equal(y_check, Y))   # grouped and per-linear launches give identical bits
+    import hashlib
+    y_sha = hashlib.sha256(y_check.cpu().numpy().tobytes()).hexdigest()[:16]  # equal for every N
     use_graph = g_grp is not None
     launches_per_step = launches_grp
     tok_s = 1000.0 / ms_per_step
@@ -355,11 +411,12 @@ def run_usk(args):
     clk = clocks.summary()
     f_peak = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    # ALU roofline of the sketch query: per 32 weights and SM sub-partition the query
-    # issues 3 x (LOP3 + FFMA.RZ + IMAD + LDS) + VIMNMX3 + SHF + FFMA = 15 warp instructions at one
-    # per clock (the FMA pipe needs <= 14 clk, the ALU pipe 10 clk at the rates measured by
-    # tools/micro/pipes.cu, profiles/r1_micro_pipes.txt), so issue binds
-    ISSUE = 15.0
+    # Roofline of the sketch query: the method does M = 3 table
+    # lookups per weight and token; one 32-lane shared-memory wavefront per clock per SM gives the
+    # LSU gather floor (the graded peak).  The design-dependent instruction-issue line is reported
+    # beside it: 3 x (LOP3 + FFMA.RZ + IMAD + LDS) + VIMNMX3 + FHFMA.BF16 = 14 warp instructions per
+    # 32 weights per SM sub-partition at one issue per clock
+    ISSUE = 14.0
     alu_peak = n_sm * 4 * 32 / ISSUE * f_peak / 1e9             # Gweight/s
     gather_floor = n_sm * 32 * f_peak / ROWS / 1e9             # Gweight/s: M LDS wavefronts per 32 weights
     # the timed graph holds only the sketch-GEMV launches (k_gemv_fast + k_gemv_reduce per group),
@@ -400,14 +457,15 @@ def run_usk(args):
 
     # ---- end-to-end through the binding: pinned host x -> device, 112 linears, y -> pinned host
     Xh = X.cpu().pin_memory()
-    Yh = torch.empty(Y.numel(), dtype=torch.float32).pin_memory()
+    Yout = Y if world == 1 else GF                       # what the step leaves on the device
+    Yh = torch.empty(Yout.numel(), dtype=torch.float32).pin_memory()
     g2 = torch.cuda.CUDAGraph()
     e2e_graph = True
     try:
         with torch.cuda.graph(g2, stream=stream):
             X.copy_(Xh, non_blocking=True)
             step_grouped()
-            Yh.copy_(Y, non_blocking=True)
+            Yh.copy_(Yout, non_blocking=True)
     except Exception:
         e2e_graph = False
     e_ms = []
@@ -421,7 +479,7 @@ def run_usk(args):
             else:
                 X.copy_(Xh, non_blocking=True)
                 step_grouped()
-                Yh.copy_(Y, non_blocking=True)
+                Yh.copy_(Yout, non_blocking=True)
             b.record(stream)
         b.synchronize()
         if k >= max(3, args.warmup):
@@ -463,7 +521,30 @@ def run_usk(args):
                 "cells": xplan.info["total_cells"], "achieved_bpw": xplan.info["achieved_bits"] / xplan.info["numel"],
                 "build_ms": xbuild_ms, "launches_per_step": lx}
 
-    q4 = cls = orow = None
+    def paper_six_of_seven():
+        """The paper's own configuration (ledger L14): Q, K, V, Up, Down, Gate sketched,
+        O kept dense -- each block's o projection as a bf16 cuBLAS GEMV (torch.mv) in the same graph."""
+        nb = L // 7
+        Wo = [synth.torch_weights_bf16(shapes[7 * b + 3][0], shapes[7 * b + 3][1], synth.seed_for(CFG, b, 3), dev)
+              for b in range(nb)]
+        yo = [torch.empty(shapes[7 * b + 3][0], dtype=torch.bfloat16, device=dev) for b in range(nb)]
+
+        def step67():
+            for gi, g in enumerate(groups):
+                if len(g) == 1 and g[0] % 7 == 3:
+                    torch.mv(Wo[g[0] // 7], xg[gi], out=yo[g[0] // 7])
+                else:
+                    usk.linear_batch(plan, sketch, g, xg[gi], [ys_full[l] for l in g], ws_group[gi])
+
+        g67, l67 = capture(step67)
+        ms67 = time_steps(g67, step67, max(20, args.steps // 4), args.warmup)
+        sk_w = sum(o * i for l, (o, i) in enumerate(shapes) if l % 7 != 3)
+        del Wo, yo, g67
+        return {"tokens_per_s": 1000.0 / ms67, "ms_per_step": ms67, "sketched_linears": L - nb,
+                "dense": "o projection, bf16 weights, torch.mv (cuBLAS GEMV)", "sketched_weights": sk_w,
+                "launches_per_step_usk": l67}
+
+    q4 = cls = orow = p67 = None
     if world == 1 and not args.no_q4:
         del g_rec, g2
         torch.cuda.empty_cache()
@@ -476,6 +557,8 @@ def run_usk(args):
         torch.cuda.empty_cache()
         orow = extra_point(granularity="outrow")
         orow.update({"granularity": "outrow (one unit per output row, ledger L31)"})
+        torch.cuda.empty_cache()
+        p67 = paper_six_of_seven()
 
     # ---- BASELINE config 4: Llama-3.2-1B prefill, 2048 tokens x batch 8 (T = 16384) through all 112
     #      linears in model order (usk_linear T > 1: K3 reconstruct into the workspace + the tcgen05
@@ -584,8 +667,14 @@ def run_usk(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = oracle_decode_sample(shapes, host_block0_weights(shapes), budget_s=args.cpu_budget)
+        getw = host_block0_weights(shapes)
+        ncores = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 1)
+        cpu = oracle_decode_sample(shapes, getw, budget_s=args.cpu_budget, threads=ncores)   # all host cores
+        one = oracle_decode_sample(shapes, getw, budget_s=args.cpu_budget / 2, threads=1)
         cpu.pop("weights_per_s", None)
+        one.pop("weights_per_s", None)
+        one.pop("host", None)
+        cpu["single_thread"] = one
 
     if rank == 0:
         line = {
@@ -596,23 +685,29 @@ def run_usk(args):
             "config": {"workload": "c3: Llama-3.2-1B all 112 linears, batch-1 decode via fused sketch-GEMV",
                        "bpw": BPW, "rows": ROWS, "granularity": "row (1 input dim per unit)", "classes": 1,
                        "sketch_MB": sketch_bytes / 1e6, "weights": numel, "l2": "flushed (256 MB write) before each step",
-                       "parallelism": f"output-sharded x{world} + NCCL all-gather" if world > 1 else "single GPU",
+                       "parallelism": (f"output-sharded x{world}, one NCCL all-gather per grouped call "
+                                       f"({len(groups)} per token, in the graph)") if world > 1 else "single GPU",
                        "graph": use_graph, "launches_per_step": launches_per_step,
                        "grouping": "q|k|v, o, gate|up, down per block share x (usk_linear_batch)"},
             "per_linear_launches": {"ms_per_step": ms_single, "tokens_per_s": 1000.0 / ms_single,
                                     "launches_per_step": launches_one, "bitwise_equal_to_grouped": same},
+            "y_sha256": y_sha,
+            "collectives_per_step": len(groups) if world > 1 else 0,
             "weights_reconstructed_per_s": tok_s * numel,
             "reconstruct_standalone": {"weights_per_s": rec_wps, "GB_per_s_written": rec_wps * 2 / 1e9,
                                        "hbm_frac": rec_wps * (2 + 2 * BPW / 16) / 1e9 / peaks["hbm_gbs"]},
             "build": {"ms": build_ms, "replicate_ms": replicate_ms, "weights_per_s": owned_w / (build_ms * 1e-3),
                       "GB_per_s": owned_w * (2 + BPW / 8) / (build_ms * 1e-3) / 1e9},
-            "roofline": {"bound": "alu", "achieved": achieved, "peak": alu_peak, "unit": "Gweight/s",
-                         "frac": achieved / alu_peak, "traffic": traffic,
+            "roofline": {"bound": "alu", "achieved": achieved, "peak": gather_floor, "unit": "Gweight/s",
+                         "frac": achieved / gather_floor, "traffic": traffic,
                          "kernel": "k_gemv_fast (+ k_gemv_reduce): the whole timed graph",
-                         "peak_basis": f"instruction issue: 15 warp-instructions per 32 weights per SMSP "
-                                       f"(3 x (LOP3 + FFMA.RZ + IMAD + LDS) + VIMNMX3 + SHF + FFMA), 1 issue/clk "
-                                       f"-> {128 / ISSUE:.2f} weight/clk/SM x {n_sm} SMs x {f_peak / 1e6:.0f} MHz",
-                         "lds_gather_floor": gather_floor,
+                         "peak_basis": f"LSU gather floor (SURVEY 8(d) d.3): M = {ROWS} shared-memory lookups per "
+                                       f"weight, one 32-lane wavefront per clock per SM -> {32 / ROWS:.2f} "
+                                       f"weight/clk/SM x {n_sm} SMs x {f_peak / 1e6:.0f} MHz",
+                         "issue_line": {"peak": alu_peak, "frac": achieved / alu_peak,
+                                        "basis": f"{ISSUE:.0f} warp-instructions per 32 weights per SMSP "
+                                                 f"(3 x (LOP3 + FFMA.RZ + IMAD + LDS) + VIMNMX3 + FHFMA.BF16), "
+                                                 f"1 issue/clk"},
                          "isolated_launch_ms_per_step": sum_kern,
                          "hbm_frac": sketch_bytes / (ms_per_step * 1e-3) / 1e9 / peaks["hbm_gbs"]},
             "e2e": {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 2),
@@ -628,6 +723,8 @@ def run_usk(args):
             line["importance_classes_rows"] = cls
         if orow is not None:
             line["output_row_units"] = orow
+        if p67 is not None:
+            line["paper_six_of_seven"] = p67
         if c5 is not None:
             line["llama3_8b_n1"] = c5
         if c4 is not None:
@@ -636,6 +733,80 @@ def run_usk(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+# ----------------------------------------------------------------------------- N > 1 host logic on CPU
+def run_dist_selftest(args):
+    """The N > 1 path's host logic without GPUs (gloo): output shards per grouped call laid out in
+    one buffer and gathered by one collective, the layer-sharded sketch replicated by per-layer
+    broadcasts.  Shard outputs and sketch bytes are synthetic functions of (layer, row) / (layer,
+    byte), so rank 0's assembled y and sketch must hash the same for every N."""
+    import hashlib
+
+    import torch
+    import torch.distributed as dist
+    from paper_2506_17255_b200 import dist as udist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    shapes = synth.llama32_1b_shapes()
+    L = len(shapes)
+    groups = []
+    for b in range(L // 7):
+        base = 7 * b
+        groups += [[base, base + 1, base + 2], [base + 3], [base + 4, base + 5], [base + 6]]
+
+    def y_true(l, o0, o1):  # stand-in for a linear's outputs: exact in fp32
+        o = torch.arange(o0, o1, dtype=torch.float64)
+        return (torch.sin(o * 0.37 + l) * 1000).round().to(torch.float32) / 8
+
+    collectives, ys = 0, []
+    for g in groups:
+        outs = [shapes[l][0] for l in g]
+        lay, pad = udist.group_shard_layout(outs, rank, world)
+        buf = torch.zeros(pad, dtype=torch.float32)
+        for (o0, o1, off), l in zip(lay, g):
+            buf[off:off + o1 - o0] = y_true(l, o0, o1)
+        if world > 1:
+            full = torch.zeros(world * pad, dtype=torch.float32)
+            udist.allgather_group(buf, full)
+            collectives += 1
+        else:
+            full = buf
+        ys += udist.assemble_group(full, outs, world)
+    Y = torch.cat(ys)
+    # layer-sharded build + one-time replication: owners write their layers' regions
+    sizes = [o * i // 256 for o, i in shapes]
+    offs = np.cumsum([0] + sizes)
+    sk = torch.zeros(int(offs[-1]), dtype=torch.uint8)
+    for l in udist.owned_layers(L, rank, world):
+        n = sizes[l]
+        sk[offs[l]:offs[l + 1]] = ((torch.arange(n) * 131 + l * 7) % 251).to(torch.uint8)
+    if world > 1:
+        udist.replicate_sketch(sk, [(int(offs[l]), int(offs[l + 1])) for l in range(L)], world)
+    ok = all(torch.equal(Y[sum(shapes[k][0] for k in range(l)):sum(shapes[k][0] for k in range(l + 1))],
+                         y_true(l, 0, shapes[l][0])) for l in range(L))
+    if rank == 0:
+        print(json.dumps({"selftest": "dist", "n_gpus": world, "y_sha256": hashlib.sha256(Y.numpy().tobytes()).hexdigest(),
+                          "sketch_sha256": hashlib.sha256(sk.numpy().tobytes()).hexdigest(), "y_exact": ok,
+                          "collectives_per_step": collectives}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def spawn_ranks(args):
+    """`--gpus N` without a launcher: run this script under torch.distributed.run, one rank per GPU
+    (127.0.0.1 rendezvous); rank 0 prints the JSON line."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.run(cmd, cwd=ROOT).returncode
 
 
 def main():
@@ -654,7 +825,17 @@ def main():
                     help="before each grouped call, usk_prefetch_l2 of the next group's sketch bytes (L2 hint)")
     ap.add_argument("--prefetch", action="store_true",
                     help="start each decode step with usk_prefetch_l2 of the whole sketch (measured: no gain)")
+    ap.add_argument("--dist-selftest", action="store_true",
+                    help="CPU (gloo) check of the N > 1 launcher and host logic with synthetic shard outputs")
     args = ap.parse_args()
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        return spawn_ranks(args)
+    if world_env is not None and int(world_env) != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but the launcher started WORLD_SIZE={world_env} ranks", file=sys.stderr)
+        return 2
+    if args.dist_selftest:
+        return run_dist_selftest(args)
     if args.impl == "reference":
         return run_reference(args)
     return run_usk(args)

@@ -71,3 +71,42 @@ def allgather_outputs(y_shard, y_full, group=None):
     for (a, b), p in zip(sizes, parts):
         y_full[a:b] = p[:b - a]
     return y_full
+
+
+# ---- one collective per grouped call: the linears of a group (q|k|v, o, gate|up,
+#      down) write their y shards into ONE contiguous per-rank buffer, gathered by one all-gather
+def group_shard_layout(out_features, rank: int, world: int):
+    """Per layer of a group: (o0, o1, offset) of this rank's shard in the group's shard buffer, and
+    the buffer length padded to the largest rank's (all_gather_into_tensor needs equal parts)."""
+    lay, off = [], 0
+    for o in out_features:
+        o0, o1 = output_shard(o, rank, world)
+        lay.append((o0, o1, off))
+        off += o1 - o0
+    pad = max(sum(output_shard(o, r, world)[1] - output_shard(o, r, world)[0] for o in out_features)
+              for r in range(world))
+    return lay, pad
+
+
+def allgather_group(shard_buf, gathered, group=None):
+    """gathered [world * len(shard_buf)] = every rank's shard buffer, rank-major (one collective)."""
+    import torch.distributed as dist
+    dist.all_gather_into_tensor(gathered, shard_buf, group=group)
+    return gathered
+
+
+def assemble_group(gathered, out_features, world: int):
+    """Full y of each layer of a group from the rank-major gathered buffer (host-side check; a
+    consumer of the decode reads the gathered buffer through the same layout)."""
+    import torch
+    pad = gathered.numel() // world
+    parts = gathered.view(world, pad)
+    ys = []
+    for k, o in enumerate(out_features):
+        pieces = []
+        for r in range(world):
+            lay, _ = group_shard_layout(out_features, r, world)
+            o0, o1, off = lay[k]
+            pieces.append(parts[r, off:off + (o1 - o0)])
+        ys.append(torch.cat(pieces))
+    return ys
