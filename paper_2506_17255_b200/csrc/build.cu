@@ -24,6 +24,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -67,10 +68,12 @@ struct BuildArgs {
   void* sketch;
   int* err;
   uint32_t kap_max;  // largest accepted weight key: 0xFEFFFFFF (finite), 0xFF000000 (+Inf = excluded outlier)
+  int32_t stages;    // ring depth: as many stages as the shared memory left beside the keys holds (<= kMaxStages)
 };
 
-template <int ES>
-constexpr int stages_for() { return (ES == 2 ? 6 : 4) * 32 / kRO; }
+constexpr int kMaxStages = 16;   // ring depth cap (the mbarrier header holds 2 x 16 barriers)
+constexpr int kMinStages = 3;
+constexpr int kBuildHdr = 256;   // full[16] + empty[16] mbarriers
 
 template <typename E, int UPL>
 constexpr int stage_bytes() { return kRO * 16 + kRO * 32 * UPL * (int)sizeof(E); }
@@ -88,13 +91,13 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   constexpr int ES = sizeof(E);
   constexpr int TJ = 32 * UPL;
   constexpr int ROWB = TJ * ES;
-  constexpr int S = stages_for<ES>();
+  const int S = A.stages;  // ring depth (host: as many stages as fit beside the keys)
   constexpr int STAGEB = stage_bytes<E, UPL>();
   constexpr int MR = MT > 0 ? MT : 8;
   extern __shared__ __align__(128) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem);
-  uint64_t* empty = full + S;
-  uint8_t* stages = smem + 128;
+  uint64_t* empty = full + kMaxStages;
+  uint8_t* stages = smem + kBuildHdr;
   uint32_t* keys = reinterpret_cast<uint32_t*>(stages + S * STAGEB);
   const uint32_t smem_keys = smem_u32(keys);
 
@@ -185,64 +188,91 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       const uint8_t* st = stages + s * STAGEB;
       const int64_t o0 = it * kRO;
       const int rows = (int)min((int64_t)kRO, T.out - o0);
+      constexpr int RR = kRO / kConsumers;
+      if (FAST && ES == 2 && UPL == 4 && rows == kRO) {
+        // a full stage: every row's weights and position mixes are loaded before any update, so the
+        // shared-load latency of a row overlaps the previous rows' hashing and atomics
+        uint2 w2[RR];
+        uint4 R4v[RR];
 #pragma unroll
-      for (int rr = 0; rr < kRO / kConsumers; ++rr) {
-        const int r = cw + rr * kConsumers;
-        if (r >= rows) break;
-        const uint32_t o = (uint32_t)(o0 + r);
-        const uint8_t* row = st + kRO * 16 + r * ROWB;
-        uint32_t bits[UPL];
-        if constexpr (ES == 2 && UPL == 4) {
-          const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
-          bits[0] = v2.x << 16;
-          bits[1 % UPL] = v2.x & 0xFFFF0000u;
-          bits[2 % UPL] = v2.y << 16;
-          bits[3 % UPL] = v2.y & 0xFFFF0000u;
-        } else if constexpr (ES == 2 && UPL == 2) {
-          const uint32_t v2 = reinterpret_cast<const uint32_t*>(row)[lane];
-          bits[0] = v2 << 16;
-          bits[1 % UPL] = v2 & 0xFFFF0000u;
-        } else if constexpr (ES == 2) {
-          bits[0] = (uint32_t)reinterpret_cast<const uint16_t*>(row)[lane] << 16;
-        } else if constexpr (UPL == 4) {
-          const uint4 v4 = reinterpret_cast<const uint4*>(row)[lane];
-          bits[0] = v4.x;
-          bits[1 % UPL] = v4.y;
-          bits[2 % UPL] = v4.z;
-          bits[3 % UPL] = v4.w;
-        } else if constexpr (UPL == 2) {
-          const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
-          bits[0] = v2.x;
-          bits[1 % UPL] = v2.y;
-        } else {
-          bits[0] = reinterpret_cast<const uint32_t*>(row)[lane];
+        for (int rr = 0; rr < RR; ++rr) {
+          const int r = cw + rr * kConsumers;
+          w2[rr] = reinterpret_cast<const uint2*>(st + kRO * 16 + r * ROWB)[lane];
+          R4v[rr] = reinterpret_cast<const uint4*>(st)[r];  // broadcast
         }
-        if constexpr (FAST) {
-          const uint4 R4 = reinterpret_cast<const uint4*>(st)[r];  // broadcast shared load
-          const uint32_t R23[3] = {R4.x, R4.y, R4.z};
 #pragma unroll
-          for (int v = 0; v < UPL; ++v) {
-            const uint32_t kap = rotl1(bits[v]);  // missing units: zero-filled by the tensor copy
+        for (int rr = 0; rr < RR; ++rr) {
+          const uint32_t bts[4] = {w2[rr].x << 16, w2[rr].x & 0xFFFF0000u, w2[rr].y << 16, w2[rr].y & 0xFFFF0000u};
+          const uint32_t R23[3] = {R4v[rr].x, R4v[rr].y, R4v[rr].z};
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            const uint32_t kap = rotl1(bts[v]);
             kmax = max(kmax, kap);
 #pragma unroll
-            for (int i = 0; i < MT; ++i) key_min(short_fma_bits(R23[i], fk[v][i], Nf[v], cb[v][i]) * 128u + kbase, kap);
+            for (int i = 0; i < (MT > 0 ? MT : 1); ++i)
+              key_min(short_fma_bits(R23[i], fk[v % UPL][i % KR], Nf[v % UPL], cb[v % UPL][i % KR]) * 128u + kbase, kap);
           }
-        } else {
+        }
+      } else {
 #pragma unroll
-          for (int v = 0; v < UPL; ++v) {
-            const uint32_t kap = rotl1(bits[v]);  // missing units: zero-filled by the tensor copy
-            kmax = max(kmax, kap);
-#pragma unroll
-            for (int i = 0; i < MR; ++i) {
-              if (MT == 0 && i >= M) break;
-              uint32_t idx;
-              if constexpr (HASH == USK_HASH_X) idx = hash_index_x(A.hc, o, K[v], i, N[v]);
-              else idx = o % N[v];
-              key_min(smem_keys + rb[v][i] + (idx << 7), kap);
+        for (int rr = 0; rr < kRO / kConsumers; ++rr) {
+          const int r = cw + rr * kConsumers;
+          if (r >= rows) break;
+          const uint32_t o = (uint32_t)(o0 + r);
+          const uint8_t* row = st + kRO * 16 + r * ROWB;
+          uint32_t bits[UPL];
+          if constexpr (ES == 2 && UPL == 4) {
+            const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
+            bits[0] = v2.x << 16;
+            bits[1 % UPL] = v2.x & 0xFFFF0000u;
+            bits[2 % UPL] = v2.y << 16;
+            bits[3 % UPL] = v2.y & 0xFFFF0000u;
+          } else if constexpr (ES == 2 && UPL == 2) {
+            const uint32_t v2 = reinterpret_cast<const uint32_t*>(row)[lane];
+            bits[0] = v2 << 16;
+            bits[1 % UPL] = v2 & 0xFFFF0000u;
+          } else if constexpr (ES == 2) {
+            bits[0] = (uint32_t)reinterpret_cast<const uint16_t*>(row)[lane] << 16;
+          } else if constexpr (UPL == 4) {
+            const uint4 v4 = reinterpret_cast<const uint4*>(row)[lane];
+            bits[0] = v4.x;
+            bits[1 % UPL] = v4.y;
+            bits[2 % UPL] = v4.z;
+            bits[3 % UPL] = v4.w;
+          } else if constexpr (UPL == 2) {
+            const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
+            bits[0] = v2.x;
+            bits[1 % UPL] = v2.y;
+          } else {
+            bits[0] = reinterpret_cast<const uint32_t*>(row)[lane];
+          }
+          if constexpr (FAST) {
+            const uint4 R4 = reinterpret_cast<const uint4*>(st)[r];  // broadcast shared load
+            const uint32_t R23[3] = {R4.x, R4.y, R4.z};
+  #pragma unroll
+            for (int v = 0; v < UPL; ++v) {
+              const uint32_t kap = rotl1(bits[v]);  // missing units: zero-filled by the tensor copy
+              kmax = max(kmax, kap);
+  #pragma unroll
+              for (int i = 0; i < MT; ++i) key_min(short_fma_bits(R23[i], fk[v][i], Nf[v], cb[v][i]) * 128u + kbase, kap);
+            }
+          } else {
+  #pragma unroll
+            for (int v = 0; v < UPL; ++v) {
+              const uint32_t kap = rotl1(bits[v]);  // missing units: zero-filled by the tensor copy
+              kmax = max(kmax, kap);
+  #pragma unroll
+              for (int i = 0; i < MR; ++i) {
+                if (MT == 0 && i >= M) break;
+                uint32_t idx;
+                if constexpr (HASH == USK_HASH_X) idx = hash_index_x(A.hc, o, K[v], i, N[v]);
+                else idx = o % N[v];
+                key_min(smem_keys + rb[v][i] + (idx << 7), kap);
+              }
             }
           }
         }
-      }
+        }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
       if (++s == S) {
@@ -254,8 +284,18 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   }
   __syncthreads();
 
-  // ---------------- write states: lane L's units, cells k spread over all warps
+  // ---------------- write states.  The tile's units are consecutive in the sketch, so its cells are
+  // ONE contiguous range [c0, c1).  Keys -> states into a staging copy of that range in the (now
+  // idle) ring memory -- lane L reads its own units' keys (bank L, conflict-free) -- then one bulk
+  // copy shared -> global for the 16-B aligned middle; the few cells of the unaligned head / tail go
+  // out as plain stores.  (Per-lane stores straight from the keys would be 2-byte writes ~MN cells
+  // apart: 32 sectors per warp store instruction.)
   E* out = reinterpret_cast<E*>(A.sketch);
+  const int64_t c0 = A.offsets[T.unit_base + j0], c1 = A.offsets[T.unit_base + j0 + nu];
+  const int64_t ncell = c1 - c0;
+  const uint32_t lead = (uint32_t)((c0 * ES) & 15);  // staging byte offset = global byte address mod 16
+  const bool staged = (size_t)ncell * ES + 16 <= (size_t)S * STAGEB;
+  E* stg = reinterpret_cast<E*>(stages + lead);
 #pragma unroll
   for (int v = 0; v < UPL; ++v) {
     const int ul = UPL * lane + v;
@@ -269,8 +309,25 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       // a cell that only outliers (or nothing) map to holds +0 (DESIGN.md ledger L29)
       const uint32_t b32 = (A.kap_max >= 0xFF000000u && key >= 0xFF000000u) ? 0u
                            : (key == ~0u) ? 0x7F800000u : rotr1(key);
-      if constexpr (ES == 2) out[off + k] = (uint16_t)(b32 >> 16);
-      else out[off + k] = b32;
+      const E cv = ES == 2 ? (E)(b32 >> 16) : (E)b32;
+      if (staged) stg[off - c0 + k] = cv;
+      else out[off + k] = cv;
+    }
+  }
+  if (staged) {
+    const int64_t g0 = c0 * ES, g1 = c1 * ES;              // tile byte range in the sketch
+    const int64_t a0 = (g0 + 15) & ~int64_t(15), a1 = g1 & ~int64_t(15);
+    fence_proxy_async_smem();                              // generic-proxy staging writes -> bulk copy
+    __syncthreads();
+    if (a1 > a0) {
+      if (threadIdx.x == 0) {
+        bulk_s2g(reinterpret_cast<uint8_t*>(A.sketch) + a0, stages + lead + (a0 - g0), (uint32_t)(a1 - a0));
+        bulk_s2g_wait();                                   // complete before the CTA exits
+      }
+      for (int64_t c = c0 + threadIdx.x; c * ES < a0 && c < c1; c += blockDim.x) out[c] = stg[c - c0];
+      for (int64_t c = a1 / ES + threadIdx.x; c < c1; c += blockDim.x) out[c] = stg[c - c0];
+    } else {
+      for (int64_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) out[c] = stg[c - c0];
     }
   }
 }
@@ -559,8 +616,8 @@ int fast_upl(const usk_plan* pl, int32_t l, bool pitch_ok = false) {
   const int es = pl->cell_bytes();
   if (!pitch_ok && ((outrow ? L.out : L.in) * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
-  const int S = (es == 2 ? 6 : 4) * 32 / kRO;
-  auto smem = [&](int upl) { return (int64_t)128 + S * (kRO * 16 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
+  const int S = kMinStages;
+  auto smem = [&](int upl) { return (int64_t)kBuildHdr + S * (kRO * 16 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
   for (int upl : {4, 2, 1})
     if (smem(upl) <= (int64_t)kSmemLimit) return upl;
   return 0;
@@ -568,8 +625,15 @@ int fast_upl(const usk_plan* pl, int32_t l, bool pitch_ok = false) {
 
 template <typename E, int UPL, int MT, int HASH>
 usk_status launch_fast_t(BuildArgs& A, int n_ctas, cudaStream_t st) {
-  constexpr int S = stages_for<sizeof(E)>();
-  const size_t smem = 128 + (size_t)S * stage_bytes<E, UPL>() + (size_t)32 * UPL * A.maxMN * 4 + 128;
+  // ring depth: every stage the shared memory beside the keys holds (the bulk copies in flight per SM
+  // must cover the HBM latency-bandwidth product: 3 stages of gate/up tiles are ~52 KB)
+  const size_t keys = (size_t)32 * UPL * A.maxMN * 4 + 128;
+  static const int forced = [] { const char* e = std::getenv("USK_BUILD_STAGES"); return e ? std::atoi(e) : 0; }();
+  int S = (int)std::min<size_t>(kMaxStages, (kSmemLimit - kBuildHdr - keys) / stage_bytes<E, UPL>());
+  if (forced > 0) S = std::min(S, forced);
+  if (S < kMinStages) return fail(USK_EINVAL, "usk_build: tile does not fit shared memory");
+  A.stages = S;
+  const size_t smem = kBuildHdr + (size_t)S * stage_bytes<E, UPL>() + keys;
   auto kern = k_build_fast<E, UPL, MT, HASH>;
   USK_CUDA(ensure_smem((const void*)kern, 227 * 1024));  // one limit per (device, kernel): the opt-in maximum
   kern<<<n_ctas, kBuildThreads, smem, st>>>(A);
