@@ -1583,7 +1583,9 @@ usk_status launch_reconstruct(const usk_plan* pl, const void* sketch, int32_t l,
     A.rows = rows;
     const int grid = partition_items(A, G);
     first_copies(pl, A, G, grid);
-    usk_status s = launch_q(G.kern, A, grid, G.smem, false, st);
+    // PDL: the kernel stages its sketch chunk (read-only) before griddepcontrol.wait and writes w_out
+    // only after it, so it may start under the previous launch's tail (back-to-back reconstructs)
+    usk_status s = launch_q(G.kern, A, grid, G.smem, true, st);
     if (s != USK_OK) return s;
   } else {
     GenQ Q = make_genq(pl, l, sketch);
