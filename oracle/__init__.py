@@ -23,7 +23,8 @@ LIB = os.path.join(HERE, "liboracle.so")
 
 F32, BF16 = 0, 1
 ABSMAXMIN, ABSMINMAX, COUNTMIN = 0, 1, 2
-HASH_X, HASH_IDENTITY = 0, 1
+HASH_X, HASH_IDENTITY, HASH_XG = 0, 1, 2
+KEY_GROUP = 8  # USK-XG: units t = 8g..8g+7 of a layer share the unit key K_(l, g) (L32)
 GRAN_ROW, GRAN_LAYER, GRAN_OUTROW = 0, 1, 2
 OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE = 0, 1, 2, 3, 4
 

@@ -54,6 +54,8 @@
 
 #define UO_HASH_X 0
 #define UO_HASH_IDENTITY 1
+#define UO_HASH_XG 2 /* USK-X with unit keys shared by groups of UO_KEY_GROUP consecutive units (ledger L32) */
+#define UO_KEY_GROUP 8
 
 #define UO_GRAN_ROW 0
 #define UO_GRAN_LAYER 1
@@ -119,6 +121,10 @@ uint32_t uo_hash_word(uint64_t seed, uint32_t layer, uint32_t t, int32_t row, ui
 uint32_t uo_hash_index(int32_t kind, uint64_t seed, uint32_t layer, uint32_t t, int32_t row,
                        uint32_t p, uint32_t ncols) {
   if (kind == UO_HASH_IDENTITY) return p % ncols; /* SPEC.md:54 test_hash: flat_index mod columns */
+  /* USK-XG (DESIGN.md ledger L32): the M hash functions H_i of PAPER.md:243 are shared by the
+   * UO_KEY_GROUP consecutive units t = 8g .. 8g+7 of a layer -- the unit key is that of the group,
+   * K_(l, floor(t / 8)) -- and unchanged otherwise */
+  if (kind == UO_HASH_XG) t = t / UO_KEY_GROUP;
   {
     uint32_t h = uo_hash_word(seed, layer, t, row, p);
     if (ncols <= 65536u) return (uint32_t)(((uint64_t)(h & 0x7FFFFFu) * (uint64_t)ncols) >> 23);

@@ -25,7 +25,7 @@ def _to_bits(vals, dtype):
 
 
 @pytest.mark.parametrize("dtype", [0, 1])
-@pytest.mark.parametrize("hash_kind", [0, 1])
+@pytest.mark.parametrize("hash_kind", [0, 1, 2])
 def test_brute_force_buckets_and_reconstruction(orc, dtype, hash_kind):
     rng = np.random.default_rng(100 + 10 * dtype + hash_kind)
     n_cases = 0

@@ -85,3 +85,55 @@ def test_short_unit_float_form(orc):
         bits = (152 << 23) + (rz - (1 << 25)) // 4
         assert bits - 0x4C000000 - off == (k * N) >> 23
         assert (bits * 128) % (1 << 32) == ((off + ((k * N) >> 23)) * 128) % (1 << 32)
+
+
+def usk_xg(seed, layer, t, row, p, N):
+    """USK-XG (DESIGN.md ledger L32), from the text: USK-X with the unit key of the key group
+    floor(t / 8) in place of t."""
+    return usk_x(seed, layer, t // 8, row, p, N)
+
+
+def test_xg_second_implementation(orc):
+    rng = np.random.default_rng(11)
+    for _ in range(3000):
+        seed = int(rng.integers(0, 2**63))
+        layer, t = int(rng.integers(0, 300)), int(rng.integers(0, 20000))
+        row, p = int(rng.integers(0, 8)), int(rng.integers(0, 2**32))
+        N = int(rng.integers(1, 2**31)) if rng.integers(0, 2) else int(rng.integers(1, 2**16 + 2))
+        assert orc.hash_index(orc.HASH_XG, seed, layer, t, row, p, N) == usk_xg(seed, layer, t, row, p, N)
+
+
+def test_xg_groups(orc):
+    """The 8 units of a key group hash every position identically (for equal N); units of
+    different groups, and the same unit under USK-X, hash differently (row-wise independent
+    functions, PAPER.md:233-235)."""
+    pos = np.arange(4096, dtype=np.uint32)
+    N = 85
+    base = orc.hash_indices(orc.HASH_XG, 5, 3, 16, 3, pos, N)
+    for t in range(17, 24):
+        np.testing.assert_array_equal(orc.hash_indices(orc.HASH_XG, 5, 3, t, 3, pos, N), base)
+    for t in (15, 24, 1000):
+        assert (orc.hash_indices(orc.HASH_XG, 5, 3, t, 3, pos, N) != base).mean() > 0.9
+    # group g of USK-XG is unit g of USK-X
+    np.testing.assert_array_equal(base, orc.hash_indices(orc.HASH_X, 5, 3, 2, 3, pos, N))
+
+
+def test_packed_float_form():
+    """The packed decode kernel (L32) evaluates the short-unit reduction with the result
+    at ulp 512: with f = 1 + k/2^23 and c = 2^32 + B - 512 N (B a multiple of 512, B + 512 N < 2^32),
+    RZ(f * 512N + c) = 2^32 + B + 512 floor(k N / 2^23), so bits * 512 mod 2^32 = B + 512 idx -- the
+    byte address of column idx in a 512-B-per-column slot row.  Checked with exact rationals."""
+    from fractions import Fraction
+    rng = np.random.default_rng(6)
+    for _ in range(3000):
+        k = int(rng.integers(0, 1 << 23))
+        N = int(rng.integers(1, 1 << 16))
+        B = int(rng.integers(0, ((1 << 32) - 512 * N) // 512)) * 512
+        c = (1 << 32) + B - 512 * N
+        # c must be an fp32 number: a multiple of its ulp (256 below 2^32, 512 above)
+        assert c % (256 if c < (1 << 32) else 512) == 0 and (1 << 31) <= c < (1 << 33)
+        exact = Fraction((1 << 23) + k, 1 << 23) * (512 * N) + c
+        rz = (exact.numerator // exact.denominator) // 512 * 512  # toward zero, ulp 512 in [2^32, 2^33)
+        assert (1 << 32) <= rz < (1 << 33)
+        bits = (159 << 23) + (rz - (1 << 32)) // 512
+        assert (bits * 512) % (1 << 32) == B + 512 * ((k * N) >> 23)

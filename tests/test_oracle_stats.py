@@ -110,3 +110,34 @@ def test_eq6_error_bound(orc, lam, p):
     cov = float((s >= L).mean())
     se = math.sqrt(p * (1 - p) / occ.sum())
     assert abs(cov - p) <= 4 * se + 1e-3, (cov, p)
+
+
+def test_xg_layer_untouched_and_loads(orc):
+    """USK-XG (L32) at the config-3 load: a ROW-unit layer (2048 positions per unit,
+    M = 3, 0.5 bpw bf16 -> N = 21) sketched and reconstructed by the oracle.  Within each unit the
+    family is the USK-X one, so the untouched fraction must still match Appendix B's closed form,
+    and the per-row bucket loads of a group must be Binomial(k, 1/N); the 8 units of a key group
+    share every index, different groups do not."""
+    import oracle as O
+    out, inn = 2048, 256
+    pl = O.plan([(out, inn)], 0.5, M=3, dtype=O.BF16, hash_kind=O.HASH_XG, seed=41)
+    N = int(pl.ncols[0])
+    assert (np.asarray(pl.ncols) == N).all()
+    rng = np.random.default_rng(41)
+    W = (0.02 * rng.standard_normal((out, inn))).astype(np.float32)
+    Wb = O.f32_to_bf16_rne(W.view(np.uint32)).astype(np.uint16)
+    sk = O.build_model(pl, [Wb])
+    rec = O.reconstruct_rows(pl, sk, 0)
+    frac = float((rec == Wb).mean())
+    expect = untouched_closed_form(out, N, 3)
+    assert abs(frac - expect) <= 4 * math.sqrt(expect * (1 - expect) / (out * inn)) + 2e-3, (frac, expect)
+    pos = np.arange(out, dtype=np.uint32)
+    for g in range(0, inn // 8, 7):
+        idx = O.hash_indices(O.HASH_XG, 41, 0, 8 * g, 3, pos, N)
+        np.testing.assert_array_equal(idx, O.hash_indices(O.HASH_XG, 41, 0, 8 * g + 7, 3, pos, N))
+        if g:
+            assert (idx != O.hash_indices(O.HASH_XG, 41, 0, 0, 3, pos, N)).mean() > 0.8
+        for i in range(3):
+            loads = np.bincount(idx[i], minlength=N)
+            chi2 = (((loads - out / N) ** 2) / (out / N)).sum()
+            assert chi2 < stats.chi2.ppf(0.9999, N - 1)
