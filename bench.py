@@ -211,7 +211,10 @@ def run_usk(args):
     numel = sum(o * i for o, i in shapes)
 
     # ---- plan + build (layer-sharded across ranks, then a one-time replication of the sketch)
-    plan = usk.plan_allocation(shapes, bpw=BPW, rows=ROWS, seed=SEED)
+    # the headline plan: USK-XG unit keys (ledger L32) in the query layout (usk.h USK_LAYOUT_QUERY,
+    # packed decode kernels K4p/K3p); --layout unit_major times the round-1 plan (USK-X, K4)
+    LAY = {"query": dict(hash="xg", layout="query"), "unit_major": dict(hash="x", layout="unit_major")}[args.layout]
+    plan = usk.plan_allocation(shapes, bpw=BPW, rows=ROWS, seed=SEED, **LAY)
     sketch = plan.new_sketch(dev)
     sketch.zero_()
     owned = udist.owned_layers(L, rank, world)  # whole blocks round-robin over ranks
@@ -237,8 +240,11 @@ def run_usk(args):
     owned_w = sum(shapes[l][0] * shapes[l][1] for l in owned)
     replicate_ms = 0.0
     if world > 1:  # one-time replication of the layer-sharded sketch (deployment step)
-        regions = [(plan.layers[l].cell_begin * 2, (plan.layers[l].cell_begin + plan.layers[l].n_cells) * 2)
-                   for l in range(L)]
+        if args.layout == "query":
+            regions = [(plan.layers[l].qbyte_begin, plan.layers[l].qbyte_begin + plan.layers[l].qbytes) for l in range(L)]
+        else:
+            regions = [(plan.layers[l].cell_begin * 2, (plan.layers[l].cell_begin + plan.layers[l].n_cells) * 2)
+                       for l in range(L)]
         torch.cuda.synchronize()
         ev0.record()
         udist.replicate_sketch(sketch, regions, world)
@@ -411,14 +417,18 @@ def run_usk(args):
     clk = clocks.summary()
     f_peak = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
     n_sm = torch.cuda.get_device_properties(dev).multi_processor_count
-    # Roofline of the sketch query: the method does M = 3 table
-    # lookups per weight and token; one 32-lane shared-memory wavefront per clock per SM gives the
-    # LSU gather floor (the graded peak).  The design-dependent instruction-issue line is reported
-    # beside it: 3 x (LOP3 + FFMA.RZ + IMAD + LDS) + VIMNMX3 + FHFMA.BF16 = 14 warp instructions per
-    # 32 weights per SM sub-partition at one issue per clock
-    ISSUE = 14.0
+    # Roofline of the sketch query: the method gathers M = 3 cells per
+    # weight and token from shared memory.  The floor is the shared-memory bandwidth, 128 B/clk/SM:
+    #  * query layout (K4p): 2-byte cells, a key group's 8 cells in one 16-B load -> 64 / M weight/clk/SM
+    #  * unit-major layout (K4): one 32-bit word per lookup -> 32 / M weight/clk/SM
+    # The design-dependent instruction-issue line is reported beside it (per 256 weights of a warp in
+    # K4p: LDS.128 of R + 3 x (LOP3 + FFMA.RZ + IMAD + LDS.128) + 4 VIMNMX3.U16x2 + 4 x (SHF + SHL +
+    # LOP3) + 8 FHFMA.BF16 = 37; in K4: 14 per 32 weights)
+    QL = args.layout == "query"
+    ISSUE = 37.0 / 8 if QL else 14.0
     alu_peak = n_sm * 4 * 32 / ISSUE * f_peak / 1e9             # Gweight/s
-    gather_floor = n_sm * 32 * f_peak / ROWS / 1e9             # Gweight/s: M LDS wavefronts per 32 weights
+    per_clk = (128.0 / (2 * ROWS)) if QL else 32.0 / ROWS
+    gather_floor = n_sm * per_clk * f_peak / 1e9                 # Gweight/s
     # the timed graph holds only the sketch-GEMV launches (k_gemv_fast + k_gemv_reduce per group),
     # so their achieved rate over the timed region is the step's weights / step time
     achieved = w_rank / (ms_per_step * 1e-3) / 1e9
@@ -544,10 +554,14 @@ def run_usk(args):
                 "dense": "o projection, bf16 weights, torch.mv (cuBLAS GEMV)", "sketched_weights": sk_w,
                 "launches_per_step_usk": l67}
 
-    q4 = cls = orow = p67 = None
+    q4 = cls = orow = p67 = um = None
     if world == 1 and not args.no_q4:
         del g_rec, g2
         torch.cuda.empty_cache()
+        if args.layout == "query":  # the round-1 plan on the same workload: USK-X keys, unit-major K4
+            um = extra_point(hash="x", layout="unit_major")
+            um.update({"hash": "USK-X (one key per unit)", "layout": "unit_major", "kernels": "k_gemv_fast + k_gemv_reduce"})
+            torch.cuda.empty_cache()
         q4 = extra_point(state_bits=4, group_size=128)
         q4.update({"state_bits": 4, "group_size": 128})
         torch.cuda.empty_cache()
@@ -595,7 +609,7 @@ def run_usk(args):
 
         flop = 2.0 * T * numel
         ms05 = time_pass(plan, sketch)
-        plan08 = usk.plan_allocation(shapes, bpw=0.8, rows=ROWS, seed=SEED)
+        plan08 = usk.plan_allocation(shapes, bpw=0.8, rows=ROWS, seed=SEED, **LAY)
         sk08 = plan08.new_sketch(dev)
         w8_ = [synth.torch_weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, l // 7, l % 7), dev)
                for l in range(L)]
@@ -624,7 +638,7 @@ def run_usk(args):
         torch.cuda.empty_cache()
         shapes8 = synth.llama3_8b_shapes()
         L8 = len(shapes8)
-        plan8 = usk.plan_allocation(shapes8, bpw=BPW, rows=ROWS, seed=SEED)
+        plan8 = usk.plan_allocation(shapes8, bpw=BPW, rows=ROWS, seed=SEED, **LAY)
         sk8 = plan8.new_sketch(dev)
         w8 = [synth.torch_weights_bf16(o, i, synth.seed_for(5, l // 7, l % 7), dev) for l, (o, i) in enumerate(shapes8)]
         usk.build(plan8, w8, sk8)
@@ -700,14 +714,16 @@ def run_usk(args):
                       "GB_per_s": owned_w * (2 + BPW / 8) / (build_ms * 1e-3) / 1e9},
             "roofline": {"bound": "alu", "achieved": achieved, "peak": gather_floor, "unit": "Gweight/s",
                          "frac": achieved / gather_floor, "traffic": traffic,
-                         "kernel": "k_gemv_fast (+ k_gemv_reduce): the whole timed graph",
-                         "peak_basis": f"LSU gather floor (SURVEY 8(d) d.3): M = {ROWS} shared-memory lookups per "
-                                       f"weight, one 32-lane wavefront per clock per SM -> {32 / ROWS:.2f} "
-                                       f"weight/clk/SM x {n_sm} SMs x {f_peak / 1e6:.0f} MHz",
+                         "kernel": ("k_qgemv (+ k_qreduce)" if QL else "k_gemv_fast (+ k_gemv_reduce)") +
+                                   ": the whole timed graph",
+                         "peak_basis": (f"shared-memory bandwidth floor (SURVEY 8(d) d.3): M = {ROWS} cell gathers "
+                                        f"per weight, " + ("2-B cells, 8 per 16-B load (query layout)" if QL else
+                                                           "one 4-B word per lookup") +
+                                        f", 128 B/clk/SM -> {per_clk:.2f} weight/clk/SM x {n_sm} SMs x "
+                                        f"{f_peak / 1e6:.0f} MHz"),
+                         "lds_floor_32bit_words": n_sm * 32.0 / ROWS * f_peak / 1e9,
                          "issue_line": {"peak": alu_peak, "frac": achieved / alu_peak,
-                                        "basis": f"{ISSUE:.0f} warp-instructions per 32 weights per SMSP "
-                                                 f"(3 x (LOP3 + FFMA.RZ + IMAD + LDS) + VIMNMX3 + FHFMA.BF16), "
-                                                 f"1 issue/clk"},
+                                        "basis": f"{ISSUE:.3f} warp-instructions per 32 weights per SMSP, 1 issue/clk"},
                          "isolated_launch_ms_per_step": sum_kern,
                          "hbm_frac": sketch_bytes / (ms_per_step * 1e-3) / 1e9 / peaks["hbm_gbs"]},
             "e2e": {"value": 1000.0 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": int(Xh.numel() * 2),
@@ -725,6 +741,8 @@ def run_usk(args):
             line["output_row_units"] = orow
         if p67 is not None:
             line["paper_six_of_seven"] = p67
+        if um is not None:
+            line["unit_major_usk_x"] = um
         if c5 is not None:
             line["llama3_8b_n1"] = c5
         if c4 is not None:
@@ -819,6 +837,8 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=None, help="--impl reference: oracle seconds per step")
     ap.add_argument("--no-q4", action="store_true", help="skip the extra plans (q4 states, classes, output-row units)")
+    ap.add_argument("--layout", default="query", choices=["query", "unit_major"],
+                    help="headline plan: query layout + USK-XG keys (default) or the unit-major USK-X plan")
     ap.add_argument("--no-8b", action="store_true", help="skip the Llama-3-8B (config 5) build + decode at N=1")
     ap.add_argument("--no-prefill", action="store_true", help="skip the config-4 prefill passes")
     ap.add_argument("--prefetch-next", action="store_true",

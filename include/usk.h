@@ -21,7 +21,7 @@
  *     (order independence); usk_linear is deterministic for fixed inputs.
  *
  * Citations: PAPER.md:<line> (section / equation).  Readings where the paper is silent are
- * listed in DESIGN.md ("ledger" L1..L31) and referenced below.
+ * listed in DESIGN.md ("ledger" L1..L32) and referenced below.
  */
 #ifndef USK_H
 #define USK_H
@@ -73,7 +73,29 @@ typedef enum { USK_GRAN_ROW = 0, USK_GRAN_LAYER = 1, USK_GRAN_OUTROW = 2 } usk_g
  * reduced to [0, N_u) by the top 23 bits times N_u (short units, N_u <= 2^16; exact as one fp32
  * FMA.RZ on the device) or a 32-bit multiply-high (long units); USK_HASH_IDENTITY = p mod N
  * (tests only). */
-typedef enum { USK_HASH_X = 0, USK_HASH_IDENTITY = 1 } usk_hash;
+typedef enum { USK_HASH_X = 0, USK_HASH_IDENTITY = 1, USK_HASH_XG = 2 } usk_hash;
+/* USK_HASH_XG (DESIGN.md ledger L32): USK-X with the unit key of the KEY GROUP floor(t / 8) -- the
+ * 8 consecutive units t = 8g .. 8g+7 of a layer share the M functions H_i of PAPER.md:239-243
+ * ("I = H(Addr(w))", one set of independent H_0..H_{M-1} of the weight's bias), groups use
+ * independent ones.  Required by the query layout below. */
+
+/* Sketch storage layout.
+ * USK_LAYOUT_UNIT_MAJOR (default): the cells of unit u at [offsets[u], offsets[u+1]) in the state
+ *   dtype, row-major (i, c) inside the unit (usk_plan_export).
+ * USK_LAYOUT_QUERY (round 2; bf16 states, ROW units with dims_per_unit 1, USK_HASH_XG, AbsMaxMin,
+ *   raw states, no Top-K, in_features % 8 == 0, every key group of 8 units with one N): the same
+ *   cells, permuted and re-encoded for the decode so that one 16-byte shared load gathers a key
+ *   group's 8 cells of a sketch row (DESIGN.md §4 / §5 K4p).  Each layer occupies
+ *   [qbyte_begin, qbyte_begin + qbytes) (usk_layer_info); its units form chunks of 256 (32 key
+ *   groups; the last chunk of a layer may be partial).  Chunk k of the layer has maxN_k = the
+ *   largest N_u of its units and takes rows * maxN_k * 512 bytes (rows = usk_plan_info.rows),
+ *   chunks back to back from qbyte_begin.  Inside chunk k, the 16-bit word at byte
+ *       ((i * maxN_k + c) * 32 + g) * 16 + 2 * v
+ *   holds cell (i, c) of unit 256 k + 8 g + v of the layer as the retrieve key
+ *       rho16 = ((b << 1) | (b >> 15)) ^ 1  (b = the bf16 bits of the state; mag << 1 | 1 - sign),
+ *   and 0 where the unit does not exist, c >= N_u or i >= M_u (0 is below every key: neutral for
+ *   the Eq. 5 max).  The encoding is a bijection of the unit-major cells (same bits per weight). */
+typedef enum { USK_LAYOUT_UNIT_MAJOR = 0, USK_LAYOUT_QUERY = 1 } usk_layout;
 
 /* Sketch variant (Appendix C.2): USK_ABSMAXMIN = the paper's sketch (keep the
  * min |.|, retrieve the max |.|); USK_ABSMINMAX = the order of min and max swapped (cells start at
@@ -126,6 +148,12 @@ typedef struct {
                             x_c = T W_c / (W n_c class_rows[c]).  Unit u has M_u = class_rows[cls_u]
                             rows (usk_plan_export nrows); usk_plan_info.rows = max_c class_rows[c].
                             AbsMaxMin only; not with layer_importance. */
+  int32_t layout;        /* usk_layout of the sketch buffer (USK_LAYOUT_UNIT_MAJOR = 0 by default).
+                            USK_LAYOUT_QUERY: usk_build writes the query layout, usk_reconstruct /
+                            usk_linear / usk_linear_batch / usk_prefetch_l2 read it; usk_stats,
+                            usk_aggregate_grad and usk_build_rows return USK_EUNSUPPORTED.  A plan
+                            that does not meet the layout's conditions fails with USK_EUNSUPPORTED. */
+  int32_t reserved;
 } usk_params;
 
 typedef struct usk_plan usk_plan;
@@ -149,6 +177,8 @@ typedef struct {
   int64_t scales_offset;  /* quantised plans: byte offset of the fp32 scales in the sketch buffer;
                              the codes (packed, cell c at bit c*state_bits) start at byte 0 */
   int64_t topk;           /* Top-K outliers per layer (0 = none) */
+  int32_t layout;         /* usk_layout of the sketch buffer */
+  int32_t hash;           /* usk_hash */
 } usk_plan_info;
 
 typedef struct {
@@ -166,6 +196,8 @@ typedef struct {
   int64_t outlier_offset; /* Top-K: byte offset in the sketch of the layer's side table: n_outliers
                              int32 flat indices (ascending), then at the next 16-B boundary their
                              states in the plan dtype */
+  int64_t qbyte_begin;    /* USK_LAYOUT_QUERY: byte offset of the layer's region in the sketch */
+  int64_t qbytes;         /*   and its size (0 for the unit-major layout) */
 } usk_layer_info;
 
 /* Importance metric, Eq. 7: I[j] = (1/N) sum_k A[k, j]^2.

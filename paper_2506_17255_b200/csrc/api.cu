@@ -119,7 +119,7 @@ static bool layer_cells(int L, const double* imp, const std::vector<int64_t>& nu
 
 static void free_plan(usk_plan* p) {
   if (!p) return;
-  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R4, p->d_err};
+  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R4, p->d_err, p->d_qc_off, p->d_qc_N};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete p;
@@ -173,7 +173,17 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
     return fail(USK_EINVAL, "granularity");
   if (P.granularity == USK_GRAN_OUTROW && (P.n_classes > 1 || P.dims_per_unit != 1))
     return fail(USK_EINVAL, "OUTROW units form one class (n_classes 0 or 1) with dims_per_unit 1");
-  if (P.hash != USK_HASH_X && P.hash != USK_HASH_IDENTITY) return fail(USK_EINVAL, "hash");
+  if (P.hash != USK_HASH_X && P.hash != USK_HASH_IDENTITY && P.hash != USK_HASH_XG) return fail(USK_EINVAL, "hash");
+  if (P.layout != USK_LAYOUT_UNIT_MAJOR && P.layout != USK_LAYOUT_QUERY) return fail(USK_EINVAL, "layout");
+  if (P.layout == USK_LAYOUT_QUERY) {  // usk.h: the query layout's conditions (L32, §4)
+    if (P.hash != USK_HASH_XG) return fail(USK_EUNSUPPORTED, "query layout: needs USK_HASH_XG (key groups of 8 units)");
+    if (P.granularity != USK_GRAN_ROW || P.dims_per_unit != 1)
+      return fail(USK_EUNSUPPORTED, "query layout: ROW units with dims_per_unit 1 only");
+    if (P.dtype != USK_BF16 || P.state_bits || P.variant != USK_ABSMAXMIN || P.topk)
+      return fail(USK_EUNSUPPORTED, "query layout: raw bf16 states, AbsMaxMin, no Top-K");
+    for (int l = 0; l < n_layers; ++l)
+      if (layers[l].in_features % 8 != 0) return fail(USK_EUNSUPPORTED, "query layout: in_features % 8 != 0");
+  }
   if (P.dtype != USK_F32 && P.dtype != USK_BF16) return fail(USK_EINVAL, "dtype");
   if (P.min_cols < 1) return fail(USK_EINVAL, "min_cols must be >= 1");
   if (P.n_classes < 0 || P.n_classes > 64) return fail(USK_EINVAL, "n_classes must be in [0, 64]");
@@ -224,7 +234,9 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
   pl->g = g;
   pl->C = n_cls;
   pl->min_cols = P.min_cols;
-  pl->hash = P.hash;
+  pl->hash = P.hash == USK_HASH_XG ? USK_HASH_X : P.hash;  // same kernels; grouped keys in d_keys
+  pl->hash_api = P.hash;
+  pl->layout = P.layout;
   pl->variant = P.variant;
   pl->topk = P.topk;
   pl->dtype = P.dtype;
@@ -367,6 +379,13 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
                             : L.n_cells * state_bits + L.meta_bits + L.n_out * (32 + state_bits);
     pl->achieved_bits += L.achieved_bits;
   }
+  if (pl->layout == USK_LAYOUT_QUERY) {
+    s = qlayout_geometry(pl);
+    if (s != USK_OK) {
+      free_plan(pl);
+      return s;
+    }
+  }
   *plan_out = pl;
   return USK_OK;
 }
@@ -382,6 +401,9 @@ usk_status usk_plan_query(const usk_plan* pl, usk_plan_info* out) {
   const int64_t bytes = pl->q ? pl->scales_off + pl->n_groups * 4
                               : (pl->total_cells * pl->cell_bytes() + 255) / 256 * 256 + pl->side_bytes;
   out->sketch_bytes = ((bytes + 255) / 256) * 256 + 256;
+  if (pl->layout == USK_LAYOUT_QUERY) out->sketch_bytes = (pl->qtotal + 255) / 256 * 256 + 256;
+  out->layout = pl->layout;
+  out->hash = pl->hash_api;
   out->state_bits = pl->q;
   out->group_size = pl->q ? pl->G : 0;
   out->n_groups = pl->n_groups;
@@ -398,7 +420,8 @@ usk_status usk_plan_layer(const usk_plan* pl, int32_t layer, usk_layer_info* out
   if (layer < 0 || layer >= pl->n_layers) return fail(USK_ESHAPE, "usk_plan_layer: layer out of range");
   const LayerGeom& L = pl->layers[layer];
   *out = usk_layer_info{L.out,         L.in,        L.unit_begin, L.n_units,       L.cell_begin, L.n_cells,
-                        L.budget_bits, L.meta_bits, L.cells_T,    L.achieved_bits, L.n_out,      L.out_off};
+                        L.budget_bits, L.meta_bits, L.cells_T,    L.achieved_bits, L.n_out,      L.out_off,
+                        L.qoff,        L.qbytes};
   return USK_OK;
 }
 
@@ -422,6 +445,7 @@ usk_status usk_build_rows(const usk_plan* pl, int32_t layer, int64_t row_begin, 
   if (!pl || !weight_rows || !sketch) return fail(USK_EINVAL, "usk_build_rows: null pointer");
   if (!aligned16(sketch) || !aligned16(weight_rows)) return fail(USK_EINVAL, "usk_build_rows: 16-B alignment");
   if (pl->gran != USK_GRAN_OUTROW || pl->q) return fail(USK_EINVAL, "usk_build_rows: OUTROW plans with raw states");
+  if (pl->layout != USK_LAYOUT_UNIT_MAJOR) return fail(USK_EUNSUPPORTED, "usk_build_rows: unit-major layout only");
   if (layer < 0 || layer >= pl->n_layers) return fail(USK_ESHAPE, "usk_build_rows: layer out of range");
   if (row_begin < 0 || row_end > pl->layers[layer].out || row_begin > row_end)
     return fail(USK_ESHAPE, "usk_build_rows: row range outside [0, out)");
@@ -443,6 +467,7 @@ usk_status usk_build(const usk_plan* pl, const void* const* weights, const int32
     if (!weights[k]) return fail(USK_EINVAL, "usk_build: null weight pointer");
     if (!aligned16(weights[k])) return fail(USK_EINVAL, "usk_build: weights must be 16-B aligned");
   }
+  if (pl->layout == USK_LAYOUT_QUERY) return launch_qbuild(pl, weights, layer_ids, n, sketch, (cudaStream_t)stream);
   return launch_build(pl, weights, layer_ids, n, sketch, (cudaStream_t)stream);
 }
 
@@ -454,6 +479,8 @@ usk_status usk_reconstruct(const usk_plan* pl, const void* sketch, int32_t layer
   if (row_begin < 0 || row_end > L.out || row_begin > row_end)
     return fail(USK_ESHAPE, "usk_reconstruct: row range outside [0, out_features)");
   if (ld_out < L.in) return fail(USK_ESHAPE, "usk_reconstruct: ld_out < in_features");
+  if (pl->layout == USK_LAYOUT_QUERY)
+    return launch_qreconstruct(pl, sketch, layer, row_begin, row_end, w_out, ld_out, (cudaStream_t)stream);
   return launch_reconstruct(pl, sketch, layer, row_begin, row_end, w_out, ld_out, (cudaStream_t)stream);
 }
 
@@ -471,7 +498,8 @@ size_t usk_linear_workspace_bytes(const usk_plan* pl, int32_t layer, int64_t T, 
   const LayerGeom& L = pl->layers[layer];
   if (out_begin < 0 || out_end > L.out || out_begin > out_end) return 0;
   if (T == 1) {
-    size_t b = gemv_workspace_bytes(pl, layer, out_begin, out_end);
+    size_t b = pl->layout == USK_LAYOUT_QUERY ? qgemv_batch_workspace_bytes(pl, &layer, &out_begin, &out_end, 1)
+                                              : gemv_workspace_bytes(pl, layer, out_begin, out_end);
     return b ? b : 256;
   }
   return (size_t)((out_end - out_begin) * L.in * 2 + 255) / 256 * 256;
@@ -492,15 +520,20 @@ usk_status usk_linear(const usk_plan* pl, const void* sketch, int32_t layer, con
   const size_t need = usk_linear_workspace_bytes(pl, layer, T, out_begin, out_end);
   if (workspace_bytes < need || (need && !workspace)) return fail(USK_ESHAPE, "usk_linear: workspace too small");
   cudaStream_t st = (cudaStream_t)stream;
-  if (T == 1)
+  if (T == 1) {
+    if (pl->layout == USK_LAYOUT_QUERY)
+      return launch_qgemv_batch(pl, sketch, &layer, &out_begin, &out_end, 1, x, x_dtype, &y, y_dtype, workspace, st);
     return launch_gemv(pl, sketch, layer, x, x_dtype, y, y_dtype, out_begin, out_end, workspace, workspace_bytes, st);
+  }
   if (pl->dtype != USK_BF16 || x_dtype != USK_BF16)
     return fail(USK_EUNSUPPORTED, "usk_linear: T > 1 needs bf16 weights and bf16 x (tcgen05 kind::f16)");
   const int64_t rows = out_end - out_begin;
   if (rows == 0) return USK_OK;
   if (!aligned16(workspace)) return fail(USK_EINVAL, "usk_linear: workspace alignment");
   // the paper's decompression: rebuild the output-row slice of W' ...
-  usk_status s = launch_reconstruct(pl, sketch, layer, out_begin, out_end, workspace, L.in, st);
+  usk_status s = pl->layout == USK_LAYOUT_QUERY
+                     ? launch_qreconstruct(pl, sketch, layer, out_begin, out_end, workspace, L.in, st)
+                     : launch_reconstruct(pl, sketch, layer, out_begin, out_end, workspace, L.in, st);
   if (s != USK_OK) return s;
   // ... then the computation stage on the tensor cores
   return launch_gemm_bf16(x, workspace, y, y_dtype, T, rows, L.in, L.in, st);
@@ -527,6 +560,7 @@ static usk_status batch_ranges(const usk_plan* pl, const int32_t* layers, const 
 size_t usk_linear_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* ranges, int32_t n) {
   std::vector<int64_t> o0, o1;
   if (batch_ranges(pl, layers, ranges, n, o0, o1) != USK_OK) return 0;
+  if (pl->layout == USK_LAYOUT_QUERY) return qgemv_batch_workspace_bytes(pl, layers, o0.data(), o1.data(), n);
   return gemv_batch_workspace_bytes(pl, layers, o0.data(), o1.data(), n);
 }
 
@@ -543,6 +577,12 @@ usk_status usk_linear_batch(const usk_plan* pl, const void* sketch, const int32_
     return fail(USK_EINVAL, "usk_linear_batch: 16-B alignment");
   for (int k = 0; k < n; ++k)
     if (!y[k] || !aligned16(y[k])) return fail(USK_EINVAL, "usk_linear_batch: y pointer");
+  if (pl->layout == USK_LAYOUT_QUERY) {
+    if (workspace_bytes < qgemv_batch_workspace_bytes(pl, layers, o0.data(), o1.data(), n))
+      return fail(USK_ESHAPE, "usk_linear_batch: workspace too small");
+    return launch_qgemv_batch(pl, sketch, layers, o0.data(), o1.data(), n, x, x_dtype, y, y_dtype, workspace,
+                              (cudaStream_t)stream);
+  }
   if (workspace_bytes < gemv_batch_workspace_bytes(pl, layers, o0.data(), o1.data(), n))
     return fail(USK_ESHAPE, "usk_linear_batch: workspace too small");
   return launch_gemv_batch(pl, sketch, layers, o0.data(), o1.data(), n, x, x_dtype, y, y_dtype, workspace,

@@ -141,7 +141,15 @@ struct LayerGeom {
   int32_t scope;      // budget scope id
   int64_t n_out = 0;  // Top-K outliers of the layer (L29)
   int64_t out_off = 0;  // byte offset of the layer's side table in the sketch (indices, then states)
+  // query layout (usk.h USK_LAYOUT_QUERY): byte region of the layer, its first global chunk, chunks
+  int64_t qoff = 0, qbytes = 0, qchunk0 = 0;
+  int32_t qchunks = 0;
 };
+
+constexpr int kQGroup = 8;           // units per key group (USK-XG, ledger L32) = cells per 16-B load
+constexpr int kQChunkGroups = 32;    // key groups per query-layout chunk (one per lane)
+constexpr int kQChunkUnits = kQGroup * kQChunkGroups;
+constexpr int kQSlice = kQChunkGroups * 16;  // bytes of one (sketch row, column) slice of a chunk
 
 }  // namespace usk
 
@@ -174,6 +182,14 @@ struct usk_plan {
   int64_t side_bytes = 0;     // bytes of all outlier side tables (after the cells)
   int64_t n_groups = 0;       // total_cells / G (quantised)
   int64_t scales_off = 0;     // byte offset of the fp32 group scales in the sketch (quantised)
+  int32_t hash_api = 0;       // usk_hash as given; `hash` is the kernel family (USK-XG runs as USK-X: its
+                              // grouped unit keys live in d_keys)
+  int32_t layout = 0;         // usk_layout
+  int64_t qtotal = 0;         // query layout: bytes of all layer regions
+  std::vector<int64_t> h_qc_off;  // query layout: absolute byte offset of every chunk, [chunks + 1]
+  std::vector<int32_t> h_qc_N;    //   and its maxN
+  int64_t* d_qc_off = nullptr;
+  int32_t* d_qc_N = nullptr;
   int cell_bytes() const { return dtype == USK_BF16 ? 2 : 4; }  // raw state bytes
   int64_t code_bytes() const { return (total_cells * q + 7) / 8; }
 };
@@ -205,6 +221,17 @@ usk_status launch_fixed_accumulate(const usk_plan* pl, int32_t l, const void* va
                                    unsigned long long* acc, int* err, cudaStream_t st);
 bool layer_fast_ok(const usk_plan* pl, int32_t layer);
 bool outrow_fast_ok(const usk_plan* pl, const int32_t* layers, int n);
+// query layout (packed.cu)
+usk_status qlayout_geometry(usk_plan* pl);
+usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
+                         void* sketch, cudaStream_t st);
+usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t layer, int64_t r0, int64_t r1,
+                               void* w_out, int64_t ld, cudaStream_t st);
+size_t qgemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* o0, const int64_t* o1,
+                                   int n);
+usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
+                              const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
+                              void* ws, cudaStream_t st);
 usk_status launch_gemv_outrow(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
                               const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
                               cudaStream_t st);

@@ -1,0 +1,852 @@
+// packed.cu -- the query layout (usk.h USK_LAYOUT_QUERY; DESIGN.md §4, §5 "K4p", ledger L32).
+//
+// Query of one weight (Eq. 3 + Eq. 5; §3.1 decompress -> compute):
+//   w'(o, j) = the bonded cell of maximum |.| over the M sketch rows (ties -> non-negative, L1/L2).
+// Under USK-XG the 8 units (input dims) of a key group share the hash functions H_i (ledger L32), so
+// for an output row o they read the SAME column idx_i(o) of their own cells.  The query layout puts
+// those 8 cells side by side as 16-bit retrieve keys rho16 = rotl16(b, 1) ^ 1 (b = bf16 bits):
+//
+//   chunk = 256 units = 32 key groups (one per lane); slice (i, c) of a chunk = 32 x 16 B
+//   byte ((i * maxN + c) * 32 + g) * 16 + 2 v  <-  cell (i, c) of unit 256 k + 8 g + v
+//
+// so a warp's gather of sketch row i for one output row is ONE ld.shared.v4 per lane (8 cells, four
+// conflict-free 128-B wavefronts) instead of 8 scalar loads, the Eq. 5 max of two units is one
+// VIMNMX3.U16x2 over the M = 3 rows, and the chunk is staged with one TMA bulk copy (no shared ->
+// shared conversion: the layout IS the shared-memory layout).  The shared address of column idx is
+// one FFMA.RZ with the result at ulp 512 (tests/test_oracle_hash.py::test_packed_float_form):
+//   RZ(f * 512 N + (2^32 + B - 512 N)) = 2^32 + B + 512 idx,  f = 1 + (h mod 2^23) / 2^23
+// and bits * 512 mod 2^32 = B + 512 idx: one IMAD adds the lane's 16 B.
+//
+// Kernels: k_qpack (unit-major cells -> query layout, build time), k_qgemv (decode, split-K over
+// chunks, partials [rows][CP]) + k_qreduce (fixed-order sum, PDL-chained), k_qrecon (W' rows).
+#include <algorithm>
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+#include <tuple>
+#include <vector>
+
+#include "common.cuh"
+#include "ptx.cuh"
+
+namespace usk {
+namespace {
+
+constexpr int kPThreads = 512;
+constexpr int kPWarps = kPThreads / 32;
+constexpr int kPSub = 16;          // output rows per warp work item (subtile)
+constexpr int kPMaxLayers = 8;
+constexpr int kPMaxCtas = 256;
+constexpr int kPMaxM = 4;          // sketch rows of the query-layout kernels
+constexpr int kPRedThreads = 256;
+constexpr int kPHdr = 64;          // [2 mbarriers][s_next][pad]
+constexpr int kPRtab = kPWarps * kPSub * 16;  // per warp: 16 rows x {R_0..R_3}
+constexpr int kPTS = 8;            // USK_TRACE stamps per CTA
+
+extern __shared__ __align__(16) unsigned char psm[];
+
+struct PLayer {
+  int64_t unit_base;   // global unit id of the layer's unit 0
+  int64_t chunk0;      // global index of the layer's chunk 0 (d_qc_off / d_qc_N)
+  int64_t o_begin;     // first output row of the launch range
+  int64_t rows;
+  int64_t item_begin;  // first work item (chunk-major, subtile-minor)
+  int64_t row_begin;   // first row in the launch's reduction order
+  int32_t n_chunks, n_sub, CP, pad;
+  void* y;
+  float* partial;      // [rows][CP]
+  void* w_out;         // reconstruct
+  int64_t ld_out;
+};
+
+struct PArgs {
+  PLayer layer[kPMaxLayers];
+  int32_t n_layers;
+  int32_t nslot;        // staging slots (2: the next segment's bulk copy under this one's math)
+  uint32_t slot_bytes;  // bytes per slot (max chunk bytes of the launch, 1024-aligned)
+  int32_t y_bf16;
+  int64_t in, items, rows;
+  const unsigned char* sketch;
+  const int64_t* qc_off;  // absolute byte offset of every chunk, [chunks + 1]
+  const int32_t* qc_N;    // maxN of every chunk
+  const int32_t* ncols;
+  const uint32_t* ukeys;
+  HashConsts hc;
+  const void* x;
+  int32_t red_lanes;
+  int32_t st_aligned;   // reconstruct: ld and w_out allow 16-B row stores
+  int32_t cta_item[kPMaxCtas + 1];
+  uint64_t first_off[kPMaxCtas];   // CTA c's first bulk copy (host-computed: no dependent load)
+  uint32_t first_bytes[kPMaxCtas];
+  unsigned long long* timeline;    // tuning only (USK_TRACE)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+__device__ __forceinline__ uint4 lds128(uint32_t a) {
+  uint4 q;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(a));
+  return q;
+}
+__device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.u16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+// rotr16 of both halves of a pair of retrieve keys: the bf16 bits of -w' in each half
+__device__ __forceinline__ uint32_t neg_w(uint32_t p) {
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, 0x7FFF7FFF, 0xE4;" : "=r"(d) : "r"(p >> 1), "r"(p << 15));
+  return d;
+}
+// c + bf16 half of x * bf16 half of w (one FHFMA.BF16: exact product, one rounding)
+__device__ __forceinline__ float fma_lo(uint32_t x, uint32_t w, float c) {
+  float d;
+  asm("{.reg .b16 wl, wh, xl, xh;\n\tmov.b32 {wl, wh}, %2;\n\tmov.b32 {xl, xh}, %1;\n\tfma.rn.f32.bf16 %0, xl, wl, %3;}"
+      : "=f"(d) : "r"(x), "r"(w), "f"(c));
+  return d;
+}
+__device__ __forceinline__ float fma_hi(uint32_t x, uint32_t w, float c) {
+  float d;
+  asm("{.reg .b16 wl, wh, xl, xh;\n\tmov.b32 {wl, wh}, %2;\n\tmov.b32 {xl, xh}, %1;\n\tfma.rn.f32.bf16 %0, xh, wh, %3;}"
+      : "=f"(d) : "r"(x), "r"(w), "f"(c));
+  return d;
+}
+
+// Row sums of a 16-row subtile: acc[r] = this lane's partial of row r; the same fixed tree as the
+// unit-major kernels (lane bits 3, 2, 1, 0, then 4), so a row's bits depend on nothing but its
+// chunk partials.  Lane r < 16 returns row r's sum.
+__device__ __forceinline__ float transpose_reduce16(float (&acc)[kPSub], int lane) {
+#pragma unroll
+  for (int m = kPSub / 2; m >= 1; m >>= 1) {
+    const bool up = (lane & m) != 0;
+#pragma unroll
+    for (int i = 0; i < m; ++i) {
+      const float send = up ? acc[i] : acc[i + m];
+      const float keep = up ? acc[i + m] : acc[i];
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+    }
+  }
+  float t = acc[0];
+  t += __shfl_xor_sync(0xffffffffu, t, 16);
+  return t;
+}
+
+__device__ __forceinline__ uint64_t* p_bar(int s) { return reinterpret_cast<uint64_t*>(psm) + s; }
+__device__ __forceinline__ int* p_next() { return reinterpret_cast<int*>(psm + 16); }
+__device__ __forceinline__ uint32_t p_rtab() { return smem_u32(psm + kPHdr); }
+// slots start 1024-B aligned (the ulp-512 address form needs B % 512 == 0)
+__device__ __forceinline__ uint32_t p_slot(const PArgs& A, int s) {
+  const uint32_t a = smem_u32(psm + kPHdr + kPRtab);
+  return ((a + 1023u) & ~1023u) + (uint32_t)s * A.slot_bytes;
+}
+__device__ __forceinline__ void p_issue(const PArgs& A, int slot, uint64_t off, uint32_t bytes) {
+  fence_proxy_async_smem();  // earlier generic reads of the slot happen before the async-proxy write
+  mbar_arrive_expect_tx(p_bar(slot), bytes);
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   p_slot(A, slot)),
+               "l"(A.sketch + off), "r"(bytes), "r"(smem_u32(p_bar(slot)))
+               : "memory");
+}
+
+struct PSeg {
+  int li, chunk, sub_a, sub_end;
+  int64_t end;
+};
+
+__device__ __forceinline__ PSeg p_seg_at(const PArgs& A, int64_t s, int64_t s_end) {
+  PSeg g;
+  g.li = 0;
+  while (g.li + 1 < A.n_layers && A.layer[g.li + 1].item_begin <= s) ++g.li;
+  const PLayer& L = A.layer[g.li];
+  const int64_t local = s - L.item_begin;
+  g.chunk = (int)(local / L.n_sub);
+  g.sub_a = (int)(local - (int64_t)g.chunk * L.n_sub);
+  g.end = min(s_end, L.item_begin + (int64_t)(g.chunk + 1) * L.n_sub);
+  g.sub_end = g.sub_a + (int)(g.end - s);
+  return g;
+}
+
+// Per-warp table of the subtile rows' position mixes R_i(o) mod 2^23 (rows past the range repeat
+// the last row): lane r < 16 writes row r's {R_0..R_3}.
+template <int MT>
+__device__ __forceinline__ void p_fill_rtab(const PArgs& A, uint32_t rtab, int64_t o_first, int64_t o_last, int lane) {
+  __syncwarp();
+  if (lane < kPSub) {
+    const uint32_t o = (uint32_t)min(o_first + lane, o_last);
+    uint32_t r[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int i = 0; i < MT; ++i) r[i] = fmix32(o ^ A.hc.rho[i]) & 0x7FFFFFu;
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(rtab + 16u * lane), "r"(r[0]), "r"(r[1]), "r"(r[2]),
+                 "r"(r[3])
+                 : "memory");
+  }
+  __syncwarp();
+}
+
+// K4p / K3p: one CTA per SM computes the host-balanced contiguous item range [cta_item[c],
+// cta_item[c+1]) of (layer, chunk, 16-row subtile) items; warps grab the subtiles of a staged chunk.
+// GEMV: chunk partials of every row -> [rows][CP].  !GEMV: W' rows (bf16) -> w_out.
+template <int MT, bool GEMV, bool XB>
+__device__ __forceinline__ void p_query(const PArgs& A) {
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x;
+  const int64_t s_begin = A.cta_item[c], s_end = A.cta_item[c + 1];
+  unsigned long long* const tl = A.timeline ? A.timeline + (int64_t)c * kPTS : nullptr;
+  if (tl && threadIdx.x == 0) tl[0] = gtimer();
+  if (threadIdx.x == 0) {
+    mbar_init(p_bar(0), 1);
+    mbar_init(p_bar(1), 1);
+    fence_mbar_init();
+    if (s_begin < s_end) p_issue(A, 0, A.first_off[c], A.first_bytes[c]);  // before anything else
+    if (tl) tl[4] = gtimer();
+  }
+  bool waited = false;
+  if (s_begin < s_end) {
+    PSeg cur = p_seg_at(A, s_begin, s_end);
+    if (threadIdx.x == 0) *p_next() = cur.sub_a;
+    __syncthreads();  // mbarrier init + s_next visible
+    uint32_t phase[2] = {0u, 0u};
+    const uint32_t rtab = p_rtab() + (uint32_t)(threadIdx.x >> 5) * (kPSub * 16u);
+    for (int k = 0;; ++k) {
+      const int slot = A.nslot == 2 ? (k & 1) : 0;
+      const PLayer& Ly = A.layer[cur.li];
+      const bool more = cur.end < s_end;
+      PSeg nxt = cur;
+      if (more) nxt = p_seg_at(A, cur.end, s_end);
+      // the other slot is free (its segment ended with a CTA barrier): next chunk's copy now
+      if (A.nslot == 2 && more && threadIdx.x == 0) {
+        const int64_t g = A.layer[nxt.li].chunk0 + nxt.chunk;
+        const int64_t o0 = A.qc_off[g];
+        p_issue(A, slot ^ 1, (uint64_t)o0, (uint32_t)(A.qc_off[g + 1] - o0));
+      }
+      // lane state: key group g = lane of this chunk (the 8 units share K and N, ledger L32)
+      const int64_t gcol = (int64_t)cur.chunk * kQChunkGroups + lane;
+      const bool valid = gcol * kQGroup < A.in;
+      const int64_t u0 = Ly.unit_base + gcol * kQGroup;
+      const uint32_t N = valid ? (uint32_t)A.ncols[u0] : 1u;
+      const uint32_t K = valid ? A.ukeys[u0] : 0u;
+      const uint32_t maxN = (uint32_t)A.qc_N[Ly.chunk0 + cur.chunk];
+      const uint32_t B0 = p_slot(A, slot);
+      uint32_t fk[MT], cb[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        fk[i] = 0x3F800000u | (fmix32(K ^ A.hc.kap[i]) & 0x7FFFFFu);
+        // 2^32 + B_i - 512 N (a multiple of 512 in [2^31, 2^33): an fp32 number)
+        cb[i] = __float_as_uint(__ull2float_rz(4294967296ull + B0 + (unsigned long long)i * maxN * kQSlice -
+                                               (unsigned long long)kQSlice * N));
+      }
+      const float NS = (float)(kQSlice * N);
+      const uint32_t LB = 16u * (uint32_t)lane;
+      mbar_wait(p_bar(slot), phase[slot]);
+      phase[slot] ^= 1u;
+      if (!waited) {
+        if (tl && threadIdx.x == 0) tl[5] = gtimer();
+        if (GEMV) pdl_wait();  // x may be written by the previous kernel on the stream
+        else pdl_wait();       // w_out may be read by the previous kernel
+        pdl_trigger();
+        if (tl && threadIdx.x == 0) tl[7] = gtimer();
+        waited = true;
+      }
+      // -x of the group's 8 inputs (bf16 pairs: sign bits flipped; fp32: negated)
+      uint32_t nxb[4] = {0u, 0u, 0u, 0u};
+      float nxf[8];
+#pragma unroll
+      for (int v = 0; v < 8; ++v) nxf[v] = 0.f;
+      if (GEMV && valid) {
+        const int64_t j0 = gcol * kQGroup;
+        if constexpr (XB) {
+          const uint4 xv = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A.x) + j0);
+          nxb[0] = xv.x ^ 0x80008000u;
+          nxb[1] = xv.y ^ 0x80008000u;
+          nxb[2] = xv.z ^ 0x80008000u;
+          nxb[3] = xv.w ^ 0x80008000u;
+        } else {
+          const float4 a = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A.x) + j0);
+          const float4 b = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A.x) + j0 + 4);
+          nxf[0] = -a.x, nxf[1] = -a.y, nxf[2] = -a.z, nxf[3] = -a.w;
+          nxf[4] = -b.x, nxf[5] = -b.y, nxf[6] = -b.z, nxf[7] = -b.w;
+        }
+      }
+      if (tl && threadIdx.x == 0 && k == 0) tl[1] = gtimer();
+      auto grab = [&]() -> int {
+        int g = 0;
+        if (lane == 0) g = atomicAdd(p_next(), 1);
+        return __shfl_sync(0xffffffffu, g, 0);
+      };
+      int sub = grab();
+      if (sub < cur.sub_end) p_fill_rtab<MT>(A, rtab, Ly.o_begin + (int64_t)sub * kPSub, Ly.o_begin + Ly.rows - 1, lane);
+      while (sub < cur.sub_end) {
+        const int nsub = grab();  // issued now, consumed after this subtile
+        const int64_t r0 = (int64_t)sub * kPSub;
+        const int nrow = (int)min((int64_t)kPSub, Ly.rows - r0);
+        if constexpr (GEMV) {
+          float acc[kPSub];
+#pragma unroll
+          for (int r = 0; r < kPSub; ++r) {
+            const uint4 R = lds128(rtab + 16u * r);
+            const uint32_t Rv[4] = {R.x, R.y, R.z, R.w};
+            uint4 cl[MT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+              const uint32_t bits =
+                  __float_as_uint(__fmaf_rz(__uint_as_float(Rv[i] ^ fk[i]), NS, __uint_as_float(cb[i])));
+              cl[i] = lds128(bits * (uint32_t)kQSlice + LB);
+            }
+            uint4 m = cl[0];
+#pragma unroll
+            for (int i = 1; i < MT; ++i) {
+              m.x = max_u16x2(m.x, cl[i].x);
+              m.y = max_u16x2(m.y, cl[i].y);
+              m.z = max_u16x2(m.z, cl[i].z);
+              m.w = max_u16x2(m.w, cl[i].w);
+            }
+            const uint32_t wp[4] = {neg_w(m.x), neg_w(m.y), neg_w(m.z), neg_w(m.w)};
+            float a = 0.f;  // units 8g + 0 .. 7 in order
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+              if constexpr (XB) {
+                a = fma_lo(nxb[p], wp[p], a);
+                a = fma_hi(nxb[p], wp[p], a);
+              } else {
+                a = fmaf(nxf[2 * p], __uint_as_float(wp[p] << 16), a);
+                a = fmaf(nxf[2 * p + 1], __uint_as_float(wp[p] & 0xFFFF0000u), a);
+              }
+            }
+            acc[r] = a;
+          }
+          const float t = transpose_reduce16(acc, lane);
+          if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + cur.chunk] = t;
+        } else {
+          uint16_t* dst = reinterpret_cast<uint16_t*>(Ly.w_out) + r0 * Ly.ld_out + gcol * kQGroup;
+#pragma unroll 4
+          for (int r = 0; r < kPSub; ++r, dst += Ly.ld_out) {
+            if (r >= nrow) break;
+            const uint4 R = lds128(rtab + 16u * r);
+            const uint32_t Rv[4] = {R.x, R.y, R.z, R.w};
+            uint4 cl[MT];
+#pragma unroll
+            for (int i = 0; i < MT; ++i) {
+              const uint32_t bits =
+                  __float_as_uint(__fmaf_rz(__uint_as_float(Rv[i] ^ fk[i]), NS, __uint_as_float(cb[i])));
+              cl[i] = lds128(bits * (uint32_t)kQSlice + LB);
+            }
+            uint4 m = cl[0];
+#pragma unroll
+            for (int i = 1; i < MT; ++i) {
+              m.x = max_u16x2(m.x, cl[i].x);
+              m.y = max_u16x2(m.y, cl[i].y);
+              m.z = max_u16x2(m.z, cl[i].z);
+              m.w = max_u16x2(m.w, cl[i].w);
+            }
+            // bits of w' = rotr16(rho) with the sign flipped back
+            const uint4 w = make_uint4(neg_w(m.x) ^ 0x80008000u, neg_w(m.y) ^ 0x80008000u, neg_w(m.z) ^ 0x80008000u,
+                                       neg_w(m.w) ^ 0x80008000u);
+            if (valid) {
+              if (A.st_aligned) {
+                *reinterpret_cast<uint4*>(dst) = w;
+              } else {
+                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+                for (int v = 0; v < 8; ++v) dst[v] = (uint16_t)(ww[v >> 1] >> (16 * (v & 1)));
+              }
+            }
+          }
+        }
+        sub = nsub;
+        if (sub < cur.sub_end) p_fill_rtab<MT>(A, rtab, Ly.o_begin + (int64_t)sub * kPSub, Ly.o_begin + Ly.rows - 1, lane);
+      }
+      __syncthreads();  // the slot and s_next are reused
+      if (!more) break;
+      if (threadIdx.x == 0) {
+        *p_next() = nxt.sub_a;
+        if (A.nslot == 1) {
+          const int64_t g = A.layer[nxt.li].chunk0 + nxt.chunk;
+          const int64_t o0 = A.qc_off[g];
+          p_issue(A, 0, (uint64_t)o0, (uint32_t)(A.qc_off[g + 1] - o0));
+        }
+      }
+      __syncthreads();
+      cur = nxt;
+    }
+  }
+  if (!waited) {
+    pdl_wait();
+    pdl_trigger();
+  }
+  if (tl && lane == 0) {
+    atomicMax(&tl[2], gtimer());
+    atomicMax(&tl[3], gtimer());
+  }
+}
+
+template <int MT, bool XB>
+__global__ void __maxnreg__(112) k_qgemv(const __grid_constant__ PArgs A) {
+  p_query<MT, true, XB>(A);
+}
+
+template <int MT>
+__global__ void __maxnreg__(112) k_qrecon(const __grid_constant__ PArgs A) {
+  p_query<MT, false, false>(A);
+}
+
+// y[r] = the fixed-order sum of row r's chunk partials: red_lanes lanes per row, lane j sums chunks
+// [4j, 4j + 4) of every 4 * red_lanes stride (one float4 load each), then an xor butterfly (all lanes
+// end with the same bits).  Launched with PDL: it waits for the partials, and triggers at once so the
+// NEXT call's compute kernel stages its chunk while this one reduces.
+__global__ void __launch_bounds__(kPRedThreads, 8) k_qreduce(const __grid_constant__ PArgs A) {
+  pdl_trigger();
+  const int L = A.red_lanes;
+  const int64_t g = (int64_t)blockIdx.x * kPRedThreads + threadIdx.x;
+  const int64_t r = g / L;
+  const int j = (int)(g % L);
+  int li = 0;
+  if (r < A.rows)
+    while (li + 1 < A.n_layers && A.layer[li + 1].row_begin <= r) ++li;
+  const PLayer& Ly = A.layer[li];
+  const int64_t rr = r - Ly.row_begin;
+  const int nch = Ly.n_chunks;
+  const float4* p = reinterpret_cast<const float4*>(Ly.partial + rr * Ly.CP);
+  void* const yp = Ly.y;
+  const bool y_bf16 = A.y_bf16 != 0;
+  asm volatile("" ::"l"(p), "l"(yp), "r"(nch), "r"((int)y_bf16) : "memory");
+  pdl_wait();
+  float t = 0.f;
+  if (r < A.rows) {
+    for (int c = 4 * j; c < nch; c += 4 * L) {
+      const float4 q = __ldcg(p + c / 4);
+      t += q.x;
+      if (c + 1 < nch) t += q.y;
+      if (c + 2 < nch) t += q.z;
+      if (c + 3 < nch) t += q.w;
+    }
+  }
+  for (int m = 1; m < L; m <<= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
+  if (r < A.rows && j == 0) {
+    if (y_bf16) {
+      const uint32_t bb = __float_as_uint(t);
+      reinterpret_cast<uint16_t*>(yp)[rr] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
+    } else {
+      reinterpret_cast<float*>(yp)[rr] = t;
+    }
+  }
+}
+
+// Unit-major cells -> query layout, one thread per 16-byte word (8 cells of a key group).  `ranges`:
+// byte ranges [lo, hi) of the query sketch to write (whole chunks of the requested layers).
+struct PackRanges {
+  int64_t lo[16], hi[16], pre[17];  // pre: prefix of the ranges' 16-B word counts
+  int32_t n;
+};
+
+__global__ void k_qpack(const __grid_constant__ PackRanges R, const uint16_t* __restrict__ cells,
+                        const int64_t* __restrict__ qc_off, const int32_t* __restrict__ qc_N,
+                        const int64_t* __restrict__ qc_u0, const int64_t* __restrict__ qc_uend,
+                        const int64_t* __restrict__ offsets, const int32_t* __restrict__ ncols,
+                        const uint8_t* __restrict__ nrows, int64_t n_chunks, uint4* __restrict__ out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= R.pre[R.n]) return;
+  int r = 0;
+  while (r + 1 < R.n && R.pre[r + 1] <= e) ++r;
+  const int64_t byte = R.lo[r] + (e - R.pre[r]) * 16;
+  int64_t a = 0, b = n_chunks;  // chunk: qc_off[a] <= byte < qc_off[a + 1]
+  while (b - a > 1) {
+    const int64_t m = (a + b) >> 1;
+    if (qc_off[m] <= byte) a = m;
+    else b = m;
+  }
+  const int64_t local = byte - qc_off[a];
+  const int32_t maxN = qc_N[a];
+  const int64_t slice = local / kQSlice;
+  const int g = (int)((local % kQSlice) / 16);
+  const int i = (int)(slice / maxN), col = (int)(slice % maxN);
+  uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+  for (int v = 0; v < kQGroup; ++v) {
+    const int64_t u = qc_u0[a] + (int64_t)g * kQGroup + v;
+    uint32_t key = 0u;
+    if (u < qc_uend[a]) {
+      const int32_t N = ncols[u];
+      if (col < N && i < (int)nrows[u]) {
+        const uint32_t bb = cells[offsets[u] + (int64_t)i * N + col];
+        key = ((((bb << 1) | (bb >> 15)) & 0xFFFFu) ^ 1u);
+      }
+    }
+    w[v >> 1] |= key << (16 * (v & 1));
+  }
+  out[byte / 16] = make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// --------------------------------------------------------------------------------- host
+int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e ? std::atoi(e) : dflt;
+}
+
+int p_occupancy(const void* kern, size_t smem) {
+  static std::mutex mu;
+  static std::vector<std::pair<std::tuple<int, const void*, size_t>, int>> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  const auto key = std::make_tuple(dev, kern, smem);
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    for (auto& e : cache)
+      if (e.first == key) return e.second;
+  }
+  if (ensure_smem(kern, 227 * 1024) != cudaSuccess) return 0;
+  int occ = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kPThreads, smem) != cudaSuccess) {
+    (void)cudaGetLastError();
+    occ = 0;
+  }
+  std::lock_guard<std::mutex> lock(mu);
+  cache.push_back({key, occ});
+  return occ;
+}
+
+const void* pick_kernel(bool gemv, bool xb, int M) {
+  if (gemv) {
+    if (xb) {
+      switch (M) {
+        case 1: return (const void*)k_qgemv<1, true>;
+        case 2: return (const void*)k_qgemv<2, true>;
+        case 3: return (const void*)k_qgemv<3, true>;
+        default: return (const void*)k_qgemv<4, true>;
+      }
+    }
+    switch (M) {
+      case 1: return (const void*)k_qgemv<1, false>;
+      case 2: return (const void*)k_qgemv<2, false>;
+      case 3: return (const void*)k_qgemv<3, false>;
+      default: return (const void*)k_qgemv<4, false>;
+    }
+  }
+  switch (M) {
+    case 1: return (const void*)k_qrecon<1>;
+    case 2: return (const void*)k_qrecon<2>;
+    case 3: return (const void*)k_qrecon<3>;
+    default: return (const void*)k_qrecon<4>;
+  }
+}
+
+int partial_stride(int n_chunks) { return (n_chunks + 3) / 4 * 4; }
+size_t layer_ws_bytes(int n_chunks, int64_t rows) { return ((size_t)rows * partial_stride(n_chunks) * 4 + 255) / 256 * 256; }
+
+// Balanced CTA item ranges: minimise the largest per-CTA cost (items + P per chunk boundary inside
+// a range: one more bulk copy and warp drain) over at most `cap` CTAs (binary search, greedy fill).
+int p_partition(PArgs& A, int cap, int64_t P) {
+  const int64_t I = A.items;
+  cap = (int)std::min<int64_t>(std::min<int64_t>(cap, I), kPMaxCtas);
+  auto chunk_end = [&](int64_t s) {
+    int li = 0;
+    while (li + 1 < A.n_layers && A.layer[li + 1].item_begin <= s) ++li;
+    const PLayer& L = A.layer[li];
+    return L.item_begin + ((s - L.item_begin) / L.n_sub + 1) * L.n_sub;
+  };
+  auto fill = [&](int64_t T, bool write) -> int {
+    int64_t pos = 0;
+    int c = 0;
+    while (pos < I) {
+      if (c >= cap) return cap + 1;
+      if (write) A.cta_item[c] = (int32_t)pos;
+      int64_t budget = T, cur = pos;
+      for (bool first = true; cur < I; first = false) {
+        if (!first && (budget -= P) <= 0) break;
+        const int64_t take = std::min(chunk_end(cur) - cur, budget);
+        cur += take;
+        budget -= take;
+        if (budget <= 0) break;
+      }
+      pos = cur;
+      ++c;
+    }
+    if (write) A.cta_item[c] = (int32_t)I;
+    return c;
+  };
+  int64_t lo = (I + cap - 1) / cap, hi = lo;
+  while (fill(hi, false) > cap) hi *= 2;
+  while (lo < hi) {
+    const int64_t mid = (lo + hi) / 2;
+    if (fill(mid, false) <= cap) hi = mid;
+    else lo = mid + 1;
+  }
+  return fill(lo, true);
+}
+
+struct PTrace {
+  static constexpr int64_t kCap = 1 << 18;
+  std::mutex mu;
+  bool on = std::getenv("USK_TRACE") != nullptr;
+  unsigned long long* d = nullptr;
+  int64_t cursor = 0;
+};
+
+usk_status p_launch(const void* kern, const PArgs& A, int grid, int threads, size_t smem, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)grid);
+  cfg.blockDim = dim3((unsigned)threads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  void* args[] = {const_cast<PArgs*>(&A)};
+  USK_CUDA(cudaLaunchKernelExC(&cfg, kern, args));
+  count_launch();
+  return USK_OK;
+}
+
+// Query launch geometry shared by K4p and K3p: items, slots, partition, first copies.
+usk_status p_prepare(const usk_plan* pl, PArgs& A, const void* kern, bool gemv, int& grid, size_t& smem) {
+  uint32_t slot = 0;
+  for (int k = 0; k < A.n_layers; ++k) {
+    const PLayer& L = A.layer[k];
+    for (int c = 0; c < L.n_chunks; ++c)
+      slot = std::max<uint32_t>(slot, (uint32_t)(pl->h_qc_off[L.chunk0 + c + 1] - pl->h_qc_off[L.chunk0 + c]));
+  }
+  slot = (slot + 1023u) & ~1023u;
+  const size_t base = kPHdr + kPRtab + 1024;
+  static const size_t cap = (size_t)env_int("USK_QSMEM_KB", 227) * 1024;
+  static const int force_slots = env_int("USK_QSLOTS", 0);
+  A.nslot = (base + 2 * (size_t)slot <= cap && force_slots != 1) ? 2 : 1;
+  if (base + slot > 227 * 1024) return fail(USK_EUNSUPPORTED, "query layout: a chunk exceeds shared memory");
+  A.slot_bytes = slot;
+  smem = base + (size_t)A.nslot * slot;
+  if (p_occupancy(kern, smem) < 1) return fail(USK_ECUDA, "query kernel does not fit an SM");
+  // chunk-switch penalty in items (one more bulk copy + drain): ~8 items plus the copy time
+  const int64_t P = env_int("USK_QSWITCH", 8 + (int)(slot >> 14));
+  grid = p_partition(A, device_sm_count(), P);
+  for (int c = 0; c < grid; ++c) {
+    const int64_t s = A.cta_item[c];
+    A.first_off[c] = 0;
+    A.first_bytes[c] = 0;
+    if (s >= A.cta_item[c + 1]) continue;
+    int li = 0;
+    while (li + 1 < A.n_layers && A.layer[li + 1].item_begin <= s) ++li;
+    const PLayer& L = A.layer[li];
+    const int64_t g = L.chunk0 + (s - L.item_begin) / L.n_sub;
+    A.first_off[c] = (uint64_t)pl->h_qc_off[g];
+    A.first_bytes[c] = (uint32_t)(pl->h_qc_off[g + 1] - pl->h_qc_off[g]);
+  }
+  (void)gemv;
+  static PTrace T;
+  std::lock_guard<std::mutex> lock(T.mu);
+  A.timeline = nullptr;
+  if (T.on) {
+    if (!T.d) {
+      USK_CUDA(cudaMalloc(&T.d, sizeof(unsigned long long) * kPTS * PTrace::kCap));
+      USK_CUDA(cudaMemset(T.d, 0, sizeof(unsigned long long) * kPTS * PTrace::kCap));
+    }
+    if (T.cursor + grid > PTrace::kCap) T.cursor = 0;
+    A.timeline = T.d + kPTS * T.cursor;
+    T.cursor += grid;
+  }
+  return USK_OK;
+}
+
+PArgs p_base(const usk_plan* pl, const void* sketch, int64_t in) {
+  PArgs A{};
+  A.in = in;
+  A.sketch = reinterpret_cast<const unsigned char*>(sketch);
+  A.qc_off = pl->d_qc_off;
+  A.qc_N = pl->d_qc_N;
+  A.ncols = pl->d_ncols;
+  A.ukeys = pl->d_keys;
+  A.hc = pl->hc;
+  return A;
+}
+
+}  // namespace
+
+// Query-layout geometry of a plan (usk.h USK_LAYOUT_QUERY): chunks of 256 units per layer, maxN per
+// chunk, regions back to back; every key group of 8 units must have one N (the 8 cells of a slice
+// word are read at one column).
+usk_status qlayout_geometry(usk_plan* pl) {
+  if (pl->M > kPMaxM) return fail(USK_EUNSUPPORTED, "query layout: at most 4 sketch rows");
+  pl->h_qc_off.clear();
+  pl->h_qc_N.clear();
+  int64_t off = 0, chunk = 0;
+  for (int l = 0; l < pl->n_layers; ++l) {
+    LayerGeom& L = pl->layers[l];
+    L.qoff = off;
+    L.qchunk0 = chunk;
+    L.qchunks = (int32_t)((L.n_units + kQChunkUnits - 1) / kQChunkUnits);
+    for (int64_t u = 0; u < L.n_units; u += kQGroup)
+      for (int v = 1; v < kQGroup; ++v)
+        if (pl->h_ncols[L.unit_begin + u + v] != pl->h_ncols[L.unit_begin + u])
+          return fail(USK_EUNSUPPORTED, "query layout: a key group of layer " + std::to_string(l) +
+                                            " mixes column counts (importance classes split the group)");
+    for (int c = 0; c < L.qchunks; ++c) {
+      int32_t mx = 1;
+      for (int64_t u = (int64_t)c * kQChunkUnits; u < std::min<int64_t>(L.n_units, (int64_t)(c + 1) * kQChunkUnits); ++u)
+        mx = std::max(mx, pl->h_ncols[L.unit_begin + u]);
+      pl->h_qc_off.push_back(off);
+      pl->h_qc_N.push_back(mx);
+      off += (int64_t)pl->M * mx * kQSlice;
+      ++chunk;
+    }
+    L.qbytes = off - L.qoff;
+  }
+  pl->h_qc_off.push_back(off);
+  pl->qtotal = off;
+  USK_CUDA(cudaMalloc(&pl->d_qc_off, sizeof(int64_t) * pl->h_qc_off.size()));
+  USK_CUDA(cudaMalloc(&pl->d_qc_N, sizeof(int32_t) * std::max<size_t>(pl->h_qc_N.size(), 1)));
+  USK_CUDA(cudaMemcpy(pl->d_qc_off, pl->h_qc_off.data(), sizeof(int64_t) * pl->h_qc_off.size(), cudaMemcpyHostToDevice));
+  if (!pl->h_qc_N.empty())
+    USK_CUDA(cudaMemcpy(pl->d_qc_N, pl->h_qc_N.data(), sizeof(int32_t) * pl->h_qc_N.size(), cudaMemcpyHostToDevice));
+  return USK_OK;
+}
+
+// usk_build on a query-layout plan: the unit-major build (K2) into a stream-ordered scratch buffer,
+// then k_qpack writes the requested layers' chunks.
+usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
+                         void* sketch, cudaStream_t st) {
+  if (n == 0) return USK_OK;
+  void* tmp = nullptr;
+  const size_t tmp_bytes = (size_t)pl->total_cells * 2 + 512;
+  USK_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
+  usk_status s = launch_build(pl, weights, layer_ids, n, tmp, st);
+  // per-chunk unit ranges (host tables, uploaded once per call through stream-ordered scratch)
+  const int64_t nch = (int64_t)pl->h_qc_N.size();
+  std::vector<int64_t> u0(nch), uend(nch);
+  for (int l = 0; l < pl->n_layers; ++l) {
+    const LayerGeom& L = pl->layers[l];
+    for (int c = 0; c < L.qchunks; ++c) {
+      u0[L.qchunk0 + c] = L.unit_begin + (int64_t)c * kQChunkUnits;
+      uend[L.qchunk0 + c] = L.unit_begin + L.n_units;
+    }
+  }
+  int64_t* d_u = nullptr;
+  if (s == USK_OK) {
+    cudaError_t e = cudaMallocAsync(&d_u, sizeof(int64_t) * 2 * nch, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_u, u0.data(), sizeof(int64_t) * nch, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_u + nch, uend.data(), sizeof(int64_t) * nch, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the pageable host tables go out of scope
+    if (e != cudaSuccess) s = cuda_fail(e, "usk_build (query layout): chunk tables");
+  }
+  // byte ranges of the requested layers, merged when adjacent
+  std::vector<std::pair<int64_t, int64_t>> rg;
+  for (int32_t k = 0; k < n; ++k) {
+    const LayerGeom& L = pl->layers[layer_ids ? layer_ids[k] : k];
+    rg.push_back({L.qoff, L.qoff + L.qbytes});
+  }
+  std::sort(rg.begin(), rg.end());
+  std::vector<std::pair<int64_t, int64_t>> mg;
+  for (auto& r : rg) {
+    if (!mg.empty() && mg.back().second == r.first) mg.back().second = r.second;
+    else mg.push_back(r);
+  }
+  for (size_t a = 0; s == USK_OK && a < mg.size(); a += 16) {
+    PackRanges R{};
+    R.n = (int32_t)std::min<size_t>(16, mg.size() - a);
+    R.pre[0] = 0;
+    for (int r = 0; r < R.n; ++r) {
+      R.lo[r] = mg[a + r].first;
+      R.hi[r] = mg[a + r].second;
+      R.pre[r + 1] = R.pre[r] + (R.hi[r] - R.lo[r]) / 16;
+    }
+    if (R.pre[R.n] == 0) continue;
+    k_qpack<<<(unsigned)((R.pre[R.n] + 255) / 256), 256, 0, st>>>(
+        R, reinterpret_cast<const uint16_t*>(tmp), pl->d_qc_off, pl->d_qc_N, d_u, d_u + nch, pl->d_offsets,
+        pl->d_ncols, pl->d_nrows, nch, reinterpret_cast<uint4*>(sketch));
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) s = cuda_fail(e, "k_qpack");
+    else count_launch();
+  }
+  if (d_u) (void)cudaFreeAsync(d_u, st);
+  (void)cudaFreeAsync(tmp, st);
+  return s;
+}
+
+size_t qgemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* o0, const int64_t* o1,
+                                   int n) {
+  size_t b = 0;
+  for (int k = 0; k < n; ++k) b += layer_ws_bytes(pl->layers[layers[k]].qchunks, o1[k] - o0[k]);
+  return std::max<size_t>(b, 256);
+}
+
+usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
+                              const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
+                              void* ws, cudaStream_t st) {
+  const int64_t in = pl->layers[layers[0]].in;
+  PArgs A = p_base(pl, sketch, in);
+  A.x = x;
+  A.y_bf16 = y_dtype == USK_BF16;
+  char* w = reinterpret_cast<char*>(ws);
+  int max_chunks = 1;
+  for (int k = 0; k < n; ++k) {
+    const LayerGeom& L = pl->layers[layers[k]];
+    const int64_t rows = o1[k] - o0[k];
+    if (rows > 0) {
+      PLayer& Ly = A.layer[A.n_layers++];
+      Ly.unit_base = L.unit_begin;
+      Ly.chunk0 = L.qchunk0;
+      Ly.o_begin = o0[k];
+      Ly.rows = rows;
+      Ly.item_begin = A.items;
+      Ly.row_begin = A.rows;
+      Ly.n_chunks = L.qchunks;
+      Ly.n_sub = (int32_t)((rows + kPSub - 1) / kPSub);
+      Ly.CP = partial_stride(L.qchunks);
+      Ly.y = y[k];
+      Ly.partial = reinterpret_cast<float*>(w);
+      A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
+      A.rows += rows;
+      max_chunks = std::max(max_chunks, L.qchunks);
+    }
+    w += layer_ws_bytes(L.qchunks, rows);
+  }
+  if (!A.n_layers) return USK_OK;
+  const void* kern = pick_kernel(true, x_dtype == USK_BF16, pl->M);
+  int grid = 0;
+  size_t smem = 0;
+  usk_status s = p_prepare(pl, A, kern, true, grid, smem);
+  if (s != USK_OK) return s;
+  A.red_lanes = 1;
+  while (A.red_lanes < 32 && 4 * A.red_lanes < max_chunks) A.red_lanes *= 2;
+  s = p_launch(kern, A, grid, kPThreads, smem, st);
+  if (s != USK_OK) return s;
+  (void)ensure_func_attr((const void*)k_qreduce, (int)cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+  return p_launch((const void*)k_qreduce, A, (int)((A.rows * A.red_lanes + kPRedThreads - 1) / kPRedThreads),
+                  kPRedThreads, 0, st);
+}
+
+usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t l, int64_t r0, int64_t r1, void* w_out,
+                               int64_t ld, cudaStream_t st) {
+  const LayerGeom& L = pl->layers[l];
+  const int64_t rows = r1 - r0;
+  if (rows == 0) return USK_OK;
+  PArgs A = p_base(pl, sketch, L.in);
+  PLayer& Ly = A.layer[A.n_layers++];
+  Ly.unit_base = L.unit_begin;
+  Ly.chunk0 = L.qchunk0;
+  Ly.o_begin = r0;
+  Ly.rows = rows;
+  Ly.n_chunks = L.qchunks;
+  Ly.n_sub = (int32_t)((rows + kPSub - 1) / kPSub);
+  Ly.w_out = w_out;
+  Ly.ld_out = ld;
+  A.items = (int64_t)Ly.n_chunks * Ly.n_sub;
+  A.rows = rows;
+  A.st_aligned = (ld % 8 == 0) && (reinterpret_cast<uintptr_t>(w_out) % 16 == 0);
+  const void* kern = pick_kernel(false, false, pl->M);
+  int grid = 0;
+  size_t smem = 0;
+  usk_status s = p_prepare(pl, A, kern, false, grid, smem);
+  if (s != USK_OK) return s;
+  return p_launch(kern, A, grid, kPThreads, smem, st);
+}
+
+}  // namespace usk

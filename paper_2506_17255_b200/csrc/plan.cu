@@ -39,6 +39,7 @@ struct PlanDev {
   const int64_t* numel;       // [L]
   const float* const* sal;    // [L] device pointers (may be null entries)
   int32_t L, gran, g, C, M;
+  int32_t key_shift;          // USK-XG (ledger L32): unit t takes the key of group t >> 3
 };
 
 __device__ __forceinline__ int find_layer(const int64_t* unit_base, int L, int64_t u) {
@@ -198,7 +199,8 @@ __global__ void k_unit_sizes(PlanDev P, ClassRows Mc, int64_t U, uint64_t seed, 
   const int32_t m = Mc.m[cls[u]];
   nrows[u] = (uint8_t)m;
   sizes[u] = (int64_t)m * N;
-  ukeys[u] = (uint32_t)splitmix64(seed ^ splitmix64(((uint64_t)(uint32_t)l << 32) | (uint64_t)t));
+  const uint64_t kt = (uint64_t)t >> P.key_shift;
+  ukeys[u] = (uint32_t)splitmix64(seed ^ splitmix64(((uint64_t)(uint32_t)l << 32) | kt));
 }
 
 // ---- device-wide exclusive scan of int64 sizes -> offsets[0..U] (3 kernels) ----
@@ -360,7 +362,7 @@ usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStr
   USK_CUDA(cudaMemsetAsync(d_Wc, 0, sizeof(unsigned long long) * n_scopes * C, st));
   USK_CUDA(cudaMemsetAsync(pl->d_err, 0, sizeof(int), st));
 
-  PlanDev P{d_unit_base, d_in, d_numel, d_sal, L, pl->gran, pl->g, C, pl->M};
+  PlanDev P{d_unit_base, d_in, d_numel, d_sal, L, pl->gran, pl->g, C, pl->M, pl->hash_api == USK_HASH_XG ? 3 : 0};
   const int T256 = 256;
   k_unit_scores<<<blocks_for(U, T256), T256, 0, st>>>(P, U, d_s, pl->d_err);
   USK_LAUNCHED("k_unit_scores");

@@ -1455,6 +1455,14 @@ GenQ make_genq(const usk_plan* pl, int32_t l, const void* sketch) {
 // metadata the query kernels read before their first cell (offsets, N_u, M_u, keys, classes)
 usk_status launch_prefetch(const usk_plan* pl, const void* sketch, int32_t a, int32_t b, cudaStream_t st) {
   if (a >= b) return USK_OK;
+  if (pl->layout == USK_LAYOUT_QUERY) {  // the layers' query-layout regions
+    PfRanges R{};
+    const int64_t lo = pl->layers[a].qoff, hi = pl->layers[b - 1].qoff + pl->layers[b - 1].qbytes;
+    R.base[0] = reinterpret_cast<const char*>(sketch) + lo;
+    R.bytes[0] = hi - lo;
+    R.n = 1;
+    return launch_prefetch_l2(R, st);
+  }
   const LayerGeom& La = pl->layers[a];
   const LayerGeom& Lb = pl->layers[b - 1];
   const int64_t c0 = La.cell_begin, c1 = Lb.cell_begin + Lb.n_cells;
@@ -1643,6 +1651,7 @@ usk_status usk_stats(const usk_plan* pl, const void* sketch, int32_t layer, cons
   if (!pl || !sketch || !W || !counts || !workspace) return usk::fail(USK_EINVAL, "usk_stats: null pointer");
   if (layer < 0 || layer >= pl->n_layers) return usk::fail(USK_ESHAPE, "usk_stats: layer out of range");
   if (workspace_bytes < usk::stats_workspace_bytes(pl, layer)) return usk::fail(USK_ESHAPE, "usk_stats: workspace");
+  if (pl->layout != USK_LAYOUT_UNIT_MAJOR) return usk::fail(USK_EUNSUPPORTED, "usk_stats: unit-major layout only");
   return usk::launch_stats(pl, sketch, layer, W, counts, workspace, (cudaStream_t)stream);
 }
 

@@ -17,7 +17,8 @@ LIB_PATH = os.path.join(HERE, "libusk.so")
 OK, EINVAL, ESHAPE, EBUDGET, ENONFINITE, ECUDA, EUNSUPPORTED, ERANGE = range(8)
 F32, BF16 = 0, 1
 GRAN = {"row": 0, "layer": 1, "outrow": 2}
-HASH = {"x": 0, "identity": 1}
+HASH = {"x": 0, "identity": 1, "xg": 2}
+LAYOUT = {"unit_major": 0, "query": 1}
 VARIANT = {"absmaxmin": 0, "absminmax": 1, "countmin": 2}
 STATS_KEYS = ("weights", "untouched", "sign_errors", "zero_weights", "rel_exact", "rel_lt_1e-3", "rel_1e-3",
               "rel_1e-2", "rel_1e-1", "rel_1", "rel_ge_10", "cells", "unoccupied")
@@ -43,7 +44,7 @@ class _Params(ct.Structure):
                 ("dims_per_unit", ct.c_int32), ("n_classes", ct.c_int32), ("min_cols", ct.c_int32),
                 ("hash", ct.c_int32), ("dtype", ct.c_int32), ("seed", ct.c_uint64), ("state_bits", ct.c_int32),
                 ("group_size", ct.c_int32), ("variant", ct.c_int32), ("layer_importance", ct.c_void_p),
-                ("topk", ct.c_int64), ("class_rows", ct.c_void_p)]
+                ("topk", ct.c_int64), ("class_rows", ct.c_void_p), ("layout", ct.c_int32), ("reserved", ct.c_int32)]
 
 
 class _PlanInfo(ct.Structure):
@@ -51,14 +52,15 @@ class _PlanInfo(ct.Structure):
                 ("n_units", ct.c_int64), ("total_cells", ct.c_int64), ("sketch_bytes", ct.c_int64),
                 ("numel", ct.c_int64), ("budget_bits", ct.c_int64), ("achieved_bits", ct.c_int64),
                 ("state_bits", ct.c_int32), ("group_size", ct.c_int32), ("n_groups", ct.c_int64),
-                ("scales_offset", ct.c_int64), ("topk", ct.c_int64)]
+                ("scales_offset", ct.c_int64), ("topk", ct.c_int64), ("layout", ct.c_int32), ("hash", ct.c_int32)]
 
 
 class _LayerInfo(ct.Structure):
     _fields_ = [("out_features", ct.c_int64), ("in_features", ct.c_int64), ("unit_begin", ct.c_int64),
                 ("n_units", ct.c_int64), ("cell_begin", ct.c_int64), ("n_cells", ct.c_int64),
                 ("budget_bits", ct.c_int64), ("meta_bits", ct.c_int64), ("cells_T", ct.c_int64),
-                ("achieved_bits", ct.c_int64), ("n_outliers", ct.c_int64), ("outlier_offset", ct.c_int64)]
+                ("achieved_bits", ct.c_int64), ("n_outliers", ct.c_int64), ("outlier_offset", ct.c_int64),
+                ("qbyte_begin", ct.c_int64), ("qbytes", ct.c_int64)]
 
 
 def _load():
@@ -158,6 +160,8 @@ class LayerInfo:
     achieved_bits: int
     n_outliers: int = 0
     outlier_offset: int = 0
+    qbyte_begin: int = 0
+    qbytes: int = 0
 
 
 class Plan:
@@ -205,14 +209,17 @@ class Plan:
 def plan_allocation(shapes, *, bpw: float, rows: int = 3, granularity: str = "row", dims_per_unit: int = 1,
                     n_classes: int = 0, min_cols: int = 1, hash: str = "x", dtype: str = "bf16", seed: int = 0,
                     saliency=None, state_bits: int = 0, group_size: int = 0, variant: str = "absmaxmin",
-                    layer_importance=None, topk: int = 0, class_rows=None, stream=None) -> Plan:
+                    layer_importance=None, topk: int = 0, class_rows=None, layout: str = "unit_major",
+                    stream=None) -> Plan:
     """usk_plan_allocation. saliency: None or list of (None | float32 CUDA tensor [in_features]).
     state_bits 4 / 8: stacked state quantisation with group_size cells per scale (0 = 128).
-    class_rows: None or the sketch rows of each importance class (ledger L30)."""
+    class_rows: None or the sketch rows of each importance class (ledger L30).
+    hash "xg" + layout "query": the packed decode layout (usk.h USK_LAYOUT_QUERY, ledger L32)."""
     n = len(shapes)
     arr = (_Shape * n)(*[_Shape(int(o), int(i)) for (o, i) in shapes])
     prm = _Params(float(bpw), rows, GRAN[granularity], dims_per_unit, n_classes, min_cols, HASH[hash],
-                  DTYPE[dtype], seed & (2**64 - 1), state_bits, group_size, VARIANT[variant], None, int(topk), None)
+                  DTYPE[dtype], seed & (2**64 - 1), state_bits, group_size, VARIANT[variant], None, int(topk), None,
+                  LAYOUT[layout], 0)
     limp = None
     if layer_importance is not None:  # host doubles, kept alive for the call
         limp = (ct.c_double * n)(*[float(v) for v in layer_importance])

@@ -1,0 +1,177 @@
+"""GPU parity of the query layout (usk.h USK_LAYOUT_QUERY, USK-XG keys; DESIGN.md ledger L32) through
+the C ABI against the CPU oracle on the same seeded inputs:
+
+* sketch bytes: the GPU query sketch, unpacked with tests/qlayout.py (written from usk.h's text), equals
+  the oracle's unit-major sketch bit for bit, and every padding word is 0;
+* reconstruction (K3p) bit-exact, any row range and leading dimension;
+* sketch-GEMV (K4p) within max_o |y - y64| / sum_j |x_j w'_oj| <= 1e-5 of the oracle's fp64 result for
+  bf16 and fp32 x, fp32 and bf16 y; deterministic; output shards and batched calls bit-identical to
+  the single full call."""
+import numpy as np
+import pytest
+
+import synth
+import qlayout  # tests/qlayout.py (pytest puts tests/ on sys.path)
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def usk():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2506_17255_b200 import usk as u
+    return u
+
+
+def to_dev(W):
+    return torch.from_numpy(W.view(np.int16).copy()).view(torch.bfloat16).cuda()
+
+
+def gemv_err(y, y64, x, Wr):
+    scale = np.maximum(np.abs(x)[None, :] @ np.abs(Wr).T, 1e-30)
+    return float(np.max(np.abs(y - y64) / scale))
+
+
+def build_both(orc, usk, shapes, bpw=0.5, M=3, seed=77, wseed=5, kind=None, saliency=None, C=None):
+    Ws = []
+    for k, (o, i) in enumerate(shapes):
+        Ws.append(synth.edge_matrix_bf16(kind, o, i, wseed + k) if kind else synth.weights_bf16(o, i, wseed + k))
+    sal_dev = None if saliency is None else [torch.from_numpy(s).cuda() for s in saliency]
+    pl = usk.plan_allocation(shapes, bpw=bpw, rows=M, hash="xg", layout="query", seed=seed, saliency=sal_dev,
+                             n_classes=0 if C is None else C)
+    opl = orc.plan(shapes, bpw, M=M, dtype=orc.BF16, hash_kind=orc.HASH_XG, seed=seed, saliency=saliency, C=C)
+    sk = pl.new_sketch()
+    sk.fill_(0xCD)
+    usk.build(pl, [to_dev(W) for W in Ws], sk)
+    usk.check(pl)
+    osk = orc.build_model(opl, Ws)
+    return pl, opl, sk, osk, Ws
+
+
+SHAPES = [
+    [(256, 512), (96, 512)],                # whole chunks; rows not a multiple of 16
+    [(200, 72), (49, 72)],                  # one partial chunk (9 key groups)
+    [(130, 264)],                           # a full chunk + a 1-group chunk
+    [(2048, 512), (512, 512), (8192, 256)], # Llama-like N = 21, 5, 85
+]
+BPW = {0: 0.5, 1: 1.0, 2: 0.5, 3: 0.5}
+
+
+@pytest.mark.parametrize("shapes", SHAPES, ids=[str(s[0]) for s in SHAPES])
+def test_query_sketch_bytes_and_reconstruct(orc, usk, shapes):
+    pl, opl, sk, osk, Ws = build_both(orc, usk, shapes, bpw=BPW[SHAPES.index(shapes)])
+    q = sk.cpu().numpy().view(np.uint16)
+    offs, total = qlayout.model_offsets([opl.ncols[slice(*opl.layer_units(l))] for l in range(len(shapes))], 3)
+    assert pl.info["layout"] == 1 and pl.info["hash"] == 2
+    for l, (o, i) in enumerate(shapes):
+        u0, u1 = opl.layer_units(l)
+        li = pl.layers[l]
+        assert li.qbyte_begin == offs[l]
+        qb = q[li.qbyte_begin // 2:(li.qbyte_begin + li.qbytes) // 2]
+        cells, pad_ok = qlayout.unpack_layer(qb, opl.offsets[u0:u1 + 1], opl.ncols[u0:u1], opl.nrows[u0:u1], 3)
+        np.testing.assert_array_equal(cells, osk[opl.offsets[u0]:opl.offsets[u1]])
+        assert pad_ok
+        # reconstruction: full, a ragged row range, and an odd leading dimension
+        w = torch.empty(o, i, dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, w)
+        ref = orc.reconstruct_rows(opl, osk, l)
+        np.testing.assert_array_equal(w.cpu().view(torch.int16).numpy().view(np.uint16).reshape(-1), ref.reshape(-1))
+        r0, r1 = min(3, o - 1), o
+        buf = torch.zeros(r1 - r0, i + 3, dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, buf, r0, r1)
+        got = buf[:, :i].cpu().view(torch.int16).numpy().view(np.uint16)
+        np.testing.assert_array_equal(got.reshape(-1), orc.reconstruct_rows(opl, osk, l, r0, r1).reshape(-1))
+    assert total + 256 <= pl.sketch_bytes
+
+
+@pytest.mark.parametrize("kind", ["pm_pairs", "zeros", "subnormal", "all_equal", "mixed", "outlier"])
+def test_query_edge_values(orc, usk, kind):
+    shapes = [(64, 256), (40, 64)]
+    pl, opl, sk, osk, Ws = build_both(orc, usk, shapes, bpw=4.0, kind=kind)
+    for l, (o, i) in enumerate(shapes):
+        w = torch.empty(o, i, dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, w)
+        np.testing.assert_array_equal(w.cpu().view(torch.int16).numpy().view(np.uint16).reshape(-1),
+                                      orc.reconstruct_rows(opl, osk, l).reshape(-1))
+
+
+@pytest.mark.parametrize("shapes", SHAPES, ids=[str(s[0]) for s in SHAPES])
+def test_query_gemv(orc, usk, shapes):
+    pl, opl, sk, osk, Ws = build_both(orc, usk, shapes, bpw=BPW[SHAPES.index(shapes)])
+    for l, (o, i) in enumerate(shapes):
+        Wr = orc.value_of(orc.reconstruct_rows(opl, osk, l), orc.BF16).reshape(o, i)
+        for xdt in ("bf16", "f32"):
+            x = synth.vector(i, seed=l + 11)[0]
+            if xdt == "bf16":
+                xb = synth.f32_to_bf16_bits(x)
+                xd = torch.from_numpy(xb.view(np.int16).copy()).view(torch.bfloat16).cuda()
+                x64 = synth.bf16_bits_to_f32(xb).astype(np.float64)
+            else:
+                xd = torch.from_numpy(x).cuda()
+                x64 = x.astype(np.float64)
+            y64 = orc.linear_rows(opl, osk, l, x64)[0]
+            ws = usk.new_workspace(pl, l)
+            y = torch.empty(o, dtype=torch.float32, device="cuda")
+            usk.linear(pl, sk, l, xd.view(1, -1), y.view(1, -1), ws)
+            assert gemv_err(y.cpu().numpy().astype(np.float64), y64, x64, Wr) <= 1e-5
+            y2 = torch.empty_like(y)
+            usk.linear(pl, sk, l, xd.view(1, -1), y2.view(1, -1), ws)
+            assert torch.equal(y, y2)
+            yb = torch.empty(o, dtype=torch.bfloat16, device="cuda")
+            usk.linear(pl, sk, l, xd.view(1, -1), yb.view(1, -1), ws)
+            assert torch.equal(yb, y.to(torch.bfloat16))  # RNE of the same fp32 sum
+            for h, e in ((o // 2, o), (o // 3 + 1, o - 5), (7, min(o, 47))):
+                if e <= h:
+                    continue
+                ys = torch.empty(e - h, dtype=torch.float32, device="cuda")
+                usk.linear(pl, sk, l, xd.view(1, -1), ys.view(1, -1), usk.new_workspace(pl, l, 1, h, e), h, e)
+                assert torch.equal(ys, y[h:e]), (h, e)
+    # all layers of a shape group that share in_features in one call == single calls
+    by_in = {}
+    for l, (o, i) in enumerate(shapes):
+        by_in.setdefault(i, []).append(l)
+    for i, layers in by_in.items():
+        xb = synth.f32_to_bf16_bits(synth.vector(i, seed=3)[0])
+        xd = torch.from_numpy(xb.view(np.int16).copy()).view(torch.bfloat16).cuda()
+        ys = [torch.empty(shapes[l][0], dtype=torch.float32, device="cuda") for l in layers]
+        usk.linear_batch(pl, sk, layers, xd, ys, usk.new_batch_workspace(pl, layers))
+        for k, l in enumerate(layers):
+            y1 = torch.empty(shapes[l][0], dtype=torch.float32, device="cuda")
+            usk.linear(pl, sk, l, xd.view(1, -1), y1.view(1, -1), usk.new_workspace(pl, l))
+            assert torch.equal(ys[k], y1)
+
+
+def test_query_prefill(orc, usk):
+    """T > 1 on the query layout: K3p into the workspace + the tcgen05 GEMM, within the bf16
+    tensor-core tolerance (2e-2 of the fp64 result, scaled as for the GEMV)."""
+    shapes = [(384, 512)]
+    pl, opl, sk, osk, Ws = build_both(orc, usk, shapes)
+    T = 300
+    X = synth.weights_bf16(T, 512, 99)
+    Xd = to_dev(X)
+    Y = torch.empty(T, 384, dtype=torch.float32, device="cuda")
+    usk.linear(pl, sk, 0, Xd, Y, usk.new_workspace(pl, 0, T))
+    Wr = orc.value_of(orc.reconstruct_rows(opl, osk, 0), orc.BF16).reshape(384, 512)
+    X64 = synth.bf16_bits_to_f32(X).astype(np.float64).reshape(T, 512)
+    ref = X64 @ Wr.T
+    scale = np.maximum(np.abs(X64) @ np.abs(Wr).T, 1e-30)
+    assert float(np.max(np.abs(Y.cpu().numpy() - ref) / scale)) <= 2e-2
+
+
+def test_query_layout_rejections(usk):
+    with pytest.raises(usk.UskError) as e:
+        usk.plan_allocation([(64, 64)], bpw=1.0, layout="query")  # USK-X keys
+    assert e.value.status == usk.EUNSUPPORTED
+    with pytest.raises(usk.UskError) as e:
+        usk.plan_allocation([(64, 60)], bpw=1.0, hash="xg", layout="query")  # in % 8
+    assert e.value.status == usk.EUNSUPPORTED
+    with pytest.raises(usk.UskError) as e:
+        usk.plan_allocation([(64, 64)], bpw=1.0, hash="xg", layout="query", dtype="f32")
+    assert e.value.status == usk.EUNSUPPORTED
+    pl = usk.plan_allocation([(64, 64)], bpw=1.0, hash="xg", layout="query")
+    W = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
+    with pytest.raises(usk.UskError) as e:
+        usk.stats(pl, pl.new_sketch(), 0, W)
+    assert e.value.status == usk.EUNSUPPORTED

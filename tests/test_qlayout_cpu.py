@@ -1,0 +1,35 @@
+"""CPU checks of tests/qlayout.py (the query layout of include/usk.h, written from its text) on
+oracle sketches: pack / unpack is a bijection of the unit-major cells, padding is 0, sizes follow
+the header's formula; and the library exports the query-layout entry fields (no GPU needed)."""
+import numpy as np
+
+import qlayout
+import synth
+
+
+def test_pack_unpack_roundtrip(orc):
+    shapes = [(200, 72), (130, 264), (96, 512)]
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, hash_kind=orc.HASH_XG, seed=3)
+    Ws = [synth.weights_bf16(o, i, 40 + k) for k, (o, i) in enumerate(shapes)]
+    sk = orc.build_model(opl, Ws)
+    for l, (o, i) in enumerate(shapes):
+        u0, u1 = opl.layer_units(l)
+        offs = opl.offsets[u0:u1 + 1]
+        q = qlayout.pack_layer(sk[offs[0]:], offs - offs[0], opl.ncols[u0:u1], opl.nrows[u0:u1], 3)
+        mx, sizes = qlayout.layer_geometry(opl.ncols[u0:u1], 3)
+        assert q.size * 2 == sum(sizes) and len(mx) == (i + 255) // 256
+        cells, pad_ok = qlayout.unpack_layer(q, offs, opl.ncols[u0:u1], opl.nrows[u0:u1], 3)
+        np.testing.assert_array_equal(cells, sk[offs[0]:offs[-1]])
+        assert pad_ok
+        # rho16 is a bijection of the bf16 bits ordered by (|w|, non-negative first)
+        b = np.arange(1 << 16, dtype=np.uint16)
+        r = qlayout.rho16(b)
+        assert np.unique(r).size == 1 << 16
+        np.testing.assert_array_equal(qlayout.unrho16(r), b)
+
+
+def test_abi_declares_query_layout():
+    import re, os
+    h = open(os.path.join(os.path.dirname(__file__), "..", "include", "usk.h")).read()
+    assert re.search(r"USK_LAYOUT_QUERY\s*=\s*1", h) and re.search(r"USK_HASH_XG\s*=\s*2", h)
+    assert "qbyte_begin" in h and "int32_t layout;" in h
