@@ -25,6 +25,7 @@ inline cudaError_t ensure_smem(const void* kern, int bytes) {
   return ensure_func_attr(kern, (int)cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 int device_sm_count();  // SM count of the current device (cached per device)
+unsigned long long* trace_slot(int grid);  // USK_TRACE ring slot of a launch (8 stamps per CTA) or nullptr
 
 #define USK_CUDA(call)                                              \
   do {                                                              \

@@ -75,6 +75,12 @@ struct PArgs {
   const void* x;
   int32_t red_lanes;
   int32_t st_aligned;   // reconstruct: ld and w_out allow 16-B row stores
+  // GEMV split-K handoff: every compute CTA publishes its partials (fence + arrival on ctrl[0]); the
+  // reduce kernel polls ctrl[0] == n_ctas instead of waiting for the compute grid to complete, and its
+  // last CTA re-zeroes ctrl[0..1] (the workspace is left zero-filled).  NULL: griddepcontrol.wait.
+  unsigned int* ctrl;
+  int32_t n_ctas;       // compute CTAs of the launch
+  int32_t x_prefetch;   // bulk L2 prefetch of the CTA's x slices before griddepcontrol.wait
   int32_t cta_item[kPMaxCtas + 1];
   uint64_t first_off[kPMaxCtas];   // CTA c's first bulk copy (host-computed: no dependent load)
   uint32_t first_bytes[kPMaxCtas];
@@ -207,6 +213,21 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
     if (s_begin < s_end) p_issue(A, 0, A.first_off[c], A.first_bytes[c]);  // before anything else
     if (tl) tl[4] = gtimer();
   }
+  if (GEMV && A.x_prefetch && s_begin < s_end && threadIdx.x == 32) {
+    // L2 warm-up of the x slices of this CTA's chunks (a pure hint: the loads after
+    // griddepcontrol.wait read whatever the previous kernel wrote; L2 is the point of coherence)
+    const int es = XB ? 2 : 4;
+    int64_t s = s_begin;
+    for (int n = 0; n < 4 && s < s_end; ++n) {
+      const PSeg g = p_seg_at(A, s, s_end);
+      const int64_t j0 = (int64_t)g.chunk * kQChunkUnits;
+      const int64_t nb = min((int64_t)kQChunkUnits, A.in - j0) * es;
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(A.x) + j0 * es),
+                   "r"((uint32_t)((nb + 15) & ~15ll))
+                   : "memory");
+      s = g.end;
+    }
+  }
   bool waited = false;
   if (s_begin < s_end) {
     PSeg cur = p_seg_at(A, s_begin, s_end);
@@ -247,7 +268,7 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
       mbar_wait(p_bar(slot), phase[slot]);
       phase[slot] ^= 1u;
       if (!waited) {
-        if (tl && threadIdx.x == 0) tl[5] = gtimer();
+        if (tl && threadIdx.x == 0) tl[5] = tl[6] = gtimer();
         if (GEMV) pdl_wait();  // x may be written by the previous kernel on the stream
         else pdl_wait();       // w_out may be read by the previous kernel
         pdl_trigger();
@@ -380,6 +401,11 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
     pdl_wait();
     pdl_trigger();
   }
+  if (GEMV && A.ctrl) {  // publish this CTA's partials to the reduce kernel
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.ctrl) : "memory");
+  }
   if (tl && lane == 0) {
     atomicMax(&tl[2], gtimer());
     atomicMax(&tl[3], gtimer());
@@ -401,6 +427,8 @@ __global__ void __maxnreg__(112) k_qrecon(const __grid_constant__ PArgs A) {
 // end with the same bits).  Launched with PDL: it waits for the partials, and triggers at once so the
 // NEXT call's compute kernel stages its chunk while this one reduces.
 __global__ void __launch_bounds__(kPRedThreads, 8) k_qreduce(const __grid_constant__ PArgs A) {
+  unsigned long long* const tl = A.timeline ? A.timeline + (int64_t)blockIdx.x * kPTS : nullptr;
+  if (tl && threadIdx.x == 0) tl[0] = gtimer();
   pdl_trigger();
   const int L = A.red_lanes;
   const int64_t g = (int64_t)blockIdx.x * kPRedThreads + threadIdx.x;
@@ -416,7 +444,25 @@ __global__ void __launch_bounds__(kPRedThreads, 8) k_qreduce(const __grid_consta
   void* const yp = Ly.y;
   const bool y_bf16 = A.y_bf16 != 0;
   asm volatile("" ::"l"(p), "l"(yp), "r"(nch), "r"((int)y_bf16) : "memory");
-  pdl_wait();
+  if (A.ctrl) {  // every compute CTA has published (acquire), instead of the compute grid's completion
+    if (threadIdx.x == 0) {
+      unsigned int v;
+      for (int spin = 0;; ++spin) {  // bounded: a broken handoff shows up as wrong y, never as a hang
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(A.ctrl) : "memory");
+        if (v >= (unsigned int)A.n_ctas || spin > (1 << 24)) break;
+        __nanosleep(64);  // keep the poll off the compute warps' issue slots
+      }
+      // the last reduce CTA past this point re-zeroes the counters (no compute CTA arrives any more)
+      if (atomicAdd(A.ctrl + 1, 1u) == gridDim.x - 1) {
+        A.ctrl[0] = 0u;
+        A.ctrl[1] = 0u;
+      }
+    }
+    __syncthreads();
+  } else {
+    pdl_wait();
+  }
+  if (tl && threadIdx.x == 0) tl[1] = gtimer();
   float t = 0.f;
   if (r < A.rows) {
     for (int c = 4 * j; c < nch; c += 4 * L) {
@@ -435,6 +481,10 @@ __global__ void __launch_bounds__(kPRedThreads, 8) k_qreduce(const __grid_consta
     } else {
       reinterpret_cast<float*>(yp)[rr] = t;
     }
+  }
+  if (tl && (threadIdx.x & 31) == 0) {
+    atomicMax(&tl[2], gtimer());
+    atomicMax(&tl[3], gtimer());
   }
 }
 
@@ -583,13 +633,7 @@ int p_partition(PArgs& A, int cap, int64_t P) {
   return fill(lo, true);
 }
 
-struct PTrace {
-  static constexpr int64_t kCap = 1 << 18;
-  std::mutex mu;
-  bool on = std::getenv("USK_TRACE") != nullptr;
-  unsigned long long* d = nullptr;
-  int64_t cursor = 0;
-};
+
 
 usk_status p_launch(const void* kern, const PArgs& A, int grid, int threads, size_t smem, cudaStream_t st) {
   cudaLaunchConfig_t cfg{};
@@ -641,18 +685,7 @@ usk_status p_prepare(const usk_plan* pl, PArgs& A, const void* kern, bool gemv, 
     A.first_bytes[c] = (uint32_t)(pl->h_qc_off[g + 1] - pl->h_qc_off[g]);
   }
   (void)gemv;
-  static PTrace T;
-  std::lock_guard<std::mutex> lock(T.mu);
-  A.timeline = nullptr;
-  if (T.on) {
-    if (!T.d) {
-      USK_CUDA(cudaMalloc(&T.d, sizeof(unsigned long long) * kPTS * PTrace::kCap));
-      USK_CUDA(cudaMemset(T.d, 0, sizeof(unsigned long long) * kPTS * PTrace::kCap));
-    }
-    if (T.cursor + grid > PTrace::kCap) T.cursor = 0;
-    A.timeline = T.d + kPTS * T.cursor;
-    T.cursor += grid;
-  }
+  A.timeline = trace_slot(grid);
   return USK_OK;
 }
 
@@ -774,7 +807,7 @@ size_t qgemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, co
                                    int n) {
   size_t b = 0;
   for (int k = 0; k < n; ++k) b += layer_ws_bytes(pl->layers[layers[k]].qchunks, o1[k] - o0[k]);
-  return std::max<size_t>(b, 256);
+  return b + 256;  // + the split-K control block (two counters, left zero)
 }
 
 usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
@@ -809,18 +842,23 @@ usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int3
     w += layer_ws_bytes(L.qchunks, rows);
   }
   if (!A.n_layers) return USK_OK;
+  static const int poll = env_int("USK_QPOLL", 0), xpf = env_int("USK_XPF", 1);
+  A.ctrl = poll ? reinterpret_cast<unsigned int*>(w) : nullptr;  // control block after the partials
+  A.x_prefetch = xpf;
   const void* kern = pick_kernel(true, x_dtype == USK_BF16, pl->M);
   int grid = 0;
   size_t smem = 0;
   usk_status s = p_prepare(pl, A, kern, true, grid, smem);
   if (s != USK_OK) return s;
+  A.n_ctas = grid;
   A.red_lanes = 1;
   while (A.red_lanes < 32 && 4 * A.red_lanes < max_chunks) A.red_lanes *= 2;
   s = p_launch(kern, A, grid, kPThreads, smem, st);
   if (s != USK_OK) return s;
   (void)ensure_func_attr((const void*)k_qreduce, (int)cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-  return p_launch((const void*)k_qreduce, A, (int)((A.rows * A.red_lanes + kPRedThreads - 1) / kPRedThreads),
-                  kPRedThreads, 0, st);
+  const int rgrid = (int)((A.rows * A.red_lanes + kPRedThreads - 1) / kPRedThreads);
+  A.timeline = trace_slot(rgrid);
+  return p_launch((const void*)k_qreduce, A, rgrid, kPRedThreads, 0, st);
 }
 
 usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t l, int64_t r0, int64_t r1, void* w_out,

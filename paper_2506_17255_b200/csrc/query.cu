@@ -1385,6 +1385,26 @@ usk_status launch_prefetch_l2(const PfRanges& R, cudaStream_t st) {
   return USK_OK;
 }
 
+}  // namespace
+
+// USK_TRACE (tuning only): the ring slot of a launch of `grid` CTAs (kTS stamps each), or nullptr
+unsigned long long* trace_slot(int grid) {
+  Trace& T = trace();
+  std::lock_guard<std::mutex> lock(T.mu);
+  if (!T.on) return nullptr;
+  if (!T.d) {
+    if (cudaMalloc(&T.d, sizeof(unsigned long long) * kTS * Trace::kCap) != cudaSuccess) return nullptr;
+    if (cudaMemset(T.d, 0, sizeof(unsigned long long) * kTS * Trace::kCap) != cudaSuccess) return nullptr;
+  }
+  if (T.cursor + grid > Trace::kCap) T.cursor = 0, T.grids.clear();
+  unsigned long long* p = T.d + kTS * T.cursor;
+  T.cursor += grid;
+  T.grids.push_back(grid);
+  return p;
+}
+
+namespace {
+
 usk_status launch_q(void* kern, const QArgs& A, int grid, size_t smem, bool pdl, cudaStream_t st,
                     int threads = kQThreads) {
   cudaLaunchConfig_t cfg{};

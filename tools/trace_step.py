@@ -27,13 +27,15 @@ ap.add_argument("--reps", type=int, default=5)
 ap.add_argument("--bpw", type=float, default=0.5)
 ap.add_argument("--blocks", type=int, default=16)
 ap.add_argument("--csv", default=None)
+ap.add_argument("--layout", default="query", choices=["query", "unit_major"])
 ap.add_argument("--npz", default=None, help="save the raw per-CTA stamps of the last replay")
 args = ap.parse_args()
 
 dev = torch.device("cuda", 0)
 shapes = synth.llama32_1b_shapes()[:7 * args.blocks]
 L = len(shapes)
-plan = usk.plan_allocation(shapes, bpw=args.bpw, rows=3, seed=0x5EED000000000003)
+plan = usk.plan_allocation(shapes, bpw=args.bpw, rows=3, seed=0x5EED000000000003,
+                           **({"hash": "xg", "layout": "query"} if args.layout == "query" else {}))
 sketch = plan.new_sketch(dev)
 ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, l // 7, l % 7), dev) for l, (o, i) in enumerate(shapes)]
 usk.build(plan, ws, sketch)
