@@ -125,21 +125,34 @@ __device__ __forceinline__ float fma_hi(uint32_t x, uint32_t w, float c) {
   return d;
 }
 
-// Row sums of a 16-row subtile: acc[r] = this lane's partial of row r; the same fixed tree as the
-// unit-major kernels (lane bits 3, 2, 1, 0, then 4), so a row's bits depend on nothing but its
-// chunk partials.  Lane r < 16 returns row r's sum.
-__device__ __forceinline__ float transpose_reduce16(float (&acc)[kPSub], int lane) {
+// Row sums of an SR-row subtile (SR = 16, 8 or 4): acc[r] = this lane's partial of row r.  Every row
+// is summed over the 32 lanes by ONE fixed tree whatever SR: lane bits 3, 2, 1, 0, then 4, each stage
+// adding the partials of the two lanes across that bit (fp addition commutes, so both lanes of a
+// pair agree).  With LS = 16 / SR, exchange-and-halve stages run on lane bits 3 .. log2(LS) (row
+// bits SR/2 .. 1), plain butterflies on the lane bits below, then bit 4.  So a row's bits do not
+// depend on SR (a per-launch choice), the output range, the batch or the GPU count (bit-identical
+// shards).  The sum of row p_row<SR>(lane) is returned.
+template <int SR>
+__device__ __forceinline__ int p_row(int lane) { return (lane / (16 / SR)) & (SR - 1); }
+template <int SR>
+__device__ __forceinline__ bool p_writer(int lane) { return (lane & ((16 / SR - 1) | 16)) == 0; }
+
+template <int SR>
+__device__ __forceinline__ float transpose_reduce(float (&acc)[SR], int lane) {
+  constexpr int LS = 16 / SR;
 #pragma unroll
-  for (int m = kPSub / 2; m >= 1; m >>= 1) {
-    const bool up = (lane & m) != 0;
+  for (int m = SR / 2; m >= 1; m >>= 1) {
+    const bool up = (lane & (LS * m)) != 0;
 #pragma unroll
     for (int i = 0; i < m; ++i) {
       const float send = up ? acc[i] : acc[i + m];
       const float keep = up ? acc[i + m] : acc[i];
-      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, m);
+      acc[i] = keep + __shfl_xor_sync(0xffffffffu, send, LS * m);
     }
   }
   float t = acc[0];
+#pragma unroll
+  for (int b = LS / 2; b >= 1; b >>= 1) t += __shfl_xor_sync(0xffffffffu, t, b);
   t += __shfl_xor_sync(0xffffffffu, t, 16);
   return t;
 }
@@ -181,10 +194,10 @@ __device__ __forceinline__ PSeg p_seg_at(const PArgs& A, int64_t s, int64_t s_en
 
 // Per-warp table of the subtile rows' position mixes R_i(o) mod 2^23 (rows past the range repeat
 // the last row): lane r < 16 writes row r's {R_0..R_3}.
-template <int MT>
+template <int MT, int SR>
 __device__ __forceinline__ void p_fill_rtab(const PArgs& A, uint32_t rtab, int64_t o_first, int64_t o_last, int lane) {
   __syncwarp();
-  if (lane < kPSub) {
+  if (lane < SR) {
     const uint32_t o = (uint32_t)min(o_first + lane, o_last);
     uint32_t r[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
@@ -199,7 +212,7 @@ __device__ __forceinline__ void p_fill_rtab(const PArgs& A, uint32_t rtab, int64
 // K4p / K3p: one CTA per SM computes the host-balanced contiguous item range [cta_item[c],
 // cta_item[c+1]) of (layer, chunk, 16-row subtile) items; warps grab the subtiles of a staged chunk.
 // GEMV: chunk partials of every row -> [rows][CP].  !GEMV: W' rows (bf16) -> w_out.
-template <int MT, bool GEMV, bool XB>
+template <int MT, bool GEMV, bool XB, int SR>
 __device__ __forceinline__ void p_query(const PArgs& A) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x;
@@ -302,15 +315,15 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
         return __shfl_sync(0xffffffffu, g, 0);
       };
       int sub = grab();
-      if (sub < cur.sub_end) p_fill_rtab<MT>(A, rtab, Ly.o_begin + (int64_t)sub * kPSub, Ly.o_begin + Ly.rows - 1, lane);
+      if (sub < cur.sub_end) p_fill_rtab<MT, SR>(A, rtab, Ly.o_begin + (int64_t)sub * SR, Ly.o_begin + Ly.rows - 1, lane);
       while (sub < cur.sub_end) {
         const int nsub = grab();  // issued now, consumed after this subtile
-        const int64_t r0 = (int64_t)sub * kPSub;
-        const int nrow = (int)min((int64_t)kPSub, Ly.rows - r0);
+        const int64_t r0 = (int64_t)sub * SR;
+        const int nrow = (int)min((int64_t)SR, Ly.rows - r0);
         if constexpr (GEMV) {
-          float acc[kPSub];
+          float acc[SR];
 #pragma unroll
-          for (int r = 0; r < kPSub; ++r) {
+          for (int r = 0; r < SR; ++r) {
             const uint4 R = lds128(rtab + 16u * r);
             const uint32_t Rv[4] = {R.x, R.y, R.z, R.w};
             uint4 cl[MT];
@@ -342,12 +355,13 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
             }
             acc[r] = a;
           }
-          const float t = transpose_reduce16(acc, lane);
-          if (lane < nrow) Ly.partial[(r0 + lane) * Ly.CP + cur.chunk] = t;
+          const float t = transpose_reduce<SR>(acc, lane);
+          const int rr = p_row<SR>(lane);
+          if (p_writer<SR>(lane) && rr < nrow) Ly.partial[(r0 + rr) * Ly.CP + cur.chunk] = t;
         } else {
           uint16_t* dst = reinterpret_cast<uint16_t*>(Ly.w_out) + r0 * Ly.ld_out + gcol * kQGroup;
 #pragma unroll 4
-          for (int r = 0; r < kPSub; ++r, dst += Ly.ld_out) {
+          for (int r = 0; r < SR; ++r, dst += Ly.ld_out) {
             if (r >= nrow) break;
             const uint4 R = lds128(rtab + 16u * r);
             const uint32_t Rv[4] = {R.x, R.y, R.z, R.w};
@@ -381,7 +395,7 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
           }
         }
         sub = nsub;
-        if (sub < cur.sub_end) p_fill_rtab<MT>(A, rtab, Ly.o_begin + (int64_t)sub * kPSub, Ly.o_begin + Ly.rows - 1, lane);
+        if (sub < cur.sub_end) p_fill_rtab<MT, SR>(A, rtab, Ly.o_begin + (int64_t)sub * SR, Ly.o_begin + Ly.rows - 1, lane);
       }
       __syncthreads();  // the slot and s_next are reused
       if (!more) break;
@@ -412,14 +426,14 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
   }
 }
 
-template <int MT, bool XB>
+template <int MT, bool XB, int SR>
 __global__ void __maxnreg__(112) k_qgemv(const __grid_constant__ PArgs A) {
-  p_query<MT, true, XB>(A);
+  p_query<MT, true, XB, SR>(A);
 }
 
 template <int MT>
 __global__ void __maxnreg__(112) k_qrecon(const __grid_constant__ PArgs A) {
-  p_query<MT, false, false>(A);
+  p_query<MT, false, false, 16>(A);
 }
 
 // y[r] = the fixed-order sum of row r's chunk partials: red_lanes lanes per row, lane j sums chunks
@@ -564,23 +578,26 @@ int p_occupancy(const void* kern, size_t smem) {
   return occ;
 }
 
-const void* pick_kernel(bool gemv, bool xb, int M) {
-  if (gemv) {
-    if (xb) {
-      switch (M) {
-        case 1: return (const void*)k_qgemv<1, true>;
-        case 2: return (const void*)k_qgemv<2, true>;
-        case 3: return (const void*)k_qgemv<3, true>;
-        default: return (const void*)k_qgemv<4, true>;
-      }
-    }
+template <int SR>
+const void* pick_gemv(bool xb, int M) {
+  if (xb) {
     switch (M) {
-      case 1: return (const void*)k_qgemv<1, false>;
-      case 2: return (const void*)k_qgemv<2, false>;
-      case 3: return (const void*)k_qgemv<3, false>;
-      default: return (const void*)k_qgemv<4, false>;
+      case 1: return (const void*)k_qgemv<1, true, SR>;
+      case 2: return (const void*)k_qgemv<2, true, SR>;
+      case 3: return (const void*)k_qgemv<3, true, SR>;
+      default: return (const void*)k_qgemv<4, true, SR>;
     }
   }
+  switch (M) {
+    case 1: return (const void*)k_qgemv<1, false, SR>;
+    case 2: return (const void*)k_qgemv<2, false, SR>;
+    case 3: return (const void*)k_qgemv<3, false, SR>;
+    default: return (const void*)k_qgemv<4, false, SR>;
+  }
+}
+
+const void* pick_kernel(bool gemv, bool xb, int M, int SR = 16) {
+  if (gemv) return SR == 4 ? pick_gemv<4>(xb, M) : SR == 8 ? pick_gemv<8>(xb, M) : pick_gemv<16>(xb, M);
   switch (M) {
     case 1: return (const void*)k_qrecon<1>;
     case 2: return (const void*)k_qrecon<2>;
@@ -653,7 +670,7 @@ usk_status p_launch(const void* kern, const PArgs& A, int grid, int threads, siz
 }
 
 // Query launch geometry shared by K4p and K3p: items, slots, partition, first copies.
-usk_status p_prepare(const usk_plan* pl, PArgs& A, const void* kern, bool gemv, int& grid, size_t& smem) {
+usk_status p_prepare(const usk_plan* pl, PArgs& A, const void* kern, bool gemv, int& grid, size_t& smem, int sr = 16) {
   uint32_t slot = 0;
   for (int k = 0; k < A.n_layers; ++k) {
     const PLayer& L = A.layer[k];
@@ -670,7 +687,7 @@ usk_status p_prepare(const usk_plan* pl, PArgs& A, const void* kern, bool gemv, 
   smem = base + (size_t)A.nslot * slot;
   if (p_occupancy(kern, smem) < 1) return fail(USK_ECUDA, "query kernel does not fit an SM");
   // chunk-switch penalty in items (one more bulk copy + drain): ~8 items plus the copy time
-  const int64_t P = env_int("USK_QSWITCH", 8 + (int)(slot >> 14));
+  const int64_t P = (int64_t)env_int("USK_QSWITCH", 8 + (int)(slot >> 14)) * 16 / sr;
   grid = p_partition(A, device_sm_count(), P);
   for (int c = 0; c < grid; ++c) {
     const int64_t s = A.cta_item[c];
@@ -828,14 +845,11 @@ usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int3
       Ly.chunk0 = L.qchunk0;
       Ly.o_begin = o0[k];
       Ly.rows = rows;
-      Ly.item_begin = A.items;
       Ly.row_begin = A.rows;
       Ly.n_chunks = L.qchunks;
-      Ly.n_sub = (int32_t)((rows + kPSub - 1) / kPSub);
       Ly.CP = partial_stride(L.qchunks);
       Ly.y = y[k];
       Ly.partial = reinterpret_cast<float*>(w);
-      A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
       A.rows += rows;
       max_chunks = std::max(max_chunks, L.qchunks);
     }
@@ -845,10 +859,23 @@ usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int3
   static const int poll = env_int("USK_QPOLL", 0), xpf = env_int("USK_XPF", 1);
   A.ctrl = poll ? reinterpret_cast<unsigned int*>(w) : nullptr;  // control block after the partials
   A.x_prefetch = xpf;
-  const void* kern = pick_kernel(true, x_dtype == USK_BF16, pl->M);
+  // subtile height: 16 rows; 8 when a 16-row launch gives each SM fewer than ~9 subtiles for its 16
+  // warps (in-graph trace, Llama-3.2-1B o: 1.74 vs 1.99 us; q|k|v at ~10.7 per SM: 2.66 vs 2.57)
+  static const int forced_sr = env_int("USK_QSR", 0);
+  int64_t items16 = 0;
+  for (int k = 0; k < A.n_layers; ++k) items16 += (int64_t)A.layer[k].n_chunks * ((A.layer[k].rows + 15) / 16);
+  const int SR = forced_sr ? forced_sr : (items16 < 9 * (int64_t)device_sm_count() ? 8 : 16);
+  A.items = 0;
+  for (int k = 0; k < A.n_layers; ++k) {
+    PLayer& Ly = A.layer[k];
+    Ly.n_sub = (int32_t)((Ly.rows + SR - 1) / SR);
+    Ly.item_begin = A.items;
+    A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
+  }
+  const void* kern = pick_kernel(true, x_dtype == USK_BF16, pl->M, SR);
   int grid = 0;
   size_t smem = 0;
-  usk_status s = p_prepare(pl, A, kern, true, grid, smem);
+  usk_status s = p_prepare(pl, A, kern, true, grid, smem, SR);
   if (s != USK_OK) return s;
   A.n_ctas = grid;
   A.red_lanes = 1;
@@ -873,7 +900,7 @@ usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t l
   Ly.o_begin = r0;
   Ly.rows = rows;
   Ly.n_chunks = L.qchunks;
-  Ly.n_sub = (int32_t)((rows + kPSub - 1) / kPSub);
+  Ly.n_sub = (int32_t)((rows + 15) / 16);
   Ly.w_out = w_out;
   Ly.ld_out = ld;
   A.items = (int64_t)Ly.n_chunks * Ly.n_sub;

@@ -71,3 +71,14 @@ def unpack_layer(q_u16, offsets, ncols, nrows, rows):
         pad_ok &= bool((words[~seen] == 0).all())
         base += sizes[k]
     return cells, pad_ok
+
+
+def unit_cells(q_u16, ncols, nrows, t, rows):
+    """Unit-major cells (M_u * N_u, row-major) of unit t of a layer from the layer's query bytes."""
+    mx, sizes = layer_geometry(ncols, rows)
+    k = t // CHUNK
+    base = sum(sizes[:k])
+    words = q_u16[base // 2:(base + sizes[k]) // 2].reshape(rows, mx[k], 32, 8)
+    g, v = (t - k * CHUNK) // 8, (t - k * CHUNK) % 8
+    N, M = int(ncols[t]), int(nrows[t])
+    return unrho16(words[:M, :N, g, v]).reshape(-1)

@@ -215,3 +215,108 @@ def test_q4_gemv_gate_up_batch(orc, usk):
         y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 8)[0]
         Wdq = orc.linear_rows(opl, osk, l, np.eye(2048), r0, r0 + 8).T  # fp32-dequantised W' rows
         assert gemv_err(y.cpu().numpy()[r0:r0 + 8].astype(np.float64), y64, x64, Wdq) <= 1e-5
+
+
+def _query_units(orc, usk, pl, opl, sk, l, W_dev, n_units, rng):
+    """Query layout: sampled units of layer l rebuilt by the oracle from the same weights, compared
+    with the units read back from the GPU query bytes (tests/qlayout.py, from usk.h's text)."""
+    import qlayout
+    o, i = opl.shapes[l]
+    ts = np.sort(rng.choice(i, n_units, replace=False))
+    Wh = np.zeros((o, i), np.uint16)
+    Wh[:, ts] = host_bits(W_dev[:, torch.from_numpy(ts).cuda()].contiguous())
+    osk = np.zeros(opl.total_cells, np.uint16)
+    for t in ts:
+        orc.build_layer(opl, l, Wh, osk, int(t), int(t) + 1)
+    u0, u1 = opl.layer_units(l)
+    li = pl.layers[l]
+    q = sk.cpu().numpy().view(np.uint16)[li.qbyte_begin // 2:(li.qbyte_begin + li.qbytes) // 2]
+    for t in ts:
+        a, b = opl.offsets[u0 + t], opl.offsets[u0 + t + 1]
+        got = qlayout.unit_cells(q, opl.ncols[u0:u1], opl.nrows[u0:u1], int(t), opl.M)
+        assert np.array_equal(got, osk[a:b]), (l, t)
+    Wr = torch.empty((o, i), dtype=torch.bfloat16, device="cuda")
+    usk.reconstruct(pl, sk, l, Wr)
+    oj = np.stack([rng.integers(0, o, 256), rng.choice(ts, 256)], 1)
+    assert np.array_equal(host_bits(Wr)[oj[:, 0], oj[:, 1]].astype(np.uint32), orc.reconstruct_entries(opl, osk, l, oj))
+
+
+def test_c3_query_layout_full_model_sampled(orc, usk):
+    """The bench's headline plan: USK-XG keys in the query layout (ledger L32), all 112 linears built
+    in one call; sampled units + reconstructed entries, and sampled rows of every grouped GEMV kind."""
+    shapes = synth.llama32_1b_shapes()
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query")
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED, hash_kind=orc.HASH_XG)
+    assert pl.info["total_cells"] == opl.total_cells
+    sk = pl.new_sketch()
+    ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, l // 7, l % 7), "cuda") for l, (o, i) in enumerate(shapes)]
+    usk.build(pl, ws, sk)
+    usk.check(pl)
+    rng = np.random.default_rng(11)
+    for l in [0, 1, 3, 4, 6, 7 * 15 + 2, 7 * 15 + 5]:
+        _query_units(orc, usk, pl, opl, sk, l, ws[l], 6, rng)
+    for g in ([0, 1, 2], [3], [4, 5], [6], [7 * 15 + 4, 7 * 15 + 5]):
+        i = shapes[g[0]][1]
+        x = synth.torch_vector(i, 1000 + g[0], "cuda", torch.bfloat16)[0]
+        ys = [torch.empty(shapes[l][0], dtype=torch.float32, device="cuda") for l in g]
+        usk.linear_batch(pl, sk, g, x, ys, usk.new_batch_workspace(pl, g))
+        x64 = synth.bf16_bits_to_f32(host_bits(x)).astype(np.float64)
+        for l, y in zip(g, ys):
+            o = shapes[l][0]
+            osk = np.zeros(opl.total_cells, np.uint16)
+            orc.build_layer(opl, l, host_bits(ws[l]), osk)
+            for r0 in (0, int(rng.integers(0, o - 8)), o - 8):
+                y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 8)[0]
+                W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, r0, r0 + 8), orc.BF16).reshape(8, i)
+                assert gemv_err(y.cpu().numpy()[r0:r0 + 8].astype(np.float64), y64, x64, W64) <= 1e-5
+
+
+@pytest.mark.parametrize("k", [4, 6, 1], ids=["gate", "down", "k"])
+def test_c4_query_prefill_16384_tokens(orc, usk, k):
+    """Config 4 on the query layout (K3p into the workspace + the tcgen05 GEMM), T = 16384."""
+    o, i = synth.llama_block(2048, 512, 8192)[k]
+    T = 16384
+    W = synth.torch_weights_bf16(o, i, synth.seed_for(4, 0, k), "cuda")
+    pl = usk.plan_allocation([(o, i)], bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query")
+    opl = orc.plan([(o, i)], 0.5, M=3, dtype=orc.BF16, seed=SEED, hash_kind=orc.HASH_XG)
+    sk = pl.new_sketch()
+    usk.build(pl, [W], sk)
+    X = synth.torch_vector(i, 7, "cuda", torch.bfloat16, T=T)
+    Y = torch.empty((T, o), dtype=torch.bfloat16, device="cuda")
+    usk.linear(pl, sk, 0, X, Y, usk.new_workspace(pl, 0, T))
+    osk = np.zeros(opl.total_cells, np.uint16)
+    orc.build_layer(opl, 0, host_bits(W), osk)
+    rng = np.random.default_rng(5)
+    toks = rng.choice(T, 64, replace=False)
+    Xh = synth.bf16_bits_to_f32(host_bits(X[torch.from_numpy(toks).cuda()])).astype(np.float64)
+    Yh = Y.float().cpu().numpy()
+    for r in rng.choice(o, 8, replace=False):
+        y64 = orc.linear_rows(opl, osk, 0, Xh, int(r), int(r) + 1)[:, 0]
+        w64 = orc.value_of(orc.reconstruct_rows(opl, osk, 0, int(r), int(r) + 1), orc.BF16).reshape(i)
+        err = np.max(np.abs(Yh[toks, r] - y64) / np.maximum(np.abs(Xh) @ np.abs(w64), 1e-30))
+        assert err <= 2e-2, err
+
+
+def test_c5_query_llama8b_block(orc, usk):
+    """Llama-3-8B block on the query layout: 14336-wide down (56 chunks), sampled units and rows."""
+    shapes = synth.llama3_8b_shapes()[:7]
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query")
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED, hash_kind=orc.HASH_XG)
+    sk = pl.new_sketch()
+    ws = [synth.torch_weights_bf16(o, i, synth.seed_for(5, 0, l), "cuda") for l, (o, i) in enumerate(shapes)]
+    usk.build(pl, ws, sk)
+    usk.check(pl)
+    rng = np.random.default_rng(13)
+    for l in (0, 4, 6):
+        _query_units(orc, usk, pl, opl, sk, l, ws[l], 4, rng)
+    l = 6
+    o, i = shapes[l]
+    x = synth.torch_vector(i, 11, "cuda", torch.bfloat16)
+    y = torch.empty((1, o), dtype=torch.float32, device="cuda")
+    usk.linear(pl, sk, l, x, y, usk.new_workspace(pl, l))
+    osk = np.zeros(opl.total_cells, np.uint16)
+    orc.build_layer(opl, l, host_bits(ws[l]), osk)
+    x64 = synth.bf16_bits_to_f32(host_bits(x)[0]).astype(np.float64)
+    y64 = orc.linear_rows(opl, osk, l, x64, 1000, 1008)[0]
+    W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, 1000, 1008), orc.BF16).reshape(8, i)
+    assert gemv_err(y.cpu().numpy()[0, 1000:1008].astype(np.float64), y64, x64, W64) <= 1e-5
