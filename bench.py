@@ -436,7 +436,7 @@ def run_usk(args):
     traffic = None
     tp = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tp):
-        traffic = json.load(open(tp)).get("k_gemv_fast_bytes_per_launch")
+        traffic = json.load(open(tp)).get("k_qgemv_bytes_per_launch" if QL else "k_gemv_fast_bytes_per_launch")
 
     # ---- standalone reconstruct throughput (weights reconstructed/s, HBM-bound kernel): the 112
     #      layer reconstructions into one scratch buffer, captured as one CUDA graph, L2 flushed
@@ -638,7 +638,14 @@ def run_usk(args):
         torch.cuda.empty_cache()
         shapes8 = synth.llama3_8b_shapes()
         L8 = len(shapes8)
-        plan8 = usk.plan_allocation(shapes8, bpw=BPW, rows=ROWS, seed=SEED, **LAY)
+        lay8 = args.layout
+        try:
+            plan8 = usk.plan_allocation(shapes8, bpw=BPW, rows=ROWS, seed=SEED, **LAY)
+        except usk.UskError as e:  # 8B gate/up chunks (N = 149) exceed shared memory in the query layout
+            if e.status != usk.EUNSUPPORTED:
+                raise
+            lay8 = "unit_major"
+            plan8 = usk.plan_allocation(shapes8, bpw=BPW, rows=ROWS, seed=SEED)
         sk8 = plan8.new_sketch(dev)
         w8 = [synth.torch_weights_bf16(o, i, synth.seed_for(5, l // 7, l % 7), dev) for l, (o, i) in enumerate(shapes8)]
         usk.build(plan8, w8, sk8)
@@ -675,7 +682,7 @@ def run_usk(args):
               "decode_weights_per_s": n8 * 1000.0 / ms8, "launches_per_step": l8,
               "build_ms": b8_ms, "build_GB_per_s": n8 * (2 + BPW / 8) / (b8_ms * 1e-3) / 1e9,
               "build_hbm_frac": n8 * (2 + BPW / 8) / (b8_ms * 1e-3) / 1e9 / peaks["hbm_gbs"],
-              "sketch_MB": plan8.sketch_bytes / 1e6, "weights": n8}
+              "sketch_MB": plan8.sketch_bytes / 1e6, "weights": n8, "layout": lay8}
         del sk8, plan8, ws8, y8, x8, g8
         torch.cuda.empty_cache()
 

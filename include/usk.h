@@ -83,7 +83,8 @@ typedef enum { USK_HASH_X = 0, USK_HASH_IDENTITY = 1, USK_HASH_XG = 2 } usk_hash
  * USK_LAYOUT_UNIT_MAJOR (default): the cells of unit u at [offsets[u], offsets[u+1]) in the state
  *   dtype, row-major (i, c) inside the unit (usk_plan_export).
  * USK_LAYOUT_QUERY (round 2; bf16 states, ROW units with dims_per_unit 1, USK_HASH_XG, AbsMaxMin,
- *   raw states, no Top-K, in_features % 8 == 0, every key group of 8 units with one N): the same
+ *   raw states, no Top-K, in_features % 8 == 0, every key group of 8 units with one N, and each
+ *   256-unit chunk's rows * maxN * 512 bytes within shared memory -- maxN <= 142 at 3 rows): the same
  *   cells, permuted and re-encoded for the decode so that one 16-byte shared load gathers a key
  *   group's 8 cells of a sketch row (DESIGN.md §4 / §5 K4p).  Each layer occupies
  *   [qbyte_begin, qbyte_begin + qbytes) (usk_layer_info); its units form chunks of 256 (32 key

@@ -52,6 +52,7 @@ struct alignas(64) BuildTask {
   int64_t unit_base;   // global unit id of the layer's first unit
   int32_t tile_begin;  // first CTA of this task
   int32_t pad;
+  int64_t qchunk0;     // query layout: global index of the layer's first chunk
 };
 
 struct BuildArgs {
@@ -69,6 +70,11 @@ struct BuildArgs {
   int* err;
   uint32_t kap_max;  // largest accepted weight key: 0xFEFFFFFF (finite), 0xFF000000 (+Inf = excluded outlier)
   int32_t stages;    // ring depth: as many stages as the shared memory left beside the keys holds (<= kMaxStages)
+  // query layout (usk.h USK_LAYOUT_QUERY): write the tile's cells as rho16 words of its key groups'
+  // chunk slices instead of unit-major cells (bf16 plans)
+  unsigned char* qsketch;
+  const int64_t* qc_off;
+  const int32_t* qc_N;
 };
 
 constexpr int kMaxStages = 16;   // ring depth cap (the mbarrier header holds 2 x 16 barriers)
@@ -284,6 +290,47 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   }
   __syncthreads();
 
+  if (ES == 2 && A.qsketch) {
+    // ---------------- query layout: word (i, k, g) of the chunk = the 8 rho16 keys of key group g's
+    // cell (i, k) (usk.h).  The tile holds groups [g_lo, g_lo + TJ / 8) of chunk j0 / 256; the layer's
+    // last tile also writes the chunk's missing groups (zeros).  N_u and M_u of the tile's units are
+    // staged in the idle ring first.
+    int32_t* tN = reinterpret_cast<int32_t*>(stages);
+    int32_t* tM = tN + TJ;
+    for (int ul = threadIdx.x; ul < TJ; ul += blockDim.x) {
+      const bool ok = ul < nu;
+      tN[ul] = ok ? A.ncols[T.unit_base + j0 + ul] : 0;
+      tM[ul] = ok ? (int)A.nrows[T.unit_base + j0 + ul] : 0;
+    }
+    __syncthreads();
+    const int64_t chunk = j0 / kQChunkUnits;
+    const int g_lo = (int)((j0 % kQChunkUnits) / kQGroup);
+    const bool last = j0 + TJ >= T.in;
+    const int g_hi = last ? kQChunkGroups : g_lo + TJ / kQGroup;
+    const int ng = g_hi - g_lo;
+    const int maxN = A.qc_N[T.qchunk0 + chunk];
+    uint4* qo = reinterpret_cast<uint4*>(A.qsketch + A.qc_off[T.qchunk0 + chunk]);
+    const int64_t words = (int64_t)A.M * maxN * ng;
+    for (int64_t e = threadIdx.x; e < words; e += blockDim.x) {
+      const int gg = (int)(e % ng);
+      const int64_t ik = e / ng;
+      const int i = (int)(ik / maxN), k = (int)(ik % maxN);
+      uint32_t w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+      for (int v8 = 0; v8 < kQGroup; ++v8) {
+        const int ul = gg * kQGroup + v8;
+        if (ul >= TJ) break;
+        const int N = tN[ul];
+        if (k < N && i < tM[ul]) {
+          const uint32_t key = keys[(ul % UPL) * stride_v + (i * N + k) * 32 + ul / UPL];
+          const uint32_t b = (key == ~0u) ? 0x7F80u : (rotr1(key) >> 16);  // empty = +Inf
+          w[v8 >> 1] |= ((((b << 1) | (b >> 15)) & 0xFFFFu) ^ 1u) << (16 * (v8 & 1));
+        }
+      }
+      qo[ik * kQChunkGroups + g_lo + gg] = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+    return;
+  }
   // ---------------- write states.  The tile's units are consecutive in the sketch, so its cells are
   // ONE contiguous range [c0, c1).  Keys -> states into a staging copy of that range in the (now
   // idle) ring memory -- lane L reads its own units' keys (bank L, conflict-free) -- then one bulk
@@ -653,7 +700,7 @@ usk_status launch_fast_m(BuildArgs& A, int n_ctas, int hash, cudaStream_t st) {
 }
 
 usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_t, const void*>>& group,
-                       void* sketch, cudaStream_t st, uint32_t kap_max) {
+                       void* sketch, cudaStream_t st, uint32_t kap_max, void* qsketch = nullptr) {
   // longest tasks first (largest out) so the big CTAs start in the first wave
   std::stable_sort(group.begin(), group.end(), [&](auto& a, auto& b) {
     return pl->layers[a.first].out > pl->layers[b.first].out;
@@ -670,6 +717,9 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
     A.sketch = sketch;
     A.err = pl->d_err;
     A.kap_max = kap_max;
+    A.qsketch = reinterpret_cast<unsigned char*>(qsketch);
+    A.qc_off = pl->d_qc_off;
+    A.qc_N = pl->d_qc_N;
     int tiles = 0, maxmn = 1;
     const int TJ = 32 * upl;
     for (size_t k = g0; k < std::min(group.size(), g0 + kMaxTasks); ++k) {
@@ -683,6 +733,7 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
       t.out = outrow ? L.in : L.out;
       t.in = outrow ? L.out : L.in;
       t.unit_base = L.unit_begin;
+      t.qchunk0 = L.qchunk0;
       t.tile_begin = tiles;
       tiles += (int)((t.in + TJ - 1) / TJ);
       maxmn = std::max(maxmn, pl->M * L.max_ncols);
@@ -898,6 +949,30 @@ static usk_status launch_build_topk(const usk_plan* pl, const void* const* weigh
   if (s == USK_OK) s = launch_build_raw(pl, wb.data(), layer_ids, n, sketch, st, 0xFF000000u);
   for (void* t : temps) cudaFreeAsync(t, st);
   return s;
+}
+
+// query layout (usk.h USK_LAYOUT_QUERY): K2 writes the rho16 chunk slices directly when every requested
+// layer takes the fast build (else packed.cu builds unit-major cells into scratch and packs them)
+bool build_qfast_ok(const usk_plan* pl, const int32_t* layer_ids, int32_t n) {
+  if (pl->dtype != USK_BF16 || pl->gran != USK_GRAN_ROW || pl->q || pl->topk) return false;
+  for (int32_t k = 0; k < n; ++k)
+    if (!fast_upl(pl, layer_ids ? layer_ids[k] : k)) return false;
+  return true;
+}
+
+usk_status launch_build_qfast(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
+                              void* qsketch, cudaStream_t st) {
+  std::vector<std::pair<int32_t, const void*>> grp[5];
+  for (int32_t k = 0; k < n; ++k) {
+    const int32_t l = layer_ids ? layer_ids[k] : k;
+    grp[fast_upl(pl, l)].push_back({l, weights[k]});
+  }
+  for (int upl : {4, 2, 1}) {
+    if (grp[upl].empty()) continue;
+    usk_status s = launch_fast(pl, upl, grp[upl], nullptr, st, 0xFEFFFFFFu, qsketch);
+    if (s != USK_OK) return s;
+  }
+  return USK_OK;
 }
 
 usk_status launch_build_rows(const usk_plan* pl, int32_t l, int64_t r0, int64_t r1, const void* w_rows, void* sketch,

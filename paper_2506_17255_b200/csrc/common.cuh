@@ -224,6 +224,9 @@ bool layer_fast_ok(const usk_plan* pl, int32_t layer);
 bool outrow_fast_ok(const usk_plan* pl, const int32_t* layers, int n);
 // query layout (packed.cu)
 usk_status qlayout_geometry(usk_plan* pl);
+bool build_qfast_ok(const usk_plan* pl, const int32_t* layer_ids, int32_t n);
+usk_status launch_build_qfast(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
+                              void* qsketch, cudaStream_t st);
 usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
                          void* sketch, cudaStream_t st);
 usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t layer, int64_t r0, int64_t r1,

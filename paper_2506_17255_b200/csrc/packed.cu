@@ -742,6 +742,9 @@ usk_status qlayout_geometry(usk_plan* pl) {
       int32_t mx = 1;
       for (int64_t u = (int64_t)c * kQChunkUnits; u < std::min<int64_t>(L.n_units, (int64_t)(c + 1) * kQChunkUnits); ++u)
         mx = std::max(mx, pl->h_ncols[L.unit_begin + u]);
+      if ((int64_t)pl->M * mx * kQSlice + kPHdr + kPRtab + 1024 > 227 * 1024)
+        return fail(USK_EUNSUPPORTED, "query layout: a 256-unit chunk of layer " + std::to_string(l) +
+                                          " (rows x max N x 512 B) exceeds shared memory");
       pl->h_qc_off.push_back(off);
       pl->h_qc_N.push_back(mx);
       off += (int64_t)pl->M * mx * kQSlice;
@@ -764,6 +767,8 @@ usk_status qlayout_geometry(usk_plan* pl) {
 usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
                          void* sketch, cudaStream_t st) {
   if (n == 0) return USK_OK;
+  static const int force_pack = env_int("USK_QBUILD_PACK", 0);
+  if (!force_pack && build_qfast_ok(pl, layer_ids, n)) return launch_build_qfast(pl, weights, layer_ids, n, sketch, st);
   void* tmp = nullptr;
   const size_t tmp_bytes = (size_t)pl->total_cells * 2 + 512;
   USK_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));

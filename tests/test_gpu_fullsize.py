@@ -298,8 +298,14 @@ def test_c4_query_prefill_16384_tokens(orc, usk, k):
 
 
 def test_c5_query_llama8b_block(orc, usk):
-    """Llama-3-8B block on the query layout: 14336-wide down (56 chunks), sampled units and rows."""
-    shapes = synth.llama3_8b_shapes()[:7]
+    """Llama-3-8B block on the query layout: q, k, v, o and the 14336-wide down (56 chunks), sampled
+    units and rows.  gate/up ([14336, 4096], N = 149 at 0.5 bpw: 3 x 149 x 512 B = 229 KB per 256-unit
+    chunk) exceed shared memory and are rejected with USK_EUNSUPPORTED (usk.h)."""
+    full = synth.llama3_8b_shapes()[:7]
+    with pytest.raises(usk.UskError) as e:
+        usk.plan_allocation(full, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query")
+    assert e.value.status == usk.EUNSUPPORTED
+    shapes = [full[k] for k in (0, 1, 2, 3, 6)]
     pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query")
     opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED, hash_kind=orc.HASH_XG)
     sk = pl.new_sketch()
@@ -307,9 +313,9 @@ def test_c5_query_llama8b_block(orc, usk):
     usk.build(pl, ws, sk)
     usk.check(pl)
     rng = np.random.default_rng(13)
-    for l in (0, 4, 6):
+    for l in (0, 3, 4):
         _query_units(orc, usk, pl, opl, sk, l, ws[l], 4, rng)
-    l = 6
+    l = 4
     o, i = shapes[l]
     x = synth.torch_vector(i, 11, "cuda", torch.bfloat16)
     y = torch.empty((1, o), dtype=torch.float32, device="cuda")

@@ -160,6 +160,26 @@ def test_query_prefill(orc, usk):
     assert float(np.max(np.abs(Y.cpu().numpy() - ref) / scale)) <= 2e-2
 
 
+def test_query_build_paths_agree(usk):
+    """The fused K2 write-out (default) and the unit-major build + k_qpack (USK_QBUILD_PACK=1, the
+    fallback) write the same query bytes; run in a child process so the env switch takes effect."""
+    import os, subprocess, sys
+    code = (
+        "import sys, hashlib, torch; sys.path.insert(0, %r); import synth; "
+        "from paper_2506_17255_b200 import usk; "
+        "sh=[(2048,512),(512,512),(200,72)]; "
+        "pl=usk.plan_allocation(sh, bpw=0.5, hash='xg', layout='query', seed=9); sk=pl.new_sketch(); sk.zero_(); "
+        "ws=[synth.torch_weights_bf16(o,i,30+k,'cuda') for k,(o,i) in enumerate(sh)]; usk.build(pl, ws, sk); usk.check(pl); "
+        "print(hashlib.sha256(sk.cpu().numpy().tobytes()).hexdigest())") % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = []
+    for flag in ("0", "1"):
+        env = dict(os.environ, USK_QBUILD_PACK=flag)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr
+        out.append(r.stdout.strip().splitlines()[-1])
+    assert out[0] == out[1]
+
+
 def test_query_layout_rejections(usk):
     with pytest.raises(usk.UskError) as e:
         usk.plan_allocation([(64, 64)], bpw=1.0, layout="query")  # USK-X keys
@@ -169,6 +189,9 @@ def test_query_layout_rejections(usk):
     assert e.value.status == usk.EUNSUPPORTED
     with pytest.raises(usk.UskError) as e:
         usk.plan_allocation([(64, 64)], bpw=1.0, hash="xg", layout="query", dtype="f32")
+    assert e.value.status == usk.EUNSUPPORTED
+    with pytest.raises(usk.UskError) as e:  # a 256-unit chunk (3 x 833 columns) exceeds shared memory
+        usk.plan_allocation([(40000, 16)], bpw=1.0, hash="xg", layout="query")
     assert e.value.status == usk.EUNSUPPORTED
     pl = usk.plan_allocation([(64, 64)], bpw=1.0, hash="xg", layout="query")
     W = torch.zeros(64, 64, dtype=torch.bfloat16, device="cuda")
