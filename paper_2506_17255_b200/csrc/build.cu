@@ -92,7 +92,12 @@ __device__ __forceinline__ void key_min(uint32_t saddr, uint32_t kap) {
   asm volatile("red.shared.min.u32 [%0], %1;" ::"r"(saddr), "r"(kap) : "memory");
 }
 
-template <typename E, int UPL, int MT, int HASH>
+// GK (grouped keys, USK-XG with one N per key group, ledger L32): the UPL units of a lane lie in one
+// key group, so they share the hash and N -- one shared address per (row o, sketch row i) serves all
+// UPL units.  Keys then live at word (kidx * UPL + v) * 32 + lane (kidx = i * N + c): unit v is the
+// immediate offset v * 128 from the row's address, which one FFMA.RZ at ulp UPL * 128 and one IMAD give
+// (the packed-decode form, tests/test_oracle_hash.py::test_packed_float_form for ulp 512).
+template <typename E, int UPL, int MT, int HASH, bool GK = false>
 __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_constant__ BuildArgs A) {
   constexpr int ES = sizeof(E);
   constexpr int TJ = 32 * UPL;
@@ -105,7 +110,15 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   uint64_t* empty = full + kMaxStages;
   uint8_t* stages = smem + kBuildHdr;
   uint32_t* keys = reinterpret_cast<uint32_t*>(stages + S * STAGEB);
+  if constexpr (GK) {  // the grouped address form needs a 512-B aligned key base (host adds the slack)
+    const uint32_t a = smem_u32(keys);
+    keys += ((512u - (a & 511u)) & 511u) / 4u;
+  }
   const uint32_t smem_keys = smem_u32(keys);
+  // key of tile-local unit ul, cell kidx (= i * N_u + c)
+  auto key_at = [&](int ul, int kidx) -> uint32_t {
+    return GK ? keys[(kidx * UPL + ul % UPL) * 32 + ul / UPL] : keys[(ul % UPL) * (32 * A.maxMN) + kidx * 32 + ul / UPL];
+  };
 
   const int b = blockIdx.x;
   int ti = 0;
@@ -156,6 +169,93 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   } else {
     // ---------------- consumers: warp cw takes rows cw and cw + 16 of every stage
     const int cw = warp - 1;
+    if constexpr (GK && MT > 0 && HASH == USK_HASH_X) {
+      constexpr uint32_t SLB = 128u * UPL;  // bytes per kidx row of a lane's UPL unit slots
+      const bool valid0 = UPL * lane < nu;
+      const int64_t u0 = T.unit_base + j0 + (valid0 ? UPL * lane : 0);
+      const uint32_t Kg = A.ukeys[u0];
+      const uint32_t Ng = valid0 ? (uint32_t)A.ncols[u0] : 1u;
+      uint32_t fk[MT], cb[MT];
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        fk[i] = short_fkey(row_key(Kg, A.hc.kap[i]));
+        // SLB * 2^23 + B_i - SLB * N: result of the FFMA at ulp SLB, B_i = key base + i * N * SLB
+        cb[i] = __float_as_uint(__ull2float_rz((unsigned long long)SLB * 8388608ull + smem_keys +
+                                               (unsigned long long)i * Ng * SLB - (unsigned long long)SLB * Ng));
+      }
+      const float NS = (float)(SLB * Ng);
+      // bits * SLB keeps (biased exponent << 23) * SLB mod 2^32 (zero for SLB 512 / 256, 2^30 for 128)
+      constexpr uint32_t EXP = 127u + 23u + (SLB == 512u ? 9u : SLB == 256u ? 8u : 7u);
+      const uint32_t LB = 4u * (uint32_t)lane - (EXP << 23) * SLB;
+      uint32_t kmax = 0;
+      int s = 0;
+      uint32_t ph = 0;
+      for (int64_t it = 0; it < n_it; ++it) {
+        mbar_wait(&full[s], ph);
+        const uint8_t* st = stages + s * STAGEB;
+        const int64_t o0 = it * kRO;
+        const int rows = (int)min((int64_t)kRO, T.out - o0);
+        constexpr int RR = kRO / kConsumers;
+        // every row's weights and position mixes are loaded before any update (the atomics' asm
+        // "memory" clobbers would otherwise keep the next row's shared loads behind them); rows past
+        // a partial last stage read the (zero-filled / stale) ring and are skipped at the update
+        using WT = typename std::conditional<ES * UPL == 8, uint2,
+                   typename std::conditional<ES * UPL == 16, uint4,
+                   typename std::conditional<ES * UPL == 4, uint32_t, uint16_t>::type>::type>::type;
+        WT wv[RR];
+        uint4 R4v[RR];
+#pragma unroll
+        for (int rr = 0; rr < RR; ++rr) {
+          const int r = cw + rr * kConsumers;
+          wv[rr] = reinterpret_cast<const WT*>(st + kRO * 16 + r * ROWB)[lane];
+          R4v[rr] = reinterpret_cast<const uint4*>(st)[r];  // broadcast shared load
+        }
+#pragma unroll
+        for (int rr = 0; rr < RR; ++rr) {
+          const int r = cw + rr * kConsumers;
+          if (r >= rows) break;
+          uint32_t kap[UPL];
+          if constexpr (ES == 2 && UPL == 4) {
+            kap[0] = rotl1(wv[rr].x << 16);
+            kap[1 % UPL] = rotl1(wv[rr].x & 0xFFFF0000u);
+            kap[2 % UPL] = rotl1(wv[rr].y << 16);
+            kap[3 % UPL] = rotl1(wv[rr].y & 0xFFFF0000u);
+          } else if constexpr (ES == 2 && UPL == 2) {
+            kap[0] = rotl1((uint32_t)wv[rr] << 16);
+            kap[1 % UPL] = rotl1((uint32_t)wv[rr] & 0xFFFF0000u);
+          } else if constexpr (ES == 2) {
+            kap[0] = rotl1((uint32_t)wv[rr] << 16);
+          } else if constexpr (UPL == 4) {
+            kap[0] = rotl1(wv[rr].x);
+            kap[1 % UPL] = rotl1(wv[rr].y);
+            kap[2 % UPL] = rotl1(wv[rr].z);
+            kap[3 % UPL] = rotl1(wv[rr].w);
+          } else if constexpr (UPL == 2) {
+            kap[0] = rotl1(wv[rr].x);
+            kap[1 % UPL] = rotl1(wv[rr].y);
+          } else {
+            kap[0] = rotl1((uint32_t)wv[rr]);
+          }
+#pragma unroll
+          for (int v = 0; v < UPL; ++v) kmax = max(kmax, kap[v]);
+          const uint32_t R23[3] = {R4v[rr].x, R4v[rr].y, R4v[rr].z};
+#pragma unroll
+          for (int i = 0; i < MT; ++i) {
+            const uint32_t a =
+                __float_as_uint(__fmaf_rz(__uint_as_float(R23[i] ^ fk[i]), NS, __uint_as_float(cb[i]))) * SLB + LB;
+#pragma unroll
+            for (int v = 0; v < UPL; ++v) key_min(a + 128u * v, kap[v]);  // missing units: scratch slots
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        if (++s == S) {
+          s = 0;
+          ph ^= 1u;
+        }
+      }
+      if (kmax > A.kap_max) atomicOr(A.err, 1);  // NaN / Inf weight (USK_ENONFINITE)
+    } else {
     constexpr bool FAST = MT > 0 && HASH == USK_HASH_X;  // short-unit FFMA.RZ form
     constexpr int KR = FAST ? MT : 1;
     uint32_t K[UPL], N[UPL];
@@ -287,6 +387,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       }
     }
     if (kmax > A.kap_max) atomicOr(A.err, 1);  // NaN / Inf weight (USK_ENONFINITE)
+    }
   }
   __syncthreads();
 
@@ -322,7 +423,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
         if (ul >= TJ) break;
         const int N = tN[ul];
         if (k < N && i < tM[ul]) {
-          const uint32_t key = keys[(ul % UPL) * stride_v + (i * N + k) * 32 + ul / UPL];
+          const uint32_t key = key_at(ul, i * N + k);
           const uint32_t b = (key == ~0u) ? 0x7F80u : (rotr1(key) >> 16);  // empty = +Inf
           w[v8 >> 1] |= ((((b << 1) | (b >> 15)) & 0xFFFFu) ^ 1u) << (16 * (v8 & 1));
         }
@@ -351,7 +452,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
     const int mn = (int)A.nrows[u] * A.ncols[u];  // the unit's own rows (<= M)
     const int64_t off = A.offsets[u];
     for (int k = warp; k < mn; k += kConsumers + 1) {
-      const uint32_t key = keys[v * stride_v + k * 32 + lane];
+      const uint32_t key = key_at(ul, k);
       // empty = +Inf; Top-K builds (kap_max accepts the +Inf of excluded outliers):
       // a cell that only outliers (or nothing) map to holds +0 (DESIGN.md ledger L29)
       const uint32_t b32 = (A.kap_max >= 0xFF000000u && key >= 0xFF000000u) ? 0u
@@ -664,24 +765,27 @@ int fast_upl(const usk_plan* pl, int32_t l, bool pitch_ok = false) {
   if (!pitch_ok && ((outrow ? L.out : L.in) * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
   const int S = kMinStages;
-  auto smem = [&](int upl) { return (int64_t)kBuildHdr + S * (kRO * 16 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128; };
+  auto smem = [&](int upl) { return (int64_t)kBuildHdr + S * (kRO * 16 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128 + 512; };
   for (int upl : {4, 2, 1})
     if (smem(upl) <= (int64_t)kSmemLimit) return upl;
   return 0;
 }
 
-template <typename E, int UPL, int MT, int HASH>
+template <typename E, int UPL, int MT, int HASH, bool GK = false>
 usk_status launch_fast_t(BuildArgs& A, int n_ctas, cudaStream_t st) {
   // ring depth: every stage the shared memory beside the keys holds (the bulk copies in flight per SM
   // must cover the HBM latency-bandwidth product: 3 stages of gate/up tiles are ~52 KB)
-  const size_t keys = (size_t)32 * UPL * A.maxMN * 4 + 128;
+  const size_t keys = (size_t)32 * UPL * A.maxMN * 4 + 128 + (GK ? 512 : 0);
   static const int forced = [] { const char* e = std::getenv("USK_BUILD_STAGES"); return e ? std::atoi(e) : 0; }();
   int S = (int)std::min<size_t>(kMaxStages, (kSmemLimit - kBuildHdr - keys) / stage_bytes<E, UPL>());
+  // grouped-key builds: 4 stages measured best (1B: 0.80 ms at 4, 0.81 at 3, 0.83 at 8, 0.84 at all
+  // that fit) -- the consumers are latency-bound, a deeper ring only adds L2 pressure
+  if (GK) S = std::min(S, 4);
   if (forced > 0) S = std::min(S, forced);
   if (S < kMinStages) return fail(USK_EINVAL, "usk_build: tile does not fit shared memory");
   A.stages = S;
   const size_t smem = kBuildHdr + (size_t)S * stage_bytes<E, UPL>() + keys;
-  auto kern = k_build_fast<E, UPL, MT, HASH>;
+  auto kern = k_build_fast<E, UPL, MT, HASH, GK>;
   USK_CUDA(ensure_smem((const void*)kern, 227 * 1024));  // one limit per (device, kernel): the opt-in maximum
   kern<<<n_ctas, kBuildThreads, smem, st>>>(A);
   USK_LAUNCHED("k_build_fast");
@@ -689,8 +793,16 @@ usk_status launch_fast_t(BuildArgs& A, int n_ctas, cudaStream_t st) {
 }
 
 template <typename E, int UPL>
-usk_status launch_fast_m(BuildArgs& A, int n_ctas, int hash, cudaStream_t st) {
+usk_status launch_fast_m(BuildArgs& A, int n_ctas, int hash, cudaStream_t st, bool gk = false) {
   if (hash == USK_HASH_IDENTITY) return launch_fast_t<E, UPL, 0, USK_HASH_IDENTITY>(A, n_ctas, st);
+  if (gk) {  // grouped keys (USK-XG, one N per key group)
+    switch (A.M) {
+      case 1: return launch_fast_t<E, UPL, 1, USK_HASH_X, true>(A, n_ctas, st);
+      case 2: return launch_fast_t<E, UPL, 2, USK_HASH_X, true>(A, n_ctas, st);
+      case 3: return launch_fast_t<E, UPL, 3, USK_HASH_X, true>(A, n_ctas, st);
+      default: break;
+    }
+  }
   switch (A.M) {
     case 1: return launch_fast_t<E, UPL, 1, USK_HASH_X>(A, n_ctas, st);
     case 2: return launch_fast_t<E, UPL, 2, USK_HASH_X>(A, n_ctas, st);
@@ -700,7 +812,7 @@ usk_status launch_fast_m(BuildArgs& A, int n_ctas, int hash, cudaStream_t st) {
 }
 
 usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_t, const void*>>& group,
-                       void* sketch, cudaStream_t st, uint32_t kap_max, void* qsketch = nullptr) {
+                       void* sketch, cudaStream_t st, uint32_t kap_max, void* qsketch = nullptr, bool gk = false) {
   // longest tasks first (largest out) so the big CTAs start in the first wave
   std::stable_sort(group.begin(), group.end(), [&](auto& a, auto& b) {
     return pl->layers[a.first].out > pl->layers[b.first].out;
@@ -741,16 +853,27 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
     A.maxMN = maxmn;
     usk_status s;
     if (pl->dtype == USK_BF16)
-      s = upl == 4   ? launch_fast_m<uint16_t, 4>(A, tiles, pl->hash, st)
-          : upl == 2 ? launch_fast_m<uint16_t, 2>(A, tiles, pl->hash, st)
-                     : launch_fast_m<uint16_t, 1>(A, tiles, pl->hash, st);
+      s = upl == 4   ? launch_fast_m<uint16_t, 4>(A, tiles, pl->hash, st, gk)
+          : upl == 2 ? launch_fast_m<uint16_t, 2>(A, tiles, pl->hash, st, gk)
+                     : launch_fast_m<uint16_t, 1>(A, tiles, pl->hash, st, gk);
     else
-      s = upl == 4   ? launch_fast_m<uint32_t, 4>(A, tiles, pl->hash, st)
-          : upl == 2 ? launch_fast_m<uint32_t, 2>(A, tiles, pl->hash, st)
-                     : launch_fast_m<uint32_t, 1>(A, tiles, pl->hash, st);
+      s = upl == 4   ? launch_fast_m<uint32_t, 4>(A, tiles, pl->hash, st, gk)
+          : upl == 2 ? launch_fast_m<uint32_t, 2>(A, tiles, pl->hash, st, gk)
+                     : launch_fast_m<uint32_t, 1>(A, tiles, pl->hash, st, gk);
     if (s != USK_OK) return s;
   }
   return USK_OK;
+}
+
+// grouped-key build eligible: USK-XG keys and one N per key group in the layer (ledger L32), M <= 3
+bool layer_gk_ok(const usk_plan* pl, int32_t l) {
+  static const int off = [] { const char* e = std::getenv("USK_BUILD_GK"); return e ? std::atoi(e) == 0 : 0; }();
+  if (off || pl->hash_api != USK_HASH_XG || pl->M > 3 || pl->gran != USK_GRAN_ROW) return false;
+  const LayerGeom& L = pl->layers[l];
+  for (int64_t u = 0; u < L.n_units; u += kQGroup)
+    for (int v = 1; v < kQGroup && u + v < L.n_units; ++v)
+      if (pl->h_ncols[L.unit_begin + u + v] != pl->h_ncols[L.unit_begin + u]) return false;
+  return true;
 }
 
 template <int ES>
@@ -834,12 +957,13 @@ __global__ void k_transpose(const void* src, void* dst, int64_t rows, int64_t co
 static usk_status launch_build_raw(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids,
                                    int32_t n, void* sketch, cudaStream_t st, uint32_t kap_max = 0xFEFFFFFFu) {
   std::vector<std::pair<int32_t, const void*>> grp[5];  // by units per lane (1, 2, 4)
+  std::vector<std::pair<int32_t, const void*>> ggrp[5];  // grouped keys (USK-XG)
   std::vector<std::pair<int32_t, const void*>> tgrp[5];  // output-row units: built from W^T
   for (int32_t k = 0; k < n; ++k) {
     const int32_t l = layer_ids ? layer_ids[k] : k;
     const int upl = fast_upl(pl, l);
     if (upl) {
-      (pl->gran == USK_GRAN_OUTROW ? tgrp : grp)[upl].push_back({l, weights[k]});
+      (pl->gran == USK_GRAN_OUTROW ? tgrp : layer_gk_ok(pl, l) ? ggrp : grp)[upl].push_back({l, weights[k]});
     } else {
       usk_status s = pl->dtype == USK_BF16 ? launch_generic_t<2>(pl, l, weights[k], sketch, st, kap_max)
                                             : launch_generic_t<4>(pl, l, weights[k], sketch, st, kap_max);
@@ -848,8 +972,8 @@ static usk_status launch_build_raw(const usk_plan* pl, const void* const* weight
   }
   usk_status s = USK_OK;
   for (int upl : {4, 2, 1}) {
-    if (grp[upl].empty() || s != USK_OK) continue;
-    s = launch_fast(pl, upl, grp[upl], sketch, st, kap_max);
+    if (!grp[upl].empty() && s == USK_OK) s = launch_fast(pl, upl, grp[upl], sketch, st, kap_max);
+    if (!ggrp[upl].empty() && s == USK_OK) s = launch_fast(pl, upl, ggrp[upl], sketch, st, kap_max, nullptr, true);
   }
   // output-row units (L31): transpose batches of layers (<= 64 MB, or one layer) into a stream-ordered
   // scratch buffer and build them as input-dim units of W^T; stream order serialises the batches
@@ -962,14 +1086,15 @@ bool build_qfast_ok(const usk_plan* pl, const int32_t* layer_ids, int32_t n) {
 
 usk_status launch_build_qfast(const usk_plan* pl, const void* const* weights, const int32_t* layer_ids, int32_t n,
                               void* qsketch, cudaStream_t st) {
-  std::vector<std::pair<int32_t, const void*>> grp[5];
+  std::vector<std::pair<int32_t, const void*>> grp[5], ggrp[5];
   for (int32_t k = 0; k < n; ++k) {
     const int32_t l = layer_ids ? layer_ids[k] : k;
-    grp[fast_upl(pl, l)].push_back({l, weights[k]});
+    (layer_gk_ok(pl, l) ? ggrp : grp)[fast_upl(pl, l)].push_back({l, weights[k]});
   }
   for (int upl : {4, 2, 1}) {
-    if (grp[upl].empty()) continue;
-    usk_status s = launch_fast(pl, upl, grp[upl], nullptr, st, 0xFEFFFFFFu, qsketch);
+    usk_status s = USK_OK;
+    if (!grp[upl].empty()) s = launch_fast(pl, upl, grp[upl], nullptr, st, 0xFEFFFFFFu, qsketch);
+    if (s == USK_OK && !ggrp[upl].empty()) s = launch_fast(pl, upl, ggrp[upl], nullptr, st, 0xFEFFFFFFu, qsketch, true);
     if (s != USK_OK) return s;
   }
   return USK_OK;

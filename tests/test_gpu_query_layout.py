@@ -198,3 +198,43 @@ def test_query_layout_rejections(usk):
     with pytest.raises(usk.UskError) as e:
         usk.stats(pl, pl.new_sketch(), 0, W)
     assert e.value.status == usk.EUNSUPPORTED
+
+
+@pytest.mark.parametrize("shapes,bpw,M", [([(256, 512), (96, 512)], 0.5, 3), ([(200, 72), (49, 72)], 1.0, 3),
+                                          ([(130, 264), (2048, 64)], 1.0, 2), ([(512, 40)], 2.0, 1)],
+                         ids=["block", "ragged", "M2", "M1"])
+def test_xg_unit_major_build_bit_exact(orc, usk, shapes, bpw, M):
+    """USK-XG plans in the unit-major layout build with the grouped-key K2 (one shared address per key
+    group and sketch row): every sketch byte equals the oracle's, reconstruction and GEMV as usual."""
+    Ws = [synth.weights_bf16(o, i, 60 + k) for k, (o, i) in enumerate(shapes)]
+    pl = usk.plan_allocation(shapes, bpw=bpw, rows=M, hash="xg", seed=31)
+    opl = orc.plan(shapes, bpw, M=M, dtype=orc.BF16, hash_kind=orc.HASH_XG, seed=31)
+    sk = pl.new_sketch()
+    sk.fill_(0x5A)
+    usk.build(pl, [to_dev(W) for W in Ws], sk)
+    usk.check(pl)
+    osk = orc.build_model(opl, Ws)
+    np.testing.assert_array_equal(sk.cpu().numpy().view(np.uint16)[:opl.total_cells], osk)
+    for l, (o, i) in enumerate(shapes):
+        w = torch.empty(o, i, dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, w)
+        np.testing.assert_array_equal(w.cpu().view(torch.int16).numpy().view(np.uint16).reshape(-1),
+                                      orc.reconstruct_rows(opl, osk, l).reshape(-1))
+
+
+def test_xg_importance_classes_build(orc, usk):
+    """USK-XG with C = 4 saliency classes: key groups mix column counts, so those layers take the
+    per-unit build path; bytes still equal the oracle's (and the query layout is refused)."""
+    shapes = [(256, 512), (128, 256)]
+    sal = [synth.saliency_like(i, 70 + k) for k, (o, i) in enumerate(shapes)]
+    Ws = [synth.weights_bf16(o, i, 80 + k) for k, (o, i) in enumerate(shapes)]
+    pl = usk.plan_allocation(shapes, bpw=0.5, hash="xg", seed=8, saliency=[torch.from_numpy(s).cuda() for s in sal])
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, hash_kind=orc.HASH_XG, seed=8, saliency=sal, C=4)
+    sk = pl.new_sketch()
+    usk.build(pl, [to_dev(W) for W in Ws], sk)
+    osk = orc.build_model(opl, Ws)
+    np.testing.assert_array_equal(sk.cpu().numpy().view(np.uint16)[:opl.total_cells], osk)
+    with pytest.raises(usk.UskError) as e:
+        usk.plan_allocation(shapes, bpw=0.5, hash="xg", layout="query", seed=8,
+                            saliency=[torch.from_numpy(s).cuda() for s in sal])
+    assert e.value.status == usk.EUNSUPPORTED

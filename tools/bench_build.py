@@ -18,11 +18,14 @@ from paper_2506_17255_b200 import usk  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=7)
 ap.add_argument("--8b", dest="b8", action="store_true")
+ap.add_argument("--hash", default="xg", choices=["x", "xg"])
+ap.add_argument("--layout", default="query", choices=["query", "unit_major"])
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 shapes = synth.llama3_8b_shapes() if args.b8 else synth.llama32_1b_shapes()
 cfg = 5 if args.b8 else 3
-pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=0x5EED000000000003)
+pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=0x5EED000000000003, hash=args.hash,
+                         layout="unit_major" if args.b8 else args.layout)
 sk = pl.new_sketch(dev)
 ws = [synth.torch_weights_bf16(o, i, synth.seed_for(cfg, l // 7, l % 7), dev) for l, (o, i) in enumerate(shapes)]
 usk.build(pl, ws, sk)
