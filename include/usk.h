@@ -83,16 +83,17 @@ typedef enum { USK_HASH_X = 0, USK_HASH_IDENTITY = 1, USK_HASH_XG = 2 } usk_hash
  * USK_LAYOUT_UNIT_MAJOR (default): the cells of unit u at [offsets[u], offsets[u+1]) in the state
  *   dtype, row-major (i, c) inside the unit (usk_plan_export).
  * USK_LAYOUT_QUERY (round 2; bf16 states, ROW units with dims_per_unit 1, USK_HASH_XG, AbsMaxMin,
- *   raw states, no Top-K, in_features % 8 == 0, every key group of 8 units with one N, and each
- *   256-unit chunk's rows * maxN * 512 bytes within shared memory -- maxN <= 142 at 3 rows): the same
- *   cells, permuted and re-encoded for the decode so that one 16-byte shared load gathers a key
- *   group's 8 cells of a sketch row (DESIGN.md §4 / §5 K4p).  Each layer occupies
- *   [qbyte_begin, qbyte_begin + qbytes) (usk_layer_info); its units form chunks of 256 (32 key
- *   groups; the last chunk of a layer may be partial).  Chunk k of the layer has maxN_k = the
- *   largest N_u of its units and takes rows * maxN_k * 512 bytes (rows = usk_plan_info.rows),
- *   chunks back to back from qbyte_begin.  Inside chunk k, the 16-bit word at byte
- *       ((i * maxN_k + c) * 32 + g) * 16 + 2 * v
- *   holds cell (i, c) of unit 256 k + 8 g + v of the layer as the retrieve key
+ *   raw states, no Top-K, in_features % 8 == 0, every key group of 8 units with one N, and a
+ *   128-unit chunk's rows * maxN * 256 bytes within shared memory -- maxN <= 285 at 3 rows): the same
+ *   cells, permuted and re-encoded for the decode so that one 16-byte (or 8-byte) shared load
+ *   gathers a lane's 8 (4) cells of a sketch row (DESIGN.md §4 / §5 K4p).  Each layer occupies
+ *   [qbyte_begin, qbyte_begin + qbytes) (usk_layer_info); its units form chunks of CW = qchunk_units
+ *   units -- 256 when rows * (largest N of the layer) * 512 bytes fits shared memory, else 128 --
+ *   the last chunk of a layer may be partial.  Chunk k has maxN_k = the largest N_u of its units and
+ *   takes rows * maxN_k * 2 * CW bytes (rows = usk_plan_info.rows), chunks back to back from
+ *   qbyte_begin.  Inside chunk k, the 16-bit word at byte
+ *       ((i * maxN_k + c) * CW + t) * 2
+ *   holds cell (i, c) of unit CW * k + t of the layer as the retrieve key
  *       rho16 = ((b << 1) | (b >> 15)) ^ 1  (b = the bf16 bits of the state; mag << 1 | 1 - sign),
  *   and 0 where the unit does not exist, c >= N_u or i >= M_u (0 is below every key: neutral for
  *   the Eq. 5 max).  The encoding is a bijection of the unit-major cells (same bits per weight). */
@@ -199,6 +200,8 @@ typedef struct {
                              states in the plan dtype */
   int64_t qbyte_begin;    /* USK_LAYOUT_QUERY: byte offset of the layer's region in the sketch */
   int64_t qbytes;         /*   and its size (0 for the unit-major layout) */
+  int32_t qchunk_units;   /*   units per chunk CW (256, or 128 when a 256-unit chunk exceeds shared memory) */
+  int32_t reserved;
 } usk_layer_info;
 
 /* Importance metric, Eq. 7: I[j] = (1/N) sum_k A[k, j]^2.

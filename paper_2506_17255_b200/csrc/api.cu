@@ -421,7 +421,7 @@ usk_status usk_plan_layer(const usk_plan* pl, int32_t layer, usk_layer_info* out
   const LayerGeom& L = pl->layers[layer];
   *out = usk_layer_info{L.out,         L.in,        L.unit_begin, L.n_units,       L.cell_begin, L.n_cells,
                         L.budget_bits, L.meta_bits, L.cells_T,    L.achieved_bits, L.n_out,      L.out_off,
-                        L.qoff,        L.qbytes};
+                        L.qoff,        L.qbytes,    L.qcw};
   return USK_OK;
 }
 

@@ -53,6 +53,8 @@ struct alignas(64) BuildTask {
   int32_t tile_begin;  // first CTA of this task
   int32_t pad;
   int64_t qchunk0;     // query layout: global index of the layer's first chunk
+  int32_t qcw;         //   and its chunk width (units)
+  int32_t pad2;
 };
 
 struct BuildArgs {
@@ -404,10 +406,11 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       tM[ul] = ok ? (int)A.nrows[T.unit_base + j0 + ul] : 0;
     }
     __syncthreads();
-    const int64_t chunk = j0 / kQChunkUnits;
-    const int g_lo = (int)((j0 % kQChunkUnits) / kQGroup);
+    const int CWG = T.qcw / kQGroup;  // 16-B words (key groups) per slice of the chunk
+    const int64_t chunk = j0 / T.qcw;
+    const int g_lo = (int)((j0 % T.qcw) / kQGroup);
     const bool last = j0 + TJ >= T.in;
-    const int g_hi = last ? kQChunkGroups : g_lo + TJ / kQGroup;
+    const int g_hi = last ? CWG : g_lo + TJ / kQGroup;
     const int ng = g_hi - g_lo;
     const int maxN = A.qc_N[T.qchunk0 + chunk];
     uint4* qo = reinterpret_cast<uint4*>(A.qsketch + A.qc_off[T.qchunk0 + chunk]);
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
           w[v8 >> 1] |= ((((b << 1) | (b >> 15)) & 0xFFFFu) ^ 1u) << (16 * (v8 & 1));
         }
       }
-      qo[ik * kQChunkGroups + g_lo + gg] = make_uint4(w[0], w[1], w[2], w[3]);
+      qo[ik * CWG + g_lo + gg] = make_uint4(w[0], w[1], w[2], w[3]);
     }
     return;
   }
@@ -846,6 +849,7 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
       t.in = outrow ? L.out : L.in;
       t.unit_base = L.unit_begin;
       t.qchunk0 = L.qchunk0;
+      t.qcw = L.qcw;
       t.tile_begin = tiles;
       tiles += (int)((t.in + TJ - 1) / TJ);
       maxmn = std::max(maxmn, pl->M * L.max_ncols);

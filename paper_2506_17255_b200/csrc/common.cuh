@@ -145,12 +145,10 @@ struct LayerGeom {
   // query layout (usk.h USK_LAYOUT_QUERY): byte region of the layer, its first global chunk, chunks
   int64_t qoff = 0, qbytes = 0, qchunk0 = 0;
   int32_t qchunks = 0;
+  int32_t qcw = 0;  // query layout: units per chunk (256, or 128 when a 256-unit chunk exceeds shared memory)
 };
 
-constexpr int kQGroup = 8;           // units per key group (USK-XG, ledger L32) = cells per 16-B load
-constexpr int kQChunkGroups = 32;    // key groups per query-layout chunk (one per lane)
-constexpr int kQChunkUnits = kQGroup * kQChunkGroups;
-constexpr int kQSlice = kQChunkGroups * 16;  // bytes of one (sketch row, column) slice of a chunk
+constexpr int kQGroup = 8;  // units per key group (USK-XG, ledger L32) = cells per 16-B word of the query layout
 
 }  // namespace usk
 

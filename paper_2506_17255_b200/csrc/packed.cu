@@ -75,10 +75,6 @@ struct PArgs {
   const void* x;
   int32_t red_lanes;
   int32_t st_aligned;   // reconstruct: ld and w_out allow 16-B row stores
-  // GEMV split-K handoff: every compute CTA publishes its partials (fence + arrival on ctrl[0]); the
-  // reduce kernel polls ctrl[0] == n_ctas instead of waiting for the compute grid to complete, and its
-  // last CTA re-zeroes ctrl[0..1] (the workspace is left zero-filled).  NULL: griddepcontrol.wait.
-  unsigned int* ctrl;
   int32_t n_ctas;       // compute CTAs of the launch
   int32_t x_prefetch;   // bulk L2 prefetch of the CTA's x slices before griddepcontrol.wait
   int32_t cta_item[kPMaxCtas + 1];
@@ -99,6 +95,16 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   uint4 q;
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(a));
   return q;
+}
+// the lane's UPL/2 words (UPL 16-bit cells) of one slice row: ld.shared.v4 (UPL 8) or .v2 (UPL 4)
+template <int UPL>
+__device__ __forceinline__ void lds_cells(uint32_t a, uint32_t (&w)[UPL / 2]) {
+  if constexpr (UPL == 8) {
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1 % (UPL / 2)]), "=r"(w[2 % (UPL / 2)]),
+                 "=r"(w[3 % (UPL / 2)]) : "r"(a));
+  } else {
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1 % (UPL / 2)]) : "r"(a));
+  }
 }
 __device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
   uint32_t d;
@@ -212,8 +218,11 @@ __device__ __forceinline__ void p_fill_rtab(const PArgs& A, uint32_t rtab, int64
 // K4p / K3p: one CTA per SM computes the host-balanced contiguous item range [cta_item[c],
 // cta_item[c+1]) of (layer, chunk, 16-row subtile) items; warps grab the subtiles of a staged chunk.
 // GEMV: chunk partials of every row -> [rows][CP].  !GEMV: W' rows (bf16) -> w_out.
-template <int MT, bool GEMV, bool XB, int SR>
+template <int MT, bool GEMV, bool XB, int SR, int UPL>
 __device__ __forceinline__ void p_query(const PArgs& A) {
+  constexpr int CW = 32 * UPL;        // units per chunk (one lane's UPL units each)
+  constexpr uint32_t SLB = 2u * CW;   // bytes per (sketch row, column) slice = the FFMA's ulp
+  constexpr int PW = UPL / 2;         // 32-bit words (unit pairs) per lane and slice
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x;
   const int64_t s_begin = A.cta_item[c], s_end = A.cta_item[c + 1];
@@ -233,8 +242,8 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
     int64_t s = s_begin;
     for (int n = 0; n < 4 && s < s_end; ++n) {
       const PSeg g = p_seg_at(A, s, s_end);
-      const int64_t j0 = (int64_t)g.chunk * kQChunkUnits;
-      const int64_t nb = min((int64_t)kQChunkUnits, A.in - j0) * es;
+      const int64_t j0 = (int64_t)g.chunk * CW;
+      const int64_t nb = min((int64_t)CW, A.in - j0) * es;
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(A.x) + j0 * es),
                    "r"((uint32_t)((nb + 15) & ~15ll))
                    : "memory");
@@ -260,10 +269,11 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
         const int64_t o0 = A.qc_off[g];
         p_issue(A, slot ^ 1, (uint64_t)o0, (uint32_t)(A.qc_off[g + 1] - o0));
       }
-      // lane state: key group g = lane of this chunk (the 8 units share K and N, ledger L32)
-      const int64_t gcol = (int64_t)cur.chunk * kQChunkGroups + lane;
-      const bool valid = gcol * kQGroup < A.in;
-      const int64_t u0 = Ly.unit_base + gcol * kQGroup;
+      // lane state: units j0 .. j0 + UPL - 1 of the layer, inside one key group (they share K and N,
+      // ledger L32; UPL 4: two lanes per group)
+      const int64_t j0 = (int64_t)cur.chunk * CW + UPL * lane;
+      const bool valid = j0 < A.in;  // in % 8 == 0: a lane's units all exist or none
+      const int64_t u0 = Ly.unit_base + j0;
       const uint32_t N = valid ? (uint32_t)A.ncols[u0] : 1u;
       const uint32_t K = valid ? A.ukeys[u0] : 0u;
       const uint32_t maxN = (uint32_t)A.qc_N[Ly.chunk0 + cur.chunk];
@@ -272,12 +282,14 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         fk[i] = 0x3F800000u | (fmix32(K ^ A.hc.kap[i]) & 0x7FFFFFu);
-        // 2^32 + B_i - 512 N (a multiple of 512 in [2^31, 2^33): an fp32 number)
-        cb[i] = __float_as_uint(__ull2float_rz(4294967296ull + B0 + (unsigned long long)i * maxN * kQSlice -
-                                               (unsigned long long)kQSlice * N));
+        // SLB * 2^23 + B_i - SLB * N (a multiple of SLB in [SLB 2^22, SLB 2^24): an fp32 number); the
+        // FFMA.RZ result lies at ulp SLB and bits * SLB mod 2^32 = B_i + SLB * idx (biased exponent
+        // 159 / 158 for SLB 512 / 256: (exp << 23) * SLB wraps to 0)
+        cb[i] = __float_as_uint(__ull2float_rz((unsigned long long)SLB * 8388608ull + B0 +
+                                               (unsigned long long)i * maxN * SLB - (unsigned long long)SLB * N));
       }
-      const float NS = (float)(kQSlice * N);
-      const uint32_t LB = 16u * (uint32_t)lane;
+      const float NS = (float)(SLB * N);
+      const uint32_t LB = 2u * UPL * (uint32_t)lane;
       mbar_wait(p_bar(slot), phase[slot]);
       phase[slot] ^= 1u;
       if (!waited) {
@@ -288,24 +300,32 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
         if (tl && threadIdx.x == 0) tl[7] = gtimer();
         waited = true;
       }
-      // -x of the group's 8 inputs (bf16 pairs: sign bits flipped; fp32: negated)
-      uint32_t nxb[4] = {0u, 0u, 0u, 0u};
-      float nxf[8];
+      // -x of the lane's UPL inputs (bf16 pairs: sign bits flipped; fp32: negated)
+      uint32_t nxb[PW];
+      float nxf[UPL];
 #pragma unroll
-      for (int v = 0; v < 8; ++v) nxf[v] = 0.f;
+      for (int p = 0; p < PW; ++p) nxb[p] = 0u;
+#pragma unroll
+      for (int v = 0; v < UPL; ++v) nxf[v] = 0.f;
       if (GEMV && valid) {
-        const int64_t j0 = gcol * kQGroup;
         if constexpr (XB) {
-          const uint4 xv = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A.x) + j0);
-          nxb[0] = xv.x ^ 0x80008000u;
-          nxb[1] = xv.y ^ 0x80008000u;
-          nxb[2] = xv.z ^ 0x80008000u;
-          nxb[3] = xv.w ^ 0x80008000u;
+          if constexpr (UPL == 8) {
+            const uint4 xv = *reinterpret_cast<const uint4*>(reinterpret_cast<const uint16_t*>(A.x) + j0);
+            nxb[0] = xv.x ^ 0x80008000u;
+            nxb[1 % PW] = xv.y ^ 0x80008000u;
+            nxb[2 % PW] = xv.z ^ 0x80008000u;
+            nxb[3 % PW] = xv.w ^ 0x80008000u;
+          } else {
+            const uint2 xv = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(A.x) + j0);
+            nxb[0] = xv.x ^ 0x80008000u;
+            nxb[1 % PW] = xv.y ^ 0x80008000u;
+          }
         } else {
-          const float4 a = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A.x) + j0);
-          const float4 b = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A.x) + j0 + 4);
-          nxf[0] = -a.x, nxf[1] = -a.y, nxf[2] = -a.z, nxf[3] = -a.w;
-          nxf[4] = -b.x, nxf[5] = -b.y, nxf[6] = -b.z, nxf[7] = -b.w;
+#pragma unroll
+          for (int q = 0; q < UPL / 4; ++q) {
+            const float4 a = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A.x) + j0 + 4 * q);
+            nxf[4 * q] = -a.x, nxf[4 * q + 1] = -a.y, nxf[4 * q + 2] = -a.z, nxf[4 * q + 3] = -a.w;
+          }
         }
       }
       if (tl && threadIdx.x == 0 && k == 0) tl[1] = gtimer();
@@ -326,31 +346,26 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
           for (int r = 0; r < SR; ++r) {
             const uint4 R = lds128(rtab + 16u * r);
             const uint32_t Rv[4] = {R.x, R.y, R.z, R.w};
-            uint4 cl[MT];
+            uint32_t cl[MT][PW];
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
               const uint32_t bits =
                   __float_as_uint(__fmaf_rz(__uint_as_float(Rv[i] ^ fk[i]), NS, __uint_as_float(cb[i])));
-              cl[i] = lds128(bits * (uint32_t)kQSlice + LB);
+              lds_cells<UPL>(bits * SLB + LB, cl[i]);
             }
-            uint4 m = cl[0];
+            float a = 0.f;  // the lane's units in order
 #pragma unroll
-            for (int i = 1; i < MT; ++i) {
-              m.x = max_u16x2(m.x, cl[i].x);
-              m.y = max_u16x2(m.y, cl[i].y);
-              m.z = max_u16x2(m.z, cl[i].z);
-              m.w = max_u16x2(m.w, cl[i].w);
-            }
-            const uint32_t wp[4] = {neg_w(m.x), neg_w(m.y), neg_w(m.z), neg_w(m.w)};
-            float a = 0.f;  // units 8g + 0 .. 7 in order
+            for (int p = 0; p < PW; ++p) {
+              uint32_t m = cl[0][p];
 #pragma unroll
-            for (int p = 0; p < 4; ++p) {
+              for (int i = 1; i < MT; ++i) m = max_u16x2(m, cl[i][p]);
+              const uint32_t wp = neg_w(m);
               if constexpr (XB) {
-                a = fma_lo(nxb[p], wp[p], a);
-                a = fma_hi(nxb[p], wp[p], a);
+                a = fma_lo(nxb[p], wp, a);
+                a = fma_hi(nxb[p], wp, a);
               } else {
-                a = fmaf(nxf[2 * p], __uint_as_float(wp[p] << 16), a);
-                a = fmaf(nxf[2 * p + 1], __uint_as_float(wp[p] & 0xFFFF0000u), a);
+                a = fmaf(nxf[2 * p], __uint_as_float(wp << 16), a);
+                a = fmaf(nxf[2 * p + 1], __uint_as_float(wp & 0xFFFF0000u), a);
               }
             }
             acc[r] = a;
@@ -359,37 +374,35 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
           const int rr = p_row<SR>(lane);
           if (p_writer<SR>(lane) && rr < nrow) Ly.partial[(r0 + rr) * Ly.CP + cur.chunk] = t;
         } else {
-          uint16_t* dst = reinterpret_cast<uint16_t*>(Ly.w_out) + r0 * Ly.ld_out + gcol * kQGroup;
+          uint16_t* dst = reinterpret_cast<uint16_t*>(Ly.w_out) + r0 * Ly.ld_out + j0;
 #pragma unroll 4
           for (int r = 0; r < SR; ++r, dst += Ly.ld_out) {
             if (r >= nrow) break;
             const uint4 R = lds128(rtab + 16u * r);
             const uint32_t Rv[4] = {R.x, R.y, R.z, R.w};
-            uint4 cl[MT];
+            uint32_t cl[MT][PW];
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
               const uint32_t bits =
                   __float_as_uint(__fmaf_rz(__uint_as_float(Rv[i] ^ fk[i]), NS, __uint_as_float(cb[i])));
-              cl[i] = lds128(bits * (uint32_t)kQSlice + LB);
-            }
-            uint4 m = cl[0];
-#pragma unroll
-            for (int i = 1; i < MT; ++i) {
-              m.x = max_u16x2(m.x, cl[i].x);
-              m.y = max_u16x2(m.y, cl[i].y);
-              m.z = max_u16x2(m.z, cl[i].z);
-              m.w = max_u16x2(m.w, cl[i].w);
+              lds_cells<UPL>(bits * SLB + LB, cl[i]);
             }
             // bits of w' = rotr16(rho) with the sign flipped back
-            const uint4 w = make_uint4(neg_w(m.x) ^ 0x80008000u, neg_w(m.y) ^ 0x80008000u, neg_w(m.z) ^ 0x80008000u,
-                                       neg_w(m.w) ^ 0x80008000u);
+            uint32_t w[PW];
+#pragma unroll
+            for (int p = 0; p < PW; ++p) {
+              uint32_t m = cl[0][p];
+#pragma unroll
+              for (int i = 1; i < MT; ++i) m = max_u16x2(m, cl[i][p]);
+              w[p] = neg_w(m) ^ 0x80008000u;
+            }
             if (valid) {
               if (A.st_aligned) {
-                *reinterpret_cast<uint4*>(dst) = w;
+                if constexpr (UPL == 8) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1 % PW], w[2 % PW], w[3 % PW]);
+                else *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1 % PW]);
               } else {
-                const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-                for (int v = 0; v < 8; ++v) dst[v] = (uint16_t)(ww[v >> 1] >> (16 * (v & 1)));
+                for (int v = 0; v < UPL; ++v) dst[v] = (uint16_t)(w[v >> 1] >> (16 * (v & 1)));
               }
             }
           }
@@ -415,25 +428,20 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
     pdl_wait();
     pdl_trigger();
   }
-  if (GEMV && A.ctrl) {  // publish this CTA's partials to the reduce kernel
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(A.ctrl) : "memory");
-  }
   if (tl && lane == 0) {
     atomicMax(&tl[2], gtimer());
     atomicMax(&tl[3], gtimer());
   }
 }
 
-template <int MT, bool XB, int SR>
+template <int MT, bool XB, int SR, int UPL>
 __global__ void __maxnreg__(112) k_qgemv(const __grid_constant__ PArgs A) {
-  p_query<MT, true, XB, SR>(A);
+  p_query<MT, true, XB, SR, UPL>(A);
 }
 
-template <int MT>
+template <int MT, int UPL>
 __global__ void __maxnreg__(112) k_qrecon(const __grid_constant__ PArgs A) {
-  p_query<MT, false, false, 16>(A);
+  p_query<MT, false, false, 16, UPL>(A);
 }
 
 // y[r] = the fixed-order sum of row r's chunk partials: red_lanes lanes per row, lane j sums chunks
@@ -458,24 +466,7 @@ __global__ void __launch_bounds__(kPRedThreads, 8) k_qreduce(const __grid_consta
   void* const yp = Ly.y;
   const bool y_bf16 = A.y_bf16 != 0;
   asm volatile("" ::"l"(p), "l"(yp), "r"(nch), "r"((int)y_bf16) : "memory");
-  if (A.ctrl) {  // every compute CTA has published (acquire), instead of the compute grid's completion
-    if (threadIdx.x == 0) {
-      unsigned int v;
-      for (int spin = 0;; ++spin) {  // bounded: a broken handoff shows up as wrong y, never as a hang
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(A.ctrl) : "memory");
-        if (v >= (unsigned int)A.n_ctas || spin > (1 << 24)) break;
-        __nanosleep(64);  // keep the poll off the compute warps' issue slots
-      }
-      // the last reduce CTA past this point re-zeroes the counters (no compute CTA arrives any more)
-      if (atomicAdd(A.ctrl + 1, 1u) == gridDim.x - 1) {
-        A.ctrl[0] = 0u;
-        A.ctrl[1] = 0u;
-      }
-    }
-    __syncthreads();
-  } else {
-    pdl_wait();
-  }
+  pdl_wait();  // all chunk partials written (the compute grid completed)
   if (tl && threadIdx.x == 0) tl[1] = gtimer();
   float t = 0.f;
   if (r < A.rows) {
@@ -512,6 +503,7 @@ struct PackRanges {
 __global__ void k_qpack(const __grid_constant__ PackRanges R, const uint16_t* __restrict__ cells,
                         const int64_t* __restrict__ qc_off, const int32_t* __restrict__ qc_N,
                         const int64_t* __restrict__ qc_u0, const int64_t* __restrict__ qc_uend,
+                        const int32_t* __restrict__ qc_cw,
                         const int64_t* __restrict__ offsets, const int32_t* __restrict__ ncols,
                         const uint8_t* __restrict__ nrows, int64_t n_chunks, uint4* __restrict__ out) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -527,8 +519,9 @@ __global__ void k_qpack(const __grid_constant__ PackRanges R, const uint16_t* __
   }
   const int64_t local = byte - qc_off[a];
   const int32_t maxN = qc_N[a];
-  const int64_t slice = local / kQSlice;
-  const int g = (int)((local % kQSlice) / 16);
+  const int cw = qc_cw[a];  // chunk width (units): slices of 2 * cw bytes, 8 units per 16-B word
+  const int64_t slice = local / (2 * cw);
+  const int g = (int)((local % (2 * cw)) / 16);
   const int i = (int)(slice / maxN), col = (int)(slice % maxN);
   uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
@@ -578,32 +571,41 @@ int p_occupancy(const void* kern, size_t smem) {
   return occ;
 }
 
-template <int SR>
+template <int SR, int UPL>
 const void* pick_gemv(bool xb, int M) {
   if (xb) {
     switch (M) {
-      case 1: return (const void*)k_qgemv<1, true, SR>;
-      case 2: return (const void*)k_qgemv<2, true, SR>;
-      case 3: return (const void*)k_qgemv<3, true, SR>;
-      default: return (const void*)k_qgemv<4, true, SR>;
+      case 1: return (const void*)k_qgemv<1, true, SR, UPL>;
+      case 2: return (const void*)k_qgemv<2, true, SR, UPL>;
+      case 3: return (const void*)k_qgemv<3, true, SR, UPL>;
+      default: return (const void*)k_qgemv<4, true, SR, UPL>;
     }
   }
   switch (M) {
-    case 1: return (const void*)k_qgemv<1, false, SR>;
-    case 2: return (const void*)k_qgemv<2, false, SR>;
-    case 3: return (const void*)k_qgemv<3, false, SR>;
-    default: return (const void*)k_qgemv<4, false, SR>;
+    case 1: return (const void*)k_qgemv<1, false, SR, UPL>;
+    case 2: return (const void*)k_qgemv<2, false, SR, UPL>;
+    case 3: return (const void*)k_qgemv<3, false, SR, UPL>;
+    default: return (const void*)k_qgemv<4, false, SR, UPL>;
   }
 }
 
-const void* pick_kernel(bool gemv, bool xb, int M, int SR = 16) {
-  if (gemv) return SR == 4 ? pick_gemv<4>(xb, M) : SR == 8 ? pick_gemv<8>(xb, M) : pick_gemv<16>(xb, M);
+template <int UPL>
+const void* pick_recon(int M) {
   switch (M) {
-    case 1: return (const void*)k_qrecon<1>;
-    case 2: return (const void*)k_qrecon<2>;
-    case 3: return (const void*)k_qrecon<3>;
-    default: return (const void*)k_qrecon<4>;
+    case 1: return (const void*)k_qrecon<1, UPL>;
+    case 2: return (const void*)k_qrecon<2, UPL>;
+    case 3: return (const void*)k_qrecon<3, UPL>;
+    default: return (const void*)k_qrecon<4, UPL>;
   }
+}
+
+// UPL: units per lane of the layer's chunk width (qcw = 32 * UPL: 256 -> 8, 128 -> 4)
+const void* pick_kernel(bool gemv, bool xb, int M, int SR, int upl) {
+  if (gemv) {
+    if (upl == 8) return SR == 4 ? pick_gemv<4, 8>(xb, M) : SR == 8 ? pick_gemv<8, 8>(xb, M) : pick_gemv<16, 8>(xb, M);
+    return SR == 4 ? pick_gemv<4, 4>(xb, M) : SR == 8 ? pick_gemv<8, 4>(xb, M) : pick_gemv<16, 4>(xb, M);
+  }
+  return upl == 8 ? pick_recon<8>(M) : pick_recon<4>(M);
 }
 
 int partial_stride(int n_chunks) { return (n_chunks + 3) / 4 * 4; }
@@ -732,22 +734,26 @@ usk_status qlayout_geometry(usk_plan* pl) {
     LayerGeom& L = pl->layers[l];
     L.qoff = off;
     L.qchunk0 = chunk;
-    L.qchunks = (int32_t)((L.n_units + kQChunkUnits - 1) / kQChunkUnits);
     for (int64_t u = 0; u < L.n_units; u += kQGroup)
       for (int v = 1; v < kQGroup; ++v)
         if (pl->h_ncols[L.unit_begin + u + v] != pl->h_ncols[L.unit_begin + u])
           return fail(USK_EUNSUPPORTED, "query layout: a key group of layer " + std::to_string(l) +
                                             " mixes column counts (importance classes split the group)");
+    // chunk width: 256 units (8 per lane, 16-B gathers) when a chunk of the layer's widest units fits
+    // shared memory, else 128 (4 per lane, 8-B gathers; e.g. Llama-3-8B gate/up at 0.5 bpw, N = 149)
+    const int64_t smem_cap = 227 * 1024 - (kPHdr + kPRtab + 1024);
+    L.qcw = (int64_t)pl->M * L.max_ncols * 512 <= smem_cap ? 256 : 128;
+    if ((int64_t)pl->M * L.max_ncols * 2 * L.qcw > smem_cap)
+      return fail(USK_EUNSUPPORTED, "query layout: a 128-unit chunk of layer " + std::to_string(l) +
+                                        " (rows x max N x 256 B) exceeds shared memory");
+    L.qchunks = (int32_t)((L.n_units + L.qcw - 1) / L.qcw);
     for (int c = 0; c < L.qchunks; ++c) {
       int32_t mx = 1;
-      for (int64_t u = (int64_t)c * kQChunkUnits; u < std::min<int64_t>(L.n_units, (int64_t)(c + 1) * kQChunkUnits); ++u)
+      for (int64_t u = (int64_t)c * L.qcw; u < std::min<int64_t>(L.n_units, (int64_t)(c + 1) * L.qcw); ++u)
         mx = std::max(mx, pl->h_ncols[L.unit_begin + u]);
-      if ((int64_t)pl->M * mx * kQSlice + kPHdr + kPRtab + 1024 > 227 * 1024)
-        return fail(USK_EUNSUPPORTED, "query layout: a 256-unit chunk of layer " + std::to_string(l) +
-                                          " (rows x max N x 512 B) exceeds shared memory");
       pl->h_qc_off.push_back(off);
       pl->h_qc_N.push_back(mx);
-      off += (int64_t)pl->M * mx * kQSlice;
+      off += (int64_t)pl->M * mx * 2 * L.qcw;
       ++chunk;
     }
     L.qbytes = off - L.qoff;
@@ -775,19 +781,23 @@ usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const i
   usk_status s = launch_build(pl, weights, layer_ids, n, tmp, st);
   // per-chunk unit ranges (host tables, uploaded once per call through stream-ordered scratch)
   const int64_t nch = (int64_t)pl->h_qc_N.size();
-  std::vector<int64_t> u0(nch), uend(nch);
+  std::vector<int64_t> u0(nch), uend(nch), cw(nch);
   for (int l = 0; l < pl->n_layers; ++l) {
     const LayerGeom& L = pl->layers[l];
     for (int c = 0; c < L.qchunks; ++c) {
-      u0[L.qchunk0 + c] = L.unit_begin + (int64_t)c * kQChunkUnits;
+      u0[L.qchunk0 + c] = L.unit_begin + (int64_t)c * L.qcw;
       uend[L.qchunk0 + c] = L.unit_begin + L.n_units;
+      cw[L.qchunk0 + c] = L.qcw;
     }
   }
+  std::vector<int32_t> cw32(cw.begin(), cw.end());
   int64_t* d_u = nullptr;
   if (s == USK_OK) {
-    cudaError_t e = cudaMallocAsync(&d_u, sizeof(int64_t) * 2 * nch, st);
+    cudaError_t e = cudaMallocAsync(&d_u, sizeof(int64_t) * 3 * nch, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_u, u0.data(), sizeof(int64_t) * nch, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaMemcpyAsync(d_u + nch, uend.data(), sizeof(int64_t) * nch, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(d_u + 2 * nch, cw32.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the pageable host tables go out of scope
     if (e != cudaSuccess) s = cuda_fail(e, "usk_build (query layout): chunk tables");
   }
@@ -814,7 +824,8 @@ usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const i
     }
     if (R.pre[R.n] == 0) continue;
     k_qpack<<<(unsigned)((R.pre[R.n] + 255) / 256), 256, 0, st>>>(
-        R, reinterpret_cast<const uint16_t*>(tmp), pl->d_qc_off, pl->d_qc_N, d_u, d_u + nch, pl->d_offsets,
+        R, reinterpret_cast<const uint16_t*>(tmp), pl->d_qc_off, pl->d_qc_N, d_u, d_u + nch,
+        reinterpret_cast<const int32_t*>(d_u + 2 * nch), pl->d_offsets,
         pl->d_ncols, pl->d_nrows, nch, reinterpret_cast<uint4*>(sketch));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) s = cuda_fail(e, "k_qpack");
@@ -832,41 +843,35 @@ size_t qgemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, co
   return b + 256;  // + the split-K control block (two counters, left zero)
 }
 
-usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
-                              const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
-                              void* ws, cudaStream_t st) {
-  const int64_t in = pl->layers[layers[0]].in;
+// one launch pair (K4p + reduce) over layers of one chunk width; ws_of[k] = layer k's partials
+usk_status qgemv_launch(const usk_plan* pl, const void* sketch, const std::vector<int>& ks, const int32_t* layers,
+                        const int64_t* o0, const int64_t* o1, const std::vector<char*>& ws_of, const void* x,
+                        int32_t x_dtype, void* const* y, int32_t y_dtype, cudaStream_t st) {
+  const int64_t in = pl->layers[layers[ks[0]]].in;
+  const int upl = pl->layers[layers[ks[0]]].qcw / 32;
   PArgs A = p_base(pl, sketch, in);
   A.x = x;
   A.y_bf16 = y_dtype == USK_BF16;
-  char* w = reinterpret_cast<char*>(ws);
   int max_chunks = 1;
-  for (int k = 0; k < n; ++k) {
+  for (int k : ks) {
     const LayerGeom& L = pl->layers[layers[k]];
-    const int64_t rows = o1[k] - o0[k];
-    if (rows > 0) {
-      PLayer& Ly = A.layer[A.n_layers++];
-      Ly.unit_base = L.unit_begin;
-      Ly.chunk0 = L.qchunk0;
-      Ly.o_begin = o0[k];
-      Ly.rows = rows;
-      Ly.row_begin = A.rows;
-      Ly.n_chunks = L.qchunks;
-      Ly.CP = partial_stride(L.qchunks);
-      Ly.y = y[k];
-      Ly.partial = reinterpret_cast<float*>(w);
-      A.rows += rows;
-      max_chunks = std::max(max_chunks, L.qchunks);
-    }
-    w += layer_ws_bytes(L.qchunks, rows);
+    PLayer& Ly = A.layer[A.n_layers++];
+    Ly.unit_base = L.unit_begin;
+    Ly.chunk0 = L.qchunk0;
+    Ly.o_begin = o0[k];
+    Ly.rows = o1[k] - o0[k];
+    Ly.row_begin = A.rows;
+    Ly.n_chunks = L.qchunks;
+    Ly.CP = partial_stride(L.qchunks);
+    Ly.y = y[k];
+    Ly.partial = reinterpret_cast<float*>(ws_of[k]);
+    A.rows += Ly.rows;
+    max_chunks = std::max(max_chunks, L.qchunks);
   }
-  if (!A.n_layers) return USK_OK;
-  static const int poll = env_int("USK_QPOLL", 0), xpf = env_int("USK_XPF", 1);
-  A.ctrl = poll ? reinterpret_cast<unsigned int*>(w) : nullptr;  // control block after the partials
+  static const int xpf = env_int("USK_XPF", 1), forced_sr = env_int("USK_QSR", 0);
   A.x_prefetch = xpf;
   // subtile height: 16 rows; 8 when a 16-row launch gives each SM fewer than ~9 subtiles for its 16
   // warps (in-graph trace, Llama-3.2-1B o: 1.74 vs 1.99 us; q|k|v at ~10.7 per SM: 2.66 vs 2.57)
-  static const int forced_sr = env_int("USK_QSR", 0);
   int64_t items16 = 0;
   for (int k = 0; k < A.n_layers; ++k) items16 += (int64_t)A.layer[k].n_chunks * ((A.layer[k].rows + 15) / 16);
   const int SR = forced_sr ? forced_sr : (items16 < 9 * (int64_t)device_sm_count() ? 8 : 16);
@@ -877,7 +882,7 @@ usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int3
     Ly.item_begin = A.items;
     A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
   }
-  const void* kern = pick_kernel(true, x_dtype == USK_BF16, pl->M, SR);
+  const void* kern = pick_kernel(true, x_dtype == USK_BF16, pl->M, SR, upl);
   int grid = 0;
   size_t smem = 0;
   usk_status s = p_prepare(pl, A, kern, true, grid, smem, SR);
@@ -891,6 +896,28 @@ usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int3
   const int rgrid = (int)((A.rows * A.red_lanes + kPRedThreads - 1) / kPRedThreads);
   A.timeline = trace_slot(rgrid);
   return p_launch((const void*)k_qreduce, A, rgrid, kPRedThreads, 0, st);
+}
+
+usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
+                              const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
+                              void* ws, cudaStream_t st) {
+  // workspace: the layers' partials in call order (qgemv_batch_workspace_bytes); layers of the two
+  // chunk widths (256 / 128 units) run as separate launch pairs
+  std::vector<char*> ws_of(n);
+  char* w = reinterpret_cast<char*>(ws);
+  std::vector<int> by[2];
+  for (int k = 0; k < n; ++k) {
+    const LayerGeom& L = pl->layers[layers[k]];
+    ws_of[k] = w;
+    w += layer_ws_bytes(L.qchunks, o1[k] - o0[k]);
+    if (o1[k] > o0[k]) by[L.qcw == 256 ? 0 : 1].push_back(k);
+  }
+  for (auto& ks : by) {
+    if (ks.empty()) continue;
+    usk_status s = qgemv_launch(pl, sketch, ks, layers, o0, o1, ws_of, x, x_dtype, y, y_dtype, st);
+    if (s != USK_OK) return s;
+  }
+  return USK_OK;
 }
 
 usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t l, int64_t r0, int64_t r1, void* w_out,
@@ -911,7 +938,7 @@ usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t l
   A.items = (int64_t)Ly.n_chunks * Ly.n_sub;
   A.rows = rows;
   A.st_aligned = (ld % 8 == 0) && (reinterpret_cast<uintptr_t>(w_out) % 16 == 0);
-  const void* kern = pick_kernel(false, false, pl->M);
+  const void* kern = pick_kernel(false, false, pl->M, 16, L.qcw / 32);
   int grid = 0;
   size_t smem = 0;
   usk_status s = p_prepare(pl, A, kern, false, grid, smem);

@@ -60,7 +60,8 @@ class _LayerInfo(ct.Structure):
                 ("n_units", ct.c_int64), ("cell_begin", ct.c_int64), ("n_cells", ct.c_int64),
                 ("budget_bits", ct.c_int64), ("meta_bits", ct.c_int64), ("cells_T", ct.c_int64),
                 ("achieved_bits", ct.c_int64), ("n_outliers", ct.c_int64), ("outlier_offset", ct.c_int64),
-                ("qbyte_begin", ct.c_int64), ("qbytes", ct.c_int64)]
+                ("qbyte_begin", ct.c_int64), ("qbytes", ct.c_int64), ("qchunk_units", ct.c_int32),
+                ("reserved", ct.c_int32)]
 
 
 def _load():
@@ -162,6 +163,8 @@ class LayerInfo:
     outlier_offset: int = 0
     qbyte_begin: int = 0
     qbytes: int = 0
+    qchunk_units: int = 0
+    reserved: int = 0
 
 
 class Plan:

@@ -8,7 +8,11 @@ cell (i, c) of unit 256 k + 8 g + v as rho16 = ((b << 1) | (b >> 15)) ^ 1 (b = b
 unit does not exist, c >= N_u or i >= M_u."""
 import numpy as np
 
-CHUNK = 256
+SMEM_CAP = 227 * 1024 - (64 + 16 * 16 * 16 + 1024)  # the header's shared-memory budget for a chunk
+
+
+def chunk_width(ncols, rows):
+    return 256 if rows * int(max(ncols)) * 512 <= SMEM_CAP else 128
 
 
 def rho16(b):
@@ -22,10 +26,11 @@ def unrho16(r):
 
 
 def layer_geometry(ncols, rows):
-    """(chunk maxN list, chunk byte sizes) of one layer from its per-unit N."""
+    """(chunk maxN list, chunk byte sizes, chunk width) of one layer from its per-unit N."""
     n = len(ncols)
-    mx = [int(max(ncols[k:k + CHUNK])) for k in range(0, n, CHUNK)]
-    return mx, [rows * m * 512 for m in mx]
+    cw = chunk_width(ncols, rows)
+    mx = [int(max(ncols[k:k + cw])) for k in range(0, n, cw)]
+    return mx, [rows * m * 2 * cw for m in mx], cw
 
 
 def model_offsets(ncols_per_layer, rows):
@@ -38,36 +43,36 @@ def model_offsets(ncols_per_layer, rows):
 
 def pack_layer(cells_u16, offsets, ncols, nrows, rows):
     """Unit-major cells of ONE layer (offsets relative to the array) -> the layer's query bytes (uint16)."""
-    mx, sizes = layer_geometry(ncols, rows)
+    mx, sizes, cw = layer_geometry(ncols, rows)
     out = np.zeros(sum(sizes) // 2, np.uint16)
     base = 0
     n = len(ncols)
     for k, m in enumerate(mx):
-        words = out[base // 2:(base + sizes[k]) // 2].reshape(rows, m, 32, 8)
-        for u in range(k * CHUNK, min(n, (k + 1) * CHUNK)):
-            g, v = (u - k * CHUNK) // 8, (u - k * CHUNK) % 8
+        words = out[base // 2:(base + sizes[k]) // 2].reshape(rows, m, cw)
+        for u in range(k * cw, min(n, (k + 1) * cw)):
+            t = u - k * cw
             N, M = int(ncols[u]), int(nrows[u])
             c = cells_u16[offsets[u]:offsets[u] + M * N].reshape(M, N)
-            words[:M, :N, g, v] = rho16(c)
+            words[:M, :N, t] = rho16(c)
         base += sizes[k]
     return out
 
 
 def unpack_layer(q_u16, offsets, ncols, nrows, rows):
     """Inverse of pack_layer: the unit-major cells of the layer (and whether the padding is 0)."""
-    mx, sizes = layer_geometry(ncols, rows)
+    mx, sizes, cw = layer_geometry(ncols, rows)
     n = len(ncols)
     cells = np.zeros(int(offsets[n] - offsets[0]), np.uint16)
     pad_ok = True
     base = 0
     for k, m in enumerate(mx):
-        words = q_u16[base // 2:(base + sizes[k]) // 2].reshape(rows, m, 32, 8)
+        words = q_u16[base // 2:(base + sizes[k]) // 2].reshape(rows, m, cw)
         seen = np.zeros(words.shape, bool)
-        for u in range(k * CHUNK, min(n, (k + 1) * CHUNK)):
-            g, v = (u - k * CHUNK) // 8, (u - k * CHUNK) % 8
+        for u in range(k * cw, min(n, (k + 1) * cw)):
+            t = u - k * cw
             N, M = int(ncols[u]), int(nrows[u])
-            cells[offsets[u] - offsets[0]:offsets[u] - offsets[0] + M * N] = unrho16(words[:M, :N, g, v]).reshape(-1)
-            seen[:M, :N, g, v] = True
+            cells[offsets[u] - offsets[0]:offsets[u] - offsets[0] + M * N] = unrho16(words[:M, :N, t]).reshape(-1)
+            seen[:M, :N, t] = True
         pad_ok &= bool((words[~seen] == 0).all())
         base += sizes[k]
     return cells, pad_ok
@@ -75,10 +80,9 @@ def unpack_layer(q_u16, offsets, ncols, nrows, rows):
 
 def unit_cells(q_u16, ncols, nrows, t, rows):
     """Unit-major cells (M_u * N_u, row-major) of unit t of a layer from the layer's query bytes."""
-    mx, sizes = layer_geometry(ncols, rows)
-    k = t // CHUNK
+    mx, sizes, cw = layer_geometry(ncols, rows)
+    k = t // cw
     base = sum(sizes[:k])
-    words = q_u16[base // 2:(base + sizes[k]) // 2].reshape(rows, mx[k], 32, 8)
-    g, v = (t - k * CHUNK) // 8, (t - k * CHUNK) % 8
+    words = q_u16[base // 2:(base + sizes[k]) // 2].reshape(rows, mx[k], cw)
     N, M = int(ncols[t]), int(nrows[t])
-    return unrho16(words[:M, :N, g, v]).reshape(-1)
+    return unrho16(words[:M, :N, t - k * cw]).reshape(-1)

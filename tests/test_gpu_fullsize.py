@@ -298,24 +298,33 @@ def test_c4_query_prefill_16384_tokens(orc, usk, k):
 
 
 def test_c5_query_llama8b_block(orc, usk):
-    """Llama-3-8B block on the query layout: q, k, v, o and the 14336-wide down (56 chunks), sampled
-    units and rows.  gate/up ([14336, 4096], N = 149 at 0.5 bpw: 3 x 149 x 512 B = 229 KB per 256-unit
-    chunk) exceed shared memory and are rejected with USK_EUNSUPPORTED (usk.h)."""
-    full = synth.llama3_8b_shapes()[:7]
-    with pytest.raises(usk.UskError) as e:
-        usk.plan_allocation(full, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query")
-    assert e.value.status == usk.EUNSUPPORTED
-    shapes = [full[k] for k in (0, 1, 2, 3, 6)]
+    """Llama-3-8B block on the query layout: gate/up ([14336, 4096], N = 149 at 0.5 bpw: a 256-unit
+    chunk would take 229 KB) use 128-unit chunks (usk.h), the others 256; the 14336-wide down has 56
+    chunks.  Sampled units and rows of q, gate and down."""
+    shapes = synth.llama3_8b_shapes()[:7]
     pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query")
+    assert [pl.layers[l].qchunk_units for l in range(7)] == [256, 256, 256, 256, 128, 128, 256]
     opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED, hash_kind=orc.HASH_XG)
     sk = pl.new_sketch()
     ws = [synth.torch_weights_bf16(o, i, synth.seed_for(5, 0, l), "cuda") for l, (o, i) in enumerate(shapes)]
     usk.build(pl, ws, sk)
     usk.check(pl)
     rng = np.random.default_rng(13)
-    for l in (0, 3, 4):
+    for l in (0, 4, 6):
         _query_units(orc, usk, pl, opl, sk, l, ws[l], 4, rng)
-    l = 4
+    g = [4, 5]  # gate|up: the 128-unit chunk kernels, one grouped call
+    x = synth.torch_vector(4096, 12, "cuda", torch.bfloat16)[0]
+    ys = [torch.empty(14336, dtype=torch.float32, device="cuda") for _ in g]
+    usk.linear_batch(pl, sk, g, x, ys, usk.new_batch_workspace(pl, g))
+    x64 = synth.bf16_bits_to_f32(host_bits(x)).astype(np.float64)
+    for l, yv in zip(g, ys):
+        osk = np.zeros(opl.total_cells, np.uint16)
+        orc.build_layer(opl, l, host_bits(ws[l]), osk)
+        for r0 in (0, 7000, 14336 - 8):
+            y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 8)[0]
+            W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, r0, r0 + 8), orc.BF16).reshape(8, 4096)
+            assert gemv_err(yv.cpu().numpy()[r0:r0 + 8].astype(np.float64), y64, x64, W64) <= 1e-5
+    l = 6
     o, i = shapes[l]
     x = synth.torch_vector(i, 11, "cuda", torch.bfloat16)
     y = torch.empty((1, o), dtype=torch.float32, device="cuda")

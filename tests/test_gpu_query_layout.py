@@ -55,8 +55,9 @@ SHAPES = [
     [(200, 72), (49, 72)],                  # one partial chunk (9 key groups)
     [(130, 264)],                           # a full chunk + a 1-group chunk
     [(2048, 512), (512, 512), (8192, 256)], # Llama-like N = 21, 5, 85
+    [(8192, 264), (96, 264)],               # N = 170: 128-unit chunks (ld.shared.v2 kernels)
 ]
-BPW = {0: 0.5, 1: 1.0, 2: 0.5, 3: 0.5}
+BPW = {0: 0.5, 1: 1.0, 2: 0.5, 3: 0.5, 4: 1.0}
 
 
 @pytest.mark.parametrize("shapes", SHAPES, ids=[str(s[0]) for s in SHAPES])

@@ -16,8 +16,8 @@ def test_pack_unpack_roundtrip(orc):
         u0, u1 = opl.layer_units(l)
         offs = opl.offsets[u0:u1 + 1]
         q = qlayout.pack_layer(sk[offs[0]:], offs - offs[0], opl.ncols[u0:u1], opl.nrows[u0:u1], 3)
-        mx, sizes = qlayout.layer_geometry(opl.ncols[u0:u1], 3)
-        assert q.size * 2 == sum(sizes) and len(mx) == (i + 255) // 256
+        mx, sizes, cw = qlayout.layer_geometry(opl.ncols[u0:u1], 3)
+        assert q.size * 2 == sum(sizes) and len(mx) == (i + cw - 1) // cw
         cells, pad_ok = qlayout.unpack_layer(q, offs, opl.ncols[u0:u1], opl.nrows[u0:u1], 3)
         np.testing.assert_array_equal(cells, sk[offs[0]:offs[-1]])
         assert pad_ok
