@@ -32,7 +32,13 @@
 namespace usk {
 namespace {
 
-constexpr int kPThreads = 512;
+#ifndef USK_QTHREADS
+#define USK_QTHREADS 512
+#endif
+#ifndef USK_QMAXREG
+#define USK_QMAXREG 112  // K4p / K3p (<= 96 used) + k_qreduce (256 x 32) share an SM's 64 K registers
+#endif
+constexpr int kPThreads = USK_QTHREADS;
 constexpr int kPWarps = kPThreads / 32;
 constexpr int kPSub = 16;          // output rows per warp work item (subtile)
 constexpr int kPMaxLayers = 8;
@@ -435,12 +441,12 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
 }
 
 template <int MT, bool XB, int SR, int UPL>
-__global__ void __maxnreg__(112) k_qgemv(const __grid_constant__ PArgs A) {
+__global__ void __maxnreg__(USK_QMAXREG) k_qgemv(const __grid_constant__ PArgs A) {
   p_query<MT, true, XB, SR, UPL>(A);
 }
 
 template <int MT, int UPL>
-__global__ void __maxnreg__(112) k_qrecon(const __grid_constant__ PArgs A) {
+__global__ void __maxnreg__(USK_QMAXREG) k_qrecon(const __grid_constant__ PArgs A) {
   p_query<MT, false, false, 16, UPL>(A);
 }
 
