@@ -289,6 +289,11 @@ def run_usk(args):
 
     group_of = {l: gi for gi, g in enumerate(groups) for l in g}
 
+    peer_bufs = None
+    if world > 1 and args.collective == "peer":  # fused y all-gather in the reduce kernel (symmetric memory)
+        peer_bufs = udist.PeerYBuffers(usk, [[shapes[l][0] for l in g] for g in groups], dev)
+        ws_peer = [usk.new_batch_workspace(plan, g, [ranges[l] for l in g], device=dev) for g in groups]
+
     def gather(ls):  # one all-gather per grouped call (per linear for the 112-launch variant)
         if world > 1:
             gi = group_of[ls[0]]
@@ -307,6 +312,11 @@ def run_usk(args):
         for gi, g in enumerate(groups):
             if args.prefetch_next and gi + 1 < len(groups):  # L2 hint: the next group's sketch + metadata
                 usk.prefetch_l2(plan, sketch, groups[gi + 1][0], groups[gi + 1][-1] + 1)
+            if peer_bufs is not None:
+                usk.linear_batch_peers(plan, sketch, g, xg[gi], peer_bufs.peers(gi), ws_peer[gi],
+                                       ranges=[ranges[l] for l in g])
+                usk.peer_wait(plan, peer_bufs.peers(gi))
+                continue
             usk.linear_batch(plan, sketch, g, xg[gi], [out_of(l) for l in g], ws_group[gi],
                              ranges=[ranges[l] for l in g])
             gather(g)
@@ -380,6 +390,8 @@ def run_usk(args):
     def full_y():  # the step's outputs in layer order (N > 1: assembled from the gathered buffers)
         if world == 1:
             return Y.clone()
+        if peer_bufs is not None:
+            return torch.cat([t for yg in peer_bufs.y for t in yg])
         ys = []
         for gi, g in enumerate(groups):
             ys += udist.assemble_group(Gfull[gi], [shapes[l][0] for l in g], world)
@@ -467,7 +479,7 @@ def run_usk(args):
 
     # ---- end-to-end through the binding: pinned host x -> device, 112 linears, y -> pinned host
     Xh = X.cpu().pin_memory()
-    Yout = Y if world == 1 else GF                       # what the step leaves on the device
+    Yout = Y if world == 1 else (peer_bufs.yflat if peer_bufs is not None else GF)  # what the step leaves
     Yh = torch.empty(Yout.numel(), dtype=torch.float32).pin_memory()
     g2 = torch.cuda.CUDAGraph()
     e2e_graph = True
@@ -706,8 +718,10 @@ def run_usk(args):
             "config": {"workload": "c3: Llama-3.2-1B all 112 linears, batch-1 decode via fused sketch-GEMV",
                        "bpw": BPW, "rows": ROWS, "granularity": "row (1 input dim per unit)", "classes": 1,
                        "sketch_MB": sketch_bytes / 1e6, "weights": numel, "l2": "flushed (256 MB write) before each step",
-                       "parallelism": (f"output-sharded x{world}, one NCCL all-gather per grouped call "
-                                       f"({len(groups)} per token, in the graph)") if world > 1 else "single GPU",
+                       "parallelism": ((f"output-sharded x{world}, one NCCL all-gather per grouped call "
+                                        f"({len(groups)} per token, in the graph)") if args.collective == "nccl" else
+                                       (f"output-sharded x{world}, y all-gather fused into the reduce kernel "
+                                        f"(NVLink peer stores + flags, symmetric memory)")) if world > 1 else "single GPU",
                        "graph": use_graph, "launches_per_step": launches_per_step,
                        "grouping": "q|k|v, o, gate|up, down per block share x (usk_linear_batch)"},
             "per_linear_launches": {"ms_per_step": ms_single, "tokens_per_s": 1000.0 / ms_single,
@@ -844,6 +858,9 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-step-s", type=float, default=None, help="--impl reference: oracle seconds per step")
     ap.add_argument("--no-q4", action="store_true", help="skip the extra plans (q4 states, classes, output-row units)")
+    ap.add_argument("--collective", default="nccl", choices=["nccl", "peer"],
+                    help="N > 1 y exchange: one NCCL all-gather per grouped call (default), or the fused peer-store "
+                         "epilogue of the reduce kernel over symmetric memory (usk_linear_batch_peers; query layout)")
     ap.add_argument("--layout", default="query", choices=["query", "unit_major"],
                     help="headline plan: query layout + USK-XG keys (default) or the unit-major USK-X plan")
     ap.add_argument("--no-8b", action="store_true", help="skip the Llama-3-8B (config 5) build + decode at N=1")

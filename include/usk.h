@@ -310,6 +310,35 @@ USK_API usk_status usk_linear_batch(const usk_plan* plan, const void* sketch, co
                                     void* const* y, int32_t y_dtype, void* workspace,
                                     size_t workspace_bytes, usk_stream stream);
 
+/* Output-sharded decode with the y all-gather fused into the split-K reduction (SURVEY 8(e),
+ * north star "each linear's output features are sharded for inference"; B200-native collective in
+ * place of an NCCL all-gather).  Rank my_rank of n_peers computes rows [ranges[2k], ranges[2k+1])
+ * of each layer as usk_linear_batch does (query-layout plans), but its reduce kernel stores every
+ * row at its GLOBAL position o in the full y of EVERY rank (y_peer: device pointers of the peers'
+ * buffers mapped into this process -- CUDA IPC / symmetric memory over NVLink), then raises this
+ * rank's flag sig_peer[p][my_rank] = *epoch + 1 in every rank's signal array (system-scope release
+ * after all of its rows are visible).  usk_peer_wait, enqueued by each rank after its call, waits
+ * (acquire) until all n_peers flags of its own signal array reach *epoch + 1 and advances *epoch:
+ * then every rank's full y holds every rank's rows.  Graph-replayable (the epoch lives on the device).
+ *   peers: host struct; y_peer host array [n_peers * n] (y_peer[p * n + k] = rank p's full y of
+ *          layers[k], out_features elements of y_dtype, 16-B aligned); sig_peer host array [n_peers]
+ *          of device uint32[n_peers] arrays (zero-filled before first use); epoch: device uint32, the
+ *          same value on every rank (0 at first use).
+ * Layers of one call must share the query layout's chunk width (USK_EUNSUPPORTED otherwise).  The
+ * spin of usk_peer_wait is bounded: a peer that never signals is reported by usk_check (USK_ECUDA). */
+typedef struct {
+  int32_t n_peers;            /* ranks P in [1, 8] */
+  int32_t my_rank;
+  void* const* y_peer;        /* host [P * n] device pointers */
+  uint32_t* const* sig_peer;  /* host [P] device pointers */
+  uint32_t* epoch;            /* device uint32 */
+} usk_peers;
+USK_API usk_status usk_linear_batch_peers(const usk_plan* plan, const void* sketch, const int32_t* layers,
+                                          const int64_t* ranges, int32_t n, const void* x, int32_t x_dtype,
+                                          int32_t y_dtype, const usk_peers* peers, void* workspace,
+                                          size_t workspace_bytes, usk_stream stream);
+USK_API usk_status usk_peer_wait(const usk_plan* plan, const usk_peers* peers, usk_stream stream);
+
 /* Aggregated-gradient baseline of finetuning (§3.3, Figure 4a; SPEC.md
  * aggregated_backward): the gradient of a shared sketch state is the sum of the gradients of the
  * weights mapped to it.  For every weight (o, j) of `layer` and every sketch row i,

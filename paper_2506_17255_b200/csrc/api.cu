@@ -589,6 +589,41 @@ usk_status usk_linear_batch(const usk_plan* pl, const void* sketch, const int32_
                            (cudaStream_t)stream);
 }
 
+usk_status usk_linear_batch_peers(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* ranges,
+                                  int32_t n, const void* x, int32_t x_dtype, int32_t y_dtype, const usk_peers* peers,
+                                  void* workspace, size_t workspace_bytes, usk_stream stream) {
+  std::vector<int64_t> o0, o1;
+  usk_status s = batch_ranges(pl, layers, ranges, n, o0, o1);
+  if (s != USK_OK) return s;
+  if (!peers || !sketch || !x || !workspace || !peers->y_peer || !peers->sig_peer || !peers->epoch)
+    return fail(USK_EINVAL, "usk_linear_batch_peers: null pointer");
+  if (pl->layout != USK_LAYOUT_QUERY) return fail(USK_EUNSUPPORTED, "usk_linear_batch_peers: query-layout plans only");
+  if (peers->n_peers < 1 || peers->n_peers > 8 || peers->my_rank < 0 || peers->my_rank >= peers->n_peers)
+    return fail(USK_EINVAL, "usk_linear_batch_peers: n_peers in [1, 8], 0 <= my_rank < n_peers");
+  if (x_dtype != USK_F32 && x_dtype != USK_BF16) return fail(USK_EINVAL, "usk_linear_batch_peers: x_dtype");
+  if (y_dtype != USK_F32 && y_dtype != USK_BF16) return fail(USK_EINVAL, "usk_linear_batch_peers: y_dtype");
+  if (!aligned16(x) || !aligned16(sketch) || !aligned16(workspace))
+    return fail(USK_EINVAL, "usk_linear_batch_peers: 16-B alignment");
+  for (int q = 0; q < peers->n_peers; ++q) {
+    if (!peers->sig_peer[q]) return fail(USK_EINVAL, "usk_linear_batch_peers: null signal pointer");
+    for (int k = 0; k < n; ++k)
+      if (!peers->y_peer[(size_t)q * n + k]) return fail(USK_EINVAL, "usk_linear_batch_peers: null y pointer");
+  }
+  if (workspace_bytes < qgemv_batch_workspace_bytes(pl, layers, o0.data(), o1.data(), n))
+    return fail(USK_ESHAPE, "usk_linear_batch_peers: workspace too small");
+  std::vector<void*> ymine(n);
+  for (int k = 0; k < n; ++k) ymine[k] = peers->y_peer[(size_t)peers->my_rank * n + k];
+  return launch_qgemv_batch(pl, sketch, layers, o0.data(), o1.data(), n, x, x_dtype, ymine.data(), y_dtype, workspace,
+                            (cudaStream_t)stream, peers);
+}
+
+usk_status usk_peer_wait(const usk_plan* pl, const usk_peers* peers, usk_stream stream) {
+  if (!pl || !peers || !peers->sig_peer || !peers->epoch) return fail(USK_EINVAL, "usk_peer_wait: null pointer");
+  if (peers->n_peers < 1 || peers->n_peers > 8 || peers->my_rank < 0 || peers->my_rank >= peers->n_peers)
+    return fail(USK_EINVAL, "usk_peer_wait: n_peers in [1, 8], 0 <= my_rank < n_peers");
+  return launch_peer_wait(pl, peers, (cudaStream_t)stream);
+}
+
 usk_status usk_check(const usk_plan* pl, usk_stream stream) {
   if (!pl) return fail(USK_EINVAL, "usk_check: null plan");
   USK_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
@@ -597,6 +632,7 @@ usk_status usk_check(const usk_plan* pl, usk_stream stream) {
   if (h) {
     USK_CUDA(cudaMemset(pl->d_err, 0, sizeof(int)));
     if (h & 1) return fail(USK_ENONFINITE, "a build or aggregation saw NaN or Inf values");
+    if (h & 4) return fail(USK_ECUDA, "usk_peer_wait: a peer rank never raised its flag (bounded spin expired)");
     return fail(USK_ERANGE, "a value of |v| >= 2^15 reached the 2^-48 fixed-point sums (CountMin / usk_aggregate_grad)");
   }
   return USK_OK;

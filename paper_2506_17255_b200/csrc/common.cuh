@@ -233,7 +233,8 @@ size_t qgemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, co
                                    int n);
 usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
                               const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
-                              void* ws, cudaStream_t st);
+                              void* ws, cudaStream_t st, const usk_peers* peers = nullptr);
+usk_status launch_peer_wait(const usk_plan* pl, const usk_peers* peers, cudaStream_t st);
 usk_status launch_gemv_outrow(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
                               const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
                               cudaStream_t st);

@@ -48,6 +48,7 @@ constexpr int kPRedThreads = 256;
 constexpr int kPHdr = 64;          // [2 mbarriers][s_next][pad]
 constexpr int kPRtab = kPWarps * kPSub * 16;  // per warp: 16 rows x {R_0..R_3}
 constexpr int kPTS = 8;            // USK_TRACE stamps per CTA
+constexpr int kPMaxPeers = 8;      // ranks of a fused y all-gather (one NVLink domain of B200s)
 
 extern __shared__ __align__(16) unsigned char psm[];
 
@@ -87,6 +88,14 @@ struct PArgs {
   uint64_t first_off[kPMaxCtas];   // CTA c's first bulk copy (host-computed: no dependent load)
   uint32_t first_bytes[kPMaxCtas];
   unsigned long long* timeline;    // tuning only (USK_TRACE)
+  // fused y all-gather of an output-sharded decode (usk_linear_batch_peers): the reduce
+  // kernel stores every row into the full y of each of the n_peers ranks (peer-mapped pointers), and
+  // its last CTA raises this rank's flag in every rank's signal array to epoch + 1
+  int32_t n_peers, my_rank;
+  void* ypeer[kPMaxPeers][kPMaxLayers];  // [p][layer of the launch] -> rank p's full y of that layer
+  uint32_t* sig[kPMaxPeers];             // rank p's signal array (uint32[n_peers])
+  const uint32_t* epoch;                 // this rank's call counter (advanced by usk_peer_wait)
+  unsigned int* done;                    // CTA arrival counter (workspace; left zero)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -486,17 +495,65 @@ __global__ void __launch_bounds__(kPRedThreads, 8) k_qreduce(const __grid_consta
   }
   for (int m = 1; m < L; m <<= 1) t += __shfl_xor_sync(0xffffffffu, t, m);
   if (r < A.rows && j == 0) {
-    if (y_bf16) {
-      const uint32_t bb = __float_as_uint(t);
-      reinterpret_cast<uint16_t*>(yp)[rr] = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
-    } else {
-      reinterpret_cast<float*>(yp)[rr] = t;
+    const uint32_t bb = __float_as_uint(t);
+    const uint16_t hb = (uint16_t)((bb + 0x7FFFu + ((bb >> 16) & 1u)) >> 16);
+    if (A.n_peers == 0) {
+      if (y_bf16) reinterpret_cast<uint16_t*>(yp)[rr] = hb;
+      else reinterpret_cast<float*>(yp)[rr] = t;
+    } else {  // the row at its global position in every rank's full y (NVLink peer stores)
+      const int64_t o = Ly.o_begin + rr;
+      for (int q = 0; q < A.n_peers; ++q) {
+        void* yq = A.ypeer[q][li];
+        if (y_bf16) reinterpret_cast<uint16_t*>(yq)[o] = hb;
+        else reinterpret_cast<float*>(yq)[o] = t;
+      }
+    }
+  }
+  if (A.n_peers) {
+    // publish: every CTA's peer stores are system-visible before its arrival; the last CTA to arrive
+    // (it observed every arrival) raises this rank's flag in each rank's signal array
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned int prev = atomicAdd(A.done, 1u);
+      if (prev == gridDim.x - 1) {
+        __threadfence_system();
+        const uint32_t e = *reinterpret_cast<const volatile uint32_t*>(A.epoch) + 1u;
+        for (int q = 0; q < A.n_peers; ++q)
+          asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(A.sig[q] + A.my_rank), "r"(e) : "memory");
+        *A.done = 0u;
+      }
     }
   }
   if (tl && (threadIdx.x & 31) == 0) {
     atomicMax(&tl[2], gtimer());
     atomicMax(&tl[3], gtimer());
   }
+}
+
+// usk_peer_wait: thread q < n_peers spins (acquire, system scope) until rank q's flag in this rank's
+// signal array reaches epoch + 1, then the epoch advances.  Bounded: a peer that never signals leaves
+// the flag short and sets err (reported by usk_check) instead of hanging the GPU.
+__global__ void k_peer_wait(const uint32_t* sig, int32_t n_peers, uint32_t* epoch, int* err) {
+  pdl_wait();
+  const uint32_t want = *reinterpret_cast<const volatile uint32_t*>(epoch) + 1u;
+  bool ok = true;
+  if ((int)threadIdx.x < n_peers) {
+    uint32_t v = 0;
+    for (long spin = 0;; ++spin) {
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(sig + threadIdx.x) : "memory");
+      if ((int32_t)(v - want) >= 0) break;
+      if (spin > (1L << 24)) {
+        ok = false;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  if (!ok) atomicOr(err, 4);  // a peer never signalled (usk_check: USK_ECUDA)
+  __syncthreads();
+  if (threadIdx.x == 0) *epoch = want;
+  pdl_trigger();
 }
 
 // Unit-major cells -> query layout, one thread per 16-byte word (8 cells of a key group).  `ranges`:
@@ -852,7 +909,8 @@ size_t qgemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, co
 // one launch pair (K4p + reduce) over layers of one chunk width; ws_of[k] = layer k's partials
 usk_status qgemv_launch(const usk_plan* pl, const void* sketch, const std::vector<int>& ks, const int32_t* layers,
                         const int64_t* o0, const int64_t* o1, const std::vector<char*>& ws_of, const void* x,
-                        int32_t x_dtype, void* const* y, int32_t y_dtype, cudaStream_t st) {
+                        int32_t x_dtype, void* const* y, int32_t y_dtype, cudaStream_t st,
+                        const usk_peers* peers = nullptr, int n = 0, unsigned int* done = nullptr) {
   const int64_t in = pl->layers[layers[ks[0]]].in;
   const int upl = pl->layers[layers[ks[0]]].qcw / 32;
   PArgs A = p_base(pl, sketch, in);
@@ -898,6 +956,16 @@ usk_status qgemv_launch(const usk_plan* pl, const void* sketch, const std::vecto
   while (A.red_lanes < 32 && 4 * A.red_lanes < max_chunks) A.red_lanes *= 2;
   s = p_launch(kern, A, grid, kPThreads, smem, st);
   if (s != USK_OK) return s;
+  if (peers) {
+    A.n_peers = peers->n_peers;
+    A.my_rank = peers->my_rank;
+    for (int q = 0; q < peers->n_peers; ++q) {
+      for (int k = 0; k < (int)ks.size(); ++k) A.ypeer[q][k] = peers->y_peer[(size_t)q * n + ks[k]];
+      A.sig[q] = peers->sig_peer[q];
+    }
+    A.epoch = peers->epoch;
+    A.done = done;
+  }
   (void)ensure_func_attr((const void*)k_qreduce, (int)cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   const int rgrid = (int)((A.rows * A.red_lanes + kPRedThreads - 1) / kPRedThreads);
   A.timeline = trace_slot(rgrid);
@@ -906,7 +974,7 @@ usk_status qgemv_launch(const usk_plan* pl, const void* sketch, const std::vecto
 
 usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
                               const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
-                              void* ws, cudaStream_t st) {
+                              void* ws, cudaStream_t st, const usk_peers* peers) {
   // workspace: the layers' partials in call order (qgemv_batch_workspace_bytes); layers of the two
   // chunk widths (256 / 128 units) run as separate launch pairs
   std::vector<char*> ws_of(n);
@@ -918,11 +986,30 @@ usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int3
     w += layer_ws_bytes(L.qchunks, o1[k] - o0[k]);
     if (o1[k] > o0[k]) by[L.qcw == 256 ? 0 : 1].push_back(k);
   }
+  if (peers && !by[0].empty() && !by[1].empty())  // one flag per call: one launch pair
+    return fail(USK_EUNSUPPORTED, "usk_linear_batch_peers: layers of both chunk widths in one call");
+  unsigned int* done = reinterpret_cast<unsigned int*>(w);  // control block after the partials
   for (auto& ks : by) {
     if (ks.empty()) continue;
-    usk_status s = qgemv_launch(pl, sketch, ks, layers, o0, o1, ws_of, x, x_dtype, y, y_dtype, st);
+    usk_status s = qgemv_launch(pl, sketch, ks, layers, o0, o1, ws_of, x, x_dtype, y, y_dtype, st, peers, n, done);
     if (s != USK_OK) return s;
   }
+  return USK_OK;
+}
+
+usk_status launch_peer_wait(const usk_plan* pl, const usk_peers* peers, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(32);
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  USK_CUDA(cudaLaunchKernelEx(&cfg, k_peer_wait, (const uint32_t*)peers->sig_peer[peers->my_rank], peers->n_peers,
+                              peers->epoch, pl->d_err));
+  count_launch();
   return USK_OK;
 }
 

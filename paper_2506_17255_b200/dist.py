@@ -110,3 +110,47 @@ def assemble_group(gathered, out_features, world: int):
             pieces.append(parts[r, off:off + (o1 - o0)])
         ys.append(torch.cat(pieces))
     return ys
+
+
+# ---- fused y all-gather (usk_linear_batch_peers): the split-K reduce kernel of each rank
+#      stores its rows straight into every rank's full y over NVLink and raises a flag; usk_peer_wait
+#      completes the exchange.  The peer buffers come from torch symmetric memory (one rendezvous).
+def peer_layout(group_out_features):
+    """Byte layout of the symmetric buffer: every grouped call's full fp32 y (256-B aligned pieces, in
+    call order), then one int32 signal array.  Returns (per-call offsets, signal offset, total bytes)."""
+    offs, off = [], 0
+    for outs in group_out_features:
+        o = []
+        for n_out in outs:
+            o.append(off)
+            off += (n_out * 4 + 255) // 256 * 256
+        offs.append(o)
+    return offs, off, off + 256
+
+
+class PeerYBuffers:
+    """Every grouped call's full-y buffers (fp32) and one signal array (int32[world]) in ONE symmetric-
+    memory allocation, mapped on every rank; `peers(gi)` is the usk.Peers of grouped call gi."""
+
+    def __init__(self, usk, group_out_features, device, group=None):
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        self.world = dist.get_world_size(group)
+        self.rank = dist.get_rank(group)
+        offs, sig_off, total = peer_layout(group_out_features)
+        self.buf = symm_mem.empty(total, dtype=torch.uint8, device=device)
+        self.buf.zero_()
+        self.handle = symm_mem.rendezvous(self.buf, group if group is not None else dist.group.WORLD)
+        ptrs = [int(p) for p in self.handle.buffer_ptrs]
+        self.epoch = torch.zeros(1, dtype=torch.int32, device=device)
+        self.y = [[self.buf[a:a + n * 4].view(torch.float32) for a, n in zip(o, outs)]
+                  for o, outs in zip(offs, group_out_features)]
+        self.yflat = self.buf[:sig_off].view(torch.float32)  # every full y (256-B aligned pieces)
+        self._peers = [usk.Peers(self.world, self.rank, [[p + a for a in o] for p in ptrs], [p + sig_off for p in ptrs],
+                                 self.epoch) for o in offs]
+        torch.cuda.synchronize(device)
+        dist.barrier(group)  # every rank's signal array is zero before the first flag
+
+    def peers(self, gi: int):
+        return self._peers[gi]

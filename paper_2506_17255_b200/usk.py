@@ -94,6 +94,8 @@ def _load():
         "usk_stats": (i32, [p, p, i32, p, p, p, ct.c_size_t, p]),
         "usk_aggregate_grad": (i32, [p, i32, p, i32, p, p, ct.c_size_t, p]),
         "usk_trace_read": (i32, [p, i64, p, i32]),
+        "usk_linear_batch_peers": (i32, [p, p, p, p, i32, p, i32, i32, p, p, ct.c_size_t, p]),
+        "usk_peer_wait": (i32, [p, p, p]),
         "usk_trace_reset": (None, []),
     }
     for name, (res, args) in sig.items():
@@ -339,6 +341,40 @@ def linear_batch(plan: Plan, sketch, layers, x, ys, workspace, ranges=None, stre
     _check(lib.usk_linear_batch(plan.handle, _ptr(sketch), ids, rg, n, _ptr(x), _dtype_code(x), yp,
                                 _dtype_code(ys[0]), _ptr(workspace), workspace.numel() * workspace.element_size(),
                                 _stream(stream)))
+
+
+class _Peers(ct.Structure):
+    _fields_ = [("n_peers", ct.c_int32), ("my_rank", ct.c_int32), ("y_peer", ct.c_void_p), ("sig_peer", ct.c_void_p),
+                ("epoch", ct.c_void_p)]
+
+
+class Peers:
+    """usk_peers (include/usk.h): the peer-mapped full-y pointers of every rank per layer of a grouped
+    call, every rank's signal array, and this rank's device epoch counter.  Pointers are ints
+    (device addresses valid in this process, e.g. torch symmetric-memory buffer_ptrs)."""
+
+    def __init__(self, n_peers: int, my_rank: int, y_ptrs, sig_ptrs, epoch):
+        n = len(y_ptrs[0])
+        self._y = (ct.c_void_p * (n_peers * n))(*[int(y_ptrs[q][k]) for q in range(n_peers) for k in range(n)])
+        self._s = (ct.c_void_p * n_peers)(*[int(v) for v in sig_ptrs])
+        self.epoch = epoch
+        self.c = _Peers(n_peers, my_rank, ct.cast(self._y, ct.c_void_p), ct.cast(self._s, ct.c_void_p),
+                        ct.c_void_p(epoch.data_ptr()))
+
+
+def linear_batch_peers(plan: Plan, sketch, layers, x, peers: Peers, workspace, ranges=None, y_dtype="f32", stream=None):
+    """usk_linear_batch_peers: this rank's output ranges, stored into every rank's full y + flags."""
+    n, ids, rg = _batch_args(layers, ranges)
+    _need(x, "linear_batch_peers: x")
+    _need(workspace, "linear_batch_peers: workspace")
+    _check(lib.usk_linear_batch_peers(plan.handle, _ptr(sketch), ids, rg, n, _ptr(x), _dtype_code(x), DTYPE[y_dtype],
+                                      ct.byref(peers.c), _ptr(workspace), workspace.numel() * workspace.element_size(),
+                                      _stream(stream)))
+
+
+def peer_wait(plan: Plan, peers: Peers, stream=None):
+    """usk_peer_wait: wait until every rank's flag reached epoch + 1, then advance the epoch."""
+    _check(lib.usk_peer_wait(plan.handle, ct.byref(peers.c), _stream(stream)))
 
 
 def importance(A, out, stream=None):

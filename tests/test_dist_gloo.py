@@ -159,3 +159,16 @@ def test_outrow_disjoint_shards_gloo(orc):
     for l, (o, i) in enumerate(shapes):
         x = synth.vector(i, seed=l)[0].astype(np.float64)
         np.testing.assert_array_equal(ys[l], orc.linear_rows(opl, ref, l, x)[0])
+
+
+def test_peer_layout_host_logic():
+    """dist.peer_layout (the symmetric buffer behind usk_linear_batch_peers): every grouped call's
+    full y has its own 256-B aligned, non-overlapping piece in call order, and the signal array
+    follows them."""
+    from paper_2506_17255_b200 import dist as udist
+    groups = [[3072, 512, 512], [2048], [8192, 8192], [2048]]
+    offs, sig_off, total = udist.peer_layout(groups)
+    spans = [(a, a + n * 4) for o, outs in zip(offs, groups) for a, n in zip(o, outs)]
+    for (a0, a1), (b0, b1) in zip(spans, spans[1:]):
+        assert a0 % 256 == 0 and a1 <= b0
+    assert spans[-1][1] <= sig_off and sig_off % 256 == 0 and total >= sig_off + 4 * 8

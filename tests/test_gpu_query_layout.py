@@ -239,3 +239,38 @@ def test_xg_importance_classes_build(orc, usk):
         usk.plan_allocation(shapes, bpw=0.5, hash="xg", layout="query", seed=8,
                             saliency=[torch.from_numpy(s).cuda() for s in sal])
     assert e.value.status == usk.EUNSUPPORTED
+
+
+def test_peer_allgather_epilogue_two_virtual_ranks(orc, usk):
+    """usk_linear_batch_peers + usk_peer_wait (fused y all-gather) with two ranks simulated
+    in one process on one GPU: each 'rank' computes its output shard and stores it into BOTH full-y
+    buffers and both signal arrays; the waits then pass and both full y equal the single-GPU call bit
+    for bit, over two epochs (graph-style replays).  No rank waits on a kernel of another (the launches
+    are stream-ordered), so this checks the data placement and the flag protocol, not NVLink timing."""
+    shapes = [(3000, 512), (700, 512), (1100, 512)]
+    pl, opl, sk, osk, Ws = build_both(orc, usk, shapes)
+    layers = [0, 1, 2]
+    P = 2
+    yfull = [[torch.zeros(o, dtype=torch.float32, device="cuda") for (o, i) in shapes] for _ in range(P)]
+    sig = [torch.zeros(P, dtype=torch.int32, device="cuda") for _ in range(P)]
+    epoch = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in range(P)]
+    ref = [torch.empty(o, dtype=torch.float32, device="cuda") for (o, i) in shapes]
+    for it in range(2):
+        xb = synth.f32_to_bf16_bits(synth.vector(512, seed=40 + it)[0])
+        x = torch.from_numpy(xb.view(np.int16).copy()).view(torch.bfloat16).cuda()
+        usk.linear_batch(pl, sk, layers, x, ref, usk.new_batch_workspace(pl, layers))
+        peers = []
+        for r in range(P):
+            ranges = [((o * r) // P, (o * (r + 1)) // P) for (o, i) in shapes]
+            pr = usk.Peers(P, r, [[t.data_ptr() for t in yfull[q]] for q in range(P)], [s.data_ptr() for s in sig],
+                           epoch[r])
+            peers.append(pr)
+            usk.linear_batch_peers(pl, sk, layers, x, pr, usk.new_batch_workspace(pl, layers, ranges), ranges=ranges)
+        for r in range(P):
+            usk.peer_wait(pl, peers[r])
+        usk.check(pl)
+        for r in range(P):
+            assert int(epoch[r].item()) == it + 1
+            assert sig[r].cpu().tolist() == [it + 1] * P
+            for k in range(3):
+                assert torch.equal(yfull[r][k], ref[k]), (it, r, k)
