@@ -606,18 +606,20 @@ def run_usk(args):
             for l, (o, i) in enumerate(shapes):
                 usk.linear(pl_, sk_, l, Xw[i], Yw[o], ws_p, stream=stream)
 
-        def time_pass(pl_, sk_, reps=3):
+        def time_pass(pl_, sk_, reps=7):
             with torch.cuda.stream(stream):
                 prefill_pass(pl_, sk_)
             torch.cuda.synchronize()
-            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            with torch.cuda.stream(stream):
-                a.record(stream)
-                for _ in range(reps):
+            ts = []
+            for _ in range(reps):  # median of single passes (X, Y and the workspace exceed L2 anyway)
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                with torch.cuda.stream(stream):
+                    a.record(stream)
                     prefill_pass(pl_, sk_)
-                b.record(stream)
-            b.synchronize()
-            return a.elapsed_time(b) / reps
+                    b.record(stream)
+                b.synchronize()
+                ts.append(a.elapsed_time(b))
+            return float(np.median(ts))
 
         flop = 2.0 * T * numel
         ms05 = time_pass(plan, sketch)

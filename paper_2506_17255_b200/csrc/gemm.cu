@@ -96,6 +96,13 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+// two fp32 -> packed bf16 pair, round to nearest even (one F2FP; lo in the low half)
+__device__ __forceinline__ uint32_t pack_bf16x2(uint32_t lo, uint32_t hi) {
+  uint32_t d;
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(__uint_as_float(hi)), "f"(__uint_as_float(lo)));
+  return d;
+}
+
 __device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
   const uint32_t b = __float_as_uint(f);
   if ((b & 0x7F800000u) == 0x7F800000u) return (uint16_t)((b >> 16) | ((b & 0xFFFFu) ? 0x40u : 0u));
@@ -107,17 +114,20 @@ struct GemmArgs {
   int32_t y_bf16;
   int64_t T, N, K;
   int64_t ldy;
+  int32_t group_n;  // n-blocks per raster group (host: as many as keep the group's B rows L2-resident)
+  int32_t pad;
 };
 
-// tile index -> (m block, n block): groups of kGroupN n-blocks, m fastest inside a group
-constexpr int kGroupN = 8;
-__device__ __forceinline__ void tile_coords(int64_t t, int mblocks, int nblocks, int& mb, int& nb) {
-  const int64_t per_group = (int64_t)mblocks * kGroupN;
+// tile index -> (m block, n block): groups of group_n n-blocks, n fastest inside a group, so the
+// concurrent tiles share a few A (X) row blocks and the group's B (W') rows stay in L2 while the
+// m blocks advance: X is read from HBM once per group (one group covers all of W' when W' fits)
+__device__ __forceinline__ void tile_coords(int64_t t, int mblocks, int nblocks, int group_n, int& mb, int& nb) {
+  const int64_t per_group = (int64_t)mblocks * group_n;
   const int g = (int)(t / per_group);
   const int64_t r = t - (int64_t)g * per_group;
-  const int gw = min(kGroupN, nblocks - g * kGroupN);  // n-blocks in this group
+  const int gw = min(group_n, nblocks - g * group_n);  // n-blocks in this group
   mb = (int)(r / gw);
-  nb = g * kGroupN + (int)(r % gw);
+  nb = g * group_n + (int)(r % gw);
 }
 
 __global__ void __launch_bounds__(kGemmThreads, 1)
@@ -167,7 +177,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       int64_t it = 0;  // global stage counter across tiles
       for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
         int mb, nb;
-        tile_coords(t, mblocks, nblocks, mb, nb);
+        tile_coords(t, mblocks, nblocks, G.group_n, mb, nb);
         for (int kb = 0; kb < nkb; ++kb, ++it) {
           const int s = (int)(it % kStages);
           if (it >= kStages) mbar_wait(&empty[s], (uint32_t)((it / kStages) - 1) & 1u);
@@ -208,7 +218,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++local) {
       const int b = local & 1;
       int mb, nb;
-      tile_coords(t, mblocks, nblocks, mb, nb);
+      tile_coords(t, mblocks, nblocks, G.group_n, mb, nb);
       mbar_wait(&acc_full[b], (uint32_t)(local >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row = (int64_t)mb * BM + q * 32 + lane;
@@ -227,14 +237,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               uint4 pk;
-              pk.x = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 0])) |
-                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 1])) << 16);
-              pk.y = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 2])) |
-                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 3])) << 16);
-              pk.z = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 4])) |
-                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 5])) << 16);
-              pk.w = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 6])) |
-                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 7])) << 16);
+              pk.x = pack_bf16x2(r[8 * v + 0], r[8 * v + 1]);
+              pk.y = pack_bf16x2(r[8 * v + 2], r[8 * v + 3]);
+              pk.z = pack_bf16x2(r[8 * v + 4], r[8 * v + 5]);
+              pk.w = pack_bf16x2(r[8 * v + 6], r[8 * v + 7]);
               reinterpret_cast<uint4*>(dst)[v] = pk;
             }
           } else {
@@ -369,13 +375,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   cluster_sync_all();  // barriers of both CTAs initialised before any remote arrive / complete_tx
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // programmatic dependent launch: the set-up above overlaps the previous kernel (the reconstruction
+  // of W' into the workspace); X, W' and Y are touched only after it completed
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 
   if (warp == 0) {
     if (lane == 0) {
       int64_t it = 0;
       for (int64_t t = pair; t < tiles; t += npairs) {
         int mp, nb;
-        tile_coords(t, mpairs, nblocks, mp, nb);
+        tile_coords(t, mpairs, nblocks, G.group_n, mp, nb);
         const int arow = mp * 2 * BM + (int)rank * BM;
         const int brow = nb * BN + (int)rank * 128;
         for (int kb = 0; kb < nkb; ++kb, ++it) {
@@ -422,7 +432,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int64_t t = pair; t < tiles; t += npairs, ++local) {
       const int b = local & 1;
       int mp, nb;
-      tile_coords(t, mpairs, nblocks, mp, nb);
+      tile_coords(t, mpairs, nblocks, G.group_n, mp, nb);
       mbar_wait(&acc_full[b], (uint32_t)(local >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int64_t row = (int64_t)mp * 2 * BM + (int64_t)rank * BM + q * 32 + lane;
@@ -441,14 +451,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
               uint4 pk;
-              pk.x = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 0])) |
-                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 1])) << 16);
-              pk.y = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 2])) |
-                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 3])) << 16);
-              pk.z = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 4])) |
-                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 5])) << 16);
-              pk.w = (uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 6])) |
-                     ((uint32_t)f32_to_bf16_rne(__uint_as_float(r[8 * v + 7])) << 16);
+              pk.x = pack_bf16x2(r[8 * v + 0], r[8 * v + 1]);
+              pk.y = pack_bf16x2(r[8 * v + 2], r[8 * v + 3]);
+              pk.z = pack_bf16x2(r[8 * v + 4], r[8 * v + 5]);
+              pk.w = pack_bf16x2(r[8 * v + 6], r[8 * v + 7]);
               reinterpret_cast<uint4*>(dst)[v] = pk;
             }
           } else {
@@ -518,7 +524,16 @@ usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dty
   CUtensorMap ma, mb;
   if (!make_map(&ma, X, T, K, BM) || !make_map(&mb, W, n_out, K, one_sm ? BN : 128))
     return fail(USK_ECUDA, "cuTensorMapEncodeTiled failed");
-  GemmArgs G{Y, y_dtype == USK_BF16, T, n_out, K, n_out};
+  GemmArgs G{Y, y_dtype == USK_BF16, T, n_out, K, n_out, 8, 0};
+  {
+    // raster groups: the B rows of a group (group_n x 256 rows x K bf16) within ~48 MB of L2, so X is
+    // read from HBM once per group (ncu, 1B gate [8192 x 2048], groups of 8: 300 MB DRAM reads for
+    // 100 MB of operands -- X re-read per group as the 268 MB of Y stream through L2)
+    static const int forced = [] { const char* e = std::getenv("USK_GEMM_GROUPN"); return e ? std::atoi(e) : 0; }();
+    const int64_t nblocks = (n_out + BN - 1) / BN;
+    const int64_t fit = std::max<int64_t>(8, (48ll << 20) / ((int64_t)BN * K * 2));
+    G.group_n = forced > 0 ? forced : (int)std::min<int64_t>(nblocks, fit);
+  }
   const int sms2 = device_sm_count();
   if (!one_sm) {
     USK_CUDA(ensure_smem((const void*)k_gemm_tc2, (int)kGemmSmem2));
@@ -534,8 +549,14 @@ usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dty
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    // PDL for the GEMM (its set-up under the reconstruction's tail) measured no gain on the config-4
+    // pass (27.6 / 27.6 vs 27.4 / 27.1 ms, same box): opt-in only
+    static const bool pdl = [] { const char* e = std::getenv("USK_GEMM_PDL"); return e && e[0] == '1'; }();
+    cudaLaunchAttribute attr2[2] = {attr[0], {}};
+    attr2[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr2[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr2;
+    cfg.numAttrs = pdl ? 2 : 1;
     const cudaError_t e = cudaLaunchKernelEx(&cfg, k_gemm_tc2, ma, mb, G);
     if (e != cudaSuccess) return fail(USK_ECUDA, cudaGetErrorString(e));
     USK_LAUNCHED("k_gemm_tc2");

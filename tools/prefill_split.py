@@ -25,7 +25,7 @@ args = ap.parse_args()
 dev = torch.device("cuda", 0)
 shapes = synth.llama_block(2048, 512, 8192)
 names = ["q", "k", "v", "o", "gate", "up", "down"]
-pl = usk.plan_allocation(shapes, bpw=args.bpw, rows=3, seed=0x5EED000000000003)
+pl = usk.plan_allocation(shapes, bpw=args.bpw, rows=3, seed=0x5EED000000000003, hash="xg", layout="query")
 sk = pl.new_sketch(dev)
 ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, 0, k), dev) for k, (o, i) in enumerate(shapes)]
 usk.build(pl, ws, sk)
