@@ -1,0 +1,73 @@
+"""Config-4 prefill pass timing variants (tuning aid): all 112 Llama-3.2-1B linears at T = 16384 in model
+order through usk_linear (K3p reconstruct into the workspace + the tcgen05 GEMM), eager vs captured in
+one CUDA graph, plus the 112 reconstructions alone (eager and graph): where the pass time goes.
+  python tools/prefill_pass.py [--bpw 0.5] [--reps 5]
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import synth  # noqa: E402
+from paper_2506_17255_b200 import usk  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--bpw", type=float, default=0.5)
+ap.add_argument("--reps", type=int, default=5)
+args = ap.parse_args()
+dev = torch.device("cuda", 0)
+shapes = synth.llama32_1b_shapes()
+pl = usk.plan_allocation(shapes, bpw=args.bpw, rows=3, seed=0x5EED000000000003, hash="xg", layout="query")
+sk = pl.new_sketch(dev)
+usk.build(pl, [synth.torch_weights_bf16(o, i, synth.seed_for(3, l // 7, l % 7), dev) for l, (o, i) in enumerate(shapes)], sk)
+T = 16384
+Xp = synth.torch_vector(8192, 77, dev, torch.bfloat16, T=T).reshape(-1)
+Yp = torch.empty(T * 8192, dtype=torch.bfloat16, device=dev)
+Xw = {i: Xp[:T * i].view(T, i) for i in {i for _, i in shapes}}
+Yw = {o: Yp[:T * o].view(T, o) for o in {o for o, _ in shapes}}
+wsp = torch.zeros(max(usk.linear_workspace_bytes(pl, l, T) for l in range(len(shapes))), dtype=torch.uint8, device=dev)
+st = torch.cuda.Stream(device=dev)
+
+
+def pass_full():
+    for l, (o, i) in enumerate(shapes):
+        usk.linear(pl, sk, l, Xw[i], Yw[o], wsp, stream=st)
+
+
+def pass_recon():
+    for l, (o, i) in enumerate(shapes):
+        usk.reconstruct(pl, sk, l, wsp[:o * i * 2].view(torch.bfloat16).view(o, i), stream=st)
+
+
+def timed(fn, graph):
+    with torch.cuda.stream(st):
+        fn()
+    torch.cuda.synchronize()
+    g = None
+    if graph:
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=st):
+            fn()
+    ts = []
+    for _ in range(args.reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(st):
+            a.record(st)
+            g.replay() if g is not None else fn()
+            b.record(st)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+out = {"bpw": args.bpw}
+for name, fn in (("pass", pass_full), ("recon_only", pass_recon)):
+    for graph in (False, True):
+        out[f"{name}_{'graph' if graph else 'eager'}_ms"] = timed(fn, graph)
+print(json.dumps(out), flush=True)
