@@ -452,11 +452,20 @@ def run_usk(args):
 
     # ---- standalone reconstruct throughput (weights reconstructed/s, HBM-bound kernel): the 112
     #      layer reconstructions into one scratch buffer, captured as one CUDA graph, L2 flushed
-    scratch = torch.empty(max(o * i for o, i in shapes), dtype=torch.bfloat16, device=dev)
+    # query layout: usk_reconstruct_batch, each block's q|k|v|o|gate|up in one K3p launch (in = 2048)
+    # and down in another, every layer into its own region of a block-sized scratch
+    blk = shapes[:7]
+    scratch = torch.empty(sum(o * i for o, i in blk), dtype=torch.bfloat16, device=dev)
+    soff = np.cumsum([0] + [o * i for o, i in blk])
+    souts = [scratch[soff[k]:soff[k + 1]].view(o, i) for k, (o, i) in enumerate(blk)]
 
     def rec_all():
+        if args.layout == "query":
+            for b in range(L // 7):
+                usk.reconstruct_batch(plan, sketch, list(range(7 * b, 7 * b + 7)), souts, stream=stream)
+            return
         for l, (o, i) in enumerate(shapes):
-            usk.reconstruct(plan, sketch, l, scratch[:o * i].view(o, i), stream=stream)
+            usk.reconstruct(plan, sketch, l, souts[l % 7], stream=stream)
 
     with torch.cuda.stream(stream):
         rec_all()

@@ -266,6 +266,13 @@ USK_API usk_status usk_reconstruct(const usk_plan* plan, const void* sketch, int
                            int64_t row_begin, int64_t row_end, void* w_out, int64_t ld_out,
                            usk_stream stream);
 
+/* Reconstruction of whole layers, several per launch (query layout: consecutive layers with one
+ * in_features and chunk width share a K3p launch, up to 8; unit-major: one launch per layer):
+ * layer layers[k] into w_out[k] (device, row-major [out, in] of the plan dtype, leading dimension
+ * ld_out[k] >= in_features).  Same bytes as usk_reconstruct of each layer. */
+USK_API usk_status usk_reconstruct_batch(const usk_plan* plan, const void* sketch, const int32_t* layers, int32_t n,
+                                         void* const* w_out, const int64_t* ld_out, usk_stream stream);
+
 /* L2 warm-up of the sketch bytes of layers [layer_begin, layer_end) (cells, or codes + group
  * scales of a quantised plan, and their Top-K side tables): bulk L2 prefetches issued by a small
  * grid launched with programmatic dependent launch, so it overlaps the running kernel; the

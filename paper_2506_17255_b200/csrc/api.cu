@@ -484,6 +484,24 @@ usk_status usk_reconstruct(const usk_plan* pl, const void* sketch, int32_t layer
   return launch_reconstruct(pl, sketch, layer, row_begin, row_end, w_out, ld_out, (cudaStream_t)stream);
 }
 
+usk_status usk_reconstruct_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, int32_t n,
+                                 void* const* w_out, const int64_t* ld_out, usk_stream stream) {
+  if (!pl || !sketch || !layers || !w_out || !ld_out) return fail(USK_EINVAL, "usk_reconstruct_batch: null pointer");
+  if (n < 0) return fail(USK_ESHAPE, "usk_reconstruct_batch: n < 0");
+  for (int32_t k = 0; k < n; ++k) {
+    if (layers[k] < 0 || layers[k] >= pl->n_layers) return fail(USK_ESHAPE, "usk_reconstruct_batch: layer out of range");
+    if (!w_out[k]) return fail(USK_EINVAL, "usk_reconstruct_batch: null w_out");
+    if (ld_out[k] < pl->layers[layers[k]].in) return fail(USK_ESHAPE, "usk_reconstruct_batch: ld_out < in_features");
+  }
+  if (pl->layout == USK_LAYOUT_QUERY) return launch_qreconstruct_batch(pl, sketch, layers, n, w_out, ld_out, (cudaStream_t)stream);
+  for (int32_t k = 0; k < n; ++k) {  // unit-major plans: one K3 launch per layer
+    const LayerGeom& L = pl->layers[layers[k]];
+    usk_status s = launch_reconstruct(pl, sketch, layers[k], 0, L.out, w_out[k], ld_out[k], (cudaStream_t)stream);
+    if (s != USK_OK) return s;
+  }
+  return USK_OK;
+}
+
 usk_status usk_prefetch_l2(const usk_plan* pl, const void* sketch, int32_t layer_begin, int32_t layer_end,
                            usk_stream stream) {
   if (!pl || !sketch) return fail(USK_EINVAL, "usk_prefetch_l2: null pointer");

@@ -229,6 +229,8 @@ usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const i
                          void* sketch, cudaStream_t st);
 usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t layer, int64_t r0, int64_t r1,
                                void* w_out, int64_t ld, cudaStream_t st);
+usk_status launch_qreconstruct_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, int n,
+                                     void* const* w_out, const int64_t* ld, cudaStream_t st);
 size_t qgemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* o0, const int64_t* o1,
                                    int n);
 usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,

@@ -59,7 +59,8 @@ struct PLayer {
   int64_t rows;
   int64_t item_begin;  // first work item (chunk-major, subtile-minor)
   int64_t row_begin;   // first row in the launch's reduction order
-  int32_t n_chunks, n_sub, CP, pad;
+  int32_t n_chunks, n_sub, CP;
+  int32_t st_al;       // reconstruct: ld_out and w_out allow 16-B row stores
   void* y;
   float* partial;      // [rows][CP]
   void* w_out;         // reconstruct
@@ -81,7 +82,6 @@ struct PArgs {
   HashConsts hc;
   const void* x;
   int32_t red_lanes;
-  int32_t st_aligned;   // reconstruct: ld and w_out allow 16-B row stores
   int32_t n_ctas;       // compute CTAs of the launch
   int32_t x_prefetch;   // bulk L2 prefetch of the CTA's x slices before griddepcontrol.wait
   int32_t cta_item[kPMaxCtas + 1];
@@ -412,7 +412,7 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
               w[p] = neg_w(m) ^ 0x80008000u;
             }
             if (valid) {
-              if (A.st_aligned) {
+              if (Ly.st_al) {
                 if constexpr (UPL == 8) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1 % PW], w[2 % PW], w[3 % PW]);
                 else *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1 % PW]);
               } else {
@@ -1013,30 +1013,60 @@ usk_status launch_peer_wait(const usk_plan* pl, const usk_peers* peers, cudaStre
   return USK_OK;
 }
 
-usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t l, int64_t r0, int64_t r1, void* w_out,
-                               int64_t ld, cudaStream_t st) {
-  const LayerGeom& L = pl->layers[l];
-  const int64_t rows = r1 - r0;
-  if (rows == 0) return USK_OK;
-  PArgs A = p_base(pl, sketch, L.in);
-  PLayer& Ly = A.layer[A.n_layers++];
-  Ly.unit_base = L.unit_begin;
-  Ly.chunk0 = L.qchunk0;
-  Ly.o_begin = r0;
-  Ly.rows = rows;
-  Ly.n_chunks = L.qchunks;
-  Ly.n_sub = (int32_t)((rows + 15) / 16);
-  Ly.w_out = w_out;
-  Ly.ld_out = ld;
-  A.items = (int64_t)Ly.n_chunks * Ly.n_sub;
-  A.rows = rows;
-  A.st_aligned = (ld % 8 == 0) && (reinterpret_cast<uintptr_t>(w_out) % 16 == 0);
-  const void* kern = pick_kernel(false, false, pl->M, 16, L.qcw / 32);
+// K3p over several layers in one launch (usk_reconstruct, usk_reconstruct_batch): layers sharing
+// in_features and chunk width, up to kPMaxLayers per launch, full or partial row ranges
+usk_status qrecon_launch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* r0,
+                         const int64_t* r1, void* const* w_out, const int64_t* ld, int n, cudaStream_t st) {
+  const LayerGeom& L0 = pl->layers[layers[0]];
+  PArgs A = p_base(pl, sketch, L0.in);
+  for (int k = 0; k < n; ++k) {
+    const LayerGeom& L = pl->layers[layers[k]];
+    const int64_t rows = r1[k] - r0[k];
+    if (rows <= 0) continue;
+    PLayer& Ly = A.layer[A.n_layers++];
+    Ly.unit_base = L.unit_begin;
+    Ly.chunk0 = L.qchunk0;
+    Ly.o_begin = r0[k];
+    Ly.rows = rows;
+    Ly.n_chunks = L.qchunks;
+    Ly.n_sub = (int32_t)((rows + 15) / 16);
+    Ly.w_out = w_out[k];
+    Ly.ld_out = ld[k];
+    Ly.st_al = (ld[k] % 8 == 0) && (reinterpret_cast<uintptr_t>(w_out[k]) % 16 == 0);
+    Ly.item_begin = A.items;
+    Ly.row_begin = A.rows;
+    A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
+    A.rows += rows;
+  }
+  if (!A.n_layers) return USK_OK;
+  const void* kern = pick_kernel(false, false, pl->M, 16, L0.qcw / 32);
   int grid = 0;
   size_t smem = 0;
   usk_status s = p_prepare(pl, A, kern, false, grid, smem);
   if (s != USK_OK) return s;
   return p_launch(kern, A, grid, kPThreads, smem, st);
+}
+
+usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t l, int64_t r0, int64_t r1, void* w_out,
+                               int64_t ld, cudaStream_t st) {
+  return qrecon_launch(pl, sketch, &l, &r0, &r1, &w_out, &ld, 1, st);
+}
+
+usk_status launch_qreconstruct_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, int n,
+                                     void* const* w_out, const int64_t* ld, cudaStream_t st) {
+  // consecutive runs of layers with one (in_features, chunk width), at most kPMaxLayers per launch
+  for (int a = 0; a < n;) {
+    int b = a + 1;
+    while (b < n && b - a < kPMaxLayers && pl->layers[layers[b]].in == pl->layers[layers[a]].in &&
+           pl->layers[layers[b]].qcw == pl->layers[layers[a]].qcw)
+      ++b;
+    std::vector<int64_t> r0(b - a, 0), r1(b - a);
+    for (int k = a; k < b; ++k) r1[k - a] = pl->layers[layers[k]].out;
+    usk_status s = qrecon_launch(pl, sketch, layers + a, r0.data(), r1.data(), w_out + a, ld + a, b - a, st);
+    if (s != USK_OK) return s;
+    a = b;
+  }
+  return USK_OK;
 }
 
 }  // namespace usk

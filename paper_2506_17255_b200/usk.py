@@ -80,6 +80,7 @@ def _load():
         "usk_build_rows": (i32, [p, i32, i64, i64, p, p, p]),
         "usk_reconstruct": (i32, [p, p, i32, i64, i64, p, i64, p]),
         "usk_prefetch_l2": (i32, [p, p, i32, i32, p]),
+        "usk_reconstruct_batch": (i32, [p, p, p, i32, p, p, p]),
         "usk_linear_workspace_bytes": (ct.c_size_t, [p, i32, i64, i64, i64]),
         "usk_linear": (i32, [p, p, i32, p, i32, i64, p, i32, i64, i64, p, ct.c_size_t, p]),
         "usk_linear_batch_workspace_bytes": (ct.c_size_t, [p, p, p, i32]),
@@ -274,6 +275,20 @@ def reconstruct(plan: Plan, sketch, layer: int, w_out, row_begin: int = 0, row_e
                                f"unit column stride (got {tuple(w_out.shape)}, strides {tuple(w_out.stride())})")
     _check(lib.usk_reconstruct(plan.handle, _ptr(sketch), layer, row_begin, row_end, _ptr(w_out), w_out.stride(0),
                                _stream(stream)))
+
+
+def reconstruct_batch(plan: Plan, sketch, layers, w_outs, stream=None):
+    """usk_reconstruct_batch: whole layers (w_outs[k] = [out, >= in] row-major, unit column stride)."""
+    n = len(layers)
+    for k, (l, w) in enumerate(zip(layers, w_outs)):
+        _need(w, f"reconstruct_batch: w_outs[{k}]", dtype=plan.dtype, contiguous=False)
+        if 0 <= l < len(plan.shapes) and (w.dim() != 2 or w.stride(1) != 1 or w.shape[0] < plan.shapes[l][0]
+                                          or w.shape[1] < plan.shapes[l][1]):
+            raise UskError(ESHAPE, f"reconstruct_batch: w_outs[{k}] shape {tuple(w.shape)}")
+    ids = (ct.c_int32 * n)(*layers)
+    ptrs = (ct.c_void_p * n)(*[w.data_ptr() for w in w_outs])
+    lds = (ct.c_int64 * n)(*[w.stride(0) for w in w_outs])
+    _check(lib.usk_reconstruct_batch(plan.handle, _ptr(sketch), ids, n, ptrs, lds, _stream(stream)))
 
 
 def prefetch_l2(plan: Plan, sketch, layer_begin: int = 0, layer_end=None, stream=None):

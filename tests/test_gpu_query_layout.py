@@ -274,3 +274,15 @@ def test_peer_allgather_epilogue_two_virtual_ranks(orc, usk):
             assert sig[r].cpu().tolist() == [it + 1] * P
             for k in range(3):
                 assert torch.equal(yfull[r][k], ref[k]), (it, r, k)
+
+
+def test_query_reconstruct_batch(orc, usk):
+    """usk_reconstruct_batch: consecutive layers with one in_features share a K3p launch; every layer's
+    W' equals its single usk_reconstruct and the oracle, with padded leading dimensions."""
+    shapes = [(2048, 512), (512, 512), (8192, 256), (130, 264), (96, 264)]
+    pl, opl, sk, osk, Ws = build_both(orc, usk, shapes)
+    outs = [torch.zeros(o, i + 8 * (k % 2), dtype=torch.bfloat16, device="cuda") for k, (o, i) in enumerate(shapes)]
+    usk.reconstruct_batch(pl, sk, list(range(len(shapes))), outs)
+    for l, (o, i) in enumerate(shapes):
+        got = outs[l][:, :i].cpu().view(torch.int16).numpy().view(np.uint16)
+        np.testing.assert_array_equal(got.reshape(-1), orc.reconstruct_rows(opl, osk, l).reshape(-1))
