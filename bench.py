@@ -110,6 +110,9 @@ def _cpu_model():
     return "unknown"
 
 
+_ORACLE_CTX = {}
+
+
 def oracle_decode_sample(shapes, weights_for_layer, budget_s=12.0, threads=1, rows_per_call=32):
     """Time the CPU oracle's fp64 sketch-GEMV (reconstruct-on-the-fly + FMA, oracle/usk_oracle.c, as
     it stands) on a bounded sample: the 7 linears of block 0, output rows in round-robin until
@@ -120,11 +123,16 @@ def oracle_decode_sample(shapes, weights_for_layer, budget_s=12.0, threads=1, ro
 
     import oracle
     blk = shapes[:7]
-    opl = oracle.plan(blk, BPW, M=ROWS, dtype=oracle.BF16, seed=SEED)
-    sk = np.zeros(opl.total_cells, np.uint16)
-    for l in range(7):
-        oracle.build_layer(opl, l, weights_for_layer(l), sk)
-    xs = [synth.vector(i, seed=1000 + l)[0].astype(np.float64) for l, (o, i) in enumerate(blk)]
+    # the oracle's block-0 plan and sketch are built once per process (the timed sample is the GEMV)
+    key = (tuple(blk), id(weights_for_layer))
+    if _ORACLE_CTX.get("key") != key:
+        opl = oracle.plan(blk, BPW, M=ROWS, dtype=oracle.BF16, seed=SEED)
+        sk = np.zeros(opl.total_cells, np.uint16)
+        for l in range(7):
+            oracle.build_layer(opl, l, weights_for_layer(l), sk)
+        xs = [synth.vector(i, seed=1000 + l)[0].astype(np.float64) for l, (o, i) in enumerate(blk)]
+        _ORACLE_CTX.update(key=key, opl=opl, sk=sk, xs=xs)
+    opl, sk, xs = _ORACLE_CTX["opl"], _ORACLE_CTX["sk"], _ORACLE_CTX["xs"]
     RS = rows_per_call  # output rows per oracle call
 
     def worker(k):
@@ -173,7 +181,9 @@ def run_reference(args):
     else:
         getw = lambda l: synth.weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, 0, l))
     per_step = []
-    budget = args.ref_step_s if args.ref_step_s else max(2.0, 60.0 / max(1, args.steps + args.warmup))
+    # the whole --steps K --warmup W run samples ~60 s of oracle work (each step a bounded sample of
+    # the same workload, >= 0.2 s), after one build of the oracle's block-0 sketch
+    budget = args.ref_step_s if args.ref_step_s else max(0.2, 60.0 / max(1, args.steps + args.warmup))
     ncores = max(1, len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count() or 1)
     for k in range(args.warmup + args.steps):
         r = oracle_decode_sample(shapes, getw, budget_s=budget, threads=ncores)  # the box's host cores
