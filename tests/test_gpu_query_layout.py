@@ -286,3 +286,30 @@ def test_query_reconstruct_batch(orc, usk):
     for l, (o, i) in enumerate(shapes):
         got = outs[l][:, :i].cpu().view(torch.int16).numpy().view(np.uint16)
         np.testing.assert_array_equal(got.reshape(-1), orc.reconstruct_rows(opl, osk, l).reshape(-1))
+
+
+@pytest.mark.parametrize("M", [1, 2, 4])
+def test_query_rows_1_2_4(orc, usk, M):
+    """Query-layout kernels for M = 1, 2 and 4 sketch rows (template variants of K4p / K3p / the
+    query write-out): bytes, reconstruction and GEMV against the oracle."""
+    shapes = [(512, 512), (200, 264)]
+    pl, opl, sk, osk, Ws = build_both(orc, usk, shapes, bpw=1.0, M=M)
+    q = sk.cpu().numpy().view(np.uint16)
+    for l, (o, i) in enumerate(shapes):
+        u0, u1 = opl.layer_units(l)
+        li = pl.layers[l]
+        cells, pad_ok = qlayout.unpack_layer(q[li.qbyte_begin // 2:(li.qbyte_begin + li.qbytes) // 2],
+                                             opl.offsets[u0:u1 + 1], opl.ncols[u0:u1], opl.nrows[u0:u1], M)
+        np.testing.assert_array_equal(cells, osk[opl.offsets[u0]:opl.offsets[u1]])
+        assert pad_ok
+        w = torch.empty(o, i, dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, w)
+        np.testing.assert_array_equal(w.cpu().view(torch.int16).numpy().view(np.uint16).reshape(-1),
+                                      orc.reconstruct_rows(opl, osk, l).reshape(-1))
+        xb = synth.f32_to_bf16_bits(synth.vector(i, seed=l + 5)[0])
+        xd = torch.from_numpy(xb.view(np.int16).copy()).view(torch.bfloat16).cuda()
+        x64 = synth.bf16_bits_to_f32(xb).astype(np.float64)
+        y = torch.empty(o, dtype=torch.float32, device="cuda")
+        usk.linear(pl, sk, l, xd.view(1, -1), y.view(1, -1), usk.new_workspace(pl, l))
+        Wr = orc.value_of(orc.reconstruct_rows(opl, osk, l), orc.BF16).reshape(o, i)
+        assert gemv_err(y.cpu().numpy().astype(np.float64), orc.linear_rows(opl, osk, l, x64)[0], x64, Wr) <= 1e-5
