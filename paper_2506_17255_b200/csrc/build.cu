@@ -40,7 +40,11 @@ namespace {
 #define USK_BUILD_ROWS 64
 #endif
 constexpr int kRO = USK_BUILD_ROWS;  // weight rows per stage (each consumer warp takes kRO / 16 of them)
-constexpr int kConsumers = 16;  // consumer warps (2 rows of every stage each)
+#ifndef USK_BUILD_CONSUMERS
+#define USK_BUILD_CONSUMERS 16
+#endif
+constexpr int kConsumers = USK_BUILD_CONSUMERS;  // consumer warps (kRO / kConsumers rows of every stage each)
+static_assert(kRO % kConsumers == 0, "rows per stage must divide over the consumer warps");
 constexpr int kBuildThreads = 32 * (kConsumers + 1);
 constexpr int kMaxTasks = 48;
 constexpr size_t kSmemLimit = 227 * 1024;
