@@ -79,6 +79,9 @@ def lib():
         L.uo_allocate.argtypes = [i64, p, p, i64, i32, p, i32, p, p]
         L.uo_plan.restype = i32
         L.uo_plan.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, i32, i32, p, i64, p, p, p, p, p, p, p]
+        L.uo_plan2.restype = i32
+        L.uo_plan2.argtypes = [i32, p, p, i32, p, ct.c_double, i32, i32, i32, i32, i32, i32, i32, p, i64, p, i32, p, p, p,
+                               p, p, p]
         L.uo_topk.restype = i32
         L.uo_topk.argtypes = [i32, p, i64, i64, p, p]
         L.uo_layer_cells.restype = i32
@@ -278,11 +281,13 @@ def plan(shapes, bpw, M=3, dtype=BF16, saliency=None, gran=GRAN_ROW, g=1, C=None
         if len(crows) != C:
             raise OracleError(EINVAL, "plan: class_rows needs one row count per class")
     nrows = np.zeros(max(U, 1), dtype=np.uint8)
-    st = lib().uo_plan(L, _ptr(outf), _ptr(inf), dtype,
-                       ct.cast(sal_ptrs, ct.c_void_p) if sal_ptrs is not None else None,
-                       float(bpw), M, gran, g, C, min_cols, state_bits, group,
-                       None if limp is None else _ptr(limp), int(topk), None if crows is None else _ptr(crows),
-                       _ptr(unit_base), _ptr(cls), _ptr(ncols), _ptr(nrows), _ptr(offsets), _ptr(acct))
+    # USK-XG plans score each ROW unit by its key group's mean importance (ledger L33)
+    score_group = KEY_GROUP if (hash_kind == HASH_XG and gran == GRAN_ROW) else 1
+    st = lib().uo_plan2(L, _ptr(outf), _ptr(inf), dtype,
+                        ct.cast(sal_ptrs, ct.c_void_p) if sal_ptrs is not None else None,
+                        float(bpw), M, gran, g, C, min_cols, state_bits, group,
+                        None if limp is None else _ptr(limp), int(topk), None if crows is None else _ptr(crows),
+                        score_group, _ptr(unit_base), _ptr(cls), _ptr(ncols), _ptr(nrows), _ptr(offsets), _ptr(acct))
     _check(st, "plan")
     return Plan(list(map(tuple, zip(outf.tolist(), inf.tolist()))), dtype, M, gran, g, C, min_cols, hash_kind,
                 seed, unit_base, cls[:U], ncols[:U], offsets[:U + 1], acct.reshape(L, 4), state_bits, group, variant,

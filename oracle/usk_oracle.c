@@ -529,11 +529,29 @@ int32_t uo_layer_cells(int32_t L, const double* imp, const int64_t* numel, const
   return UO_OK;
 }
 
+/* score_group (ledger L33): ROW units score by the mean importance of their group of score_group
+ * consecutive units -- the key group under USK-XG (8), so the units of a group share a class and N;
+ * 1 = every unit its own score (the plain reading of §3.4) */
+int32_t uo_plan2(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32_t dtype,
+                 const float* const* sal, double bpw, int32_t M, int32_t gran, int32_t g, int32_t C,
+                 int32_t min_cols, int32_t q, int32_t G, const double* layer_imp, int64_t topk,
+                 const int32_t* class_rows, int32_t score_group, int64_t* unit_base, uint8_t* cls, int32_t* ncols,
+                 uint8_t* nrows, int64_t* offsets, int64_t* layer_acct);
+
 int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32_t dtype,
                 const float* const* sal, double bpw, int32_t M, int32_t gran, int32_t g, int32_t C,
                 int32_t min_cols, int32_t q, int32_t G, const double* layer_imp, int64_t topk,
                 const int32_t* class_rows, int64_t* unit_base, uint8_t* cls, int32_t* ncols, uint8_t* nrows,
                 int64_t* offsets, int64_t* layer_acct) {
+  return uo_plan2(n_layers, outf, inf, dtype, sal, bpw, M, gran, g, C, min_cols, q, G, layer_imp, topk, class_rows, 1,
+                  unit_base, cls, ncols, nrows, offsets, layer_acct);
+}
+
+int32_t uo_plan2(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32_t dtype,
+                 const float* const* sal, double bpw, int32_t M, int32_t gran, int32_t g, int32_t C,
+                 int32_t min_cols, int32_t q, int32_t G, const double* layer_imp, int64_t topk,
+                 const int32_t* class_rows, int32_t score_group, int64_t* unit_base, uint8_t* cls, int32_t* ncols,
+                 uint8_t* nrows, int64_t* offsets, int64_t* layer_acct) {
   int32_t l, c;
   int64_t U = 0, u;
   int32_t state_bits = (dtype == UO_BF16) ? 16 : 32;
@@ -607,7 +625,9 @@ int32_t uo_plan(int32_t n_layers, const int64_t* outf, const int64_t* inf, int32
       L_u = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)Ul);
       for (t = 0; t < Ul; t++) {
         double s = 0.0;
-        const int64_t ja = (gran == UO_GRAN_OUTROW) ? 0 : t * g, jb = (gran == UO_GRAN_OUTROW) ? inf[l] : (t + 1) * g;
+        const int64_t sg = (gran == UO_GRAN_ROW && score_group > 1) ? score_group : 1; /* ledger L33 */
+        const int64_t t0 = t / sg * sg, t1 = (t0 + sg < Ul) ? t0 + sg : Ul;
+        const int64_t ja = (gran == UO_GRAN_OUTROW) ? 0 : t0 * g, jb = (gran == UO_GRAN_OUTROW) ? inf[l] : t1 * g;
         for (j = ja; j < jb; j++) {
           double v = sal && sal[l] ? (double)sal[l][j] : 1.0;
           if (!(v >= 0.0) || !isfinite(v)) {
