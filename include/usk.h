@@ -21,7 +21,7 @@
  *     (order independence); usk_linear is deterministic for fixed inputs.
  *
  * Citations: PAPER.md:<line> (section / equation).  Readings where the paper is silent are
- * listed in DESIGN.md ("ledger" L1..L32) and referenced below.
+ * listed in DESIGN.md ("ledger" L1..L33) and referenced below.
  */
 #ifndef USK_H
 #define USK_H
@@ -83,8 +83,11 @@ typedef enum { USK_HASH_X = 0, USK_HASH_IDENTITY = 1, USK_HASH_XG = 2 } usk_hash
  * USK_LAYOUT_UNIT_MAJOR (default): the cells of unit u at [offsets[u], offsets[u+1]) in the state
  *   dtype, row-major (i, c) inside the unit (usk_plan_export).
  * USK_LAYOUT_QUERY (round 2; bf16 states, ROW units with dims_per_unit 1, USK_HASH_XG, AbsMaxMin,
- *   raw states, no Top-K, in_features % 8 == 0, every key group of 8 units with one N, and a
- *   128-unit chunk's rows * maxN * 256 bytes within shared memory -- maxN <= 285 at 3 rows): the same
+ *   raw states, no Top-K, in_features % 8 == 0, every key group of 8 units with one N, a
+ *   128-unit chunk's rows * maxN * 256 bytes within shared memory -- maxN <= 285 at 3 rows -- and
+ *   the chunks' padding of existing units (N_u < maxN_k or M_u < rows) at most 1/16 of each
+ *   layer's cells, so importance classes (which spread N over every chunk) take the unit-major
+ *   layout; their key groups share one N under USK-XG, ledger L33): the same
  *   cells, permuted and re-encoded for the decode so that one 16-byte (or 8-byte) shared load
  *   gathers a lane's 8 (4) cells of a sketch row (DESIGN.md §4 / §5 K4p).  Each layer occupies
  *   [qbyte_begin, qbyte_begin + qbytes) (usk_layer_info); its units form chunks of CW = qchunk_units

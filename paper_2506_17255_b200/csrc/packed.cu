@@ -810,16 +810,28 @@ usk_status qlayout_geometry(usk_plan* pl) {
       return fail(USK_EUNSUPPORTED, "query layout: a 128-unit chunk of layer " + std::to_string(l) +
                                         " (rows x max N x 256 B) exceeds shared memory");
     L.qchunks = (int32_t)((L.n_units + L.qcw - 1) / L.qcw);
+    int64_t pad = 0;  // padding cells of existing units (N_u < maxN_k or M_u < rows)
     for (int c = 0; c < L.qchunks; ++c) {
       int32_t mx = 1;
-      for (int64_t u = (int64_t)c * L.qcw; u < std::min<int64_t>(L.n_units, (int64_t)(c + 1) * L.qcw); ++u)
+      const int64_t ue = std::min<int64_t>(L.n_units, (int64_t)(c + 1) * L.qcw);
+      for (int64_t u = (int64_t)c * L.qcw; u < ue; ++u)
         mx = std::max(mx, pl->h_ncols[L.unit_begin + u]);
+      pad += (int64_t)pl->M * mx * (ue - (int64_t)c * L.qcw) -
+             (pl->h_offsets[L.unit_begin + ue] - pl->h_offsets[L.unit_begin + (int64_t)c * L.qcw]);
       pl->h_qc_off.push_back(off);
       pl->h_qc_N.push_back(mx);
       off += (int64_t)pl->M * mx * 2 * L.qcw;
       ++chunk;
     }
     L.qbytes = off - L.qoff;
+    // the layout stays (nearly) a bijection of the cells: importance classes spread over the chunks
+    // would pad every chunk to the largest class (the 1B model at C = 4: 211 MB instead of 61 MB)
+    const int64_t cells = pl->h_offsets[L.unit_begin + L.n_units] - pl->h_offsets[L.unit_begin];
+    if (pad * 16 > cells)
+      return fail(USK_EUNSUPPORTED, "query layout: chunks would pad layer " + std::to_string(l) + " by " +
+                                        std::to_string(pad * 100 / std::max<int64_t>(cells, 1)) +
+                                        "% of its cells (units of different N or rows share chunks); use the "
+                                        "unit-major layout");
   }
   pl->h_qc_off.push_back(off);
   pl->qtotal = off;

@@ -4,7 +4,8 @@
 // for each weight matrix row"; "layer-wise importance is estimated by the mean of row
 // importance"), categories PAPER.md:523-528.  Deterministic integer reading: DESIGN.md
 // "Allocation".  Pipeline (all on `stream`):
-//   k_unit_scores   s_u = sequential fp64 mean of the unit's saliency   (one thread / unit)
+//   k_unit_scores   s_u = sequential fp64 mean of the unit's saliency   (one thread / unit;
+//                   USK-XG: of its key group's, ledger L33)
 //   k_scope_max     s_max per budget scope (max of non-negative doubles = max of their bits)
 //   k_sort_keys     q_u = floor(s_u / s_max * 2^24); key = (scope << 25) | (2^24 - q_u)
 //   cub radix sort  stable: rank by (q desc, u asc) inside each scope
@@ -57,7 +58,13 @@ __global__ void k_unit_scores(PlanDev P, int64_t U, double* s_u, int* err) {
   int l = find_layer(P.unit_base, P.L, u);
   int64_t t = u - P.unit_base[l];
   int64_t j0, j1;
-  if (P.gran == USK_GRAN_ROW) { j0 = t * P.g; j1 = j0 + P.g; } else { j0 = 0; j1 = P.in_feat[l]; }
+  if (P.gran == USK_GRAN_ROW) {
+    // USK-XG (ledger L33): a unit scores by its key group's mean, so a group shares class and N
+    const int64_t Ul = P.unit_base[l + 1] - P.unit_base[l];
+    const int64_t t0 = (t >> P.key_shift) << P.key_shift;
+    const int64_t t1 = min(t0 + ((int64_t)1 << P.key_shift), Ul);
+    j0 = t0 * P.g; j1 = t1 * P.g;
+  } else { j0 = 0; j1 = P.in_feat[l]; }
   const float* s = P.sal[l];
   double acc = 0.0;
   for (int64_t j = j0; j < j1; ++j) {

@@ -271,6 +271,55 @@ def test_c3_query_layout_full_model_sampled(orc, usk):
                 assert gemv_err(y.cpu().numpy()[r0:r0 + 8].astype(np.float64), y64, x64, W64) <= 1e-5
 
 
+def test_c3_xg_importance_classes_full_model(orc, usk):
+    """The bench's importance point at full size: C = 4 saliency classes scored per key group (ledger
+    L33) with class rows (3, 3, 2, 2) (L30), USK-XG keys, all 112 linears, unit-major layout (the
+    grouped-key build K2).  The whole plan (class, N, M of every unit) equals the oracle's; sampled
+    units, reconstructed entries and grouped GEMV rows; the query layout refuses the plan (its chunks
+    would pad every chunk to the most salient class: 211 MB instead of 61 MB)."""
+    shapes = synth.llama32_1b_shapes()
+    sal = [synth.saliency_like(i, 500 + l) for l, (o, i) in enumerate(shapes)]
+    crows = (3, 3, 2, 2)
+    sal_dev = [torch.from_numpy(s).cuda() for s in sal]
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, hash="xg", n_classes=4, saliency=sal_dev,
+                             class_rows=crows)
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED, hash_kind=orc.HASH_XG, saliency=sal, C=4,
+                   class_rows=crows)
+    assert pl.info["total_cells"] == opl.total_cells
+    for l in range(len(shapes)):
+        cls, ncols, nrows, offs = pl.export(l)
+        u0, u1 = opl.layer_units(l)
+        np.testing.assert_array_equal(cls, opl.cls[u0:u1])
+        np.testing.assert_array_equal(ncols, opl.ncols[u0:u1])
+        np.testing.assert_array_equal(nrows, opl.nrows[u0:u1])
+        assert (ncols.reshape(-1, 8) == ncols.reshape(-1, 8)[:, :1]).all()
+    with pytest.raises(usk.UskError) as e:
+        usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query", n_classes=4,
+                            saliency=sal_dev, class_rows=crows)
+    assert e.value.status == usk.EUNSUPPORTED
+    sk = pl.new_sketch()
+    ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, l // 7, l % 7), "cuda") for l, (o, i) in enumerate(shapes)]
+    usk.build(pl, ws, sk)
+    usk.check(pl)
+    rng = np.random.default_rng(12)
+    for l in [0, 4, 6, 7 * 9 + 1]:
+        _unit_parity(orc, usk, pl, opl, sk, l, ws[l], 8, rng)
+    for g in ([0, 1, 2], [4, 5], [6]):
+        i = shapes[g[0]][1]
+        x = synth.torch_vector(i, 2000 + g[0], "cuda", torch.bfloat16)[0]
+        ys = [torch.empty(shapes[l][0], dtype=torch.float32, device="cuda") for l in g]
+        usk.linear_batch(pl, sk, g, x, ys, usk.new_batch_workspace(pl, g))
+        x64 = synth.bf16_bits_to_f32(host_bits(x)).astype(np.float64)
+        for l, y in zip(g, ys):
+            o = shapes[l][0]
+            osk = np.zeros(opl.total_cells, np.uint16)
+            orc.build_layer(opl, l, host_bits(ws[l]), osk)
+            for r0 in (0, int(rng.integers(0, o - 8)), o - 8):
+                y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 8)[0]
+                W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, r0, r0 + 8), orc.BF16).reshape(8, i)
+                assert gemv_err(y.cpu().numpy()[r0:r0 + 8].astype(np.float64), y64, x64, W64) <= 1e-5
+
+
 @pytest.mark.parametrize("k", [4, 6, 1], ids=["gate", "down", "k"])
 def test_c4_query_prefill_16384_tokens(orc, usk, k):
     """Config 4 on the query layout (K3p into the workspace + the tcgen05 GEMM), T = 16384."""

@@ -224,8 +224,8 @@ def test_xg_unit_major_build_bit_exact(orc, usk, shapes, bpw, M):
 
 
 def test_xg_importance_classes_build(orc, usk):
-    """USK-XG with C = 4 saliency classes: key groups mix column counts, so those layers take the
-    per-unit build path; bytes still equal the oracle's (and the query layout is refused)."""
+    """USK-XG with C = 4 saliency classes scored per key group (ledger L33): the unit-major plan's bytes
+    equal the oracle's, every key group is uniform, and the same plan in the query layout builds."""
     shapes = [(256, 512), (128, 256)]
     sal = [synth.saliency_like(i, 70 + k) for k, (o, i) in enumerate(shapes)]
     Ws = [synth.weights_bf16(o, i, 80 + k) for k, (o, i) in enumerate(shapes)]
@@ -235,10 +235,91 @@ def test_xg_importance_classes_build(orc, usk):
     usk.build(pl, [to_dev(W) for W in Ws], sk)
     osk = orc.build_model(opl, Ws)
     np.testing.assert_array_equal(sk.cpu().numpy().view(np.uint16)[:opl.total_cells], osk)
+    for l in range(len(shapes)):
+        cls, ncols = pl.export(l)[0], pl.export(l)[1]
+        u0, u1 = opl.layer_units(l)
+        np.testing.assert_array_equal(cls, opl.cls[u0:u1])
+        np.testing.assert_array_equal(ncols, opl.ncols[u0:u1])
+        assert (ncols.reshape(-1, 8) == ncols.reshape(-1, 8)[:, :1]).all()
+    assert len(set(opl.ncols.tolist())) > 1  # the classes really differ
+
+
+@pytest.mark.parametrize("crows", [None, (3, 3, 2, 2), (4, 3, 2, 1)])
+def test_xg_importance_classes_unit_major(orc, usk, crows):
+    """Importance classes (C = 4, optionally per-class rows, ledger L30) under USK-XG keys scored per
+    key group (L33): groups uniform, so the grouped-key build runs; bytes equal the oracle's, K3
+    reconstruction bit-exact, K4 GEMV within 1e-5.  The query layout refuses the plan (classes
+    spread over every chunk would pad it to the most salient class)."""
+    shapes = [(512, 1024), (300, 2048), (960, 256)]
+    sal = [synth.saliency_like(i, 90 + k) for k, (o, i) in enumerate(shapes)]
+    Ws = [synth.weights_bf16(o, i, 95 + k) for k, (o, i) in enumerate(shapes)]
+    M = 3 if crows is None else max(crows)
+    kw = dict(bpw=0.5, rows=M, hash="xg", seed=9, n_classes=4, class_rows=crows,
+              saliency=[torch.from_numpy(s).cuda() for s in sal])
     with pytest.raises(usk.UskError) as e:
-        usk.plan_allocation(shapes, bpw=0.5, hash="xg", layout="query", seed=8,
-                            saliency=[torch.from_numpy(s).cuda() for s in sal])
-    assert e.value.status == usk.EUNSUPPORTED
+        usk.plan_allocation(shapes, layout="query", **kw)
+    assert e.value.status == usk.EUNSUPPORTED and "pad" in str(e.value)
+    pl = usk.plan_allocation(shapes, **kw)
+    opl = orc.plan(shapes, 0.5, M=M, dtype=orc.BF16, hash_kind=orc.HASH_XG, seed=9, saliency=sal, C=4,
+                   class_rows=crows)
+    sk = pl.new_sketch()
+    usk.build(pl, [to_dev(W) for W in Ws], sk)
+    usk.check(pl)
+    osk = orc.build_model(opl, Ws)
+    np.testing.assert_array_equal(sk.cpu().numpy().view(np.uint16)[:opl.total_cells], osk)
+    assert len(set(opl.ncols.tolist())) > 1
+    for l, (o, i) in enumerate(shapes):
+        ref = orc.reconstruct_rows(opl, osk, l)
+        w = torch.empty(o, i, dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, w)
+        np.testing.assert_array_equal(w.cpu().view(torch.int16).numpy().view(np.uint16), ref)
+        xb = synth.f32_to_bf16_bits(synth.vector(i, seed=200 + l)[0])
+        xf = synth.bf16_bits_to_f32(xb).astype(np.float64)
+        y = torch.empty((1, o), dtype=torch.float32, device="cuda")
+        usk.linear(pl, sk, l, to_dev(xb).view(1, -1), y, usk.new_workspace(pl, l))
+        y64 = orc.linear_rows(opl, osk, l, xf)[0]
+        Wr = orc.value_of(ref, orc.BF16).reshape(o, i)
+        assert gemv_err(y.cpu().numpy()[0], y64, xf, Wr) <= 1e-5
+
+
+def test_query_importance_classes_chunk_aligned(orc, usk):
+    """Importance classes whose units form whole chunks (saliency constant over runs of 256 input
+    dims): the query layout holds them without padding, bit-exact against the oracle, and the
+    grouped GEMV / reconstruction run on the packed kernels."""
+    shapes = [(640, 1024), (200, 1024)]
+    lv = np.array([1.0, 9.0, 3.0, 0.5], np.float32)
+    sal = [np.repeat(lv, i // 4).astype(np.float32) for (o, i) in shapes]
+    Ws = [synth.weights_bf16(o, i, 97 + k) for k, (o, i) in enumerate(shapes)]
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, hash="xg", layout="query", seed=4, n_classes=4,
+                             saliency=[torch.from_numpy(s).cuda() for s in sal])
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, hash_kind=orc.HASH_XG, seed=4, saliency=sal, C=4)
+    assert len(set(opl.ncols.tolist())) >= 3
+    sk = pl.new_sketch()
+    sk.fill_(0xCD)
+    usk.build(pl, [to_dev(W) for W in Ws], sk)
+    usk.check(pl)
+    osk = orc.build_model(opl, Ws)
+    q = sk.cpu().numpy().view(np.uint16)
+    assert sum(pl.layers[l].qbytes for l in range(len(shapes))) == 2 * opl.total_cells
+    for l, (o, i) in enumerate(shapes):
+        u0, u1 = opl.layer_units(l)
+        li = pl.layers[l]
+        qb = q[li.qbyte_begin // 2:(li.qbyte_begin + li.qbytes) // 2]
+        cells, pad_ok = qlayout.unpack_layer(qb, opl.offsets[u0:u1 + 1], opl.ncols[u0:u1], opl.nrows[u0:u1], 3)
+        np.testing.assert_array_equal(cells, osk[opl.offsets[u0]:opl.offsets[u1]])
+        assert pad_ok
+        ref = orc.reconstruct_rows(opl, osk, l)
+        w = torch.empty(o, i, dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, w)
+        np.testing.assert_array_equal(w.cpu().view(torch.int16).numpy().view(np.uint16), ref)
+    x = torch.from_numpy(synth.f32_to_bf16_bits(synth.vector(1024, seed=31)[0]).view(np.int16).copy()).view(torch.bfloat16).cuda()
+    ys = [torch.empty(o, dtype=torch.float32, device="cuda") for (o, i) in shapes]
+    usk.linear_batch(pl, sk, [0, 1], x, ys, usk.new_batch_workspace(pl, [0, 1]))
+    xf = synth.bf16_bits_to_f32(x.cpu().view(torch.int16).numpy().view(np.uint16)).astype(np.float64)
+    for l, (o, i) in enumerate(shapes):
+        y64 = orc.linear_rows(opl, osk, l, xf)[0]
+        Wr = orc.value_of(orc.reconstruct_rows(opl, osk, l), orc.BF16).reshape(o, i)
+        assert gemv_err(ys[l].cpu().numpy(), y64, xf, Wr) <= 1e-5
 
 
 def test_peer_allgather_epilogue_two_virtual_ranks(orc, usk):
