@@ -643,42 +643,60 @@ def run_usk(args):
         p67 = paper_six_of_seven()
 
     # ---- BASELINE config 4: Llama-3.2-1B prefill, 2048 tokens x batch 8 (T = 16384) through all 112
-    #      linears in model order (usk_linear T > 1: K3 reconstruct into the workspace + the tcgen05
-    #      GEMM K5), at 0.5 bpw (the decode plan) and 0.8 bpw; X/Y (268 MB each) exceed L2
+    #      linears in model order, grouped as the decode (usk_linear_batch_tokens: K3 reconstruct of the
+    #      group into the workspace + one tcgen05 GEMM K5), at 0.5 bpw (the decode plan) and 0.8 bpw;
+    #      X/Y (268+ MB each) exceed L2
     c4 = None
     if world == 1 and not args.no_prefill:
         torch.cuda.empty_cache()
         T = 16384
         Xp = synth.torch_vector(8192, 77, dev, torch.bfloat16, T=T).reshape(-1)  # T x 8192 bf16 N(0,1)
-        Yp = torch.empty(T * 8192, dtype=torch.bfloat16, device=dev)
-        # dense row-major [T, in] / [T, out] per layer width (usk_linear's T > 1 layout; the binding
-        # rejects strided views)
+        gout = max(sum(shapes[l][0] for l in g) for g in groups)
+        Yp = torch.empty(T * gout, dtype=torch.bfloat16, device=dev)
+        # dense row-major [T, in] / [T, out] per layer (the T > 1 layout; the binding rejects strided
+        # views); a group's outputs are consecutive [T, out_k] blocks of Yp
         Xw = {i: Xp[:T * i].view(T, i) for i in {i for _, i in shapes}}
         Yw = {o: Yp[:T * o].view(T, o) for o in {o for o, _ in shapes}}
-        ws_p = torch.zeros(max(usk.linear_workspace_bytes(plan, l, T) for l in range(L)), dtype=torch.uint8,
-                           device=dev)
+
+        def group_ys(g):
+            ys, off = [], 0
+            for l in g:
+                ys.append(Yp[off:off + T * shapes[l][0]].view(T, shapes[l][0]))
+                off += T * shapes[l][0]
+            return ys
+
+        Yg = [group_ys(g) for g in groups]
+        ws_p = torch.zeros(max(max(usk.linear_workspace_bytes(plan, l, T) for l in range(L)),
+                               max(usk.linear_batch_tokens_workspace_bytes(plan, g, T) for g in groups)),
+                           dtype=torch.uint8, device=dev)
 
         def prefill_pass(pl_, sk_):
+            # per group (q|k|v, o, gate|up, down): the group's W' rebuilt once into the workspace,
+            # then one tcgen05 GEMM writing each layer's Y (usk_linear_batch_tokens)
+            for gi, g in enumerate(groups):
+                usk.linear_batch_tokens(pl_, sk_, g, Xw[shapes[g[0]][1]], Yg[gi], ws_p, stream=stream)
+
+        def prefill_pass_single(pl_, sk_):
             for l, (o, i) in enumerate(shapes):
                 usk.linear(pl_, sk_, l, Xw[i], Yw[o], ws_p, stream=stream)
 
-        def time_pass(pl_, sk_, reps=7, graph=True):
-            # the 224 launches of a pass captured in one CUDA graph, as the decode step (eager timing is
+        def time_pass(pl_, sk_, reps=7, graph=True, fn=prefill_pass):
+            # the launches of a pass captured in one CUDA graph, as the decode step (eager timing is
             # reported beside); median of single passes (X, Y and the workspace exceed L2 anyway)
             with torch.cuda.stream(stream):
-                prefill_pass(pl_, sk_)
+                fn(pl_, sk_)
             torch.cuda.synchronize()
             gp = None
             if graph:
                 gp = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(gp, stream=stream):
-                    prefill_pass(pl_, sk_)
+                    fn(pl_, sk_)
             ts = []
             for _ in range(reps):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 with torch.cuda.stream(stream):
                     a.record(stream)
-                    gp.replay() if gp is not None else prefill_pass(pl_, sk_)
+                    gp.replay() if gp is not None else fn(pl_, sk_)
                     b.record(stream)
                 b.synchronize()
                 ts.append(a.elapsed_time(b))
@@ -688,6 +706,7 @@ def run_usk(args):
         flop = 2.0 * T * numel
         ms05 = time_pass(plan, sketch)
         ms05_eager = time_pass(plan, sketch, graph=False)
+        ms05_single = time_pass(plan, sketch, fn=prefill_pass_single)
         plan08 = usk.plan_allocation(shapes, bpw=0.8, rows=ROWS, seed=SEED, **LAY)
         sk08 = plan08.new_sketch(dev)
         w8_ = [synth.torch_weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, l // 7, l % 7), dev)
@@ -698,15 +717,18 @@ def run_usk(args):
         ms08 = time_pass(plan08, sk08)
         pk, pk_s = peaks.get("bf16_tflops", 1666.6), peaks.get("bf16_tflops_sustained", 1352.0)
         c4 = {"workload": "c4: Llama-3.2-1B prefill, 2048 tokens x batch 8 (T = 16384), all 112 linears, M=3",
-              "bpw_0.5": {"ms_per_pass": ms05, "ms_per_pass_eager": ms05_eager, "TFLOP_per_s": flop / (ms05 * 1e-3) / 1e12,
+              "bpw_0.5": {"ms_per_pass": ms05, "ms_per_pass_eager": ms05_eager,
+                          "ms_per_pass_per_layer_calls": ms05_single, "TFLOP_per_s": flop / (ms05 * 1e-3) / 1e12,
                           "frac_of_bf16_sustained": flop / (ms05 * 1e-3) / 1e12 / pk_s,
                           "frac_of_bf16_burst": flop / (ms05 * 1e-3) / 1e12 / pk},
               "bpw_0.8": {"ms_per_pass": ms08, "TFLOP_per_s": flop / (ms08 * 1e-3) / 1e12,
                           "frac_of_bf16_sustained": flop / (ms08 * 1e-3) / 1e12 / pk_s,
                           "frac_of_bf16_burst": flop / (ms08 * 1e-3) / 1e12 / pk},
-              "flop_per_pass": flop, "graph": "224 launches per pass in one CUDA graph (eager beside)",
+              "flop_per_pass": flop, "calls": "64 usk_linear_batch_tokens per pass (q|k|v, o, gate|up, down of 16 blocks: "
+                                                  "one batched reconstruction + one GEMM each, 128 launches) in one CUDA graph "
+                                                  "(eager beside; 112 per-layer usk_linear calls beside)",
               "peak_basis": "MEASURED_PEAKS.json bf16 (torch 8192^3): sustained for a 25 ms pass, burst shown beside"}
-        del Xp, Yp, Xw, Yw, ws_p, sk08, plan08
+        del Xp, Yp, Xw, Yw, Yg, ws_p, sk08, plan08
         torch.cuda.empty_cache()
 
     # ---- BASELINE config 5 at N = 1: Llama-3-8B-shaped linears (224, 6.98 G weights, 13.96 GB bf16)

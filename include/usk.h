@@ -320,6 +320,25 @@ USK_API usk_status usk_linear_batch(const usk_plan* plan, const void* sketch, co
                                     void* const* y, int32_t y_dtype, void* workspace,
                                     size_t workspace_bytes, usk_stream stream);
 
+/* Prefill form of usk_linear_batch: T tokens through several layers that share one input
+ * (q|k|v, gate|up), the paper's decompression -> computation done once per
+ * group: the W' rows of all n layers are rebuilt into consecutive rows of `workspace`
+ * (usk_reconstruct's bytes), then ONE tcgen05 GEMM over the concatenated rows writes each layer's
+ * columns straight into its own y[k].  For k < n, t < T:
+ *   y[k][t, o - ranges[2k]] = sum_j x[t, j] * w'_{layers[k]}(o, j),  o in [ranges[2k], ranges[2k+1]).
+ *   x: device [T, in] bf16 (bf16 plans); y[k]: device [T, rows_k] of y_dtype, row-major, contiguous.
+ *   Same numerics as n calls of usk_linear with T tokens (fp32 accumulation of the same products
+ *   in the same K order).  One GEMM needs every layer but the last to have rows_k % 32 == 0 and
+ *   full ranges; otherwise the layers run one after another through the same workspace (same
+ *   results).  T == 1 is usk_linear_batch.  workspace: >= usk_linear_batch_tokens_workspace_bytes
+ *   (...), 16-B aligned.  USK_EUNSUPPORTED for fp32 plans or fp32 x with T > 1. */
+USK_API size_t usk_linear_batch_tokens_workspace_bytes(const usk_plan* plan, const int32_t* layers,
+                                                       const int64_t* ranges, int32_t n, int64_t T);
+USK_API usk_status usk_linear_batch_tokens(const usk_plan* plan, const void* sketch, const int32_t* layers,
+                                           const int64_t* ranges, int32_t n, const void* x, int32_t x_dtype,
+                                           int64_t T, void* const* y, int32_t y_dtype, void* workspace,
+                                           size_t workspace_bytes, usk_stream stream);
+
 /* Output-sharded decode with the y all-gather fused into the split-K reduction (SURVEY 8(e),
  * north star "each linear's output features are sharded for inference"; B200-native collective in
  * place of an NCCL all-gather).  Rank my_rank of n_peers computes rows [ranges[2k], ranges[2k+1])

@@ -575,6 +575,84 @@ static usk_status batch_ranges(const usk_plan* pl, const int32_t* layers, const 
   return USK_OK;
 }
 
+static bool tokens_fused(const usk_plan* pl, const int32_t* layers, const std::vector<int64_t>& o0,
+                         const std::vector<int64_t>& o1, int32_t n) {
+  for (int k = 0; k < n; ++k) {
+    const LayerGeom& L = pl->layers[layers[k]];
+    if (o0[k] != 0 || o1[k] != L.out) return false;
+    if (k + 1 < n && L.out % 32 != 0) return false;
+  }
+  return true;
+}
+
+size_t usk_linear_batch_tokens_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* ranges,
+                                               int32_t n, int64_t T) {
+  if (T == 1) return usk_linear_batch_workspace_bytes(pl, layers, ranges, n);
+  std::vector<int64_t> o0, o1;
+  if (T < 1 || batch_ranges(pl, layers, ranges, n, o0, o1) != USK_OK) return 0;
+  const int64_t in = pl->layers[layers[0]].in;
+  int64_t rows = 0, mx = 0;
+  for (int k = 0; k < n; ++k) {
+    rows += o1[k] - o0[k];
+    mx = std::max(mx, o1[k] - o0[k]);
+  }
+  return (size_t)(tokens_fused(pl, layers, o0, o1, n) ? rows : mx) * (size_t)in * 2;
+}
+
+usk_status usk_linear_batch_tokens(const usk_plan* pl, const void* sketch, const int32_t* layers,
+                                   const int64_t* ranges, int32_t n, const void* x, int32_t x_dtype, int64_t T,
+                                   void* const* y, int32_t y_dtype, void* workspace, size_t workspace_bytes,
+                                   usk_stream stream) {
+  if (T == 1)
+    return usk_linear_batch(pl, sketch, layers, ranges, n, x, x_dtype, y, y_dtype, workspace, workspace_bytes,
+                            stream);
+  if (T < 1) return fail(USK_ESHAPE, "usk_linear_batch_tokens: T must be >= 1");
+  std::vector<int64_t> o0, o1;
+  usk_status s = batch_ranges(pl, layers, ranges, n, o0, o1);
+  if (s != USK_OK) return s;
+  if (!sketch || !x || !y || !workspace) return fail(USK_EINVAL, "usk_linear_batch_tokens: null pointer");
+  if (y_dtype != USK_F32 && y_dtype != USK_BF16) return fail(USK_EINVAL, "usk_linear_batch_tokens: y_dtype");
+  if (pl->dtype != USK_BF16 || x_dtype != USK_BF16)
+    return fail(USK_EUNSUPPORTED, "usk_linear_batch_tokens: T > 1 needs bf16 weights and bf16 x (tcgen05 kind::f16)");
+  if (!aligned16(x) || !aligned16(sketch) || !aligned16(workspace))
+    return fail(USK_EINVAL, "usk_linear_batch_tokens: 16-B alignment");
+  for (int k = 0; k < n; ++k)
+    if (!y[k] || !aligned16(y[k])) return fail(USK_EINVAL, "usk_linear_batch_tokens: y pointer");
+  if (workspace_bytes < usk_linear_batch_tokens_workspace_bytes(pl, layers, ranges, n, T))
+    return fail(USK_ESHAPE, "usk_linear_batch_tokens: workspace too small");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t in = pl->layers[layers[0]].in;
+  unsigned char* ws = reinterpret_cast<unsigned char*>(workspace);
+  if (!tokens_fused(pl, layers, o0, o1, n)) {  // one layer after another through the workspace
+    for (int k = 0; k < n; ++k) {
+      if (o1[k] == o0[k]) continue;
+      s = pl->layout == USK_LAYOUT_QUERY ? launch_qreconstruct(pl, sketch, layers[k], o0[k], o1[k], ws, in, st)
+                                         : launch_reconstruct(pl, sketch, layers[k], o0[k], o1[k], ws, in, st);
+      if (s == USK_OK) s = launch_gemm_bf16(x, ws, y[k], y_dtype, T, o1[k] - o0[k], in, in, st);
+      if (s != USK_OK) return s;
+    }
+    return USK_OK;
+  }
+  // decompression of the whole group (one launch on the query layout), then one GEMM
+  std::vector<void*> wk(n);
+  std::vector<int64_t> ld(n, in);
+  std::vector<GemmOut> outs(n);
+  int64_t row = 0;
+  for (int k = 0; k < n; ++k) {
+    wk[k] = ws + (size_t)row * in * 2;
+    outs[k] = GemmOut{y[k], o1[k], o1[k]};
+    row += o1[k];
+  }
+  if (pl->layout == USK_LAYOUT_QUERY) {
+    s = launch_qreconstruct_batch(pl, sketch, layers, n, wk.data(), ld.data(), st);
+  } else {
+    for (int k = 0; k < n && s == USK_OK; ++k)
+      s = launch_reconstruct(pl, sketch, layers[k], 0, o1[k], wk[k], in, st);
+  }
+  if (s != USK_OK) return s;
+  return launch_gemm_bf16_seg(x, ws, outs.data(), n, y_dtype, T, in, st);
+}
+
 size_t usk_linear_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* ranges, int32_t n) {
   std::vector<int64_t> o0, o1;
   if (batch_ranges(pl, layers, ranges, n, o0, o1) != USK_OK) return 0;

@@ -213,6 +213,14 @@ usk_status launch_gemv_batch(const usk_plan* pl, const void* sketch, const int32
                              void* ws, cudaStream_t st);
 usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dtype, int64_t T,
                             int64_t n_out, int64_t K, int64_t ldw, cudaStream_t st);
+// one GEMM over the concatenated W' rows of several layers, output columns split into segments
+struct GemmOut {
+  void* y;       // [T, cols] of the output dtype, leading dimension ld
+  int64_t cols;  // inner segments: multiples of 32
+  int64_t ld;
+};
+usk_status launch_gemm_bf16_seg(const void* X, const void* W, const GemmOut* outs, int nseg, int32_t y_dtype,
+                                int64_t T, int64_t K, cudaStream_t st);
 usk_status launch_importance(const void* A, int32_t a_dtype, int64_t N, int64_t d, float* I,
                              cudaStream_t st);
 usk_status build_plan_device(usk_plan* pl, const float* const* saliency, cudaStream_t st);

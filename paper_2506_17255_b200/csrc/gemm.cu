@@ -38,6 +38,7 @@ namespace usk {
 namespace {
 
 constexpr int BM = 128, BN = 256, BK = 64;
+constexpr int kGemmSegs = 8;
 constexpr int kStages = 4;
 constexpr int kGemmThreads = 256;
 constexpr uint32_t kABytes = BM * BK * 2;  // 16 KB
@@ -110,13 +111,27 @@ __device__ __forceinline__ uint16_t f32_to_bf16_rne(float f) {
 }
 
 struct GemmArgs {
-  void* Y;
   int32_t y_bf16;
-  int64_t T, N, K;
-  int64_t ldy;
   int32_t group_n;  // n-blocks per raster group (host: as many as keep the group's B rows L2-resident)
+  int64_t T, N, K;
+  // output column segments (usk_linear_batch_tokens: the layers of one GEMM): columns
+  // [seg_col[s], seg_col[s+1]) go to seg_y[s] with leading dimension seg_ld[s]; inner boundaries are
+  // multiples of 32 (one epilogue chunk never straddles two outputs)
+  int32_t nseg;
   int32_t pad;
+  int64_t seg_col[kGemmSegs + 1];
+  void* seg_y[kGemmSegs];
+  int64_t seg_ld[kGemmSegs];
 };
+
+// the output of a 32-column chunk starting at col: destination element and valid columns
+template <typename T>
+__device__ __forceinline__ T* out_at(const GemmArgs& G, int64_t row, int64_t col, int& nvalid) {
+  int s = 0;
+  while (s + 1 < G.nseg && col >= G.seg_col[s + 1]) ++s;
+  nvalid = (int)min((int64_t)32, G.seg_col[s + 1] - col);
+  return reinterpret_cast<T*>(G.seg_y[s]) + row * G.seg_ld[s] + (col - G.seg_col[s]);
+}
 
 // tile index -> (m block, n block): groups of group_n n-blocks, n fastest inside a group, so the
 // concurrent tiles share a few A (X) row blocks and the group's B (W') rows stay in L2 while the
@@ -230,9 +245,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (row >= G.T) continue;
         const int64_t col = n0 + c0;
         if (col >= G.N) continue;
-        const int nvalid = (int)min((int64_t)32, G.N - col);
+        int nvalid;
         if (G.y_bf16) {
-          uint16_t* dst = reinterpret_cast<uint16_t*>(G.Y) + row * G.ldy + col;
+          uint16_t* dst = out_at<uint16_t>(G, row, col, nvalid);
           if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
@@ -247,7 +262,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int v = 0; v < nvalid; ++v) dst[v] = f32_to_bf16_rne(__uint_as_float(r[v]));
           }
         } else {
-          float* dst = reinterpret_cast<float*>(G.Y) + row * G.ldy + col;
+          float* dst = out_at<float>(G, row, col, nvalid);
           if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
             for (int v = 0; v < 8; ++v)
@@ -444,9 +459,9 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (row >= G.T) continue;
         const int64_t col = n0 + c0;
         if (col >= G.N) continue;
-        const int nvalid = (int)min((int64_t)32, G.N - col);
+        int nvalid;
         if (G.y_bf16) {
-          uint16_t* dst = reinterpret_cast<uint16_t*>(G.Y) + row * G.ldy + col;
+          uint16_t* dst = out_at<uint16_t>(G, row, col, nvalid);
           if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
             for (int v = 0; v < 4; ++v) {
@@ -461,7 +476,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int v = 0; v < nvalid; ++v) dst[v] = f32_to_bf16_rne(__uint_as_float(r[v]));
           }
         } else {
-          float* dst = reinterpret_cast<float*>(G.Y) + row * G.ldy + col;
+          float* dst = out_at<float>(G, row, col, nvalid);
           if (nvalid == 32 && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
 #pragma unroll
             for (int v = 0; v < 8; ++v)
@@ -513,8 +528,32 @@ bool make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t cols, int 
 
 usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dtype, int64_t T, int64_t n_out,
                             int64_t K, int64_t ldw, cudaStream_t st) {
-  if ((K * 2) % 16 != 0 || ldw != K)
+  if (ldw != K) return fail(USK_EUNSUPPORTED, "tcgen05 path needs a dense W' (ldw == in_features)");
+  const GemmOut out{Y, n_out, n_out};
+  return launch_gemm_bf16_seg(X, W, &out, 1, y_dtype, T, K, st);
+}
+
+usk_status launch_gemm_bf16_seg(const void* X, const void* W, const GemmOut* outs, int nseg, int32_t y_dtype,
+                                int64_t T, int64_t K, cudaStream_t st) {
+  if ((K * 2) % 16 != 0)
     return fail(USK_EUNSUPPORTED, "tcgen05 path needs in_features % 8 == 0 (16-B TMA row pitch)");
+  if (nseg < 1 || nseg > kGemmSegs) return fail(USK_EINVAL, "tcgen05 GEMM: 1..8 output segments");
+  GemmArgs G{};
+  G.y_bf16 = y_dtype == USK_BF16;
+  G.T = T;
+  G.K = K;
+  G.nseg = nseg;
+  int64_t n_out = 0;
+  for (int s = 0; s < nseg; ++s) {
+    if (s + 1 < nseg && outs[s].cols % 32 != 0)
+      return fail(USK_EINVAL, "tcgen05 GEMM: inner output segments must have a multiple of 32 columns");
+    G.seg_col[s] = n_out;
+    G.seg_y[s] = outs[s].y;
+    G.seg_ld[s] = outs[s].ld;
+    n_out += outs[s].cols;
+  }
+  G.seg_col[nseg] = n_out;
+  G.N = n_out;
   if ((reinterpret_cast<uintptr_t>(X) & 15) || (reinterpret_cast<uintptr_t>(W) & 15))
     return fail(USK_EINVAL, "tcgen05 path needs 16-B aligned operands");
   static const bool one_sm = [] {
@@ -524,7 +563,6 @@ usk_status launch_gemm_bf16(const void* X, const void* W, void* Y, int32_t y_dty
   CUtensorMap ma, mb;
   if (!make_map(&ma, X, T, K, BM) || !make_map(&mb, W, n_out, K, one_sm ? BN : 128))
     return fail(USK_ECUDA, "cuTensorMapEncodeTiled failed");
-  GemmArgs G{Y, y_dtype == USK_BF16, T, n_out, K, n_out, 8, 0};
   {
     // raster groups: the B rows of a group (group_n x 256 rows x K bf16) within ~48 MB of L2, so X is
     // read from HBM once per group (ncu, 1B gate [8192 x 2048], groups of 8: 300 MB DRAM reads for

@@ -85,6 +85,8 @@ def _load():
         "usk_linear": (i32, [p, p, i32, p, i32, i64, p, i32, i64, i64, p, ct.c_size_t, p]),
         "usk_linear_batch_workspace_bytes": (ct.c_size_t, [p, p, p, i32]),
         "usk_linear_batch": (i32, [p, p, p, p, i32, p, i32, p, i32, p, ct.c_size_t, p]),
+        "usk_linear_batch_tokens_workspace_bytes": (ct.c_size_t, [p, p, p, i32, i64]),
+        "usk_linear_batch_tokens": (i32, [p, p, p, p, i32, p, i32, i64, p, i32, p, ct.c_size_t, p]),
         "usk_check": (i32, [p, p]),
         "usk_plan_destroy": (None, [p]),
         "usk_status_string": (ct.c_char_p, [i32]),
@@ -356,6 +358,32 @@ def linear_batch(plan: Plan, sketch, layers, x, ys, workspace, ranges=None, stre
     _check(lib.usk_linear_batch(plan.handle, _ptr(sketch), ids, rg, n, _ptr(x), _dtype_code(x), yp,
                                 _dtype_code(ys[0]), _ptr(workspace), workspace.numel() * workspace.element_size(),
                                 _stream(stream)))
+
+
+def linear_batch_tokens_workspace_bytes(plan: Plan, layers, T: int, ranges=None) -> int:
+    n, ids, rg = _batch_args(layers, ranges)
+    return int(lib.usk_linear_batch_tokens_workspace_bytes(plan.handle, ids, rg, n, int(T)))
+
+
+def linear_batch_tokens(plan: Plan, sketch, layers, x, ys, workspace, ranges=None, stream=None):
+    """usk_linear_batch_tokens: T tokens (x [T, in] bf16) through several layers sharing x; the group's
+    W' rows rebuilt once into the workspace, one tcgen05 GEMM; ys[k]: contiguous [T, rows_k]."""
+    n, ids, rg = _batch_args(layers, ranges)
+    if len(ys) != n:
+        raise UskError(ESHAPE, f"linear_batch_tokens: {len(ys)} outputs for {n} layers")
+    _need(x, "linear_batch_tokens: x")
+    T = x.shape[0] if x.dim() == 2 else 1
+    for k, (l, y) in enumerate(zip(layers, ys)):
+        if 0 <= l < len(plan.shapes):
+            r = (0, plan.shapes[l][0]) if ranges is None else ranges[k]
+            _need(y, f"linear_batch_tokens: ys[{k}]")
+            if y.numel() != T * (r[1] - r[0]):
+                raise UskError(ESHAPE, f"linear_batch_tokens: ys[{k}] has {y.numel()} elements, needs {T * (r[1] - r[0])}")
+    _need(workspace, "linear_batch_tokens: workspace")
+    yp = (ct.c_void_p * n)(*[y.data_ptr() for y in ys])
+    _check(lib.usk_linear_batch_tokens(plan.handle, _ptr(sketch), ids, rg, n, _ptr(x), _dtype_code(x), T, yp,
+                                       _dtype_code(ys[0]), _ptr(workspace),
+                                       workspace.numel() * workspace.element_size(), _stream(stream)))
 
 
 class _Peers(ct.Structure):

@@ -92,3 +92,64 @@ def test_prefetch_l2_is_a_pure_hint(usk):
         usk.prefetch_l2(pl, sk, 0, 3)
     with pytest.raises(usk.UskError):
         usk.prefetch_l2(pl, sk, 2, 1)
+
+
+def _group(orc, usk, shapes, layout, seed=21):
+    Ws = [synth.weights_bf16(o, i, seed=seed + k) for k, (o, i) in enumerate(shapes)]
+    kw = dict(hash="xg", layout="query") if layout == "query" else {}
+    pl = usk.plan_allocation(shapes, bpw=1.0, rows=3, seed=seed, **kw)
+    opl = orc.plan(shapes, 1.0, M=3, dtype=orc.BF16, seed=seed,
+                   hash_kind=orc.HASH_XG if layout == "query" else orc.HASH_X)
+    sk = pl.new_sketch()
+    usk.build(pl, [_bf16_dev(W) for W in Ws], sk)
+    return pl, opl, sk, orc.build_model(opl, Ws)
+
+
+@pytest.mark.parametrize("layout", ["unit_major", "query"])
+@pytest.mark.parametrize("shapes", [[(96, 256), (160, 256), (300, 256)],   # one GEMM, ragged last layer
+                                    [(100, 256), (64, 256)]],               # 100 % 32 != 0: layer by layer
+                         ids=["fused", "sequential"])
+@pytest.mark.parametrize("T", [3, 130, 257])
+def test_batch_tokens_matches_oracle_and_single_calls(orc, usk, layout, shapes, T):
+    """usk_linear_batch_tokens (the group's W' rebuilt once, one GEMM with per-layer output
+    segments): every y[k] equals usk_linear of layer k bit for bit (same products, same K order), and
+    the fp32 results are within 1e-5 of the oracle's fp64 sums."""
+    pl, opl, sk, osk = _group(orc, usk, shapes, layout)
+    i = shapes[0][1]
+    xb = synth.f32_to_bf16_bits(synth.vector(i, seed=T + 5, T=T))
+    x = _bf16_dev(xb)
+    x64 = synth.bf16_bits_to_f32(xb).astype(np.float64)
+    layers = list(range(len(shapes)))
+    for dt in (torch.float32, torch.bfloat16):
+        ys = [torch.full((T, o), 7.0, dtype=dt, device="cuda") for (o, _) in shapes]
+        ws = torch.zeros(usk.linear_batch_tokens_workspace_bytes(pl, layers, T), dtype=torch.uint8, device="cuda")
+        usk.linear_batch_tokens(pl, sk, layers, x, ys, ws)
+        for l, (o, _) in enumerate(shapes):
+            ref = torch.empty((T, o), dtype=dt, device="cuda")
+            usk.linear(pl, sk, l, x, ref, usk.new_workspace(pl, l, T))
+            assert torch.equal(ys[l], ref), (l, dt)
+            if dt == torch.float32:
+                y64 = orc.linear_rows(opl, osk, l, x64)
+                Wr = orc.value_of(orc.reconstruct_rows(opl, osk, l), orc.BF16).reshape(o, i)
+                err = np.max(np.abs(ys[l].cpu().numpy() - y64) / np.maximum(np.abs(x64) @ np.abs(Wr).T, 1e-30))
+                assert err <= 1e-5, err
+
+
+def test_batch_tokens_ranges_and_rejections(orc, usk):
+    """Output ranges (sharded prefill) run layer by layer with the same bytes as usk_linear on each
+    range; fp32 x is refused with USK_EUNSUPPORTED."""
+    shapes = [(256, 128), (192, 128)]
+    pl, opl, sk, osk = _group(orc, usk, shapes, "query", seed=5)
+    T = 77
+    x = _bf16_dev(synth.f32_to_bf16_bits(synth.vector(128, seed=9, T=T)))
+    ranges = [(32, 200), (0, 100)]
+    ys = [torch.empty((T, b - a), dtype=torch.float32, device="cuda") for a, b in ranges]
+    ws = torch.zeros(usk.linear_batch_tokens_workspace_bytes(pl, [0, 1], T, ranges), dtype=torch.uint8, device="cuda")
+    usk.linear_batch_tokens(pl, sk, [0, 1], x, ys, ws, ranges=ranges)
+    for l, (a, b) in enumerate(ranges):
+        ref = torch.empty((T, b - a), dtype=torch.float32, device="cuda")
+        usk.linear(pl, sk, l, x, ref, usk.new_workspace(pl, l, T, a, b), out_begin=a, out_end=b)
+        assert torch.equal(ys[l], ref)
+    with pytest.raises(usk.UskError) as e:
+        usk.linear_batch_tokens(pl, sk, [0, 1], x.float(), [torch.empty((T, o), device="cuda") for o, _ in shapes], ws)
+    assert e.value.status == usk.EUNSUPPORTED

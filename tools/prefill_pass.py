@@ -1,6 +1,7 @@
 """Config-4 prefill pass timing variants (tuning aid): all 112 Llama-3.2-1B linears at T = 16384 in model
-order through usk_linear (K3p reconstruct into the workspace + the tcgen05 GEMM), eager vs captured in
-one CUDA graph, plus the 112 reconstructions alone (eager and graph): where the pass time goes.
+order through usk_linear (K3p reconstruct into the workspace + the tcgen05 GEMM), the same grouped as
+q|k|v, o, gate|up, down through usk_linear_batch_tokens (one reconstruction + one GEMM per group), eager
+vs captured in one CUDA graph, plus the 112 reconstructions alone: where the pass time goes.
   python tools/prefill_pass.py [--bpw 0.5] [--reps 5]
 """
 import argparse
@@ -31,13 +32,31 @@ Xp = synth.torch_vector(8192, 77, dev, torch.bfloat16, T=T).reshape(-1)
 Yp = torch.empty(T * 8192, dtype=torch.bfloat16, device=dev)
 Xw = {i: Xp[:T * i].view(T, i) for i in {i for _, i in shapes}}
 Yw = {o: Yp[:T * o].view(T, o) for o in {o for o, _ in shapes}}
-wsp = torch.zeros(max(usk.linear_workspace_bytes(pl, l, T) for l in range(len(shapes))), dtype=torch.uint8, device=dev)
+Yp2 = torch.empty(T * 16384, dtype=torch.bfloat16, device=dev)
+wsp = torch.zeros(max(usk.linear_workspace_bytes(pl, l, T) for l in range(len(shapes))) * 2, dtype=torch.uint8, device=dev)
 st = torch.cuda.Stream(device=dev)
 
 
 def pass_full():
     for l, (o, i) in enumerate(shapes):
         usk.linear(pl, sk, l, Xw[i], Yw[o], wsp, stream=st)
+
+
+groups = []
+for b in range(len(shapes) // 7):
+    groups += [[7 * b, 7 * b + 1, 7 * b + 2], [7 * b + 3], [7 * b + 4, 7 * b + 5], [7 * b + 6]]
+Yg = []
+for g in groups:
+    ys, off = [], 0
+    for l in g:
+        ys.append(Yp2[off:off + T * shapes[l][0]].view(T, shapes[l][0]))
+        off += T * shapes[l][0]
+    Yg.append(ys)
+
+
+def pass_grouped():
+    for gi, g in enumerate(groups):
+        usk.linear_batch_tokens(pl, sk, g, Xw[shapes[g[0]][1]], Yg[gi], wsp, stream=st)
 
 
 def pass_recon():
@@ -67,7 +86,7 @@ def timed(fn, graph):
 
 
 out = {"bpw": args.bpw}
-for name, fn in (("pass", pass_full), ("recon_only", pass_recon)):
+for name, fn in (("pass", pass_full), ("pass_grouped", pass_grouped), ("recon_only", pass_recon)):
     for graph in (False, True):
         out[f"{name}_{'graph' if graph else 'eager'}_ms"] = timed(fn, graph)
 print(json.dumps(out), flush=True)
