@@ -384,3 +384,37 @@ def test_c5_query_llama8b_block(orc, usk):
     y64 = orc.linear_rows(opl, osk, l, x64, 1000, 1008)[0]
     W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, 1000, 1008), orc.BF16).reshape(8, i)
     assert gemv_err(y.cpu().numpy()[0, 1000:1008].astype(np.float64), y64, x64, W64) <= 1e-5
+
+
+def test_c4_batch_tokens_groups_16384_tokens(orc, usk):
+    """Config 4 as the bench runs it: q|k|v and gate|up of a Llama-3.2-1B block through
+    usk_linear_batch_tokens at T = 16384 (one batched reconstruction + one GEMM per group) equal the
+    per-layer usk_linear results bit for bit; sampled entries within 2e-2 of the oracle."""
+    shapes = synth.llama_block(2048, 512, 8192)
+    T = 16384
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query")
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED, hash_kind=orc.HASH_XG)
+    ws = [synth.torch_weights_bf16(o, i, synth.seed_for(4, 0, k), "cuda") for k, (o, i) in enumerate(shapes)]
+    sk = pl.new_sketch()
+    usk.build(pl, ws, sk)
+    X = synth.torch_vector(2048, 8, "cuda", torch.bfloat16, T=T)
+    rng = np.random.default_rng(6)
+    toks = rng.choice(T, 32, replace=False)
+    Xh = synth.bf16_bits_to_f32(host_bits(X[torch.from_numpy(toks).cuda()])).astype(np.float64)
+    for g in ([0, 1, 2], [4, 5]):
+        ys = [torch.empty((T, shapes[l][0]), dtype=torch.bfloat16, device="cuda") for l in g]
+        wsp = torch.zeros(usk.linear_batch_tokens_workspace_bytes(pl, g, T), dtype=torch.uint8, device="cuda")
+        usk.linear_batch_tokens(pl, sk, g, X, ys, wsp)
+        for l, y in zip(g, ys):
+            o = shapes[l][0]
+            ref = torch.empty((T, o), dtype=torch.bfloat16, device="cuda")
+            usk.linear(pl, sk, l, X, ref, usk.new_workspace(pl, l, T))
+            assert torch.equal(y, ref), l
+            osk = np.zeros(opl.total_cells, np.uint16)
+            orc.build_layer(opl, l, host_bits(ws[l]), osk)
+            Yh = y.float().cpu().numpy()
+            for r in rng.choice(o, 4, replace=False):
+                y64 = orc.linear_rows(opl, osk, l, Xh, int(r), int(r) + 1)[:, 0]
+                w64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, int(r), int(r) + 1), orc.BF16).reshape(-1)
+                err = np.max(np.abs(Yh[toks, r] - y64) / np.maximum(np.abs(Xh) @ np.abs(w64), 1e-30))
+                assert err <= 2e-2, err
