@@ -1,7 +1,7 @@
 """Small driver for ncu: builds the Llama-3.2-1B block-0 sketch and launches the hot kernels in
 the order: grouped sketch-GEMVs (q|k|v, o, gate|up, down -- as bench.py launches them), the build,
-the reconstruction of gate, and (with --prefill) one 2048-token prefill of gate (reconstruct +
-tcgen05 GEMM).
+the reconstruction of gate, and (with --prefill) one 2048-token prefill of gate|up (batched
+reconstruction + one tcgen05 GEMM).  Default plan: USK-XG keys, query layout (the bench's).
 
   python tools/prof_kernels.py [--reps 1] [--prefill]
 """
@@ -22,10 +22,12 @@ ap.add_argument("--reps", type=int, default=1)
 ap.add_argument("--bpw", type=float, default=0.5)
 ap.add_argument("--prefill", action="store_true")
 ap.add_argument("--gran", default="row")
+ap.add_argument("--layout", default="query", choices=["query", "unit_major"])
 args = ap.parse_args()
 dev = torch.device("cuda", 0)
 shapes = synth.llama_block(2048, 512, 8192)
-pl = usk.plan_allocation(shapes, bpw=args.bpw, rows=3, seed=0x5EED000000000003, granularity=args.gran)
+pl = usk.plan_allocation(shapes, bpw=args.bpw, rows=3, seed=0x5EED000000000003, granularity=args.gran,
+                         **({"hash": "xg", "layout": "query"} if args.layout == "query" else {}))
 sk = pl.new_sketch(dev)
 ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, 0, k), dev) for k, (o, i) in enumerate(shapes)]
 torch.cuda.synchronize()
@@ -47,7 +49,8 @@ for _ in range(args.reps):
 if args.prefill:
     T = 2048
     X = synth.torch_vector(2048, 5, dev, torch.bfloat16, T=T)
-    Y = torch.empty((T, 8192), dtype=torch.bfloat16, device=dev)
-    usk.linear(pl, sk, 4, X, Y, usk.new_workspace(pl, 4, T, device=dev))
+    ys = [torch.empty((T, 8192), dtype=torch.bfloat16, device=dev) for _ in range(2)]
+    wsp = torch.zeros(usk.linear_batch_tokens_workspace_bytes(pl, [4, 5], T), dtype=torch.uint8, device=dev)
+    usk.linear_batch_tokens(pl, sk, [4, 5], X, ys, wsp)  # gate|up: one reconstruction + one GEMM
 torch.cuda.synchronize()
 print("ok")

@@ -14,7 +14,7 @@ $CMD > gpurun_out/plain.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_bench.csv $CMD > gpurun_out/ncu_launch.log 2>&1
 echo "launches rc=$?" >> gpurun_out/ncu_launch.log
 python tools/prof_kernels.py --reps 1 --prefill > gpurun_out/prof_plain.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"k_gemv_fast|k_gemv_reduce|k_build_fast|k_recon_fast|k_gemm_tc" -c 12 -o gpurun_out/prof_round -f python tools/prof_kernels.py --reps 1 --prefill > gpurun_out/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_qgemv|k_qreduce|k_build_fast|k_qrecon|k_gemm_tc" -c 14 -o gpurun_out/prof_round -f python tools/prof_kernels.py --reps 1 --prefill > gpurun_out/ncu_full.log 2>&1
 echo "full rc=$?" >> gpurun_out/ncu_full.log
 USK_TRACE=1 python tools/trace_step.py --reps 30 --csv gpurun_out/trace_round.csv > gpurun_out/trace_round.log 2>&1
 tail -2 gpurun_out/pytest_gpu.log; tail -c 300 gpurun_out/bench_full.log; tail -1 gpurun_out/ncu_launch.log; tail -1 gpurun_out/ncu_full.log; head -1 gpurun_out/trace_round.log
