@@ -74,8 +74,9 @@ gemv_bytes = []
 with open(os.path.join(PROF, f"{args.tag}_ncu_full_summary.txt"), "w") as f:
     f.write("# ncu --set full --clock-control none --import-source on of tools/prof_kernels.py --reps 1 --prefill\n"
             "# order: per grouped call (q|k|v, o, gate|up, down of Llama-3.2-1B block 0, 0.5 bpw, M=3) the compute\n"
-            "# kernel k_gemv_fast + its k_gemv_reduce; the block build; the gate reconstruct; the 2048-token gate\n"
-            "# prefill (reconstruct + tcgen05 GEMM).  Serialised, cold-cache replays (ncu), not bench numbers.\n")
+            "# kernel (k_qgemv on the query layout, k_gemv_fast unit-major) + its reduce; the block build; the gate\n"
+            "# reconstruct; the 2048-token gate|up prefill (one batched reconstruction + one tcgen05 GEMM).\n"
+            "# Serialised, cold-cache replays (ncu), not bench numbers.\n")
     for row in rows[2:]:
         r = dict(zip(hdr, row))
         name = r.get("Kernel Name", "")
@@ -84,25 +85,30 @@ with open(os.path.join(PROF, f"{args.tag}_ncu_full_summary.txt"), "w") as f:
             if k in r:
                 rec[k] = r[k]
         f.write(json.dumps(rec) + "\n")
-        if "k_gemv_fast" in name:
+        if "k_gemv_fast" in name or "k_qgemv" in name:
             unit = r.get("dram__bytes_read.sum", "0")
             gemv_bytes.append((float(r["dram__bytes_read.sum"]) + float(r["dram__bytes_write.sum"])) * 1e6)
 
-# ---- traffic.json: DRAM bytes per k_gemv_fast launch (MB in the raw page) vs algorithmic
+# ---- traffic.json: DRAM bytes per decode-kernel launch (MB in the raw page) vs algorithmic
 if gemv_bytes:
-    # algorithmic bytes of the 4 grouped calls of block 0: the block's sketch cells (bf16) + x + y
-    import oracle  # noqa: E402  (CPU plan: same cell counts as the GPU plan, tests/test_gpu_parity)
+    # algorithmic bytes of the 4 grouped calls of block 0 (USK-XG query plan, the bench's): the block's
+    # sketch bytes + x (bf16) + the fp32 chunk partials [rows][in / 256]
+    import oracle  # noqa: E402  (CPU plan: same cell counts as the GPU plan, tests/test_gpu_query_layout)
     import synth  # noqa: E402
     shapes = synth.llama_block(2048, 512, 8192)
-    cells = oracle.plan(shapes, 0.5, M=3, dtype=oracle.BF16, seed=0x5EED000000000003).total_cells
-    xy = sum(2 * i + 4 * o for o, i in shapes)
-    alg = (2 * cells + xy) / 4
-    json.dump({"k_gemv_fast_bytes_per_launch": sum(gemv_bytes) / len(gemv_bytes),
-               "algorithmic_bytes_per_launch": alg,
-               "source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of the 4 grouped k_gemv_fast "
-                         "launches of Llama-3.2-1B block 0, averaged per launch; algorithmic = the block's sketch "
-                         "bytes + x (bf16) + y (fp32) over 4 launches (profiles/%s_ncu_full_summary.txt)" % args.tag},
-              open(os.path.join(PROF, "traffic.json"), "w"), indent=1)
+    cells = oracle.plan(shapes, 0.5, M=3, dtype=oracle.BF16, seed=0x5EED000000000003,
+                        hash_kind=oracle.HASH_XG).total_cells
+    xy = 2 * (2048 + 2048 + 2048 + 8192) + sum(4 * o * (i // 256) for o, i in shapes)
+    alg = (2 * cells + xy) / len(gemv_bytes)
+    tp = os.path.join(PROF, "traffic.json")
+    tj = json.load(open(tp)) if os.path.exists(tp) else {}
+    tj.update({"k_qgemv_bytes_per_launch": sum(gemv_bytes) / len(gemv_bytes),
+               "k_qgemv_algorithmic_bytes_per_launch": alg,
+               "k_qgemv_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of the %d grouped k_qgemv "
+                                 "launches of Llama-3.2-1B block 0 (profiles/%s_ncu_full_summary.txt), averaged per "
+                                 "launch; algorithmic = the block's query-layout sketch bytes + x (bf16) + fp32 chunk "
+                                 "partials over the same launches" % (len(gemv_bytes), args.tag)})
+    json.dump(tj, open(tp, "w"), indent=1)
 
 # ---- decode trace
 tl = os.path.join(OUT, "trace_round.log")
