@@ -26,6 +26,9 @@
  *   per-class sketch rows (uo_plan class_rows, uo_allocate Mc, ledger L30) --
  *       pinned (hand-worked allocation, reduction to the uniform plan, conservation, the set-based
  *       enumerator per unit incl. LAYER units, Appendix B's untouched closed form per class).
+ *   key-group scores (uo_plan2 score_group = 8 under USK-XG, ledger L33) -- pinned (group means
+ *       computed apart in tests/test_oracle_xg_classes.py fed to the pinned allocator; uniform
+ *       groups, class order, USK-X plans unchanged, uniform saliency gives identical plans).
  *   output-row units (UO_GRAN_OUTROW, ledger L31) -- pinned (byte-identical to
  *       input-dim units of W^T, set-based enumerator per unit, accounting, untouched closed form).
  *   uo_importance -- pinned (SPEC Eq. 7 examples, constant activations).
