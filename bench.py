@@ -631,11 +631,13 @@ def run_usk(args):
         q4.update({"state_bits": 4, "group_size": 128})
         torch.cuda.empty_cache()
         sal = [torch.from_numpy(synth.saliency_like(i, 500 + l)).to(dev) for l, (o, i) in enumerate(shapes)]
-        # USK-XG keys, classes scored per key group (ledger L33): one N per group, so the grouped-key
-        # build runs; unit-major layout (the query layout refuses classes spread over its chunks)
-        cls = extra_point(saliency=sal, n_classes=4, class_rows=(3, 3, 2, 2), hash="xg")
+        # USK-XG keys, classes scored per key group (ledger L33): one N per group; in the query layout
+        # the key groups are in class order, the top class of gate/up in 64-unit chunks (ledger L34)
+        ckw = {"hash": "xg", "layout": "query"} if args.layout == "query" else {}
+        cls = extra_point(saliency=sal, n_classes=4, class_rows=(3, 3, 2, 2), **ckw)
         cls.update({"n_classes": 4, "class_rows": [3, 3, 2, 2], "saliency": "synth.saliency_like (log-normal, 1% of dims x400)",
-                    "hash": "USK-XG (classes per key group, ledger L33)", "layout": "unit_major"})
+                    "hash": "USK-XG (classes per key group, ledger L33)" if ckw else "USK-X",
+                    "layout": ckw.get("layout", "unit_major")})
         torch.cuda.empty_cache()
         orow = extra_point(granularity="outrow")
         orow.update({"granularity": "outrow (one unit per output row, ledger L31)"})

@@ -21,7 +21,7 @@
  *     (order independence); usk_linear is deterministic for fixed inputs.
  *
  * Citations: PAPER.md:<line> (section / equation).  Readings where the paper is silent are
- * listed in DESIGN.md ("ledger" L1..L33) and referenced below.
+ * listed in DESIGN.md ("ledger" L1..L34) and referenced below.
  */
 #ifndef USK_H
 #define USK_H
@@ -83,23 +83,28 @@ typedef enum { USK_HASH_X = 0, USK_HASH_IDENTITY = 1, USK_HASH_XG = 2 } usk_hash
  * USK_LAYOUT_UNIT_MAJOR (default): the cells of unit u at [offsets[u], offsets[u+1]) in the state
  *   dtype, row-major (i, c) inside the unit (usk_plan_export).
  * USK_LAYOUT_QUERY (round 2; bf16 states, ROW units with dims_per_unit 1, USK_HASH_XG, AbsMaxMin,
- *   raw states, no Top-K, in_features % 8 == 0, every key group of 8 units with one N, a
- *   128-unit chunk's rows * maxN * 256 bytes within shared memory -- maxN <= 285 at 3 rows -- and
- *   the chunks' padding of existing units (N_u < maxN_k or M_u < rows) at most 1/16 of each
- *   layer's cells, so importance classes (which spread N over every chunk) take the unit-major
- *   layout; their key groups share one N under USK-XG, ledger L33): the same
- *   cells, permuted and re-encoded for the decode so that one 16-byte (or 8-byte) shared load
- *   gathers a lane's 8 (4) cells of a sketch row (DESIGN.md §4 / §5 K4p).  Each layer occupies
- *   [qbyte_begin, qbyte_begin + qbytes) (usk_layer_info); its units form chunks of CW = qchunk_units
- *   units -- 256 when rows * (largest N of the layer) * 512 bytes fits shared memory, else 128 --
- *   the last chunk of a layer may be partial.  Chunk k has maxN_k = the largest N_u of its units and
- *   takes rows * maxN_k * 2 * CW bytes (rows = usk_plan_info.rows), chunks back to back from
- *   qbyte_begin.  Inside chunk k, the 16-bit word at byte
- *       ((i * maxN_k + c) * CW + t) * 2
- *   holds cell (i, c) of unit CW * k + t of the layer as the retrieve key
+ *   raw states, no Top-K, in_features % 8 == 0, every key group of 8 units with one N, a 64-unit
+ *   chunk's M_k * maxN_k * 128 bytes within the chunk budget of 226,240 bytes, and the chunks' padding of existing units
+ *   (N_u < maxN_k or M_u < M_k) at most 1/16 of each layer's cells): the same cells, permuted and
+ *   re-encoded for the decode so that one 16-, 8- or 4-byte shared load gathers a lane's 8, 4 or 2
+ *   cells of a sketch row (DESIGN.md §4 / §5 K4p, ledger L32, L34).  Each layer occupies
+ *   [qbyte_begin, qbyte_begin + qbytes) (usk_layer_info).
+ *   Query order of a layer: its key groups (units 8g .. 8g+7) in order of the class of their units
+ *   (usk_plan_export cls; stable, so by g inside a class) -- the identity when all groups share a
+ *   class; query position q is unit 8 * group(q / 8) + q % 8.
+ *   Chunks cover consecutive query positions from 0: a chunk starts where the previous ends and
+ *   takes CW_k positions, cut short at the layer end and, when the layer has several classes, at the
+ *   next class boundary.  CW_k = 256 when M_k * maxN_k * 512 <= 226,240 bytes, else 128,
+ *   else 64 (maxN_k, M_k: the largest N_u and sketch rows M_u of the chunk's units); a layer with one
+ *   class takes one CW for all its chunks, from its largest M_u and N_u (usk_layer_info
+ *   qchunk_units; 0 when a layer's chunks have several widths).  Chunk k takes
+ *   M_k * maxN_k * 2 * CW_k bytes (the chunk's whole width, present units or not), chunks back to
+ *   back from qbyte_begin.  Inside chunk k, the 16-bit word at byte
+ *       ((i * maxN_k + c) * CW_k + s) * 2
+ *   holds cell (i, c) of the unit at query position q0_k + s as the retrieve key
  *       rho16 = ((b << 1) | (b >> 15)) ^ 1  (b = the bf16 bits of the state; mag << 1 | 1 - sign),
- *   and 0 where the unit does not exist, c >= N_u or i >= M_u (0 is below every key: neutral for
- *   the Eq. 5 max).  The encoding is a bijection of the unit-major cells (same bits per weight). */
+ *   and 0 where the position is past the chunk's units, c >= N_u or i >= M_u (0 is below every key:
+ *   neutral for the Eq. 5 max). */
 typedef enum { USK_LAYOUT_UNIT_MAJOR = 0, USK_LAYOUT_QUERY = 1 } usk_layout;
 
 /* Sketch variant (Appendix C.2): USK_ABSMAXMIN = the paper's sketch (keep the
@@ -203,7 +208,7 @@ typedef struct {
                              states in the plan dtype */
   int64_t qbyte_begin;    /* USK_LAYOUT_QUERY: byte offset of the layer's region in the sketch */
   int64_t qbytes;         /*   and its size (0 for the unit-major layout) */
-  int32_t qchunk_units;   /*   units per chunk CW (256, or 128 when a 256-unit chunk exceeds shared memory) */
+  int32_t qchunk_units;   /*   units per chunk CW (256, 128 or 64); 0 when the layer mixes widths */
   int32_t reserved;
 } usk_layer_info;
 
@@ -270,7 +275,8 @@ USK_API usk_status usk_reconstruct(const usk_plan* plan, const void* sketch, int
                            usk_stream stream);
 
 /* Reconstruction of whole layers, several per launch (query layout: consecutive layers with one
- * in_features and chunk width share a K3p launch, up to 8; unit-major: one launch per layer):
+ * in_features share K3p launches, one per chunk width present, up to 8 layers; unit-major: one
+ * launch per layer):
  * layer layers[k] into w_out[k] (device, row-major [out, in] of the plan dtype, leading dimension
  * ld_out[k] >= in_features).  Same bytes as usk_reconstruct of each layer. */
 USK_API usk_status usk_reconstruct_batch(const usk_plan* plan, const void* sketch, const int32_t* layers, int32_t n,
@@ -353,8 +359,7 @@ USK_API usk_status usk_linear_batch_tokens(const usk_plan* plan, const void* ske
  *          layers[k], out_features elements of y_dtype, 16-B aligned); sig_peer host array [n_peers]
  *          of device uint32[n_peers] arrays (zero-filled before first use); epoch: device uint32, the
  *          same value on every rank (0 at first use).
- * Layers of one call must share the query layout's chunk width (USK_EUNSUPPORTED otherwise).  The
- * spin of usk_peer_wait is bounded: a peer that never signals is reported by usk_check (USK_ECUDA). */
+ * The spin of usk_peer_wait is bounded: a peer that never signals is reported by usk_check (USK_ECUDA). */
 typedef struct {
   int32_t n_peers;            /* ranks P in [1, 8] */
   int32_t my_rank;

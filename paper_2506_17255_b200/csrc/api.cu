@@ -119,7 +119,7 @@ static bool layer_cells(int L, const double* imp, const std::vector<int64_t>& nu
 
 static void free_plan(usk_plan* p) {
   if (!p) return;
-  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R4, p->d_err, p->d_qc_off, p->d_qc_N};
+  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R4, p->d_err, p->d_qc_off, p->d_qc_N, p->d_qc_aux, p->d_qperm};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete p;
@@ -421,7 +421,7 @@ usk_status usk_plan_layer(const usk_plan* pl, int32_t layer, usk_layer_info* out
   const LayerGeom& L = pl->layers[layer];
   *out = usk_layer_info{L.out,         L.in,        L.unit_begin, L.n_units,       L.cell_begin, L.n_cells,
                         L.budget_bits, L.meta_bits, L.cells_T,    L.achieved_bits, L.n_out,      L.out_off,
-                        L.qoff,        L.qbytes,    L.qcw};
+                        L.qoff,        L.qbytes,    L.qmixed ? 0 : L.qcw};
   return USK_OK;
 }
 

@@ -1091,8 +1091,16 @@ static usk_status launch_build_topk(const usk_plan* pl, const void* const* weigh
 // layer takes the fast build (else packed.cu builds unit-major cells into scratch and packs them)
 bool build_qfast_ok(const usk_plan* pl, const int32_t* layer_ids, int32_t n) {
   if (pl->dtype != USK_BF16 || pl->gran != USK_GRAN_ROW || pl->q || pl->topk) return false;
-  for (int32_t k = 0; k < n; ++k)
-    if (!fast_upl(pl, layer_ids ? layer_ids[k] : k)) return false;
+  for (int32_t k = 0; k < n; ++k) {
+    const int32_t l = layer_ids ? layer_ids[k] : k;
+    if (!fast_upl(pl, l)) return false;
+    // the fused write-out fills whole slices of identity-ordered chunks of >= 128 units and all rows
+    // (class-ordered layers, ledger L34, take the scratch build + k_qpack)
+    const LayerGeom& L = pl->layers[l];
+    if (L.qperm || L.qmixed || L.qcw < 128) return false;
+    for (int c = 0; c < L.qchunks; ++c)
+      if (pl->h_qc_M[L.qchunk0 + c] != pl->M) return false;
+  }
   return true;
 }
 

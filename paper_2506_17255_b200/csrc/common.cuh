@@ -145,7 +145,13 @@ struct LayerGeom {
   // query layout (usk.h USK_LAYOUT_QUERY): byte region of the layer, its first global chunk, chunks
   int64_t qoff = 0, qbytes = 0, qchunk0 = 0;
   int32_t qchunks = 0;
-  int32_t qcw = 0;  // query layout: units per chunk (256, or 128 when a 256-unit chunk exceeds shared memory)
+  int32_t qcw = 0;  // query layout: units per chunk of the layer's first chunk (256 / 128 / 64)
+  int32_t qperm = 0;   // query layout: key groups in class order (importance classes, ledger L34)
+  int32_t qmixed = 0;  // query layout: chunks of several widths
+  struct QRun {        // maximal run of consecutive chunks of one width
+    int32_t c0, n, cw;
+  };
+  std::vector<QRun> qruns;
 };
 
 constexpr int kQGroup = 8;  // units per key group (USK-XG, ledger L32) = cells per 16-B word of the query layout
@@ -189,6 +195,11 @@ struct usk_plan {
   std::vector<int32_t> h_qc_N;    //   and its maxN
   int64_t* d_qc_off = nullptr;
   int32_t* d_qc_N = nullptr;
+  // per chunk (ledger L34): first query position (units, within the layer), units present, sketch rows,
+  // width; per key group of the model: the layer-local group at each query position
+  std::vector<int32_t> h_qc_q0, h_qc_n, h_qc_M, h_qc_cw, h_qperm;
+  int32_t* d_qc_aux = nullptr;  // [4][chunks]: q0, n, M, cw
+  int32_t* d_qperm = nullptr;   // [U / 8]
   int cell_bytes() const { return dtype == USK_BF16 ? 2 : 4; }  // raw state bytes
   int64_t code_bytes() const { return (total_cells * q + 7) / 8; }
 };

@@ -48,6 +48,7 @@ constexpr int kPRedThreads = 256;
 constexpr int kPHdr = 64;          // [2 mbarriers][s_next][pad]
 constexpr int kPRtab = kPWarps * kPSub * 16;  // per warp: 16 rows x {R_0..R_3}
 constexpr int kPTS = 8;            // USK_TRACE stamps per CTA
+constexpr int kPZero = 1024;       // zero block before the slots (rows i >= M_k of a chunk, ledger L34)
 constexpr int kPMaxPeers = 8;      // ranks of a fused y all-gather (one NVLink domain of B200s)
 
 extern __shared__ __align__(16) unsigned char psm[];
@@ -61,6 +62,8 @@ struct PLayer {
   int64_t row_begin;   // first row in the launch's reduction order
   int32_t n_chunks, n_sub, CP;
   int32_t st_al;       // reconstruct: ld_out and w_out allow 16-B row stores
+  int32_t pc0;         // partial column of the entry's first chunk (entries are runs of one width)
+  int32_t perm;        // chunk tables + qperm (class-ordered layers, ledger L34); else c * CW, M rows
   void* y;
   float* partial;      // [rows][CP]
   void* w_out;         // reconstruct
@@ -77,6 +80,10 @@ struct PArgs {
   const unsigned char* sketch;
   const int64_t* qc_off;  // absolute byte offset of every chunk, [chunks + 1]
   const int32_t* qc_N;    // maxN of every chunk
+  const int32_t* qc_q0;   // first query position (units, within the layer) of every chunk
+  const int32_t* qc_n;    // units present in every chunk
+  const int32_t* qc_M;    // sketch rows of every chunk (rows >= M_k read row 0: max unchanged)
+  const int32_t* qperm;   // layer-local key group at each query position
   const int32_t* ncols;
   const uint32_t* ukeys;
   HashConsts hc;
@@ -111,14 +118,16 @@ __device__ __forceinline__ uint4 lds128(uint32_t a) {
   asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(q.x), "=r"(q.y), "=r"(q.z), "=r"(q.w) : "r"(a));
   return q;
 }
-// the lane's UPL/2 words (UPL 16-bit cells) of one slice row: ld.shared.v4 (UPL 8) or .v2 (UPL 4)
+// the lane's UPL/2 words (UPL 16-bit cells) of one slice row: ld.shared.v4 (UPL 8), .v2 (UPL 4), .u32 (UPL 2)
 template <int UPL>
 __device__ __forceinline__ void lds_cells(uint32_t a, uint32_t (&w)[UPL / 2]) {
   if constexpr (UPL == 8) {
     asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(w[0]), "=r"(w[1 % (UPL / 2)]), "=r"(w[2 % (UPL / 2)]),
                  "=r"(w[3 % (UPL / 2)]) : "r"(a));
-  } else {
+  } else if constexpr (UPL == 4) {
     asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1 % (UPL / 2)]) : "r"(a));
+  } else {
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[0]) : "r"(a));
   }
 }
 __device__ __forceinline__ uint32_t max_u16x2(uint32_t a, uint32_t b) {
@@ -182,15 +191,21 @@ __device__ __forceinline__ uint64_t* p_bar(int s) { return reinterpret_cast<uint
 __device__ __forceinline__ int* p_next() { return reinterpret_cast<int*>(psm + 16); }
 __device__ __forceinline__ uint32_t p_rtab() { return smem_u32(psm + kPHdr); }
 // slots start 1024-B aligned (the ulp-512 address form needs B % 512 == 0)
-__device__ __forceinline__ uint32_t p_slot(const PArgs& A, int s) {
+// a 1024-B zero block (1024-aligned) precedes the slots: sketch rows a chunk does not have read it
+__device__ __forceinline__ uint32_t p_zero() {
   const uint32_t a = smem_u32(psm + kPHdr + kPRtab);
-  return ((a + 1023u) & ~1023u) + (uint32_t)s * A.slot_bytes;
+  return (a + 1023u) & ~1023u;
 }
+template <bool TAB>
+__device__ __forceinline__ uint32_t p_slot(const PArgs& A, int s) {
+  return p_zero() + (TAB ? kPZero : 0u) + (uint32_t)s * A.slot_bytes;
+}
+template <bool TAB>
 __device__ __forceinline__ void p_issue(const PArgs& A, int slot, uint64_t off, uint32_t bytes) {
   fence_proxy_async_smem();  // earlier generic reads of the slot happen before the async-proxy write
   mbar_arrive_expect_tx(p_bar(slot), bytes);
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   p_slot(A, slot)),
+                   p_slot<TAB>(A, slot)),
                "l"(A.sketch + off), "r"(bytes), "r"(smem_u32(p_bar(slot)))
                : "memory");
 }
@@ -233,7 +248,7 @@ __device__ __forceinline__ void p_fill_rtab(const PArgs& A, uint32_t rtab, int64
 // K4p / K3p: one CTA per SM computes the host-balanced contiguous item range [cta_item[c],
 // cta_item[c+1]) of (layer, chunk, 16-row subtile) items; warps grab the subtiles of a staged chunk.
 // GEMV: chunk partials of every row -> [rows][CP].  !GEMV: W' rows (bf16) -> w_out.
-template <int MT, bool GEMV, bool XB, int SR, int UPL>
+template <int MT, bool GEMV, bool XB, int SR, int UPL, bool TAB>
 __device__ __forceinline__ void p_query(const PArgs& A) {
   constexpr int CW = 32 * UPL;        // units per chunk (one lane's UPL units each)
   constexpr uint32_t SLB = 2u * CW;   // bytes per (sketch row, column) slice = the FFMA's ulp
@@ -247,9 +262,12 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
     mbar_init(p_bar(0), 1);
     mbar_init(p_bar(1), 1);
     fence_mbar_init();
-    if (s_begin < s_end) p_issue(A, 0, A.first_off[c], A.first_bytes[c]);  // before anything else
+    if (s_begin < s_end) p_issue<TAB>(A, 0, A.first_off[c], A.first_bytes[c]);  // before anything else
     if (tl) tl[4] = gtimer();
   }
+  if (TAB && threadIdx.x >= 64 && threadIdx.x < 64 + kPZero / 16)  // the zero block (read after the barrier below)
+    asm volatile("st.shared.v4.u32 [%0], {%1, %1, %1, %1};" ::"r"(p_zero() + 16u * (threadIdx.x - 64)), "r"(0u)
+                 : "memory");
   if (GEMV && A.x_prefetch && s_begin < s_end && threadIdx.x == 32) {
     // L2 warm-up of the x slices of this CTA's chunks (a pure hint: the loads after
     // griddepcontrol.wait read whatever the previous kernel wrote; L2 is the point of coherence)
@@ -257,11 +275,14 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
     int64_t s = s_begin;
     for (int n = 0; n < 4 && s < s_end; ++n) {
       const PSeg g = p_seg_at(A, s, s_end);
-      const int64_t j0 = (int64_t)g.chunk * CW;
-      const int64_t nb = min((int64_t)CW, A.in - j0) * es;
-      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(A.x) + j0 * es),
-                   "r"((uint32_t)((nb + 15) & ~15ll))
-                   : "memory");
+      const PLayer& Lp = A.layer[g.li];
+      if (!TAB) {  // class-ordered chunks read x at scattered groups: no bulk hint
+        const int64_t j0 = (int64_t)g.chunk * CW;
+        const int64_t nb = min((int64_t)CW, A.in - j0) * es;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(reinterpret_cast<const char*>(A.x) + j0 * es),
+                     "r"((uint32_t)((nb + 15) & ~15ll))
+                     : "memory");
+      }
       s = g.end;
     }
   }
@@ -282,29 +303,48 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
       if (A.nslot == 2 && more && threadIdx.x == 0) {
         const int64_t g = A.layer[nxt.li].chunk0 + nxt.chunk;
         const int64_t o0 = A.qc_off[g];
-        p_issue(A, slot ^ 1, (uint64_t)o0, (uint32_t)(A.qc_off[g + 1] - o0));
+        p_issue<TAB>(A, slot ^ 1, (uint64_t)o0, (uint32_t)(A.qc_off[g + 1] - o0));
       }
       // lane state: units j0 .. j0 + UPL - 1 of the layer, inside one key group (they share K and N,
-      // ledger L32; UPL 4: two lanes per group)
-      const int64_t j0 = (int64_t)cur.chunk * CW + UPL * lane;
-      const bool valid = j0 < A.in;  // in % 8 == 0: a lane's units all exist or none
+      // ledger L32; UPL 4 / 2: two / four lanes per group).  Chunk k holds query positions
+      // q0_k .. q0_k + n_k - 1; a position is the unit itself, or (class-ordered layers, ledger L34)
+      // unit 8 qperm[g0 + q / 8] + q % 8
+      const int64_t gch = Ly.chunk0 + cur.chunk;
+      int64_t j0;
+      bool valid;
+      int Mk = MT;
+      if constexpr (!TAB) {  // identity order, one width: chunk c of the layer starts at unit c * CW, all rows
+        j0 = (int64_t)cur.chunk * CW + UPL * lane;  // identity layers: one run, pc0 = 0
+        valid = j0 < A.in;  // in % 8 == 0: a lane's units all exist or none
+      } else {  // chunk tables (class-ordered layers, ledger L34; 64-unit chunks)
+        const int qp = A.qc_q0[gch] + UPL * lane;
+        valid = UPL * lane < A.qc_n[gch];
+        j0 = valid ? 8 * (int64_t)A.qperm[(Ly.unit_base >> 3) + (qp >> 3)] + (qp & 7) : 0;  // unit_base % 8 == 0
+        Mk = A.qc_M[gch];
+      }
       const int64_t u0 = Ly.unit_base + j0;
       const uint32_t N = valid ? (uint32_t)A.ncols[u0] : 1u;
       const uint32_t K = valid ? A.ukeys[u0] : 0u;
-      const uint32_t maxN = (uint32_t)A.qc_N[Ly.chunk0 + cur.chunk];
-      const uint32_t B0 = p_slot(A, slot);
+      const uint32_t maxN = (uint32_t)A.qc_N[gch];
+      const uint32_t B0 = p_slot<TAB>(A, slot);
       uint32_t fk[MT], cb[MT];
+      float NS[TAB ? MT : 1];
 #pragma unroll
       for (int i = 0; i < MT; ++i) {
         fk[i] = 0x3F800000u | (fmix32(K ^ A.hc.kap[i]) & 0x7FFFFFu);
         // SLB * 2^23 + B_i - SLB * N (a multiple of SLB in [SLB 2^22, SLB 2^24): an fp32 number); the
-        // FFMA.RZ result lies at ulp SLB and bits * SLB mod 2^32 = B_i + SLB * idx (biased exponent
-        // 159 / 158 for SLB 512 / 256: (exp << 23) * SLB wraps to 0)
-        cb[i] = __float_as_uint(__ull2float_rz((unsigned long long)SLB * 8388608ull + B0 +
-                                               (unsigned long long)i * maxN * SLB - (unsigned long long)SLB * N));
+        // FFMA.RZ result lies at ulp SLB and bits * SLB mod 2^32 = B_i + SLB * idx + (exp << 23) * SLB
+        // (biased exponent 159 / 158 / 157 for SLB 512 / 256 / 128: the last term wraps to 0, 0, 2^30;
+        // LB removes it).  Sketch rows i >= M_k of the chunk (fewer rows than the kernel's): NS = 0 and
+        // the FFMA returns SLB * 2^23 + Z exactly -- the zero block, neutral for the max.
+        const bool row = !TAB || i < Mk;
+        NS[TAB ? i : 0] = row ? (float)(SLB * N) : 0.f;
+        cb[i] = __float_as_uint(__ull2float_rz(
+            (unsigned long long)SLB * 8388608ull +
+            (row ? B0 + (unsigned long long)i * maxN * SLB - (unsigned long long)SLB * N : p_zero())));
       }
-      const float NS = (float)(SLB * N);
-      const uint32_t LB = 2u * UPL * (uint32_t)lane;
+      constexpr uint32_t EXPB = 127u + 23u + (SLB == 512u ? 9u : SLB == 256u ? 8u : 7u);
+      const uint32_t LB = 2u * UPL * (uint32_t)lane - (EXPB << 23) * SLB;
       mbar_wait(p_bar(slot), phase[slot]);
       phase[slot] ^= 1u;
       if (!waited) {
@@ -330,17 +370,22 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
             nxb[1 % PW] = xv.y ^ 0x80008000u;
             nxb[2 % PW] = xv.z ^ 0x80008000u;
             nxb[3 % PW] = xv.w ^ 0x80008000u;
-          } else {
+          } else if constexpr (UPL == 4) {
             const uint2 xv = *reinterpret_cast<const uint2*>(reinterpret_cast<const uint16_t*>(A.x) + j0);
             nxb[0] = xv.x ^ 0x80008000u;
             nxb[1 % PW] = xv.y ^ 0x80008000u;
+          } else {
+            nxb[0] = *reinterpret_cast<const uint32_t*>(reinterpret_cast<const uint16_t*>(A.x) + j0) ^ 0x80008000u;
           }
-        } else {
+        } else if constexpr (UPL >= 4) {
 #pragma unroll
           for (int q = 0; q < UPL / 4; ++q) {
             const float4 a = *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(A.x) + j0 + 4 * q);
             nxf[4 * q] = -a.x, nxf[4 * q + 1] = -a.y, nxf[4 * q + 2] = -a.z, nxf[4 * q + 3] = -a.w;
           }
+        } else {
+          const float2 a = *reinterpret_cast<const float2*>(reinterpret_cast<const float*>(A.x) + j0);
+          nxf[0] = -a.x, nxf[1 % UPL] = -a.y;
         }
       }
       if (tl && threadIdx.x == 0 && k == 0) tl[1] = gtimer();
@@ -365,7 +410,7 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
               const uint32_t bits =
-                  __float_as_uint(__fmaf_rz(__uint_as_float(Rv[i] ^ fk[i]), NS, __uint_as_float(cb[i])));
+                  __float_as_uint(__fmaf_rz(__uint_as_float(Rv[i] ^ fk[i]), NS[TAB ? i : 0], __uint_as_float(cb[i])));
               lds_cells<UPL>(bits * SLB + LB, cl[i]);
             }
             float a = 0.f;  // the lane's units in order
@@ -387,7 +432,7 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
           }
           const float t = transpose_reduce<SR>(acc, lane);
           const int rr = p_row<SR>(lane);
-          if (p_writer<SR>(lane) && rr < nrow) Ly.partial[(r0 + rr) * Ly.CP + cur.chunk] = t;
+          if (p_writer<SR>(lane) && rr < nrow) Ly.partial[(r0 + rr) * Ly.CP + (TAB ? Ly.pc0 : 0) + cur.chunk] = t;
         } else {
           uint16_t* dst = reinterpret_cast<uint16_t*>(Ly.w_out) + r0 * Ly.ld_out + j0;
 #pragma unroll 4
@@ -399,7 +444,7 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
 #pragma unroll
             for (int i = 0; i < MT; ++i) {
               const uint32_t bits =
-                  __float_as_uint(__fmaf_rz(__uint_as_float(Rv[i] ^ fk[i]), NS, __uint_as_float(cb[i])));
+                  __float_as_uint(__fmaf_rz(__uint_as_float(Rv[i] ^ fk[i]), NS[TAB ? i : 0], __uint_as_float(cb[i])));
               lds_cells<UPL>(bits * SLB + LB, cl[i]);
             }
             // bits of w' = rotr16(rho) with the sign flipped back
@@ -414,7 +459,8 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
             if (valid) {
               if (Ly.st_al) {
                 if constexpr (UPL == 8) *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1 % PW], w[2 % PW], w[3 % PW]);
-                else *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1 % PW]);
+                else if constexpr (UPL == 4) *reinterpret_cast<uint2*>(dst) = make_uint2(w[0], w[1 % PW]);
+                else *reinterpret_cast<uint32_t*>(dst) = w[0];
               } else {
 #pragma unroll
                 for (int v = 0; v < UPL; ++v) dst[v] = (uint16_t)(w[v >> 1] >> (16 * (v & 1)));
@@ -432,7 +478,7 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
         if (A.nslot == 1) {
           const int64_t g = A.layer[nxt.li].chunk0 + nxt.chunk;
           const int64_t o0 = A.qc_off[g];
-          p_issue(A, 0, (uint64_t)o0, (uint32_t)(A.qc_off[g + 1] - o0));
+          p_issue<TAB>(A, 0, (uint64_t)o0, (uint32_t)(A.qc_off[g + 1] - o0));
         }
       }
       __syncthreads();
@@ -449,14 +495,14 @@ __device__ __forceinline__ void p_query(const PArgs& A) {
   }
 }
 
-template <int MT, bool XB, int SR, int UPL>
+template <int MT, bool XB, int SR, int UPL, bool TAB>
 __global__ void __maxnreg__(USK_QMAXREG) k_qgemv(const __grid_constant__ PArgs A) {
-  p_query<MT, true, XB, SR, UPL>(A);
+  p_query<MT, true, XB, SR, UPL, TAB>(A);
 }
 
-template <int MT, int UPL>
+template <int MT, int UPL, bool TAB>
 __global__ void __maxnreg__(USK_QMAXREG) k_qrecon(const __grid_constant__ PArgs A) {
-  p_query<MT, false, false, 16, UPL>(A);
+  p_query<MT, false, false, 16, UPL, TAB>(A);
 }
 
 // y[r] = the fixed-order sum of row r's chunk partials: red_lanes lanes per row, lane j sums chunks
@@ -565,8 +611,8 @@ struct PackRanges {
 
 __global__ void k_qpack(const __grid_constant__ PackRanges R, const uint16_t* __restrict__ cells,
                         const int64_t* __restrict__ qc_off, const int32_t* __restrict__ qc_N,
-                        const int64_t* __restrict__ qc_u0, const int64_t* __restrict__ qc_uend,
-                        const int32_t* __restrict__ qc_cw,
+                        const int64_t* __restrict__ qc_ub, const int64_t* __restrict__ qc_g0,
+                        const int32_t* __restrict__ qc_aux, const int32_t* __restrict__ qperm,
                         const int64_t* __restrict__ offsets, const int32_t* __restrict__ ncols,
                         const uint8_t* __restrict__ nrows, int64_t n_chunks, uint4* __restrict__ out) {
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -582,16 +628,18 @@ __global__ void k_qpack(const __grid_constant__ PackRanges R, const uint16_t* __
   }
   const int64_t local = byte - qc_off[a];
   const int32_t maxN = qc_N[a];
-  const int cw = qc_cw[a];  // chunk width (units): slices of 2 * cw bytes, 8 units per 16-B word
-  const int64_t slice = local / (2 * cw);
+  const int q0 = qc_aux[a], nu = qc_aux[n_chunks + a], Mk = qc_aux[2 * n_chunks + a], cw = qc_aux[3 * n_chunks + a];
+  const int64_t slice = local / (2 * cw);  // slices of 2 * cw bytes, 8 units per 16-B word
   const int g = (int)((local % (2 * cw)) / 16);
   const int i = (int)(slice / maxN), col = (int)(slice % maxN);
   uint32_t w[4] = {0u, 0u, 0u, 0u};
 #pragma unroll
   for (int v = 0; v < kQGroup; ++v) {
-    const int64_t u = qc_u0[a] + (int64_t)g * kQGroup + v;
+    const int s = g * kQGroup + v;  // slot in the chunk
     uint32_t key = 0u;
-    if (u < qc_uend[a]) {
+    if (s < nu && i < Mk) {
+      const int qp = q0 + s;  // query position in the layer -> unit (class order: ledger L34)
+      const int64_t u = qc_ub[a] + (qc_g0[a] >= 0 ? 8 * (int64_t)qperm[qc_g0[a] + (qp >> 3)] + (qp & 7) : (int64_t)qp);
       const int32_t N = ncols[u];
       if (col < N && i < (int)nrows[u]) {
         const uint32_t bb = cells[offsets[u] + (int64_t)i * N + col];
@@ -634,41 +682,50 @@ int p_occupancy(const void* kern, size_t smem) {
   return occ;
 }
 
-template <int SR, int UPL>
+template <int SR, int UPL, bool TAB>
 const void* pick_gemv(bool xb, int M) {
   if (xb) {
     switch (M) {
-      case 1: return (const void*)k_qgemv<1, true, SR, UPL>;
-      case 2: return (const void*)k_qgemv<2, true, SR, UPL>;
-      case 3: return (const void*)k_qgemv<3, true, SR, UPL>;
-      default: return (const void*)k_qgemv<4, true, SR, UPL>;
+      case 1: return (const void*)k_qgemv<1, true, SR, UPL, TAB>;
+      case 2: return (const void*)k_qgemv<2, true, SR, UPL, TAB>;
+      case 3: return (const void*)k_qgemv<3, true, SR, UPL, TAB>;
+      default: return (const void*)k_qgemv<4, true, SR, UPL, TAB>;
     }
   }
   switch (M) {
-    case 1: return (const void*)k_qgemv<1, false, SR, UPL>;
-    case 2: return (const void*)k_qgemv<2, false, SR, UPL>;
-    case 3: return (const void*)k_qgemv<3, false, SR, UPL>;
-    default: return (const void*)k_qgemv<4, false, SR, UPL>;
+    case 1: return (const void*)k_qgemv<1, false, SR, UPL, TAB>;
+    case 2: return (const void*)k_qgemv<2, false, SR, UPL, TAB>;
+    case 3: return (const void*)k_qgemv<3, false, SR, UPL, TAB>;
+    default: return (const void*)k_qgemv<4, false, SR, UPL, TAB>;
   }
 }
 
-template <int UPL>
+template <int UPL, bool TAB>
 const void* pick_recon(int M) {
   switch (M) {
-    case 1: return (const void*)k_qrecon<1, UPL>;
-    case 2: return (const void*)k_qrecon<2, UPL>;
-    case 3: return (const void*)k_qrecon<3, UPL>;
-    default: return (const void*)k_qrecon<4, UPL>;
+    case 1: return (const void*)k_qrecon<1, UPL, TAB>;
+    case 2: return (const void*)k_qrecon<2, UPL, TAB>;
+    case 3: return (const void*)k_qrecon<3, UPL, TAB>;
+    default: return (const void*)k_qrecon<4, UPL, TAB>;
   }
 }
 
-// UPL: units per lane of the layer's chunk width (qcw = 32 * UPL: 256 -> 8, 128 -> 4)
-const void* pick_kernel(bool gemv, bool xb, int M, int SR, int upl) {
+// UPL: units per lane of the chunk width (cw = 32 * UPL: 256 -> 8, 128 -> 4, 64 -> 2).  tab: the
+// launch has class-ordered layers (ledger L34) or 64-unit chunks -- the kernels read the chunk tables;
+// identity-ordered launches compile without them (16- and 8-row subtiles only for tab)
+const void* pick_kernel(bool gemv, bool xb, int M, int SR, int upl, bool tab) {
   if (gemv) {
-    if (upl == 8) return SR == 4 ? pick_gemv<4, 8>(xb, M) : SR == 8 ? pick_gemv<8, 8>(xb, M) : pick_gemv<16, 8>(xb, M);
-    return SR == 4 ? pick_gemv<4, 4>(xb, M) : SR == 8 ? pick_gemv<8, 4>(xb, M) : pick_gemv<16, 4>(xb, M);
+    if (tab || upl == 2) {
+      if (upl == 8) return SR == 16 ? pick_gemv<16, 8, true>(xb, M) : pick_gemv<8, 8, true>(xb, M);
+      if (upl == 4) return SR == 16 ? pick_gemv<16, 4, true>(xb, M) : pick_gemv<8, 4, true>(xb, M);
+      return SR == 16 ? pick_gemv<16, 2, true>(xb, M) : pick_gemv<8, 2, true>(xb, M);
+    }
+    if (upl == 8)
+      return SR == 4 ? pick_gemv<4, 8, false>(xb, M) : SR == 8 ? pick_gemv<8, 8, false>(xb, M) : pick_gemv<16, 8, false>(xb, M);
+    return SR == 4 ? pick_gemv<4, 4, false>(xb, M) : SR == 8 ? pick_gemv<8, 4, false>(xb, M) : pick_gemv<16, 4, false>(xb, M);
   }
-  return upl == 8 ? pick_recon<8>(M) : pick_recon<4>(M);
+  if (tab || upl == 2) return upl == 8 ? pick_recon<8, true>(M) : upl == 4 ? pick_recon<4, true>(M) : pick_recon<2, true>(M);
+  return upl == 8 ? pick_recon<8, false>(M) : pick_recon<4, false>(M);
 }
 
 int partial_stride(int n_chunks) { return (n_chunks + 3) / 4 * 4; }
@@ -735,7 +792,8 @@ usk_status p_launch(const void* kern, const PArgs& A, int grid, int threads, siz
 }
 
 // Query launch geometry shared by K4p and K3p: items, slots, partition, first copies.
-usk_status p_prepare(const usk_plan* pl, PArgs& A, const void* kern, bool gemv, int& grid, size_t& smem, int sr = 16) {
+usk_status p_prepare(const usk_plan* pl, PArgs& A, const void* kern, bool gemv, int& grid, size_t& smem, int sr = 16,
+                     bool tab = false) {
   uint32_t slot = 0;
   for (int k = 0; k < A.n_layers; ++k) {
     const PLayer& L = A.layer[k];
@@ -743,7 +801,7 @@ usk_status p_prepare(const usk_plan* pl, PArgs& A, const void* kern, bool gemv, 
       slot = std::max<uint32_t>(slot, (uint32_t)(pl->h_qc_off[L.chunk0 + c + 1] - pl->h_qc_off[L.chunk0 + c]));
   }
   slot = (slot + 1023u) & ~1023u;
-  const size_t base = kPHdr + kPRtab + 1024;
+  const size_t base = kPHdr + kPRtab + 1024 + (tab ? kPZero : 0);
   static const size_t cap = (size_t)env_int("USK_QSMEM_KB", 227) * 1024;
   static const int force_slots = env_int("USK_QSLOTS", 0);
   A.nslot = (base + 2 * (size_t)slot <= cap && force_slots != 1) ? 2 : 1;
@@ -777,6 +835,11 @@ PArgs p_base(const usk_plan* pl, const void* sketch, int64_t in) {
   A.sketch = reinterpret_cast<const unsigned char*>(sketch);
   A.qc_off = pl->d_qc_off;
   A.qc_N = pl->d_qc_N;
+  const size_t nch = pl->h_qc_N.size();
+  A.qc_q0 = pl->d_qc_aux;
+  A.qc_n = pl->d_qc_aux + nch;
+  A.qc_M = pl->d_qc_aux + 2 * nch;
+  A.qperm = pl->d_qperm;
   A.ncols = pl->d_ncols;
   A.ukeys = pl->d_keys;
   A.hc = pl->hc;
@@ -785,48 +848,129 @@ PArgs p_base(const usk_plan* pl, const void* sketch, int64_t in) {
 
 }  // namespace
 
-// Query-layout geometry of a plan (usk.h USK_LAYOUT_QUERY): chunks of 256 units per layer, maxN per
-// chunk, regions back to back; every key group of 8 units must have one N (the 8 cells of a slice
-// word are read at one column).
+// Query-layout geometry of a plan (usk.h USK_LAYOUT_QUERY; ledger L32, L34).  Per layer:
+//  * every key group of 8 units must have one N (the 8 cells of a slice word are read at one column);
+//  * key groups of one class (all of them when the layer's groups share a class) keep their order;
+//    with several classes the groups are ordered by (class, group) -- a permutation the class map
+//    already fixes, so no index is stored -- and chunks end at class boundaries;
+//  * chunk width: 256 units when rows_k * maxN_k * 512 bytes fit shared memory, else 128, else 64
+//    (identity layers: one width for the whole layer, from its widest units);
+//  * chunk k takes M_k * maxN_k * 2 * CW_k bytes (M_k, maxN_k: the largest rows / N of its units).
 usk_status qlayout_geometry(usk_plan* pl) {
   if (pl->M > kPMaxM) return fail(USK_EUNSUPPORTED, "query layout: at most 4 sketch rows");
   pl->h_qc_off.clear();
   pl->h_qc_N.clear();
+  pl->h_qc_q0.clear();
+  pl->h_qc_n.clear();
+  pl->h_qc_M.clear();
+  pl->h_qc_cw.clear();
+  pl->h_qperm.assign((size_t)(pl->U / kQGroup), 0);
+  const int64_t smem_cap = 227 * 1024 - (kPHdr + kPRtab + 1024 + kPZero);  // usk.h: 226,240 B per chunk
+  auto M_of = [&](int64_t u) {
+    const int c = pl->h_cls[u];
+    return c < (int)pl->Mc.size() ? pl->Mc[c] : pl->M;
+  };
   int64_t off = 0, chunk = 0;
   for (int l = 0; l < pl->n_layers; ++l) {
     LayerGeom& L = pl->layers[l];
     L.qoff = off;
     L.qchunk0 = chunk;
+    L.qruns.clear();
+    const int64_t ub = L.unit_begin, G = L.n_units / kQGroup;
     for (int64_t u = 0; u < L.n_units; u += kQGroup)
       for (int v = 1; v < kQGroup; ++v)
-        if (pl->h_ncols[L.unit_begin + u + v] != pl->h_ncols[L.unit_begin + u])
+        if (pl->h_ncols[ub + u + v] != pl->h_ncols[ub + u])
           return fail(USK_EUNSUPPORTED, "query layout: a key group of layer " + std::to_string(l) +
                                             " mixes column counts (importance classes split the group)");
-    // chunk width: 256 units (8 per lane, 16-B gathers) when a chunk of the layer's widest units fits
-    // shared memory, else 128 (4 per lane, 8-B gathers; e.g. Llama-3-8B gate/up at 0.5 bpw, N = 149)
-    const int64_t smem_cap = 227 * 1024 - (kPHdr + kPRtab + 1024);
-    L.qcw = (int64_t)pl->M * L.max_ncols * 512 <= smem_cap ? 256 : 128;
-    if ((int64_t)pl->M * L.max_ncols * 2 * L.qcw > smem_cap)
-      return fail(USK_EUNSUPPORTED, "query layout: a 128-unit chunk of layer " + std::to_string(l) +
-                                        " (rows x max N x 256 B) exceeds shared memory");
-    L.qchunks = (int32_t)((L.n_units + L.qcw - 1) / L.qcw);
-    int64_t pad = 0;  // padding cells of existing units (N_u < maxN_k or M_u < rows)
-    for (int c = 0; c < L.qchunks; ++c) {
-      int32_t mx = 1;
-      const int64_t ue = std::min<int64_t>(L.n_units, (int64_t)(c + 1) * L.qcw);
-      for (int64_t u = (int64_t)c * L.qcw; u < ue; ++u)
-        mx = std::max(mx, pl->h_ncols[L.unit_begin + u]);
-      pad += (int64_t)pl->M * mx * (ue - (int64_t)c * L.qcw) -
-             (pl->h_offsets[L.unit_begin + ue] - pl->h_offsets[L.unit_begin + (int64_t)c * L.qcw]);
+    // group order: by class of the group's first unit (stable); identity when one class
+    std::vector<int32_t> order((size_t)G);
+    for (int64_t g = 0; g < G; ++g) order[g] = (int32_t)g;
+    bool multi = false;
+    for (int64_t g = 1; g < G && !multi; ++g) multi = pl->h_cls[ub + 8 * g] != pl->h_cls[ub];
+    if (multi)
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int32_t a, int32_t b) { return pl->h_cls[ub + 8 * (int64_t)a] < pl->h_cls[ub + 8 * (int64_t)b]; });
+    for (int64_t g = 0; g < G; ++g) pl->h_qperm[(size_t)(ub / kQGroup + g)] = order[g];
+    L.qperm = multi;
+    auto unit_at = [&](int64_t q) { return ub + 8 * (int64_t)order[q >> 3] + (q & 7); };  // query pos -> unit
+    auto width_for = [&](int64_t mr, int64_t mx) -> int {
+      for (int cw : {256, 128, 64})
+        if (mr * mx * 2 * cw <= smem_cap) return cw;
+      return 0;
+    };
+    int fixed_cw = 0;
+    if (!multi) {  // one width for the layer
+      int mr = 1;
+      for (int64_t u = 0; u < L.n_units; ++u) mr = std::max(mr, M_of(ub + u));
+      fixed_cw = width_for(mr, L.max_ncols);
+      if (!fixed_cw)
+        return fail(USK_EUNSUPPORTED, "query layout: a 64-unit chunk of layer " + std::to_string(l) +
+                                          " (rows x max N x 128 B) exceeds shared memory");
+    }
+    int64_t pad = 0;  // padding cells of existing units (N_u < maxN_k or M_u < M_k)
+    L.qchunks = 0;
+    for (int64_t q = 0; q < L.n_units;) {
+      // the chunk's class run ends at the next class boundary (multi) or the layer end
+      int64_t run_end = L.n_units;
+      if (multi) {
+        const uint8_t c0 = pl->h_cls[unit_at(q)];
+        run_end = q;
+        while (run_end < L.n_units && pl->h_cls[unit_at(run_end)] == c0) run_end += kQGroup;
+      }
+      int cw = fixed_cw;
+      int64_t e = 0;
+      int32_t mx = 1, mr = 1;
+      if (multi) {  // the widest chunk whose units fit
+        cw = 0;
+        for (int w : {256, 128, 64}) {
+          e = std::min<int64_t>(q + w, run_end);
+          mx = 1;
+          mr = 1;
+          for (int64_t t = q; t < e; ++t) {
+            mx = std::max(mx, pl->h_ncols[unit_at(t)]);
+            mr = std::max(mr, M_of(unit_at(t)));
+          }
+          if ((int64_t)mr * mx * 2 * w <= smem_cap) {
+            cw = w;
+            break;
+          }
+        }
+        if (!cw)
+          return fail(USK_EUNSUPPORTED, "query layout: a 64-unit chunk of layer " + std::to_string(l) +
+                                            " (rows x max N x 128 B) exceeds shared memory");
+      } else {
+        e = std::min<int64_t>(q + cw, L.n_units);
+        for (int64_t t = q; t < e; ++t) {
+          mx = std::max(mx, pl->h_ncols[unit_at(t)]);
+          mr = std::max(mr, M_of(unit_at(t)));
+        }
+      }
+      for (int64_t t = q; t < e; ++t) {
+        const int64_t u = unit_at(t);
+        pad += (int64_t)mr * mx - (pl->h_offsets[u + 1] - pl->h_offsets[u]);
+      }
+      if (L.qruns.empty() || L.qruns.back().cw != cw) L.qruns.push_back({L.qchunks, 0, cw});
+      ++L.qruns.back().n;
       pl->h_qc_off.push_back(off);
       pl->h_qc_N.push_back(mx);
-      off += (int64_t)pl->M * mx * 2 * L.qcw;
+      pl->h_qc_q0.push_back((int32_t)q);
+      pl->h_qc_n.push_back((int32_t)(e - q));
+      pl->h_qc_M.push_back(mr);
+      pl->h_qc_cw.push_back(cw);
+      off += (int64_t)mr * mx * 2 * cw;
       ++chunk;
+      ++L.qchunks;
+      q = e;
     }
+    // the kernels take identity layers' chunk starts and rows arithmetically (c * CW, all M rows);
+    // a one-class layer with fewer rows than the plan (per-class rows) reads the tables instead
+    for (int c = 0; c < L.qchunks && !L.qperm; ++c)
+      if (pl->h_qc_M[L.qchunk0 + c] != pl->M) L.qperm = 1;
+    L.qcw = L.qruns.empty() ? 256 : L.qruns[0].cw;
+    L.qmixed = L.qruns.size() > 1;
     L.qbytes = off - L.qoff;
-    // the layout stays (nearly) a bijection of the cells: importance classes spread over the chunks
-    // would pad every chunk to the largest class (the 1B model at C = 4: 211 MB instead of 61 MB)
-    const int64_t cells = pl->h_offsets[L.unit_begin + L.n_units] - pl->h_offsets[L.unit_begin];
+    // the layout stays (nearly) a bijection of the cells
+    const int64_t cells = pl->h_offsets[ub + L.n_units] - pl->h_offsets[ub];
     if (pad * 16 > cells)
       return fail(USK_EUNSUPPORTED, "query layout: chunks would pad layer " + std::to_string(l) + " by " +
                                         std::to_string(pad * 100 / std::max<int64_t>(cells, 1)) +
@@ -835,11 +979,21 @@ usk_status qlayout_geometry(usk_plan* pl) {
   }
   pl->h_qc_off.push_back(off);
   pl->qtotal = off;
+  const size_t nch = pl->h_qc_N.size();
   USK_CUDA(cudaMalloc(&pl->d_qc_off, sizeof(int64_t) * pl->h_qc_off.size()));
-  USK_CUDA(cudaMalloc(&pl->d_qc_N, sizeof(int32_t) * std::max<size_t>(pl->h_qc_N.size(), 1)));
+  USK_CUDA(cudaMalloc(&pl->d_qc_N, sizeof(int32_t) * std::max<size_t>(nch, 1)));
+  USK_CUDA(cudaMalloc(&pl->d_qc_aux, sizeof(int32_t) * 4 * std::max<size_t>(nch, 1)));
+  USK_CUDA(cudaMalloc(&pl->d_qperm, sizeof(int32_t) * std::max<size_t>(pl->h_qperm.size(), 1)));
   USK_CUDA(cudaMemcpy(pl->d_qc_off, pl->h_qc_off.data(), sizeof(int64_t) * pl->h_qc_off.size(), cudaMemcpyHostToDevice));
-  if (!pl->h_qc_N.empty())
-    USK_CUDA(cudaMemcpy(pl->d_qc_N, pl->h_qc_N.data(), sizeof(int32_t) * pl->h_qc_N.size(), cudaMemcpyHostToDevice));
+  if (nch) {
+    USK_CUDA(cudaMemcpy(pl->d_qc_N, pl->h_qc_N.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice));
+    USK_CUDA(cudaMemcpy(pl->d_qc_aux, pl->h_qc_q0.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice));
+    USK_CUDA(cudaMemcpy(pl->d_qc_aux + nch, pl->h_qc_n.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice));
+    USK_CUDA(cudaMemcpy(pl->d_qc_aux + 2 * nch, pl->h_qc_M.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice));
+    USK_CUDA(cudaMemcpy(pl->d_qc_aux + 3 * nch, pl->h_qc_cw.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice));
+  }
+  if (!pl->h_qperm.empty())
+    USK_CUDA(cudaMemcpy(pl->d_qperm, pl->h_qperm.data(), sizeof(int32_t) * pl->h_qperm.size(), cudaMemcpyHostToDevice));
   return USK_OK;
 }
 
@@ -854,25 +1008,21 @@ usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const i
   const size_t tmp_bytes = (size_t)pl->total_cells * 2 + 512;
   USK_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
   usk_status s = launch_build(pl, weights, layer_ids, n, tmp, st);
-  // per-chunk unit ranges (host tables, uploaded once per call through stream-ordered scratch)
+  // per-chunk layer tables (host, uploaded once per call through stream-ordered scratch): the layer's
+  // first unit and, for class-ordered layers (ledger L34), its first key group in qperm (else -1)
   const int64_t nch = (int64_t)pl->h_qc_N.size();
-  std::vector<int64_t> u0(nch), uend(nch), cw(nch);
+  std::vector<int64_t> ub(2 * nch);
   for (int l = 0; l < pl->n_layers; ++l) {
     const LayerGeom& L = pl->layers[l];
     for (int c = 0; c < L.qchunks; ++c) {
-      u0[L.qchunk0 + c] = L.unit_begin + (int64_t)c * L.qcw;
-      uend[L.qchunk0 + c] = L.unit_begin + L.n_units;
-      cw[L.qchunk0 + c] = L.qcw;
+      ub[L.qchunk0 + c] = L.unit_begin;
+      ub[nch + L.qchunk0 + c] = L.qperm ? L.unit_begin / kQGroup : -1;
     }
   }
-  std::vector<int32_t> cw32(cw.begin(), cw.end());
   int64_t* d_u = nullptr;
   if (s == USK_OK) {
-    cudaError_t e = cudaMallocAsync(&d_u, sizeof(int64_t) * 3 * nch, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_u, u0.data(), sizeof(int64_t) * nch, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_u + nch, uend.data(), sizeof(int64_t) * nch, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(d_u + 2 * nch, cw32.data(), sizeof(int32_t) * nch, cudaMemcpyHostToDevice, st);
+    cudaError_t e = cudaMallocAsync(&d_u, sizeof(int64_t) * 2 * std::max<int64_t>(nch, 1), st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(d_u, ub.data(), sizeof(int64_t) * 2 * nch, cudaMemcpyHostToDevice, st);
     if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the pageable host tables go out of scope
     if (e != cudaSuccess) s = cuda_fail(e, "usk_build (query layout): chunk tables");
   }
@@ -899,9 +1049,8 @@ usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const i
     }
     if (R.pre[R.n] == 0) continue;
     k_qpack<<<(unsigned)((R.pre[R.n] + 255) / 256), 256, 0, st>>>(
-        R, reinterpret_cast<const uint16_t*>(tmp), pl->d_qc_off, pl->d_qc_N, d_u, d_u + nch,
-        reinterpret_cast<const int32_t*>(d_u + 2 * nch), pl->d_offsets,
-        pl->d_ncols, pl->d_nrows, nch, reinterpret_cast<uint4*>(sketch));
+        R, reinterpret_cast<const uint16_t*>(tmp), pl->d_qc_off, pl->d_qc_N, d_u, d_u + nch, pl->d_qc_aux,
+        pl->d_qperm, pl->d_offsets, pl->d_ncols, pl->d_nrows, nch, reinterpret_cast<uint4*>(sketch));
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) s = cuda_fail(e, "k_qpack");
     else count_launch();
@@ -918,15 +1067,78 @@ size_t qgemv_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, co
   return b + 256;  // + the split-K control block (two counters, left zero)
 }
 
-// one launch pair (K4p + reduce) over layers of one chunk width; ws_of[k] = layer k's partials
-usk_status qgemv_launch(const usk_plan* pl, const void* sketch, const std::vector<int>& ks, const int32_t* layers,
-                        const int64_t* o0, const int64_t* o1, const std::vector<char*>& ws_of, const void* x,
-                        int32_t x_dtype, void* const* y, int32_t y_dtype, cudaStream_t st,
-                        const usk_peers* peers = nullptr, int n = 0, unsigned int* done = nullptr) {
-  const int64_t in = pl->layers[layers[ks[0]]].in;
-  const int upl = pl->layers[layers[ks[0]]].qcw / 32;
+// entries of one chunk width: every run of that width of the call's layers (ledger L34: a class-ordered
+// layer has runs of several widths; the others one run)
+struct PEntry {
+  int k;  // index in the call
+  LayerGeom::QRun run;
+};
+
+std::vector<PEntry> entries_of_width(const usk_plan* pl, const int32_t* layers, const std::vector<int>& ks, int cw) {
+  std::vector<PEntry> es;
+  for (int k : ks)
+    for (const auto& r : pl->layers[layers[k]].qruns)
+      if (r.cw == cw) es.push_back({k, r});
+  return es;
+}
+
+void fill_entry(const usk_plan* pl, PLayer& Ly, const LayerGeom& L, const LayerGeom::QRun& r) {
+  Ly.unit_base = L.unit_begin;
+  Ly.chunk0 = L.qchunk0 + r.c0;
+  Ly.n_chunks = r.n;
+  Ly.pc0 = r.c0;
+  Ly.perm = L.qperm;
+  (void)pl;
+}
+
+// K4p over entries of one chunk width (partials only)
+usk_status qgemv_compute(const usk_plan* pl, const void* sketch, const std::vector<PEntry>& es, int cw,
+                         const int32_t* layers, const int64_t* o0, const int64_t* o1, const std::vector<char*>& ws_of,
+                         const void* x, int32_t x_dtype, cudaStream_t st) {
+  const int64_t in = pl->layers[layers[es[0].k]].in;
   PArgs A = p_base(pl, sketch, in);
   A.x = x;
+  bool any_perm = false;
+  for (const PEntry& e : es) {
+    const LayerGeom& L = pl->layers[layers[e.k]];
+    PLayer& Ly = A.layer[A.n_layers++];
+    fill_entry(pl, Ly, L, e.run);
+    Ly.o_begin = o0[e.k];
+    Ly.rows = o1[e.k] - o0[e.k];
+    Ly.CP = partial_stride(L.qchunks);
+    Ly.partial = reinterpret_cast<float*>(ws_of[e.k]);
+    any_perm |= L.qperm != 0;
+  }
+  static const int xpf = env_int("USK_XPF", 1), forced_sr = env_int("USK_QSR", 0);
+  A.x_prefetch = any_perm ? 0 : xpf;
+  // subtile height: 16 rows; 8 when a 16-row launch gives each SM fewer than ~9 subtiles for its 16
+  // warps (in-graph trace, Llama-3.2-1B o: 1.74 vs 1.99 us; q|k|v at ~10.7 per SM: 2.66 vs 2.57)
+  int64_t items16 = 0;
+  for (int k = 0; k < A.n_layers; ++k) items16 += (int64_t)A.layer[k].n_chunks * ((A.layer[k].rows + 15) / 16);
+  int SR = forced_sr ? forced_sr : (items16 < 9 * (int64_t)device_sm_count() ? 8 : 16);
+  const bool tab = any_perm || cw == 64;
+  if (tab && SR == 4) SR = 8;
+  A.items = 0;
+  for (int k = 0; k < A.n_layers; ++k) {
+    PLayer& Ly = A.layer[k];
+    Ly.n_sub = (int32_t)((Ly.rows + SR - 1) / SR);
+    Ly.item_begin = A.items;
+    A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
+  }
+  const void* kern = pick_kernel(true, x_dtype == USK_BF16, pl->M, SR, cw / 32, tab);
+  int grid = 0;
+  size_t smem = 0;
+  usk_status s = p_prepare(pl, A, kern, true, grid, smem, SR, tab);
+  if (s != USK_OK) return s;
+  A.n_ctas = grid;
+  return p_launch(kern, A, grid, kPThreads, smem, st);
+}
+
+// the split-K reduction of the call's layers (one launch, after every compute launch of the call)
+usk_status qreduce_launch(const usk_plan* pl, const void* sketch, const std::vector<int>& ks, const int32_t* layers,
+                          const int64_t* o0, const int64_t* o1, const std::vector<char*>& ws_of, void* const* y,
+                          int32_t y_dtype, cudaStream_t st, const usk_peers* peers, int n, unsigned int* done) {
+  PArgs A = p_base(pl, sketch, pl->layers[layers[ks[0]]].in);
   A.y_bf16 = y_dtype == USK_BF16;
   int max_chunks = 1;
   for (int k : ks) {
@@ -944,30 +1156,8 @@ usk_status qgemv_launch(const usk_plan* pl, const void* sketch, const std::vecto
     A.rows += Ly.rows;
     max_chunks = std::max(max_chunks, L.qchunks);
   }
-  static const int xpf = env_int("USK_XPF", 1), forced_sr = env_int("USK_QSR", 0);
-  A.x_prefetch = xpf;
-  // subtile height: 16 rows; 8 when a 16-row launch gives each SM fewer than ~9 subtiles for its 16
-  // warps (in-graph trace, Llama-3.2-1B o: 1.74 vs 1.99 us; q|k|v at ~10.7 per SM: 2.66 vs 2.57)
-  int64_t items16 = 0;
-  for (int k = 0; k < A.n_layers; ++k) items16 += (int64_t)A.layer[k].n_chunks * ((A.layer[k].rows + 15) / 16);
-  const int SR = forced_sr ? forced_sr : (items16 < 9 * (int64_t)device_sm_count() ? 8 : 16);
-  A.items = 0;
-  for (int k = 0; k < A.n_layers; ++k) {
-    PLayer& Ly = A.layer[k];
-    Ly.n_sub = (int32_t)((Ly.rows + SR - 1) / SR);
-    Ly.item_begin = A.items;
-    A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
-  }
-  const void* kern = pick_kernel(true, x_dtype == USK_BF16, pl->M, SR, upl);
-  int grid = 0;
-  size_t smem = 0;
-  usk_status s = p_prepare(pl, A, kern, true, grid, smem, SR);
-  if (s != USK_OK) return s;
-  A.n_ctas = grid;
   A.red_lanes = 1;
   while (A.red_lanes < 32 && 4 * A.red_lanes < max_chunks) A.red_lanes *= 2;
-  s = p_launch(kern, A, grid, kPThreads, smem, st);
-  if (s != USK_OK) return s;
   if (peers) {
     A.n_peers = peers->n_peers;
     A.my_rank = peers->my_rank;
@@ -987,26 +1177,28 @@ usk_status qgemv_launch(const usk_plan* pl, const void* sketch, const std::vecto
 usk_status launch_qgemv_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* o0,
                               const int64_t* o1, int n, const void* x, int32_t x_dtype, void* const* y, int32_t y_dtype,
                               void* ws, cudaStream_t st, const usk_peers* peers) {
-  // workspace: the layers' partials in call order (qgemv_batch_workspace_bytes); layers of the two
-  // chunk widths (256 / 128 units) run as separate launch pairs
+  // workspace: the layers' partials in call order (qgemv_batch_workspace_bytes).  One K4p launch per
+  // chunk width present (256 / 128 / 64 units), then ONE reduce launch over all the call's layers.
   std::vector<char*> ws_of(n);
   char* w = reinterpret_cast<char*>(ws);
-  std::vector<int> by[2];
+  std::vector<int> ks;
   for (int k = 0; k < n; ++k) {
     const LayerGeom& L = pl->layers[layers[k]];
     ws_of[k] = w;
     w += layer_ws_bytes(L.qchunks, o1[k] - o0[k]);
-    if (o1[k] > o0[k]) by[L.qcw == 256 ? 0 : 1].push_back(k);
+    if (o1[k] > o0[k]) ks.push_back(k);
   }
-  if (peers && !by[0].empty() && !by[1].empty())  // one flag per call: one launch pair
-    return fail(USK_EUNSUPPORTED, "usk_linear_batch_peers: layers of both chunk widths in one call");
+  if (ks.empty()) return USK_OK;
   unsigned int* done = reinterpret_cast<unsigned int*>(w);  // control block after the partials
-  for (auto& ks : by) {
-    if (ks.empty()) continue;
-    usk_status s = qgemv_launch(pl, sketch, ks, layers, o0, o1, ws_of, x, x_dtype, y, y_dtype, st, peers, n, done);
-    if (s != USK_OK) return s;
+  for (int cw : {256, 128, 64}) {
+    std::vector<PEntry> es = entries_of_width(pl, layers, ks, cw);
+    for (size_t a = 0; a < es.size(); a += kPMaxLayers) {
+      std::vector<PEntry> part(es.begin() + a, es.begin() + std::min(es.size(), a + kPMaxLayers));
+      usk_status s = qgemv_compute(pl, sketch, part, cw, layers, o0, o1, ws_of, x, x_dtype, st);
+      if (s != USK_OK) return s;
+    }
   }
-  return USK_OK;
+  return qreduce_launch(pl, sketch, ks, layers, o0, o1, ws_of, y, y_dtype, st, peers, n, done);
 }
 
 usk_status launch_peer_wait(const usk_plan* pl, const usk_peers* peers, cudaStream_t st) {
@@ -1025,38 +1217,46 @@ usk_status launch_peer_wait(const usk_plan* pl, const usk_peers* peers, cudaStre
   return USK_OK;
 }
 
-// K3p over several layers in one launch (usk_reconstruct, usk_reconstruct_batch): layers sharing
-// in_features and chunk width, up to kPMaxLayers per launch, full or partial row ranges
+// K3p over several layers (usk_reconstruct, usk_reconstruct_batch): layers sharing in_features, full
+// or partial row ranges; one launch per chunk width present, at most kPMaxLayers runs per launch
 usk_status qrecon_launch(const usk_plan* pl, const void* sketch, const int32_t* layers, const int64_t* r0,
                          const int64_t* r1, void* const* w_out, const int64_t* ld, int n, cudaStream_t st) {
   const LayerGeom& L0 = pl->layers[layers[0]];
-  PArgs A = p_base(pl, sketch, L0.in);
-  for (int k = 0; k < n; ++k) {
-    const LayerGeom& L = pl->layers[layers[k]];
-    const int64_t rows = r1[k] - r0[k];
-    if (rows <= 0) continue;
-    PLayer& Ly = A.layer[A.n_layers++];
-    Ly.unit_base = L.unit_begin;
-    Ly.chunk0 = L.qchunk0;
-    Ly.o_begin = r0[k];
-    Ly.rows = rows;
-    Ly.n_chunks = L.qchunks;
-    Ly.n_sub = (int32_t)((rows + 15) / 16);
-    Ly.w_out = w_out[k];
-    Ly.ld_out = ld[k];
-    Ly.st_al = (ld[k] % 8 == 0) && (reinterpret_cast<uintptr_t>(w_out[k]) % 16 == 0);
-    Ly.item_begin = A.items;
-    Ly.row_begin = A.rows;
-    A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
-    A.rows += rows;
+  std::vector<int> ks;
+  for (int k = 0; k < n; ++k)
+    if (r1[k] > r0[k]) ks.push_back(k);
+  for (int cw : {256, 128, 64}) {
+    std::vector<PEntry> es = entries_of_width(pl, layers, ks, cw);
+    for (size_t a = 0; a < es.size(); a += kPMaxLayers) {
+      PArgs A = p_base(pl, sketch, L0.in);
+      for (size_t e = a; e < std::min(es.size(), a + kPMaxLayers); ++e) {
+        const int k = es[e].k;
+        const LayerGeom& L = pl->layers[layers[k]];
+        const int64_t rows = r1[k] - r0[k];
+        PLayer& Ly = A.layer[A.n_layers++];
+        fill_entry(pl, Ly, L, es[e].run);
+        Ly.o_begin = r0[k];
+        Ly.rows = rows;
+        Ly.n_sub = (int32_t)((rows + 15) / 16);
+        Ly.w_out = w_out[k];
+        Ly.ld_out = ld[k];
+        Ly.st_al = (ld[k] % 8 == 0) && (reinterpret_cast<uintptr_t>(w_out[k]) % 16 == 0);
+        Ly.item_begin = A.items;
+        Ly.row_begin = A.rows;
+        A.items += (int64_t)Ly.n_chunks * Ly.n_sub;
+        A.rows += rows;
+      }
+      bool tab = cw == 64;
+      for (int k = 0; k < A.n_layers; ++k) tab |= A.layer[k].perm != 0;
+      const void* kern = pick_kernel(false, false, pl->M, 16, cw / 32, tab);
+      int grid = 0;
+      size_t smem = 0;
+      usk_status s = p_prepare(pl, A, kern, false, grid, smem, 16, tab);
+      if (s == USK_OK) s = p_launch(kern, A, grid, kPThreads, smem, st);
+      if (s != USK_OK) return s;
+    }
   }
-  if (!A.n_layers) return USK_OK;
-  const void* kern = pick_kernel(false, false, pl->M, 16, L0.qcw / 32);
-  int grid = 0;
-  size_t smem = 0;
-  usk_status s = p_prepare(pl, A, kern, false, grid, smem);
-  if (s != USK_OK) return s;
-  return p_launch(kern, A, grid, kPThreads, smem, st);
+  return USK_OK;
 }
 
 usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t l, int64_t r0, int64_t r1, void* w_out,
@@ -1066,12 +1266,10 @@ usk_status launch_qreconstruct(const usk_plan* pl, const void* sketch, int32_t l
 
 usk_status launch_qreconstruct_batch(const usk_plan* pl, const void* sketch, const int32_t* layers, int n,
                                      void* const* w_out, const int64_t* ld, cudaStream_t st) {
-  // consecutive runs of layers with one (in_features, chunk width), at most kPMaxLayers per launch
+  // consecutive runs of layers with one in_features, at most kPMaxLayers per launch
   for (int a = 0; a < n;) {
     int b = a + 1;
-    while (b < n && b - a < kPMaxLayers && pl->layers[layers[b]].in == pl->layers[layers[a]].in &&
-           pl->layers[layers[b]].qcw == pl->layers[layers[a]].qcw)
-      ++b;
+    while (b < n && b - a < kPMaxLayers && pl->layers[layers[b]].in == pl->layers[layers[a]].in) ++b;
     std::vector<int64_t> r0(b - a, 0), r1(b - a);
     for (int k = a; k < b; ++k) r1[k - a] = pl->layers[layers[k]].out;
     usk_status s = qrecon_launch(pl, sketch, layers + a, r0.data(), r1.data(), w_out + a, ld + a, b - a, st);

@@ -275,8 +275,8 @@ def test_c3_xg_importance_classes_full_model(orc, usk):
     """The bench's importance point at full size: C = 4 saliency classes scored per key group (ledger
     L33) with class rows (3, 3, 2, 2) (L30), USK-XG keys, all 112 linears, unit-major layout (the
     grouped-key build K2).  The whole plan (class, N, M of every unit) equals the oracle's; sampled
-    units, reconstructed entries and grouped GEMV rows; the query layout refuses the plan (its chunks
-    would pad every chunk to the most salient class: 211 MB instead of 61 MB)."""
+    units, reconstructed entries and grouped GEMV rows.  (The query layout of the same plan:
+    test_c3_query_importance_classes_full_model.)"""
     shapes = synth.llama32_1b_shapes()
     sal = [synth.saliency_like(i, 500 + l) for l, (o, i) in enumerate(shapes)]
     crows = (3, 3, 2, 2)
@@ -293,10 +293,6 @@ def test_c3_xg_importance_classes_full_model(orc, usk):
         np.testing.assert_array_equal(ncols, opl.ncols[u0:u1])
         np.testing.assert_array_equal(nrows, opl.nrows[u0:u1])
         assert (ncols.reshape(-1, 8) == ncols.reshape(-1, 8)[:, :1]).all()
-    with pytest.raises(usk.UskError) as e:
-        usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query", n_classes=4,
-                            saliency=sal_dev, class_rows=crows)
-    assert e.value.status == usk.EUNSUPPORTED
     sk = pl.new_sketch()
     ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, l // 7, l % 7), "cuda") for l, (o, i) in enumerate(shapes)]
     usk.build(pl, ws, sk)
@@ -307,6 +303,60 @@ def test_c3_xg_importance_classes_full_model(orc, usk):
     for g in ([0, 1, 2], [4, 5], [6]):
         i = shapes[g[0]][1]
         x = synth.torch_vector(i, 2000 + g[0], "cuda", torch.bfloat16)[0]
+        ys = [torch.empty(shapes[l][0], dtype=torch.float32, device="cuda") for l in g]
+        usk.linear_batch(pl, sk, g, x, ys, usk.new_batch_workspace(pl, g))
+        x64 = synth.bf16_bits_to_f32(host_bits(x)).astype(np.float64)
+        for l, y in zip(g, ys):
+            o = shapes[l][0]
+            osk = np.zeros(opl.total_cells, np.uint16)
+            orc.build_layer(opl, l, host_bits(ws[l]), osk)
+            for r0 in (0, int(rng.integers(0, o - 8)), o - 8):
+                y64 = orc.linear_rows(opl, osk, l, x64, r0, r0 + 8)[0]
+                W64 = orc.value_of(orc.reconstruct_rows(opl, osk, l, r0, r0 + 8), orc.BF16).reshape(8, i)
+                assert gemv_err(y.cpu().numpy()[r0:r0 + 8].astype(np.float64), y64, x64, W64) <= 1e-5
+
+
+def test_c3_query_importance_classes_full_model(orc, usk):
+    """The bench's importance point in the query layout (ledger L34): key groups in class order, the
+    most salient class of gate/up (N ~ 300 at 3 rows) in 64-unit chunks, the others in 256-unit
+    chunks; bytes of all layers = the unit-major bytes (no padding).  Sampled units (read back with
+    tests/qlayout.py from usk.h's text), reconstructed entries and grouped GEMV rows vs the oracle."""
+    import qlayout
+    shapes = synth.llama32_1b_shapes()
+    sal = [synth.saliency_like(i, 500 + l) for l, (o, i) in enumerate(shapes)]
+    crows = (3, 3, 2, 2)
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, seed=SEED, hash="xg", layout="query", n_classes=4,
+                             saliency=[torch.from_numpy(s).cuda() for s in sal], class_rows=crows)
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, seed=SEED, hash_kind=orc.HASH_XG, saliency=sal, C=4,
+                   class_rows=crows)
+    assert pl.sketch_bytes <= 2 * opl.total_cells + 512 * 112 * 64  # class-cut chunks: a few partial slots
+    sk = pl.new_sketch()
+    ws = [synth.torch_weights_bf16(o, i, synth.seed_for(3, l // 7, l % 7), "cuda") for l, (o, i) in enumerate(shapes)]
+    usk.build(pl, ws, sk)
+    usk.check(pl)
+    rng = np.random.default_rng(13)
+    q = sk.cpu().numpy().view(np.uint16)
+    for l in [0, 1, 4, 5, 6, 7 * 9 + 4]:
+        o, i = shapes[l]
+        u0, u1 = opl.layer_units(l)
+        li = pl.layers[l]
+        qb = q[li.qbyte_begin // 2:(li.qbyte_begin + li.qbytes) // 2]
+        ts = np.sort(rng.choice(i, 6, replace=False))
+        Wh = np.zeros((o, i), np.uint16)
+        Wh[:, ts] = host_bits(ws[l][:, torch.from_numpy(ts).cuda()].contiguous())
+        osk = np.zeros(opl.total_cells, np.uint16)
+        for t in ts:
+            orc.build_layer(opl, l, Wh, osk, int(t), int(t) + 1)
+            a, b = opl.offsets[u0 + t], opl.offsets[u0 + t + 1]
+            got = qlayout.unit_cells(qb, opl.ncols[u0:u1], opl.nrows[u0:u1], int(t), 3, opl.cls[u0:u1])
+            assert np.array_equal(got, osk[a:b]), (l, t)
+        Wr = torch.empty((o, i), dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, Wr)
+        oj = np.stack([rng.integers(0, o, 128), rng.choice(ts, 128)], 1)
+        assert np.array_equal(host_bits(Wr)[oj[:, 0], oj[:, 1]].astype(np.uint32), orc.reconstruct_entries(opl, osk, l, oj))
+    for g in ([0, 1, 2], [4, 5], [6]):
+        i = shapes[g[0]][1]
+        x = synth.torch_vector(i, 3000 + g[0], "cuda", torch.bfloat16)[0]
         ys = [torch.empty(shapes[l][0], dtype=torch.float32, device="cuda") for l in g]
         usk.linear_batch(pl, sk, g, x, ys, usk.new_batch_workspace(pl, g))
         x64 = synth.bf16_bits_to_f32(host_bits(x)).astype(np.float64)

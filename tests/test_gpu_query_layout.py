@@ -244,30 +244,41 @@ def test_xg_importance_classes_build(orc, usk):
     assert len(set(opl.ncols.tolist())) > 1  # the classes really differ
 
 
+@pytest.mark.parametrize("layout", ["unit_major", "query"])
 @pytest.mark.parametrize("crows", [None, (3, 3, 2, 2), (4, 3, 2, 1)])
-def test_xg_importance_classes_unit_major(orc, usk, crows):
+def test_xg_importance_classes(orc, usk, crows, layout):
     """Importance classes (C = 4, optionally per-class rows, ledger L30) under USK-XG keys scored per
-    key group (L33): groups uniform, so the grouped-key build runs; bytes equal the oracle's, K3
-    reconstruction bit-exact, K4 GEMV within 1e-5.  The query layout refuses the plan (classes
-    spread over every chunk would pad it to the most salient class)."""
+    key group (L33): groups uniform, so the grouped-key build runs; in the query layout the key groups
+    are in class order with chunks cut at class boundaries (L34; no padding).  Bytes equal the
+    oracle's (query bytes unpacked with tests/qlayout.py, from usk.h), reconstruction bit-exact, GEMV
+    within 1e-5; a grouped call equals the single call bit for bit."""
     shapes = [(512, 1024), (300, 2048), (960, 256)]
     sal = [synth.saliency_like(i, 90 + k) for k, (o, i) in enumerate(shapes)]
     Ws = [synth.weights_bf16(o, i, 95 + k) for k, (o, i) in enumerate(shapes)]
     M = 3 if crows is None else max(crows)
-    kw = dict(bpw=0.5, rows=M, hash="xg", seed=9, n_classes=4, class_rows=crows,
-              saliency=[torch.from_numpy(s).cuda() for s in sal])
-    with pytest.raises(usk.UskError) as e:
-        usk.plan_allocation(shapes, layout="query", **kw)
-    assert e.value.status == usk.EUNSUPPORTED and "pad" in str(e.value)
-    pl = usk.plan_allocation(shapes, **kw)
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=M, hash="xg", seed=9, n_classes=4, class_rows=crows,
+                             saliency=[torch.from_numpy(s).cuda() for s in sal], layout=layout)
     opl = orc.plan(shapes, 0.5, M=M, dtype=orc.BF16, hash_kind=orc.HASH_XG, seed=9, saliency=sal, C=4,
                    class_rows=crows)
     sk = pl.new_sketch()
+    sk.fill_(0xCD)
     usk.build(pl, [to_dev(W) for W in Ws], sk)
     usk.check(pl)
     osk = orc.build_model(opl, Ws)
-    np.testing.assert_array_equal(sk.cpu().numpy().view(np.uint16)[:opl.total_cells], osk)
     assert len(set(opl.ncols.tolist())) > 1
+    if layout == "unit_major":
+        np.testing.assert_array_equal(sk.cpu().numpy().view(np.uint16)[:opl.total_cells], osk)
+    else:
+        q = sk.cpu().numpy().view(np.uint16)
+        for l in range(len(shapes)):
+            u0, u1 = opl.layer_units(l)
+            li = pl.layers[l]
+            qb = q[li.qbyte_begin // 2:(li.qbyte_begin + li.qbytes) // 2]
+            assert li.qbytes == sum(qlayout.layer_geometry(opl.ncols[u0:u1], M, opl.nrows[u0:u1], opl.cls[u0:u1])[1])
+            cells, pad_ok = qlayout.unpack_layer(qb, opl.offsets[u0:u1 + 1], opl.ncols[u0:u1], opl.nrows[u0:u1], M,
+                                                 opl.cls[u0:u1])
+            np.testing.assert_array_equal(cells, osk[opl.offsets[u0]:opl.offsets[u1]])
+            assert pad_ok
     for l, (o, i) in enumerate(shapes):
         ref = orc.reconstruct_rows(opl, osk, l)
         w = torch.empty(o, i, dtype=torch.bfloat16, device="cuda")
@@ -280,6 +291,61 @@ def test_xg_importance_classes_unit_major(orc, usk, crows):
         y64 = orc.linear_rows(opl, osk, l, xf)[0]
         Wr = orc.value_of(ref, orc.BF16).reshape(o, i)
         assert gemv_err(y.cpu().numpy()[0], y64, xf, Wr) <= 1e-5
+    xb = synth.f32_to_bf16_bits(synth.vector(2048, seed=300)[0])
+    ys = [torch.empty(300, dtype=torch.float32, device="cuda") for _ in range(2)]
+    usk.linear_batch(pl, sk, [1, 1], to_dev(xb), ys, usk.new_batch_workspace(pl, [1, 1]))
+    y1 = torch.empty((1, 300), dtype=torch.float32, device="cuda")
+    usk.linear(pl, sk, 1, to_dev(xb).view(1, -1), y1, usk.new_workspace(pl, 1))
+    assert torch.equal(ys[0], y1[0]) and torch.equal(ys[1], y1[0])
+
+
+def test_query_class_order_wide_chunks(orc, usk):
+    """A class-ordered layer whose top class needs 64-unit chunks (a 128-unit chunk of its units would
+    exceed shared memory) beside 256-unit chunks of the other classes: bytes, K3p reconstruction (one
+    launch per width) and the K4p GEMV (one compute launch per width + one reduce) against the
+    oracle, bf16 and fp32 x; an output shard equals the full call bit for bit."""
+    shapes = [(2048, 512), (700, 512)]
+    lv = np.array([1.0, 1.0, 40.0, 1.0], np.float32)
+    rng = np.random.default_rng(3)
+    sal = [np.repeat(lv, i // 4)[rng.permutation(i)].astype(np.float32) for (o, i) in shapes]
+    Ws = [synth.weights_bf16(o, i, 61 + k) for k, (o, i) in enumerate(shapes)]
+    pl = usk.plan_allocation(shapes, bpw=5.0, rows=3, hash="xg", layout="query", seed=12, n_classes=4,
+                             saliency=[torch.from_numpy(s).cuda() for s in sal])
+    opl = orc.plan(shapes, 5.0, M=3, dtype=orc.BF16, hash_kind=orc.HASH_XG, seed=12, saliency=sal, C=4)
+    u0, u1 = opl.layer_units(0)
+    ch, order = qlayout.chunks(opl.ncols[u0:u1], opl.nrows[u0:u1], 3, opl.cls[u0:u1])
+    assert {c[2] for c in ch} >= {64, 256} and pl.layers[0].qchunk_units == 0, ch
+    sk = pl.new_sketch()
+    sk.fill_(0xCD)
+    usk.build(pl, [to_dev(W) for W in Ws], sk)
+    usk.check(pl)
+    osk = orc.build_model(opl, Ws)
+    q = sk.cpu().numpy().view(np.uint16)
+    for l, (o, i) in enumerate(shapes):
+        u0, u1 = opl.layer_units(l)
+        li = pl.layers[l]
+        qb = q[li.qbyte_begin // 2:(li.qbyte_begin + li.qbytes) // 2]
+        cells, pad_ok = qlayout.unpack_layer(qb, opl.offsets[u0:u1 + 1], opl.ncols[u0:u1], opl.nrows[u0:u1], 3,
+                                             opl.cls[u0:u1])
+        np.testing.assert_array_equal(cells, osk[opl.offsets[u0]:opl.offsets[u1]])
+        assert pad_ok
+        ref = orc.reconstruct_rows(opl, osk, l)
+        w = torch.empty(o, i, dtype=torch.bfloat16, device="cuda")
+        usk.reconstruct(pl, sk, l, w)
+        np.testing.assert_array_equal(w.cpu().view(torch.int16).numpy().view(np.uint16), ref)
+    for xdt in (torch.bfloat16, torch.float32):
+        xb = synth.f32_to_bf16_bits(synth.vector(512, seed=77)[0])
+        x = to_dev(xb) if xdt == torch.bfloat16 else torch.from_numpy(synth.bf16_bits_to_f32(xb)).cuda()
+        xf = synth.bf16_bits_to_f32(xb).astype(np.float64)
+        ys = [torch.empty(o, dtype=torch.float32, device="cuda") for (o, i) in shapes]
+        usk.linear_batch(pl, sk, [0, 1], x, ys, usk.new_batch_workspace(pl, [0, 1]))
+        for l, (o, i) in enumerate(shapes):
+            y64 = orc.linear_rows(opl, osk, l, xf)[0]
+            Wr = orc.value_of(orc.reconstruct_rows(opl, osk, l), orc.BF16).reshape(o, i)
+            assert gemv_err(ys[l].cpu().numpy(), y64, xf, Wr) <= 1e-5
+        part = torch.empty(2048 - 333, dtype=torch.float32, device="cuda")
+        usk.linear_batch(pl, sk, [0], x, [part], usk.new_batch_workspace(pl, [0], [(333, 2048)]), ranges=[(333, 2048)])
+        assert torch.equal(part, ys[0][333:])
 
 
 def test_query_importance_classes_chunk_aligned(orc, usk):
@@ -305,7 +371,8 @@ def test_query_importance_classes_chunk_aligned(orc, usk):
         u0, u1 = opl.layer_units(l)
         li = pl.layers[l]
         qb = q[li.qbyte_begin // 2:(li.qbyte_begin + li.qbytes) // 2]
-        cells, pad_ok = qlayout.unpack_layer(qb, opl.offsets[u0:u1 + 1], opl.ncols[u0:u1], opl.nrows[u0:u1], 3)
+        cells, pad_ok = qlayout.unpack_layer(qb, opl.offsets[u0:u1 + 1], opl.ncols[u0:u1], opl.nrows[u0:u1], 3,
+                                             opl.cls[u0:u1])
         np.testing.assert_array_equal(cells, osk[opl.offsets[u0]:opl.offsets[u1]])
         assert pad_ok
         ref = orc.reconstruct_rows(opl, osk, l)
