@@ -375,6 +375,13 @@ usk_status usk_plan_allocation(const usk_shape* layers, int32_t n_layers, const 
     int32_t mx = 0;
     for (int64_t u = L.unit_begin; u < L.unit_begin + L.n_units; ++u) mx = std::max(mx, pl->h_ncols[u]);
     L.max_ncols = mx;
+    L.groups_one_n = 1;  // every key group of 8 units has one N (grouped-key build, query layout)
+    for (int64_t u = 0; u < L.n_units && L.groups_one_n; u += kQGroup)
+      for (int v = 1; v < kQGroup && u + v < L.n_units; ++v)
+        if (pl->h_ncols[L.unit_begin + u + v] != pl->h_ncols[L.unit_begin + u]) {
+          L.groups_one_n = 0;
+          break;
+        }
     L.achieved_bits = pl->q ? (L.n_cells + pl->G - 1) / pl->G * ((int64_t)pl->q * pl->G + 32) + L.meta_bits
                             : L.n_cells * state_bits + L.meta_bits + L.n_out * (32 + state_bits);
     pl->achieved_bits += L.achieved_bits;

@@ -139,6 +139,7 @@ struct LayerGeom {
   int64_t cell_begin, n_cells;
   int64_t budget_bits, meta_bits, cells_T, achieved_bits;
   int32_t max_ncols;  // max N over the layer's units
+  int32_t groups_one_n = 0;  // every key group of 8 consecutive units has one N
   int32_t scope;      // budget scope id
   int64_t n_out = 0;  // Top-K outliers of the layer (L29)
   int64_t out_off = 0;  // byte offset of the layer's side table in the sketch (indices, then states)

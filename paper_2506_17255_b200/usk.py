@@ -250,11 +250,14 @@ def plan_allocation(shapes, *, bpw: float, rows: int = 3, granularity: str = "ro
 
 
 def build(plan: Plan, weights, sketch, layer_ids=None, stream=None):
+    import torch
     n = len(weights)
-    for k, w in enumerate(weights):
+    want = torch.bfloat16 if plan.dtype == BF16 else torch.float32
+    shapes = plan.shapes
+    for k, w in enumerate(weights):  # one cheap pass; the detailed message only on a mismatch
         l = k if layer_ids is None else layer_ids[k]
-        if 0 <= l < len(plan.shapes):
-            _need(w, f"build: weights[{k}]", plan.shapes[l], plan.dtype)
+        if 0 <= l < len(shapes) and (w.dtype != want or w.shape != shapes[l] or not w.is_contiguous()):
+            _need(w, f"build: weights[{k}]", shapes[l], plan.dtype)
     wp = (ct.c_void_p * n)(*[w.data_ptr() for w in weights])
     ids = None if layer_ids is None else (ct.c_int32 * n)(*layer_ids)
     _check(lib.usk_build(plan.handle, wp, ids, n, _ptr(sketch), _stream(stream)))
