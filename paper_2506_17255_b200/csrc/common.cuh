@@ -200,6 +200,8 @@ struct usk_plan {
   // width; per key group of the model: the layer-local group at each query position
   std::vector<int32_t> h_qc_q0, h_qc_n, h_qc_M, h_qc_cw, h_qperm;
   int32_t* d_qc_aux = nullptr;  // [4][chunks]: q0, n, M, cw
+  int64_t* d_qc_lay = nullptr;  // [2][chunks]: the chunk's layer first unit; its first key group in
+                                //   d_qperm for class-ordered layers, else -1 (k_qpack)
   int32_t* d_qperm = nullptr;   // [U / 8]
   int cell_bytes() const { return dtype == USK_BF16 ? 2 : 4; }  // raw state bytes
   int64_t code_bytes() const { return (total_cells * q + 7) / 8; }

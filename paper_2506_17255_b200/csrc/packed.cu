@@ -994,6 +994,17 @@ usk_status qlayout_geometry(usk_plan* pl) {
   }
   if (!pl->h_qperm.empty())
     USK_CUDA(cudaMemcpy(pl->d_qperm, pl->h_qperm.data(), sizeof(int32_t) * pl->h_qperm.size(), cudaMemcpyHostToDevice));
+  // k_qpack's per-chunk layer tables (uploaded once here, not per build call)
+  std::vector<int64_t> lay(2 * std::max<size_t>(nch, 1), 0);
+  for (int l = 0; l < pl->n_layers; ++l) {
+    const LayerGeom& L = pl->layers[l];
+    for (int c = 0; c < L.qchunks; ++c) {
+      lay[L.qchunk0 + c] = L.unit_begin;
+      lay[nch + L.qchunk0 + c] = L.qperm ? L.unit_begin / kQGroup : -1;
+    }
+  }
+  USK_CUDA(cudaMalloc(&pl->d_qc_lay, sizeof(int64_t) * lay.size()));
+  USK_CUDA(cudaMemcpy(pl->d_qc_lay, lay.data(), sizeof(int64_t) * lay.size(), cudaMemcpyHostToDevice));
   return USK_OK;
 }
 
@@ -1008,24 +1019,8 @@ usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const i
   const size_t tmp_bytes = (size_t)pl->total_cells * 2 + 512;
   USK_CUDA(cudaMallocAsync(&tmp, tmp_bytes, st));
   usk_status s = launch_build(pl, weights, layer_ids, n, tmp, st);
-  // per-chunk layer tables (host, uploaded once per call through stream-ordered scratch): the layer's
-  // first unit and, for class-ordered layers (ledger L34), its first key group in qperm (else -1)
   const int64_t nch = (int64_t)pl->h_qc_N.size();
-  std::vector<int64_t> ub(2 * nch);
-  for (int l = 0; l < pl->n_layers; ++l) {
-    const LayerGeom& L = pl->layers[l];
-    for (int c = 0; c < L.qchunks; ++c) {
-      ub[L.qchunk0 + c] = L.unit_begin;
-      ub[nch + L.qchunk0 + c] = L.qperm ? L.unit_begin / kQGroup : -1;
-    }
-  }
-  int64_t* d_u = nullptr;
-  if (s == USK_OK) {
-    cudaError_t e = cudaMallocAsync(&d_u, sizeof(int64_t) * 2 * std::max<int64_t>(nch, 1), st);
-    if (e == cudaSuccess) e = cudaMemcpyAsync(d_u, ub.data(), sizeof(int64_t) * 2 * nch, cudaMemcpyHostToDevice, st);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(st);  // the pageable host tables go out of scope
-    if (e != cudaSuccess) s = cuda_fail(e, "usk_build (query layout): chunk tables");
-  }
+  const int64_t* d_u = pl->d_qc_lay;  // per-chunk layer tables (plan)
   // byte ranges of the requested layers, merged when adjacent
   std::vector<std::pair<int64_t, int64_t>> rg;
   for (int32_t k = 0; k < n; ++k) {
@@ -1055,7 +1050,6 @@ usk_status launch_qbuild(const usk_plan* pl, const void* const* weights, const i
     if (e != cudaSuccess) s = cuda_fail(e, "k_qpack");
     else count_launch();
   }
-  if (d_u) (void)cudaFreeAsync(d_u, st);
   (void)cudaFreeAsync(tmp, st);
   return s;
 }
