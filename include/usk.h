@@ -345,6 +345,15 @@ USK_API usk_status usk_linear_batch_tokens(const usk_plan* plan, const void* ske
                                            int64_t T, void* const* y, int32_t y_dtype, void* workspace,
                                            size_t workspace_bytes, usk_stream stream);
 
+/* The computation stage alone ("computation"): Y_k = X . W'_k^T for n weight
+ * blocks stored back to back, row-major, in w (bf16 [sum rows_k, in]; e.g. W' rebuilt by
+ * usk_reconstruct_batch), ONE tcgen05 GEMM whose epilogue writes block k's columns to y[k]
+ * ([T, rows_k] of y_dtype, contiguous).  Lets a caller overlap the decompression of the next group
+ * with this group's GEMM (two workspaces, two streams).  rows[k] % 32 == 0 for k < n - 1, n <= 8;
+ * x, w 16-B aligned; in % 8 == 0.  Same results as usk_linear_batch_tokens on the same W'. */
+USK_API usk_status usk_gemm_tokens(const void* x, int64_t T, int64_t in, const void* w, const int64_t* rows,
+                                   int32_t n, void* const* y, int32_t y_dtype, usk_stream stream);
+
 /* Output-sharded decode with the y all-gather fused into the split-K reduction (SURVEY 8(e),
  * north star "each linear's output features are sharded for inference"; B200-native collective in
  * place of an NCCL all-gather).  Rank my_rank of n_peers computes rows [ranges[2k], ranges[2k+1])

@@ -660,6 +660,21 @@ usk_status usk_linear_batch_tokens(const usk_plan* pl, const void* sketch, const
   return launch_gemm_bf16_seg(x, ws, outs.data(), n, y_dtype, T, in, st);
 }
 
+usk_status usk_gemm_tokens(const void* x, int64_t T, int64_t in, const void* w, const int64_t* rows, int32_t n,
+                           void* const* y, int32_t y_dtype, usk_stream stream) {
+  if (!x || !w || !rows || !y) return fail(USK_EINVAL, "usk_gemm_tokens: null pointer");
+  if (n < 1 || n > 8 || T < 1 || in < 8 || in % 8 != 0) return fail(USK_ESHAPE, "usk_gemm_tokens: n, T or in");
+  if (y_dtype != USK_F32 && y_dtype != USK_BF16) return fail(USK_EINVAL, "usk_gemm_tokens: y_dtype");
+  if (!aligned16(x) || !aligned16(w)) return fail(USK_EINVAL, "usk_gemm_tokens: 16-B alignment");
+  std::vector<GemmOut> outs(n);
+  for (int k = 0; k < n; ++k) {
+    if (rows[k] < 1 || (k + 1 < n && rows[k] % 32 != 0) || !y[k] || !aligned16(y[k]))
+      return fail(USK_ESHAPE, "usk_gemm_tokens: rows[k] (inner blocks % 32 == 0) or y[k]");
+    outs[k] = GemmOut{y[k], rows[k], rows[k]};
+  }
+  return launch_gemm_bf16_seg(x, w, outs.data(), n, y_dtype, T, in, (cudaStream_t)stream);
+}
+
 size_t usk_linear_batch_workspace_bytes(const usk_plan* pl, const int32_t* layers, const int64_t* ranges, int32_t n) {
   std::vector<int64_t> o0, o1;
   if (batch_ranges(pl, layers, ranges, n, o0, o1) != USK_OK) return 0;

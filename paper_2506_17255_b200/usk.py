@@ -87,6 +87,7 @@ def _load():
         "usk_linear_batch": (i32, [p, p, p, p, i32, p, i32, p, i32, p, ct.c_size_t, p]),
         "usk_linear_batch_tokens_workspace_bytes": (ct.c_size_t, [p, p, p, i32, i64]),
         "usk_linear_batch_tokens": (i32, [p, p, p, p, i32, p, i32, i64, p, i32, p, ct.c_size_t, p]),
+        "usk_gemm_tokens": (i32, [p, i64, i64, p, p, i32, p, i32, p]),
         "usk_check": (i32, [p, p]),
         "usk_plan_destroy": (None, [p]),
         "usk_status_string": (ct.c_char_p, [i32]),
@@ -387,6 +388,24 @@ def linear_batch_tokens(plan: Plan, sketch, layers, x, ys, workspace, ranges=Non
     _check(lib.usk_linear_batch_tokens(plan.handle, _ptr(sketch), ids, rg, n, _ptr(x), _dtype_code(x), T, yp,
                                        _dtype_code(ys[0]), _ptr(workspace),
                                        workspace.numel() * workspace.element_size(), _stream(stream)))
+
+
+def gemm_tokens(x, w, rows, ys, stream=None):
+    """usk_gemm_tokens: the computation stage alone -- ys[k] = x @ w[block k]^T with the blocks of
+    `rows` stacked in w (bf16 [sum rows, in], e.g. filled by reconstruct_batch); one GEMM."""
+    _need(x, "gemm_tokens: x")
+    _need(w, "gemm_tokens: w")
+    n = len(rows)
+    T = x.shape[0] if x.dim() == 2 else 1
+    if len(ys) != n:
+        raise UskError(ESHAPE, f"gemm_tokens: {len(ys)} outputs for {n} blocks")
+    for k, y in enumerate(ys):
+        _need(y, f"gemm_tokens: ys[{k}]")
+        if y.numel() != T * rows[k]:
+            raise UskError(ESHAPE, f"gemm_tokens: ys[{k}] has {y.numel()} elements, needs {T * rows[k]}")
+    rw = (ct.c_int64 * n)(*rows)
+    yp = (ct.c_void_p * n)(*[y.data_ptr() for y in ys])
+    _check(lib.usk_gemm_tokens(_ptr(x), T, x.shape[-1], _ptr(w), rw, n, yp, _dtype_code(ys[0]), _stream(stream)))
 
 
 class _Peers(ct.Structure):

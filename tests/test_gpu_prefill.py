@@ -153,3 +153,30 @@ def test_batch_tokens_ranges_and_rejections(orc, usk):
     with pytest.raises(usk.UskError) as e:
         usk.linear_batch_tokens(pl, sk, [0, 1], x.float(), [torch.empty((T, o), device="cuda") for o, _ in shapes], ws)
     assert e.value.status == usk.EUNSUPPORTED
+
+
+def test_gemm_tokens_equals_batch_tokens(orc, usk):
+    """usk_gemm_tokens (the computation stage alone, on W' rebuilt by usk_reconstruct_batch) gives the
+    bytes of usk_linear_batch_tokens; rejects an inner block with rows % 32 != 0."""
+    shapes = [(96, 256), (160, 256), (300, 256)]
+    pl, opl, sk, osk = _group(orc, usk, shapes, "query", seed=33)
+    T = 70
+    x = _bf16_dev(synth.f32_to_bf16_bits(synth.vector(256, seed=4, T=T)))
+    layers = [0, 1, 2]
+    ref = [torch.empty((T, o), dtype=torch.float32, device="cuda") for o, _ in shapes]
+    usk.linear_batch_tokens(pl, sk, layers, x, ref,
+                            torch.zeros(usk.linear_batch_tokens_workspace_bytes(pl, layers, T), dtype=torch.uint8,
+                                        device="cuda"))
+    w = torch.empty((sum(o for o, _ in shapes), 256), dtype=torch.bfloat16, device="cuda")
+    views, r = [], 0
+    for o, _ in shapes:
+        views.append(w[r:r + o])
+        r += o
+    usk.reconstruct_batch(pl, sk, layers, views)
+    ys = [torch.empty((T, o), dtype=torch.float32, device="cuda") for o, _ in shapes]
+    usk.gemm_tokens(x, w, [o for o, _ in shapes], ys)
+    for a, b in zip(ys, ref):
+        assert torch.equal(a, b)
+    with pytest.raises(usk.UskError):
+        usk.gemm_tokens(x, w[:100 + 160], [100, 160], [torch.empty((T, 100), device="cuda"),
+                                                       torch.empty((T, 160), device="cuda")])

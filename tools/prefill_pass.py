@@ -59,6 +59,49 @@ def pass_grouped():
         usk.linear_batch_tokens(pl, sk, g, Xw[shapes[g[0]][1]], Yg[gi], wsp, stream=st)
 
 
+# pipelined: the next group's W' rebuilt (usk_reconstruct_batch) on a side stream into the other of
+# two workspaces while this group's GEMM (usk_gemm_tokens) runs
+side = torch.cuda.Stream(device=dev)
+gmax = max(sum(shapes[l][0] for l in g) * shapes[g[0]][1] for g in groups)
+wsx = [torch.empty(gmax, dtype=torch.bfloat16, device=dev) for _ in range(2)]
+
+
+def w_views(gi):
+    g = groups[gi]
+    i = shapes[g[0]][1]
+    out, off = [], 0
+    for l in g:
+        o = shapes[l][0]
+        out.append(wsx[gi % 2][off:off + o * i].view(o, i))
+        off += o * i
+    return out
+
+
+def pass_pipelined():
+    n = len(groups)
+    ev_r = [torch.cuda.Event() for _ in range(n)]
+    ev_g = [torch.cuda.Event() for _ in range(n)]
+    start = torch.cuda.Event()
+    start.record(st)
+    side.wait_event(start)
+    with torch.cuda.stream(side):
+        usk.reconstruct_batch(pl, sk, groups[0], w_views(0), stream=side)
+        ev_r[0].record(side)
+    for gi, g in enumerate(groups):
+        if gi + 1 < n:
+            if gi >= 1:
+                side.wait_event(ev_g[gi - 1])  # its workspace is free once GEMM gi-1 is done
+            with torch.cuda.stream(side):
+                usk.reconstruct_batch(pl, sk, groups[gi + 1], w_views(gi + 1), stream=side)
+                ev_r[gi + 1].record(side)
+        st.wait_event(ev_r[gi])
+        i = shapes[g[0]][1]
+        usk.gemm_tokens(Xw[i], wsx[gi % 2][:sum(shapes[l][0] for l in g) * i].view(-1, i),
+                        [shapes[l][0] for l in g], Yg[gi], stream=st)
+        ev_g[gi].record(st)
+    st.wait_stream(side)
+
+
 def pass_recon():
     for l, (o, i) in enumerate(shapes):
         usk.reconstruct(pl, sk, l, wsp[:o * i * 2].view(torch.bfloat16).view(o, i), stream=st)
@@ -86,7 +129,18 @@ def timed(fn, graph):
 
 
 out = {"bpw": args.bpw}
-for name, fn in (("pass", pass_full), ("pass_grouped", pass_grouped), ("recon_only", pass_recon)):
+for name, fn in (("pass", pass_full), ("pass_grouped", pass_grouped), ("pass_pipelined", pass_pipelined),
+                 ("recon_only", pass_recon)):
     for graph in (False, True):
         out[f"{name}_{'graph' if graph else 'eager'}_ms"] = timed(fn, graph)
 print(json.dumps(out), flush=True)
+# the pipelined pass writes the same Y as the grouped one (same W', same GEMM)
+with torch.cuda.stream(st):
+    pass_grouped()
+torch.cuda.synchronize()
+ref = Yp2.clone()
+Yp2.zero_()
+with torch.cuda.stream(st):
+    pass_pipelined()
+torch.cuda.synchronize()
+print(json.dumps({"pipelined_equals_grouped": bool(torch.equal(ref, Yp2))}), flush=True)
