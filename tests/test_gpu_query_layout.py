@@ -461,3 +461,35 @@ def test_query_rows_1_2_4(orc, usk, M):
         usk.linear(pl, sk, l, xd.view(1, -1), y.view(1, -1), usk.new_workspace(pl, l))
         Wr = orc.value_of(orc.reconstruct_rows(opl, osk, l), orc.BF16).reshape(o, i)
         assert gemv_err(y.cpu().numpy().astype(np.float64), orc.linear_rows(opl, osk, l, x64)[0], x64, Wr) <= 1e-5
+
+
+def test_query_class_order_prefill(orc, usk):
+    """T > 1 on a class-ordered plan (ledger L34): the batched reconstruction reads the chunk tables,
+    then the tcgen05 GEMM; fp32 y within 1e-5 of the oracle's fp64 sums for every row of a few
+    tokens, and the whole of y equal to the single-layer calls."""
+    shapes = [(512, 1024), (300, 1024)]
+    sal = [synth.saliency_like(i, 140 + k) for k, (o, i) in enumerate(shapes)]
+    Ws = [synth.weights_bf16(o, i, 150 + k) for k, (o, i) in enumerate(shapes)]
+    pl = usk.plan_allocation(shapes, bpw=0.5, rows=3, hash="xg", layout="query", seed=21, n_classes=4,
+                             saliency=[torch.from_numpy(s).cuda() for s in sal], class_rows=(3, 3, 2, 2))
+    opl = orc.plan(shapes, 0.5, M=3, dtype=orc.BF16, hash_kind=orc.HASH_XG, seed=21, saliency=sal, C=4,
+                   class_rows=(3, 3, 2, 2))
+    sk = pl.new_sketch()
+    usk.build(pl, [to_dev(W) for W in Ws], sk)
+    osk = orc.build_model(opl, Ws)
+    T = 45
+    xb = synth.f32_to_bf16_bits(synth.vector(1024, seed=8, T=T))
+    x = to_dev(xb)
+    ys = [torch.empty((T, o), dtype=torch.float32, device="cuda") for o, _ in shapes]
+    usk.linear_batch_tokens(pl, sk, [0, 1], x, ys,
+                            torch.zeros(usk.linear_batch_tokens_workspace_bytes(pl, [0, 1], T), dtype=torch.uint8,
+                                        device="cuda"))
+    x64 = synth.bf16_bits_to_f32(xb).astype(np.float64)
+    for l, (o, i) in enumerate(shapes):
+        ref = torch.empty((T, o), dtype=torch.float32, device="cuda")
+        usk.linear(pl, sk, l, x, ref, usk.new_workspace(pl, l, T))
+        assert torch.equal(ys[l], ref)
+        y64 = orc.linear_rows(opl, osk, l, x64[:5])
+        Wr = orc.value_of(orc.reconstruct_rows(opl, osk, l), orc.BF16).reshape(o, i)
+        err = np.max(np.abs(ys[l].cpu().numpy()[:5] - y64) / np.maximum(np.abs(x64[:5]) @ np.abs(Wr).T, 1e-30))
+        assert err <= 1e-5, err
