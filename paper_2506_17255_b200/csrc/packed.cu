@@ -809,8 +809,9 @@ usk_status p_prepare(const usk_plan* pl, PArgs& A, const void* kern, bool gemv, 
   A.slot_bytes = slot;
   smem = base + (size_t)A.nslot * slot;
   if (p_occupancy(kern, smem) < 1) return fail(USK_ECUDA, "query kernel does not fit an SM");
-  // chunk-switch penalty in items (one more bulk copy + drain): ~8 items plus the copy time
-  const int64_t P = (int64_t)env_int("USK_QSWITCH", 8 + (int)(slot >> 14)) * 16 / sr;
+  // chunk-switch penalty in 16-row items (one more bulk copy + drain): 14 measured best on the 1B step
+  // (2069 tok/s vs 2057 with 8 + slot / 16 KB, 1934 at 4, 1991 at 28; same box, interleaved)
+  const int64_t P = (int64_t)env_int("USK_QSWITCH", 14) * 16 / sr;
   grid = p_partition(A, device_sm_count(), P);
   for (int c = 0; c < grid; ++c) {
     const int64_t s = A.cta_item[c];
