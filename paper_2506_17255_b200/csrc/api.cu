@@ -119,7 +119,7 @@ static bool layer_cells(int L, const double* imp, const std::vector<int64_t>& nu
 
 static void free_plan(usk_plan* p) {
   if (!p) return;
-  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R4, p->d_err, p->d_qc_off, p->d_qc_N, p->d_qc_aux, p->d_qperm, p->d_qc_lay};
+  void* ptrs[] = {p->d_cls, p->d_ncols, p->d_nrows, p->d_offsets, p->d_keys, p->d_R4, p->d_err, p->d_qc_off, p->d_qc_N, p->d_qc_aux, p->d_qperm, p->d_qc_lay, p->d_qg};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   delete p;

@@ -62,7 +62,7 @@ struct alignas(64) BuildTask {
   int32_t pad;
   int64_t qchunk0;     // query layout: global index of the layer's first chunk
   int32_t qcw;         //   and its chunk width (units)
-  int32_t pad2;
+  int32_t qtab;        //   table-driven layer (class order, ledger L34): chunk per key group from qg
 };
 
 struct BuildArgs {
@@ -85,6 +85,9 @@ struct BuildArgs {
   unsigned char* qsketch;
   const int64_t* qc_off;
   const int32_t* qc_N;
+  const int32_t* qc_aux;  // [4][chunks]: first query position, units, rows, width
+  const int32_t* qg;      // [2][groups]: query position, chunk
+  int64_t n_chunks, n_groups;
 };
 
 static_assert(sizeof(BuildArgs) <= 32764, "BuildArgs must fit the 32 KB kernel-parameter limit");
@@ -416,6 +419,44 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       tM[ul] = ok ? (int)A.nrows[T.unit_base + j0 + ul] : 0;
     }
     __syncthreads();
+    if (T.qtab) {
+      // class-ordered layer (ledger L34): each key group of the tile goes to its own chunk / slot;
+      // the group at a chunk's last query positions also writes the chunk's empty slots (zeros)
+      const int ngt = (nu + kQGroup - 1) / kQGroup;
+      for (int gg = 0; gg < ngt; ++gg) {
+        const int64_t G = (T.unit_base + j0) / kQGroup + gg;
+        const int qpos = A.qg[G];
+        const int64_t a = A.qg[A.n_groups + G];
+        const int q0 = A.qc_aux[a], na = A.qc_aux[A.n_chunks + a], Ma = A.qc_aux[2 * A.n_chunks + a];
+        const int CWa = A.qc_aux[3 * A.n_chunks + a], maxN = A.qc_N[a];
+        const int slot = (qpos - q0) / kQGroup, CWG = CWa / kQGroup;
+        const bool lastg = qpos + kQGroup >= q0 + na;
+        const int nz = lastg ? CWG - (slot + 1) : 0;  // empty slots after this group
+        uint4* qo = reinterpret_cast<uint4*>(A.qsketch + A.qc_off[a]);
+        const int64_t words = (int64_t)Ma * maxN;
+        for (int64_t ik = threadIdx.x; ik < words * (1 + nz); ik += blockDim.x) {
+          const int64_t sl = ik % words;
+          const int extra = (int)(ik / words);  // 0: this group; 1..nz: the empty slots after it
+          uint32_t w[4] = {0u, 0u, 0u, 0u};
+          if (extra == 0) {
+            const int i = (int)(sl / maxN), k = (int)(sl % maxN);
+#pragma unroll
+            for (int v8 = 0; v8 < kQGroup; ++v8) {
+              const int ul = gg * kQGroup + v8;
+              if (ul >= TJ) break;
+              const int N = tN[ul];
+              if (k < N && i < tM[ul]) {
+                const uint32_t key = key_at(ul, i * N + k);
+                const uint32_t b = (key == ~0u) ? 0x7F80u : (rotr1(key) >> 16);  // empty = +Inf
+                w[v8 >> 1] |= ((((b << 1) | (b >> 15)) & 0xFFFFu) ^ 1u) << (16 * (v8 & 1));
+              }
+            }
+          }
+          qo[sl * CWG + slot + extra] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+      return;
+    }
     const int CWG = T.qcw / kQGroup;  // 16-B words (key groups) per slice of the chunk
     const int64_t chunk = j0 / T.qcw;
     const int g_lo = (int)((j0 % T.qcw) / kQGroup);
@@ -869,6 +910,10 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
     A.qsketch = reinterpret_cast<unsigned char*>(qsketch);
     A.qc_off = pl->d_qc_off;
     A.qc_N = pl->d_qc_N;
+    A.qc_aux = pl->d_qc_aux;
+    A.qg = pl->d_qg;
+    A.n_chunks = (int64_t)pl->h_qc_N.size();
+    A.n_groups = (int64_t)pl->h_qperm.size();
     int tiles = 0, maxmn = 1;
     const int TJ = 32 * upl;
     for (size_t k = g0; k < std::min(group.size(), g0 + kMaxTasks); ++k) {
@@ -884,6 +929,7 @@ usk_status launch_fast(const usk_plan* pl, int upl, std::vector<std::pair<int32_
       t.unit_base = L.unit_begin;
       t.qchunk0 = L.qchunk0;
       t.qcw = L.qcw;
+      t.qtab = L.qperm;
       t.tile_begin = tiles;
       tiles += (int)((t.in + TJ - 1) / TJ);
       maxmn = std::max(maxmn, pl->M * L.max_ncols);
@@ -1116,10 +1162,11 @@ bool build_qfast_ok(const usk_plan* pl, const int32_t* layer_ids, int32_t n) {
   for (int32_t k = 0; k < n; ++k) {
     const int32_t l = layer_ids ? layer_ids[k] : k;
     if (!fast_upl(pl, l)) return false;
-    // the fused write-out fills whole slices of identity-ordered chunks of >= 128 units and all rows
-    // (class-ordered layers, ledger L34, take the scratch build + k_qpack)
+    // the fused write-out fills whole slices of identity-ordered chunks of >= 128 units and all rows,
+    // or (table-driven, class-ordered layers, ledger L34) each key group's slices of its own chunk
     const LayerGeom& L = pl->layers[l];
-    if (L.qperm || L.qmixed || L.qcw < 128) return false;
+    if (L.qperm) continue;  // table-driven write-out (per key group: chunk, slot, rows from the plan)
+    if (L.qmixed || L.qcw < 128) return false;
     for (int c = 0; c < L.qchunks; ++c)
       if (pl->h_qc_M[L.qchunk0 + c] != pl->M) return false;
   }

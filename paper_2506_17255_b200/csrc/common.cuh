@@ -203,6 +203,7 @@ struct usk_plan {
   int64_t* d_qc_lay = nullptr;  // [2][chunks]: the chunk's layer first unit; its first key group in
                                 //   d_qperm for class-ordered layers, else -1 (k_qpack)
   int32_t* d_qperm = nullptr;   // [U / 8]
+  int32_t* d_qg = nullptr;      // [2][U / 8]: each key group's query position (layer-local) and chunk
   int cell_bytes() const { return dtype == USK_BF16 ? 2 : 4; }  // raw state bytes
   int64_t code_bytes() const { return (total_cells * q + 7) / 8; }
 };

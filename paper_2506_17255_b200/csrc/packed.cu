@@ -1006,6 +1006,23 @@ usk_status qlayout_geometry(usk_plan* pl) {
   }
   USK_CUDA(cudaMalloc(&pl->d_qc_lay, sizeof(int64_t) * lay.size()));
   USK_CUDA(cudaMemcpy(pl->d_qc_lay, lay.data(), sizeof(int64_t) * lay.size(), cudaMemcpyHostToDevice));
+  // the build's fused write-out for table-driven layers: every key group's query position and chunk
+  const size_t G = pl->h_qperm.size();
+  std::vector<int32_t> qg(2 * std::max<size_t>(G, 1), 0);
+  for (int l = 0; l < pl->n_layers; ++l) {
+    const LayerGeom& L = pl->layers[l];
+    const int64_t gb = L.unit_begin / kQGroup;
+    for (int c = 0; c < L.qchunks; ++c) {
+      const int64_t a = L.qchunk0 + c;
+      for (int32_t q = pl->h_qc_q0[a]; q < pl->h_qc_q0[a] + pl->h_qc_n[a]; q += kQGroup) {
+        const int64_t g = gb + pl->h_qperm[gb + q / kQGroup];
+        qg[g] = q;
+        qg[G + g] = (int32_t)a;
+      }
+    }
+  }
+  USK_CUDA(cudaMalloc(&pl->d_qg, sizeof(int32_t) * qg.size()));
+  USK_CUDA(cudaMemcpy(pl->d_qg, qg.data(), sizeof(int32_t) * qg.size(), cudaMemcpyHostToDevice));
   return USK_OK;
 }
 
