@@ -571,6 +571,13 @@ def run_usk(args):
     #      * importance-aware allocation with per-class rows (ledger L30): C = 4
     #        saliency classes (synth recipe), class rows (3, 3, 2, 2)
     def extra_point(**kw):
+        try:
+            return extra_point_(**kw)
+        except usk.UskError as e:  # a plan the library refuses is reported, the headline line stays
+            print(f"[bench] extra point {kw.get('layout', '')} failed: {e}", file=sys.stderr)
+            return {"error": str(e)}
+
+    def extra_point_(**kw):
         xplan = usk.plan_allocation(shapes, bpw=BPW, rows=ROWS, seed=SEED, **kw)
         xsk = xplan.new_sketch(dev)
         wq = [synth.torch_weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, l // 7, l % 7), dev)
