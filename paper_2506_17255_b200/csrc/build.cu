@@ -46,7 +46,17 @@ constexpr int kRO = USK_BUILD_ROWS;  // weight rows per stage (each consumer war
 #define USK_BUILD_CONSUMERS 16
 #endif
 constexpr int kConsumers = USK_BUILD_CONSUMERS;  // consumer warps (kRO / kConsumers rows of every stage each)
-static_assert(kRO % kConsumers == 0, "rows per stage must divide over the consumer warps");
+#ifndef USK_BUILD_ROWS_SMALL
+#define USK_BUILD_ROWS_SMALL 128
+#endif
+// rows per stage by units per lane: 2- and 1-unit tiles (wide-key layers, e.g. Llama-3-8B gate/up) take
+// twice the rows, spreading the per-row cost over as many weights (8B build 6.6 -> 4.9 ms; 4-unit
+// tiles keep 64: 0.66 vs 0.78 ms for the 1B model)
+template <int UPL>
+constexpr int ro_of() { return UPL <= 2 ? USK_BUILD_ROWS_SMALL : kRO; }
+inline int ro_host(int upl) { return upl <= 2 ? USK_BUILD_ROWS_SMALL : kRO; }
+static_assert(kRO % kConsumers == 0 && USK_BUILD_ROWS_SMALL % kConsumers == 0,
+              "rows per stage must divide over the consumer warps");
 constexpr int kBuildThreads = 32 * (kConsumers + 1);
 // layers per launch.  Launches group layers of similar key size (tasks are sorted by out): one grid
 // of all 112 Llama-3.2-1B layers sizes every CTA's keys for gate/up and measured 0.89 vs 0.80 ms
@@ -97,7 +107,7 @@ constexpr int kMinStages = 3;
 constexpr int kBuildHdr = 256;   // full[16] + empty[16] mbarriers
 
 template <typename E, int UPL>
-constexpr int stage_bytes() { return kRO * 16 + kRO * 32 * UPL * (int)sizeof(E); }
+constexpr int stage_bytes() { return ro_of<UPL>() * 16 + ro_of<UPL>() * 32 * UPL * (int)sizeof(E); }
 
 // kappa-min update of one shared key: an unconditional red.shared.min (no return value).  A
 // plain-load pre-check would skip most atomics, but ptxas turns the predicated atomic into a branch
@@ -142,7 +152,8 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
   const int64_t j0 = (int64_t)(b - T.tile_begin) * TJ;
   const int nu = (int)min((int64_t)TJ, T.in - j0);
   const int M = MT > 0 ? MT : A.M;
-  const int64_t n_it = (T.out + kRO - 1) / kRO;
+  constexpr int RO = ro_of<UPL>();  // weight rows per stage
+  const int64_t n_it = (T.out + RO - 1) / RO;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int stride_v = 32 * A.maxMN;  // words per unit slot
 
@@ -169,14 +180,14 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       for (int64_t it = 0; it < n_it; ++it) {
         const int s = (int)(it % S);
         if (it >= S) mbar_wait(&empty[s], (uint32_t)((it / S) - 1) & 1u);
-        const int64_t o0 = it * kRO;
-        const int rows = (int)min((int64_t)kRO, T.out - o0);
+        const int64_t o0 = it * RO;
+        const int rows = (int)min((int64_t)RO, T.out - o0);
         uint8_t* st = stages + s * STAGEB;
-        mbar_arrive_expect_tx(&full[s], (uint32_t)rows * 16u + (uint32_t)(kRO * ROWB));
+        mbar_arrive_expect_tx(&full[s], (uint32_t)rows * 16u + (uint32_t)(RO * ROWB));
         bulk_g2s(st, A.R4 + o0, (uint32_t)rows * 16u, &full[s]);  // the rows' position mixes
         asm volatile(
             "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
-                smem_u32(st + kRO * 16)),
+                smem_u32(st + RO * 16)),
             "l"(reinterpret_cast<uint64_t>(&T.map)), "r"((int)j0), "r"((int)o0), "r"(smem_u32(&full[s]))
             : "memory");
       }
@@ -208,9 +219,9 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
       for (int64_t it = 0; it < n_it; ++it) {
         mbar_wait(&full[s], ph);
         const uint8_t* st = stages + s * STAGEB;
-        const int64_t o0 = it * kRO;
-        const int rows = (int)min((int64_t)kRO, T.out - o0);
-        constexpr int RR = kRO / kConsumers;
+        const int64_t o0 = it * RO;
+        const int rows = (int)min((int64_t)RO, T.out - o0);
+        constexpr int RR = RO / kConsumers;
         // every row's weights and position mixes are loaded before any update (the atomics' asm
         // "memory" clobbers would otherwise keep the next row's shared loads behind them); rows past
         // a partial last stage read the (zero-filled / stale) ring and are skipped at the update
@@ -222,7 +233,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
 #pragma unroll
         for (int rr = 0; rr < RR; ++rr) {
           const int r = cw + rr * kConsumers;
-          wv[rr] = reinterpret_cast<const WT*>(st + kRO * 16 + r * ROWB)[lane];
+          wv[rr] = reinterpret_cast<const WT*>(st + RO * 16 + r * ROWB)[lane];
           R4v[rr] = reinterpret_cast<const uint4*>(st)[r];  // broadcast shared load
         }
 #pragma unroll
@@ -307,10 +318,10 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
     for (int64_t it = 0; it < n_it; ++it) {
       mbar_wait(&full[s], ph);
       const uint8_t* st = stages + s * STAGEB;
-      const int64_t o0 = it * kRO;
-      const int rows = (int)min((int64_t)kRO, T.out - o0);
-      constexpr int RR = kRO / kConsumers;
-      if (FAST && ES == 2 && UPL == 4 && rows == kRO) {
+      const int64_t o0 = it * RO;
+      const int rows = (int)min((int64_t)RO, T.out - o0);
+      constexpr int RR = RO / kConsumers;
+      if (FAST && ES == 2 && UPL == 4 && rows == RO) {
         // a full stage: every row's weights and position mixes are loaded before any update, so the
         // shared-load latency of a row overlaps the previous rows' hashing and atomics
         uint2 w2[RR];
@@ -318,7 +329,7 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
 #pragma unroll
         for (int rr = 0; rr < RR; ++rr) {
           const int r = cw + rr * kConsumers;
-          w2[rr] = reinterpret_cast<const uint2*>(st + kRO * 16 + r * ROWB)[lane];
+          w2[rr] = reinterpret_cast<const uint2*>(st + RO * 16 + r * ROWB)[lane];
           R4v[rr] = reinterpret_cast<const uint4*>(st)[r];  // broadcast
         }
 #pragma unroll
@@ -336,11 +347,11 @@ __global__ void __launch_bounds__(kBuildThreads) k_build_fast(const __grid_const
         }
       } else {
 #pragma unroll
-        for (int rr = 0; rr < kRO / kConsumers; ++rr) {
+        for (int rr = 0; rr < RO / kConsumers; ++rr) {
           const int r = cw + rr * kConsumers;
           if (r >= rows) break;
           const uint32_t o = (uint32_t)(o0 + r);
-          const uint8_t* row = st + kRO * 16 + r * ROWB;
+          const uint8_t* row = st + RO * 16 + r * ROWB;
           uint32_t bits[UPL];
           if constexpr (ES == 2 && UPL == 4) {
             const uint2 v2 = reinterpret_cast<const uint2*>(row)[lane];
@@ -824,7 +835,7 @@ bool make_w_map_uncached(CUtensorMap* m, const void* base, int64_t rows, int64_t
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
   cuuint64_t strides[1] = {(cuuint64_t)(ld ? ld : cols) * es};
-  cuuint32_t box[2] = {(cuuint32_t)tj, (cuuint32_t)kRO};
+  cuuint32_t box[2] = {(cuuint32_t)tj, (cuuint32_t)ro_host(tj / 32)};
   cuuint32_t estr[2] = {1, 1};
   return fn(m, es == 2 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base),
             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -843,7 +854,10 @@ int fast_upl(const usk_plan* pl, int32_t l, bool pitch_ok = false) {
   if (!pitch_ok && ((outrow ? L.out : L.in) * es) % 16 != 0) return 0;
   const int64_t mn = (int64_t)pl->M * L.max_ncols;
   const int S = kMinStages;
-  auto smem = [&](int upl) { return (int64_t)kBuildHdr + S * (kRO * 16 + kRO * 32 * upl * es) + 32LL * upl * mn * 4 + 128 + 512; };
+  auto smem = [&](int upl) {
+    const int64_t ro = ro_host(upl);
+    return (int64_t)kBuildHdr + S * (ro * 16 + ro * 32 * upl * es) + 32LL * upl * mn * 4 + 128 + 512;
+  };
   for (int upl : {4, 2, 1})
     if (smem(upl) <= (int64_t)kSmemLimit) return upl;
   return 0;
