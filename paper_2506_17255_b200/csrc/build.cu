@@ -47,11 +47,11 @@ constexpr int kRO = USK_BUILD_ROWS;  // weight rows per stage (each consumer war
 #endif
 constexpr int kConsumers = USK_BUILD_CONSUMERS;  // consumer warps (kRO / kConsumers rows of every stage each)
 #ifndef USK_BUILD_ROWS_SMALL
-#define USK_BUILD_ROWS_SMALL 128
+#define USK_BUILD_ROWS_SMALL 256
 #endif
 // rows per stage by units per lane: 2- and 1-unit tiles (wide-key layers, e.g. Llama-3-8B gate/up) take
-// twice the rows, spreading the per-row cost over as many weights (8B build 6.6 -> 4.9 ms; 4-unit
-// tiles keep 64: 0.66 vs 0.78 ms for the 1B model)
+// 256 rows, spreading the per-row cost over as many weights (8B build 6.6 -> 5.0 ms at 128 rows,
+// 4.85 at 256); 4-unit tiles keep 64 (0.66 vs 0.78 ms at 128 for the 1B model)
 template <int UPL>
 constexpr int ro_of() { return UPL <= 2 ? USK_BUILD_ROWS_SMALL : kRO; }
 inline int ro_host(int upl) { return upl <= 2 ? USK_BUILD_ROWS_SMALL : kRO; }
