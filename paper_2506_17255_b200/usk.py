@@ -255,11 +255,13 @@ def build(plan: Plan, weights, sketch, layer_ids=None, stream=None):
     n = len(weights)
     want = torch.bfloat16 if plan.dtype == BF16 else torch.float32
     shapes = plan.shapes
+    ptrs = [0] * n
     for k, w in enumerate(weights):  # one cheap pass; the detailed message only on a mismatch
         l = k if layer_ids is None else layer_ids[k]
         if 0 <= l < len(shapes) and (w.dtype != want or w.shape != shapes[l] or not w.is_contiguous()):
             _need(w, f"build: weights[{k}]", shapes[l], plan.dtype)
-    wp = (ct.c_void_p * n)(*[w.data_ptr() for w in weights])
+        ptrs[k] = w.data_ptr()
+    wp = (ct.c_void_p * n)(*ptrs)
     ids = None if layer_ids is None else (ct.c_int32 * n)(*layer_ids)
     _check(lib.usk_build(plan.handle, wp, ids, n, _ptr(sketch), _stream(stream)))
 
