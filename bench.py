@@ -234,7 +234,7 @@ def run_usk(args):
     ws = [synth.torch_weights_bf16(shapes[l][0], shapes[l][1], synth.seed_for(CFG, l // 7, l % 7), dev) for l in owned]
     usk.build(plan, ws, sketch, layer_ids=owned)  # warm-up (module load, attributes)
     build_times = []
-    for _ in range(3):
+    for _ in range(7):
         flush_b = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
         flush_b.fill_(1)
         del flush_b
