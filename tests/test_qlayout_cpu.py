@@ -61,3 +61,12 @@ def test_abi_declares_query_layout():
     h = open(os.path.join(os.path.dirname(__file__), "..", "include", "usk.h")).read()
     assert re.search(r"USK_LAYOUT_QUERY\s*=\s*1", h) and re.search(r"USK_HASH_XG\s*=\s*2", h)
     assert "qbyte_begin" in h and "int32_t layout;" in h
+
+
+def test_header_chunk_budget_matches_spec():
+    """tests/qlayout.py takes the chunk budget from include/usk.h's text (226,240 bytes)."""
+    import os
+    import re
+    h = open(os.path.join(os.path.dirname(__file__), "..", "include", "usk.h")).read()
+    nums = {int(m.replace(",", "")) for m in re.findall(r"(\d{3},\d{3}) bytes", h)}
+    assert qlayout.SMEM_CAP in nums, nums
